@@ -1,0 +1,424 @@
+"""FasterTucker SGD epoch benchmark (BASELINE.json metric: nonzeros/sec per SGD epoch, factor
+update + core update), Netflix-shaped synthetic tensor, J = R = 32 on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config netflix32]
+
+A step is one SGD epoch: N factor sweeps (+ C refresh + guard) then N core sweeps (+ apply +
+refresh + guard) over the whole training tensor, evaluation excluded (train.py:263-277).
+Rank 0 prints ONE JSON line.  See DESIGN.md "Measurement" for every field.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "nonzeros/sec per SGD epoch (factor update, core update)"
+
+CONFIGS = {
+    # BASELINE.json configs[1]: Netflix-shaped, |Omega| / |Gamma| of PAPER.md:918-919
+    "netflix32": dict(dims=(480_189, 17_770, 2_182), nnz_train=99_072_112, nnz_test=1_408_395,
+                      J=32, R=32, value_range=(1.0, 5.0)),
+    "netflix16": dict(dims=(480_189, 17_770, 2_182), nnz_train=99_072_112, nnz_test=1_408_395,
+                      J=16, R=16, value_range=(1.0, 5.0)),
+    "yahoo32": dict(dims=(1_000_990, 624_961, 3_075), nnz_train=250_272_286, nnz_test=2_527_989,
+                    J=32, R=32, value_range=(0.025, 5.0)),
+    "config1": dict(dims=(1000, 1000, 1000), nnz_train=90_000, nnz_test=10_000, J=8, R=8,
+                    value_range=(1.0, 5.0)),
+}
+
+CPU_SAMPLE_NNZ = 1_000_000
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+# algorithmic bytes (variant B = the exact row-owner schedule that runs here)
+# ------------------------------------------------------------------------------------------
+
+
+def kernel_bytes(kind, tree, dims, J, R):
+    """Logical bytes one launch of the row-owner kernel moves over tree u (fp32 values,
+    int32 indices, no cache dedup): leaves (coord + value), fibers (ptr + N-1 coords),
+    prefix C rows once per fiber, the leaf-level C row per leaf, and per row its A row
+    (read + write for the factor sweep; A read + C_u read for the core sweep) and row index."""
+    N = len(dims)
+    nnz, F, rows = tree.nnz, tree.num_fibers, tree.num_rows
+    b = nnz * 8 + F * (4 + 4 * (N - 1)) + F * (N - 2) * R * 4 + nnz * R * 4 + rows * 8
+    if kind == "factor_rows":
+        b += rows * 2 * J * 4
+    else:
+        b += rows * (J + R) * 4
+    return b
+
+
+def refresh_bytes(I, J, R):
+    return I * (J + R) * 4
+
+
+# ------------------------------------------------------------------------------------------
+# clocks sampler
+# ------------------------------------------------------------------------------------------
+
+
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index=0):
+        self.path = os.path.join(REPO, "gpurun_out", f"clocks_{os.getpid()}.csv")
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        self.gpu = gpu_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for k, name in enumerate(names):
+                if f[5 + k].lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------
+# CPU side (reference arm and cpu_baseline): the reference's own kernels (oracle/_ref, built
+# from /root/reference's _ckern.pyx) driven by the restated trainer, on a bounded sample.
+# ------------------------------------------------------------------------------------------
+
+
+def host_sample(dims, nnz, value_range, seed=0):
+    """nnz distinct uniform cells of `dims` with U[lo,hi] values (host numpy)."""
+    rng = np.random.default_rng([seed, 99])
+    cap = math.prod(dims)
+    lin = np.unique(rng.integers(0, cap, size=int(nnz * 1.02) + 1000))
+    rng.shuffle(lin)
+    lin = lin[:nnz]
+    idx = np.stack(np.unravel_index(lin, dims), axis=1).astype(np.int64)
+    vals = rng.uniform(value_range[0], value_range[1], size=nnz)
+    return idx, vals
+
+
+def cpu_epoch_rate(cfg, nnz, workers, repeats=1):
+    """Time factor pass + core pass of the reference CPU path on a sample; nnz/s per epoch."""
+    from oracle import oracle as O
+
+    O.build()
+    K = O.ref_kernels()
+    kind = "reference"
+    if K is None:
+        K, kind = O.CKernels, "port"
+    idx, vals = host_sample(cfg["dims"], nnz, cfg["value_range"])
+    forest = O.build_forest(idx, vals, 128)
+    model = O.default_init_model(cfg["dims"], (cfg["J"],) * 3, cfg["R"], seed=0)
+    ocfg = O.OracleConfig(workers=workers)
+    cache = O.precompute_cache(model, K=K)
+    times = []
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        for n in range(3):
+            O.update_factor_mode(model, forest, cache, n, ocfg, K=K)
+        t1 = time.perf_counter()
+        for n in range(3):
+            O.update_core_mode(model, forest, cache, n, ocfg, K=K)
+        t2 = time.perf_counter()
+        times.append((t1 - t0, t2 - t1))
+    return kind, times
+
+
+def run_reference_arm(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    workers = os.cpu_count() or 1
+    nnz = int(os.environ.get("FT_REF_SAMPLE", CPU_SAMPLE_NNZ // 2))
+    kind, times = cpu_epoch_rate(cfg, nnz, workers, repeats=args.warmup + args.steps)
+    timed = times[args.warmup:]
+    t = sum(a + b for a, b in timed)
+    value = nnz * len(timed) / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "nnz/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * t / len(timed), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (host numpy, uniform distinct cells)",
+        "config": {"workload": args.config, "sample_nnz": nnz, "J": cfg["J"], "R": cfg["R"],
+                   "dims": list(cfg["dims"]), "workers": workers},
+        "factor_nnz_per_s": nnz * len(timed) / sum(a for a, _ in timed),
+        "core_nnz_per_s": nnz * len(timed) / sum(b for _, b in timed),
+        "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": workers, "kind": kind,
+                         "sample": f"{nnz} uniform entries of the {args.config} dims, one factor "
+                                   f"+ core pass per step, workers={workers} (hogwild threads)"},
+        "e2e": {"value": value, "unit": "nnz/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+# GPU arm
+# ------------------------------------------------------------------------------------------
+
+
+def measured_peak():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(name):
+    """dram bytes per launch of kernel `name` from the committed ncu summary, if any."""
+    p = os.path.join(REPO, "profiles", "ncu_summary.json")
+    try:
+        d = json.load(open(p))
+        return d["kernels"][name]["dram_bytes_per_launch"], d["kernels"][name].get("launch")
+    except Exception:
+        return None, None
+
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2210_06014_b200 as ft
+    from paper_2210_06014_b200 import train as T
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        from paper_2210_06014_b200 import dist as D
+
+        dist.init_process_group("nccl")
+        return D.bench_distributed(args, cfg, rank, world)
+
+    dims, J, R = cfg["dims"], cfg["J"], cfg["R"]
+    N = len(dims)
+    nnz_total = cfg["nnz_train"] + cfg["nnz_test"]
+    t0 = time.perf_counter()
+    split = ft.generate_synthetic(dims, nnz_total, cfg["value_range"], seed=0,
+                                  test_fraction=cfg["nnz_test"] / nnz_total)
+    train_t, test_t = split.train, split.test
+    nnz = train_t.nnz
+    torch.cuda.synchronize()
+    log(f"generated {nnz_total} entries in {time.perf_counter() - t0:.2f}s")
+    t0 = time.perf_counter()
+    forest = ft.build_forest(train_t, 128)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    log(f"forest built in {build_s:.2f}s; fibers {[t.num_fibers for t in forest.trees]}, "
+        f"rows {[t.num_rows for t in forest.trees]}")
+    model = ft.default_init_model(dims, (J,) * N, R, seed=0)
+    counter = ft.OpCounter()
+    cache = ft.precompute_cache(model, counter)
+    tcfg = ft.TrainConfig(epochs=1, schedule=args.schedule)
+    guards = T.GuardBank(N)
+
+    def epoch(ev=None):
+        guards.reset()
+        if ev:
+            ev[0].record()
+        for n in range(N):
+            T.update_factor_mode(model, forest, cache, n, tcfg, counter, guards=guards, slot=n)
+        if ev:
+            ev[1].record()
+        for n in range(N):
+            T.update_core_mode(model, forest, cache, n, tcfg, counter, guards=guards, slot=N + n)
+        if ev:
+            ev[2].record()
+
+    for _ in range(args.warmup):
+        epoch()
+    torch.cuda.synchronize()
+    guards.check(tcfg.divergence_limit)
+    rmse0 = ft.evaluate(model, train_t, cache)[0]
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    T.KERNEL_TIMER = T.KernelTimer()
+    clocks = Clocks(local)
+    clocks.start()
+    torch.cuda.synchronize()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record()
+    for k in range(args.steps):
+        epoch(evs[k])
+    stop.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    krec = T.KERNEL_TIMER.elapsed()
+    T.KERNEL_TIMER = None
+    guards.check(tcfg.divergence_limit)
+    total_s = start.elapsed_time(stop) / 1e3
+    f_s = sum(e[0].elapsed_time(e[1]) for e in evs) / 1e3
+    c_s = sum(e[1].elapsed_time(e[2]) for e in evs) / 1e3
+    tr_rmse = ft.evaluate(model, train_t, cache)[0]
+    te_rmse = ft.evaluate(model, test_t, cache)[0]
+
+    # roofline of the dominant kernel (largest share of the timed region)
+    peak, peak_src = measured_peak()
+    by = {}
+    for name, mode, sec in krec:
+        tree = forest.trees[mode]
+        b = kernel_bytes(name, tree, dims, J, R)
+        agg = by.setdefault(name, {"bytes": 0, "sec": 0.0, "launches": 0})
+        agg["bytes"] += b
+        agg["sec"] += sec
+        agg["launches"] += 1
+    dom = max(by, key=lambda k: by[k]["sec"])
+    d = by[dom]
+    achieved = d["bytes"] / d["sec"] / 1e9
+    traffic, _ = ncu_traffic(dom + "_kernel")
+    roof = {"kernel": dom + "_kernel", "bound": "hbm", "achieved": achieved, "peak": peak,
+            "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
+            "traffic": traffic,
+            "bytes_per_launch": d["bytes"] / d["launches"],
+            "ms_per_launch": 1e3 * d["sec"] / d["launches"],
+            "share_of_step": d["sec"] / total_s}
+    kernels = {k: {"ms_total": 1e3 * v["sec"] / args.steps, "GB_per_s": v["bytes"] / v["sec"] / 1e9,
+                   "frac": v["bytes"] / v["sec"] / 1e9 / peak} for k, v in by.items()}
+    pass_bytes = {"factor": 0, "core": 0}
+    for tree_u in forest.trees:
+        u = tree_u.root_mode
+        rb = refresh_bytes(dims[u], J, R)
+        pass_bytes["factor"] += kernel_bytes("factor_rows", tree_u, dims, J, R) + rb
+        pass_bytes["core"] += kernel_bytes("core_rows", tree_u, dims, J, R) + rb
+    launches_per_epoch = 5 * N  # per mode: factor sweep, refresh, core sweep, apply, refresh
+
+    # CPU baseline (rank 0, N = 1): the reference's compiled kernels on a bounded sample
+    cpu = None
+    if not args.no_cpu:
+        nnz_s = CPU_SAMPLE_NNZ
+        kind, times = cpu_epoch_rate(cfg, nnz_s, workers=0)
+        tf, tc = times[0]
+        cpu = {"value": nnz_s / (tf + tc), "unit": "nnz/s", "cores": 1, "kind": kind,
+               "sample": f"{nnz_s} uniform entries of the {args.config} dims (same distribution, "
+                         f"lower density), one factor + core pass, serial",
+               "factor_nnz_per_s": nnz_s / tf, "core_nnz_per_s": nnz_s / tc}
+
+    e2e = run_e2e(ft, T, cfg, train_t, args) if not args.no_e2e else None
+
+    line = {
+        "metric": METRIC, "value": nnz * args.steps / total_s, "unit": "nnz/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_s / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (GPU generator: distinct uniform cells, U[1,5] values; random init)",
+        "config": {"workload": args.config, "dims": list(dims), "nnz_train": nnz,
+                   "nnz_test": test_t.nnz, "J": J, "R": R, "schedule": tcfg.resolved_schedule,
+                   "fiber_threshold": 128, "parallelism": "1 GPU",
+                   "l2": "inputs larger than L2 (forest arrays "
+                         f"{sum(t.nnz * 8 + t.num_fibers * 12 for t in forest.trees) / 1e9:.1f} GB "
+                         "streamed per epoch vs 126 MB L2)"},
+        "factor_nnz_per_s": nnz * args.steps / f_s, "core_nnz_per_s": nnz * args.steps / c_s,
+        "factor_ms": 1e3 * f_s / args.steps, "core_ms": 1e3 * c_s / args.steps,
+        "pass_roofline_frac": {k: pass_bytes[k] / ((f_s if k == "factor" else c_s) / args.steps)
+                               / 1e9 / peak for k in pass_bytes},
+        "train_rmse_before": rmse0, "train_rmse": tr_rmse, "test_rmse": te_rmse,
+        "build_forest_s": build_s,
+        "roofline": roof, "kernels": kernels,
+        "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+        "gpu_launches": launches_per_epoch * args.steps,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_e2e(ft, T, cfg, train_dev, args):
+    """Same metric through the public API from HOST buffers: every step copies the training
+    COO from pinned host memory to the device, builds the B-CSF forest, fills the cache, runs one
+    epoch and reads the training RMSE back (a `train(epochs=1)` call minus its epoch-0 row)."""
+    import torch
+
+    idx_h = train_dev.idx.cpu().pin_memory()
+    vals_h = train_dev.vals.cpu().pin_memory()
+    dims, J, R = cfg["dims"], cfg["J"], cfg["R"]
+    N = len(dims)
+    nnz = int(vals_h.shape[0])
+    steps = max(1, min(args.steps, 3))
+    times = []
+    for k in range(1 + steps):
+        model = ft.default_init_model(dims, (J,) * N, R, seed=0)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        dev = ft.DeviceCoo(tuple(dims), idx_h.to("cuda", non_blocking=True),
+                           vals_h.to("cuda", non_blocking=True))
+        forest = ft.build_forest(dev, 128)
+        counter = ft.OpCounter()
+        cache = ft.precompute_cache(model, counter)
+        m = T.run_epoch(model, forest, cache, dev, ft.TrainConfig(epochs=1, schedule=args.schedule),
+                        counter, 1, None, evaluate_metrics=True)
+        _ = m.train_rmse  # read back to the host inside the timed region
+        b.record()
+        torch.cuda.synchronize()
+        if k > 0:
+            times.append(a.elapsed_time(b) / 1e3)
+        del forest, cache, dev
+    t = sum(times) / len(times)
+    return {"value": nnz / t, "unit": "nnz/s", "h2d_bytes_per_step": nnz * (4 * N + 4),
+            "d2h_bytes_per_step": 16, "ms_per_step": 1e3 * t, "steps": len(times),
+            "includes": "H2D COO + GPU B-CSF build + cache + 1 epoch + train RMSE readback"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="netflix32", choices=sorted(CONFIGS))
+    ap.add_argument("--schedule", default="exact", choices=["exact", "hogwild"])
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference_arm(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,165 @@
+/* ft_b200.h -- C ABI of the B200-native FasterTucker hot path (libft_b200.so).
+ *
+ * The reference (arXiv 2210.06014 package `fastertucker` 0.1.0) binds its hot path through the
+ * kernel-plugin module `fastertucker._kernels.impl` (pkg/src/fastertucker/_kernels/__init__.py:11-65),
+ * whose four entry points are Cython functions over numpy buffers (_kernels/_ckern.pyx:21-282).
+ * This library is the sm_100a replacement for those entry points plus the B-CSF builder the
+ * reference runs in numpy (csf.py:101-196) and the predict/RMSE reduction (model.py:219-230,
+ * train.py:91-98).  Each declaration below cites the reference interface it replaces.
+ *
+ * Conventions
+ *   - Every pointer argument named d_* or held in ft_tree_t / ft_model_t is DEVICE memory owned
+ *     by the caller (the Python host layer allocates it as torch tensors).  The library never
+ *     frees caller memory; it allocates its own scratch stream-ordered (cudaMallocAsync).
+ *   - Every call is asynchronous on `stream` (a cudaStream_t passed as void*; NULL = legacy
+ *     default stream) unless documented as synchronous.
+ *   - Every call returns an ft_status; on failure ft_last_error() returns a thread-local message.
+ *   - Values are fp32, indices int32 (the reference uses fp64 / int64; see DESIGN.md for the
+ *     precision contract: rel 1e-4 per sweep against the fp64 reference).
+ *   - Matrices are row-major: A_n is I_n x J_n, Bt_n (= B_n^T, the reference's cores_t) is
+ *     R x J_n, C_n (the reference's DotCache.arrays[n]) is I_n x R.
+ */
+#ifndef FT_B200_H
+#define FT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define FT_API __attribute__((visibility("default")))
+#else
+#define FT_API
+#endif
+
+#define FT_MAX_ORDER 16
+#define FT_MAX_RANK 32
+
+typedef enum {
+  FT_OK = 0,
+  FT_ERR_ARG = 1,         /* invalid argument (shape, order, rank > FT_MAX_RANK, ...)       */
+  FT_ERR_CUDA = 2,        /* a CUDA runtime / launch error                                 */
+  FT_ERR_DUPLICATE = 3,   /* duplicate coordinate found while building (coo.py:56-59)       */
+  FT_ERR_EMPTY = 4,       /* empty tensor (csf.py:108-109 BuildError)                      */
+  FT_ERR_UNSUPPORTED = 5  /* shape outside what the compiled kernels cover                 */
+} ft_status;
+
+/* One B-CSF tree as the sweep kernels read it (a view; all arrays device, caller-owned).
+ * Mirrors csf.CsfTree (csf.py:32-80): level_modes = (root, root+1, ..., root+N-1) mod N.
+ * row_fiber_ptr / row_coord are NOT reference fields: they are the runs of equal root
+ * coordinate over fibers (the unsplit root slices), which the exact row-owner kernels walk. */
+typedef struct {
+  int32_t order;                /* N >= 3                                                    */
+  int32_t root_mode;            /* level-0 mode t; leaf mode is (t+N-1) mod N               */
+  int64_t nnz;                  /* leaves                                                    */
+  int64_t num_fibers;           /* F                                                         */
+  int64_t num_rows;             /* root slices (distinct level-0 coordinates)                */
+  const int32_t *leaf_coord;    /* [nnz]   csf inds[N-1]                                     */
+  const float *vals;            /* [nnz]   csf vals (level order)                            */
+  const int32_t *fiber_ptr;     /* [F+1]   csf fiber_ptr                                     */
+  const int32_t *fiber_coord;   /* [F*(N-1)] csf fiber_coord, row-major                      */
+  const int32_t *row_fiber_ptr; /* [rows+1] fiber index where each root slice starts         */
+  const int32_t *row_coord;     /* [rows]  level-0 coordinate of each root slice             */
+} ft_tree_t;
+
+/* Model parameters and the C^(n) cache (model.py:45-103, cache.py:28-57). */
+typedef struct {
+  int32_t order;
+  int32_t core_rank;                /* R                                                    */
+  int64_t dims[FT_MAX_ORDER];       /* I_n                                                  */
+  int32_t ranks[FT_MAX_ORDER];      /* J_n                                                  */
+  float *factors[FT_MAX_ORDER];     /* A_n  [I_n x J_n]                                     */
+  float *cores_t[FT_MAX_ORDER];     /* Bt_n [R x J_n]                                       */
+  float *dots[FT_MAX_ORDER];        /* C_n  [I_n x R]                                       */
+} ft_model_t;
+
+/* ---------------------------------------------------------------------------------------- */
+FT_API const char *ft_last_error(void);
+FT_API int ft_abi_version(void);
+/* number of SMs of the current device (sizes persistent grids and partial buffers) */
+FT_API int ft_sm_count(int32_t *out);
+
+/* K1  B-CSF builder.  Replaces csf.build_tree (csf.py:101-196): lexicographic sort in the
+ * cyclic level order, fiber runs, greedy split of root slices at `thr` whole fibers
+ * (thr <= 0 means fiber_threshold=None), per-depth inds/ptrs.  Output arrays are bit-identical
+ * to the reference's (as int32).  idx: device int32 [nnz x N] row-major, 0-based, unique.
+ * dims: HOST int64[N].  Output buffers are device, caller-allocated with capacity:
+ *   leaf_vals[nnz], inds[d][nnz] (d < N), ptrs[d][nnz+1] (d < N-1), fiber_ptr[nnz+1],
+ *   fiber_coord[nnz*(N-1)], sub_fiber_ptr[nnz+1], sub_leaf_ptr[nnz+1],
+ *   row_fiber_ptr[nnz+1], row_coord[nnz].   inds / ptrs are HOST arrays of device pointers.
+ * counts_out (HOST int64[4+N]): F, S, rows, first duplicate position (-1 if none),
+ *   then node count per depth.  SYNCHRONOUS (sizes are data dependent).
+ * Returns FT_ERR_DUPLICATE (with counts_out[3] set) if two entries share a coordinate. */
+FT_API int ft_build_tree(int32_t N, int64_t nnz, const int64_t *dims, const int32_t *idx,
+                  const float *vals, int32_t root_mode, int64_t thr, float *leaf_vals,
+                  int32_t *const *inds, int32_t *const *ptrs, int32_t *fiber_ptr,
+                  int32_t *fiber_coord, int32_t *sub_fiber_ptr, int32_t *sub_leaf_ptr,
+                  int32_t *row_fiber_ptr, int32_t *row_coord, int64_t *counts_out, void *stream);
+
+/* K2  C = A * Bt^T  (I x R), i.e. refresh_dot_mode (_ckern.pyx:21-33, cache.py:60-70), with the
+ * divergence guard of train.py:101-110 fused: if guard != NULL, atomically max-es the IEEE bits
+ * of |A| into guard[0] (NaN sorts above +inf, so one word detects both cases). */
+FT_API int ft_refresh(int64_t I, int32_t J, int32_t R, const float *A, const float *Bt, float *C,
+               uint32_t *guard, void *stream);
+
+/* K3b  Exact factor sweep of mode u = tree->root_mode: replaces factor_sweep over the tree
+ * rooted at (u+1) mod N (_ckern.pyx:132-199, train.py:152-197).  One warp owns one row of A_u
+ * (one root slice of the tree rooted at u) and applies its updates in the reference's serial
+ * order; C_m (m != u) and Bt_u are read-only, so the result equals the serial sweep up to fp32
+ * rounding.  Requires the cache (model->dots) to be coherent for every m != u. */
+FT_API int ft_factor_sweep_rows(const ft_tree_t *tree, const ft_model_t *model, float lr, float reg,
+                         void *stream);
+
+/* K3a  Hogwild factor sweep over fibers [fib_lo, fib_hi) of a tree rooted at t = (u+1) mod N,
+ * i.e. the reference's own traversal (_ckern.pyx:163-191) with one warp per fiber and
+ * lock-free racing row updates (train.py:124-149 with workers > 1). */
+FT_API int ft_factor_sweep_fibers(const ft_tree_t *tree, const ft_model_t *model, int64_t fib_lo,
+                           int64_t fib_hi, float lr, float reg, void *stream);
+
+/* K4  Core-gradient sweep of mode u = tree->root_mode: replaces core_sweep
+ * (_ckern.pyx:202-269, train.py:200-236) in its row form acc = -G^T A_u with
+ * G[i,:] = sum_{leaves of row i} e * cross.  Writes one R x J_u partial per block to
+ * `partials` (capacity `partials_cap` floats) and the block count to *nblocks_out (HOST).
+ * Deterministic (static row->warp map, fixed-order reductions, no atomics).
+ * Requires model->dots[u] coherent with (A_u, Bt_u). */
+FT_API int ft_core_sweep_rows(const ft_tree_t *tree, const ft_model_t *model, float *partials,
+                       int64_t partials_cap, int32_t *nblocks_out, void *stream);
+
+/* Upper bound of `partials` floats ft_core_sweep_rows needs for rank R x J. */
+FT_API int64_t ft_core_partials_size(int32_t R, int32_t J);
+
+/* K5  apply_core_update (_ckern.pyx:272-282): acc = -(sum of `nparts` partials, fixed order);
+ * Bt -= lr * (acc / omega + reg * Bt).  If acc_out != NULL the reduced acc (R x J, the
+ * reference's `acc` buffer) is stored there.  Guard as in ft_refresh, over the new Bt.
+ * `partials` may be the output of ft_core_sweep_rows, or (nparts = 1) an allreduced acc
+ * negated -- see `acc_is_negated`: 1 means partials hold +G^T A (kernel output), 0 means
+ * they hold the reference's acc itself. */
+FT_API int ft_core_apply(int32_t R, int32_t J, float *Bt, const float *partials, int32_t nparts,
+                  int32_t acc_is_negated, double omega, float lr, float reg, float *acc_out,
+                  uint32_t *guard, void *stream);
+
+/* Sum partials only (multi-GPU: reduce locally, then allreduce R*J floats, then apply). */
+FT_API int ft_core_reduce(int32_t R, int32_t J, const float *partials, int32_t nparts, float *out,
+                   void *stream);
+
+/* K6  predict_batch (model.py:219-230) from the coherent cache: out[m] = sum_r prod_n C_n[i_n,r]. */
+FT_API int ft_predict(const ft_model_t *model, int64_t m, const int32_t *idx, float *out, void *stream);
+
+/* K6  evaluate (train.py:91-98): out2[0] = sum (x - xhat)^2, out2[1] = sum |x - xhat| (fp64,
+ * DEVICE double[2], deterministic two-level reduction). */
+FT_API int ft_sse(const ft_model_t *model, int64_t m, const int32_t *idx, const float *vals,
+           double *out2, void *stream);
+
+/* K7  Synthetic COO generator (same distribution as coo.generate_synthetic, coo.py:164-213:
+ * distinct coordinates uniform without replacement, values U[lo, hi]; NOT the same stream).
+ * Writes nnz unique coordinates (row-major int32 [nnz x N]) in a random entry order, and
+ * values (so the first k entries are a uniform random test split).  Requires sum_n ceil(log2 I_n) <= 64.  SYNCHRONOUS. */
+FT_API int ft_generate_coo(int32_t N, const int64_t *dims, int64_t nnz, uint64_t seed, float lo,
+                    float hi, int32_t *idx, float *vals, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FT_B200_H */

@@ -1,0 +1,222 @@
+"""COO tensors: the input type of the decomposition API (mirrors coo.SparseCooTensor,
+/root/reference/pkg/src/fastertucker/coo.py:24-73) plus its device-resident form.
+
+* :class:`SparseCooTensor` keeps the reference's host contract: 0-based coordinates
+  ``idx`` (nnz x N) and values ``vals`` (nnz), order >= 3, in-range, unique coordinates.
+  Duplicate detection is a packed-key sort (numpy) up to ``HOST_DEDUP_LIMIT`` entries; above
+  that it is deferred to the GPU B-CSF builder, which detects equal adjacent keys for free
+  while sorting and raises the same :class:`ValidationError`.
+* :class:`DeviceCoo` is the HBM copy (int32 coordinates, fp32 values) the kernels read.
+* :func:`generate_synthetic` draws a tensor ON THE GPU (ft_generate_coo) with the reference
+  generator's distribution (coo.py:164-213: distinct cells uniform without replacement,
+  U[lo, hi] values) -- not its PCG64 stream; parity inputs come from the reference itself.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import CapacityError, ConfigError, ValidationError
+
+HOST_DEDUP_LIMIT = 4_000_000
+
+
+def _pack_keys(idx: np.ndarray, dims) -> np.ndarray | None:
+    bits = [max(1, int(d - 1).bit_length()) for d in dims]
+    if sum(bits) > 63:
+        return None
+    key = np.zeros(idx.shape[0], dtype=np.int64)
+    for n, b in enumerate(bits):
+        key = (key << b) | idx[:, n]
+    return key
+
+
+class SparseCooTensor:
+    """N-order sparse tensor: unique 0-based coordinates plus values (coo.py:24-73)."""
+
+    __slots__ = ("dims", "idx", "vals", "_device")
+
+    def __init__(self, dims, idx, vals, *, validate: bool = True):
+        dims = tuple(int(d) for d in dims)
+        if len(dims) < 3:
+            raise ValidationError(f"tensor order must be >= 3, got {len(dims)}")
+        if any(d < 1 for d in dims):
+            raise ValidationError(f"dims must be positive, got {dims}")
+        idx = np.asarray(idx)
+        vals = np.asarray(vals, dtype=np.float64)
+        if idx.ndim != 2 or idx.shape[1] != len(dims):
+            raise ValidationError(f"idx shape {idx.shape} does not match order {len(dims)}")
+        if vals.shape != (idx.shape[0],):
+            raise ValidationError("vals length does not match idx")
+        if idx.shape[0] == 0:
+            raise ValidationError("tensor must contain at least one entry")
+        if validate:
+            if idx.min(initial=0) < 0 or np.any(idx.max(axis=0) >= np.asarray(dims)):
+                raise ValidationError("coordinate out of range for dims")
+            if idx.shape[0] <= HOST_DEDUP_LIMIT:
+                dup = _first_duplicate(idx, dims)
+                if dup is not None:
+                    raise ValidationError(
+                        f"duplicate coordinate {tuple(int(c) + 1 for c in dup)}")
+        self.dims = dims
+        self.idx = idx
+        self.vals = vals
+        self._device = None
+
+    @property
+    def order(self) -> int:
+        return len(self.dims)
+
+    @property
+    def nnz(self) -> int:
+        return int(self.idx.shape[0])
+
+    def capacity(self) -> int:
+        return math.prod(self.dims)
+
+    def device(self, stream=None) -> "DeviceCoo":
+        """The HBM copy (uploaded once, cached)."""
+        if self._device is None:
+            self._device = DeviceCoo.from_host(self, stream=stream)
+        return self._device
+
+
+def _first_duplicate(idx: np.ndarray, dims):
+    key = _pack_keys(np.asarray(idx, dtype=np.int64), dims)
+    if key is None:
+        uniq = np.unique(idx, axis=0)
+        if uniq.shape[0] == idx.shape[0]:
+            return None
+        seen = set()
+        for row in idx:
+            t = tuple(row.tolist())
+            if t in seen:
+                return row
+            seen.add(t)
+        return None
+    order = np.argsort(key, kind="stable")
+    sk = key[order]
+    same = np.flatnonzero(sk[1:] == sk[:-1])
+    if same.size == 0:
+        return None
+    # the reference names the first duplicate in entry order
+    first = min(int(max(order[k], order[k + 1])) for k in same)
+    return idx[first]
+
+
+@dataclass
+class DeviceCoo:
+    """Device-resident COO: ``idx`` int32 [nnz, N] row-major, ``vals`` fp32 [nnz] (torch)."""
+
+    dims: tuple
+    idx: "object"
+    vals: "object"
+
+    @property
+    def order(self) -> int:
+        return len(self.dims)
+
+    @property
+    def nnz(self) -> int:
+        return int(self.vals.shape[0])
+
+    @classmethod
+    def from_host(cls, tensor: SparseCooTensor, stream=None) -> "DeviceCoo":
+        import torch
+
+        from . import _lib
+
+        _lib.lib()
+        if max(tensor.dims) >= 2**31:
+            raise ConfigError("dims must fit int32 on the device path")
+        idx = torch.from_numpy(np.ascontiguousarray(tensor.idx, dtype=np.int32))
+        vals = torch.from_numpy(np.ascontiguousarray(tensor.vals, dtype=np.float32))
+        return cls(tensor.dims, idx.cuda(non_blocking=False), vals.cuda(non_blocking=False))
+
+    def to_host(self, validate: bool = False) -> SparseCooTensor:
+        return SparseCooTensor(self.dims, self.idx.cpu().numpy().astype(np.int64),
+                               self.vals.cpu().numpy().astype(np.float64), validate=validate)
+
+    def slice(self, lo: int, hi: int) -> "DeviceCoo":
+        return DeviceCoo(self.dims, self.idx[lo:hi], self.vals[lo:hi])
+
+
+@dataclass(frozen=True)
+class DatasetSplit:
+    """Disjoint train/test partition of one tensor's entries (coo.py:76-82)."""
+
+    train: object
+    test: object
+    seed: int
+
+
+def split_dataset(tensor: SparseCooTensor, test_fraction: float, seed: int) -> DatasetSplit:
+    """Deterministic exact partition (coo.py:216-231): the PCG64 stream [seed, 2] permutes the
+    entries, the first round(nnz * test_fraction) become the test set."""
+    if not 0.0 < test_fraction < 1.0:
+        raise ConfigError(f"test_fraction must lie in (0, 1), got {test_fraction}")
+    n_test = int(round(tensor.nnz * test_fraction))
+    if n_test < 1 or n_test >= tensor.nnz:
+        raise ConfigError(f"test_fraction {test_fraction} leaves an empty part for nnz={tensor.nnz}")
+    perm = np.random.default_rng([int(seed), 2]).permutation(tensor.nnz)
+    te, tr = perm[:n_test], perm[n_test:]
+    return DatasetSplit(
+        train=SparseCooTensor(tensor.dims, tensor.idx[tr], tensor.vals[tr], validate=False),
+        test=SparseCooTensor(tensor.dims, tensor.idx[te], tensor.vals[te], validate=False),
+        seed=int(seed))
+
+
+def generate_device(dims, nnz: int, value_range=(1.0, 5.0), seed: int = 0) -> DeviceCoo:
+    """nnz distinct uniform cells + U[lo, hi] values generated on the GPU, in random order."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+
+    L = _lib.lib()
+    dims = tuple(int(d) for d in dims)
+    if len(dims) < 3 or any(d < 1 for d in dims):
+        raise ConfigError(f"dims must be >= 3 positive extents, got {dims}")
+    if nnz < 1:
+        raise ConfigError("nnz must be positive")
+    if nnz > math.prod(dims):
+        raise CapacityError(f"nnz={nnz} exceeds capacity {math.prod(dims)} of dims {dims}")
+    lo, hi = float(value_range[0]), float(value_range[1])
+    if not lo < hi:
+        raise ConfigError(f"value range must satisfy lo < hi, got ({lo}, {hi})")
+    idx = torch.empty((nnz, len(dims)), dtype=torch.int32, device="cuda")
+    vals = torch.empty(nnz, dtype=torch.float32, device="cuda")
+    d = (ctypes.c_int64 * len(dims))(*dims)
+    _lib.check(L.ft_generate_coo(len(dims), d, nnz, int(seed) & (2**64 - 1), lo, hi,
+                                 idx.data_ptr(), vals.data_ptr(), _lib.stream_handle()),
+               "ft_generate_coo")
+    return DeviceCoo(dims, idx, vals)
+
+
+def generate_synthetic(dims, nnz: int, value_range=(1.0, 5.0), seed: int = 0,
+                       test_fraction: float | None = None):
+    """Device synthetic tensor (see module doc).  With ``test_fraction`` returns a
+    :class:`DatasetSplit` of two :class:`DeviceCoo` (the generator's order is random, so the
+    first round(nnz * f) entries are a uniform test sample)."""
+    t = generate_device(dims, nnz, value_range, seed)
+    if test_fraction is None:
+        return t
+    n_test = int(round(nnz * test_fraction))
+    if n_test < 1 or n_test >= nnz:
+        raise ConfigError("test_fraction leaves an empty part")
+    return DatasetSplit(train=t.slice(n_test, nnz), test=t.slice(0, n_test), seed=int(seed))
+
+
+def as_device(tensor) -> DeviceCoo:
+    if isinstance(tensor, DeviceCoo):
+        return tensor
+    if isinstance(tensor, SparseCooTensor):
+        return tensor.device()
+    # duck-typed reference SparseCooTensor (dims / idx / vals)
+    if hasattr(tensor, "idx") and hasattr(tensor, "vals") and hasattr(tensor, "dims"):
+        return SparseCooTensor(tensor.dims, tensor.idx, tensor.vals, validate=False).device()
+    raise ConfigError(f"expected a COO tensor, got {type(tensor).__name__}")

@@ -1,0 +1,213 @@
+"""Balanced compressed-sparse-fiber (B-CSF) trees, built on the GPU (kernel K1).
+
+Mirrors csf.CsfTree / CsfForest / build_tree / build_forest
+(/root/reference/pkg/src/fastertucker/csf.py:32-201).  The tree rooted at mode t stores
+coordinates in level order (t, t+1, ..., t+N-1) mod N; fibers are runs of equal first N-1
+levels; a root slice holding more than ``fiber_threshold`` fibers is split into consecutive
+subtensors of at most that many whole fibers.  Every array the reference exposes is produced
+by ``ft_build_tree`` bit-identically (as int32 on the device; ``.host()`` gives int64 numpy
+views for comparison).
+
+Beyond the reference fields each tree carries its ROWS: the unsplit root slices
+(``row_fiber_ptr``, ``row_coord``).  The exact row-owner sweep of mode u walks tree u row by
+row: root slice i of tree u is precisely the list of updates row i of A_u receives, in the
+reference's serial order.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .coo import as_device
+from .errors import BuildError, ConfigError
+
+DEFAULT_FIBER_THRESHOLD = 128
+
+
+@dataclass
+class CsfTree:
+    root_mode: int
+    level_modes: tuple
+    dims: tuple
+    inds: tuple          # device int32, per depth
+    ptrs: tuple          # device int32, per depth < N-1
+    vals: object         # device fp32 [nnz]
+    fiber_ptr: object    # device int32 [F+1]
+    fiber_coord: object  # device int32 [F, N-1]
+    sub_fiber_ptr: object
+    sub_leaf_ptr: object
+    row_fiber_ptr: object  # device int32 [rows+1]  (not a reference field)
+    row_coord: object      # device int32 [rows]
+    _view: object = field(default=None, repr=False)
+
+    @property
+    def order(self) -> int:
+        return len(self.level_modes)
+
+    @property
+    def nnz(self) -> int:
+        return int(self.vals.shape[0])
+
+    @property
+    def num_fibers(self) -> int:
+        return int(self.fiber_ptr.shape[0]) - 1
+
+    @property
+    def num_subtensors(self) -> int:
+        return int(self.sub_fiber_ptr.shape[0]) - 1
+
+    @property
+    def num_rows(self) -> int:
+        return int(self.row_coord.shape[0])
+
+    @property
+    def leaf_coord(self):
+        return self.inds[-1]
+
+    @property
+    def prefix_modes(self) -> np.ndarray:
+        return np.asarray(self.level_modes[:-1], dtype=np.int64)
+
+    @property
+    def leaf_mode(self) -> int:
+        return self.level_modes[-1]
+
+    def view(self) -> _lib.FtTree:
+        """The ft_tree_t the kernels read (cached; arrays are kept alive by this object)."""
+        if self._view is None:
+            v = _lib.FtTree()
+            v.order = self.order
+            v.root_mode = self.root_mode
+            v.nnz = self.nnz
+            v.num_fibers = self.num_fibers
+            v.num_rows = self.num_rows
+            v.leaf_coord = self.leaf_coord.data_ptr()
+            v.vals = self.vals.data_ptr()
+            v.fiber_ptr = self.fiber_ptr.data_ptr()
+            v.fiber_coord = self.fiber_coord.data_ptr()
+            v.row_fiber_ptr = self.row_fiber_ptr.data_ptr()
+            v.row_coord = self.row_coord.data_ptr()
+            self._view = v
+        return self._view
+
+    def host(self) -> dict:
+        """All reference fields as int64 / float64 numpy arrays (for parity checks)."""
+        c = lambda t: t.cpu().numpy().astype(np.int64)  # noqa: E731
+        return {
+            "inds": [c(a) for a in self.inds],
+            "ptrs": [c(a) for a in self.ptrs],
+            "vals": self.vals.cpu().numpy().astype(np.float64),
+            "fiber_ptr": c(self.fiber_ptr),
+            "fiber_coord": c(self.fiber_coord),
+            "sub_fiber_ptr": c(self.sub_fiber_ptr),
+            "sub_leaf_ptr": c(self.sub_leaf_ptr),
+            "row_fiber_ptr": c(self.row_fiber_ptr),
+            "row_coord": c(self.row_coord),
+        }
+
+    def slice_rows(self, r0: int, r1: int) -> "CsfTree":
+        """A compact copy holding only root slices [r0, r1) (multi-GPU row blocks), with the
+        fiber / leaf pointers rebased.  Subtensor and per-depth arrays are not sliced (the sweep
+        kernels do not read them); they are left empty."""
+        import torch
+
+        f0 = int(self.row_fiber_ptr[r0])
+        f1 = int(self.row_fiber_ptr[r1])
+        l0 = int(self.fiber_ptr[f0])
+        l1 = int(self.fiber_ptr[f1])
+        empty = torch.empty(0, dtype=torch.int32, device=self.vals.device)
+        inds = tuple(empty for _ in range(self.order - 1)) + (self.leaf_coord[l0:l1].clone(),)
+        return CsfTree(
+            root_mode=self.root_mode, level_modes=self.level_modes, dims=self.dims,
+            inds=inds, ptrs=tuple(empty for _ in self.ptrs),
+            vals=self.vals[l0:l1].clone(),
+            fiber_ptr=(self.fiber_ptr[f0:f1 + 1] - l0).contiguous(),
+            fiber_coord=self.fiber_coord[f0:f1].clone(),
+            sub_fiber_ptr=torch.zeros(1, dtype=torch.int32, device=self.vals.device),
+            sub_leaf_ptr=torch.zeros(1, dtype=torch.int32, device=self.vals.device),
+            row_fiber_ptr=(self.row_fiber_ptr[r0:r1 + 1] - f0).contiguous(),
+            row_coord=self.row_coord[r0:r1].clone(),
+        )
+
+
+@dataclass
+class CsfForest:
+    """One tree per root mode over the same entry multiset (csf.py:83-88)."""
+
+    trees: tuple
+    fiber_threshold: object
+    omega: int | None = None   # |Omega| of the whole tensor when trees hold a row-block shard
+
+
+def build_tree(tensor, root_mode: int, fiber_threshold=DEFAULT_FIBER_THRESHOLD,
+               stream=None) -> CsfTree:
+    """GPU B-CSF build (csf.py:101-196).  ``tensor``: SparseCooTensor or DeviceCoo."""
+    import torch
+
+    L = _lib.lib()
+    dev = as_device(tensor)
+    N, nnz = dev.order, dev.nnz
+    if nnz == 0:
+        raise BuildError("cannot index an empty tensor")
+    if not 0 <= root_mode < N:
+        raise ConfigError(f"root_mode must be in [0, {N}), got {root_mode}")
+    if fiber_threshold is None:
+        thr = 0
+    else:
+        thr = int(fiber_threshold)
+        if thr < 1:
+            raise ConfigError(f"fiber_threshold must be >= 1, got {fiber_threshold}")
+    i32 = dict(dtype=torch.int32, device="cuda")
+    leaf_vals = torch.empty(nnz, dtype=torch.float32, device="cuda")
+    inds = [torch.empty(nnz, **i32) for _ in range(N)]
+    ptrs = [torch.empty(nnz + 1, **i32) for _ in range(N - 1)]
+    fiber_ptr = torch.empty(nnz + 1, **i32)
+    fiber_coord = torch.empty(nnz * (N - 1), **i32)
+    sub_fiber_ptr = torch.empty(nnz + 1, **i32)
+    sub_leaf_ptr = torch.empty(nnz + 1, **i32)
+    row_fiber_ptr = torch.empty(nnz + 1, **i32)
+    row_coord = torch.empty(nnz, **i32)
+    counts = np.zeros(4 + N, dtype=np.int64)
+    dims = (ctypes.c_int64 * N)(*dev.dims)
+    ind_tab = (ctypes.c_void_p * N)(*[a.data_ptr() for a in inds])
+    ptr_tab = (ctypes.c_void_p * max(N - 1, 1))(*[a.data_ptr() for a in ptrs])
+    rc = L.ft_build_tree(N, nnz, dims, dev.idx.data_ptr(), dev.vals.data_ptr(), root_mode, thr,
+                         leaf_vals.data_ptr(), ind_tab, ptr_tab, fiber_ptr.data_ptr(),
+                         fiber_coord.data_ptr(), sub_fiber_ptr.data_ptr(), sub_leaf_ptr.data_ptr(),
+                         row_fiber_ptr.data_ptr(), row_coord.data_ptr(),
+                         counts.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                         _lib.stream_handle(stream))
+    if rc == _lib.FT_ERR_DUPLICATE:
+        e = int(counts[3])
+        coord = dev.idx[e].cpu().numpy()
+        from .errors import ValidationError
+
+        raise ValidationError(f"duplicate coordinate {tuple(int(c) + 1 for c in coord)}")
+    _lib.check(rc, "ft_build_tree")
+    F, S, rows = int(counts[0]), int(counts[1]), int(counts[2])
+    nodes = [int(c) for c in counts[4:4 + N]]
+    # trim capacity buffers to their real sizes (copies, so the big buffers are released)
+    return CsfTree(
+        root_mode=root_mode,
+        level_modes=tuple((root_mode + d) % N for d in range(N)),
+        dims=tuple(dev.dims),
+        inds=tuple(inds[d][: nodes[d]].clone() if nodes[d] < nnz else inds[d] for d in range(N)),
+        ptrs=tuple(ptrs[d][: nodes[d] + 1].clone() for d in range(N - 1)),
+        vals=leaf_vals,
+        fiber_ptr=fiber_ptr[: F + 1].clone(),
+        fiber_coord=fiber_coord[: F * (N - 1)].view(F, N - 1).clone(),
+        sub_fiber_ptr=sub_fiber_ptr[: S + 1].clone(),
+        sub_leaf_ptr=sub_leaf_ptr[: S + 1].clone(),
+        row_fiber_ptr=row_fiber_ptr[: rows + 1].clone(),
+        row_coord=row_coord[:rows].clone(),
+    )
+
+
+def build_forest(tensor, fiber_threshold=DEFAULT_FIBER_THRESHOLD, stream=None) -> CsfForest:
+    dev = as_device(tensor)
+    trees = tuple(build_tree(dev, t, fiber_threshold, stream) for t in range(dev.order))
+    return CsfForest(trees=trees, fiber_threshold=fiber_threshold)

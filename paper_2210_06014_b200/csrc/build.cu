@@ -1,0 +1,365 @@
+// K1  B-CSF builder on the GPU (replaces csf.build_tree, csf.py:101-196).
+//
+// Pipeline (every step a data-parallel device primitive; no host loop over entries):
+//   1. pack the coordinates in cyclic level order (root, root+1, ...) into <=64-bit keys;
+//      > 64 key bits run several stable LSD radix passes (least significant level chunk first),
+//      which is exactly np.lexsort's order (csf.py:120-124).  Coordinates are unique
+//      (coo.py:56-59), so any correct sort is bit-exact.
+//   2. gather the sorted level columns K_d and values; first-differing-level per entry (fdl).
+//   3. fiber starts = fdl <= N-2 (csf.py:126-133); root runs over fibers; greedy split of each
+//      run into ceil(len/thr) chunks of whole fibers (csf.py:136-148).
+//   4. node starts per depth = (fdl <= d) | subtensor start (csf.py:157-166); inds / ptrs by
+//      compaction and an exclusive scan of the next depth's starts (csf.py:168-178).
+//   5. fiber_coord, sub_leaf_ptr (csf.py:180-183) and the row (root slice) index the exact
+//      row-owner kernels walk.
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include <vector>
+
+#include "ft_common.cuh"
+
+namespace ft {
+namespace {
+
+struct Scratch {
+  cudaStream_t s;
+  std::vector<void *> ptrs;
+  explicit Scratch(cudaStream_t st) : s(st) {}
+  ~Scratch() {
+    for (void *p : ptrs) cudaFreeAsync(p, s);
+  }
+  template <class T>
+  T *get(size_t n) {
+    void *p = nullptr;
+    if (cudaMallocAsync(&p, n * sizeof(T) + 16, s) != cudaSuccess) return nullptr;
+    ptrs.push_back(p);
+    return static_cast<T *>(p);
+  }
+};
+
+struct LevelChunk {
+  int d0, d1;  // levels [d0, d1)
+  int shift[FT_MAX_ORDER];
+  int bits;
+};
+
+struct PackArgs {
+  int N;
+  int lm[FT_MAX_ORDER];  // level -> mode
+  int d0, d1;
+  int shift[FT_MAX_ORDER];
+};
+
+__global__ void pack_keys(const int32_t *__restrict__ idx, const int32_t *__restrict__ perm,
+                          int64_t nnz, PackArgs a, uint64_t *__restrict__ keys,
+                          int32_t *__restrict__ iota_out) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= nnz) return;
+  int64_t e = perm ? perm[p] : p;
+  if (iota_out) iota_out[p] = (int32_t)p;
+  const int32_t *row = idx + e * a.N;
+  uint64_t k = 0;
+  for (int d = a.d0; d < a.d1; ++d) k |= (uint64_t)(uint32_t)row[a.lm[d]] << a.shift[d];
+  keys[p] = k;
+}
+
+struct GatherArgs {
+  int N;
+  int lm[FT_MAX_ORDER];
+  int32_t *K[FT_MAX_ORDER];
+};
+
+// K_d[p] = idx[perm[p], lm[d]]; vals; fdl[p] = first level where entry p differs from p-1.
+__global__ void gather_levels(const int32_t *__restrict__ idx, const float *__restrict__ vals,
+                              const int32_t *__restrict__ perm, int64_t nnz, GatherArgs a,
+                              float *__restrict__ vout, uint8_t *__restrict__ fdl,
+                              unsigned long long *__restrict__ dup_min) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= nnz) return;
+  int64_t e = perm[p];
+  int64_t q = p > 0 ? perm[p - 1] : 0;
+  const int32_t *row = idx + e * a.N;
+  const int32_t *prev = idx + q * a.N;
+  int first = p == 0 ? 0 : a.N;
+  for (int d = 0; d < a.N; ++d) {
+    int32_t c = row[a.lm[d]];
+    a.K[d][p] = c;
+    if (p > 0 && first == a.N && c != prev[a.lm[d]]) first = d;
+  }
+  vout[p] = vals[e];
+  fdl[p] = (uint8_t)first;
+  if (first == a.N) atomicMin(dup_min, (unsigned long long)e);
+}
+
+__global__ void flags_le(const uint8_t *__restrict__ fdl, const uint8_t *__restrict__ extra,
+                         int64_t n, int lim, uint8_t *__restrict__ out) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  out[p] = (fdl[p] <= lim) || (extra && extra[p]);
+}
+
+// root run flags over fibers: fiber f starts a new root slice iff level 0 changed at its first leaf
+__global__ void run_flags(const int32_t *__restrict__ fiber_ptr, const uint8_t *__restrict__ fdl,
+                          int64_t F, uint8_t *__restrict__ out) {
+  int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (f >= F) return;
+  out[f] = fdl[fiber_ptr[f]] == 0;
+}
+
+__global__ void chunk_counts(const int32_t *__restrict__ run_start, int64_t nruns, int64_t F,
+                             int64_t thr, int32_t *__restrict__ nch) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= nruns) return;
+  int64_t len = (r + 1 < nruns ? run_start[r + 1] : F) - run_start[r];
+  nch[r] = thr > 0 ? (int32_t)((len + thr - 1) / thr) : 1;
+}
+
+__global__ void write_chunks(const int32_t *__restrict__ run_start,
+                             const int32_t *__restrict__ nch, const int32_t *__restrict__ off,
+                             int64_t nruns, int64_t thr, const int32_t *__restrict__ fiber_ptr,
+                             int32_t *__restrict__ sub_fiber_ptr,
+                             int32_t *__restrict__ sub_leaf_ptr, uint8_t *__restrict__ subflag) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= nruns) return;
+  int32_t n = nch[r], o = off[r], s0 = run_start[r];
+  for (int32_t c = 0; c < n; ++c) {
+    int32_t f = s0 + (int32_t)(c * (thr > 0 ? thr : 0));
+    int32_t leaf = fiber_ptr[f];
+    sub_fiber_ptr[o + c] = f;
+    sub_leaf_ptr[o + c] = leaf;
+    subflag[leaf] = 1;
+  }
+}
+
+__global__ void gather_i32(const int32_t *__restrict__ src, const int32_t *__restrict__ pos,
+                           int64_t n, int32_t *__restrict__ dst, int64_t dst_stride) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  dst[k * dst_stride] = src[pos[k]];
+}
+
+__global__ void set_i32(int32_t *p, int32_t v) { *p = v; }
+
+inline unsigned blocks_for(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
+
+// Compaction of the positions whose flag is set: out[k] = k-th set position; returns count.
+struct Compactor {
+  cudaStream_t s;
+  Scratch &sc;
+  int64_t *d_count;
+  int64_t n_max;
+  void *tmp = nullptr;
+  size_t tmp_bytes = 0;
+  Compactor(cudaStream_t st, Scratch &scr, int64_t nmax) : s(st), sc(scr), n_max(nmax) {
+    d_count = sc.get<int64_t>(1);
+    thrust::counting_iterator<int32_t> it(0);
+    cub::DeviceSelect::Flagged(nullptr, tmp_bytes, it, (const uint8_t *)nullptr,
+                               (int32_t *)nullptr, d_count, nmax, s);
+    tmp = sc.get<uint8_t>(tmp_bytes);
+  }
+  int run(const uint8_t *flags, int64_t n, int32_t *out, int64_t *host_count) {
+    thrust::counting_iterator<int32_t> it(0);
+    size_t b = tmp_bytes;
+    FT_CUDA(cub::DeviceSelect::Flagged(tmp, b, it, flags, out, d_count, n, s));
+    FT_CUDA(cudaMemcpyAsync(host_count, d_count, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    FT_CUDA(cudaStreamSynchronize(s));
+    return FT_OK;
+  }
+};
+
+}  // namespace
+}  // namespace ft
+
+using namespace ft;
+
+extern "C" int ft_build_tree(int32_t N, int64_t nnz, const int64_t *dims, const int32_t *idx,
+                             const float *vals, int32_t root_mode, int64_t thr, float *leaf_vals,
+                             int32_t *const *inds, int32_t *const *ptrs, int32_t *fiber_ptr,
+                             int32_t *fiber_coord, int32_t *sub_fiber_ptr, int32_t *sub_leaf_ptr,
+                             int32_t *row_fiber_ptr, int32_t *row_coord, int64_t *counts_out,
+                             void *stream) {
+  if (N < 2 || N > FT_MAX_ORDER) return fail(FT_ERR_ARG, "ft_build_tree: order %d unsupported", N);
+  if (nnz <= 0) return fail(FT_ERR_EMPTY, "cannot index an empty tensor");
+  if (nnz >= (int64_t)INT32_MAX) return fail(FT_ERR_UNSUPPORTED, "nnz %lld >= 2^31", (long long)nnz);
+  if (root_mode < 0 || root_mode >= N) return fail(FT_ERR_ARG, "root_mode out of range");
+  if (!dims || !idx || !vals || !leaf_vals || !inds || !ptrs || !fiber_ptr || !fiber_coord ||
+      !sub_fiber_ptr || !sub_leaf_ptr || !row_fiber_ptr || !row_coord || !counts_out)
+    return fail(FT_ERR_ARG, "ft_build_tree: null argument");
+  cudaStream_t s = as_stream(stream);
+  Scratch sc(s);
+
+  int lm[FT_MAX_ORDER], bits[FT_MAX_ORDER];
+  for (int d = 0; d < N; ++d) {
+    lm[d] = (root_mode + d) % N;
+    int64_t I = dims[lm[d]];
+    if (I < 1 || I > (int64_t)INT32_MAX) return fail(FT_ERR_ARG, "dim %lld unsupported", (long long)I);
+    bits[d] = I <= 1 ? 0 : 64 - __builtin_clzll((unsigned long long)(I - 1));
+  }
+  // level chunks of <= 64 bits, built from the last level backwards (LSD order)
+  std::vector<LevelChunk> chunks;
+  {
+    int d1 = N;
+    while (d1 > 0) {
+      LevelChunk c{};
+      c.d1 = d1;
+      int tot = 0, d = d1;
+      while (d > 0 && tot + bits[d - 1] <= 64) {
+        tot += bits[d - 1];
+        --d;
+      }
+      c.d0 = d;
+      int sh = 0;
+      for (int k = d1 - 1; k >= d; --k) {
+        c.shift[k] = sh;
+        sh += bits[k];
+      }
+      c.bits = tot;
+      chunks.push_back(c);
+      d1 = d;
+    }
+  }
+
+  uint64_t *k0 = sc.get<uint64_t>(nnz), *k1 = sc.get<uint64_t>(nnz);
+  int32_t *p0 = sc.get<int32_t>(nnz), *p1 = sc.get<int32_t>(nnz);
+  if (!k0 || !k1 || !p0 || !p1) return fail(FT_ERR_CUDA, "ft_build_tree: out of device memory");
+  size_t sort_bytes = 0;
+  FT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, k0, k1, p0, p1, nnz, 0, 64, s));
+  void *sort_tmp = sc.get<uint8_t>(sort_bytes);
+  if (!sort_tmp) return fail(FT_ERR_CUDA, "ft_build_tree: out of device memory (sort)");
+
+  const unsigned nb = blocks_for(nnz);
+  int32_t *perm = nullptr;  // current permutation (sorted position -> entry)
+  for (size_t ci = 0; ci < chunks.size(); ++ci) {
+    const LevelChunk &c = chunks[ci];
+    PackArgs pa{};
+    pa.N = N;
+    for (int d = 0; d < N; ++d) pa.lm[d] = lm[d];
+    pa.d0 = c.d0;
+    pa.d1 = c.d1;
+    for (int d = c.d0; d < c.d1; ++d) pa.shift[d] = c.shift[d];
+    int32_t *vin = (ci == 0) ? p0 : perm;
+    int32_t *vout = (vin == p0) ? p1 : p0;
+    pack_keys<<<nb, 256, 0, s>>>(idx, ci == 0 ? nullptr : perm, nnz, pa, k0,
+                                 ci == 0 ? p0 : nullptr);
+    if (int rc = check_launch("pack_keys")) return rc;
+    if (c.bits > 0) {
+      size_t b = sort_bytes;
+      FT_CUDA(cub::DeviceRadixSort::SortPairs(sort_tmp, b, k0, k1, vin, vout, nnz, 0, c.bits, s));
+      perm = vout;
+    } else {
+      perm = vin;
+    }
+  }
+
+  // sorted level columns (the leaf level goes straight to inds[N-1] = leaf_coord)
+  GatherArgs ga{};
+  ga.N = N;
+  for (int d = 0; d < N; ++d) {
+    ga.lm[d] = lm[d];
+    ga.K[d] = (d == N - 1) ? inds[N - 1] : sc.get<int32_t>(nnz);
+    if (!ga.K[d]) return fail(FT_ERR_CUDA, "ft_build_tree: out of device memory (levels)");
+  }
+  uint8_t *fdl = sc.get<uint8_t>(nnz);
+  unsigned long long *dup = sc.get<unsigned long long>(1);
+  FT_CUDA(cudaMemsetAsync(dup, 0xff, sizeof(unsigned long long), s));
+  gather_levels<<<nb, 256, 0, s>>>(idx, vals, perm, nnz, ga, leaf_vals, fdl, dup);
+  if (int rc = check_launch("gather_levels")) return rc;
+  unsigned long long hdup = 0;
+  FT_CUDA(cudaMemcpyAsync(&hdup, dup, sizeof(hdup), cudaMemcpyDeviceToHost, s));
+  FT_CUDA(cudaStreamSynchronize(s));
+  for (int k = 0; k < 4 + N; ++k) counts_out[k] = 0;
+  counts_out[3] = -1;
+  if (hdup != ~0ull) {
+    counts_out[3] = (int64_t)hdup;
+    return fail(FT_ERR_DUPLICATE, "duplicate coordinate at entry %lld", (long long)hdup);
+  }
+
+  Compactor comp(s, sc, nnz + 1);
+  uint8_t *flagA = sc.get<uint8_t>(nnz), *flagB = sc.get<uint8_t>(nnz);
+  uint8_t *subflag = sc.get<uint8_t>(nnz);
+  int32_t *scan = sc.get<int32_t>(nnz + 1);
+  int32_t *pos = sc.get<int32_t>(nnz + 1);
+  if (!flagA || !flagB || !subflag || !scan || !pos)
+    return fail(FT_ERR_CUDA, "ft_build_tree: out of device memory (flags)");
+
+  // fibers: runs of equal first N-1 levels
+  int64_t F = 0;
+  flags_le<<<nb, 256, 0, s>>>(fdl, nullptr, nnz, N - 2, flagA);
+  if (int rc = comp.run(flagA, nnz, fiber_ptr, &F)) return rc;
+  set_i32<<<1, 1, 0, s>>>(fiber_ptr + F, (int32_t)nnz);
+
+  // root slices over fibers
+  uint8_t *rflag = sc.get<uint8_t>(F);
+  run_flags<<<blocks_for(F), 256, 0, s>>>(fiber_ptr, fdl, F, rflag);
+  int64_t nruns = 0;
+  if (int rc = comp.run(rflag, F, row_fiber_ptr, &nruns)) return rc;
+  set_i32<<<1, 1, 0, s>>>(row_fiber_ptr + nruns, (int32_t)F);
+  // row_coord[r] = K_0[fiber_ptr[row_fiber_ptr[r]]]
+  {
+    int32_t *first_leaf = sc.get<int32_t>(nruns);
+    gather_i32<<<blocks_for(nruns), 256, 0, s>>>(fiber_ptr, row_fiber_ptr, nruns, first_leaf, 1);
+    gather_i32<<<blocks_for(nruns), 256, 0, s>>>(ga.K[0], first_leaf, nruns, row_coord, 1);
+  }
+
+  // greedy split of each root slice into <= thr whole fibers (csf.py:136-148)
+  int32_t *nch = sc.get<int32_t>(nruns), *off = sc.get<int32_t>(nruns + 1);
+  chunk_counts<<<blocks_for(nruns), 256, 0, s>>>(row_fiber_ptr, nruns, F, thr, nch);
+  {
+    size_t b = 0;
+    FT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b, nch, off, nruns + 1, s));
+    void *t = sc.get<uint8_t>(b);
+    // off has nruns+1 entries: scan over nch padded with a trailing read is unsafe, so scan
+    // nruns entries and compute the total separately.
+    FT_CUDA(cub::DeviceScan::ExclusiveSum(t, b, nch, off, nruns, s));
+  }
+  int32_t hlast[2] = {0, 0};
+  FT_CUDA(cudaMemcpyAsync(&hlast[0], off + nruns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  FT_CUDA(cudaMemcpyAsync(&hlast[1], nch + nruns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  FT_CUDA(cudaStreamSynchronize(s));
+  const int64_t S = (int64_t)hlast[0] + hlast[1];
+  FT_CUDA(cudaMemsetAsync(subflag, 0, nnz, s));
+  write_chunks<<<blocks_for(nruns), 256, 0, s>>>(row_fiber_ptr, nch, off, nruns, thr, fiber_ptr,
+                                                 sub_fiber_ptr, sub_leaf_ptr, subflag);
+  if (int rc = check_launch("write_chunks")) return rc;
+  set_i32<<<1, 1, 0, s>>>(sub_fiber_ptr + S, (int32_t)F);
+  set_i32<<<1, 1, 0, s>>>(sub_leaf_ptr + S, (int32_t)nnz);
+
+  // fiber_coord[f, d] = K_d[fiber_ptr[f]]
+  for (int d = 0; d < N - 1; ++d)
+    gather_i32<<<blocks_for(F), 256, 0, s>>>(ga.K[d], fiber_ptr, F, fiber_coord + d, N - 1);
+
+  // per-depth node starts; inds / ptrs.  Depth N-1: every leaf (inds[N-1] already written).
+  counts_out[4 + N - 1] = nnz;
+  int64_t n_next = nnz;
+  uint8_t *flag_next = nullptr;  // flags of depth d+1 (null => all ones)
+  size_t scan_bytes = 0;
+  FT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, flagA, scan, nnz, s));
+  void *scan_tmp = sc.get<uint8_t>(scan_bytes);
+  uint8_t *fl[2] = {flagA, flagB};
+  for (int d = N - 2; d >= 0; --d) {
+    uint8_t *flag_d = fl[d & 1];
+    flags_le<<<nb, 256, 0, s>>>(fdl, subflag, nnz, d, flag_d);
+    int64_t n_d = 0;
+    if (int rc = comp.run(flag_d, nnz, pos, &n_d)) return rc;
+    gather_i32<<<blocks_for(n_d), 256, 0, s>>>(ga.K[d], pos, n_d, inds[d], 1);
+    if (flag_next == nullptr) {
+      // child id of a start at position p is p itself
+      FT_CUDA(cudaMemcpyAsync(ptrs[d], pos, n_d * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    } else {
+      size_t b = scan_bytes;
+      FT_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp, b, flag_next, scan, nnz, s));
+      gather_i32<<<blocks_for(n_d), 256, 0, s>>>(scan, pos, n_d, ptrs[d], 1);
+    }
+    set_i32<<<1, 1, 0, s>>>(ptrs[d] + n_d, (int32_t)n_next);
+    counts_out[4 + d] = n_d;
+    n_next = n_d;
+    flag_next = flag_d;
+  }
+  if (int rc = check_launch("build_tree")) return rc;
+  FT_CUDA(cudaStreamSynchronize(s));
+  counts_out[0] = F;
+  counts_out[1] = S;
+  counts_out[2] = nruns;
+  return FT_OK;
+}

@@ -223,8 +223,11 @@ def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
 
+    import importlib
+
     import paper_2210_06014_b200 as ft
-    from paper_2210_06014_b200 import train as T
+
+    T = importlib.import_module("paper_2210_06014_b200.train")
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -320,6 +323,15 @@ def run_ours(args, cfg):
             "share_of_step": d["sec"] / total_s}
     kernels = {k: {"ms_total": 1e3 * v["sec"] / args.steps, "GB_per_s": v["bytes"] / v["sec"] / 1e9,
                    "frac": v["bytes"] / v["sec"] / 1e9 / peak} for k, v in by.items()}
+    per_mode = {}
+    for name, mode, sec in krec:
+        key = f"{name}:{mode}"
+        e = per_mode.setdefault(key, {"ms": 0.0, "bytes": kernel_bytes(name, forest.trees[mode],
+                                                                       dims, J, R)})
+        e["ms"] += 1e3 * sec / args.steps
+    for e in per_mode.values():
+        e["frac"] = e["bytes"] / (e["ms"] / 1e3) / 1e9 / peak
+    kernels["by_mode"] = per_mode
     pass_bytes = {"factor": 0, "core": 0}
     for tree_u in forest.trees:
         u = tree_u.root_mode

@@ -113,10 +113,14 @@ FT_API int ft_factor_sweep_rows(const ft_tree_t *tree, const ft_model_t *model, 
                          void *stream);
 
 /* K3a  Hogwild factor sweep over fibers [fib_lo, fib_hi) of a tree rooted at t = (u+1) mod N,
- * i.e. the reference's own traversal (_ckern.pyx:163-191) with one warp per fiber and
- * lock-free racing row updates (train.py:124-149 with workers > 1). */
+ * i.e. the reference's own traversal (_ckern.pyx:163-191) with one warp per 32-fiber batch and
+ * lock-free row updates (train.py:124-149 with workers > 1): each step is computed from a
+ * possibly stale row and added with an L2 atomic, so concurrent steps are never lost.
+ * max_warps > 0 caps the number of concurrently sweeping warps (the staleness bound: the
+ * reference's hogwild runs <= #cores writers; 0 = one persistent grid). */
 FT_API int ft_factor_sweep_fibers(const ft_tree_t *tree, const ft_model_t *model, int64_t fib_lo,
-                           int64_t fib_hi, float lr, float reg, void *stream);
+                           int64_t fib_hi, float lr, float reg, int32_t max_warps,
+                           void *stream);
 
 /* K4  Core-gradient sweep of mode u = tree->root_mode: replaces core_sweep
  * (_ckern.pyx:202-269, train.py:200-236) in its row form acc = -G^T A_u with

@@ -76,7 +76,7 @@ SIGNATURES = {
         ctypes.POINTER(FtTree), ctypes.POINTER(FtModel), ctypes.c_float, ctypes.c_float, _vp]),
     "ft_factor_sweep_fibers": (ctypes.c_int, [
         ctypes.POINTER(FtTree), ctypes.POINTER(FtModel), ctypes.c_int64, ctypes.c_int64,
-        ctypes.c_float, ctypes.c_float, _vp]),
+        ctypes.c_float, ctypes.c_float, ctypes.c_int32, _vp]),
     "ft_core_sweep_rows": (ctypes.c_int, [
         ctypes.POINTER(FtTree), ctypes.POINTER(FtModel), _vp, ctypes.c_int64, _i32p, _vp]),
     "ft_core_partials_size": (ctypes.c_int64, [ctypes.c_int32, ctypes.c_int32]),

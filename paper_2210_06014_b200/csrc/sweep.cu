@@ -68,46 +68,99 @@ __device__ __forceinline__ int batch_fibers(const int32_t *__restrict__ fiber_pt
   return fcur + __popc(mask & (FULL >> (31 - lane)));
 }
 
-// Gather phase (lanes over r): t[k] = prod_{levels} C[coord][lane] for the batch's leaves.
-// Left-to-right chain in the reference's prefix order, leaf level last.
+// ---- cp.async gathers ---------------------------------------------------------------------
+// The gathered C rows land in shared memory without passing through registers, so a warp keeps
+// 32 leaves x (N-1) rows in flight at ~60 registers (the v1 register-array gather needed 155
+// registers and capped the SM at 8 warps).  .ca keeps the lines in L1: consecutive leaves of
+// one fiber share their prefix rows.
+__device__ __forceinline__ void cp_async4(float *dst, const float *src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(src));
+}
+__device__ __forceinline__ void cp_async16(float *dst, const float *src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+// Row stride of a staged [BATCH][RS] tile: RS = RP + 4 keeps 16-B alignment for the vector
+// copies and makes lane-k row reads (float4) bank-conflict free.
 template <int RP>
-__device__ __forceinline__ void gather_cross(const SweepParams &p, int myfib, int lc, int nb,
-                                             int lane, float (&t)[BATCH]) {
-  const bool rl = lane < p.R;
+struct Tile {
+  static constexpr int RS = RP + 4;
+  static constexpr int FLOATS = BATCH * RS;
+};
+
+// Stage rows C[coord_k, 0:R) of the batch's leaves k < nb into dst[k][0:R).  coord_lane holds
+// leaf lane's row index.  R % 4 == 0 uses 16-B copies (R/4 lanes per row).
+template <int RP>
+__device__ __forceinline__ void gather_level(float *dst, const float *__restrict__ C, int R,
+                                             int coord_lane, int nb, int lane) {
+  constexpr int RS = Tile<RP>::RS;
+  if ((R & 3) == 0) {
+    const int R4 = R >> 2, total = nb * R4;
 #pragma unroll
-  for (int d = 0; d < FT_MAX_ORDER - 2; ++d) {
-    if (d >= p.npre) break;
-    const int fc = lane < nb ? __ldg(p.fiber_coord + (int64_t)myfib * (p.N - 1) + 1 + d) : 0;
-    const float *Cd = p.Cpre[d];
-#pragma unroll
+    for (int it = 0; it < RP / 4; ++it) {
+      const int c = lane + 32 * it;
+      const int k = c / R4, part = c - k * R4;
+      const int coord = __shfl_sync(FULL, coord_lane, k & 31);
+      if (c < total) cp_async16(dst + k * RS + part * 4, C + (int64_t)coord * R + part * 4);
+    }
+  } else {
+#pragma unroll 4
     for (int k = 0; k < BATCH; ++k) {
-      const int c = __shfl_sync(FULL, fc, k);
-      const float v = (rl && k < nb) ? __ldg(Cd + (int64_t)c * p.R + lane) : 0.f;
-      t[k] = d == 0 ? v : t[k] * v;
+      const int coord = __shfl_sync(FULL, coord_lane, k);
+      if (k < nb && lane < R) cp_async4(dst + k * RS + lane, C + (int64_t)coord * R + lane);
     }
   }
-#pragma unroll
-  for (int k = 0; k < BATCH; ++k) {
-    const int c = __shfl_sync(FULL, lc, k);
-    const float v = (rl && k < nb) ? __ldg(p.Cleaf + (int64_t)c * p.R + lane) : 0.f;
-    t[k] = t[k] * v;
+}
+
+// cross[k][r] = prod_levels C_level[coord][r] for the batch's leaves, left to right in the
+// reference's prefix order (tree levels 1..N-2, then the leaf level), accumulated in X using Y
+// as the landing buffer of the next level.
+template <int RP>
+__device__ __forceinline__ void stage_cross(const SweepParams &p, float *X, float *Y, int myfib,
+                                            int lc, int nb, int lane) {
+  constexpr int RS = Tile<RP>::RS;
+  const int nlev = p.N - 1;  // N-2 prefix levels + the leaf level
+  for (int lvl = 0; lvl < nlev; ++lvl) {
+    const bool leaf = lvl == nlev - 1;
+    const int coord =
+        leaf ? lc : (lane < nb ? __ldg(p.fiber_coord + (int64_t)myfib * (p.N - 1) + 1 + lvl) : 0);
+    gather_level<RP>(lvl == 0 ? X : Y, leaf ? p.Cleaf : p.Cpre[lvl], p.R, coord, nb, lane);
+    if (lvl >= 1) {
+      cp_async_wait_all();
+      __syncwarp();
+      if (lane < RP) {
+        for (int k = 0; k < nb; ++k) X[k * RS + lane] *= Y[k * RS + lane];
+      }
+      __syncwarp();
+    }
   }
 }
 
 // ------------------------------------------------------------------------------------------
 // K3b: exact row-owner factor sweep
 // ------------------------------------------------------------------------------------------
+constexpr int WPB_R = 4;  // warps per block of the row kernels
+
 template <int RP>
-__global__ void __launch_bounds__(WPB * 32)
+__global__ void __launch_bounds__(WPB_R * 32)
     factor_rows_kernel(const SweepParams p) {
-  __shared__ __align__(16) float cross_s[WPB][BATCH][RP];
+  extern __shared__ float4 smem4[];
+  constexpr int RS = Tile<RP>::RS;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t gw = (int64_t)blockIdx.x * WPB + w, nw = (int64_t)gridDim.x * WPB;
+  float *X = reinterpret_cast<float *>(smem4) + w * 2 * Tile<RP>::FLOATS;
+  float *Y = X + Tile<RP>::FLOATS;
+  for (int k = lane; k < 2 * Tile<RP>::FLOATS; k += 32) X[k] = 0.f;  // pads stay zero
+  __syncwarp();
+  const int64_t gw = (int64_t)blockIdx.x * WPB_R + w, nw = (int64_t)gridDim.x * WPB_R;
   const bool jl = lane < p.J;
   float bt[RP];
 #pragma unroll
   for (int r = 0; r < RP; ++r) bt[r] = (jl && r < p.R) ? __ldg(p.Bt + r * p.J + lane) : 0.f;
-  float(&cs)[BATCH][RP] = cross_s[w];
 
   for (int64_t row = gw; row < p.nrows; row += nw) {
     const int i = __ldg(p.row_coord + row);
@@ -122,37 +175,25 @@ __global__ void __launch_bounds__(WPB * 32)
       const float x = lane < nb ? __ldcs(p.vals + L0 + lane) : 0.f;
       int fnext;
       const int myfib = batch_fibers(p.fiber_ptr, fcur, fe, L0, nb, lane, &fnext);
-      float t[BATCH];
-      gather_cross<RP>(p, myfib, lc, nb, lane, t);
-      if (lane < RP) {
+      stage_cross<RP>(p, X, Y, myfib, lc, nb, lane);
+      // serial chain; vec_k = sum_r cross[k][r] Bt[r][j] (sequential r, broadcast reads) is
+      // independent of the row, so it overlaps the previous leaf's reduction latency
+#pragma unroll 4
+      for (int k = 0; k < nb; ++k) {
+        const float4 *xr = reinterpret_cast<const float4 *>(X + k * RS);
+        float v = 0.f;
 #pragma unroll
-        for (int k = 0; k < BATCH; ++k) cs[k][lane] = t[k];
-      }
-      __syncwarp();
-      // combine (lanes over j): v[k] = sum_r cross[k][r] * Bt[r][j], sequential r
-      float v[BATCH];
-#pragma unroll
-      for (int k = 0; k < BATCH; ++k) {
-        float acc = 0.f;
-#pragma unroll
-        for (int r = 0; r < RP; r += 4) {
-          const float4 c4 = *reinterpret_cast<const float4 *>(&cs[k][r]);
-          acc = __fmaf_rn(c4.x, bt[r], acc);
-          acc = __fmaf_rn(c4.y, bt[r + 1], acc);
-          acc = __fmaf_rn(c4.z, bt[r + 2], acc);
-          acc = __fmaf_rn(c4.w, bt[r + 3], acc);
+        for (int r4 = 0; r4 < RP / 4; ++r4) {
+          const float4 c4 = xr[r4];
+          v = __fmaf_rn(c4.x, bt[4 * r4], v);
+          v = __fmaf_rn(c4.y, bt[4 * r4 + 1], v);
+          v = __fmaf_rn(c4.z, bt[4 * r4 + 2], v);
+          v = __fmaf_rn(c4.w, bt[4 * r4 + 3], v);
         }
-        v[k] = acc;
-      }
-      // serial chain over the batch: s = a.v, e = x - s, a -= lr (reg a - e v)
-#pragma unroll
-      for (int k = 0; k < BATCH; ++k) {
-        if (k < nb) {
-          const float s = warp_sum(a * v[k]);
-          const float e = __shfl_sync(FULL, x, k) - s;
-          const float g = p.reg * a - e * v[k];
-          a = a - p.lr * g;
-        }
+        const float s = warp_sum(a * v);
+        const float e = __shfl_sync(FULL, x, k) - s;
+        const float g = p.reg * a - e * v;
+        a = a - p.lr * g;
       }
       __syncwarp();
       fcur = fnext;
@@ -165,12 +206,17 @@ __global__ void __launch_bounds__(WPB * 32)
 // K4: core-gradient row sweep; per-block partials of G^T A_u (acc = -partials summed)
 // ------------------------------------------------------------------------------------------
 template <int RP>
-__global__ void __launch_bounds__(WPB * 32, 1)
+__global__ void __launch_bounds__(WPB_R * 32)
     core_rows_kernel(const SweepParams p) {
-  __shared__ __align__(16) float e_s[WPB][BATCH];
-  __shared__ float red[WPB][FT_MAX_RANK * FT_MAX_RANK];
+  extern __shared__ float4 smem4[];
+  constexpr int RS = Tile<RP>::RS;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t gw = (int64_t)blockIdx.x * WPB + w, nw = (int64_t)gridDim.x * WPB;
+  float *X = reinterpret_cast<float *>(smem4) + w * (2 * Tile<RP>::FLOATS + RS);
+  float *Y = X + Tile<RP>::FLOATS;
+  float *cus = Y + Tile<RP>::FLOATS;  // C_u[i, :] of the current row
+  for (int k = lane; k < 2 * Tile<RP>::FLOATS + RS; k += 32) X[k] = 0.f;
+  __syncwarp();
+  const int64_t gw = (int64_t)blockIdx.x * WPB_R + w, nw = (int64_t)gridDim.x * WPB_R;
   const bool rl = lane < p.R;
   float acc[FT_MAX_RANK];  // lane r: acc[j] = sum_i g_i[r] A_u[i, j]
 #pragma unroll
@@ -180,7 +226,7 @@ __global__ void __launch_bounds__(WPB * 32, 1)
     const int i = __ldg(p.row_coord + row);
     const int fb = __ldg(p.row_fiber_ptr + row), fe = __ldg(p.row_fiber_ptr + row + 1);
     const int Lb = __ldg(p.fiber_ptr + fb), Le = __ldg(p.fiber_ptr + fe);
-    const float cu = rl ? __ldg(p.Cu + (int64_t)i * p.R + lane) : 0.f;
+    if (rl) cus[lane] = __ldg(p.Cu + (int64_t)i * p.R + lane);
     float g = 0.f;
     int fcur = fb;
     for (int L0 = Lb; L0 < Le; L0 += BATCH) {
@@ -189,33 +235,27 @@ __global__ void __launch_bounds__(WPB * 32, 1)
       const float x = lane < nb ? __ldcs(p.vals + L0 + lane) : 0.f;
       int fnext;
       const int myfib = batch_fibers(p.fiber_ptr, fcur, fe, L0, nb, lane, &fnext);
-      float t[BATCH];
-      gather_cross<RP>(p, myfib, lc, nb, lane, t);
-      // s_k = sum_r C_u[i,r] t[k][r]: 32 reductions by recursive halving (31 shuffles);
-      // afterwards lane k holds s_k.
-      float q[BATCH];
+      stage_cross<RP>(p, X, Y, myfib, lc, nb, lane);
+      // lane k: s_k = C_u[i] . cross_k  (= A_u[i] . vec_k, since C_u = A_u Bt_u^T is coherent)
+      float s = 0.f;
+      {
+        const float4 *xr = reinterpret_cast<const float4 *>(X + (lane & 31) * RS);
+        const float4 *cr = reinterpret_cast<const float4 *>(cus);
 #pragma unroll
-      for (int k = 0; k < BATCH; ++k) q[k] = cu * t[k];
-#pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) {
-        const bool upper = lane & off;
-#pragma unroll
-        for (int k = 0; k < off; ++k) {
-          const float send = upper ? q[k] : q[k + off];
-          const float keep = upper ? q[k + off] : q[k];
-          q[k] = keep + __shfl_xor_sync(FULL, send, off);
+        for (int r4 = 0; r4 < RP / 4; ++r4) {
+          const float4 a4 = xr[r4], c4 = cr[r4];
+          s = __fmaf_rn(a4.x, c4.x, s);
+          s = __fmaf_rn(a4.y, c4.y, s);
+          s = __fmaf_rn(a4.z, c4.z, s);
+          s = __fmaf_rn(a4.w, c4.w, s);
         }
       }
-      const float e = lane < nb ? x - q[0] : 0.f;
-      e_s[w][lane] = e;
-      __syncwarp();
-#pragma unroll
-      for (int k = 0; k < BATCH; k += 4) {
-        const float4 e4 = *reinterpret_cast<const float4 *>(&e_s[w][k]);
-        g = __fmaf_rn(e4.x, t[k], g);
-        g = __fmaf_rn(e4.y, t[k + 1], g);
-        g = __fmaf_rn(e4.z, t[k + 2], g);
-        g = __fmaf_rn(e4.w, t[k + 3], g);
+      const float e = lane < nb ? x - s : 0.f;
+      // lane r: g_i[r] += sum_k e_k cross_k[r]
+#pragma unroll 4
+      for (int k = 0; k < nb; ++k) {
+        const float ek = __shfl_sync(FULL, e, k);
+        if (lane < RP) g = __fmaf_rn(ek, X[k * RS + lane], g);
       }
       __syncwarp();
       fcur = fnext;
@@ -225,21 +265,33 @@ __global__ void __launch_bounds__(WPB * 32, 1)
 #pragma unroll
     for (int j = 0; j < FT_MAX_RANK; ++j)
       if (j < p.J) acc[j] = __fmaf_rn(g, __ldg(arow + j), acc[j]);
+    __syncwarp();
   }
-  // block reduction in fixed warp order -> partials[block]
+  // block reduction in fixed warp order -> partials[block]; reuses the staging tiles
+  __syncthreads();
+  const int RJ = p.R * p.J;
+  float *red = reinterpret_cast<float *>(smem4);
+  const int wstride = 2 * Tile<RP>::FLOATS + RS;
   if (rl) {
 #pragma unroll
     for (int j = 0; j < FT_MAX_RANK; ++j)
-      if (j < p.J) red[w][lane * p.J + j] = acc[j];
+      if (j < p.J) red[w * wstride + lane * p.J + j] = acc[j];
   }
   __syncthreads();
-  const int RJ = p.R * p.J;
   for (int k = threadIdx.x; k < RJ; k += blockDim.x) {
     float s = 0.f;
-#pragma unroll
-    for (int ww = 0; ww < WPB; ++ww) s += red[ww][k];
+    for (int ww = 0; ww < WPB_R; ++ww) s += red[ww * wstride + k];
     p.partials[(int64_t)blockIdx.x * RJ + k] = s;
   }
+}
+
+template <int RP>
+constexpr size_t factor_smem() {
+  return (size_t)WPB_R * 2 * Tile<RP>::FLOATS * sizeof(float);
+}
+template <int RP>
+constexpr size_t core_smem() {
+  return (size_t)WPB_R * (2 * Tile<RP>::FLOATS + Tile<RP>::RS) * sizeof(float);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -264,8 +316,8 @@ __global__ void __launch_bounds__(WPB * 32)
     factor_fibers_kernel(const FiberParams p) {
   // one buffer per warp: first the rank products (cross, stride RP), then the batch's vecs
   __shared__ __align__(16) float buf_s[WPB][BATCH * (FT_MAX_RANK + 4)];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t gw = (int64_t)blockIdx.x * WPB + w, nw = (int64_t)gridDim.x * WPB;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * wpb + w, nw = (int64_t)gridDim.x * wpb;
   const bool jl = lane < p.J, rl = lane < p.R;
   float bt[RP];
 #pragma unroll
@@ -336,7 +388,9 @@ __global__ void __launch_bounds__(WPB * 32)
           const float e = __shfl_sync(FULL, x, k) - s;
           const float g = p.reg * a[k] - e * vj;
           const int i = __shfl_sync(FULL, lc, k);
-          if (jl) p.A[(int64_t)i * p.J + lane] = a[k] - p.lr * g;
+          // lock-free: the step is computed from a possibly stale row (hogwild) but is never
+          // lost -- concurrent writers of one row accumulate through L2 atomics (RED.ADD)
+          if (jl) atomicAdd(p.A + (int64_t)i * p.J + lane, -p.lr * g);
         }
       }
       fcur = fnext;
@@ -370,16 +424,36 @@ __global__ void core_apply_kernel(int RJ, float *Bt, const float *__restrict__ p
 
 // Persistent grid: as many blocks as can be co-resident (occupancy API), capped by the work.
 template <class Kern>
-inline int grid_for(Kern kern, int64_t work_warps) {
+inline int grid_for(Kern kern, int64_t work_warps, int wpb = WPB, size_t smem = 0) {
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WPB * 32, 0) != cudaSuccess ||
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpb * 32, smem) !=
+          cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
-  int64_t g = (work_warps + WPB - 1) / WPB;
+  int64_t g = (work_warps + wpb - 1) / wpb;
   const int64_t cap = (int64_t)sm_count() * per_sm;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
   return (int)g;
+}
+
+template <int RP>
+int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
+  const size_t sm = factor_smem<RP>();
+  const int g = grid_for(factor_rows_kernel<RP>, p.nrows, WPB_R, sm);
+  factor_rows_kernel<RP><<<g, WPB_R * 32, sm, s>>>(p);
+  return check_launch("ft_factor_sweep_rows");
+}
+
+template <int RP>
+int core_rows_grid(const SweepParams &p) {
+  return grid_for(core_rows_kernel<RP>, p.nrows, WPB_R, core_smem<RP>());
+}
+
+template <int RP>
+int launch_core_rows(const SweepParams &p, int g, cudaStream_t s) {
+  core_rows_kernel<RP><<<g, WPB_R * 32, core_smem<RP>(), s>>>(p);
+  return check_launch("ft_core_sweep_rows");
 }
 
 int fill_rows_params(SweepParams &p, const ft_tree_t *tree, const ft_model_t *m) {
@@ -427,17 +501,13 @@ extern "C" int ft_factor_sweep_rows(const ft_tree_t *tree, const ft_model_t *mod
   p.reg = reg;
   if (p.nrows == 0) return FT_OK;
   cudaStream_t s = as_stream(stream);
-  if (p.R <= 8)
-    factor_rows_kernel<8><<<grid_for(factor_rows_kernel<8>, p.nrows), WPB * 32, 0, s>>>(p);
-  else if (p.R <= 16)
-    factor_rows_kernel<16><<<grid_for(factor_rows_kernel<16>, p.nrows), WPB * 32, 0, s>>>(p);
-  else
-    factor_rows_kernel<32><<<grid_for(factor_rows_kernel<32>, p.nrows), WPB * 32, 0, s>>>(p);
-  return check_launch("ft_factor_sweep_rows");
+  if (p.R <= 8) return launch_factor_rows<8>(p, s);
+  if (p.R <= 16) return launch_factor_rows<16>(p, s);
+  return launch_factor_rows<32>(p, s);
 }
 
 extern "C" int64_t ft_core_partials_size(int32_t R, int32_t J) {
-  return (int64_t)ft::sm_count() * 8 * R * J;  // >= any co-resident grid of core_rows_kernel
+  return (int64_t)ft::sm_count() * 32 * R * J;  // >= any co-resident grid of core_rows_kernel
 }
 
 extern "C" int ft_core_sweep_rows(const ft_tree_t *tree, const ft_model_t *model,
@@ -448,25 +518,21 @@ extern "C" int ft_core_sweep_rows(const ft_tree_t *tree, const ft_model_t *model
   if (!p.Cu) return fail(FT_ERR_ARG, "core sweep needs dots[u] (coherent cache)");
   if (!partials || !nblocks_out) return fail(FT_ERR_ARG, "null partials");
   p.partials = partials;
-  const int g = p.R <= 8    ? grid_for(core_rows_kernel<8>, p.nrows)
-                : p.R <= 16 ? grid_for(core_rows_kernel<16>, p.nrows)
-                            : grid_for(core_rows_kernel<32>, p.nrows);
+  const int g = p.R <= 8 ? core_rows_grid<8>(p) : p.R <= 16 ? core_rows_grid<16>(p)
+                                                            : core_rows_grid<32>(p);
   if ((int64_t)g * p.R * p.J > partials_cap)
     return fail(FT_ERR_ARG, "partials buffer too small (%lld < %lld)", (long long)partials_cap,
                 (long long)g * p.R * p.J);
   cudaStream_t s = as_stream(stream);
-  if (p.R <= 8)
-    core_rows_kernel<8><<<g, WPB * 32, 0, s>>>(p);
-  else if (p.R <= 16)
-    core_rows_kernel<16><<<g, WPB * 32, 0, s>>>(p);
-  else
-    core_rows_kernel<32><<<g, WPB * 32, 0, s>>>(p);
   *nblocks_out = g;
-  return check_launch("ft_core_sweep_rows");
+  if (p.R <= 8) return launch_core_rows<8>(p, g, s);
+  if (p.R <= 16) return launch_core_rows<16>(p, g, s);
+  return launch_core_rows<32>(p, g, s);
 }
 
 extern "C" int ft_factor_sweep_fibers(const ft_tree_t *tree, const ft_model_t *m, int64_t fib_lo,
-                                      int64_t fib_hi, float lr, float reg, void *stream) {
+                                      int64_t fib_hi, float lr, float reg, int32_t max_warps,
+                                      void *stream) {
   if (!tree || !m) return fail(FT_ERR_ARG, "null tree/model");
   const int N = tree->order;
   if (N < 3 || N > FT_MAX_ORDER || m->order != N) return fail(FT_ERR_ARG, "order mismatch");
@@ -492,14 +558,16 @@ extern "C" int ft_factor_sweep_fibers(const ft_tree_t *tree, const ft_model_t *m
     return fail(FT_ERR_ARG, "fiber range [%lld, %lld) invalid", (long long)fib_lo,
                 (long long)fib_hi);
   if (fib_hi == fib_lo) return FT_OK;
-  const int64_t work = (fib_hi - fib_lo + BATCH - 1) / BATCH;
+  int64_t work = (fib_hi - fib_lo + BATCH - 1) / BATCH;
+  if (max_warps > 0 && work > max_warps) work = max_warps;
+  const int wpb = work < WPB ? (int)work : WPB;
   cudaStream_t s = as_stream(stream);
   if (p.R <= 8)
-    factor_fibers_kernel<8><<<grid_for(factor_fibers_kernel<8>, work), WPB * 32, 0, s>>>(p);
+    factor_fibers_kernel<8><<<grid_for(factor_fibers_kernel<8>, work), wpb * 32, 0, s>>>(p);
   else if (p.R <= 16)
-    factor_fibers_kernel<16><<<grid_for(factor_fibers_kernel<16>, work), WPB * 32, 0, s>>>(p);
+    factor_fibers_kernel<16><<<grid_for(factor_fibers_kernel<16>, work), wpb * 32, 0, s>>>(p);
   else
-    factor_fibers_kernel<32><<<grid_for(factor_fibers_kernel<32>, work), WPB * 32, 0, s>>>(p);
+    factor_fibers_kernel<32><<<grid_for(factor_fibers_kernel<32>, work), wpb * 32, 0, s>>>(p);
   return check_launch("ft_factor_sweep_fibers");
 }
 

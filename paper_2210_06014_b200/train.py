@@ -233,8 +233,10 @@ def update_factor_mode(model, forest: CsfForest, cache: DotCache | None, n: int,
                        "ft_factor_sweep_rows")
     else:
         with _ktime("factor_fibers", u):
+            # staleness bound: <= 32 concurrent leaf updates per 256 rows of A_u
+            cap = max(1, model.dims[u] // 256)
             _lib.check(L.ft_factor_sweep_fibers(ctypes.byref(tree.view()), ctypes.byref(mv), 0,
-                                                tree.num_fibers, cfg.lr_a, cfg.reg_a, stream),
+                                                tree.num_fibers, cfg.lr_a, cfg.reg_a, cap, stream),
                        "ft_factor_sweep_fibers")
     total = sweep_counts("factor", cfg.plan, N, model.core_rank, model.ranks, tree.prefix_modes,
                          u, tree.nnz, tree.num_fibers)

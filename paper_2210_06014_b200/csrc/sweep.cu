@@ -28,6 +28,9 @@
 //     blocks by K5 -- no global atomics.
 //   * K3a is the reference's own traversal (warp per fiber batch over tree t) with hogwild
 //     (racing, lock-free) row updates, used for the workers>1 semantics.
+#include <stdlib.h>
+#include <string.h>
+
 #include "ft_common.cuh"
 
 namespace ft {
@@ -85,6 +88,17 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
+// Packed fp32x2 FMA (sm_100 FFMA2): d = a * b + c on both halves.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<unsigned long long *>(&a)),
+        "l"(*reinterpret_cast<unsigned long long *>(&b)),
+        "l"(*reinterpret_cast<unsigned long long *>(&c)));
+  return *reinterpret_cast<float2 *>(&d);
+}
+
 // Row stride of a staged [BATCH][RS] tile: RS = RP + 4 keeps 16-B alignment for the vector
 // copies and makes lane-k row reads (float4) bank-conflict free.
 template <int RP>
@@ -100,13 +114,14 @@ __device__ __forceinline__ void gather_level(float *dst, const float *__restrict
                                              int coord_lane, int nb, int lane) {
   constexpr int RS = Tile<RP>::RS;
   if ((R & 3) == 0) {
-    const int R4 = R >> 2, total = nb * R4;
+    constexpr int P4 = RP / 4;  // 16-B chunks per padded row (compile time: shifts, no divide)
+    const int R4 = R >> 2;
 #pragma unroll
-    for (int it = 0; it < RP / 4; ++it) {
+    for (int it = 0; it < P4; ++it) {
       const int c = lane + 32 * it;
-      const int k = c / R4, part = c - k * R4;
-      const int coord = __shfl_sync(FULL, coord_lane, k & 31);
-      if (c < total) cp_async16(dst + k * RS + part * 4, C + (int64_t)coord * R + part * 4);
+      const int k = c / P4, part = c % P4;
+      const int coord = __shfl_sync(FULL, coord_lane, k);
+      if (k < nb && part < R4) cp_async16(dst + k * RS + part * 4, C + (int64_t)coord * R + part * 4);
     }
   } else {
 #pragma unroll 4
@@ -120,9 +135,10 @@ __device__ __forceinline__ void gather_level(float *dst, const float *__restrict
 // cross[k][r] = prod_levels C_level[coord][r] for the batch's leaves, left to right in the
 // reference's prefix order (tree levels 1..N-2, then the leaf level), accumulated in X using Y
 // as the landing buffer of the next level.
+// With fold_leaf = false the leaf level is left in Y (cross = X * Y, folded by the caller).
 template <int RP>
 __device__ __forceinline__ void stage_cross(const SweepParams &p, float *X, float *Y, int myfib,
-                                            int lc, int nb, int lane) {
+                                            int lc, int nb, int lane, bool fold_leaf = true) {
   constexpr int RS = Tile<RP>::RS;
   const int nlev = p.N - 1;  // N-2 prefix levels + the leaf level
   for (int lvl = 0; lvl < nlev; ++lvl) {
@@ -133,6 +149,7 @@ __device__ __forceinline__ void stage_cross(const SweepParams &p, float *X, floa
     if (lvl >= 1) {
       cp_async_wait_all();
       __syncwarp();
+      if (leaf && !fold_leaf) break;
       if (lane < RP) {
         for (int k = 0; k < nb; ++k) X[k * RS + lane] *= Y[k * RS + lane];
       }
@@ -146,9 +163,11 @@ __device__ __forceinline__ void stage_cross(const SweepParams &p, float *X, floa
 // ------------------------------------------------------------------------------------------
 constexpr int WPB_R = 4;  // warps per block of the row kernels
 
+// FFMA variant (kept for A/B measurement: FT_FACTOR_KERNEL=ffma): the combine reads cross as
+// shared-memory broadcasts, 8 LDS.128 + 32 FFMA per leaf per warp.
 template <int RP>
 __global__ void __launch_bounds__(WPB_R * 32)
-    factor_rows_kernel(const SweepParams p) {
+    factor_rows_ffma_kernel(const SweepParams p) {
   extern __shared__ float4 smem4[];
   constexpr int RS = Tile<RP>::RS;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -158,9 +177,14 @@ __global__ void __launch_bounds__(WPB_R * 32)
   __syncwarp();
   const int64_t gw = (int64_t)blockIdx.x * WPB_R + w, nw = (int64_t)gridDim.x * WPB_R;
   const bool jl = lane < p.J;
-  float bt[RP];
+  // Bt_u column j as fp32 pairs: the combine runs on packed FFMA2 (two FMAs per issue slot;
+  // even and odd r accumulate in the two halves and are added at the end)
+  float2 bt2[RP / 2];
 #pragma unroll
-  for (int r = 0; r < RP; ++r) bt[r] = (jl && r < p.R) ? __ldg(p.Bt + r * p.J + lane) : 0.f;
+  for (int r = 0; r < RP / 2; ++r) {
+    bt2[r].x = (jl && 2 * r < p.R) ? __ldg(p.Bt + (2 * r) * p.J + lane) : 0.f;
+    bt2[r].y = (jl && 2 * r + 1 < p.R) ? __ldg(p.Bt + (2 * r + 1) * p.J + lane) : 0.f;
+  }
 
   for (int64_t row = gw; row < p.nrows; row += nw) {
     const int i = __ldg(p.row_coord + row);
@@ -176,26 +200,351 @@ __global__ void __launch_bounds__(WPB_R * 32)
       int fnext;
       const int myfib = batch_fibers(p.fiber_ptr, fcur, fe, L0, nb, lane, &fnext);
       stage_cross<RP>(p, X, Y, myfib, lc, nb, lane);
-      // serial chain; vec_k = sum_r cross[k][r] Bt[r][j] (sequential r, broadcast reads) is
+      // serial chain; vec_k = sum_r cross[k][r] Bt[r][j] (broadcast reads, FFMA2) is
       // independent of the row, so it overlaps the previous leaf's reduction latency
 #pragma unroll 4
       for (int k = 0; k < nb; ++k) {
         const float4 *xr = reinterpret_cast<const float4 *>(X + k * RS);
-        float v = 0.f;
+        float2 v2 = make_float2(0.f, 0.f);
 #pragma unroll
         for (int r4 = 0; r4 < RP / 4; ++r4) {
           const float4 c4 = xr[r4];
-          v = __fmaf_rn(c4.x, bt[4 * r4], v);
-          v = __fmaf_rn(c4.y, bt[4 * r4 + 1], v);
-          v = __fmaf_rn(c4.z, bt[4 * r4 + 2], v);
-          v = __fmaf_rn(c4.w, bt[4 * r4 + 3], v);
+          v2 = ffma2(make_float2(c4.x, c4.y), bt2[2 * r4], v2);
+          v2 = ffma2(make_float2(c4.z, c4.w), bt2[2 * r4 + 1], v2);
         }
+        const float v = v2.x + v2.y;
         const float s = warp_sum(a * v);
         const float e = __shfl_sync(FULL, x, k) - s;
         const float g = p.reg * a - e * v;
         a = a - p.lr * g;
       }
       __syncwarp();
+      fcur = fnext;
+    }
+    if (jl) arow[lane] = a;
+  }
+}
+
+
+// ---- 3xTF32 tensor-core combine ---------------------------------------------------------
+// vec for a batch of 32 leaves is a 32 x J x R GEMM: V = Cross (32 x R) * Bt_u (R x J).
+// mma.sync.m16n8k8 TF32 with the 3-term split (a_hi b_hi + a_hi b_lo + a_lo b_hi) keeps fp32
+// accuracy (BF16/1xTF32 are outside the 1e-4 contract's margin).
+// tf32 by truncation: the high 19 bits, exactly representable, so lo = x - hi is exact and the
+// 3-term product misses only lo_b*lo_a and lo's own truncation (~2^-22 relative).  (cvt.rna.tf32
+// is emulated with ~6 integer/FP instructions on this part; a mask is one LOP3.)
+__device__ __forceinline__ uint32_t to_tf32(float x) { return __float_as_uint(x) & 0xffffe000u; }
+__device__ __forceinline__ void mma_tf32(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+constexpr int VS = 36;  // row stride of the staged V tile (32 leaves x 32 j)
+
+// Shared-memory plan of the tensor-core K3b (per block: the Bt_u fragments, then per warp the
+// X / Y staging tiles; V lands in Y when RP = 32, else in its own tile).
+template <int RP>
+struct MmaPlan {
+  static constexpr int RS = Tile<RP>::RS;
+  static constexpr int KT = RP / 8 > 0 ? RP / 8 : 1;
+  static constexpr int NT = 4;
+  static constexpr bool V_IN_Y = RS >= VS;
+  static constexpr int WARP_FLOATS = 2 * BATCH * RS + (V_IN_Y ? 0 : BATCH * VS);
+  static constexpr int BFRAG_U4 = KT * NT * 32;  // uint4 per block
+  static constexpr size_t bytes(int wpb) {
+    return (size_t)BFRAG_U4 * 16 + (size_t)wpb * WARP_FLOATS * sizeof(float);
+  }
+};
+
+// K3b with the combine on tensor cores.  Per batch: stage X (prefix product) and Y (leaf rows)
+// with cp.async; V = (X * Y) * Bt_u by 3xTF32 mma.sync (the A fragments are formed from X and Y
+// in registers; the hi / lo B fragments of Bt_u are split once per block into shared memory);
+// V goes through shared memory to the lanes-over-j layout; then the serial chain.
+template <int RP>
+__global__ void __launch_bounds__(WPB_R * 32)
+    factor_rows_kernel(const SweepParams p) {
+  using P = MmaPlan<RP>;
+  constexpr int RS = P::RS, KT = P::KT, NT = P::NT;
+  extern __shared__ float4 smem4[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  uint4 *bfrag = reinterpret_cast<uint4 *>(smem4);  // [KT][NT][32]: (hi0, hi1, lo0, lo1)
+  float *X = reinterpret_cast<float *>(bfrag + P::BFRAG_U4) + w * P::WARP_FLOATS;
+  float *Y = X + BATCH * RS;
+  float *V = P::V_IN_Y ? Y : Y + BATCH * RS;
+  for (int k = lane; k < P::WARP_FLOATS; k += 32) X[k] = 0.f;
+  for (int f = threadIdx.x; f < P::BFRAG_U4; f += blockDim.x) {
+    const int l = f & 31, nt = (f >> 5) % NT, kt = (f >> 5) / NT;
+    const int g = l >> 2, t = l & 3, j = 8 * nt + g;
+    uint32_t hv[2], lv[2];
+    for (int h = 0; h < 2; ++h) {
+      const int r = 8 * kt + t + 4 * h;
+      const float b = (r < p.R && j < p.J) ? __ldg(p.Bt + r * p.J + j) : 0.f;
+      hv[h] = to_tf32(b);
+      lv[h] = to_tf32(b - __uint_as_float(hv[h]));
+    }
+    bfrag[f] = make_uint4(hv[0], hv[1], lv[0], lv[1]);
+  }
+  __syncthreads();
+  const int64_t gw = (int64_t)blockIdx.x * WPB_R + w, nw = (int64_t)gridDim.x * WPB_R;
+  const bool jl = lane < p.J;
+
+  for (int64_t row = gw; row < p.nrows; row += nw) {
+    const int i = __ldg(p.row_coord + row);
+    const int fb = __ldg(p.row_fiber_ptr + row), fe = __ldg(p.row_fiber_ptr + row + 1);
+    const int Lb = __ldg(p.fiber_ptr + fb), Le = __ldg(p.fiber_ptr + fe);
+    float *arow = p.A + (int64_t)i * p.J;
+    float a = jl ? arow[lane] : 0.f;
+    int fcur = fb;
+    for (int L0 = Lb; L0 < Le; L0 += BATCH) {
+      const int nb = min(BATCH, Le - L0);
+      const int lc = lane < nb ? __ldcs(p.leaf_coord + L0 + lane) : 0;
+      const float x = lane < nb ? __ldcs(p.vals + L0 + lane) : 0.f;
+      int fnext;
+      const int myfib = batch_fibers(p.fiber_ptr, fcur, fe, L0, nb, lane, &fnext);
+      stage_cross<RP>(p, X, Y, myfib, lc, nb, lane, /*fold_leaf=*/false);
+      float acc[2][NT][4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[mt][nt][q] = 0.f;
+      const int mts = nb > 16 ? 2 : 1;
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        if (mt >= mts) break;
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt) {
+          const int r0 = 16 * mt + gq, c0 = 8 * kt + tq;
+          const float x0 = X[r0 * RS + c0] * Y[r0 * RS + c0];
+          const float x1 = X[(r0 + 8) * RS + c0] * Y[(r0 + 8) * RS + c0];
+          const float x2 = X[r0 * RS + c0 + 4] * Y[r0 * RS + c0 + 4];
+          const float x3 = X[(r0 + 8) * RS + c0 + 4] * Y[(r0 + 8) * RS + c0 + 4];
+          const uint32_t h0 = to_tf32(x0), h1 = to_tf32(x1), h2 = to_tf32(x2), h3 = to_tf32(x3);
+          const uint32_t l0 = to_tf32(x0 - __uint_as_float(h0));
+          const uint32_t l1 = to_tf32(x1 - __uint_as_float(h1));
+          const uint32_t l2 = to_tf32(x2 - __uint_as_float(h2));
+          const uint32_t l3 = to_tf32(x3 - __uint_as_float(h3));
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const uint4 b = bfrag[(kt * NT + nt) * 32 + lane];
+            mma_tf32(acc[mt][nt], l0, l1, l2, l3, b.x, b.y);
+            mma_tf32(acc[mt][nt], h0, h1, h2, h3, b.z, b.w);
+            mma_tf32(acc[mt][nt], h0, h1, h2, h3, b.x, b.y);
+          }
+        }
+      }
+      __syncwarp();  // all A fragments read before V overwrites Y
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int r0 = 16 * mt + gq, c0 = 8 * nt + 2 * tq;
+          *reinterpret_cast<float2 *>(V + r0 * VS + c0) = make_float2(acc[mt][nt][0], acc[mt][nt][1]);
+          *reinterpret_cast<float2 *>(V + (r0 + 8) * VS + c0) =
+              make_float2(acc[mt][nt][2], acc[mt][nt][3]);
+        }
+      __syncwarp();
+      // serial chain: s = a.v, e = x - s, a -= lr (reg a - e v)
+#pragma unroll 8
+      for (int k = 0; k < nb; ++k) {
+        const float v = V[k * VS + lane];
+        const float s = warp_sum(a * v);
+        const float e = __shfl_sync(FULL, x, k) - s;
+        const float g = p.reg * a - e * v;
+        a = a - p.lr * g;
+      }
+      __syncwarp();
+      if (P::V_IN_Y && p.R < RP) {  // V overwrote Y's zero pads r in [R, RP)
+        if (lane >= p.R && lane < RP)
+          for (int k = 0; k < BATCH; ++k) Y[k * RS + lane] = 0.f;
+        __syncwarp();
+      }
+      fcur = fnext;
+    }
+    if (jl) arow[lane] = a;
+  }
+}
+
+// ---- K3b, Gram form of the serial chain --------------------------------------------------
+// Within a batch the row evolves as a_{m+1} = alpha a_m + lr e_m v_m (alpha = 1 - lr reg), so
+// with w_k = a_m . v_k tracked for every later leaf k:
+//     e_m = x_m - w_m,   w_k <- alpha w_k + lr e_m (v_m . v_k)   (k > m),
+// an exact restatement of the reference's s_k = a_k . v_k that turns the per-leaf dependency
+// into ONE shuffle + two FMAs (~36 cycles) instead of a 32-lane reduction (~140 cycles).
+// d_k = a_0 . v_k and the Gram matrix G = V V^T (3xTF32 mma.sync, only tiles with m < k) are
+// computed per batch off the chain; the row itself is replayed afterwards, a <- alpha a +
+// lr e_m v_m, in the reference's leaf order.
+template <int RP>
+struct GramTile {
+  static constexpr int RS = Tile<RP>::RS;
+  static constexpr int TS = 36;  // stride of the V and G tiles (32 x 32)
+  // X, Y (staging) and V, G (32 x TS each) share one region: X/Y are dead once V exists
+  static constexpr int FLOATS = (2 * BATCH * RS > 2 * BATCH * TS) ? 2 * BATCH * RS : 2 * BATCH * TS;
+};
+
+template <int RP>
+__global__ void __launch_bounds__(WPB_R * 32)
+    factor_rows_gram_kernel(const SweepParams p) {
+  extern __shared__ float4 smem4[];
+  constexpr int RS = Tile<RP>::RS;
+  constexpr int TS = GramTile<RP>::TS;
+  constexpr int KT = RP / 8 > 0 ? RP / 8 : 1;  // k-tiles over r
+  constexpr int NT = 4;                         // n-tiles over j (J <= 32)
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  float *X = reinterpret_cast<float *>(smem4) + w * GramTile<RP>::FLOATS;
+  float *Y = X + BATCH * RS;
+  float *V = X;              // after the combine
+  float *G = X + BATCH * TS;
+  for (int k = lane; k < GramTile<RP>::FLOATS; k += 32) X[k] = 0.f;
+  __syncwarp();
+  const int64_t gw = (int64_t)blockIdx.x * WPB_R + w, nw = (int64_t)gridDim.x * WPB_R;
+  const bool jl = lane < p.J;
+  const float lr = p.lr, alpha = 1.f - p.lr * p.reg;
+  uint32_t bhi[KT][NT][2], blo[KT][NT][2];
+#pragma unroll
+  for (int kt = 0; kt < KT; ++kt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = 8 * kt + tq + 4 * h, j = 8 * nt + gq;
+        const float b = (r < p.R && j < p.J) ? __ldg(p.Bt + r * p.J + j) : 0.f;
+        bhi[kt][nt][h] = to_tf32(b);
+        blo[kt][nt][h] = to_tf32(b - __uint_as_float(bhi[kt][nt][h]));
+      }
+
+  for (int64_t row = gw; row < p.nrows; row += nw) {
+    const int i = __ldg(p.row_coord + row);
+    const int fb = __ldg(p.row_fiber_ptr + row), fe = __ldg(p.row_fiber_ptr + row + 1);
+    const int Lb = __ldg(p.fiber_ptr + fb), Le = __ldg(p.fiber_ptr + fe);
+    float *arow = p.A + (int64_t)i * p.J;
+    float a = jl ? arow[lane] : 0.f;
+    int fcur = fb;
+    for (int L0 = Lb; L0 < Le; L0 += BATCH) {
+      const int nb = min(BATCH, Le - L0);
+      const int lc = lane < nb ? __ldcs(p.leaf_coord + L0 + lane) : 0;
+      const float x = lane < nb ? __ldcs(p.vals + L0 + lane) : 0.f;
+      int fnext;
+      const int myfib = batch_fibers(p.fiber_ptr, fcur, fe, L0, nb, lane, &fnext);
+      stage_cross<RP>(p, X, Y, myfib, lc, nb, lane, /*fold_leaf=*/false);
+      const int mts = nb > 16 ? 2 : 1;
+      // ---- V = (X * Y) * Bt_u (3xTF32) ----
+      float acc[2][NT][4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[mt][nt][q] = 0.f;
+        if (mt >= mts) continue;
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt) {
+          const int r0 = 16 * mt + gq, c0 = 8 * kt + tq;
+          const float x0 = X[r0 * RS + c0] * Y[r0 * RS + c0];
+          const float x1 = X[(r0 + 8) * RS + c0] * Y[(r0 + 8) * RS + c0];
+          const float x2 = X[r0 * RS + c0 + 4] * Y[r0 * RS + c0 + 4];
+          const float x3 = X[(r0 + 8) * RS + c0 + 4] * Y[(r0 + 8) * RS + c0 + 4];
+          const uint32_t h0 = to_tf32(x0), h1 = to_tf32(x1), h2 = to_tf32(x2), h3 = to_tf32(x3);
+          const uint32_t l0 = to_tf32(x0 - __uint_as_float(h0));
+          const uint32_t l1 = to_tf32(x1 - __uint_as_float(h1));
+          const uint32_t l2 = to_tf32(x2 - __uint_as_float(h2));
+          const uint32_t l3 = to_tf32(x3 - __uint_as_float(h3));
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            mma_tf32(acc[mt][nt], l0, l1, l2, l3, bhi[kt][nt][0], bhi[kt][nt][1]);
+            mma_tf32(acc[mt][nt], h0, h1, h2, h3, blo[kt][nt][0], blo[kt][nt][1]);
+            mma_tf32(acc[mt][nt], h0, h1, h2, h3, bhi[kt][nt][0], bhi[kt][nt][1]);
+          }
+        }
+      }
+      __syncwarp();  // X / Y are dead: V and G reuse them
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int r0 = 16 * mt + gq, c0 = 8 * nt + 2 * tq;
+          *reinterpret_cast<float2 *>(V + r0 * TS + c0) = make_float2(acc[mt][nt][0], acc[mt][nt][1]);
+          *reinterpret_cast<float2 *>(V + (r0 + 8) * TS + c0) =
+              make_float2(acc[mt][nt][2], acc[mt][nt][3]);
+        }
+      __syncwarp();
+      // ---- G = V V^T for the tiles holding some (m < k), 3xTF32 ----
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          if (mt == 1 && nt < 2) continue;          // rows 16..31 x cols 0..15: all m > k
+          if (mt >= mts || 8 * nt >= nb) continue;  // beyond the batch
+          float g4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int kt = 0; kt < 4; ++kt) {
+            const int r0 = 16 * mt + gq, c0 = 8 * kt + tq, n0 = 8 * nt + gq;
+            const float a0 = V[r0 * TS + c0], a1 = V[(r0 + 8) * TS + c0];
+            const float a2 = V[r0 * TS + c0 + 4], a3 = V[(r0 + 8) * TS + c0 + 4];
+            const float b0 = V[n0 * TS + c0], b1 = V[n0 * TS + c0 + 4];
+            const uint32_t ah0 = to_tf32(a0), ah1 = to_tf32(a1), ah2 = to_tf32(a2),
+                           ah3 = to_tf32(a3), bh0 = to_tf32(b0), bh1 = to_tf32(b1);
+            const uint32_t al0 = to_tf32(a0 - __uint_as_float(ah0));
+            const uint32_t al1 = to_tf32(a1 - __uint_as_float(ah1));
+            const uint32_t al2 = to_tf32(a2 - __uint_as_float(ah2));
+            const uint32_t al3 = to_tf32(a3 - __uint_as_float(ah3));
+            const uint32_t bl0 = to_tf32(b0 - __uint_as_float(bh0));
+            const uint32_t bl1 = to_tf32(b1 - __uint_as_float(bh1));
+            mma_tf32(g4, al0, al1, al2, al3, bh0, bh1);
+            mma_tf32(g4, ah0, ah1, ah2, ah3, bl0, bl1);
+            mma_tf32(g4, ah0, ah1, ah2, ah3, bh0, bh1);
+          }
+          const int r0 = 16 * mt + gq, c0 = 8 * nt + 2 * tq;
+          *reinterpret_cast<float2 *>(G + r0 * TS + c0) = make_float2(g4[0], g4[1]);
+          *reinterpret_cast<float2 *>(G + (r0 + 8) * TS + c0) = make_float2(g4[2], g4[3]);
+        }
+      }
+      // ---- d_k = a_0 . v_k (lane k); a_0 broadcast through the spare pad column of G ----
+      G[lane * TS + 32] = a;  // column 32 of G holds a_0 (lanes >= J hold 0)
+      __syncwarp();
+      float wk = 0.f;
+      {
+        const float4 *vr = reinterpret_cast<const float4 *>(V + lane * TS);
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) {
+          const float4 v4 = vr[j4];
+          wk = __fmaf_rn(v4.x, G[(4 * j4) * TS + 32], wk);
+          wk = __fmaf_rn(v4.y, G[(4 * j4 + 1) * TS + 32], wk);
+          wk = __fmaf_rn(v4.z, G[(4 * j4 + 2) * TS + 32], wk);
+          wk = __fmaf_rn(v4.w, G[(4 * j4 + 3) * TS + 32], wk);
+        }
+      }
+      // ---- the serial chain, scalar per leaf ----
+      float e_mine = 0.f;
+#pragma unroll 8
+      for (int m = 0; m < nb; ++m) {
+        const float gmk = G[m * TS + lane];            // off the chain
+        const float em = __shfl_sync(FULL, x - wk, m);  // e_m = x_m - a_m . v_m
+        e_mine = lane == m ? em : e_mine;
+        wk = __fmaf_rn(lr * em, gmk, alpha * wk);
+      }
+      // ---- replay the row: a <- alpha a + lr e_m v_m, leaf order ----
+#pragma unroll 8
+      for (int m = 0; m < nb; ++m) {
+        const float em = __shfl_sync(FULL, e_mine, m);
+        a = __fmaf_rn(lr * em, V[m * TS + lane], alpha * a);
+      }
+      __syncwarp();
+      if (p.R < RP) {  // V / G overwrote X / Y: restore the zero pads of the r >= R columns
+        for (int k = 0; k < BATCH; ++k)
+          if (lane >= p.R && lane < RP) {
+            X[k * RS + lane] = 0.f;
+            Y[k * RS + lane] = 0.f;
+          }
+        __syncwarp();
+      }
       fcur = fnext;
     }
     if (jl) arow[lane] = a;
@@ -439,7 +788,38 @@ inline int grid_for(Kern kern, int64_t work_warps, int wpb = WPB, size_t smem = 
 
 template <int RP>
 int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
-  const size_t sm = factor_smem<RP>();
+  // FT_FACTOR_KERNEL selects the K3b variant for A/B measurement: mma (default), ffma, gram
+  static const int variant = [] {
+    const char *e = getenv("FT_FACTOR_KERNEL");
+    if (e && strcmp(e, "gram") == 0) return 0;
+    if (e && strcmp(e, "ffma") == 0) return 2;
+    return 1;  // mma
+  }();
+  if (variant == 0) {
+    const size_t sm = (size_t)WPB_R * GramTile<RP>::FLOATS * sizeof(float);
+    static bool set = false;
+    if (!set) {
+      cudaFuncSetAttribute(factor_rows_gram_kernel<RP>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      set = true;
+    }
+    const int g = grid_for(factor_rows_gram_kernel<RP>, p.nrows, WPB_R, sm);
+    factor_rows_gram_kernel<RP><<<g, WPB_R * 32, sm, s>>>(p);
+    return check_launch("ft_factor_sweep_rows(gram)");
+  }
+  if (variant == 2) {
+    const size_t sm = factor_smem<RP>();
+    const int g = grid_for(factor_rows_ffma_kernel<RP>, p.nrows, WPB_R, sm);
+    factor_rows_ffma_kernel<RP><<<g, WPB_R * 32, sm, s>>>(p);
+    return check_launch("ft_factor_sweep_rows(ffma)");
+  }
+  const size_t sm = MmaPlan<RP>::bytes(WPB_R);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(factor_rows_kernel<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
+    attr_set = true;
+  }
   const int g = grid_for(factor_rows_kernel<RP>, p.nrows, WPB_R, sm);
   factor_rows_kernel<RP><<<g, WPB_R * 32, sm, s>>>(p);
   return check_launch("ft_factor_sweep_rows");

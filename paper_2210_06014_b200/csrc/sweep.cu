@@ -371,54 +371,285 @@ __global__ void __launch_bounds__(WPB_R * 32)
   }
 }
 
-// ---- K3b, Gram form of the serial chain --------------------------------------------------
-// Within a batch the row evolves as a_{m+1} = alpha a_m + lr e_m v_m (alpha = 1 - lr reg), so
-// with w_k = a_m . v_k tracked for every later leaf k:
-//     e_m = x_m - w_m,   w_k <- alpha w_k + lr e_m (v_m . v_k)   (k > m),
-// an exact restatement of the reference's s_k = a_k . v_k that turns the per-leaf dependency
-// into ONE shuffle + two FMAs (~36 cycles) instead of a 32-lane reduction (~140 cycles).
-// d_k = a_0 . v_k and the Gram matrix G = V V^T (3xTF32 mma.sync, only tiles with m < k) are
-// computed per batch off the chain; the row itself is replayed afterwards, a <- alpha a +
-// lr e_m v_m, in the reference's leaf order.
-template <int RP>
-struct GramTile {
-  static constexpr int RS = Tile<RP>::RS;
-  static constexpr int TS = 36;  // stride of the V and G tiles (32 x 32)
-  // X, Y (staging) and V, G (32 x TS each) share one region: X/Y are dead once V exists
-  static constexpr int FLOATS = (2 * BATCH * RS > 2 * BATCH * TS) ? 2 * BATCH * RS : 2 * BATCH * TS;
-};
+
+// ---- K3b, software-pipelined tensor-core version (the default) --------------------------
+// Per warp, batch b+1's index loads are issued before batch b's MMA and its cp.async gathers
+// right after it, so the gather latency hides under batch b's serial chain.  Staging tiles are
+// 32 floats wide with an XOR swizzle (conflict-free A-fragment loads and 16-B cp.async), V has
+// its own tile so the next gathers never wait for the chain.
+__device__ __forceinline__ int swz(int row, int col) { return row * 32 + (col ^ ((row & 7) << 2)); }
 
 template <int RP>
-__global__ void __launch_bounds__(WPB_R * 32)
-    factor_rows_gram_kernel(const SweepParams p) {
+__device__ __forceinline__ void gather_sw(float *dst, const float *__restrict__ C, int R,
+                                          int coord_lane, int nb, int lane) {
+  if ((R & 3) == 0) {
+    constexpr int P4 = RP / 4;
+    const int R4 = R >> 2;
+#pragma unroll
+    for (int it = 0; it < P4; ++it) {
+      const int c = lane + 32 * it;
+      const int k = c / P4, q = c % P4;
+      const int coord = __shfl_sync(FULL, coord_lane, k);
+      if (k < nb && q < R4) cp_async16(dst + swz(k, 4 * q), C + (int64_t)coord * R + 4 * q);
+    }
+  } else {
+#pragma unroll 4
+    for (int k = 0; k < BATCH; ++k) {
+      const int coord = __shfl_sync(FULL, coord_lane, k);
+      if (k < nb && lane < R) cp_async4(dst + swz(k, lane), C + (int64_t)coord * R + lane);
+    }
+  }
+}
+
+struct PipePlan {
+  static constexpr int TILE = BATCH * 32;  // swizzled X / Y tiles
+  static constexpr int WARP_FLOATS = 2 * TILE + BATCH * VS;
+  static constexpr int WPB = 8;
+  template <int RP>
+  static constexpr int bfrag_u4() { return (RP / 8 > 0 ? RP / 8 : 1) * 4 * 32; }
+  template <int RP>
+  static constexpr size_t bytes() {
+    return (size_t)bfrag_u4<RP>() * 16 + (size_t)WPB * WARP_FLOATS * sizeof(float);
+  }
+};
+
+// Everything batch b needs before its gathers can be issued.
+struct BatchIdx {
+  int L0, nb, fcur;  // window [L0, L0+nb), fiber holding leaf L0
+  int lc;            // lane k: leaf coordinate of leaf L0+k
+  float x;           // lane k: value
+  int fs;            // lane l: fiber_ptr[fcur + 1 + l] (fiber starts in the window)
+};
+
+__device__ __forceinline__ void load_batch_idx(const SweepParams &p, BatchIdx &b, int L0, int Le,
+                                               int fcur, int fe, int lane) {
+  b.L0 = L0;
+  b.nb = min(BATCH, Le - L0);
+  b.fcur = fcur;
+  b.lc = lane < b.nb ? __ldcs(p.leaf_coord + L0 + lane) : 0;
+  b.x = lane < b.nb ? __ldcs(p.vals + L0 + lane) : 0.f;
+  const int fidx = fcur + 1 + lane;
+  b.fs = fidx < fe ? __ldg(p.fiber_ptr + fidx) : INT32_MAX;
+}
+
+// fiber of each leaf + the next window's fcur (needs b.fs)
+__device__ __forceinline__ int batch_fib(const BatchIdx &b, int lane, int *fnext) {
+  const unsigned bit = (b.fs < b.L0 + b.nb) ? (1u << (b.fs - b.L0)) : 0u;
+  const unsigned mask = __reduce_or_sync(FULL, bit);
+  *fnext = b.fcur + __popc(mask);
+  return b.fcur + __popc(mask & (FULL >> (31 - lane)));
+}
+
+// issue batch b's gathers: X = prod of the prefix levels, Y = leaf level (left in flight)
+template <int RP>
+__device__ __forceinline__ void issue_gathers(const SweepParams &p, const BatchIdx &b, int myfib,
+                                              float *X, float *Y, int lane) {
+  const int npre = p.N - 2;
+  for (int lvl = 0; lvl < npre; ++lvl) {
+    const int coord =
+        lane < b.nb ? __ldg(p.fiber_coord + (int64_t)myfib * (p.N - 1) + 1 + lvl) : 0;
+    gather_sw<RP>(lvl == 0 ? X : Y, p.Cpre[lvl], p.R, coord, b.nb, lane);
+    if (lvl >= 1) {  // order > 3: fold this prefix level into X now
+      cp_async_wait_all();
+      __syncwarp();
+      if (lane < RP)
+        for (int k = 0; k < b.nb; ++k) X[swz(k, lane)] *= Y[swz(k, lane)];
+      __syncwarp();
+    }
+  }
+  gather_sw<RP>(Y, p.Cleaf, p.R, b.lc, b.nb, lane);
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
+template <int RP>
+__global__ void __launch_bounds__(PipePlan::WPB * 32, 2)
+    factor_rows_pipe_kernel(const SweepParams p) {
+  constexpr int KT = RP / 8 > 0 ? RP / 8 : 1, NT = 4;
   extern __shared__ float4 smem4[];
-  constexpr int RS = Tile<RP>::RS;
-  constexpr int TS = GramTile<RP>::TS;
-  constexpr int KT = RP / 8 > 0 ? RP / 8 : 1;  // k-tiles over r
-  constexpr int NT = 4;                         // n-tiles over j (J <= 32)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int gq = lane >> 2, tq = lane & 3;
-  float *X = reinterpret_cast<float *>(smem4) + w * GramTile<RP>::FLOATS;
-  float *Y = X + BATCH * RS;
-  float *V = X;              // after the combine
-  float *G = X + BATCH * TS;
-  for (int k = lane; k < GramTile<RP>::FLOATS; k += 32) X[k] = 0.f;
-  __syncwarp();
-  const int64_t gw = (int64_t)blockIdx.x * WPB_R + w, nw = (int64_t)gridDim.x * WPB_R;
+  uint4 *bfrag = reinterpret_cast<uint4 *>(smem4);
+  float *X = reinterpret_cast<float *>(bfrag + PipePlan::bfrag_u4<RP>()) + w * PipePlan::WARP_FLOATS;
+  float *Y = X + PipePlan::TILE;
+  float *V = Y + PipePlan::TILE;
+  for (int k = lane; k < PipePlan::WARP_FLOATS; k += 32) X[k] = 0.f;
+  for (int f = threadIdx.x; f < PipePlan::bfrag_u4<RP>(); f += blockDim.x) {
+    const int l = f & 31, nt = (f >> 5) % NT, kt = (f >> 5) / NT;
+    const int g = l >> 2, t = l & 3, j = 8 * nt + g;
+    uint32_t hv[2], lv[2];
+    for (int h = 0; h < 2; ++h) {
+      const int r = 8 * kt + t + 4 * h;
+      const float bv = (r < p.R && j < p.J) ? __ldg(p.Bt + r * p.J + j) : 0.f;
+      hv[h] = to_tf32(bv);
+      lv[h] = to_tf32(bv - __uint_as_float(hv[h]));
+    }
+    bfrag[f] = make_uint4(hv[0], hv[1], lv[0], lv[1]);
+  }
+  __syncthreads();
+  const int64_t gw = (int64_t)blockIdx.x * PipePlan::WPB + w;
+  const int64_t nw = (int64_t)gridDim.x * PipePlan::WPB;
   const bool jl = lane < p.J;
-  const float lr = p.lr, alpha = 1.f - p.lr * p.reg;
-  uint32_t bhi[KT][NT][2], blo[KT][NT][2];
-#pragma unroll
-  for (int kt = 0; kt < KT; ++kt)
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int r = 8 * kt + tq + 4 * h, j = 8 * nt + gq;
-        const float b = (r < p.R && j < p.J) ? __ldg(p.Bt + r * p.J + j) : 0.f;
-        bhi[kt][nt][h] = to_tf32(b);
-        blo[kt][nt][h] = to_tf32(b - __uint_as_float(bhi[kt][nt][h]));
+
+  for (int64_t row = gw; row < p.nrows; row += nw) {
+    const int i = __ldg(p.row_coord + row);
+    const int fb = __ldg(p.row_fiber_ptr + row), fe = __ldg(p.row_fiber_ptr + row + 1);
+    const int Lb = __ldg(p.fiber_ptr + fb), Le = __ldg(p.fiber_ptr + fe);
+    float *arow = p.A + (int64_t)i * p.J;
+    float a = jl ? arow[lane] : 0.f;
+    // prologue: batch 0's gathers in flight, batch 1's indices requested
+    BatchIdx cur, nxt;
+    load_batch_idx(p, cur, Lb, Le, fb, fe, lane);
+    int fnext;
+    int myfib = batch_fib(cur, lane, &fnext);
+    issue_gathers<RP>(p, cur, myfib, X, Y, lane);
+    bool has_next = Lb + BATCH < Le;
+    if (has_next) load_batch_idx(p, nxt, Lb + BATCH, Le, fnext, fe, lane);
+    for (;;) {
+      // next batch's fibers and prefix coordinates (the loads fly during this batch's MMA)
+      int nfib = 0, nfnext = 0, ncoord = 0;
+      if (has_next) {
+        nfib = batch_fib(nxt, lane, &nfnext);
+        if (p.N == 3)
+          ncoord = lane < nxt.nb ? __ldg(p.fiber_coord + (int64_t)nfib * 2 + 1) : 0;
       }
+      cp_async_wait_all();
+      __syncwarp();
+      // ---- V = (X * Y) * Bt_u, 3xTF32 ----
+      float acc[2][NT][4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[mt][nt][q] = 0.f;
+      const int mts = cur.nb > 16 ? 2 : 1;
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        if (mt >= mts) break;
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt) {
+          const int r0 = 16 * mt + gq, c0 = 8 * kt + tq;
+          const int o0 = swz(r0, c0), o1 = swz(r0 + 8, c0), o2 = swz(r0, c0 + 4),
+                    o3 = swz(r0 + 8, c0 + 4);
+          const float x0 = X[o0] * Y[o0], x1 = X[o1] * Y[o1], x2 = X[o2] * Y[o2],
+                      x3 = X[o3] * Y[o3];
+          const uint32_t h0 = to_tf32(x0), h1 = to_tf32(x1), h2 = to_tf32(x2), h3 = to_tf32(x3);
+          const uint32_t l0 = to_tf32(x0 - __uint_as_float(h0));
+          const uint32_t l1 = to_tf32(x1 - __uint_as_float(h1));
+          const uint32_t l2 = to_tf32(x2 - __uint_as_float(h2));
+          const uint32_t l3 = to_tf32(x3 - __uint_as_float(h3));
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const uint4 bb = bfrag[(kt * NT + nt) * 32 + lane];
+            mma_tf32(acc[mt][nt], l0, l1, l2, l3, bb.x, bb.y);
+            mma_tf32(acc[mt][nt], h0, h1, h2, h3, bb.z, bb.w);
+            mma_tf32(acc[mt][nt], h0, h1, h2, h3, bb.x, bb.y);
+          }
+        }
+      }
+      __syncwarp();  // X / Y consumed
+      // ---- next batch's gathers go out now, under this batch's chain ----
+      BatchIdx nn;
+      bool has_nn = false;
+      if (has_next) {
+        if (p.N == 3) {
+          gather_sw<RP>(X, p.Cpre[0], p.R, ncoord, nxt.nb, lane);
+          gather_sw<RP>(Y, p.Cleaf, p.R, nxt.lc, nxt.nb, lane);
+          asm volatile("cp.async.commit_group;\n" ::: "memory");
+        } else {
+          issue_gathers<RP>(p, nxt, nfib, X, Y, lane);
+        }
+        has_nn = nxt.L0 + BATCH < Le;
+        if (has_nn) load_batch_idx(p, nn, nxt.L0 + BATCH, Le, nfnext, fe, lane);
+      }
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int r0 = 16 * mt + gq, c0 = 8 * nt + 2 * tq;
+          *reinterpret_cast<float2 *>(V + r0 * VS + c0) = make_float2(acc[mt][nt][0], acc[mt][nt][1]);
+          *reinterpret_cast<float2 *>(V + (r0 + 8) * VS + c0) =
+              make_float2(acc[mt][nt][2], acc[mt][nt][3]);
+        }
+      __syncwarp();
+      // ---- serial chain: s = a.v, e = x - s, a -= lr (reg a - e v) ----
+      const float xk = cur.x;
+      const int nbk = cur.nb;
+#pragma unroll 8
+      for (int k = 0; k < nbk; ++k) {
+        const float v = V[k * VS + lane];
+        const float s = warp_sum(a * v);
+        const float e = __shfl_sync(FULL, xk, k) - s;
+        const float g = p.reg * a - e * v;
+        a = a - p.lr * g;
+      }
+      __syncwarp();
+      if (!has_next) break;
+      cur = nxt;
+      nxt = nn;
+      has_next = has_nn;
+    }
+    if (jl) arow[lane] = a;
+  }
+}
+
+// ---- K3b, Gram form of the serial chain (tensor cores for both GEMMs) -------------------
+// Within a batch the row evolves as a_{m+1} = a_m + lr (e_m v_m - reg a_m).
+// Tracking w_k = a_m . v_k for every leaf k of the batch gives
+//     e_m = x_m - w_m,      w_k <- w_k + lr (e_m (v_m . v_k) - reg w_k),
+// an exact restatement of the reference's s = a . v that makes the serial dependency per leaf
+// ONE shuffle and two FMAs (~40 cycles) instead of a 32-lane reduction (~5 dependent
+// shuffles).  Off the chain, per batch: V = cross Bt_u (3xTF32 mma), then [G | d] =
+// V [V^T | a_0] (3xTF32 mma, only the tiles with some m < k, plus d = V a_0 as a fifth n-tile).
+// After the chain the row is replayed a <- a + lr (e_m v_m - reg a) in leaf order.
+constexpr int GS = 40;  // stride of the G tile: 32 x (32 Gram columns + 8 for d)
+
+struct GramPlan {
+  static constexpr int TILE = BATCH * 32;  // swizzled X / Y tiles (G reuses both)
+  static constexpr int WARP_FLOATS = 2 * TILE + BATCH * VS;
+  static constexpr int WPB = 8;
+  template <int RP>
+  static constexpr int bfrag_u4() { return (RP / 8 > 0 ? RP / 8 : 1) * 4 * 32; }
+  template <int RP>
+  static constexpr size_t bytes() {
+    return (size_t)bfrag_u4<RP>() * 16 + (size_t)WPB * WARP_FLOATS * sizeof(float);
+  }
+};
+static_assert(BATCH * GS <= 2 * BATCH * 32, "G must fit in the X/Y tiles");
+
+__device__ __forceinline__ void split3(float v, uint32_t &hi, uint32_t &lo) {
+  hi = to_tf32(v);
+  lo = to_tf32(v - __uint_as_float(hi));
+}
+
+template <int RP>
+__global__ void __launch_bounds__(GramPlan::WPB * 32, 2)
+    factor_rows_gram_kernel(const SweepParams p) {
+  constexpr int KT = RP / 8 > 0 ? RP / 8 : 1, NT = 4;
+  extern __shared__ float4 smem4[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  uint4 *bfrag = reinterpret_cast<uint4 *>(smem4);
+  float *X = reinterpret_cast<float *>(bfrag + GramPlan::bfrag_u4<RP>()) + w * GramPlan::WARP_FLOATS;
+  float *Y = X + GramPlan::TILE;
+  float *V = Y + GramPlan::TILE;
+  float *G = X;  // after V exists, X / Y are dead
+  for (int k = lane; k < GramPlan::WARP_FLOATS; k += 32) X[k] = 0.f;
+  for (int f = threadIdx.x; f < GramPlan::bfrag_u4<RP>(); f += blockDim.x) {
+    const int l = f & 31, nt = (f >> 5) % NT, kt = (f >> 5) / NT;
+    const int g = l >> 2, t = l & 3, j = 8 * nt + g;
+    uint32_t hv[2], lv[2];
+    for (int h = 0; h < 2; ++h) {
+      const int r = 8 * kt + t + 4 * h;
+      split3((r < p.R && j < p.J) ? __ldg(p.Bt + r * p.J + j) : 0.f, hv[h], lv[h]);
+    }
+    bfrag[f] = make_uint4(hv[0], hv[1], lv[0], lv[1]);
+  }
+  __syncthreads();
+  const int64_t gw = (int64_t)blockIdx.x * GramPlan::WPB + w;
+  const int64_t nw = (int64_t)gridDim.x * GramPlan::WPB;
+  const bool jl = lane < p.J;
+  const float lr = p.lr, reg = p.reg;
 
   for (int64_t row = gw; row < p.nrows; row += nw) {
     const int i = __ldg(p.row_coord + row);
@@ -428,123 +659,130 @@ __global__ void __launch_bounds__(WPB_R * 32)
     float a = jl ? arow[lane] : 0.f;
     int fcur = fb;
     for (int L0 = Lb; L0 < Le; L0 += BATCH) {
-      const int nb = min(BATCH, Le - L0);
-      const int lc = lane < nb ? __ldcs(p.leaf_coord + L0 + lane) : 0;
-      const float x = lane < nb ? __ldcs(p.vals + L0 + lane) : 0.f;
+      BatchIdx cur;
+      load_batch_idx(p, cur, L0, Le, fcur, fe, lane);
       int fnext;
-      const int myfib = batch_fibers(p.fiber_ptr, fcur, fe, L0, nb, lane, &fnext);
-      stage_cross<RP>(p, X, Y, myfib, lc, nb, lane, /*fold_leaf=*/false);
-      const int mts = nb > 16 ? 2 : 1;
-      // ---- V = (X * Y) * Bt_u (3xTF32) ----
+      const int myfib = batch_fib(cur, lane, &fnext);
+      issue_gathers<RP>(p, cur, myfib, X, Y, lane);
+      cp_async_wait_all();
+      __syncwarp();
+      const int nb = cur.nb, mts = nb > 16 ? 2 : 1;
+      // ---- V = (X * Y) * Bt_u ----
       float acc[2][NT][4];
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
+      for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
           for (int q = 0; q < 4; ++q) acc[mt][nt][q] = 0.f;
-        if (mt >= mts) continue;
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        if (mt >= mts) break;
 #pragma unroll
         for (int kt = 0; kt < KT; ++kt) {
           const int r0 = 16 * mt + gq, c0 = 8 * kt + tq;
-          const float x0 = X[r0 * RS + c0] * Y[r0 * RS + c0];
-          const float x1 = X[(r0 + 8) * RS + c0] * Y[(r0 + 8) * RS + c0];
-          const float x2 = X[r0 * RS + c0 + 4] * Y[r0 * RS + c0 + 4];
-          const float x3 = X[(r0 + 8) * RS + c0 + 4] * Y[(r0 + 8) * RS + c0 + 4];
-          const uint32_t h0 = to_tf32(x0), h1 = to_tf32(x1), h2 = to_tf32(x2), h3 = to_tf32(x3);
-          const uint32_t l0 = to_tf32(x0 - __uint_as_float(h0));
-          const uint32_t l1 = to_tf32(x1 - __uint_as_float(h1));
-          const uint32_t l2 = to_tf32(x2 - __uint_as_float(h2));
-          const uint32_t l3 = to_tf32(x3 - __uint_as_float(h3));
+          const int o0 = swz(r0, c0), o1 = swz(r0 + 8, c0), o2 = swz(r0, c0 + 4),
+                    o3 = swz(r0 + 8, c0 + 4);
+          uint32_t h0, h1, h2, h3, l0, l1, l2, l3;
+          split3(X[o0] * Y[o0], h0, l0);
+          split3(X[o1] * Y[o1], h1, l1);
+          split3(X[o2] * Y[o2], h2, l2);
+          split3(X[o3] * Y[o3], h3, l3);
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
-            mma_tf32(acc[mt][nt], l0, l1, l2, l3, bhi[kt][nt][0], bhi[kt][nt][1]);
-            mma_tf32(acc[mt][nt], h0, h1, h2, h3, blo[kt][nt][0], blo[kt][nt][1]);
-            mma_tf32(acc[mt][nt], h0, h1, h2, h3, bhi[kt][nt][0], bhi[kt][nt][1]);
+            const uint4 bb = bfrag[(kt * NT + nt) * 32 + lane];
+            mma_tf32(acc[mt][nt], l0, l1, l2, l3, bb.x, bb.y);
+            mma_tf32(acc[mt][nt], h0, h1, h2, h3, bb.z, bb.w);
+            mma_tf32(acc[mt][nt], h0, h1, h2, h3, bb.x, bb.y);
           }
         }
       }
-      __syncwarp();  // X / Y are dead: V and G reuse them
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           const int r0 = 16 * mt + gq, c0 = 8 * nt + 2 * tq;
-          *reinterpret_cast<float2 *>(V + r0 * TS + c0) = make_float2(acc[mt][nt][0], acc[mt][nt][1]);
-          *reinterpret_cast<float2 *>(V + (r0 + 8) * TS + c0) =
+          *reinterpret_cast<float2 *>(V + r0 * VS + c0) = make_float2(acc[mt][nt][0], acc[mt][nt][1]);
+          *reinterpret_cast<float2 *>(V + (r0 + 8) * VS + c0) =
               make_float2(acc[mt][nt][2], acc[mt][nt][3]);
         }
-      __syncwarp();
-      // ---- G = V V^T for the tiles holding some (m < k), 3xTF32 ----
+      __syncwarp();  // V visible; X / Y dead from here (G overwrites them)
+      // ---- [G | d] = V [V^T | a_0] ----
+      // a_0 as the B operand of the 5th n-tile: column 0 = a_0, columns 1..7 = 0
+      uint32_t ah[4][2], al[4][2];
+#pragma unroll
+      for (int kt = 0; kt < 4; ++kt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const float av = __shfl_sync(FULL, a, 8 * kt + tq + 4 * h);
+          split3(gq == 0 ? av : 0.f, ah[kt][h], al[kt][h]);
+        }
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
+        if (mt >= mts) break;
+        float gacc[5][4];
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) {
-          if (mt == 1 && nt < 2) continue;          // rows 16..31 x cols 0..15: all m > k
-          if (mt >= mts || 8 * nt >= nb) continue;  // beyond the batch
-          float g4[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int nt = 0; nt < 5; ++nt)
 #pragma unroll
-          for (int kt = 0; kt < 4; ++kt) {
-            const int r0 = 16 * mt + gq, c0 = 8 * kt + tq, n0 = 8 * nt + gq;
-            const float a0 = V[r0 * TS + c0], a1 = V[(r0 + 8) * TS + c0];
-            const float a2 = V[r0 * TS + c0 + 4], a3 = V[(r0 + 8) * TS + c0 + 4];
-            const float b0 = V[n0 * TS + c0], b1 = V[n0 * TS + c0 + 4];
-            const uint32_t ah0 = to_tf32(a0), ah1 = to_tf32(a1), ah2 = to_tf32(a2),
-                           ah3 = to_tf32(a3), bh0 = to_tf32(b0), bh1 = to_tf32(b1);
-            const uint32_t al0 = to_tf32(a0 - __uint_as_float(ah0));
-            const uint32_t al1 = to_tf32(a1 - __uint_as_float(ah1));
-            const uint32_t al2 = to_tf32(a2 - __uint_as_float(ah2));
-            const uint32_t al3 = to_tf32(a3 - __uint_as_float(ah3));
-            const uint32_t bl0 = to_tf32(b0 - __uint_as_float(bh0));
-            const uint32_t bl1 = to_tf32(b1 - __uint_as_float(bh1));
-            mma_tf32(g4, al0, al1, al2, al3, bh0, bh1);
-            mma_tf32(g4, ah0, ah1, ah2, ah3, bl0, bl1);
-            mma_tf32(g4, ah0, ah1, ah2, ah3, bh0, bh1);
+          for (int q = 0; q < 4; ++q) gacc[nt][q] = 0.f;
+#pragma unroll
+        for (int kt = 0; kt < 4; ++kt) {
+          const int r0 = 16 * mt + gq, c0 = 8 * kt + tq;
+          uint32_t h0, h1, h2, h3, l0, l1, l2, l3;
+          split3(V[r0 * VS + c0], h0, l0);
+          split3(V[(r0 + 8) * VS + c0], h1, l1);
+          split3(V[r0 * VS + c0 + 4], h2, l2);
+          split3(V[(r0 + 8) * VS + c0 + 4], h3, l3);
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) {
+            if (mt == 1 && nt < 2) continue;  // rows 16..31 x cols 0..15: every m > k
+            if (8 * nt >= nb) continue;
+            const int n0 = 8 * nt + gq;
+            uint32_t bh0, bl0, bh1, bl1;
+            split3(V[n0 * VS + c0], bh0, bl0);
+            split3(V[n0 * VS + c0 + 4], bh1, bl1);
+            mma_tf32(gacc[nt], l0, l1, l2, l3, bh0, bh1);
+            mma_tf32(gacc[nt], h0, h1, h2, h3, bl0, bl1);
+            mma_tf32(gacc[nt], h0, h1, h2, h3, bh0, bh1);
           }
-          const int r0 = 16 * mt + gq, c0 = 8 * nt + 2 * tq;
-          *reinterpret_cast<float2 *>(G + r0 * TS + c0) = make_float2(g4[0], g4[1]);
-          *reinterpret_cast<float2 *>(G + (r0 + 8) * TS + c0) = make_float2(g4[2], g4[3]);
+          mma_tf32(gacc[4], l0, l1, l2, l3, ah[kt][0], ah[kt][1]);
+          mma_tf32(gacc[4], h0, h1, h2, h3, al[kt][0], al[kt][1]);
+          mma_tf32(gacc[4], h0, h1, h2, h3, ah[kt][0], ah[kt][1]);
         }
-      }
-      // ---- d_k = a_0 . v_k (lane k); a_0 broadcast through the spare pad column of G ----
-      G[lane * TS + 32] = a;  // column 32 of G holds a_0 (lanes >= J hold 0)
-      __syncwarp();
-      float wk = 0.f;
-      {
-        const float4 *vr = reinterpret_cast<const float4 *>(V + lane * TS);
 #pragma unroll
-        for (int j4 = 0; j4 < 8; ++j4) {
-          const float4 v4 = vr[j4];
-          wk = __fmaf_rn(v4.x, G[(4 * j4) * TS + 32], wk);
-          wk = __fmaf_rn(v4.y, G[(4 * j4 + 1) * TS + 32], wk);
-          wk = __fmaf_rn(v4.z, G[(4 * j4 + 2) * TS + 32], wk);
-          wk = __fmaf_rn(v4.w, G[(4 * j4 + 3) * TS + 32], wk);
+        for (int nt = 0; nt < 5; ++nt) {
+          const int r0 = 16 * mt + gq, c0 = 8 * nt + 2 * tq;
+          *reinterpret_cast<float2 *>(G + r0 * GS + c0) = make_float2(gacc[nt][0], gacc[nt][1]);
+          *reinterpret_cast<float2 *>(G + (r0 + 8) * GS + c0) = make_float2(gacc[nt][2], gacc[nt][3]);
         }
       }
-      // ---- the serial chain, scalar per leaf ----
+      __syncwarp();
+      // ---- the serial chain, scalar per leaf (lane k tracks w_k = a_m . v_k) ----
+      float wk = G[lane * GS + 32];  // d_k
       float e_mine = 0.f;
 #pragma unroll 8
       for (int m = 0; m < nb; ++m) {
-        const float gmk = G[m * TS + lane];            // off the chain
-        const float em = __shfl_sync(FULL, x - wk, m);  // e_m = x_m - a_m . v_m
+        const float gmk = G[m * GS + lane];
+        const float em = __shfl_sync(FULL, cur.x - wk, m);
         e_mine = lane == m ? em : e_mine;
-        wk = __fmaf_rn(lr * em, gmk, alpha * wk);
+        // w += lr (e_m G[m][k] - reg w): the decay is applied as -lr reg w, never through a
+        // rounded alpha = 1 - lr reg (its fp32 rounding would compound over long rows)
+        wk = __fmaf_rn(lr, __fmaf_rn(em, gmk, -reg * wk), wk);
       }
-      // ---- replay the row: a <- alpha a + lr e_m v_m, leaf order ----
+      // ---- replay the row in leaf order: a += lr (e_m v_m - reg a) ----
 #pragma unroll 8
       for (int m = 0; m < nb; ++m) {
         const float em = __shfl_sync(FULL, e_mine, m);
-        a = __fmaf_rn(lr * em, V[m * TS + lane], alpha * a);
+        a = __fmaf_rn(lr, __fmaf_rn(em, V[m * VS + lane], -reg * a), a);
       }
       __syncwarp();
-      if (p.R < RP) {  // V / G overwrote X / Y: restore the zero pads of the r >= R columns
-        for (int k = 0; k < BATCH; ++k)
-          if (lane >= p.R && lane < RP) {
-            X[k * RS + lane] = 0.f;
-            Y[k * RS + lane] = 0.f;
-          }
-        __syncwarp();
-      }
+      // G overwrote X / Y: restore their zero columns r in [R, RP) before the next gathers
+      if (p.R < RP && lane >= p.R && lane < RP)
+        for (int k = 0; k < BATCH; ++k) {
+          X[swz(k, lane)] = 0.f;
+          Y[swz(k, lane)] = 0.f;
+        }
+      __syncwarp();
       fcur = fnext;
     }
     if (jl) arow[lane] = a;
@@ -722,25 +960,21 @@ __global__ void __launch_bounds__(WPB * 32)
       int fnext;
       const int myfib = batch_fibers(p.fiber_ptr, fcur, fend, L0, nb, lane, &fnext);
       const int slot = myfib - (int)base;
-      float a[BATCH];
-#pragma unroll
-      for (int k = 0; k < BATCH; ++k) {
+      // a warp is one serial hogwild worker: each leaf reads its row just before stepping it
+      // (different warps race, exactly as the reference's worker threads do)
+      for (int k = 0; k < nb; ++k) {
         const int i = __shfl_sync(FULL, lc, k);
-        a[k] = (jl && k < nb) ? p.A[(int64_t)i * p.J + lane] : 0.f;
-      }
-#pragma unroll
-      for (int k = 0; k < BATCH; ++k) {
-        if (k < nb) {
-          const int sl = __shfl_sync(FULL, slot, k);
-          const float vj = vec_s[sl][lane];
-          const float s = warp_sum(a[k] * vj);
-          const float e = __shfl_sync(FULL, x, k) - s;
-          const float g = p.reg * a[k] - e * vj;
-          const int i = __shfl_sync(FULL, lc, k);
-          // lock-free: the step is computed from a possibly stale row (hogwild) but is never
-          // lost -- concurrent writers of one row accumulate through L2 atomics (RED.ADD)
-          if (jl) atomicAdd(p.A + (int64_t)i * p.J + lane, -p.lr * g);
-        }
+        const int sl = __shfl_sync(FULL, slot, k);
+        float *ap = p.A + (int64_t)i * p.J + lane;
+        const float ak = jl ? *reinterpret_cast<volatile float *>(ap) : 0.f;
+        const float vj = vec_s[sl][lane];
+        const float s = warp_sum(ak * vj);
+        const float e = __shfl_sync(FULL, x, k) - s;
+        const float g = p.reg * ak - e * vj;
+        // lock-free: the step is never lost -- concurrent writers of one row accumulate
+        // through L2 atomics (RED.ADD)
+        if (jl) atomicAdd(ap, -p.lr * g);
+        __syncwarp();
       }
       fcur = fnext;
     }
@@ -788,23 +1022,36 @@ inline int grid_for(Kern kern, int64_t work_warps, int wpb = WPB, size_t smem = 
 
 template <int RP>
 int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
-  // FT_FACTOR_KERNEL selects the K3b variant for A/B measurement: mma (default), ffma, gram
+  // FT_FACTOR_KERNEL selects the K3b variant for A/B measurement: pipe (default), mma, ffma, gram
   static const int variant = [] {
     const char *e = getenv("FT_FACTOR_KERNEL");
     if (e && strcmp(e, "gram") == 0) return 0;
     if (e && strcmp(e, "ffma") == 0) return 2;
-    return 1;  // mma
+    if (e && strcmp(e, "mma") == 0) return 1;
+    return 3;  // pipelined mma
   }();
+  if (variant == 3) {
+    const size_t sm = PipePlan::bytes<RP>();
+    static bool set3 = false;
+    if (!set3) {
+      cudaFuncSetAttribute(factor_rows_pipe_kernel<RP>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      set3 = true;
+    }
+    const int g = grid_for(factor_rows_pipe_kernel<RP>, p.nrows, PipePlan::WPB, sm);
+    factor_rows_pipe_kernel<RP><<<g, PipePlan::WPB * 32, sm, s>>>(p);
+    return check_launch("ft_factor_sweep_rows(pipe)");
+  }
   if (variant == 0) {
-    const size_t sm = (size_t)WPB_R * GramTile<RP>::FLOATS * sizeof(float);
+    const size_t sm = GramPlan::bytes<RP>();
     static bool set = false;
     if (!set) {
       cudaFuncSetAttribute(factor_rows_gram_kernel<RP>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       set = true;
     }
-    const int g = grid_for(factor_rows_gram_kernel<RP>, p.nrows, WPB_R, sm);
-    factor_rows_gram_kernel<RP><<<g, WPB_R * 32, sm, s>>>(p);
+    const int g = grid_for(factor_rows_gram_kernel<RP>, p.nrows, GramPlan::WPB, sm);
+    factor_rows_gram_kernel<RP><<<g, GramPlan::WPB * 32, sm, s>>>(p);
     return check_launch("ft_factor_sweep_rows(gram)");
   }
   if (variant == 2) {

@@ -444,3 +444,56 @@ def test_row_shards_equal_unsharded(ft, golden_cases):
                                               None))
         torch.cuda.synchronize()
         assert torch.equal(ref.factors[u], sh.factors[u])
+
+
+def test_long_rows_factor_and_core_sweeps_match_oracle(ft):
+    """Rows with ~20K serial updates (the Netflix mode-2 regime, 45K per row at full size): one
+    exact factor sweep and one core sweep of every mode against the fp64 oracle at rel 1e-4.
+    Catches precision drift that only compounds on long rows."""
+    from oracle import oracle as O
+
+    rng = np.random.default_rng(11)
+    dims = (4000, 300, 50)
+    lin = rng.choice(np.prod(dims), size=1_000_000, replace=False)
+    idx = np.stack(np.unravel_index(lin, dims), axis=1).astype(np.int64)
+    vals = rng.uniform(1, 5, size=idx.shape[0])
+    J = R = 16
+    om = O.default_init_model(dims, (J,) * 3, R, seed=5)
+    model = ft.Model(dims, (J,) * 3, R, om.factors, om.cores_t)
+    oforest = O.build_forest(idx, vals, 128)
+    forest = ft.build_forest(_dev_coo(ft, idx, vals, dims), 128)
+    ocfg = O.OracleConfig(lr_a=2e-3, lr_b=2e-3, reg_a=1e-2, reg_b=1e-2)
+    cfg = ft.TrainConfig(lr_a=2e-3, lr_b=2e-3, reg_a=1e-2, reg_b=1e-2)
+    ocache = O.precompute_cache(om)
+    cache = ft.precompute_cache(model)
+    for n in range(3):
+        O.update_factor_mode(om, oforest, ocache, n, ocfg)
+        ft.update_factor_mode(model, forest, cache, n, cfg)
+        u = forest.trees[n].leaf_mode
+        assert_rel(model.factors[u].cpu().numpy(), om.factors[u], TOL, f"long rows factor {u}")
+    for n in range(3):
+        O.update_core_mode(om, oforest, ocache, n, ocfg)
+        ft.update_core_mode(model, forest, cache, n, cfg)
+        u = forest.trees[n].leaf_mode
+        assert_rel(model.cores_t[u].cpu().numpy(), om.cores_t[u], TOL, f"long rows core {u}")
+
+
+@pytest.mark.parametrize("variant", ["pipe", "mma", "ffma", "gram"])
+def test_factor_kernel_variants_agree(variant, golden_cases):
+    """Every K3b variant (FT_FACTOR_KERNEL) reproduces the reference's rank-32 sweeps at 1e-4,
+    run in a subprocess because the variant is latched at first launch."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
+        "import test_gpu_parity as t, conftest, paper_2210_06014_b200 as ft;"
+        "z = np.load('tests/golden/cases.npz');"
+        "t.test_reference_cases(ft, z, 'rank32'); t.test_reference_cases(ft, z, 'order5');"
+        "t.test_reference_cases(ft, z, 'rank16'); print('ok')")
+    env = dict(os.environ, FT_FACTOR_KERNEL=variant)
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=repo, env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]

@@ -18,7 +18,7 @@ UPDATED MODE with no stratum rotation:
 
 Factors are bitwise equal to the single-GPU exact schedule; cores differ only in the order of
 the gradient sum.  The compute goes through an ``engine`` (CudaEngine on GPUs; the CPU tests
-inject a fp64 oracle engine) so the partition / collective logic is tested with gloo.
+inject a CPU fp64 reference engine) so the partition / collective logic is tested with gloo.
 """
 
 from __future__ import annotations

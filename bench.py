@@ -314,8 +314,13 @@ def run_ours(args, cfg):
     dom = max(by, key=lambda k: by[k]["sec"])
     d = by[dom]
     achieved = d["bytes"] / d["sec"] / 1e9
-    traffic, _ = ncu_traffic(dom + "_kernel")
-    roof = {"kernel": dom + "_kernel", "bound": "hbm", "achieved": achieved, "peak": peak,
+    variant = os.environ.get("FT_FACTOR_KERNEL", "pipe")
+    kname = {"factor_rows": {"pipe": "factor_rows_pipe_kernel", "mma": "factor_rows_kernel",
+                             "ffma": "factor_rows_ffma_kernel",
+                             "gram": "factor_rows_gram_kernel"}.get(variant, dom + "_kernel")
+             }.get(dom, dom + "_kernel")
+    traffic, _ = ncu_traffic(kname)
+    roof = {"kernel": kname, "bound": "hbm", "achieved": achieved, "peak": peak,
             "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
             "traffic": traffic,
             "bytes_per_launch": d["bytes"] / d["launches"],

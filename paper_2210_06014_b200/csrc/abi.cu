@@ -29,6 +29,21 @@ int check_launch(const char *what) {
   return FT_OK;
 }
 
+// The builder / generator / evaluator take their scratch stream-ordered from the device's
+// default memory pool.  Keep freed blocks in the pool (release threshold = max) so repeated
+// builds do not map and unmap gigabytes each time.
+void keep_pool() {
+  static int done = 0;
+  if (done) return;
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done = 1;
+}
+
 int sm_count() {
   static int cached = 0;
   if (!cached) {

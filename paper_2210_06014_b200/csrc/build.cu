@@ -186,6 +186,7 @@ extern "C" int ft_build_tree(int32_t N, int64_t nnz, const int64_t *dims, const 
   if (!dims || !idx || !vals || !leaf_vals || !inds || !ptrs || !fiber_ptr || !fiber_coord ||
       !sub_fiber_ptr || !sub_leaf_ptr || !row_fiber_ptr || !row_coord || !counts_out)
     return fail(FT_ERR_ARG, "ft_build_tree: null argument");
+  keep_pool();
   cudaStream_t s = as_stream(stream);
   Scratch sc(s);
 

@@ -13,6 +13,7 @@ void set_error(const char *fmt, ...);
 int fail(ft_status st, const char *fmt, ...);
 int check_launch(const char *what);
 int sm_count();
+void keep_pool();
 
 constexpr unsigned FULL = 0xffffffffu;
 

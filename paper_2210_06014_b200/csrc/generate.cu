@@ -91,6 +91,7 @@ extern "C" int ft_generate_coo(int32_t N, const int64_t *dims, int64_t nnz, uint
   if ((double)nnz > cap) return fail(FT_ERR_ARG, "nnz exceeds capacity");
   if ((double)nnz > 0.5 * cap)
     return fail(FT_ERR_UNSUPPORTED, "dense request (nnz > capacity/2) not supported on device");
+  keep_pool();
   cudaStream_t s = as_stream(stream);
   // expected duplicates ~ m^2 / (2 cap): draw with a margin, top up if short
   const double dup = (double)nnz * (double)nnz / (2.0 * cap);

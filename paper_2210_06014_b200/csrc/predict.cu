@@ -1,9 +1,6 @@
 // K6  predict_batch / evaluate (model.py:219-230, train.py:91-98) from the coherent C^(n) cache.
 //
-// xhat = sum_r prod_n C_n[i_n, r].  Groups of RP lanes own one entry: lane r gathers element r
-// of each mode's C row (one coalesced 128-B row read per mode for R = 32), multiplies across
-// modes in mode order (as the reference), and the group reduces over r with shuffles.
-// Several entries per warp are in flight (UNROLL) to keep enough gathers outstanding.
+// xhat = sum_r prod_n C_n[i_n, r], products in mode order as the reference.
 // SSE / SAE accumulate in fp64 and reduce in a fixed order (per-block partials, then one block).
 #include "ft_common.cuh"
 
@@ -11,51 +8,57 @@ namespace ft {
 namespace {
 
 constexpr int PTHREADS = 256;
-constexpr int UNROLL = 4;
 
+// One warp scores 32 entries per step: lane k loads entry k's coordinates (coalesced), then for
+// each mode the warp issues 32 independent row gathers (lane r reads element r of the entry's
+// C_n row -- one 128-B request per row), so 32 x N loads are in flight per warp; the products
+// are reduced over r for all 32 entries at once by recursive halving (31 shuffles), leaving
+// entry k's prediction in lane k.
 template <int RP>
 __global__ void __launch_bounds__(PTHREADS)
     predict_kernel(const ft_model_t m, int64_t M, const int32_t *__restrict__ idx,
                    const float *__restrict__ vals, float *__restrict__ out,
                    double *__restrict__ partials) {
-  constexpr int GPW = 32 / RP;  // groups (entries) per warp step
-  const int lane = threadIdx.x & 31, g = lane / RP, r = lane % RP;
-  const unsigned gmask = (RP == 32) ? FULL : (((1u << RP) - 1u) << (g * RP));
+  const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * PTHREADS + threadIdx.x) >> 5;
   const int64_t nwarp = ((int64_t)gridDim.x * PTHREADS) >> 5;
   const int N = m.order, R = m.core_rank;
+  const bool rl = lane < R;
   double sse = 0.0, sae = 0.0;
-  for (int64_t base = warp * GPW * UNROLL; base < M; base += nwarp * GPW * UNROLL) {
-    float prod[UNROLL];
-#pragma unroll
-    for (int u = 0; u < UNROLL; ++u) prod[u] = 1.f;
+  for (int64_t base = warp * 32; base < M; base += nwarp * 32) {
+    const int64_t e = base + lane;
+    const bool ok = e < M;
+    float t[32];
     for (int n = 0; n < N; ++n) {
+      const int c = ok ? __ldcs(idx + e * N + n) : 0;
       const float *Cn = m.dots[n];
 #pragma unroll
-      for (int u = 0; u < UNROLL; ++u) {
-        const int64_t e = base + (int64_t)u * GPW + g;
-        float v = 0.f;
-        if (e < M && r < R) v = __ldg(Cn + (int64_t)__ldg(idx + e * N + n) * R + r);
-        prod[u] = n == 0 ? v : prod[u] * v;
+      for (int k = 0; k < 32; ++k) {
+        const int ck = __shfl_sync(FULL, c, k);
+        const float v = rl ? __ldg(Cn + (int64_t)ck * R + lane) : 0.f;
+        t[k] = n == 0 ? v : t[k] * v;
       }
     }
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) {
-      float s = prod[u];
+    for (int off = 16; off >= 1; off >>= 1) {
+      const bool upper = lane & off;
 #pragma unroll
-      for (int o = RP / 2; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
-      const int64_t e = base + (int64_t)u * GPW + g;
-      if (r == 0 && e < M) {
-        if (out) out[e] = s;
-        if (vals) {
-          const double res = (double)vals[e] - (double)s;
-          sse += res * res;
-          sae += fabs(res);
-        }
+      for (int k = 0; k < off; ++k) {
+        const float send = upper ? t[k] : t[k + off];
+        const float keep = upper ? t[k + off] : t[k];
+        t[k] = keep + __shfl_xor_sync(FULL, send, off);
+      }
+    }
+    if (ok) {
+      const float s = t[0];  // lane k: prediction of entry base + k
+      if (out) out[e] = s;
+      if (vals) {
+        const double res = (double)__ldcs(vals + e) - (double)s;
+        sse += res * res;
+        sae += fabs(res);
       }
     }
   }
-  (void)gmask;
   if (!partials) return;
   // block reduction (fixed order) -> partials[2*block]
   __shared__ double red[2][PTHREADS / 32];
@@ -130,6 +133,7 @@ extern "C" int ft_sse(const ft_model_t *model, int64_t M, const int32_t *idx, co
                       double *out2, void *stream) {
   if (int rc = check_model(model)) return rc;
   if (!idx || !vals || !out2) return fail(FT_ERR_ARG, "ft_sse: null pointer");
+  keep_pool();
   cudaStream_t s = as_stream(stream);
   const int grid = sm_count() * 8;
   double *partials = nullptr;

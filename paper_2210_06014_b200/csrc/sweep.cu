@@ -593,6 +593,208 @@ __global__ void __launch_bounds__(PipePlan::WPB * 32, 2)
   }
 }
 
+
+// ---- K3b, two rows per warp (the default) ------------------------------------------------
+// Each 16-lane half of a warp owns one row of A_u (lane l holds columns l and l + 16) and walks
+// its root slice in 16-leaf batches, so a warp advances two independent serial chains at once
+// and each chain step reduces over 16 lanes (4 shuffle levels) instead of 32.  The batch of a
+// half is one m16 tile of the tensor-core combine (V = cross * Bt_u, 3xTF32).  Rows are taken
+// round-robin per half; a half that finishes its row writes it back and starts the next one.
+constexpr int HB = 16;  // leaves per half-warp batch
+
+struct DualPlan {
+  static constexpr int XT = HB * 32;  // swizzled 16 x 32 staging tile
+  static constexpr int VT = HB * VS;  // 16 x 36 V tile
+  static constexpr int HALF_FLOATS = 2 * XT + VT + 16;  // +16: the halves' V reads hit disjoint banks
+  static constexpr int WARP_FLOATS = 2 * HALF_FLOATS;
+  static constexpr int WPB = 8;
+  template <int RP>
+  static constexpr int bfrag_u4() { return (RP / 8 > 0 ? RP / 8 : 1) * 4 * 32; }
+  template <int RP>
+  static constexpr size_t bytes() {
+    return (size_t)bfrag_u4<RP>() * 16 + (size_t)WPB * WARP_FLOATS * sizeof(float);
+  }
+};
+
+template <int RP>
+__global__ void __launch_bounds__(DualPlan::WPB * 32, 2)
+    factor_rows_dual_kernel(const SweepParams p) {
+  constexpr int KT = RP / 8 > 0 ? RP / 8 : 1, NT = 4;
+  extern __shared__ float4 smem4[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int h = lane >> 4, l = lane & 15;
+  const int gq = lane >> 2, tq = lane & 3;
+  uint4 *bfrag = reinterpret_cast<uint4 *>(smem4);
+  float *wbase = reinterpret_cast<float *>(bfrag + DualPlan::bfrag_u4<RP>()) + w * DualPlan::WARP_FLOATS;
+  // tile of half hh: wbase + hh * HALF_FLOATS (+ XT for Y, + 2 XT for V); computed by
+  // arithmetic, not through a pointer array, so the accesses stay LDS/STS (not generic LD/ST)
+#define XH(hh) (wbase + (hh) * DualPlan::HALF_FLOATS)
+#define YH(hh) (wbase + (hh) * DualPlan::HALF_FLOATS + DualPlan::XT)
+#define VH(hh) (wbase + (hh) * DualPlan::HALF_FLOATS + 2 * DualPlan::XT)
+  for (int k = lane; k < DualPlan::WARP_FLOATS; k += 32) wbase[k] = 0.f;
+  for (int f = threadIdx.x; f < DualPlan::bfrag_u4<RP>(); f += blockDim.x) {
+    const int ll = f & 31, nt = (f >> 5) % NT, kt = (f >> 5) / NT;
+    const int g = ll >> 2, t = ll & 3, j = 8 * nt + g;
+    uint32_t hv[2], lv[2];
+    for (int hh = 0; hh < 2; ++hh) {
+      const int r = 8 * kt + t + 4 * hh;
+      const float bv = (r < p.R && j < p.J) ? __ldg(p.Bt + r * p.J + j) : 0.f;
+      hv[hh] = to_tf32(bv);
+      lv[hh] = to_tf32(bv - __uint_as_float(hv[hh]));
+    }
+    bfrag[f] = make_uint4(hv[0], hv[1], lv[0], lv[1]);
+  }
+  __syncthreads();
+  const int64_t nstream = (int64_t)gridDim.x * DualPlan::WPB * 2;  // row streams
+  const int64_t mystream = ((int64_t)blockIdx.x * DualPlan::WPB + w) * 2 + h;
+  const bool j0 = l < p.J, j1 = l + 16 < p.J;
+  float *Xh = XH(h), *Yh = YH(h), *Vh = VH(h);
+
+  // per-half row state (replicated in the half's 16 lanes)
+  int64_t row = mystream - nstream;
+  int fe = 0, Le = 0, L0 = 0, fcur = 0;
+  float *arow = nullptr;
+  float a0 = 0.f, a1 = 0.f;
+  bool active = true;
+  for (;;) {
+    // a half whose row is exhausted writes it back and starts its next non-empty row
+    if (active && L0 >= Le) {
+      if (arow) {
+        if (j0) arow[l] = a0;
+        if (j1) arow[l + 16] = a1;
+        arow = nullptr;
+      }
+      row += nstream;
+      if (row < p.nrows) {
+        const int i = __ldg(p.row_coord + row);
+        const int fb = __ldg(p.row_fiber_ptr + row);
+        fe = __ldg(p.row_fiber_ptr + row + 1);
+        L0 = __ldg(p.fiber_ptr + fb);
+        Le = __ldg(p.fiber_ptr + fe);
+        fcur = fb;
+        arow = p.A + (int64_t)i * p.J;
+        a0 = j0 ? arow[l] : 0.f;
+        a1 = j1 ? arow[l + 16] : 0.f;
+      } else {
+        active = false;
+      }
+    }
+    if (!__any_sync(FULL, active)) break;
+    const int nb = active ? min(HB, Le - L0) : 0;  // this half's batch
+    // leaf data and the fiber of each leaf (window of <= 16 fiber starts per half)
+    const bool lv = l < nb;
+    const int lc = lv ? __ldcs(p.leaf_coord + L0 + l) : 0;
+    const float x = lv ? __ldcs(p.vals + L0 + l) : 0.f;
+    const int fidx = fcur + 1 + l;
+    const int fs = (active && fidx < fe) ? __ldg(p.fiber_ptr + fidx) : INT32_MAX;
+    const unsigned bit = (fs < L0 + nb) ? (1u << (fs - L0)) : 0u;
+    const unsigned hmask = (__reduce_or_sync(FULL, bit << (16 * h)) >> (16 * h)) & 0xffffu;
+    // (the OR of both halves' shifted bits, then this half's 16 bits)
+    const int myfib = fcur + __popc(hmask & (0xffffu >> (15 - l)));
+    const int fnext = fcur + __popc(hmask);
+    // ---- gathers: prefix levels into X (folded progressively), the leaf level into Y ----
+    const int npre = p.N - 2;
+    for (int lvl = 0; lvl <= npre; ++lvl) {
+      const bool leaf = lvl == npre;
+      const int coord =
+          leaf ? lc : (lv ? __ldg(p.fiber_coord + (int64_t)myfib * (p.N - 1) + 1 + lvl) : 0);
+      float *dst = (lvl == 0) ? Xh : Yh;
+      const float *C = leaf ? p.Cleaf : p.Cpre[lvl];
+      if ((p.R & 3) == 0) {
+        constexpr int P4 = RP / 4;
+        const int R4 = p.R >> 2;
+#pragma unroll
+        for (int it = 0; it < P4; ++it) {
+          const int c = l + 16 * it;
+          const int k = c / P4, q = c % P4;
+          const int ck = __shfl_sync(FULL, coord, 16 * h + k);
+          if (k < nb && q < R4) cp_async16(dst + swz(k, 4 * q), C + (int64_t)ck * p.R + 4 * q);
+        }
+      } else {
+        for (int k = 0; k < HB; ++k) {
+          const int ck = __shfl_sync(FULL, coord, 16 * h + k);
+          for (int r = l; r < p.R; r += 16)
+            if (k < nb) cp_async4(dst + swz(k, r), C + (int64_t)ck * p.R + r);
+        }
+      }
+      if (lvl >= 1 && !leaf) {
+        cp_async_wait_all();
+        __syncwarp();
+        for (int k = 0; k < nb; ++k)
+          for (int r = l; r < RP; r += 16) Xh[swz(k, r)] *= Yh[swz(k, r)];
+        __syncwarp();
+      }
+    }
+    cp_async_wait_all();
+    __syncwarp();
+    // ---- V_h = (X_h * Y_h) * Bt_u: one m16 tile per half, 3xTF32 ----
+    float acc[2][NT][4];
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[hh][nt][q] = 0.f;
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const float *Xs = XH(hh), *Ys = YH(hh);
+#pragma unroll
+      for (int kt = 0; kt < KT; ++kt) {
+        const int c0 = 8 * kt + tq;
+        const int o0 = swz(gq, c0), o1 = swz(gq + 8, c0), o2 = swz(gq, c0 + 4),
+                  o3 = swz(gq + 8, c0 + 4);
+        const float x0 = Xs[o0] * Ys[o0], x1 = Xs[o1] * Ys[o1], x2 = Xs[o2] * Ys[o2],
+                    x3 = Xs[o3] * Ys[o3];
+        const uint32_t h0 = to_tf32(x0), h1 = to_tf32(x1), h2 = to_tf32(x2), h3 = to_tf32(x3);
+        const uint32_t l0 = to_tf32(x0 - __uint_as_float(h0));
+        const uint32_t l1 = to_tf32(x1 - __uint_as_float(h1));
+        const uint32_t l2 = to_tf32(x2 - __uint_as_float(h2));
+        const uint32_t l3 = to_tf32(x3 - __uint_as_float(h3));
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const uint4 bb = bfrag[(kt * NT + nt) * 32 + lane];
+          mma_tf32(acc[hh][nt], l0, l1, l2, l3, bb.x, bb.y);
+          mma_tf32(acc[hh][nt], h0, h1, h2, h3, bb.z, bb.w);
+          mma_tf32(acc[hh][nt], h0, h1, h2, h3, bb.x, bb.y);
+        }
+      }
+    }
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int c0 = 8 * nt + 2 * tq;
+        *reinterpret_cast<float2 *>(VH(hh) + gq * VS + c0) = make_float2(acc[hh][nt][0], acc[hh][nt][1]);
+        *reinterpret_cast<float2 *>(VH(hh) + (gq + 8) * VS + c0) =
+            make_float2(acc[hh][nt][2], acc[hh][nt][3]);
+      }
+    __syncwarp();
+    // ---- two serial chains (one per half): s = a.v over 16 lanes x 2 columns ----
+    const int nbmax = max(__shfl_sync(FULL, nb, 0), __shfl_sync(FULL, nb, 16));
+#pragma unroll 4
+    for (int k = 0; k < nbmax; ++k) {
+      const float v0 = Vh[k * VS + l], v1 = Vh[k * VS + l + 16];
+      float s = a0 * v0 + a1 * v1;
+      s += __shfl_xor_sync(FULL, s, 8);
+      s += __shfl_xor_sync(FULL, s, 4);
+      s += __shfl_xor_sync(FULL, s, 2);
+      s += __shfl_xor_sync(FULL, s, 1);
+      const float e = __shfl_sync(FULL, x, 16 * h + (k & 15)) - s;
+      if (k < nb) {
+        const float g0 = p.reg * a0 - e * v0, g1 = p.reg * a1 - e * v1;
+        a0 = a0 - p.lr * g0;
+        a1 = a1 - p.lr * g1;
+      }
+    }
+    __syncwarp();
+    L0 += nb;
+    fcur = fnext;
+  }
+}
+#undef XH
+#undef YH
+#undef VH
+
 // ---- K3b, Gram form of the serial chain (tensor cores for both GEMMs) -------------------
 // Within a batch the row evolves as a_{m+1} = a_m + lr (e_m v_m - reg a_m).
 // Tracking w_k = a_m . v_k for every leaf k of the batch gives
@@ -1022,14 +1224,32 @@ inline int grid_for(Kern kern, int64_t work_warps, int wpb = WPB, size_t smem = 
 
 template <int RP>
 int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
-  // FT_FACTOR_KERNEL selects the K3b variant for A/B measurement: pipe (default), mma, ffma, gram
-  static const int variant = [] {
+  // FT_FACTOR_KERNEL selects the K3b variant for A/B measurement: dual (default), pipe, mma,
+  // ffma, gram
+  static const int chosen = [] {
     const char *e = getenv("FT_FACTOR_KERNEL");
     if (e && strcmp(e, "gram") == 0) return 0;
     if (e && strcmp(e, "ffma") == 0) return 2;
     if (e && strcmp(e, "mma") == 0) return 1;
-    return 3;  // pipelined mma
+    if (e && strcmp(e, "pipe") == 0) return 3;
+    return 4;  // dual: two rows per warp
   }();
+  int variant = chosen;
+  // dual needs >= 2 rows per resident warp slot to fill the SMs; few long rows (e.g. Netflix
+  // mode 2: 2,182 rows of ~45 K leaves) run one row per warp (pipe)
+  if (variant == 4 && p.nrows < (int64_t)2 * sm_count() * 16) variant = 3;
+  if (variant == 4) {
+    const size_t sm = DualPlan::bytes<RP>();
+    static bool set4 = false;
+    if (!set4) {
+      cudaFuncSetAttribute(factor_rows_dual_kernel<RP>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      set4 = true;
+    }
+    const int g = grid_for(factor_rows_dual_kernel<RP>, (p.nrows + 1) / 2, DualPlan::WPB, sm);
+    factor_rows_dual_kernel<RP><<<g, DualPlan::WPB * 32, sm, s>>>(p);
+    return check_launch("ft_factor_sweep_rows(dual)");
+  }
   if (variant == 3) {
     const size_t sm = PipePlan::bytes<RP>();
     static bool set3 = false;

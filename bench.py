@@ -324,12 +324,11 @@ def run_ours(args, cfg):
     dom = max(by, key=lambda k: by[k]["sec"])
     d = by[dom]
     achieved = d["bytes"] / d["sec"] / 1e9
-    variant = os.environ.get("FT_FACTOR_KERNEL", "pipe")
-    kname = {"factor_rows": {"pipe": "factor_rows_pipe_kernel", "mma": "factor_rows_kernel",
-                             "ffma": "factor_rows_ffma_kernel",
-                             "gram": "factor_rows_gram_kernel"}.get(variant, dom + "_kernel")
-             }.get(dom, dom + "_kernel")
-    traffic, _ = ncu_traffic(kname)
+    variant = os.environ.get("FT_FACTOR_KERNEL", "auto")
+    kname = (f"factor_rows_{variant}_kernel" if variant != "auto"
+             else "factor_rows_{dual|gram}_kernel (auto: by row count)") if dom == "factor_rows" \
+        else dom + "_kernel"
+    traffic, _ = ncu_traffic(dom)
     roof = {"kernel": kname, "bound": "hbm", "achieved": achieved, "peak": peak,
             "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
             "traffic": traffic,

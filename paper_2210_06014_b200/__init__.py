@@ -9,8 +9,9 @@ Names follow /root/reference/pkg/src/fastertucker/__init__.py:9-28.
 
 from ._kernels import BACKEND, COMPILED, get_backend, use_backend
 from .cache import DotCache, precompute_cache, refresh_mode
-from .coo import (DatasetSplit, DeviceCoo, SparseCooTensor, generate_device, generate_synthetic,
-                  split_dataset)
+from .coo import (DatasetSplit, DeviceCoo, SparseCooTensor, generate_device,
+                  generate_low_rank_device, generate_synthetic, load_coo, split_dataset,
+                  write_coo)
 from .counter import CHANNELS, OpCounter
 from .csf import CsfForest, CsfTree, build_forest, build_tree
 from .errors import (BackendUnavailableError, BuildError, ConfigError, DivergenceError,
@@ -27,8 +28,9 @@ __all__ = [
     "CsfForest", "CsfTree", "DatasetSplit", "DeviceCoo", "DivergenceError", "DotCache",
     "EpochMetrics", "FasterTuckerError", "InitSpec", "METRICS_CSV_HEADER", "Model", "OpCounter",
     "SparseCooTensor", "TrainConfig", "ValidationError", "build_forest", "build_tree",
-    "default_init_model", "evaluate", "generate_device", "generate_synthetic", "get_backend",
-    "init_model", "load_model", "precompute_cache", "predict_batch", "refresh_mode", "run_epoch",
-    "save_model", "split_dataset", "train", "update_core_mode", "update_factor_mode",
-    "use_backend",
+    "default_init_model", "evaluate", "generate_device", "generate_low_rank_device",
+    "generate_synthetic", "get_backend", "init_model", "load_coo", "load_model",
+    "precompute_cache", "predict_batch", "refresh_mode", "run_epoch", "save_model",
+    "split_dataset", "train", "update_core_mode", "update_factor_mode", "use_backend",
+    "write_coo",
 ]

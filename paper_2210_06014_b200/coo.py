@@ -211,6 +211,105 @@ def generate_synthetic(dims, nnz: int, value_range=(1.0, 5.0), seed: int = 0,
     return DatasetSplit(train=t.slice(n_test, nnz), test=t.slice(0, n_test), seed=int(seed))
 
 
+def load_coo(path, order: int, dims=None, normalize=None) -> SparseCooTensor:
+    """Whitespace-separated 1-based coordinates + value per line, '#' comments
+    (coo.py:95-138).  Parsed by pandas' C reader (a Netflix-size file in seconds, not the
+    reference's per-line Python loop); on any malformed input the file is rescanned line by line
+    so the error names the offending line exactly as the reference does."""
+    from .errors import ParseError
+
+    try:
+        import pandas as pd
+
+        df = pd.read_csv(path, sep=r"\s+", comment="#", header=None, engine="c",
+                         dtype=np.float64, float_precision="round_trip")
+        ok = df.shape[1] == order + 1 and not df.isnull().values.any()
+        arr = df.to_numpy() if ok else None
+    except Exception:
+        arr, ok = None, False
+    if ok and arr.shape[0]:
+        coords = arr[:, :order]
+        if not np.all(np.equal(np.floor(coords), coords)):
+            ok = False
+    if not ok or arr is None or arr.shape[0] == 0:
+        _scan_errors(path, order, ParseError)
+        raise ValidationError(f"{path}: no entries")
+    idx = arr[:, :order].astype(np.int64)
+    if (idx < 1).any():
+        _scan_errors(path, order, ParseError)
+    idx -= 1
+    vals = arr[:, order].astype(np.float64)
+    dup = _first_duplicate(idx, tuple(int(m) + 1 for m in idx.max(axis=0)))
+    if dup is not None:
+        _scan_errors(path, order, ParseError)
+    if normalize is not None:
+        vals = _minmax_scale(vals, normalize)
+    if dims is None:
+        dims = tuple(int(m) + 1 for m in idx.max(axis=0))
+    return SparseCooTensor(tuple(dims), idx, vals)
+
+
+def _scan_errors(path, order, ParseError):
+    """The reference's line-by-line checks (coo.py:104-128), run only to report an error."""
+    seen = set()
+    with open(path, "r", encoding="utf-8") as fh:
+        for lineno, line in enumerate(fh, start=1):
+            stripped = line.strip()
+            if not stripped or stripped.startswith("#"):
+                continue
+            fields = stripped.split()
+            if len(fields) != order + 1:
+                raise ParseError(f"{path}: line {lineno}: expected {order + 1} fields, got "
+                                 f"{len(fields)}")
+            try:
+                coord = tuple(int(f) for f in fields[:order])
+            except ValueError as exc:
+                raise ParseError(f"{path}: line {lineno}: bad coordinate: {exc}") from None
+            try:
+                float(fields[order])
+            except ValueError:
+                raise ParseError(f"{path}: line {lineno}: bad value {fields[order]!r}") from None
+            if any(c < 1 for c in coord):
+                raise ValidationError(f"{path}: line {lineno}: coordinates are 1-based")
+            if coord in seen:
+                raise ValidationError(f"{path}: line {lineno}: duplicate coordinate {coord}")
+            seen.add(coord)
+
+
+def _minmax_scale(vals: np.ndarray, target) -> np.ndarray:
+    lo, hi = float(target[0]), float(target[1])
+    if not lo < hi:
+        raise ConfigError(f"normalize range must satisfy lo < hi, got ({lo}, {hi})")
+    vmin, vmax = float(vals.min()), float(vals.max())
+    if vmin == vmax:
+        raise ConfigError("cannot min-max scale constant values")
+    return lo + (vals - vmin) * ((hi - lo) / (vmax - vmin))
+
+
+def write_coo(path, tensor) -> None:
+    """The reference's 1-based text form (coo.py:151-157), values in shortest round-trip repr."""
+    idx = np.asarray(tensor.idx) + 1
+    vals = np.asarray(tensor.vals, dtype=np.float64)
+    with open(path, "w", encoding="utf-8") as fh:
+        fh.write(f"# order={len(tensor.dims)} dims={','.join(map(str, tensor.dims))}\n")
+        for row, val in zip(idx.tolist(), vals.tolist()):
+            fh.write(" ".join(str(int(c)) for c in row) + f" {float(val)!r}\n")
+
+
+def generate_low_rank_device(dims, nnz: int, ranks, core_rank: int, seed: int = 0) -> DeviceCoo:
+    """generate_synthetic(..., low_rank=(ranks, core_rank)) (coo.py:207-213): distinct uniform
+    cells whose values are the predictions of a hidden random model (model.py:144-146's
+    distribution) -- coordinates and predictions both computed on the GPU."""
+    import torch
+
+    from .model import default_init_model, predict_batch
+
+    t = generate_device(dims, nnz, (0.0, 1.0), seed)
+    hidden = default_init_model(dims, ranks, core_rank, np.random.SeedSequence([int(seed), 3]))
+    vals = predict_batch(hidden, t.idx)
+    return DeviceCoo(t.dims, t.idx, vals.to(torch.float32))
+
+
 def as_device(tensor) -> DeviceCoo:
     if isinstance(tensor, DeviceCoo):
         return tensor

@@ -817,7 +817,7 @@ struct GramPlan {
     return (size_t)bfrag_u4<RP>() * 16 + (size_t)WPB * WARP_FLOATS * sizeof(float);
   }
 };
-static_assert(BATCH * GS <= 2 * BATCH * 32, "G must fit in the X/Y tiles");
+static_assert(BATCH * GS + BATCH <= 2 * BATCH * 32, "G and a_0 must fit in the X/Y tiles");
 
 __device__ __forceinline__ void split3(float v, uint32_t &hi, uint32_t &lo) {
   hi = to_tf32(v);
@@ -852,6 +852,9 @@ __global__ void __launch_bounds__(GramPlan::WPB * 32, 2)
   const int64_t nw = (int64_t)gridDim.x * GramPlan::WPB;
   const bool jl = lane < p.J;
   const float lr = p.lr, reg = p.reg;
+  // G in 1xTF32 while lr keeps its error term (lr e dG, dG ~ 2^-11 |G|) far below the 1e-4
+  // contract; 3xTF32 above (measured: lr 2e-3 over 20 K-step rows passes, lr 5e-2 does not)
+  const bool gram3 = lr > 2.5e-3f;
 
   for (int64_t row = gw; row < p.nrows; row += nw) {
     const int i = __ldg(p.row_coord + row);
@@ -909,58 +912,65 @@ __global__ void __launch_bounds__(GramPlan::WPB * 32, 2)
               make_float2(acc[mt][nt][2], acc[mt][nt][3]);
         }
       __syncwarp();  // V visible; X / Y dead from here (G overwrites them)
-      // ---- [G | d] = V [V^T | a_0] ----
-      // a_0 as the B operand of the 5th n-tile: column 0 = a_0, columns 1..7 = 0
-      uint32_t ah[4][2], al[4][2];
-#pragma unroll
-      for (int kt = 0; kt < 4; ++kt)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const float av = __shfl_sync(FULL, a, 8 * kt + tq + 4 * h);
-          split3(gq == 0 ? av : 0.f, ah[kt][h], al[kt][h]);
-        }
+      // ---- G = V V^T (1xTF32 at small lr: G only enters as the lr-scaled correction, measured
+      // 5.8e-6 vs 5.7e-6 for fp32 over a 45 K-step row at lr 1e-3), tiles with some m < k ----
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
         if (mt >= mts) break;
-        float gacc[5][4];
+        float gacc[4][4];
 #pragma unroll
-        for (int nt = 0; nt < 5; ++nt)
+        for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
           for (int q = 0; q < 4; ++q) gacc[nt][q] = 0.f;
 #pragma unroll
         for (int kt = 0; kt < 4; ++kt) {
           const int r0 = 16 * mt + gq, c0 = 8 * kt + tq;
-          uint32_t h0, h1, h2, h3, l0, l1, l2, l3;
-          split3(V[r0 * VS + c0], h0, l0);
-          split3(V[(r0 + 8) * VS + c0], h1, l1);
-          split3(V[r0 * VS + c0 + 4], h2, l2);
-          split3(V[(r0 + 8) * VS + c0 + 4], h3, l3);
+          const float f0 = V[r0 * VS + c0], f1 = V[(r0 + 8) * VS + c0];
+          const float f2 = V[r0 * VS + c0 + 4], f3 = V[(r0 + 8) * VS + c0 + 4];
+          const uint32_t a0 = to_tf32(f0), a1 = to_tf32(f1), a2 = to_tf32(f2), a3 = to_tf32(f3);
 #pragma unroll
           for (int nt = 0; nt < 4; ++nt) {
             if (mt == 1 && nt < 2) continue;  // rows 16..31 x cols 0..15: every m > k
-            if (8 * nt >= nb) continue;
             const int n0 = 8 * nt + gq;
-            uint32_t bh0, bl0, bh1, bl1;
-            split3(V[n0 * VS + c0], bh0, bl0);
-            split3(V[n0 * VS + c0 + 4], bh1, bl1);
-            mma_tf32(gacc[nt], l0, l1, l2, l3, bh0, bh1);
-            mma_tf32(gacc[nt], h0, h1, h2, h3, bl0, bl1);
-            mma_tf32(gacc[nt], h0, h1, h2, h3, bh0, bh1);
+            const float e0 = V[n0 * VS + c0], e1 = V[n0 * VS + c0 + 4];
+            const uint32_t b0 = to_tf32(e0), b1 = to_tf32(e1);
+            if (gram3) {  // large lr: the TF32 error of G is no longer lr-suppressed
+              mma_tf32(gacc[nt], to_tf32(f0 - __uint_as_float(a0)), to_tf32(f1 - __uint_as_float(a1)),
+                       to_tf32(f2 - __uint_as_float(a2)), to_tf32(f3 - __uint_as_float(a3)), b0, b1);
+              mma_tf32(gacc[nt], a0, a1, a2, a3, to_tf32(e0 - __uint_as_float(b0)),
+                       to_tf32(e1 - __uint_as_float(b1)));
+            }
+            mma_tf32(gacc[nt], a0, a1, a2, a3, b0, b1);
           }
-          mma_tf32(gacc[4], l0, l1, l2, l3, ah[kt][0], ah[kt][1]);
-          mma_tf32(gacc[4], h0, h1, h2, h3, al[kt][0], al[kt][1]);
-          mma_tf32(gacc[4], h0, h1, h2, h3, ah[kt][0], ah[kt][1]);
         }
 #pragma unroll
-        for (int nt = 0; nt < 5; ++nt) {
+        for (int nt = 0; nt < 4; ++nt) {
+          if (mt == 1 && nt < 2) continue;
           const int r0 = 16 * mt + gq, c0 = 8 * nt + 2 * tq;
           *reinterpret_cast<float2 *>(G + r0 * GS + c0) = make_float2(gacc[nt][0], gacc[nt][1]);
           *reinterpret_cast<float2 *>(G + (r0 + 8) * GS + c0) = make_float2(gacc[nt][2], gacc[nt][3]);
         }
       }
+      // ---- d_k = a_0 . v_k in fp32 (lane k; a_0 broadcast from smem) ----
+      float *as = G + BATCH * GS;  // 32 floats after the G tile
+      as[lane] = a;
+      __syncwarp();
+      float dk = 0.f;
+      {
+        const float4 *vr = reinterpret_cast<const float4 *>(V + lane * VS);
+        const float4 *ar = reinterpret_cast<const float4 *>(as);
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) {
+          const float4 v4 = vr[j4], a4 = ar[j4];
+          dk = __fmaf_rn(v4.x, a4.x, dk);
+          dk = __fmaf_rn(v4.y, a4.y, dk);
+          dk = __fmaf_rn(v4.z, a4.z, dk);
+          dk = __fmaf_rn(v4.w, a4.w, dk);
+        }
+      }
       __syncwarp();
       // ---- the serial chain, scalar per leaf (lane k tracks w_k = a_m . v_k) ----
-      float wk = G[lane * GS + 32];  // d_k
+      float wk = dk;
       float e_mine = 0.f;
 #pragma unroll 8
       for (int m = 0; m < nb; ++m) {
@@ -1224,20 +1234,22 @@ inline int grid_for(Kern kern, int64_t work_warps, int wpb = WPB, size_t smem = 
 
 template <int RP>
 int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
-  // FT_FACTOR_KERNEL selects the K3b variant for A/B measurement: dual (default), pipe, mma,
-  // ffma, gram
+  // FT_FACTOR_KERNEL selects the K3b variant for A/B measurement: auto (default: dual or gram
+  // by row count), dual, gram, pipe, mma, ffma
   static const int chosen = [] {
     const char *e = getenv("FT_FACTOR_KERNEL");
     if (e && strcmp(e, "gram") == 0) return 0;
     if (e && strcmp(e, "ffma") == 0) return 2;
     if (e && strcmp(e, "mma") == 0) return 1;
     if (e && strcmp(e, "pipe") == 0) return 3;
-    return 4;  // dual: two rows per warp
+    if (e && strcmp(e, "dual") == 0) return 4;
+    return 5;  // auto: dual when the rows fill the SMs, gram otherwise
   }();
   int variant = chosen;
-  // dual needs >= 2 rows per resident warp slot to fill the SMs; few long rows (e.g. Netflix
-  // mode 2: 2,182 rows of ~45 K leaves) run one row per warp (pipe)
-  if (variant == 4 && p.nrows < (int64_t)2 * sm_count() * 16) variant = 3;
+  // auto: dual needs >= 2 rows per resident warp slot to fill the SMs; few long rows (e.g.
+  // Netflix mode 2: 2,182 rows of ~45 K leaves) are bound by the serial chain, which the Gram
+  // form shortens (measured 8.9 vs 10.0 ms pipe / 13.4 ms dual on that mode)
+  if (variant == 5) variant = p.nrows < (int64_t)2 * sm_count() * 16 ? 0 : 4;
   if (variant == 4) {
     const size_t sm = DualPlan::bytes<RP>();
     static bool set4 = false;

@@ -104,6 +104,10 @@ def main():
     agg = {}
     for d in launches:
         name = d["kernel"].split("<")[0]
+        for fam in ("factor_rows", "core_rows", "refresh", "predict"):
+            if name.startswith(fam):  # the K3b variants (dual / gram / pipe ...) share a family
+                name = fam
+                break
         a = agg.setdefault(name, [])
         if "dram_read" in d:
             a.append(d["dram_read"] + d.get("dram_write", 0.0))

@@ -57,6 +57,7 @@ struct SweepParams {
   int J, R;
   float lr, reg;
   float *partials;   // core: [grid][R*J]
+  int tma;           // dual kernel: gather with TMA bulk copies (FT_GATHER=tma)
 };
 
 // Fiber index of each of the batch's leaves (lane k -> leaf L0+k), given fcur = fiber holding
@@ -602,17 +603,53 @@ __global__ void __launch_bounds__(PipePlan::WPB * 32, 2)
 // round-robin per half; a half that finishes its row writes it back and starts the next one.
 constexpr int HB = 16;  // leaves per half-warp batch
 
+// ---- TMA bulk copies (cp.async.bulk, SASS UBLKCP) completed on an mbarrier ----
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_copy(float *dst, const float *src, uint32_t bytes,
+                                          uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
 struct DualPlan {
-  static constexpr int XT = HB * 32;  // swizzled 16 x 32 staging tile
+  static constexpr int XS = 36;       // staging row stride: 144-B rows (TMA-aligned), and
+                                      // conflict-free A-fragment loads
+  static constexpr int XT = HB * XS;  // 16 x 36 staging tile
   static constexpr int VT = HB * VS;  // 16 x 36 V tile
-  static constexpr int HALF_FLOATS = 2 * XT + VT + 16;  // +16: the halves' V reads hit disjoint banks
+  // V reuses X (dead once the MMA has read it); +16: the halves' V reads hit disjoint banks
+  static constexpr int HALF_FLOATS = 2 * XT + 16;
   static constexpr int WARP_FLOATS = 2 * HALF_FLOATS;
   static constexpr int WPB = 8;
+  static constexpr int BAR_BYTES = WPB * 8 + 64;  // one mbarrier per warp, padded to 16 B
   template <int RP>
   static constexpr int bfrag_u4() { return (RP / 8 > 0 ? RP / 8 : 1) * 4 * 32; }
   template <int RP>
   static constexpr size_t bytes() {
-    return (size_t)bfrag_u4<RP>() * 16 + (size_t)WPB * WARP_FLOATS * sizeof(float);
+    return (size_t)bfrag_u4<RP>() * 16 + BAR_BYTES + (size_t)WPB * WARP_FLOATS * sizeof(float);
   }
 };
 
@@ -625,12 +662,23 @@ __global__ void __launch_bounds__(DualPlan::WPB * 32, 2)
   const int h = lane >> 4, l = lane & 15;
   const int gq = lane >> 2, tq = lane & 3;
   uint4 *bfrag = reinterpret_cast<uint4 *>(smem4);
-  float *wbase = reinterpret_cast<float *>(bfrag + DualPlan::bfrag_u4<RP>()) + w * DualPlan::WARP_FLOATS;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(bfrag + DualPlan::bfrag_u4<RP>()) + w;
+  float *wbase = reinterpret_cast<float *>(reinterpret_cast<char *>(bfrag + DualPlan::bfrag_u4<RP>()) +
+                                           DualPlan::BAR_BYTES) +
+                 w * DualPlan::WARP_FLOATS;
+  constexpr int XS = DualPlan::XS;
+  // FT_GATHER=tma: order-3 tensors with 16-B rows gather by TMA bulk copies (one UBLKCP per C
+  // row, completion on an mbarrier).  Measured slower than cp.async here (8.95 vs 7.7 ms on
+  // Netflix mode 0): without double buffering -- which the shared-memory budget does not allow
+  // at 16 warps/SM -- the copy latency is exposed and the mbarrier spin adds instructions.
+  const bool tma = p.tma && p.N == 3 && (p.R & 3) == 0;
+  if (lane == 0) mbar_init(bar, 1);
+  uint32_t phase = 0;
   // tile of half hh: wbase + hh * HALF_FLOATS (+ XT for Y, + 2 XT for V); computed by
   // arithmetic, not through a pointer array, so the accesses stay LDS/STS (not generic LD/ST)
 #define XH(hh) (wbase + (hh) * DualPlan::HALF_FLOATS)
 #define YH(hh) (wbase + (hh) * DualPlan::HALF_FLOATS + DualPlan::XT)
-#define VH(hh) (wbase + (hh) * DualPlan::HALF_FLOATS + 2 * DualPlan::XT)
+#define VH(hh) (wbase + (hh) * DualPlan::HALF_FLOATS)
   for (int k = lane; k < DualPlan::WARP_FLOATS; k += 32) wbase[k] = 0.f;
   for (int f = threadIdx.x; f < DualPlan::bfrag_u4<RP>(); f += blockDim.x) {
     const int ll = f & 31, nt = (f >> 5) % NT, kt = (f >> 5) / NT;
@@ -694,7 +742,22 @@ __global__ void __launch_bounds__(DualPlan::WPB * 32, 2)
     const int fnext = fcur + __popc(hmask);
     // ---- gathers: prefix levels into X (folded progressively), the leaf level into Y ----
     const int npre = p.N - 2;
-    for (int lvl = 0; lvl <= npre; ++lvl) {
+    if (tma) {
+      const int pc = lv ? __ldg(p.fiber_coord + (int64_t)myfib * 2 + 1) : 0;
+      const uint32_t rowb = (uint32_t)p.R * 4;
+      const int tot = __shfl_sync(FULL, nb, 0) + __shfl_sync(FULL, nb, 16);
+      fence_proxy_async();  // prior generic reads of X / Y before the async-proxy writes
+      __syncwarp();
+      if (lane == 0) mbar_expect_tx(bar, (uint32_t)tot * rowb * 2);
+      __syncwarp();
+      if (lv) {
+        bulk_copy(Xh + l * XS, p.Cpre[0] + (int64_t)pc * p.R, rowb, bar);
+        bulk_copy(Yh + l * XS, p.Cleaf + (int64_t)lc * p.R, rowb, bar);
+      }
+      mbar_wait(bar, phase);
+      phase ^= 1;
+    }
+    for (int lvl = 0; lvl <= npre && !tma; ++lvl) {
       const bool leaf = lvl == npre;
       const int coord =
           leaf ? lc : (lv ? __ldg(p.fiber_coord + (int64_t)myfib * (p.N - 1) + 1 + lvl) : 0);
@@ -708,24 +771,24 @@ __global__ void __launch_bounds__(DualPlan::WPB * 32, 2)
           const int c = l + 16 * it;
           const int k = c / P4, q = c % P4;
           const int ck = __shfl_sync(FULL, coord, 16 * h + k);
-          if (k < nb && q < R4) cp_async16(dst + swz(k, 4 * q), C + (int64_t)ck * p.R + 4 * q);
+          if (k < nb && q < R4) cp_async16(dst + k * XS + 4 * q, C + (int64_t)ck * p.R + 4 * q);
         }
       } else {
         for (int k = 0; k < HB; ++k) {
           const int ck = __shfl_sync(FULL, coord, 16 * h + k);
           for (int r = l; r < p.R; r += 16)
-            if (k < nb) cp_async4(dst + swz(k, r), C + (int64_t)ck * p.R + r);
+            if (k < nb) cp_async4(dst + k * XS + r, C + (int64_t)ck * p.R + r);
         }
       }
       if (lvl >= 1 && !leaf) {
         cp_async_wait_all();
         __syncwarp();
         for (int k = 0; k < nb; ++k)
-          for (int r = l; r < RP; r += 16) Xh[swz(k, r)] *= Yh[swz(k, r)];
+          for (int r = l; r < RP; r += 16) Xh[k * XS + r] *= Yh[k * XS + r];
         __syncwarp();
       }
     }
-    cp_async_wait_all();
+    if (!tma) cp_async_wait_all();
     __syncwarp();
     // ---- V_h = (X_h * Y_h) * Bt_u: one m16 tile per half, 3xTF32 ----
     float acc[2][NT][4];
@@ -741,8 +804,7 @@ __global__ void __launch_bounds__(DualPlan::WPB * 32, 2)
 #pragma unroll
       for (int kt = 0; kt < KT; ++kt) {
         const int c0 = 8 * kt + tq;
-        const int o0 = swz(gq, c0), o1 = swz(gq + 8, c0), o2 = swz(gq, c0 + 4),
-                  o3 = swz(gq + 8, c0 + 4);
+        const int o0 = gq * XS + c0, o1 = (gq + 8) * XS + c0, o2 = o0 + 4, o3 = o1 + 4;
         const float x0 = Xs[o0] * Ys[o0], x1 = Xs[o1] * Ys[o1], x2 = Xs[o2] * Ys[o2],
                     x3 = Xs[o3] * Ys[o3];
         const uint32_t h0 = to_tf32(x0), h1 = to_tf32(x1), h2 = to_tf32(x2), h3 = to_tf32(x3);
@@ -759,6 +821,7 @@ __global__ void __launch_bounds__(DualPlan::WPB * 32, 2)
         }
       }
     }
+    __syncwarp();  // every lane's A fragments are read before V overwrites X
 #pragma unroll
     for (int hh = 0; hh < 2; ++hh)
 #pragma unroll
@@ -787,6 +850,11 @@ __global__ void __launch_bounds__(DualPlan::WPB * 32, 2)
       }
     }
     __syncwarp();
+    if (p.R < RP) {  // V overwrote X's zero columns r in [R, RP): restore them
+      for (int k = 0; k < HB; ++k)
+        for (int r = p.R + l; r < RP; r += 16) Xh[k * XS + r] = 0.f;
+      __syncwarp();
+    }
     L0 += nb;
     fcur = fnext;
   }
@@ -794,6 +862,187 @@ __global__ void __launch_bounds__(DualPlan::WPB * 32, 2)
 #undef XH
 #undef YH
 #undef VH
+
+
+// ---- K3b, two rows per warp with register-direct fragments (the default for many rows) ------
+// As the dual kernel, but the rank products never touch shared memory: lane (g, t) loads exactly
+// the A-fragment elements of the m16n8k8 MMA it issues -- C_prefix[pc][r] * C_leaf[lc][r] for
+// leaves g and g+8 and r = 8kt + t (+4) -- straight from L1/L2 (the C rows are L2-resident;
+// the 4 lanes and 4 k-tiles reading one row share its L1 line), with 64 independent loads in
+// flight per lane.  Shared memory holds only the V tiles (the transpose to lanes-over-j).
+struct RDualPlan {
+  static constexpr int VT = HB * VS;              // 16 x 36 V tile per half
+  static constexpr int WARP_FLOATS = 2 * VT + 16;  // +16: the halves' V reads hit disjoint banks
+  static constexpr int WPB = 8;
+  template <int RP>
+  static constexpr int bfrag_u4() { return (RP / 8 > 0 ? RP / 8 : 1) * 4 * 32; }
+  template <int RP>
+  static constexpr size_t bytes() {
+    return (size_t)bfrag_u4<RP>() * 16 + (size_t)WPB * WARP_FLOATS * sizeof(float);
+  }
+};
+
+template <int RP>
+__global__ void __launch_bounds__(RDualPlan::WPB * 32, 2)
+    factor_rows_rdual_kernel(const SweepParams p) {
+  constexpr int KT = RP / 8 > 0 ? RP / 8 : 1, NT = 4;
+  extern __shared__ float4 smem4[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int h = lane >> 4, l = lane & 15;
+  const int gq = lane >> 2, tq = lane & 3;
+  uint4 *bfrag = reinterpret_cast<uint4 *>(smem4);
+  float *wbase = reinterpret_cast<float *>(bfrag + RDualPlan::bfrag_u4<RP>()) + w * RDualPlan::WARP_FLOATS;
+#define VHR(hh) (wbase + (hh) * (RDualPlan::VT + 16))
+  for (int f = threadIdx.x; f < RDualPlan::bfrag_u4<RP>(); f += blockDim.x) {
+    const int ll = f & 31, nt = (f >> 5) % NT, kt = (f >> 5) / NT;
+    const int g = ll >> 2, t = ll & 3, j = 8 * nt + g;
+    uint32_t hv[2], lv2[2];
+    for (int hh = 0; hh < 2; ++hh) {
+      const int r = 8 * kt + t + 4 * hh;
+      const float bv = (r < p.R && j < p.J) ? __ldg(p.Bt + r * p.J + j) : 0.f;
+      hv[hh] = to_tf32(bv);
+      lv2[hh] = to_tf32(bv - __uint_as_float(hv[hh]));
+    }
+    bfrag[f] = make_uint4(hv[0], hv[1], lv2[0], lv2[1]);
+  }
+  __syncthreads();
+  const int64_t nstream = (int64_t)gridDim.x * RDualPlan::WPB * 2;
+  const int64_t mystream = ((int64_t)blockIdx.x * RDualPlan::WPB + w) * 2 + h;
+  const bool j0 = l < p.J, j1 = l + 16 < p.J;
+  const int R = p.R, npre = p.N - 2;
+  float *Vh = VHR(h);
+
+  int64_t row = mystream - nstream;
+  int fe = 0, Le = 0, L0 = 0, fcur = 0;
+  float *arow = nullptr;
+  float a0 = 0.f, a1 = 0.f;
+  bool active = true;
+  for (;;) {
+    if (active && L0 >= Le) {
+      if (arow) {
+        if (j0) arow[l] = a0;
+        if (j1) arow[l + 16] = a1;
+        arow = nullptr;
+      }
+      row += nstream;
+      if (row < p.nrows) {
+        const int i = __ldg(p.row_coord + row);
+        const int fb = __ldg(p.row_fiber_ptr + row);
+        fe = __ldg(p.row_fiber_ptr + row + 1);
+        L0 = __ldg(p.fiber_ptr + fb);
+        Le = __ldg(p.fiber_ptr + fe);
+        fcur = fb;
+        arow = p.A + (int64_t)i * p.J;
+        a0 = j0 ? arow[l] : 0.f;
+        a1 = j1 ? arow[l + 16] : 0.f;
+      } else {
+        active = false;
+      }
+    }
+    if (!__any_sync(FULL, active)) break;
+    const int nb = active ? min(HB, Le - L0) : 0;
+    const bool lv = l < nb;
+    const int lc = lv ? __ldcs(p.leaf_coord + L0 + l) : 0;
+    const float x = lv ? __ldcs(p.vals + L0 + l) : 0.f;
+    const int fidx = fcur + 1 + l;
+    const int fs = (active && fidx < fe) ? __ldg(p.fiber_ptr + fidx) : INT32_MAX;
+    const unsigned bit = (fs < L0 + nb) ? (1u << (fs - L0)) : 0u;
+    const unsigned hmask = (__reduce_or_sync(FULL, bit << (16 * h)) >> (16 * h)) & 0xffffu;
+    const int myfib = fcur + __popc(hmask & (0xffffu >> (15 - l)));
+    const int fnext = fcur + __popc(hmask);
+    const int64_t fcbase = (int64_t)myfib * (p.N - 1) + 1;
+    // ---- V_h = cross_h * Bt_u, A fragments loaded from L1/L2 into registers ----
+    float acc[2][NT][4];
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[hh][nt][q] = 0.f;
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      // rows gq and gq+8 of half hh's tile = leaves 16hh+gq, 16hh+gq+8
+      const int s0 = 16 * hh + gq, s1 = s0 + 8;
+      const int nbh = __shfl_sync(FULL, nb, 16 * hh);
+      const bool v0 = gq < nbh, v1 = gq + 8 < nbh;
+      const float *lr0 = p.Cleaf + (int64_t)__shfl_sync(FULL, lc, s0) * R;
+      const float *lr1 = p.Cleaf + (int64_t)__shfl_sync(FULL, lc, s1) * R;
+      float x0[KT][2], x1[KT][2];  // [kt][col t / t+4] for rows gq / gq+8
+#pragma unroll
+      for (int kt = 0; kt < KT; ++kt)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int col = 8 * kt + tq + 4 * c;
+          const bool ok = col < R;
+          x0[kt][c] = (ok && v0) ? __ldg(lr0 + col) : 0.f;
+          x1[kt][c] = (ok && v1) ? __ldg(lr1 + col) : 0.f;
+        }
+      for (int lvl = 0; lvl < npre; ++lvl) {
+        const int f0 = __shfl_sync(FULL, lv ? __ldg(p.fiber_coord + fcbase + lvl) : 0, s0);
+        const int f1 = __shfl_sync(FULL, lv ? __ldg(p.fiber_coord + fcbase + lvl) : 0, s1);
+        const float *pr0 = p.Cpre[lvl] + (int64_t)f0 * R;
+        const float *pr1 = p.Cpre[lvl] + (int64_t)f1 * R;
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const int col = 8 * kt + tq + 4 * c;
+            const bool ok = col < R;
+            // prefix levels multiply in front: ((P1 * P2) ...) * leaf is the reference's
+            // left-to-right order only for N = 3; fp32 association differences are ~1 ulp
+            x0[kt][c] = (ok && v0) ? __ldg(pr0 + col) * x0[kt][c] : 0.f;
+            x1[kt][c] = (ok && v1) ? __ldg(pr1 + col) * x1[kt][c] : 0.f;
+          }
+      }
+#pragma unroll
+      for (int kt = 0; kt < KT; ++kt) {
+        const uint32_t h0 = to_tf32(x0[kt][0]), h1 = to_tf32(x1[kt][0]);
+        const uint32_t h2 = to_tf32(x0[kt][1]), h3 = to_tf32(x1[kt][1]);
+        const uint32_t l0 = to_tf32(x0[kt][0] - __uint_as_float(h0));
+        const uint32_t l1 = to_tf32(x1[kt][0] - __uint_as_float(h1));
+        const uint32_t l2 = to_tf32(x0[kt][1] - __uint_as_float(h2));
+        const uint32_t l3 = to_tf32(x1[kt][1] - __uint_as_float(h3));
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const uint4 bb = bfrag[(kt * NT + nt) * 32 + lane];
+          mma_tf32(acc[hh][nt], l0, l1, l2, l3, bb.x, bb.y);
+          mma_tf32(acc[hh][nt], h0, h1, h2, h3, bb.z, bb.w);
+          mma_tf32(acc[hh][nt], h0, h1, h2, h3, bb.x, bb.y);
+        }
+      }
+    }
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int c0 = 8 * nt + 2 * tq;
+        *reinterpret_cast<float2 *>(VHR(hh) + gq * VS + c0) = make_float2(acc[hh][nt][0], acc[hh][nt][1]);
+        *reinterpret_cast<float2 *>(VHR(hh) + (gq + 8) * VS + c0) =
+            make_float2(acc[hh][nt][2], acc[hh][nt][3]);
+      }
+    __syncwarp();
+    const int nbmax = max(__shfl_sync(FULL, nb, 0), __shfl_sync(FULL, nb, 16));
+#pragma unroll 4
+    for (int k = 0; k < nbmax; ++k) {
+      const float v0 = Vh[k * VS + l], v1 = Vh[k * VS + l + 16];
+      float s = a0 * v0 + a1 * v1;
+      s += __shfl_xor_sync(FULL, s, 8);
+      s += __shfl_xor_sync(FULL, s, 4);
+      s += __shfl_xor_sync(FULL, s, 2);
+      s += __shfl_xor_sync(FULL, s, 1);
+      const float e = __shfl_sync(FULL, x, 16 * h + (k & 15)) - s;
+      if (k < nb) {
+        const float g0 = p.reg * a0 - e * v0, g1 = p.reg * a1 - e * v1;
+        a0 = a0 - p.lr * g0;
+        a1 = a1 - p.lr * g1;
+      }
+    }
+    __syncwarp();
+    L0 += nb;
+    fcur = fnext;
+  }
+#undef VHR
+}
 
 // ---- K3b, Gram form of the serial chain (tensor cores for both GEMMs) -------------------
 // Within a batch the row evolves as a_{m+1} = a_m + lr (e_m v_m - reg a_m).
@@ -1243,13 +1492,32 @@ int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
     if (e && strcmp(e, "mma") == 0) return 1;
     if (e && strcmp(e, "pipe") == 0) return 3;
     if (e && strcmp(e, "dual") == 0) return 4;
+    if (e && strcmp(e, "rdual") == 0) return 6;
     return 5;  // auto: dual when the rows fill the SMs, gram otherwise
   }();
   int variant = chosen;
+  static const int use_tma = [] {
+    const char *e = getenv("FT_GATHER");
+    return e && strcmp(e, "tma") == 0 ? 1 : 0;
+  }();
+  SweepParams q = p;
+  q.tma = use_tma;
   // auto: dual needs >= 2 rows per resident warp slot to fill the SMs; few long rows (e.g.
   // Netflix mode 2: 2,182 rows of ~45 K leaves) are bound by the serial chain, which the Gram
   // form shortens (measured 8.9 vs 10.0 ms pipe / 13.4 ms dual on that mode)
   if (variant == 5) variant = p.nrows < (int64_t)2 * sm_count() * 16 ? 0 : 4;
+  if (variant == 6) {
+    const size_t sm = RDualPlan::bytes<RP>();
+    static bool set6 = false;
+    if (!set6) {
+      cudaFuncSetAttribute(factor_rows_rdual_kernel<RP>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      set6 = true;
+    }
+    const int g = grid_for(factor_rows_rdual_kernel<RP>, (p.nrows + 1) / 2, RDualPlan::WPB, sm);
+    factor_rows_rdual_kernel<RP><<<g, RDualPlan::WPB * 32, sm, s>>>(p);
+    return check_launch("ft_factor_sweep_rows(rdual)");
+  }
   if (variant == 4) {
     const size_t sm = DualPlan::bytes<RP>();
     static bool set4 = false;
@@ -1259,7 +1527,7 @@ int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
       set4 = true;
     }
     const int g = grid_for(factor_rows_dual_kernel<RP>, (p.nrows + 1) / 2, DualPlan::WPB, sm);
-    factor_rows_dual_kernel<RP><<<g, DualPlan::WPB * 32, sm, s>>>(p);
+    factor_rows_dual_kernel<RP><<<g, DualPlan::WPB * 32, sm, s>>>(q);
     return check_launch("ft_factor_sweep_rows(dual)");
   }
   if (variant == 3) {

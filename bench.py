@@ -36,6 +36,17 @@ CONFIGS = {
                     J=32, R=32, value_range=(0.025, 5.0)),
     "config1": dict(dims=(1000, 1000, 1000), nnz_train=90_000, nnz_test=10_000, J=8, R=8,
                     value_range=(1.0, 5.0)),
+    # BASELINE.json configs[3]: high order, 10 K per mode, 200 M entries, J = R = 16
+    "order6": dict(dims=(10_000,) * 6, nnz_train=198_000_000, nnz_test=2_000_000, J=16, R=16,
+                   value_range=(1.0, 5.0)),
+    "order10": dict(dims=(10_000,) * 10, nnz_train=198_000_000, nnz_test=2_000_000, J=16, R=16,
+                    value_range=(1.0, 5.0)),
+    # BASELINE.json configs[4] shape (order 4, 10 K per mode, J = R = 32) at the size one GPU
+    # holds with the full forest; the 1 B-entry sweep runs sharded (dist.py) over 2-8 GPUs
+    "order4": dict(dims=(10_000,) * 4, nnz_train=495_000_000, nnz_test=5_000_000, J=32, R=32,
+                   value_range=(1.0, 5.0)),
+    "order4_1b": dict(dims=(10_000,) * 4, nnz_train=990_000_000, nnz_test=10_000_000, J=32,
+                      R=32, value_range=(1.0, 5.0)),
 }
 
 CPU_SAMPLE_NNZ = 1_000_000
@@ -133,11 +144,16 @@ def host_sample(dims, nnz, value_range, seed=0):
     """nnz distinct uniform cells of `dims` with U[lo,hi] values (host numpy)."""
     rng = np.random.default_rng([seed, 99])
     cap = math.prod(dims)
-    lin = np.unique(rng.integers(0, cap, size=int(nnz * 1.02) + 1000))
-    rng.shuffle(lin)
-    lin = lin[:nnz]
-    idx = np.stack(np.unravel_index(lin, dims), axis=1).astype(np.int64)
-    vals = rng.uniform(value_range[0], value_range[1], size=nnz)
+    if cap < 2**62:
+        lin = np.unique(rng.integers(0, cap, size=int(nnz * 1.02) + 1000))
+        rng.shuffle(lin)
+        lin = lin[:nnz]
+        idx = np.stack(np.unravel_index(lin, dims), axis=1).astype(np.int64)
+    else:  # > 62-bit index space: i.i.d. cells, drop the (improbable) repeats
+        idx = np.stack([rng.integers(0, d, size=nnz) for d in dims], axis=1)
+        _, first = np.unique(idx, axis=0, return_index=True)
+        idx = idx[np.sort(first)]
+    vals = rng.uniform(value_range[0], value_range[1], size=idx.shape[0])
     return idx, vals
 
 
@@ -151,17 +167,18 @@ def cpu_epoch_rate(cfg, nnz, workers, repeats=1):
     if K is None:
         K, kind = O.CKernels, "port"
     idx, vals = host_sample(cfg["dims"], nnz, cfg["value_range"])
+    N = len(cfg["dims"])
     forest = O.build_forest(idx, vals, 128)
-    model = O.default_init_model(cfg["dims"], (cfg["J"],) * 3, cfg["R"], seed=0)
+    model = O.default_init_model(cfg["dims"], (cfg["J"],) * N, cfg["R"], seed=0)
     ocfg = O.OracleConfig(workers=workers)
     cache = O.precompute_cache(model, K=K)
     times = []
     for _ in range(repeats):
         t0 = time.perf_counter()
-        for n in range(3):
+        for n in range(N):
             O.update_factor_mode(model, forest, cache, n, ocfg, K=K)
         t1 = time.perf_counter()
-        for n in range(3):
+        for n in range(N):
             O.update_core_mode(model, forest, cache, n, ocfg, K=K)
         t2 = time.perf_counter()
         times.append((t1 - t0, t2 - t1))
@@ -260,7 +277,7 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     log(f"generated {nnz_total} entries in {time.perf_counter() - t0:.2f}s")
     t0 = time.perf_counter()
-    forest = ft.build_forest(train_t, 128)
+    forest = ft.build_forest(train_t, 128, compact=True)  # the arrays the sweeps read
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
     log(f"forest built in {build_s:.2f}s; fibers {[t.num_fibers for t in forest.trees]}, "
@@ -411,7 +428,7 @@ def run_e2e(ft, T, cfg, train_dev, args):
         a.record()
         dev = ft.DeviceCoo(tuple(dims), idx_h.to("cuda", non_blocking=True),
                            vals_h.to("cuda", non_blocking=True))
-        forest = ft.build_forest(dev, 128)
+        forest = ft.build_forest(dev, 128, compact=True)
         counter = ft.OpCounter()
         cache = ft.precompute_cache(model, counter)
         m = T.run_epoch(model, forest, cache, dev, ft.TrainConfig(epochs=1, schedule=args.schedule),

@@ -159,7 +159,9 @@ FT_API int ft_sse(const ft_model_t *model, int64_t m, const int32_t *idx, const 
 /* K7  Synthetic COO generator (same distribution as coo.generate_synthetic, coo.py:164-213:
  * distinct coordinates uniform without replacement, values U[lo, hi]; NOT the same stream).
  * Writes nnz unique coordinates (row-major int32 [nnz x N]) in a random entry order, and
- * values (so the first k entries are a uniform random test split).  Requires sum_n ceil(log2 I_n) <= 64.  SYNCHRONOUS. */
+ * values (so the first k entries are a uniform random test split).  Index spaces wider than
+ * 64 bits draw i.i.d. cells without a dedup pass (allowed only when nnz^2 / (2 capacity) <
+ * 1e-6; the builder rejects any duplicate).  SYNCHRONOUS. */
 FT_API int ft_generate_coo(int32_t N, const int64_t *dims, int64_t nnz, uint64_t seed, float lo,
                     float hi, int32_t *idx, float *vals, void *stream);
 

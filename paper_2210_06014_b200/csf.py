@@ -43,6 +43,7 @@ class CsfTree:
     row_fiber_ptr: object  # device int32 [rows+1]  (not a reference field)
     row_coord: object      # device int32 [rows]
     _view: object = field(default=None, repr=False)
+    num_subtensors_built: int = -1
 
     @property
     def order(self) -> int:
@@ -58,6 +59,8 @@ class CsfTree:
 
     @property
     def num_subtensors(self) -> int:
+        if self.num_subtensors_built >= 0:
+            return self.num_subtensors_built
         return int(self.sub_fiber_ptr.shape[0]) - 1
 
     @property
@@ -143,9 +146,19 @@ class CsfForest:
     omega: int | None = None   # |Omega| of the whole tensor when trees hold a row-block shard
 
 
+def _trim(buf, n):
+    """First n entries of a capacity buffer: a view when that keeps most of it (no transient
+    copy of a multi-GB array), a compact copy otherwise."""
+    return buf[:n] if n >= 0.75 * buf.numel() else buf[:n].clone()
+
+
 def build_tree(tensor, root_mode: int, fiber_threshold=DEFAULT_FIBER_THRESHOLD,
-               stream=None) -> CsfTree:
-    """GPU B-CSF build (csf.py:101-196).  ``tensor``: SparseCooTensor or DeviceCoo."""
+               stream=None, compact: bool = False) -> CsfTree:
+    """GPU B-CSF build (csf.py:101-196).  ``tensor``: SparseCooTensor or DeviceCoo.
+
+    ``compact=True`` keeps only what the sweep kernels read (leaf coordinates, values,
+    fiber_ptr / fiber_coord, rows): the per-depth ``inds`` / ``ptrs`` and the subtensor arrays
+    -- reference-format fields -- are not built (saves ~40 % of a tree at order 4)."""
     import torch
 
     L = _lib.lib()
@@ -163,21 +176,23 @@ def build_tree(tensor, root_mode: int, fiber_threshold=DEFAULT_FIBER_THRESHOLD,
             raise ConfigError(f"fiber_threshold must be >= 1, got {fiber_threshold}")
     i32 = dict(dtype=torch.int32, device="cuda")
     leaf_vals = torch.empty(nnz, dtype=torch.float32, device="cuda")
-    inds = [torch.empty(nnz, **i32) for _ in range(N)]
-    ptrs = [torch.empty(nnz + 1, **i32) for _ in range(N - 1)]
+    leaf = torch.empty(nnz, **i32)
+    inds = [torch.empty(nnz, **i32) for _ in range(N - 1)] + [leaf] if not compact else [leaf]
+    ptrs = [torch.empty(nnz + 1, **i32) for _ in range(N - 1)] if not compact else []
     fiber_ptr = torch.empty(nnz + 1, **i32)
     fiber_coord = torch.empty(nnz * (N - 1), **i32)
-    sub_fiber_ptr = torch.empty(nnz + 1, **i32)
-    sub_leaf_ptr = torch.empty(nnz + 1, **i32)
+    sub_fiber_ptr = torch.empty(nnz + 1, **i32) if not compact else None
+    sub_leaf_ptr = torch.empty(nnz + 1, **i32) if not compact else None
     row_fiber_ptr = torch.empty(nnz + 1, **i32)
     row_coord = torch.empty(nnz, **i32)
     counts = np.zeros(4 + N, dtype=np.int64)
     dims = (ctypes.c_int64 * N)(*dev.dims)
-    ind_tab = (ctypes.c_void_p * N)(*[a.data_ptr() for a in inds])
-    ptr_tab = (ctypes.c_void_p * max(N - 1, 1))(*[a.data_ptr() for a in ptrs])
+    ind_ptrs = [None] * (N - 1) + [leaf.data_ptr()] if compact else [a.data_ptr() for a in inds]
+    ind_tab = (ctypes.c_void_p * N)(*ind_ptrs)
+    ptr_tab = None if compact else (ctypes.c_void_p * max(N - 1, 1))(*[a.data_ptr() for a in ptrs])
     rc = L.ft_build_tree(N, nnz, dims, dev.idx.data_ptr(), dev.vals.data_ptr(), root_mode, thr,
                          leaf_vals.data_ptr(), ind_tab, ptr_tab, fiber_ptr.data_ptr(),
-                         fiber_coord.data_ptr(), sub_fiber_ptr.data_ptr(), sub_leaf_ptr.data_ptr(),
+                         fiber_coord.data_ptr(), _lib.ptr(sub_fiber_ptr), _lib.ptr(sub_leaf_ptr),
                          row_fiber_ptr.data_ptr(), row_coord.data_ptr(),
                          counts.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                          _lib.stream_handle(stream))
@@ -190,24 +205,35 @@ def build_tree(tensor, root_mode: int, fiber_threshold=DEFAULT_FIBER_THRESHOLD,
     _lib.check(rc, "ft_build_tree")
     F, S, rows = int(counts[0]), int(counts[1]), int(counts[2])
     nodes = [int(c) for c in counts[4:4 + N]]
-    # trim capacity buffers to their real sizes (copies, so the big buffers are released)
-    return CsfTree(
+    empty = torch.empty(0, **i32)
+    if compact:
+        inds_t = tuple(empty for _ in range(N - 1)) + (leaf,)
+        ptrs_t = tuple(empty for _ in range(N - 1))
+        sfp = slp = torch.zeros(1, **i32)
+    else:
+        inds_t = tuple(_trim(inds[d], nodes[d]) for d in range(N))
+        ptrs_t = tuple(_trim(ptrs[d], nodes[d] + 1) for d in range(N - 1))
+        sfp, slp = _trim(sub_fiber_ptr, S + 1), _trim(sub_leaf_ptr, S + 1)
+    tree = CsfTree(
         root_mode=root_mode,
         level_modes=tuple((root_mode + d) % N for d in range(N)),
         dims=tuple(dev.dims),
-        inds=tuple(inds[d][: nodes[d]].clone() if nodes[d] < nnz else inds[d] for d in range(N)),
-        ptrs=tuple(ptrs[d][: nodes[d] + 1].clone() for d in range(N - 1)),
+        inds=inds_t,
+        ptrs=ptrs_t,
         vals=leaf_vals,
-        fiber_ptr=fiber_ptr[: F + 1].clone(),
-        fiber_coord=fiber_coord[: F * (N - 1)].view(F, N - 1).clone(),
-        sub_fiber_ptr=sub_fiber_ptr[: S + 1].clone(),
-        sub_leaf_ptr=sub_leaf_ptr[: S + 1].clone(),
-        row_fiber_ptr=row_fiber_ptr[: rows + 1].clone(),
-        row_coord=row_coord[:rows].clone(),
+        fiber_ptr=_trim(fiber_ptr, F + 1),
+        fiber_coord=_trim(fiber_coord, F * (N - 1)).view(F, N - 1),
+        sub_fiber_ptr=sfp,
+        sub_leaf_ptr=slp,
+        row_fiber_ptr=_trim(row_fiber_ptr, rows + 1),
+        row_coord=_trim(row_coord, rows),
     )
+    tree.num_subtensors_built = S
+    return tree
 
 
-def build_forest(tensor, fiber_threshold=DEFAULT_FIBER_THRESHOLD, stream=None) -> CsfForest:
+def build_forest(tensor, fiber_threshold=DEFAULT_FIBER_THRESHOLD, stream=None,
+                 compact: bool = False) -> CsfForest:
     dev = as_device(tensor)
-    trees = tuple(build_tree(dev, t, fiber_threshold, stream) for t in range(dev.order))
+    trees = tuple(build_tree(dev, t, fiber_threshold, stream, compact) for t in range(dev.order))
     return CsfForest(trees=trees, fiber_threshold=fiber_threshold)

@@ -70,26 +70,35 @@ struct GatherArgs {
   int32_t *K[FT_MAX_ORDER];
 };
 
-// K_d[p] = idx[perm[p], lm[d]]; vals; fdl[p] = first level where entry p differs from p-1.
+// K_d[p] = idx[perm[p], lm[d]] and vals (one random read of each entry's row, coalesced writes)
 __global__ void gather_levels(const int32_t *__restrict__ idx, const float *__restrict__ vals,
                               const int32_t *__restrict__ perm, int64_t nnz, GatherArgs a,
-                              float *__restrict__ vout, uint8_t *__restrict__ fdl,
-                              unsigned long long *__restrict__ dup_min) {
+                              float *__restrict__ vout) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= nnz) return;
-  int64_t e = perm[p];
-  int64_t q = p > 0 ? perm[p - 1] : 0;
+  const int64_t e = perm[p];
   const int32_t *row = idx + e * a.N;
-  const int32_t *prev = idx + q * a.N;
-  int first = p == 0 ? 0 : a.N;
-  for (int d = 0; d < a.N; ++d) {
-    int32_t c = row[a.lm[d]];
-    a.K[d][p] = c;
-    if (p > 0 && first == a.N && c != prev[a.lm[d]]) first = d;
-  }
+  for (int d = 0; d < a.N; ++d) a.K[d][p] = row[a.lm[d]];
   vout[p] = vals[e];
+}
+
+// fdl[p] = first level where sorted entry p differs from p-1 (coalesced reads of the K_d);
+// N means an exact duplicate of its predecessor -> the smallest such original entry index
+__global__ void first_diff_level(const int32_t *__restrict__ perm, int64_t nnz, GatherArgs a,
+                                 uint8_t *__restrict__ fdl, unsigned long long *__restrict__ dup_min) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= nnz) return;
+  int first = 0;
+  if (p > 0) {
+    first = a.N;
+    for (int d = 0; d < a.N; ++d)
+      if (a.K[d][p] != a.K[d][p - 1]) {
+        first = d;
+        break;
+      }
+  }
   fdl[p] = (uint8_t)first;
-  if (first == a.N) atomicMin(dup_min, (unsigned long long)e);
+  if (first == a.N) atomicMin(dup_min, (unsigned long long)perm[p]);
 }
 
 __global__ void flags_le(const uint8_t *__restrict__ fdl, const uint8_t *__restrict__ extra,
@@ -183,8 +192,13 @@ extern "C" int ft_build_tree(int32_t N, int64_t nnz, const int64_t *dims, const 
   if (nnz <= 0) return fail(FT_ERR_EMPTY, "cannot index an empty tensor");
   if (nnz >= (int64_t)INT32_MAX) return fail(FT_ERR_UNSUPPORTED, "nnz %lld >= 2^31", (long long)nnz);
   if (root_mode < 0 || root_mode >= N) return fail(FT_ERR_ARG, "root_mode out of range");
-  if (!dims || !idx || !vals || !leaf_vals || !inds || !ptrs || !fiber_ptr || !fiber_coord ||
-      !sub_fiber_ptr || !sub_leaf_ptr || !row_fiber_ptr || !row_coord || !counts_out)
+  // compact build (ptrs == NULL): only what the sweep kernels read -- leaf coordinates, values,
+  // fiber_ptr / fiber_coord and the rows; the per-depth inds[d < N-1] / ptrs and the subtensor
+  // arrays (reference-format fields) are neither computed nor stored
+  const bool compact = ptrs == nullptr;
+  if (!dims || !idx || !vals || !leaf_vals || !inds || !inds[N - 1] || !fiber_ptr ||
+      !fiber_coord || !row_fiber_ptr || !row_coord || !counts_out ||
+      (!compact && (!sub_fiber_ptr || !sub_leaf_ptr)))
     return fail(FT_ERR_ARG, "ft_build_tree: null argument");
   keep_pool();
   cudaStream_t s = as_stream(stream);
@@ -264,7 +278,8 @@ extern "C" int ft_build_tree(int32_t N, int64_t nnz, const int64_t *dims, const 
   uint8_t *fdl = sc.get<uint8_t>(nnz);
   unsigned long long *dup = sc.get<unsigned long long>(1);
   FT_CUDA(cudaMemsetAsync(dup, 0xff, sizeof(unsigned long long), s));
-  gather_levels<<<nb, 256, 0, s>>>(idx, vals, perm, nnz, ga, leaf_vals, fdl, dup);
+  gather_levels<<<nb, 256, 0, s>>>(idx, vals, perm, nnz, ga, leaf_vals);
+  first_diff_level<<<nb, 256, 0, s>>>(perm, nnz, ga, fdl, dup);
   if (int rc = check_launch("gather_levels")) return rc;
   unsigned long long hdup = 0;
   FT_CUDA(cudaMemcpyAsync(&hdup, dup, sizeof(hdup), cudaMemcpyDeviceToHost, s));
@@ -319,12 +334,14 @@ extern "C" int ft_build_tree(int32_t N, int64_t nnz, const int64_t *dims, const 
   FT_CUDA(cudaMemcpyAsync(&hlast[1], nch + nruns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   FT_CUDA(cudaStreamSynchronize(s));
   const int64_t S = (int64_t)hlast[0] + hlast[1];
-  FT_CUDA(cudaMemsetAsync(subflag, 0, nnz, s));
-  write_chunks<<<blocks_for(nruns), 256, 0, s>>>(row_fiber_ptr, nch, off, nruns, thr, fiber_ptr,
-                                                 sub_fiber_ptr, sub_leaf_ptr, subflag);
-  if (int rc = check_launch("write_chunks")) return rc;
-  set_i32<<<1, 1, 0, s>>>(sub_fiber_ptr + S, (int32_t)F);
-  set_i32<<<1, 1, 0, s>>>(sub_leaf_ptr + S, (int32_t)nnz);
+  if (!compact) {
+    FT_CUDA(cudaMemsetAsync(subflag, 0, nnz, s));
+    write_chunks<<<blocks_for(nruns), 256, 0, s>>>(row_fiber_ptr, nch, off, nruns, thr, fiber_ptr,
+                                                   sub_fiber_ptr, sub_leaf_ptr, subflag);
+    if (int rc = check_launch("write_chunks")) return rc;
+    set_i32<<<1, 1, 0, s>>>(sub_fiber_ptr + S, (int32_t)F);
+    set_i32<<<1, 1, 0, s>>>(sub_leaf_ptr + S, (int32_t)nnz);
+  }
 
   // fiber_coord[f, d] = K_d[fiber_ptr[f]]
   for (int d = 0; d < N - 1; ++d)
@@ -338,7 +355,7 @@ extern "C" int ft_build_tree(int32_t N, int64_t nnz, const int64_t *dims, const 
   FT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, flagA, scan, nnz, s));
   void *scan_tmp = sc.get<uint8_t>(scan_bytes);
   uint8_t *fl[2] = {flagA, flagB};
-  for (int d = N - 2; d >= 0; --d) {
+  for (int d = N - 2; d >= 0 && !compact; --d) {
     uint8_t *flag_d = fl[d & 1];
     flags_le<<<nb, 256, 0, s>>>(fdl, subflag, nnz, d, flag_d);
     int64_t n_d = 0;

@@ -105,11 +105,10 @@ class CudaEngine:
         sub = DeviceCoo(coo.dims, coo.idx[mask].contiguous(), coo.vals[mask].contiguous())
         if sub.nnz == 0:
             return None, 0, 0
-        tree = build_tree(sub, u, thr)
-        t = (u + 1) % coo.order
-        # fibers of the tree rooted at t over the same entries (for the op counts)
-        ft = build_tree(sub, t, thr).num_fibers
-        return tree, sub.nnz, ft
+        # compact: only the arrays the row-owner kernels read (1 B entries must fit 180 GB / P)
+        tree = build_tree(sub, u, thr, compact=True)
+        del sub
+        return tree, tree.nnz, -1
 
     # -- compute ----------------------------------------------------------------------------
     def factor_sweep(self, shard, model, dots, lr, reg):

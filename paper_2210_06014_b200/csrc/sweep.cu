@@ -645,25 +645,25 @@ struct DualPlan {
   static constexpr int WARP_FLOATS = 2 * HALF_FLOATS;
   static constexpr int WPB = 8;
   static constexpr int BAR_BYTES = WPB * 8 + 64;  // one mbarrier per warp, padded to 16 B
-  template <int RP>
-  static constexpr int bfrag_u4() { return (RP / 8 > 0 ? RP / 8 : 1) * 4 * 32; }
-  template <int RP>
+  template <int RP, int JP>
+  static constexpr int bfrag_u4() { return (RP / 8 > 0 ? RP / 8 : 1) * (JP / 8) * 32; }
+  template <int RP, int JP>
   static constexpr size_t bytes() {
-    return (size_t)bfrag_u4<RP>() * 16 + BAR_BYTES + (size_t)WPB * WARP_FLOATS * sizeof(float);
+    return (size_t)bfrag_u4<RP, JP>() * 16 + BAR_BYTES + (size_t)WPB * WARP_FLOATS * sizeof(float);
   }
 };
 
-template <int RP>
+template <int RP, int JP>
 __global__ void __launch_bounds__(DualPlan::WPB * 32, 2)
     factor_rows_dual_kernel(const SweepParams p) {
-  constexpr int KT = RP / 8 > 0 ? RP / 8 : 1, NT = 4;
+  constexpr int KT = RP / 8 > 0 ? RP / 8 : 1, NT = JP / 8;  // JP = padded J (16 or 32)
   extern __shared__ float4 smem4[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int h = lane >> 4, l = lane & 15;
   const int gq = lane >> 2, tq = lane & 3;
   uint4 *bfrag = reinterpret_cast<uint4 *>(smem4);
-  uint64_t *bar = reinterpret_cast<uint64_t *>(bfrag + DualPlan::bfrag_u4<RP>()) + w;
-  float *wbase = reinterpret_cast<float *>(reinterpret_cast<char *>(bfrag + DualPlan::bfrag_u4<RP>()) +
+  uint64_t *bar = reinterpret_cast<uint64_t *>(bfrag + DualPlan::bfrag_u4<RP, JP>()) + w;
+  float *wbase = reinterpret_cast<float *>(reinterpret_cast<char *>(bfrag + DualPlan::bfrag_u4<RP, JP>()) +
                                            DualPlan::BAR_BYTES) +
                  w * DualPlan::WARP_FLOATS;
   constexpr int XS = DualPlan::XS;
@@ -680,7 +680,7 @@ __global__ void __launch_bounds__(DualPlan::WPB * 32, 2)
 #define YH(hh) (wbase + (hh) * DualPlan::HALF_FLOATS + DualPlan::XT)
 #define VH(hh) (wbase + (hh) * DualPlan::HALF_FLOATS)
   for (int k = lane; k < DualPlan::WARP_FLOATS; k += 32) wbase[k] = 0.f;
-  for (int f = threadIdx.x; f < DualPlan::bfrag_u4<RP>(); f += blockDim.x) {
+  for (int f = threadIdx.x; f < DualPlan::bfrag_u4<RP, JP>(); f += blockDim.x) {
     const int ll = f & 31, nt = (f >> 5) % NT, kt = (f >> 5) / NT;
     const int g = ll >> 2, t = ll & 3, j = 8 * nt + g;
     uint32_t hv[2], lv[2];
@@ -695,7 +695,7 @@ __global__ void __launch_bounds__(DualPlan::WPB * 32, 2)
   __syncthreads();
   const int64_t nstream = (int64_t)gridDim.x * DualPlan::WPB * 2;  // row streams
   const int64_t mystream = ((int64_t)blockIdx.x * DualPlan::WPB + w) * 2 + h;
-  const bool j0 = l < p.J, j1 = l + 16 < p.J;
+  const bool j0 = l < p.J, j1 = JP > 16 && l + 16 < p.J;
   float *Xh = XH(h), *Yh = YH(h), *Vh = VH(h);
 
   // per-half row state (replicated in the half's 16 lanes)
@@ -836,7 +836,7 @@ __global__ void __launch_bounds__(DualPlan::WPB * 32, 2)
     const int nbmax = max(__shfl_sync(FULL, nb, 0), __shfl_sync(FULL, nb, 16));
 #pragma unroll 4
     for (int k = 0; k < nbmax; ++k) {
-      const float v0 = Vh[k * VS + l], v1 = Vh[k * VS + l + 16];
+      const float v0 = Vh[k * VS + l], v1 = JP > 16 ? Vh[k * VS + l + 16] : 0.f;
       float s = a0 * v0 + a1 * v1;
       s += __shfl_xor_sync(FULL, s, 8);
       s += __shfl_xor_sync(FULL, s, 4);
@@ -1059,11 +1059,11 @@ struct GramPlan {
   static constexpr int TILE = BATCH * 32;  // swizzled X / Y tiles (G reuses both)
   static constexpr int WARP_FLOATS = 2 * TILE + BATCH * VS;
   static constexpr int WPB = 8;
-  template <int RP>
-  static constexpr int bfrag_u4() { return (RP / 8 > 0 ? RP / 8 : 1) * 4 * 32; }
-  template <int RP>
+  template <int RP, int JP>
+  static constexpr int bfrag_u4() { return (RP / 8 > 0 ? RP / 8 : 1) * (JP / 8) * 32; }
+  template <int RP, int JP>
   static constexpr size_t bytes() {
-    return (size_t)bfrag_u4<RP>() * 16 + (size_t)WPB * WARP_FLOATS * sizeof(float);
+    return (size_t)bfrag_u4<RP, JP>() * 16 + (size_t)WPB * WARP_FLOATS * sizeof(float);
   }
 };
 static_assert(BATCH * GS + BATCH <= 2 * BATCH * 32, "G and a_0 must fit in the X/Y tiles");
@@ -1073,20 +1073,20 @@ __device__ __forceinline__ void split3(float v, uint32_t &hi, uint32_t &lo) {
   lo = to_tf32(v - __uint_as_float(hi));
 }
 
-template <int RP>
+template <int RP, int JP>
 __global__ void __launch_bounds__(GramPlan::WPB * 32, 2)
     factor_rows_gram_kernel(const SweepParams p) {
-  constexpr int KT = RP / 8 > 0 ? RP / 8 : 1, NT = 4;
+  constexpr int KT = RP / 8 > 0 ? RP / 8 : 1, NT = JP / 8;  // JP = padded J (16 or 32)
   extern __shared__ float4 smem4[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int gq = lane >> 2, tq = lane & 3;
   uint4 *bfrag = reinterpret_cast<uint4 *>(smem4);
-  float *X = reinterpret_cast<float *>(bfrag + GramPlan::bfrag_u4<RP>()) + w * GramPlan::WARP_FLOATS;
+  float *X = reinterpret_cast<float *>(bfrag + GramPlan::bfrag_u4<RP, JP>()) + w * GramPlan::WARP_FLOATS;
   float *Y = X + GramPlan::TILE;
   float *V = Y + GramPlan::TILE;
   float *G = X;  // after V exists, X / Y are dead
   for (int k = lane; k < GramPlan::WARP_FLOATS; k += 32) X[k] = 0.f;
-  for (int f = threadIdx.x; f < GramPlan::bfrag_u4<RP>(); f += blockDim.x) {
+  for (int f = threadIdx.x; f < GramPlan::bfrag_u4<RP, JP>(); f += blockDim.x) {
     const int l = f & 31, nt = (f >> 5) % NT, kt = (f >> 5) / NT;
     const int g = l >> 2, t = l & 3, j = 8 * nt + g;
     uint32_t hv[2], lv[2];
@@ -1172,7 +1172,7 @@ __global__ void __launch_bounds__(GramPlan::WPB * 32, 2)
 #pragma unroll
           for (int q = 0; q < 4; ++q) gacc[nt][q] = 0.f;
 #pragma unroll
-        for (int kt = 0; kt < 4; ++kt) {
+        for (int kt = 0; kt < NT; ++kt) {  // the Gram contracts over j
           const int r0 = 16 * mt + gq, c0 = 8 * kt + tq;
           const float f0 = V[r0 * VS + c0], f1 = V[(r0 + 8) * VS + c0];
           const float f2 = V[r0 * VS + c0 + 4], f3 = V[(r0 + 8) * VS + c0 + 4];
@@ -1209,7 +1209,7 @@ __global__ void __launch_bounds__(GramPlan::WPB * 32, 2)
         const float4 *vr = reinterpret_cast<const float4 *>(V + lane * VS);
         const float4 *ar = reinterpret_cast<const float4 *>(as);
 #pragma unroll
-        for (int j4 = 0; j4 < 8; ++j4) {
+        for (int j4 = 0; j4 < JP / 4; ++j4) {
           const float4 v4 = vr[j4], a4 = ar[j4];
           dk = __fmaf_rn(v4.x, a4.x, dk);
           dk = __fmaf_rn(v4.y, a4.y, dk);
@@ -1481,6 +1481,34 @@ inline int grid_for(Kern kern, int64_t work_warps, int wpb = WPB, size_t smem = 
   return (int)g;
 }
 
+template <int RP, int JP>
+int launch_dual(const SweepParams &q, cudaStream_t s) {
+  const size_t sm = DualPlan::bytes<RP, JP>();
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(factor_rows_dual_kernel<RP, JP>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    set = true;
+  }
+  const int g = grid_for(factor_rows_dual_kernel<RP, JP>, (q.nrows + 1) / 2, DualPlan::WPB, sm);
+  factor_rows_dual_kernel<RP, JP><<<g, DualPlan::WPB * 32, sm, s>>>(q);
+  return check_launch("ft_factor_sweep_rows(dual)");
+}
+
+template <int RP, int JP>
+int launch_gram(const SweepParams &p, cudaStream_t s) {
+  const size_t sm = GramPlan::bytes<RP, JP>();
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(factor_rows_gram_kernel<RP, JP>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    set = true;
+  }
+  const int g = grid_for(factor_rows_gram_kernel<RP, JP>, p.nrows, GramPlan::WPB, sm);
+  factor_rows_gram_kernel<RP, JP><<<g, GramPlan::WPB * 32, sm, s>>>(p);
+  return check_launch("ft_factor_sweep_rows(gram)");
+}
+
 template <int RP>
 int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
   // FT_FACTOR_KERNEL selects the K3b variant for A/B measurement: auto (default: dual or gram
@@ -1518,18 +1546,7 @@ int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
     factor_rows_rdual_kernel<RP><<<g, RDualPlan::WPB * 32, sm, s>>>(p);
     return check_launch("ft_factor_sweep_rows(rdual)");
   }
-  if (variant == 4) {
-    const size_t sm = DualPlan::bytes<RP>();
-    static bool set4 = false;
-    if (!set4) {
-      cudaFuncSetAttribute(factor_rows_dual_kernel<RP>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      set4 = true;
-    }
-    const int g = grid_for(factor_rows_dual_kernel<RP>, (p.nrows + 1) / 2, DualPlan::WPB, sm);
-    factor_rows_dual_kernel<RP><<<g, DualPlan::WPB * 32, sm, s>>>(q);
-    return check_launch("ft_factor_sweep_rows(dual)");
-  }
+  if (variant == 4) return p.J <= 16 ? launch_dual<RP, 16>(q, s) : launch_dual<RP, 32>(q, s);
   if (variant == 3) {
     const size_t sm = PipePlan::bytes<RP>();
     static bool set3 = false;
@@ -1542,18 +1559,7 @@ int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
     factor_rows_pipe_kernel<RP><<<g, PipePlan::WPB * 32, sm, s>>>(p);
     return check_launch("ft_factor_sweep_rows(pipe)");
   }
-  if (variant == 0) {
-    const size_t sm = GramPlan::bytes<RP>();
-    static bool set = false;
-    if (!set) {
-      cudaFuncSetAttribute(factor_rows_gram_kernel<RP>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      set = true;
-    }
-    const int g = grid_for(factor_rows_gram_kernel<RP>, p.nrows, GramPlan::WPB, sm);
-    factor_rows_gram_kernel<RP><<<g, GramPlan::WPB * 32, sm, s>>>(p);
-    return check_launch("ft_factor_sweep_rows(gram)");
-  }
+  if (variant == 0) return p.J <= 16 ? launch_gram<RP, 16>(p, s) : launch_gram<RP, 32>(p, s);
   if (variant == 2) {
     const size_t sm = factor_smem<RP>();
     const int g = grid_for(factor_rows_ffma_kernel<RP>, p.nrows, WPB_R, sm);

@@ -1259,10 +1259,11 @@ __global__ void __launch_bounds__(WPB_R * 32)
   extern __shared__ float4 smem4[];
   constexpr int RS = Tile<RP>::RS;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  float *X = reinterpret_cast<float *>(smem4) + w * (2 * Tile<RP>::FLOATS + RS);
+  float *X = reinterpret_cast<float *>(smem4) + w * (2 * Tile<RP>::FLOATS + RS + BATCH);
   float *Y = X + Tile<RP>::FLOATS;
   float *cus = Y + Tile<RP>::FLOATS;  // C_u[i, :] of the current row
-  for (int k = lane; k < 2 * Tile<RP>::FLOATS + RS; k += 32) X[k] = 0.f;
+  float *es = cus + RS;               // the batch's residuals e_k
+  for (int k = lane; k < 2 * Tile<RP>::FLOATS + RS + BATCH; k += 32) X[k] = 0.f;
   __syncwarp();
   const int64_t gw = (int64_t)blockIdx.x * WPB_R + w, nw = (int64_t)gridDim.x * WPB_R;
   const bool rl = lane < p.R;
@@ -1283,27 +1284,39 @@ __global__ void __launch_bounds__(WPB_R * 32)
       const float x = lane < nb ? __ldcs(p.vals + L0 + lane) : 0.f;
       int fnext;
       const int myfib = batch_fibers(p.fiber_ptr, fcur, fe, L0, nb, lane, &fnext);
-      stage_cross<RP>(p, X, Y, myfib, lc, nb, lane);
+      // cross = X * Y is folded into both consumers below (no separate product pass)
+      stage_cross<RP>(p, X, Y, myfib, lc, nb, lane, /*fold_leaf=*/false);
       // lane k: s_k = C_u[i] . cross_k  (= A_u[i] . vec_k, since C_u = A_u Bt_u^T is coherent)
       float s = 0.f;
       {
-        const float4 *xr = reinterpret_cast<const float4 *>(X + (lane & 31) * RS);
+        const float4 *xr = reinterpret_cast<const float4 *>(X + lane * RS);
+        const float4 *yr = reinterpret_cast<const float4 *>(Y + lane * RS);
         const float4 *cr = reinterpret_cast<const float4 *>(cus);
 #pragma unroll
         for (int r4 = 0; r4 < RP / 4; ++r4) {
-          const float4 a4 = xr[r4], c4 = cr[r4];
-          s = __fmaf_rn(a4.x, c4.x, s);
-          s = __fmaf_rn(a4.y, c4.y, s);
-          s = __fmaf_rn(a4.z, c4.z, s);
-          s = __fmaf_rn(a4.w, c4.w, s);
+          const float4 a4 = xr[r4], b4 = yr[r4], c4 = cr[r4];
+          s = __fmaf_rn(a4.x * b4.x, c4.x, s);
+          s = __fmaf_rn(a4.y * b4.y, c4.y, s);
+          s = __fmaf_rn(a4.z * b4.z, c4.z, s);
+          s = __fmaf_rn(a4.w * b4.w, c4.w, s);
         }
       }
-      const float e = lane < nb ? x - s : 0.f;
-      // lane r: g_i[r] += sum_k e_k cross_k[r]
-#pragma unroll 4
-      for (int k = 0; k < nb; ++k) {
-        const float ek = __shfl_sync(FULL, e, k);
-        if (lane < RP) g = __fmaf_rn(ek, X[k * RS + lane], g);
+      es[lane] = lane < nb ? x - s : 0.f;
+      __syncwarp();
+      // lane r: g_i[r] += sum_k e_k cross_k[r]  (e_k as float4 broadcasts; e_k = 0 past nb)
+      if (lane < RP) {
+        const float4 *e4p = reinterpret_cast<const float4 *>(es);
+#pragma unroll
+        for (int k4 = 0; k4 < BATCH / 4; ++k4) {
+          if (4 * k4 < nb) {
+            const float4 e4 = e4p[k4];
+            const int b = 4 * k4 * RS + lane;
+            g = __fmaf_rn(e4.x, X[b] * Y[b], g);
+            g = __fmaf_rn(e4.y, X[b + RS] * Y[b + RS], g);
+            g = __fmaf_rn(e4.z, X[b + 2 * RS] * Y[b + 2 * RS], g);
+            g = __fmaf_rn(e4.w, X[b + 3 * RS] * Y[b + 3 * RS], g);
+          }
+        }
       }
       __syncwarp();
       fcur = fnext;
@@ -1319,7 +1332,7 @@ __global__ void __launch_bounds__(WPB_R * 32)
   __syncthreads();
   const int RJ = p.R * p.J;
   float *red = reinterpret_cast<float *>(smem4);
-  const int wstride = 2 * Tile<RP>::FLOATS + RS;
+  const int wstride = 2 * Tile<RP>::FLOATS + RS + BATCH;
   if (rl) {
 #pragma unroll
     for (int j = 0; j < FT_MAX_RANK; ++j)
@@ -1339,7 +1352,7 @@ constexpr size_t factor_smem() {
 }
 template <int RP>
 constexpr size_t core_smem() {
-  return (size_t)WPB_R * (2 * Tile<RP>::FLOATS + Tile<RP>::RS) * sizeof(float);
+  return (size_t)WPB_R * (2 * Tile<RP>::FLOATS + Tile<RP>::RS + BATCH) * sizeof(float);
 }
 
 // ------------------------------------------------------------------------------------------

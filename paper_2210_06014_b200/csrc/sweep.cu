@@ -704,6 +704,11 @@ __global__ void __launch_bounds__(DualPlan::WPB * 32, 2)
   float *arow = nullptr;
   float a0 = 0.f, a1 = 0.f;
   bool active = true;
+  // next batch's index loads, issued one batch ahead within a row (the batch header's dependent
+  // loads -- fiber window -> ballot -> coordinates -> gathers -- were the top stall)
+  bool have_pf = false;
+  int pf_lc = 0, pf_fs = INT32_MAX;
+  float pf_x = 0.f;
   for (;;) {
     // a half whose row is exhausted writes it back and starts its next non-empty row
     if (active && L0 >= Le) {
@@ -726,20 +731,40 @@ __global__ void __launch_bounds__(DualPlan::WPB * 32, 2)
       } else {
         active = false;
       }
+      have_pf = false;
     }
     if (!__any_sync(FULL, active)) break;
     const int nb = active ? min(HB, Le - L0) : 0;  // this half's batch
     // leaf data and the fiber of each leaf (window of <= 16 fiber starts per half)
     const bool lv = l < nb;
-    const int lc = lv ? __ldcs(p.leaf_coord + L0 + l) : 0;
-    const float x = lv ? __ldcs(p.vals + L0 + l) : 0.f;
-    const int fidx = fcur + 1 + l;
-    const int fs = (active && fidx < fe) ? __ldg(p.fiber_ptr + fidx) : INT32_MAX;
+    int lc, fs;
+    float x;
+    if (have_pf) {
+      lc = pf_lc;
+      x = pf_x;
+      fs = pf_fs;
+    } else {
+      lc = lv ? __ldcs(p.leaf_coord + L0 + l) : 0;
+      x = lv ? __ldcs(p.vals + L0 + l) : 0.f;
+      const int fidx = fcur + 1 + l;
+      fs = (active && fidx < fe) ? __ldg(p.fiber_ptr + fidx) : INT32_MAX;
+    }
     const unsigned bit = (fs < L0 + nb) ? (1u << (fs - L0)) : 0u;
     const unsigned hmask = (__reduce_or_sync(FULL, bit << (16 * h)) >> (16 * h)) & 0xffffu;
     // (the OR of both halves' shifted bits, then this half's 16 bits)
     const int myfib = fcur + __popc(hmask & (0xffffu >> (15 - l)));
     const int fnext = fcur + __popc(hmask);
+    {  // prefetch the next batch of this row
+      const int L1 = L0 + nb;
+      have_pf = active && L1 < Le;
+      if (have_pf) {
+        const int nb1 = min(HB, Le - L1);
+        pf_lc = l < nb1 ? __ldcs(p.leaf_coord + L1 + l) : 0;
+        pf_x = l < nb1 ? __ldcs(p.vals + L1 + l) : 0.f;
+        const int fidx = fnext + 1 + l;
+        pf_fs = fidx < fe ? __ldg(p.fiber_ptr + fidx) : INT32_MAX;
+      }
+    }
     // ---- gathers: prefix levels into X (folded progressively), the leaf level into Y ----
     const int npre = p.N - 2;
     if (tma) {
@@ -1112,11 +1137,13 @@ __global__ void __launch_bounds__(GramPlan::WPB * 32, 2)
     float *arow = p.A + (int64_t)i * p.J;
     float a = jl ? arow[lane] : 0.f;
     int fcur = fb;
+    BatchIdx nxt;  // next batch's index loads, one batch ahead (long rows: always)
+    load_batch_idx(p, nxt, Lb, Le, fcur, fe, lane);
     for (int L0 = Lb; L0 < Le; L0 += BATCH) {
-      BatchIdx cur;
-      load_batch_idx(p, cur, L0, Le, fcur, fe, lane);
+      const BatchIdx cur = nxt;
       int fnext;
       const int myfib = batch_fib(cur, lane, &fnext);
+      if (L0 + BATCH < Le) load_batch_idx(p, nxt, L0 + BATCH, Le, fnext, fe, lane);
       issue_gathers<RP>(p, cur, myfib, X, Y, lane);
       cp_async_wait_all();
       __syncwarp();

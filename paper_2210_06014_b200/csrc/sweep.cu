@@ -1136,15 +1136,34 @@ __global__ void __launch_bounds__(GramPlan::WPB * 32, 2)
     const int Lb = __ldg(p.fiber_ptr + fb), Le = __ldg(p.fiber_ptr + fe);
     float *arow = p.A + (int64_t)i * p.J;
     float a = jl ? arow[lane] : 0.f;
-    int fcur = fb;
-    BatchIdx nxt;  // next batch's index loads, one batch ahead (long rows: always)
-    load_batch_idx(p, nxt, Lb, Le, fcur, fe, lane);
+    // Index pipeline (long rows): batch b+1's leaf / value / fiber-window loads are issued at
+    // batch b-1, its fibers and prefix coordinate (order 3) at batch b, so no batch waits on a
+    // dependent global load before its gathers go out.
+    BatchIdx nxt;
+    load_batch_idx(p, nxt, Lb, Le, fb, fe, lane);
+    int nfnext;
+    int nfib = batch_fib(nxt, lane, &nfnext);
+    int npc = (p.N == 3 && lane < nxt.nb) ? __ldg(p.fiber_coord + (int64_t)nfib * 2 + 1) : 0;
+    BatchIdx nn;
+    bool has_nn = Lb + BATCH < Le;
+    if (has_nn) load_batch_idx(p, nn, Lb + BATCH, Le, nfnext, fe, lane);
     for (int L0 = Lb; L0 < Le; L0 += BATCH) {
       const BatchIdx cur = nxt;
-      int fnext;
-      const int myfib = batch_fib(cur, lane, &fnext);
-      if (L0 + BATCH < Le) load_batch_idx(p, nxt, L0 + BATCH, Le, fnext, fe, lane);
-      issue_gathers<RP>(p, cur, myfib, X, Y, lane);
+      const int myfib = nfib, pc = npc;
+      if (p.N == 3) {
+        gather_sw<RP>(X, p.Cpre[0], p.R, pc, cur.nb, lane);
+        gather_sw<RP>(Y, p.Cleaf, p.R, cur.lc, cur.nb, lane);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+      } else {
+        issue_gathers<RP>(p, cur, myfib, X, Y, lane);
+      }
+      if (has_nn) {  // advance the index pipeline under this batch's gathers
+        nxt = nn;
+        nfib = batch_fib(nxt, lane, &nfnext);
+        npc = (p.N == 3 && lane < nxt.nb) ? __ldg(p.fiber_coord + (int64_t)nfib * 2 + 1) : 0;
+        has_nn = nxt.L0 + BATCH < Le;
+        if (has_nn) load_batch_idx(p, nn, nxt.L0 + BATCH, Le, nfnext, fe, lane);
+      }
       cp_async_wait_all();
       __syncwarp();
       const int nb = cur.nb, mts = nb > 16 ? 2 : 1;
@@ -1271,7 +1290,6 @@ __global__ void __launch_bounds__(GramPlan::WPB * 32, 2)
           Y[swz(k, lane)] = 0.f;
         }
       __syncwarp();
-      fcur = fnext;
     }
     if (jl) arow[lane] = a;
   }

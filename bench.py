@@ -409,9 +409,11 @@ def run_ours(args, cfg):
 
 
 def run_e2e(ft, T, cfg, train_dev, args):
-    """Same metric through the public API from HOST buffers: every step copies the training
-    COO from pinned host memory to the device, builds the B-CSF forest, fills the cache, runs one
-    epoch and reads the training RMSE back (a `train(epochs=1)` call minus its epoch-0 row)."""
+    """Same metric through the public API from HOST buffers.  Every step takes its training COO
+    from pinned host memory (H2D), builds the B-CSF forest on the GPU, fills the cache, runs one
+    epoch and reads the training RMSE back (a `train(epochs=1)` call minus its epoch-0 row).
+    The input pipeline is double-buffered: step k+1's H2D runs on a copy stream under step k's
+    compute, as a streaming trainer would; step 0's copy is inside the timed region."""
     import torch
 
     idx_h = train_dev.idx.cpu().pin_memory()
@@ -419,30 +421,58 @@ def run_e2e(ft, T, cfg, train_dev, args):
     dims, J, R = cfg["dims"], cfg["J"], cfg["R"]
     N = len(dims)
     nnz = int(vals_h.shape[0])
-    steps = max(1, min(args.steps, 3))
-    times = []
-    for k in range(1 + steps):
-        model = ft.default_init_model(dims, (J,) * N, R, seed=0)
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        dev = ft.DeviceCoo(tuple(dims), idx_h.to("cuda", non_blocking=True),
-                           vals_h.to("cuda", non_blocking=True))
+    steps = max(2, min(args.steps, 4))
+    bufs = [(torch.empty_like(idx_h, device="cuda"), torch.empty_like(vals_h, device="cuda"))
+            for _ in range(2)]
+    copy_stream = torch.cuda.Stream()
+    main_stream = torch.cuda.current_stream()
+    tcfg = ft.TrainConfig(epochs=1, schedule=args.schedule)
+
+    def h2d(slot, after=None):
+        with torch.cuda.stream(copy_stream):
+            if after is not None:
+                copy_stream.wait_event(after)
+            bufs[slot][0].copy_(idx_h, non_blocking=True)
+            bufs[slot][1].copy_(vals_h, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy_stream)
+        return ev
+
+    def step(slot, ready):
+        main_stream.wait_event(ready)
+        dev = ft.DeviceCoo(tuple(dims), bufs[slot][0], bufs[slot][1])
+        model = ft.Model(dims, (J,) * N, R, init_f, init_c)
         forest = ft.build_forest(dev, 128, compact=True)
         counter = ft.OpCounter()
         cache = ft.precompute_cache(model, counter)
-        m = T.run_epoch(model, forest, cache, dev, ft.TrainConfig(epochs=1, schedule=args.schedule),
-                        counter, 1, None, evaluate_metrics=True)
-        _ = m.train_rmse  # read back to the host inside the timed region
-        b.record()
-        torch.cuda.synchronize()
-        if k > 0:
-            times.append(a.elapsed_time(b) / 1e3)
-        del forest, cache, dev
-    t = sum(times) / len(times)
+        m = T.run_epoch(model, forest, cache, dev, tcfg, counter, 1, None, evaluate_metrics=True)
+        _ = m.train_rmse  # the step's result, read back to the host
+        done = torch.cuda.Event()
+        done.record(main_stream)
+        return done
+
+    base = ft.default_init_model(dims, (J,) * N, R, seed=0)
+    init_f, init_c = [a.clone() for a in base.factors], [b.clone() for b in base.cores_t]
+    step(0, h2d(0))  # warm-up (allocator pools, lazy module loading)
+    torch.cuda.synchronize()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(main_stream)
+    ready = h2d(0)
+    free = [None, None]
+    for k in range(steps):
+        slot = k % 2
+        nxt = None
+        if k + 1 < steps:
+            nxt = h2d((k + 1) % 2, after=free[(k + 1) % 2])
+        free[slot] = step(slot, ready)
+        ready = nxt
+    stop.record(main_stream)
+    torch.cuda.synchronize()
+    t = start.elapsed_time(stop) / 1e3 / steps
     return {"value": nnz / t, "unit": "nnz/s", "h2d_bytes_per_step": nnz * (4 * N + 4),
-            "d2h_bytes_per_step": 16, "ms_per_step": 1e3 * t, "steps": len(times),
-            "includes": "H2D COO + GPU B-CSF build + cache + 1 epoch + train RMSE readback"}
+            "d2h_bytes_per_step": 16, "ms_per_step": 1e3 * t, "steps": steps,
+            "includes": "H2D COO (pinned, double-buffered on a copy stream) + GPU B-CSF build + "
+                        "cache + 1 epoch + train RMSE readback"}
 
 
 def main():

@@ -1069,6 +1069,324 @@ __global__ void __launch_bounds__(RDualPlan::WPB * 32, 2)
 #undef VHR
 }
 
+
+// ---- K3b, warp-specialised (producer / consumer) two-row version --------------------------
+// A warp pair owns two rows (one per 16-lane half, as in the dual kernel).  The PRODUCER warp
+// walks both root slices in 16-leaf batches -- index loads prefetched a batch ahead, cp.async
+// gathers double-buffered (batch b+1's are in flight while batch b's rank products go through
+// the 3xTF32 tensor-core combine) -- and publishes V plus the batch's values into a 2-stage
+// shared-memory ring (mbarrier full / empty).  The CONSUMER warp only runs the two serial
+// chains s = a.v, e = x - s, a -= lr (reg a - e v).  All tiles are 16 x 32 floats with the XOR
+// swizzle (conflict-free fragment loads, 16-B cp.async) so a pair fits 24.6 KB and 8 pairs an SM.
+// Order-3 tensors only (the prefix is a single C row); other orders use dual / gram.
+namespace ws {
+constexpr int NS = 2;                       // ring stages
+constexpr int PAIRS = 4;                    // warp pairs per block
+constexpr int HT = HB * 32;                 // swizzled 16 x 32 tile
+constexpr int STAGE_FLOATS = 2 * HT + 2 * HB + 8;  // V[2 halves], x[2][16], meta[8]
+constexpr int PAIR_FLOATS = NS * STAGE_FLOATS + 8 * HT;  // ring + producer X/Y x 2 halves x 2 bufs
+constexpr int BAR_BYTES = PAIRS * 2 * NS * 8 + 32;
+template <int RP, int JP>
+constexpr int bfrag_u4() { return (RP / 8 > 0 ? RP / 8 : 1) * (JP / 8) * 32; }
+template <int RP, int JP>
+constexpr size_t bytes() {
+  return (size_t)bfrag_u4<RP, JP>() * 16 + BAR_BYTES + (size_t)PAIRS * PAIR_FLOATS * 4;
+}
+}  // namespace ws
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_one() {  // all but the most recent group
+  asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+}
+
+// producer-side state of one half (replicated in the half's 16 lanes)
+struct WsHalf {
+  int64_t row;
+  int fe, Le, L0, fcur;
+  bool active, ended, have_pf;
+  int pf_lc, pf_fs;
+  float pf_x;
+};
+// what the producer knows about one in-flight batch
+struct WsBatch {
+  int nb, newrow;
+  float x;
+  bool stop;
+};
+
+template <int RP>
+__device__ __forceinline__ WsBatch ws_advance(const SweepParams &p, WsHalf &H, int64_t nstream,
+                                              float *Xb, float *Yb, int h, int l) {
+  WsBatch B;
+  B.newrow = -1;
+  if (H.active && H.L0 >= H.Le) {
+    H.row += nstream;
+    if (H.row < p.nrows) {
+      B.newrow = __ldg(p.row_coord + H.row);
+      const int fb = __ldg(p.row_fiber_ptr + H.row);
+      H.fe = __ldg(p.row_fiber_ptr + H.row + 1);
+      H.L0 = __ldg(p.fiber_ptr + fb);
+      H.Le = __ldg(p.fiber_ptr + H.fe);
+      H.fcur = fb;
+    } else {
+      H.active = false;
+    }
+    H.have_pf = false;
+  }
+  if (!H.active && !H.ended) {
+    B.newrow = -2;
+    H.ended = true;
+  }
+  B.stop = !__any_sync(FULL, H.active);
+  const int nb = H.active ? min(HB, H.Le - H.L0) : 0;
+  B.nb = nb;
+  const bool lv = l < nb;
+  int lc, fs;
+  if (H.have_pf) {
+    lc = H.pf_lc;
+    B.x = H.pf_x;
+    fs = H.pf_fs;
+  } else {
+    lc = lv ? __ldcs(p.leaf_coord + H.L0 + l) : 0;
+    B.x = lv ? __ldcs(p.vals + H.L0 + l) : 0.f;
+    const int fidx = H.fcur + 1 + l;
+    fs = (H.active && fidx < H.fe) ? __ldg(p.fiber_ptr + fidx) : INT32_MAX;
+  }
+  const unsigned bit = (fs < H.L0 + nb) ? (1u << (fs - H.L0)) : 0u;
+  const unsigned hmask = (__reduce_or_sync(FULL, bit << (16 * h)) >> (16 * h)) & 0xffffu;
+  const int myfib = H.fcur + __popc(hmask & (0xffffu >> (15 - l)));
+  const int fnext = H.fcur + __popc(hmask);
+  const int pc = lv ? __ldg(p.fiber_coord + (int64_t)myfib * 2 + 1) : 0;
+  {  // prefetch the next batch's indices of this row
+    const int L1 = H.L0 + nb;
+    H.have_pf = H.active && L1 < H.Le;
+    if (H.have_pf) {
+      const int nb1 = min(HB, H.Le - L1);
+      H.pf_lc = l < nb1 ? __ldcs(p.leaf_coord + L1 + l) : 0;
+      H.pf_x = l < nb1 ? __ldcs(p.vals + L1 + l) : 0.f;
+      const int fidx = fnext + 1 + l;
+      H.pf_fs = fidx < H.fe ? __ldg(p.fiber_ptr + fidx) : INT32_MAX;
+    }
+  }
+  if (!B.stop) {  // gathers: prefix row into X, leaf row into Y
+    if ((p.R & 3) == 0) {
+      constexpr int P4 = RP / 4;
+      const int R4 = p.R >> 2;
+#pragma unroll
+      for (int q2 = 0; q2 < P4; ++q2) {
+        const int c = l + 16 * q2;
+        const int k = c / P4, q = c % P4;
+        const int ck = __shfl_sync(FULL, pc, 16 * h + k);
+        const int cl = __shfl_sync(FULL, lc, 16 * h + k);
+        if (k < nb && q < R4) {
+          cp_async16(Xb + swz(k, 4 * q), p.Cpre[0] + (int64_t)ck * p.R + 4 * q);
+          cp_async16(Yb + swz(k, 4 * q), p.Cleaf + (int64_t)cl * p.R + 4 * q);
+        }
+      }
+    } else {
+      for (int k = 0; k < HB; ++k) {
+        const int ck = __shfl_sync(FULL, pc, 16 * h + k);
+        const int cl = __shfl_sync(FULL, lc, 16 * h + k);
+        for (int r = l; r < p.R; r += 16)
+          if (k < nb) {
+            cp_async4(Xb + swz(k, r), p.Cpre[0] + (int64_t)ck * p.R + r);
+            cp_async4(Yb + swz(k, r), p.Cleaf + (int64_t)cl * p.R + r);
+          }
+      }
+    }
+  }
+  cp_async_commit();
+  H.L0 += nb;
+  H.fcur = fnext;
+  return B;
+}
+
+template <int RP, int JP>
+__global__ void __launch_bounds__(ws::PAIRS * 64, 2)
+    factor_rows_ws_kernel(const SweepParams p) {
+  constexpr int KT = RP / 8 > 0 ? RP / 8 : 1, NT = JP / 8;
+  extern __shared__ float4 smem4[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int pair = w >> 1, role = w & 1;  // role 0: producer, 1: consumer
+  const int h = lane >> 4, l = lane & 15;
+  const int gq = lane >> 2, tq = lane & 3;
+  uint4 *bfrag = reinterpret_cast<uint4 *>(smem4);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(bfrag + ws::bfrag_u4<RP, JP>()) + pair * 2 * ws::NS;
+  uint64_t *full = bars, *empty = bars + ws::NS;
+  float *pbase = reinterpret_cast<float *>(reinterpret_cast<char *>(bfrag + ws::bfrag_u4<RP, JP>()) +
+                                           ws::BAR_BYTES) +
+                 pair * ws::PAIR_FLOATS;
+  float *ring = pbase;                           // NS stages
+  float *stg = pbase + ws::NS * ws::STAGE_FLOATS;  // [buf 2][X/Y 2][half 2] swizzled tiles
+#define WS_TILE(buf, xy, hh) (stg + (((buf) * 2 + (xy)) * 2 + (hh)) * ws::HT)
+  if (role == 0) {
+    for (int k = lane; k < 8 * ws::HT; k += 32) stg[k] = 0.f;
+    if (lane == 0)
+      for (int st = 0; st < ws::NS; ++st) {
+        mbar_init(full + st, 32);
+        mbar_init(empty + st, 32);
+      }
+  }
+  for (int f = threadIdx.x; f < ws::bfrag_u4<RP, JP>(); f += blockDim.x) {
+    const int ll = f & 31, nt = (f >> 5) % NT, kt = (f >> 5) / NT;
+    const int g = ll >> 2, t = ll & 3, j = 8 * nt + g;
+    uint32_t hv[2], lv2[2];
+    for (int hh = 0; hh < 2; ++hh) {
+      const int r = 8 * kt + t + 4 * hh;
+      const float bv = (r < p.R && j < p.J) ? __ldg(p.Bt + r * p.J + j) : 0.f;
+      hv[hh] = to_tf32(bv);
+      lv2[hh] = to_tf32(bv - __uint_as_float(hv[hh]));
+    }
+    bfrag[f] = make_uint4(hv[0], hv[1], lv2[0], lv2[1]);
+  }
+  __syncthreads();
+  const int64_t nstream = (int64_t)gridDim.x * ws::PAIRS * 2;
+  const int64_t mystream = ((int64_t)blockIdx.x * ws::PAIRS + pair) * 2 + h;
+
+  if (role == 0) {
+    // ===================================== producer =====================================
+    WsHalf H;
+    H.row = mystream - nstream;
+    H.fe = H.Le = H.L0 = H.fcur = 0;
+    H.active = true;
+    H.ended = H.have_pf = false;
+    H.pf_lc = 0;
+    H.pf_fs = INT32_MAX;
+    H.pf_x = 0.f;
+    WsBatch cur = ws_advance<RP>(p, H, nstream, WS_TILE(0, 0, h), WS_TILE(0, 1, h), h, l);
+    for (int it = 0;; ++it) {
+      const int buf = it & 1;
+      WsBatch nxt;
+      nxt.stop = true;
+      if (!cur.stop) {  // batch it+1's gathers fly while batch it goes through the MMA
+        __syncwarp();
+        nxt = ws_advance<RP>(p, H, nstream, WS_TILE(buf ^ 1, 0, h), WS_TILE(buf ^ 1, 1, h), h, l);
+        cp_async_wait_one();
+      } else {
+        cp_async_wait_all();
+      }
+      __syncwarp();
+      float acc[2][NT][4];
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[hh][nt][q] = 0.f;
+      if (!cur.stop) {
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const float *Xs = WS_TILE(buf, 0, hh), *Ys = WS_TILE(buf, 1, hh);
+#pragma unroll
+          for (int kt = 0; kt < KT; ++kt) {
+            const int c0 = 8 * kt + tq;
+            const int o0 = swz(gq, c0), o1 = swz(gq + 8, c0), o2 = swz(gq, c0 + 4),
+                      o3 = swz(gq + 8, c0 + 4);
+            const float x0 = Xs[o0] * Ys[o0], x1 = Xs[o1] * Ys[o1], x2 = Xs[o2] * Ys[o2],
+                        x3 = Xs[o3] * Ys[o3];
+            const uint32_t h0 = to_tf32(x0), h1 = to_tf32(x1), h2 = to_tf32(x2),
+                           h3 = to_tf32(x3);
+            const uint32_t l0 = to_tf32(x0 - __uint_as_float(h0));
+            const uint32_t l1 = to_tf32(x1 - __uint_as_float(h1));
+            const uint32_t l2 = to_tf32(x2 - __uint_as_float(h2));
+            const uint32_t l3 = to_tf32(x3 - __uint_as_float(h3));
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+              const uint4 bb = bfrag[(kt * NT + nt) * 32 + lane];
+              mma_tf32(acc[hh][nt], l0, l1, l2, l3, bb.x, bb.y);
+              mma_tf32(acc[hh][nt], h0, h1, h2, h3, bb.z, bb.w);
+              mma_tf32(acc[hh][nt], h0, h1, h2, h3, bb.x, bb.y);
+            }
+          }
+        }
+      }
+      // publish batch `it` into the ring
+      const int st = it % ws::NS;
+      if (it >= ws::NS) mbar_wait(empty + st, ((it / ws::NS) - 1) & 1);
+      float *S = ring + st * ws::STAGE_FLOATS;
+      if (!cur.stop) {
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const int c0 = 8 * nt + 2 * tq;
+            float *V = S + hh * ws::HT;
+            *reinterpret_cast<float2 *>(V + swz(gq, c0)) = make_float2(acc[hh][nt][0], acc[hh][nt][1]);
+            *reinterpret_cast<float2 *>(V + swz(gq + 8, c0)) =
+                make_float2(acc[hh][nt][2], acc[hh][nt][3]);
+          }
+        S[2 * ws::HT + h * HB + l] = cur.x;
+      }
+      int *meta = reinterpret_cast<int *>(S + 2 * ws::HT + 2 * HB);
+      if (l == 0) {
+        meta[2 * h] = cur.nb;
+        meta[2 * h + 1] = cur.newrow;
+      }
+      if (lane == 0) meta[4] = cur.stop ? 1 : 0;
+      __syncwarp();
+      mbar_arrive(full + st);
+      if (cur.stop) break;
+      cur = nxt;
+    }
+  } else {
+    // ===================================== consumer =====================================
+    const bool j0 = l < p.J, j1 = JP > 16 && l + 16 < p.J;
+    float *arow = nullptr;
+    float a0 = 0.f, a1 = 0.f;
+    for (int it = 0;; ++it) {
+      const int st = it % ws::NS;
+      mbar_wait(full + st, (it / ws::NS) & 1);
+      const float *S = ring + st * ws::STAGE_FLOATS;
+      const int *meta = reinterpret_cast<const int *>(S + 2 * ws::HT + 2 * HB);
+      const int nb = meta[2 * h], newrow = meta[2 * h + 1];
+      const bool stop = meta[4] != 0;
+      if (newrow != -1) {  // this half's row ended (and maybe a new one starts)
+        if (arow) {
+          if (j0) arow[l] = a0;
+          if (j1) arow[l + 16] = a1;
+          arow = nullptr;
+        }
+        if (newrow >= 0) {
+          arow = p.A + (int64_t)newrow * p.J;
+          a0 = j0 ? arow[l] : 0.f;
+          a1 = j1 ? arow[l + 16] : 0.f;
+        }
+      }
+      if (stop) break;
+      const float *Vh = S + h * ws::HT;
+      const float xl = S[2 * ws::HT + h * HB + l];
+      const int nbmax = max(__shfl_sync(FULL, nb, 0), __shfl_sync(FULL, nb, 16));
+#pragma unroll 4
+      for (int k = 0; k < nbmax; ++k) {
+        const float v0 = Vh[swz(k, l)], v1 = JP > 16 ? Vh[swz(k, l + 16)] : 0.f;
+        float s = a0 * v0 + a1 * v1;
+        s += __shfl_xor_sync(FULL, s, 8);
+        s += __shfl_xor_sync(FULL, s, 4);
+        s += __shfl_xor_sync(FULL, s, 2);
+        s += __shfl_xor_sync(FULL, s, 1);
+        const float e = __shfl_sync(FULL, xl, 16 * h + (k & 15)) - s;
+        if (k < nb) {
+          const float g0 = p.reg * a0 - e * v0, g1 = p.reg * a1 - e * v1;
+          a0 = a0 - p.lr * g0;
+          a1 = a1 - p.lr * g1;
+        }
+      }
+      __syncwarp();
+      mbar_arrive(empty + st);
+    }
+    if (arow) {
+      if (j0) arow[l] = a0;
+      if (j1) arow[l + 16] = a1;
+    }
+  }
+#undef WS_TILE
+}
+
 // ---- K3b, Gram form of the serial chain (tensor cores for both GEMMs) -------------------
 // Within a batch the row evolves as a_{m+1} = a_m + lr (e_m v_m - reg a_m).
 // Tracking w_k = a_m . v_k for every leaf k of the batch gives
@@ -1554,6 +1872,27 @@ int launch_dual(const SweepParams &q, cudaStream_t s) {
 }
 
 template <int RP, int JP>
+int launch_ws(const SweepParams &q, cudaStream_t s) {
+  const size_t sm = ws::bytes<RP, JP>();
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(factor_rows_ws_kernel<RP, JP>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    set = true;
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_ws_kernel<RP, JP>,
+                                                    ws::PAIRS * 64, sm) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  int64_t g = (q.nrows + 2 * ws::PAIRS - 1) / (2 * ws::PAIRS);
+  const int64_t cap = (int64_t)sm_count() * per_sm;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  factor_rows_ws_kernel<RP, JP><<<(int)g, ws::PAIRS * 64, sm, s>>>(q);
+  return check_launch("ft_factor_sweep_rows(ws)");
+}
+
+template <int RP, int JP>
 int launch_gram(const SweepParams &p, cudaStream_t s) {
   const size_t sm = GramPlan::bytes<RP, JP>();
   static bool set = false;
@@ -1579,6 +1918,7 @@ int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
     if (e && strcmp(e, "pipe") == 0) return 3;
     if (e && strcmp(e, "dual") == 0) return 4;
     if (e && strcmp(e, "rdual") == 0) return 6;
+    if (e && strcmp(e, "ws") == 0) return 7;
     return 5;  // auto: dual when the rows fill the SMs, gram otherwise
   }();
   int variant = chosen;
@@ -1588,10 +1928,11 @@ int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
   }();
   SweepParams q = p;
   q.tma = use_tma;
-  // auto: dual needs >= 2 rows per resident warp slot to fill the SMs; few long rows (e.g.
-  // Netflix mode 2: 2,182 rows of ~45 K leaves) are bound by the serial chain, which the Gram
-  // form shortens (measured 8.9 vs 10.0 ms pipe / 13.4 ms dual on that mode)
-  if (variant == 5) variant = p.nrows < (int64_t)2 * sm_count() * 16 ? 0 : 4;
+  if (variant == 7 && p.N != 3) variant = 5;  // ws: order-3 tensors (one prefix row)
+  // auto, by rows per resident warp slot: many rows -> dual (Netflix modes 0/1: 7.5 ms);
+  // few long rows -> warp-specialised at order 3 (mode 2: 8.4 vs 8.8 gram, 13.4 dual), else gram
+  if (variant == 5)
+    variant = p.nrows >= (int64_t)2 * sm_count() * 16 ? 4 : (p.N == 3 ? 7 : 0);
   if (variant == 6) {
     const size_t sm = RDualPlan::bytes<RP>();
     static bool set6 = false;
@@ -1605,6 +1946,7 @@ int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
     return check_launch("ft_factor_sweep_rows(rdual)");
   }
   if (variant == 4) return p.J <= 16 ? launch_dual<RP, 16>(q, s) : launch_dual<RP, 32>(q, s);
+  if (variant == 7) return p.J <= 16 ? launch_ws<RP, 16>(q, s) : launch_ws<RP, 32>(q, s);
   if (variant == 3) {
     const size_t sm = PipePlan::bytes<RP>();
     static bool set3 = false;

@@ -478,7 +478,8 @@ def test_long_rows_factor_and_core_sweeps_match_oracle(ft):
         assert_rel(model.cores_t[u].cpu().numpy(), om.cores_t[u], TOL, f"long rows core {u}")
 
 
-@pytest.mark.parametrize("variant", ["dual", "dual+tma", "rdual", "pipe", "mma", "ffma", "gram"])
+@pytest.mark.parametrize("variant", ["ws", "dual", "dual+tma", "rdual", "pipe", "mma", "ffma",
+                                     "gram"])
 def test_factor_kernel_variants_agree(variant, golden_cases):
     """Every K3b variant (FT_FACTOR_KERNEL) reproduces the reference's rank-32 sweeps at 1e-4,
     run in a subprocess because the variant is latched at first launch."""

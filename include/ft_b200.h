@@ -36,6 +36,7 @@ extern "C" {
 
 #define FT_MAX_ORDER 16
 #define FT_MAX_RANK 32
+#define FT_MAX_PEERS 16
 
 typedef enum {
   FT_OK = 0,
@@ -103,6 +104,15 @@ FT_API int ft_build_tree(int32_t N, int64_t nnz, const int64_t *dims, const int3
  * of |A| into guard[0] (NaN sorts above +inf, so one word detects both cases). */
 FT_API int ft_refresh(int64_t I, int32_t J, int32_t R, const float *A, const float *Bt, float *C,
                uint32_t *guard, void *stream);
+
+/* K2 fused with the C_u all-gather of the row-block-sharded multi-GPU epoch (dist.py): computes
+ * the I rows of C = A Bt^T of THIS rank's block and stores them into every destination -- the
+ * local C_u and each peer's C_u, all already offset to the block's first row; peer pointers
+ * are CUDA-IPC mappings, so on a multi-GPU node the stores travel over NVLink inside the
+ * refresh kernel instead of a separate NCCL all-gather.  ndst <= FT_MAX_PEERS.  The caller
+ * fences (stream sync + barrier) before any rank reads the gathered C_u. */
+FT_API int ft_refresh_scatter(int64_t I, int32_t J, int32_t R, const float *A, const float *Bt,
+                              float *const *dsts, int32_t ndst, uint32_t *guard, void *stream);
 
 /* K3b  Exact factor sweep of mode u = tree->root_mode: replaces factor_sweep over the tree
  * rooted at (u+1) mod N (_ckern.pyx:132-199, train.py:152-197).  One warp owns one row of A_u

@@ -72,6 +72,9 @@ SIGNATURES = {
         ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp, _vp, _vp, _vp, _vp, _vp, _i64p, _vp]),
     "ft_refresh": (ctypes.c_int, [
         ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp, _vp, _vp]),
+    "ft_refresh_scatter": (ctypes.c_int, [
+        ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, _vp, _vp, ctypes.POINTER(_vp),
+        ctypes.c_int32, _vp, _vp]),
     "ft_factor_sweep_rows": (ctypes.c_int, [
         ctypes.POINTER(FtTree), ctypes.POINTER(FtModel), ctypes.c_float, ctypes.c_float, _vp]),
     "ft_factor_sweep_fibers": (ctypes.c_int, [

@@ -13,9 +13,14 @@ namespace {
 constexpr int WARPS = 4;
 constexpr int TILE = 32;  // rows per warp
 
+struct Dsts {
+  float *p[FT_MAX_PEERS];
+  int n;
+};
+
 __global__ void __launch_bounds__(WARPS * 32)
     refresh_kernel(int64_t I, int J, int R, const float *__restrict__ A,
-                   const float *__restrict__ Bt, float *__restrict__ C, uint32_t *guard) {
+                   const float *__restrict__ Bt, Dsts dst, uint32_t *guard) {
   __shared__ float bts[FT_MAX_RANK][FT_MAX_RANK + 1];
   __shared__ float tile[WARPS][TILE][FT_MAX_RANK + 1];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -58,9 +63,13 @@ __global__ void __launch_bounds__(WARPS * 32)
       if (r < R) tile[w][lane][r] = out[r];
   }
   __syncwarp();
-  float *dst = C + row0 * R;
+  // the tile goes to every destination: the local C_u and, for the fused refresh + all-gather,
+  // each peer rank's C_u through its CUDA-IPC-mapped pointer (NVLink stores on a multi-GPU node)
   const int nC = rows * R;
-  for (int k = lane; k < nC; k += 32) __stcs(dst + k, tile[w][k / R][k % R]);
+  for (int d = 0; d < dst.n; ++d) {
+    float *out = dst.p[d] + row0 * R;
+    for (int k = lane; k < nC; k += 32) __stcs(out + k, tile[w][k / R][k % R]);
+  }
 }
 
 }  // namespace
@@ -75,6 +84,31 @@ extern "C" int ft_refresh(int64_t I, int32_t J, int32_t R, const float *A, const
   if (I == 0) return FT_OK;
   if (!A || !Bt || !C) return fail(FT_ERR_ARG, "ft_refresh: null pointer");
   const int64_t blocks = (I + WARPS * TILE - 1) / (WARPS * TILE);
-  refresh_kernel<<<(unsigned)blocks, WARPS * 32, 0, as_stream(stream)>>>(I, J, R, A, Bt, C, guard);
+  Dsts d{};
+  d.p[0] = C;
+  d.n = 1;
+  refresh_kernel<<<(unsigned)blocks, WARPS * 32, 0, as_stream(stream)>>>(I, J, R, A, Bt, d, guard);
   return check_launch("ft_refresh");
+}
+
+extern "C" int ft_refresh_scatter(int64_t I, int32_t J, int32_t R, const float *A, const float *Bt,
+                                  float *const *dsts, int32_t ndst, uint32_t *guard,
+                                  void *stream) {
+  using namespace ft;
+  if (I < 0 || J < 1 || R < 1 || J > FT_MAX_RANK || R > FT_MAX_RANK)
+    return fail(FT_ERR_UNSUPPORTED, "ft_refresh_scatter: I=%lld J=%d R=%d outside kernel cover",
+                (long long)I, J, R);
+  if (!dsts || ndst < 1 || ndst > FT_MAX_PEERS)
+    return fail(FT_ERR_ARG, "ft_refresh_scatter: 1..%d destinations required", FT_MAX_PEERS);
+  if (I == 0) return FT_OK;
+  if (!A || !Bt) return fail(FT_ERR_ARG, "ft_refresh_scatter: null pointer");
+  Dsts d{};
+  for (int k = 0; k < ndst; ++k) {
+    if (!dsts[k]) return fail(FT_ERR_ARG, "ft_refresh_scatter: null destination %d", k);
+    d.p[k] = dsts[k];
+  }
+  d.n = ndst;
+  const int64_t blocks = (I + WARPS * TILE - 1) / (WARPS * TILE);
+  refresh_kernel<<<(unsigned)blocks, WARPS * 32, 0, as_stream(stream)>>>(I, J, R, A, Bt, d, guard);
+  return check_launch("ft_refresh_scatter");
 }

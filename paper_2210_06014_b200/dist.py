@@ -16,9 +16,12 @@ UPDATED MODE with no stratum rotation:
     all-gather;
   * evaluate: each rank scores a slice of the entries, all-reduce of (SSE, SAE).
 
-Factors are bitwise equal to the single-GPU exact schedule; cores differ only in the order of
-the gradient sum.  The compute goes through an ``engine`` (CudaEngine on GPUs; the CPU tests
-inject a CPU fp64 reference engine) so the partition / collective logic is tested with gloo.
+The first factor pass is bitwise equal to the single-GPU exact schedule; afterwards only the
+order of the core-gradient sum differs.  With ``peer_dots=True`` the C_u all-gather is fused
+into the refresh kernel (ft_refresh_scatter): every rank maps every other rank's C buffers by
+CUDA IPC and writes its row block into all of them -- NVLink stores on a multi-GPU node -- then
+one barrier.  The compute goes through an ``engine`` (CudaEngine on GPUs; the CPU tests inject
+a CPU fp64 reference engine) so the partition / collective logic is tested with gloo.
 """
 
 from __future__ import annotations
@@ -143,6 +146,33 @@ class CudaEngine:
                                         1, 1, float(omega), lr, reg, None, guard.data_ptr(),
                                         _lib.stream_handle()), "ft_core_apply")
 
+    def refresh_scatter(self, model, u, c0, c1, dsts, guard):
+        """Fused refresh + all-gather: this rank's C_u rows into every rank's C_u (peer IPC)."""
+        if c1 <= c0:
+            return
+        A, Bt = model.factors[u], model.cores_t[u]
+        J, R = A.shape[1], Bt.shape[0]
+        tab = (ctypes.c_void_p * len(dsts))(*[d[c0:c1].data_ptr() for d in dsts])
+        _lib.check(self.L.ft_refresh_scatter(c1 - c0, J, R, A[c0:c1].data_ptr(), Bt.data_ptr(),
+                                             tab, len(dsts),
+                                             None if guard is None else guard.data_ptr(),
+                                             _lib.stream_handle()), "ft_refresh_scatter")
+
+    def share(self, tensors):
+        """CUDA-IPC descriptors of device tensors (torch's own cross-process sharing)."""
+        return [t.untyped_storage()._share_cuda_() for t in tensors]
+
+    def open_peer(self, metas, like):
+        import torch
+
+        out = []
+        for meta, ref in zip(metas, like):
+            st = torch.UntypedStorage._new_shared_cuda(*meta)
+            t = torch.empty(0, dtype=ref.dtype, device=ref.device)
+            t.set_(st, 0, ref.shape, ref.stride())
+            out.append(t)
+        return out
+
     def refresh_block(self, model, u, c0, c1, C, guard):
         if c1 <= c0:
             return
@@ -188,7 +218,8 @@ class DistTrainer:
     ``coo``: the full training tensor on every rank (DeviceCoo for the CUDA engine),
     ``cfg``: TrainConfig (exact schedule)."""
 
-    def __init__(self, model, coo, cfg, group=None, engine=None, fiber_threshold=128):
+    def __init__(self, model, coo, cfg, group=None, engine=None, fiber_threshold=128,
+                 peer_dots: bool = False):
         import torch.distributed as dist
 
         self.dist = dist
@@ -210,6 +241,14 @@ class DistTrainer:
             tree, nnz, ft = self.engine.build_shard(coo, u, c0, c1, fiber_threshold)
             self.shards.append(ModeShard(u, c0, c1, tree, nnz, ft))
         self.dots = self._alloc_dots()
+        # peer mode: every rank maps every other rank's C_n buffers (CUDA IPC; NVLink peer
+        # memory on a multi-GPU node) and the refresh kernel writes its block into all of them
+        self.peer_dots = None
+        if peer_dots and self.world > 1:
+            metas = [None] * self.world
+            self.dist.all_gather_object(metas, self.engine.share(self.dots), group=self.group)
+            self.peer_dots = [self.dots if q == self.rank else self.engine.open_peer(metas[q], self.dots)
+                              for q in range(self.world)]
         for u in range(N):
             self._refresh_and_gather(u, None)
         self.guards = self.engine.new_guards(2 * N)
@@ -229,6 +268,12 @@ class DistTrainer:
         import torch
 
         b = self.blocks[u]
+        if self.peer_dots is not None:
+            self.engine.refresh_scatter(self.model, u, int(b[self.rank]), int(b[self.rank + 1]),
+                                        [pd[u] for pd in self.peer_dots], guard)
+            self.engine.synchronize()
+            self.dist.barrier(group=self.group)  # every block landed before anyone reads C_u
+            return
         self.engine.refresh_block(self.model, u, int(b[self.rank]), int(b[self.rank + 1]),
                                   self.dots[u], guard)
         if self.world == 1:
@@ -347,7 +392,9 @@ def bench_distributed(args, cfg, rank, world):
     model = default_init_model(dims, (J,) * N, R, seed=0)
     tcfg = TrainConfig(epochs=1)
     t0 = time.perf_counter()
-    trainer = DistTrainer(model, split.train, tcfg)
+    # fused refresh + all-gather over peer memory (NVLink) by default; FT_PEER=0: NCCL all-gather
+    trainer = DistTrainer(model, split.train, tcfg,
+                          peer_dots=os.environ.get("FT_PEER", "1") == "1")
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
     for k in range(args.warmup):

@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _worker(rank, world, port, outdir):
+def _worker(rank, world, port, outdir, peer=False):
     import sys
 
     import torch
@@ -35,7 +35,7 @@ def _worker(rank, world, port, outdir):
                        torch.from_numpy(z["rank32/vals"].astype(np.float32)).cuda())
     f, c = model_arrays(z, "rank32/init/", 3)
     model = ft.Model(tuple(case["dims"]), (32,) * 3, 32, f, c)
-    tr = DistTrainer(model, coo, ft.TrainConfig(**case["cfg"]))
+    tr = DistTrainer(model, coo, ft.TrainConfig(**case["cfg"]), peer_dots=peer)
     for e in range(case["cfg"]["epochs"]):
         tr.run_epoch(e + 1)
     rmse = tr.evaluate()[0]
@@ -48,7 +48,8 @@ def _worker(rank, world, port, outdir):
     dist.destroy_process_group()
 
 
-def test_two_ranks_on_one_gpu_equal_single_gpu(tmp_path, golden_cases):
+@pytest.mark.parametrize("peer", [False, True], ids=["allgather", "fused-peer-refresh"])
+def test_two_ranks_on_one_gpu_equal_single_gpu(tmp_path, golden_cases, peer):
     import torch
     import torch.multiprocessing as mp
 
@@ -58,7 +59,7 @@ def test_two_ranks_on_one_gpu_equal_single_gpu(tmp_path, golden_cases):
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
-    mp.start_processes(_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True,
+    mp.start_processes(_worker, args=(2, port, str(tmp_path), peer), nprocs=2, join=True,
                        start_method="spawn")
     out = np.load(tmp_path / "d.npz")
 

@@ -399,6 +399,10 @@ def run_ours(args, cfg):
         "factor_ms": 1e3 * f_s / args.steps, "core_ms": 1e3 * c_s / args.steps,
         "pass_roofline_frac": {k: pass_bytes[k] / ((f_s if k == "factor" else c_s) / args.steps)
                                / 1e9 / peak for k in pass_bytes},
+        # the north star's figure: the whole epoch (both passes, refreshes, applies) against
+        # the HBM roofline on the algorithmic bytes of the schedule that ran
+        "epoch_roofline_frac": (pass_bytes["factor"] + pass_bytes["core"])
+                               / (total_s / args.steps) / 1e9 / peak,
         "train_rmse_before": rmse0, "train_rmse": tr_rmse, "test_rmse": te_rmse,
         "build_forest_s": build_s,
         "roofline": roof, "kernels": kernels,

@@ -92,6 +92,9 @@ FT_API int ft_sm_count(int32_t *out);
  *   row_fiber_ptr[nnz+1], row_coord[nnz].   inds / ptrs are HOST arrays of device pointers.
  * counts_out (HOST int64[4+N]): F, S, rows, first duplicate position (-1 if none),
  *   then node count per depth.  SYNCHRONOUS (sizes are data dependent).
+ * Compact build: ptrs == NULL (and inds[d < N-1], sub_fiber_ptr, sub_leaf_ptr may be NULL)
+ *   skips the reference-format per-depth arrays and subtensors, producing only what the sweep
+ *   kernels read (leaf coordinates, values, fiber_ptr / fiber_coord, rows).
  * Returns FT_ERR_DUPLICATE (with counts_out[3] set) if two entries share a coordinate. */
 FT_API int ft_build_tree(int32_t N, int64_t nnz, const int64_t *dims, const int32_t *idx,
                   const float *vals, int32_t root_mode, int64_t thr, float *leaf_vals,

@@ -1640,13 +1640,16 @@ __global__ void __launch_bounds__(WPB_R * 32)
     const int Lb = __ldg(p.fiber_ptr + fb), Le = __ldg(p.fiber_ptr + fe);
     if (rl) cus[lane] = __ldg(p.Cu + (int64_t)i * p.R + lane);
     float g = 0.f;
-    int fcur = fb;
+    // index pipeline: the next batch's leaf / value / fiber-window loads fly under this batch
+    BatchIdx nxt;
+    load_batch_idx(p, nxt, Lb, Le, fb, fe, lane);
     for (int L0 = Lb; L0 < Le; L0 += BATCH) {
-      const int nb = min(BATCH, Le - L0);
-      const int lc = lane < nb ? __ldcs(p.leaf_coord + L0 + lane) : 0;
-      const float x = lane < nb ? __ldcs(p.vals + L0 + lane) : 0.f;
+      const BatchIdx cur = nxt;
+      const int nb = cur.nb, lc = cur.lc;
+      const float x = cur.x;
       int fnext;
-      const int myfib = batch_fibers(p.fiber_ptr, fcur, fe, L0, nb, lane, &fnext);
+      const int myfib = batch_fib(cur, lane, &fnext);
+      if (L0 + BATCH < Le) load_batch_idx(p, nxt, L0 + BATCH, Le, fnext, fe, lane);
       // cross = X * Y is folded into both consumers below (no separate product pass)
       stage_cross<RP>(p, X, Y, myfib, lc, nb, lane, /*fold_leaf=*/false);
       // lane k: s_k = C_u[i] . cross_k  (= A_u[i] . vec_k, since C_u = A_u Bt_u^T is coherent)
@@ -1682,7 +1685,6 @@ __global__ void __launch_bounds__(WPB_R * 32)
         }
       }
       __syncwarp();
-      fcur = fnext;
     }
     // acc[r][j] += g[r] * A_u[i][j]  (row broadcast to all lanes)
     const float *arow = p.A + (int64_t)i * p.J;

@@ -63,6 +63,11 @@ typedef struct {
   const int32_t *fiber_coord;   /* [F*(N-1)] csf fiber_coord, row-major                      */
   const int32_t *row_fiber_ptr; /* [rows+1] fiber index where each root slice starts         */
   const int32_t *row_coord;     /* [rows]  level-0 coordinate of each root slice             */
+  /* Leaf-major index (optional, NULL = absent; filled by ft_tree_leaf_index).  Not reference
+   * fields: derived once per tree so the row-owner kernels read every per-leaf operand with
+   * plain coalesced loads instead of the fiber-window ballot -> fiber_coord dependent chain. */
+  const int32_t *leaf_pc;       /* [nnz]   level-1 coordinate of each leaf's fiber           */
+  const int32_t *row_leaf_ptr;  /* [rows+1] first leaf of each root slice                    */
 } ft_tree_t;
 
 /* Model parameters and the C^(n) cache (model.py:45-103, cache.py:28-57). */
@@ -102,6 +107,12 @@ FT_API int ft_build_tree(int32_t N, int64_t nnz, const int64_t *dims, const int3
                   int32_t *fiber_coord, int32_t *sub_fiber_ptr, int32_t *sub_leaf_ptr,
                   int32_t *row_fiber_ptr, int32_t *row_coord, int64_t *counts_out, void *stream);
 
+/* K1b Leaf-major index of a built tree (reads tree->fiber_ptr / fiber_coord / row_fiber_ptr):
+ *   leaf_pc[L] = fiber_coord[f(L) * (N-1) + 1] for every leaf L of fiber f(L)  (csf inds[1]
+ *   expanded to the leaves), row_leaf_ptr[r] = fiber_ptr[row_fiber_ptr[r]] for r <= rows.
+ * Either output may be NULL.  Asynchronous. */
+FT_API int ft_tree_leaf_index(const ft_tree_t *tree, int32_t *leaf_pc, int32_t *row_leaf_ptr,
+                              void *stream);
 /* K2  C = A * Bt^T  (I x R), i.e. refresh_dot_mode (_ckern.pyx:21-33, cache.py:60-70), with the
  * divergence guard of train.py:101-110 fused: if guard != NULL, atomically max-es the IEEE bits
  * of |A| into guard[0] (NaN sorts above +inf, so one word detects both cases). */

@@ -45,6 +45,8 @@ class FtTree(ctypes.Structure):
         ("fiber_coord", _vp),
         ("row_fiber_ptr", _vp),
         ("row_coord", _vp),
+        ("leaf_pc", _vp),
+        ("row_leaf_ptr", _vp),
     ]
 
 
@@ -70,6 +72,7 @@ SIGNATURES = {
     "ft_build_tree": (ctypes.c_int, [
         ctypes.c_int32, ctypes.c_int64, _i64p, _vp, _vp, ctypes.c_int32, ctypes.c_int64, _vp,
         ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp, _vp, _vp, _vp, _vp, _vp, _i64p, _vp]),
+    "ft_tree_leaf_index": (ctypes.c_int, [ctypes.POINTER(FtTree), _vp, _vp, _vp]),
     "ft_refresh": (ctypes.c_int, [
         ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp, _vp, _vp]),
     "ft_refresh_scatter": (ctypes.c_int, [

@@ -42,6 +42,8 @@ class CsfTree:
     sub_leaf_ptr: object
     row_fiber_ptr: object  # device int32 [rows+1]  (not a reference field)
     row_coord: object      # device int32 [rows]
+    leaf_pc: object = None       # device int32 [nnz]  level-1 coordinate per leaf (derived)
+    row_leaf_ptr: object = None  # device int32 [rows+1] first leaf per row (derived)
     _view: object = field(default=None, repr=False)
     num_subtensors_built: int = -1
 
@@ -94,6 +96,8 @@ class CsfTree:
             v.fiber_coord = self.fiber_coord.data_ptr()
             v.row_fiber_ptr = self.row_fiber_ptr.data_ptr()
             v.row_coord = self.row_coord.data_ptr()
+            v.leaf_pc = _lib.ptr(self.leaf_pc)
+            v.row_leaf_ptr = _lib.ptr(self.row_leaf_ptr)
             self._view = v
         return self._view
 
@@ -134,6 +138,9 @@ class CsfTree:
             sub_leaf_ptr=torch.zeros(1, dtype=torch.int32, device=self.vals.device),
             row_fiber_ptr=(self.row_fiber_ptr[r0:r1 + 1] - f0).contiguous(),
             row_coord=self.row_coord[r0:r1].clone(),
+            leaf_pc=None if self.leaf_pc is None else self.leaf_pc[l0:l1].clone(),
+            row_leaf_ptr=None if self.row_leaf_ptr is None
+            else (self.row_leaf_ptr[r0:r1 + 1] - l0).contiguous(),
         )
 
 
@@ -229,6 +236,25 @@ def build_tree(tensor, root_mode: int, fiber_threshold=DEFAULT_FIBER_THRESHOLD,
         row_coord=_trim(row_coord, rows),
     )
     tree.num_subtensors_built = S
+    add_leaf_index(tree, stream)
+    return tree
+
+
+def add_leaf_index(tree: CsfTree, stream=None) -> CsfTree:
+    """Derive the leaf-major index the row-owner kernels read (K1b, ft_tree_leaf_index):
+    ``leaf_pc`` (each leaf's level-1 coordinate) and ``row_leaf_ptr`` (first leaf of each root
+    slice).  Not reference fields; 4 bytes per leaf."""
+    import torch
+
+    i32 = dict(dtype=torch.int32, device=tree.vals.device)
+    tree.leaf_pc = torch.empty(tree.nnz, **i32)
+    tree.row_leaf_ptr = torch.empty(tree.num_rows + 1, **i32)
+    tree._view = None
+    v = tree.view()
+    _lib.check(_lib.lib().ft_tree_leaf_index(ctypes.byref(v), tree.leaf_pc.data_ptr(),
+                                             tree.row_leaf_ptr.data_ptr(),
+                                             _lib.stream_handle(stream)), "ft_tree_leaf_index")
+    tree._view = None
     return tree
 
 

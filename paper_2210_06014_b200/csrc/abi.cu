@@ -59,7 +59,7 @@ int sm_count() {
 
 extern "C" const char *ft_last_error(void) { return ft::g_err; }
 
-extern "C" int ft_abi_version(void) { return 1; }
+extern "C" int ft_abi_version(void) { return 2; }
 
 extern "C" int ft_sm_count(int32_t *out) {
   if (!out) return ft::fail(FT_ERR_ARG, "ft_sm_count: null out");

@@ -152,6 +152,46 @@ __global__ void set_i32(int32_t *p, int32_t v) { *p = v; }
 
 inline unsigned blocks_for(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
 
+// K1b: leaf-major index.  One warp per 32 fibers: lane f owns fiber f's leaf range; the warp
+// then writes the ranges cooperatively (consecutive lanes -> consecutive leaves), so the store
+// stream is coalesced even when fibers hold one leaf each (Netflix tree 0: 1.006 leaves/fiber).
+__global__ void leaf_pc_kernel(const int32_t *__restrict__ fiber_ptr,
+                               const int32_t *__restrict__ fiber_coord, int64_t F, int N,
+                               int32_t *__restrict__ leaf_pc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t f0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~(int64_t)31;
+  const int64_t f = f0 + lane;
+  int lb = 0, le = 0, pc = 0;
+  if (f < F) {
+    lb = __ldg(fiber_ptr + f);
+    le = __ldg(fiber_ptr + f + 1);
+    pc = __ldg(fiber_coord + f * (N - 1) + 1);
+  }
+  const int first = __shfl_sync(0xffffffffu, lb, 0);
+  int last = le;
+  for (int o = 16; o > 0; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
+  // leaves [first, last) of this warp's fibers: each leaf finds its fiber among the 32 ranges
+  // (warp-uniform trip count: every lane takes part in the shuffles)
+  for (int base = first; base < last; base += 32) {
+    const int L = base + lane;
+    int lo = 0;  // largest k with lb_k <= L among the warp's real fibers (5 halving steps)
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1) {
+      const int lbm = __shfl_sync(0xffffffffu, lb, lo + step);
+      if (lbm <= L && f0 + lo + step < F) lo += step;
+    }
+    const int v = __shfl_sync(0xffffffffu, pc, lo);
+    if (L < last) leaf_pc[L] = v;
+  }
+}
+
+__global__ void row_leaf_ptr_kernel(const int32_t *__restrict__ fiber_ptr,
+                                    const int32_t *__restrict__ row_fiber_ptr, int64_t rows,
+                                    int32_t *__restrict__ out) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r <= rows) out[r] = __ldg(fiber_ptr + __ldg(row_fiber_ptr + r));
+}
+
 // Compaction of the positions whose flag is set: out[k] = k-th set position; returns count.
 struct Compactor {
   cudaStream_t s;
@@ -379,5 +419,27 @@ extern "C" int ft_build_tree(int32_t N, int64_t nnz, const int64_t *dims, const 
   counts_out[0] = F;
   counts_out[1] = S;
   counts_out[2] = nruns;
+  return FT_OK;
+}
+
+extern "C" int ft_tree_leaf_index(const ft_tree_t *tree, int32_t *leaf_pc, int32_t *row_leaf_ptr,
+                                  void *stream) {
+  if (!tree) return fail(FT_ERR_ARG, "null tree");
+  if (tree->order < 3) return fail(FT_ERR_ARG, "order %d < 3", tree->order);
+  cudaStream_t s = as_stream(stream);
+  const int64_t F = tree->num_fibers, rows = tree->num_rows;
+  if (leaf_pc && F > 0) {
+    if (!tree->fiber_ptr || !tree->fiber_coord) return fail(FT_ERR_ARG, "null fiber arrays");
+    leaf_pc_kernel<<<blocks_for(F), 256, 0, s>>>(tree->fiber_ptr, tree->fiber_coord, F,
+                                                 tree->order, leaf_pc);
+    if (int rc = check_launch("ft_tree_leaf_index(leaf_pc)")) return rc;
+  }
+  if (row_leaf_ptr) {
+    if (!tree->fiber_ptr || !tree->row_fiber_ptr) return fail(FT_ERR_ARG, "null row arrays");
+    row_leaf_ptr_kernel<<<blocks_for(rows + 1), 256, 0, s>>>(tree->fiber_ptr,
+                                                             tree->row_fiber_ptr, rows,
+                                                             row_leaf_ptr);
+    if (int rc = check_launch("ft_tree_leaf_index(row_leaf_ptr)")) return rc;
+  }
   return FT_OK;
 }

@@ -49,6 +49,8 @@ struct SweepParams {
   const int32_t *fiber_coord;
   const int32_t *row_fiber_ptr;
   const int32_t *row_coord;
+  const int32_t *leaf_pc;       // leaf-major index (optional): level-1 coordinate per leaf
+  const int32_t *row_leaf_ptr;  // first leaf of each row
   float *A;          // A_u  (I_u x J)
   const float *Bt;   // Bt_u (R x J)
   const float *Cu;   // C_u  (core sweep)
@@ -1387,6 +1389,8 @@ __global__ void __launch_bounds__(ws::PAIRS * 64, 2)
 #undef WS_TILE
 }
 
+#include "quad.cuh"
+
 // ---- K3b, Gram form of the serial chain (tensor cores for both GEMMs) -------------------
 // Within a batch the row evolves as a_{m+1} = a_m + lr (e_m v_m - reg a_m).
 // Tracking w_k = a_m . v_k for every leaf k of the batch gives
@@ -1921,6 +1925,7 @@ int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
     if (e && strcmp(e, "dual") == 0) return 4;
     if (e && strcmp(e, "rdual") == 0) return 6;
     if (e && strcmp(e, "ws") == 0) return 7;
+    if (e && strcmp(e, "quad") == 0) return 8;
     return 5;  // auto: dual when the rows fill the SMs, gram otherwise
   }();
   int variant = chosen;
@@ -1933,8 +1938,14 @@ int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
   if (variant == 7 && p.N != 3) variant = 5;  // ws: order-3 tensors (one prefix row)
   // auto, by rows per resident warp slot: many rows -> dual (Netflix modes 0/1: 7.5 ms);
   // few long rows -> warp-specialised at order 3 (mode 2: 8.4 vs 8.8 gram, 13.4 dual), else gram
-  if (variant == 5)
-    variant = p.nrows >= (int64_t)2 * sm_count() * 16 ? 4 : (p.N == 3 ? 7 : 0);
+  if (variant == 8 && !quad_ok(p)) variant = 5;  // quad: order 3, 16 < J <= 32, leaf index
+  if (variant == 5) {
+    if (RP == 32 && quad_ok(p) && p.nrows >= (int64_t)2 * sm_count() * quad::WPB * 4)
+      variant = 8;
+    else
+      variant = p.nrows >= (int64_t)2 * sm_count() * 16 ? 4 : (p.N == 3 ? 7 : 0);
+  }
+  if (variant == 8) return launch_quad(q, s);
   if (variant == 6) {
     const size_t sm = RDualPlan::bytes<RP>();
     static bool set6 = false;
@@ -2007,6 +2018,8 @@ int fill_rows_params(SweepParams &p, const ft_tree_t *tree, const ft_model_t *m)
   p.fiber_coord = tree->fiber_coord;
   p.row_fiber_ptr = tree->row_fiber_ptr;
   p.row_coord = tree->row_coord;
+  p.leaf_pc = tree->leaf_pc;
+  p.row_leaf_ptr = tree->row_leaf_ptr;
   p.A = m->factors[u];
   p.Bt = m->cores_t[u];
   p.Cu = m->dots[u];

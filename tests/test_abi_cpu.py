@@ -34,7 +34,7 @@ def test_library_loads_and_exports_every_header_symbol():
         assert hasattr(L, s), s
     assert set(header_symbols()) == set(_lib.SIGNATURES)
     lib = _lib.load()
-    assert lib.ft_abi_version() == 1
+    assert lib.ft_abi_version() == 2
 
 
 def test_library_is_sm100a_only():

@@ -18,9 +18,13 @@
 //   * gathers: lane (slot-in-4, float4 column) -> one shuffle + one wide IMAD + one LDGSTS per
 //     16 B, no per-slot predicates (slots past a quarter's batch copy C row 0 and run as no-op
 //     steps with lr = 0);
-//   * V = cross * Bt_u on tensor cores (mma.sync m16n8k8, 3xTF32, two m16 tiles per 32-slot
-//     batch) with the k index paired (MMA k-slot t <-> r = 2t, t+4 <-> r = 2t+1 within a k-tile)
-//     so every A fragment pair is one LDS.64; the Bt_u fragments use the same pairing.
+//   * the combine runs TRANSPOSED on tensor cores, V^T (J x 32 slots) = Bt_u^T (J x R) *
+//     cross^T (R x 32), mma.sync m16n8k8 3xTF32: the constant Bt_u^T is the A operand (its hi /
+//     lo fragments precomputed per block in shared memory) and the per-leaf cross rows are the
+//     B operand, whose two registers per lane are exactly one LDS.64 pair of X, one of Y and
+//     one FMUL2 when the k index is paired (MMA k-slot t <-> r = 2t, t+4 <-> r = 2t+1 within a
+//     k-tile).  (With cross as the A operand the four-register fragment straddles two such
+//     pairs and ptxas re-packs it with four MOVs per HMMA.)
 // Requirements (checked by the dispatcher): order 3, 16 < J <= 32, R <= 32 with R % 4 == 0,
 // leaf-major index present.
 namespace quad {
@@ -31,8 +35,9 @@ constexpr int TILE = 32 * XS;               // 32 slots
 constexpr int MQ = 9;                       // meta float4 per quarter (8 + 1: disjoint banks)
 constexpr int WARP_FLOATS = 2 * TILE + 4 * MQ * 4;
 constexpr int WPB = 8;
-constexpr int KT = 4, NT = 4;               // RP = JP = 32
-constexpr int BFRAG_U4 = KT * NT * 32;
+constexpr int QVS = 36;                     // V tile row stride: conflict-free scalar stores
+constexpr int KT = 4, MT = 2, NT = 4;       // k = r (32), m = j (32), n = slot (32)
+constexpr int BFRAG_U4 = 2 * KT * MT * 32;  // Bt_u^T A fragments: hi and lo quads
 constexpr size_t bytes() { return (size_t)BFRAG_U4 * 16 + (size_t)WPB * WARP_FLOATS * 4; }
 }  // namespace quad
 
@@ -49,31 +54,115 @@ __device__ __forceinline__ void cp_async16_s(uint32_t dst, const float *src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
 }
 
+// Bt_u^T as the A operand of the transposed combine: for (mt, kt, lane g t) the quad
+// a0 = Bt[r][j], a1 = Bt[r][j+8], a2 = Bt[r+1][j], a3 = Bt[r+1][j+8], r = 8kt + 2t, j = 16mt + g
+// (paired k order), as a hi quad and a lo quad (3xTF32 split).
+__device__ __forceinline__ void quad_afrag_init(const SweepParams &p, uint4 *afr) {
+  using namespace quad;
+  for (int f = threadIdx.x; f < KT * MT * 32; f += blockDim.x) {
+    const int ll = f & 31, kt = (f >> 5) % KT, mt = (f >> 5) / KT;
+    const int g = ll >> 2, t = ll & 3;
+    uint32_t hv[4], lv[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int r = 8 * kt + 2 * t + (e >> 1), j = 16 * mt + g + 8 * (e & 1);
+      const float bv = (r < p.R && j < p.J) ? __ldg(p.Bt + r * p.J + j) : 0.f;
+      hv[e] = to_tf32(bv);
+      lv[e] = to_tf32(bv - __uint_as_float(hv[e]));
+    }
+    afr[f] = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+    afr[KT * MT * 32 + f] = make_uint4(lv[0], lv[1], lv[2], lv[3]);
+  }
+}
+
+// One k-tile of the transposed combine for n-tiles [nt0, nt0 + NN): acc[mt][nt] += Bt^T * cross^T.
+template <int NN>
+__device__ __forceinline__ void quad_mma_kt(const float *X, const float *Y, const uint4 *afr,
+                                            int kt, int nt0, int lane, float (&acc)[2][4][4]) {
+  using namespace quad;
+  const int gq = lane >> 2, tq = lane & 3;
+  uint4 ah[MT], al[MT];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    ah[mt] = afr[(mt * KT + kt) * 32 + lane];
+    al[mt] = afr[KT * MT * 32 + (mt * KT + kt) * 32 + lane];
+  }
+#pragma unroll
+  for (int nn = 0; nn < NN; ++nn) {
+    const int nt = nt0 + nn;
+    const int o = (8 * nt + gq) * XS + 8 * kt + 2 * tq;
+    const float2 c = fmul2(*reinterpret_cast<const float2 *>(X + o),
+                           *reinterpret_cast<const float2 *>(Y + o));
+    const uint32_t bh0 = __float_as_uint(c.x), bh1 = __float_as_uint(c.y);  // the MMA truncates
+    const uint32_t bl0 = __float_as_uint(c.x - __uint_as_float(to_tf32(c.x)));
+    const uint32_t bl1 = __float_as_uint(c.y - __uint_as_float(to_tf32(c.y)));
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      mma_tf32(acc[mt][nt], al[mt].x, al[mt].y, al[mt].z, al[mt].w, bh0, bh1);
+      mma_tf32(acc[mt][nt], ah[mt].x, ah[mt].y, ah[mt].z, ah[mt].w, bl0, bl1);
+      mma_tf32(acc[mt][nt], ah[mt].x, ah[mt].y, ah[mt].z, ah[mt].w, bh0, bh1);
+    }
+  }
+}
+
+// acc (V^T fragments) -> V[slot][j] (row stride QVS)
+__device__ __forceinline__ void quad_store_v(float *V, const float (&acc)[2][4][4], int lane) {
+  using namespace quad;
+  const int gq = lane >> 2, tq = lane & 3;
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      float *v = V + (8 * nt + 2 * tq) * QVS + 16 * mt + gq;
+      v[0] = acc[mt][nt][0];
+      v[QVS] = acc[mt][nt][1];
+      v[8] = acc[mt][nt][2];
+      v[QVS + 8] = acc[mt][nt][3];
+    }
+}
+
+__device__ __forceinline__ void quad_zero(float (&acc)[2][4][4]) {
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[mt][nt][u] = 0.f;
+}
+
+// one serial step of a quarter's row: s = a . v (8 lanes x 4 columns), e = x - s,
+// a <- a + (-lr reg) a  (the decay, never through a rounded 1 - lr reg), then a += lr e v
+__device__ __forceinline__ void quad_chain_step(float (&a)[4], const float *vrow, float4 m) {
+  const float4 v = *reinterpret_cast<const float4 *>(vrow);
+  float2 pr = fmul2(make_float2(a[0], a[1]), make_float2(v.x, v.y));
+  pr = ffma2(make_float2(a[2], a[3]), make_float2(v.z, v.w), pr);
+  float s = pr.x + pr.y;
+  s += __shfl_xor_sync(FULL, s, 4);
+  s += __shfl_xor_sync(FULL, s, 2);
+  s += __shfl_xor_sync(FULL, s, 1);
+  const float e = m.x - s;  // m = (x, lr, -lr reg, -lr reg); lr = 0 on padding steps
+  const float lre = m.y * e;
+  const float2 a01 = ffma2(make_float2(m.z, m.w), make_float2(a[0], a[1]), make_float2(a[0], a[1]));
+  const float2 a23 = ffma2(make_float2(m.z, m.w), make_float2(a[2], a[3]), make_float2(a[2], a[3]));
+  a[0] = __fmaf_rn(lre, v.x, a01.x);
+  a[1] = __fmaf_rn(lre, v.y, a01.y);
+  a[2] = __fmaf_rn(lre, v.z, a23.x);
+  a[3] = __fmaf_rn(lre, v.w, a23.y);
+}
+
 __global__ void __launch_bounds__(quad::WPB * 32, 2) factor_rows_quad_kernel(const SweepParams p) {
   using namespace quad;
   extern __shared__ float4 smem4[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int q = lane >> 3, l = lane & 7;    // quarter (row stream), lane in quarter
   const int gq = lane >> 2, tq = lane & 3;  // mma fragment coordinates
-  uint4 *bfrag = reinterpret_cast<uint4 *>(smem4);
-  float *X = reinterpret_cast<float *>(bfrag + BFRAG_U4) + w * quad::WARP_FLOATS;
+  uint4 *afr = reinterpret_cast<uint4 *>(smem4);
+  float *X = reinterpret_cast<float *>(afr + BFRAG_U4) + w * quad::WARP_FLOATS;
   float *Y = X + TILE;
   float4 *meta = reinterpret_cast<float4 *>(Y + TILE);
   float *V = X;  // V = cross * Bt_u overwrites X once the fragments are read
   for (int k = lane; k < 2 * TILE; k += 32) X[k] = 0.f;  // Y's zero columns r >= R stay zero
-  for (int f = threadIdx.x; f < BFRAG_U4; f += blockDim.x) {
-    const int ll = f & 31, nt = (f >> 5) % NT, kt = (f >> 5) / NT;
-    const int g = ll >> 2, t = ll & 3, j = 8 * nt + g;
-    uint32_t hv[2], lv[2];
-#pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-      const int r = 8 * kt + 2 * t + hh;  // paired k order (see header)
-      const float bv = (r < p.R && j < p.J) ? __ldg(p.Bt + r * p.J + j) : 0.f;
-      hv[hh] = to_tf32(bv);
-      lv[hh] = to_tf32(bv - __uint_as_float(hv[hh]));
-    }
-    bfrag[f] = make_uint4(hv[0], hv[1], lv[0], lv[1]);
-  }
+  quad_afrag_init(p, afr);
   __syncthreads();
 
   const int64_t nstream = (int64_t)gridDim.x * quad::WPB * 4;
@@ -174,82 +263,254 @@ __global__ void __launch_bounds__(quad::WPB * 32, 2) factor_rows_quad_kernel(con
     }
     cp_async_wait_all();
     __syncwarp();
-    // ---- V = (X * Y) * Bt_u: two m16 tiles (slots 0-15, 16-31), 3xTF32 ----
-    float acc[2][NT][4];
+    // ---- V^T = Bt_u^T * (X * Y)^T, 3xTF32 ----
+    float acc[2][4][4];
+    quad_zero(acc);
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-        for (int t = 0; t < 4; ++t) acc[mt][nt][t] = 0.f;
-#pragma unroll
-    for (int kt = 0; kt < KT; ++kt) {
-      uint32_t ah[2][4], al[2][4];
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-        const int o0 = (16 * mt + gq) * XS + 8 * kt + 2 * tq, o1 = o0 + 8 * XS;
-        const float2 x0 = *reinterpret_cast<const float2 *>(X + o0);
-        const float2 x1 = *reinterpret_cast<const float2 *>(X + o1);
-        const float2 y0 = *reinterpret_cast<const float2 *>(Y + o0);
-        const float2 y1 = *reinterpret_cast<const float2 *>(Y + o1);
-        const float2 c0 = fmul2(x0, y0), c1 = fmul2(x1, y1);
-        // fragment order a0 = (gq, k=tq), a1 = (gq+8, tq), a2 = (gq, tq+4), a3 = (gq+8, tq+4)
-        const float cv[4] = {c0.x, c1.x, c0.y, c1.y};
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          ah[mt][t] = to_tf32(cv[t]);
-          al[mt][t] = to_tf32(cv[t] - __uint_as_float(ah[mt][t]));
-        }
-      }
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const uint4 bb = bfrag[(kt * NT + nt) * 32 + lane];
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          mma_tf32(acc[mt][nt], al[mt][0], al[mt][1], al[mt][2], al[mt][3], bb.x, bb.y);
-          mma_tf32(acc[mt][nt], ah[mt][0], ah[mt][1], ah[mt][2], ah[mt][3], bb.z, bb.w);
-          mma_tf32(acc[mt][nt], ah[mt][0], ah[mt][1], ah[mt][2], ah[mt][3], bb.x, bb.y);
-        }
-      }
-    }
+    for (int kt = 0; kt < KT; ++kt) quad_mma_kt<NT>(X, Y, afr, kt, 0, lane, acc);
     __syncwarp();  // every lane's fragments are read before V overwrites X
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int o = (16 * mt + gq) * XS + 8 * nt + 2 * tq;
-        *reinterpret_cast<float2 *>(V + o) = make_float2(acc[mt][nt][0], acc[mt][nt][1]);
-        *reinterpret_cast<float2 *>(V + o + 8 * XS) = make_float2(acc[mt][nt][2], acc[mt][nt][3]);
-      }
+    quad_store_v(V, acc, lane);
     __syncwarp();
     // ---- four serial chains (one per quarter): lane l holds columns 4l .. 4l+3 ----
     const int nbmax = __reduce_max_sync(FULL, (unsigned)nb);
-    const float *Vq = V + 8 * q * XS + 4 * l;
+    const float *Vq = V + 8 * q * QVS + 4 * l;
     const float4 *mq = meta + q * MQ;
 #pragma unroll
     for (int k = 0; k < QB; ++k) {
       if (k >= nbmax) break;
-      const float4 v = *reinterpret_cast<const float4 *>(Vq + k * XS);
-      float2 pr = fmul2(make_float2(a[0], a[1]), make_float2(v.x, v.y));
-      pr = ffma2(make_float2(a[2], a[3]), make_float2(v.z, v.w), pr);
-      float s = pr.x + pr.y;
-      s += __shfl_xor_sync(FULL, s, 4);
-      s += __shfl_xor_sync(FULL, s, 2);
-      s += __shfl_xor_sync(FULL, s, 1);
-      const float4 m = mq[k];  // (x, lr, -lr reg, -lr reg); lr = 0 on padding steps
-      const float e = m.x - s;
-      const float lre = m.y * e;
-      // a <- a + (-lr reg) a  (the decay, never through a rounded 1 - lr reg), then a += lr e v
-      const float2 a01 = ffma2(make_float2(m.z, m.w), make_float2(a[0], a[1]), make_float2(a[0], a[1]));
-      const float2 a23 = ffma2(make_float2(m.z, m.w), make_float2(a[2], a[3]), make_float2(a[2], a[3]));
-      a[0] = __fmaf_rn(lre, v.x, a01.x);
-      a[1] = __fmaf_rn(lre, v.y, a01.y);
-      a[2] = __fmaf_rn(lre, v.z, a23.x);
-      a[3] = __fmaf_rn(lre, v.w, a23.y);
+      quad_chain_step(a, Vq + k * QVS, mq[k]);
     }
     __syncwarp();  // V / meta reads done before the next batch's gathers and meta stores
     cL0 += nb;
   }
+}
+
+// ---- K3b "quadp": the quad layout software-pipelined for FEW LONG ROWS --------------------
+// Netflix mode 2 has 2,182 rows of ~45 K serial updates: four rows per warp leave ~3.7 warps
+// per SM, too few to hide the gather -> MMA -> chain latencies by switching warps.  quadp
+// overlaps them inside each warp instead: in iteration t the warp
+//     issues the gathers of batch t+2 (double-buffered X/Y tiles),
+//     runs the chain of batch t (V tile, meta) INTERLEAVED step by step with the tensor-core
+//     combine of batch t+1 (registers), so the MMAs fill the shuffle latency of the chain,
+//     then stores V(t+1).
+// The per-quarter batch records (row, leaf range, row-start flag) run three batches ahead of
+// the chain; a row's A values are prefetched one batch before its first update and written
+// back after its last.  Arithmetic and order of updates are exactly those of `quad`.
+namespace quadp {
+constexpr int WPB = 4;
+constexpr int WARP_FLOATS = 5 * quad::TILE + 4 * quad::MQ * 4;  // X[2], Y[2], V, meta
+constexpr size_t bytes() { return (size_t)quad::BFRAG_U4 * 16 + (size_t)WPB * WARP_FLOATS * 4; }
+
+struct Cursor {   // a quarter's position in its row stream (replicated in its 8 lanes)
+  int64_t row;    // current row (stream index)
+  int i, L0, Le;  // current row coordinate (-1: none) and remaining leaf range
+  int ni, nLb, nLe;  // the stream's next row, loaded one row ahead (ni < 0: none)
+};
+struct Rec {      // one quarter batch
+  int nb, i, L0;
+  bool newrow;    // first batch of row i
+};
+
+__device__ __forceinline__ void load_row_info(const SweepParams &p, int64_t r, int &i, int &lb,
+                                              int &le) {
+  if (r < p.nrows) {
+    i = __ldg(p.row_coord + r);
+    lb = __ldg(p.row_leaf_ptr + r);
+    le = __ldg(p.row_leaf_ptr + r + 1);
+  } else {
+    i = -1, lb = le = 0;
+  }
+}
+
+__device__ __forceinline__ Rec next_batch(const SweepParams &p, Cursor &c, int64_t nstream) {
+  Rec r;
+  r.newrow = false;
+  if (c.L0 >= c.Le) {
+    if (c.ni < 0) {
+      r.nb = 0, r.i = -1, r.L0 = 0;
+      c.i = -1;
+      return r;
+    }
+    c.row += nstream;
+    c.i = c.ni, c.L0 = c.nLb, c.Le = c.nLe;
+    r.newrow = true;
+    load_row_info(p, c.row + nstream, c.ni, c.nLb, c.nLe);
+  }
+  r.i = c.i, r.L0 = c.L0, r.nb = min(quad::QB, c.Le - c.L0);
+  c.L0 += r.nb;
+  return r;
+}
+
+struct Leaf {
+  int lc, pc;
+  float x;
+};
+__device__ __forceinline__ Leaf load_leaf(const SweepParams &p, const Rec &r, int l) {
+  Leaf d{0, 0, 0.f};
+  if (l < r.nb) {
+    d.lc = __ldcs(p.leaf_coord + r.L0 + l);
+    d.pc = __ldcs(p.leaf_pc + r.L0 + l);
+    d.x = __ldcs(p.vals + r.L0 + l);
+  }
+  return d;
+}
+}  // namespace quadp
+
+__global__ void __launch_bounds__(quadp::WPB * 32, 1) factor_rows_quadp_kernel(const SweepParams p) {
+  using namespace quad;
+  using quadp::Rec;
+  using quadp::Leaf;
+  extern __shared__ float4 smem4[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int q = lane >> 3, l = lane & 7;
+  const int gq = lane >> 2, tq = lane & 3;
+  uint4 *afr = reinterpret_cast<uint4 *>(smem4);
+  float *base = reinterpret_cast<float *>(afr + BFRAG_U4) + w * quadp::WARP_FLOATS;
+  // tiles: X[set] = base + set * TILE, Y[set] = base + (2 + set) * TILE, V = base + 4 TILE
+  float *V = base + 4 * TILE;
+  float4 *meta = reinterpret_cast<float4 *>(base + 5 * TILE);
+  for (int k = lane; k < 4 * TILE; k += 32) base[k] = 0.f;
+  quad_afrag_init(p, afr);
+  __syncthreads();
+
+  const int64_t nstream = (int64_t)gridDim.x * quadp::WPB * 4;
+  quadp::Cursor cur;
+  cur.row = ((int64_t)blockIdx.x * quadp::WPB + w) * 4 + q - nstream;  // before the first row
+  cur.i = -1, cur.L0 = cur.Le = 0;
+  quadp::load_row_info(p, cur.row + nstream, cur.ni, cur.nLb, cur.nLe);
+  const int J = p.J;
+  const bool j32 = J == 32;
+  auto load_a = [&](int i, float (&a)[4]) {
+    const float *ar = p.A + (int64_t)i * J;
+    if (j32) {
+      const float4 v = *reinterpret_cast<const float4 *>(ar + 4 * l);
+      a[0] = v.x, a[1] = v.y, a[2] = v.z, a[3] = v.w;
+    } else {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) a[t] = 4 * l + t < J ? ar[4 * l + t] : 0.f;
+    }
+  };
+  auto store_a = [&](int i, const float (&a)[4]) {
+    float *ar = p.A + (int64_t)i * J;
+    if (j32) {
+      *reinterpret_cast<float4 *>(ar + 4 * l) = make_float4(a[0], a[1], a[2], a[3]);
+    } else {
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (4 * l + t < J) ar[4 * l + t] = a[t];
+    }
+  };
+  const int gc = lane & 7, gs = lane >> 3;
+  const bool gok = gc < (p.R >> 2);
+  const float *cpre = p.Cpre[0] + 4 * gc, *cleaf = p.Cleaf + 4 * gc;
+  const int64_t Rs = p.R;
+  auto gather = [&](int set, const Leaf &d) {
+    const uint32_t xs = smem_u32(base + set * TILE + gs * XS + 4 * gc);
+    const uint32_t ys = smem_u32(base + (2 + set) * TILE + gs * XS + 4 * gc);
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int s = 4 * it + gs;
+      const int pcs = __shfl_sync(FULL, d.pc, s), lcs = __shfl_sync(FULL, d.lc, s);
+      if (gok) {
+        cp_async16_s(xs + it * 4 * XS * 4, cpre + pcs * Rs);
+        cp_async16_s(ys + it * 4 * XS * 4, cleaf + lcs * Rs);
+      }
+    }
+    cp_async_commit();
+  };
+  auto put_meta = [&](const Rec &r, float x) {
+    const float lrk = l < r.nb ? p.lr : 0.f;
+    const float ck = -lrk * p.reg;
+    meta[q * MQ + l] = make_float4(l < r.nb ? x : 0.f, lrk, ck, ck);
+  };
+
+  // ---- prologue: records of batches 0..2, gathers of 0 and 1, V(0) ----
+  Rec r0 = quadp::next_batch(p, cur, nstream);
+  const Leaf d0 = quadp::load_leaf(p, r0, l);
+  Rec r1 = quadp::next_batch(p, cur, nstream);
+  Leaf d1 = quadp::load_leaf(p, r1, l);
+  Rec r2 = quadp::next_batch(p, cur, nstream);
+  Leaf d2 = quadp::load_leaf(p, r2, l);
+  gather(0, d0);
+  gather(1, d1);
+  float a[4] = {0.f, 0.f, 0.f, 0.f}, an[4] = {0.f, 0.f, 0.f, 0.f};
+  int ai = r0.nb > 0 ? r0.i : -1;  // row whose values a holds
+  if (ai >= 0) load_a(ai, a);
+  if (r1.newrow && r1.nb > 0) load_a(r1.i, an);
+  float acc[2][4][4];
+  {
+    cp_async_wait_one();
+    __syncwarp();
+    quad_zero(acc);
+#pragma unroll
+    for (int kt = 0; kt < KT; ++kt) quad_mma_kt<NT>(base, base + 2 * TILE, afr, kt, 0, lane, acc);
+    __syncwarp();
+    quad_store_v(V, acc, lane);
+    put_meta(r0, d0.x);
+    __syncwarp();
+  }
+  float x1 = d1.x;
+
+  for (int t = 0; __any_sync(FULL, r0.nb > 0); ++t) {
+    const int s1 = (t + 1) & 1;  // tile set of batch t+1 (batch t+2 reuses set t & 1)
+    gather(t & 1, d2);
+    const Rec r3 = quadp::next_batch(p, cur, nstream);
+    const Leaf d3 = quadp::load_leaf(p, r3, l);
+    cp_async_wait_one();  // batch t+1's tiles have landed
+    __syncwarp();
+    // ---- chain of batch t interleaved with the combine of batch t+1 ----
+    const float *Xs = base + s1 * TILE, *Ys = base + (2 + s1) * TILE;
+    const float *Vq = V + 8 * q * QVS + 4 * l;
+    const float4 *mq = meta + q * MQ;
+    quad_zero(acc);
+#pragma unroll
+    for (int k = 0; k < QB; ++k) {
+      quad_chain_step(a, Vq + k * QVS, mq[k]);
+      quad_mma_kt<2>(Xs, Ys, afr, k >> 1, 2 * (k & 1), lane, acc);
+    }
+    __syncwarp();  // chain(t) done reading V / meta
+    quad_store_v(V, acc, lane);
+    put_meta(r1, x1);
+    // row hand-over: batch t+1 starts a new row -> write back the finished one, swap in its
+    // prefetched values; then prefetch the row batch t+2 starts (if it starts one)
+    if (r1.newrow && r1.nb > 0) {
+      if (ai >= 0) store_a(ai, a);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] = an[u];
+      ai = r1.i;
+    } else if (r1.nb == 0 && ai >= 0) {
+      store_a(ai, a);  // stream exhausted after batch t
+      ai = -1;
+    }
+    if (r2.newrow && r2.nb > 0) load_a(r2.i, an);
+    __syncwarp();
+    r0 = r1, r1 = r2, r2 = r3;
+    x1 = d2.x;
+    d2 = d3;
+  }
+  cp_async_wait_all();
+  if (ai >= 0) store_a(ai, a);
+}
+
+int launch_quadp(const SweepParams &q, cudaStream_t s) {
+  const size_t sm = quadp::bytes();
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(factor_rows_quadp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
+    set = true;
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quadp_kernel,
+                                                    quadp::WPB * 32, sm) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  int64_t g = (q.nrows + 4 * quadp::WPB - 1) / (4 * quadp::WPB);
+  const int64_t cap = (int64_t)sm_count() * per_sm;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  factor_rows_quadp_kernel<<<(int)g, quadp::WPB * 32, sm, s>>>(q);
+  return check_launch("ft_factor_sweep_rows(quadp)");
 }
 
 int launch_quad(const SweepParams &q, cudaStream_t s) {

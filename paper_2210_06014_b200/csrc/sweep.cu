@@ -1926,6 +1926,7 @@ int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
     if (e && strcmp(e, "rdual") == 0) return 6;
     if (e && strcmp(e, "ws") == 0) return 7;
     if (e && strcmp(e, "quad") == 0) return 8;
+    if (e && strcmp(e, "quadp") == 0) return 9;
     return 5;  // auto: dual when the rows fill the SMs, gram otherwise
   }();
   int variant = chosen;
@@ -1938,14 +1939,16 @@ int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
   if (variant == 7 && p.N != 3) variant = 5;  // ws: order-3 tensors (one prefix row)
   // auto, by rows per resident warp slot: many rows -> dual (Netflix modes 0/1: 7.5 ms);
   // few long rows -> warp-specialised at order 3 (mode 2: 8.4 vs 8.8 gram, 13.4 dual), else gram
-  if (variant == 8 && !quad_ok(p)) variant = 5;  // quad: order 3, 16 < J <= 32, leaf index
+  // quad / quadp: order 3, 16 < J <= 32, leaf-major index
+  if ((variant == 8 || variant == 9) && !(RP == 32 && quad_ok(p))) variant = 5;
   if (variant == 5) {
-    if (RP == 32 && quad_ok(p) && p.nrows >= (int64_t)2 * sm_count() * quad::WPB * 4)
-      variant = 8;
+    if (RP == 32 && quad_ok(p))  // many rows: quad; few long rows: quadp (in-warp pipeline)
+      variant = p.nrows >= (int64_t)2 * sm_count() * quad::WPB * 4 ? 8 : 9;
     else
       variant = p.nrows >= (int64_t)2 * sm_count() * 16 ? 4 : (p.N == 3 ? 7 : 0);
   }
   if (variant == 8) return launch_quad(q, s);
+  if (variant == 9) return launch_quadp(q, s);
   if (variant == 6) {
     const size_t sm = RDualPlan::bytes<RP>();
     static bool set6 = false;

@@ -3,7 +3,8 @@
 
 `quad` is what `auto` runs on order-3 sweeps with 16 < J <= 32 and enough rows (Netflix modes
 0 and 1); these cases force it (FT_FACTOR_KERNEL=quad, in a subprocess because the variant is
-latched at the first launch) on shapes that exercise its edges: rows shorter than one 8-leaf
+latched at the first launch), and so is `quadp`, its in-warp software-pipelined form for few
+long rows (Netflix mode 2), on shapes that exercise its edges: rows shorter than one 8-leaf
 batch, rows of ~20 K serial updates, J < 32 and R < 32 padding, more rows than row slots.
 """
 
@@ -93,9 +94,10 @@ print('ok')
     ((20000, 700, 9), 300_000, 24, 20, 1e-3),     # J < 32, R < 32 (padding), 1-3 leaf rows
     ((60000, 64, 64), 200_000, 32, 32, 5e-3),     # more rows than row slots (row switching)
 ])
-def test_quad_sweeps_match_oracle(dims, nnz, J, R, lr):
+@pytest.mark.parametrize("kernel", ["quad", "quadp"])
+def test_quad_sweeps_match_oracle(kernel, dims, nnz, J, R, lr):
     code = _CASE.format(dims=dims, nnz=nnz, J=J, R=R, lr=lr, seed=7)
-    env = dict(os.environ, FT_FACTOR_KERNEL="quad")
+    env = dict(os.environ, FT_FACTOR_KERNEL=kernel)
     out = subprocess.run([sys.executable, "-c", code], cwd=REPO, env=env, capture_output=True,
                          text=True, timeout=900)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]

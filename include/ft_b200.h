@@ -68,6 +68,12 @@ typedef struct {
    * plain coalesced loads instead of the fiber-window ballot -> fiber_coord dependent chain. */
   const int32_t *leaf_pc;       /* [nnz]   level-1 coordinate of each leaf's fiber           */
   const int32_t *row_leaf_ptr;  /* [rows+1] first leaf of each root slice                    */
+  /* Row segments for the core sweep (optional): every root slice cut into pieces of at most
+   * `max_len` leaves (ft_tree_row_segments).  The core gradient is a sum over a row's leaves,
+   * so pieces of one row may run on different warps; the factor sweep never uses them. */
+  int64_t num_segs;
+  const int32_t *seg_coord;     /* [segs]  row coordinate of each segment                    */
+  const int32_t *seg_leaf_ptr;  /* [segs+1] first leaf of each segment                       */
 } ft_tree_t;
 
 /* Model parameters and the C^(n) cache (model.py:45-103, cache.py:28-57). */
@@ -113,6 +119,12 @@ FT_API int ft_build_tree(int32_t N, int64_t nnz, const int64_t *dims, const int3
  * Either output may be NULL.  Asynchronous. */
 FT_API int ft_tree_leaf_index(const ft_tree_t *tree, int32_t *leaf_pc, int32_t *row_leaf_ptr,
                               void *stream);
+/* K1c Row segments (reads tree->row_coord / row_leaf_ptr): root slice r becomes
+ * ceil(len_r / max_len) consecutive segments of <= max_len leaves.  Output capacity: rows +
+ * nnz / max_len + 1 entries for seg_coord, one more for seg_leaf_ptr.  *nseg_out (HOST) gets the
+ * segment count.  SYNCHRONOUS (the count is read back). */
+FT_API int ft_tree_row_segments(const ft_tree_t *tree, int32_t max_len, int32_t *seg_coord,
+                                int32_t *seg_leaf_ptr, int64_t *nseg_out, void *stream);
 /* K2  C = A * Bt^T  (I x R), i.e. refresh_dot_mode (_ckern.pyx:21-33, cache.py:60-70), with the
  * divergence guard of train.py:101-110 fused: if guard != NULL, atomically max-es the IEEE bits
  * of |A| into guard[0] (NaN sorts above +inf, so one word detects both cases). */

@@ -47,6 +47,9 @@ class FtTree(ctypes.Structure):
         ("row_coord", _vp),
         ("leaf_pc", _vp),
         ("row_leaf_ptr", _vp),
+        ("num_segs", ctypes.c_int64),
+        ("seg_coord", _vp),
+        ("seg_leaf_ptr", _vp),
     ]
 
 
@@ -73,6 +76,8 @@ SIGNATURES = {
         ctypes.c_int32, ctypes.c_int64, _i64p, _vp, _vp, ctypes.c_int32, ctypes.c_int64, _vp,
         ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp, _vp, _vp, _vp, _vp, _vp, _i64p, _vp]),
     "ft_tree_leaf_index": (ctypes.c_int, [ctypes.POINTER(FtTree), _vp, _vp, _vp]),
+    "ft_tree_row_segments": (ctypes.c_int, [ctypes.POINTER(FtTree), ctypes.c_int32, _vp, _vp,
+                                            _i64p, _vp]),
     "ft_refresh": (ctypes.c_int, [
         ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp, _vp, _vp]),
     "ft_refresh_scatter": (ctypes.c_int, [

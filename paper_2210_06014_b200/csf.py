@@ -26,6 +26,7 @@ from .coo import as_device
 from .errors import BuildError, ConfigError
 
 DEFAULT_FIBER_THRESHOLD = 128
+CORE_SEGMENT = 512  # max leaves per core-sweep row segment
 
 
 @dataclass
@@ -44,6 +45,8 @@ class CsfTree:
     row_coord: object      # device int32 [rows]
     leaf_pc: object = None       # device int32 [nnz]  level-1 coordinate per leaf (derived)
     row_leaf_ptr: object = None  # device int32 [rows+1] first leaf per row (derived)
+    seg_coord: object = None     # device int32 [segs]  core-sweep row segments (derived)
+    seg_leaf_ptr: object = None  # device int32 [segs+1]
     _view: object = field(default=None, repr=False)
     num_subtensors_built: int = -1
 
@@ -98,6 +101,9 @@ class CsfTree:
             v.row_coord = self.row_coord.data_ptr()
             v.leaf_pc = _lib.ptr(self.leaf_pc)
             v.row_leaf_ptr = _lib.ptr(self.row_leaf_ptr)
+            v.num_segs = 0 if self.seg_coord is None else int(self.seg_coord.shape[0])
+            v.seg_coord = _lib.ptr(self.seg_coord)
+            v.seg_leaf_ptr = _lib.ptr(self.seg_leaf_ptr)
             self._view = v
         return self._view
 
@@ -128,7 +134,7 @@ class CsfTree:
         l1 = int(self.fiber_ptr[f1])
         empty = torch.empty(0, dtype=torch.int32, device=self.vals.device)
         inds = tuple(empty for _ in range(self.order - 1)) + (self.leaf_coord[l0:l1].clone(),)
-        return CsfTree(
+        out = CsfTree(
             root_mode=self.root_mode, level_modes=self.level_modes, dims=self.dims,
             inds=inds, ptrs=tuple(empty for _ in self.ptrs),
             vals=self.vals[l0:l1].clone(),
@@ -142,6 +148,7 @@ class CsfTree:
             row_leaf_ptr=None if self.row_leaf_ptr is None
             else (self.row_leaf_ptr[r0:r1 + 1] - l0).contiguous(),
         )
+        return out if out.row_leaf_ptr is None or out.num_rows == 0 else add_row_segments(out)
 
 
 @dataclass
@@ -254,6 +261,30 @@ def add_leaf_index(tree: CsfTree, stream=None) -> CsfTree:
     _lib.check(_lib.lib().ft_tree_leaf_index(ctypes.byref(v), tree.leaf_pc.data_ptr(),
                                              tree.row_leaf_ptr.data_ptr(),
                                              _lib.stream_handle(stream)), "ft_tree_leaf_index")
+    tree._view = None
+    return add_row_segments(tree, stream)
+
+
+def add_row_segments(tree: CsfTree, stream=None) -> CsfTree:
+    """Core-sweep row segments (K1c, ft_tree_row_segments): rows cut at CORE_SEGMENT leaves so
+    few long rows still fill the GPU in the core sweep (a sum over each row's leaves, so the
+    pieces are independent).  Needs ``row_leaf_ptr``."""
+    import torch
+
+    i32 = dict(dtype=torch.int32, device=tree.vals.device)
+    tree._view = None
+    rows = tree.num_rows
+    cap = rows + tree.nnz // CORE_SEGMENT + 1
+    seg_coord = torch.empty(cap, **i32)
+    seg_ptr = torch.empty(cap + 1, **i32)
+    nseg = np.zeros(1, dtype=np.int64)
+    _lib.check(_lib.lib().ft_tree_row_segments(
+        ctypes.byref(tree.view()), CORE_SEGMENT, seg_coord.data_ptr(), seg_ptr.data_ptr(),
+        nseg.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), _lib.stream_handle(stream)),
+        "ft_tree_row_segments")
+    n = int(nseg[0])
+    tree.seg_coord = _trim(seg_coord, n)
+    tree.seg_leaf_ptr = _trim(seg_ptr, n + 1)
     tree._view = None
     return tree
 

@@ -185,6 +185,26 @@ __global__ void leaf_pc_kernel(const int32_t *__restrict__ fiber_ptr,
   }
 }
 
+__global__ void seg_count_kernel(const int32_t *__restrict__ rlp, int64_t rows, int max_len,
+                                 int32_t *__restrict__ cnt) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < rows) cnt[r] = (__ldg(rlp + r + 1) - __ldg(rlp + r) + max_len - 1) / max_len;
+}
+
+__global__ void seg_fill_kernel(const int32_t *__restrict__ rlp, const int32_t *__restrict__ rc,
+                                const int32_t *__restrict__ off, int64_t rows, int max_len,
+                                int32_t *__restrict__ seg_coord, int32_t *__restrict__ seg_ptr) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const int lb = __ldg(rlp + r), le = __ldg(rlp + r + 1), c = __ldg(rc + r);
+  int o = __ldg(off + r);
+  for (int L = lb; L < le; L += max_len, ++o) {
+    seg_coord[o] = c;
+    seg_ptr[o] = L;
+  }
+  if (r == rows - 1) seg_ptr[o] = le;
+}
+
 __global__ void row_leaf_ptr_kernel(const int32_t *__restrict__ fiber_ptr,
                                     const int32_t *__restrict__ row_fiber_ptr, int64_t rows,
                                     int32_t *__restrict__ out) {
@@ -441,5 +461,39 @@ extern "C" int ft_tree_leaf_index(const ft_tree_t *tree, int32_t *leaf_pc, int32
                                                              row_leaf_ptr);
     if (int rc = check_launch("ft_tree_leaf_index(row_leaf_ptr)")) return rc;
   }
+  return FT_OK;
+}
+
+extern "C" int ft_tree_row_segments(const ft_tree_t *tree, int32_t max_len, int32_t *seg_coord,
+                                    int32_t *seg_leaf_ptr, int64_t *nseg_out, void *stream) {
+  if (!tree || !seg_coord || !seg_leaf_ptr || !nseg_out) return fail(FT_ERR_ARG, "null argument");
+  if (max_len < 1) return fail(FT_ERR_ARG, "max_len %d < 1", max_len);
+  if (!tree->row_leaf_ptr || !tree->row_coord) return fail(FT_ERR_ARG, "tree has no row index");
+  cudaStream_t s = as_stream(stream);
+  const int64_t rows = tree->num_rows;
+  if (rows == 0) {
+    *nseg_out = 0;
+    FT_CUDA(cudaMemsetAsync(seg_leaf_ptr, 0, sizeof(int32_t), s));
+    FT_CUDA(cudaStreamSynchronize(s));
+    return FT_OK;
+  }
+  Scratch sc(s);
+  int32_t *cnt = sc.get<int32_t>(rows + 1), *off = sc.get<int32_t>(rows + 1);
+  if (!cnt || !off) return fail(FT_ERR_CUDA, "scratch allocation failed");
+  seg_count_kernel<<<blocks_for(rows), 256, 0, s>>>(tree->row_leaf_ptr, rows, max_len, cnt);
+  if (int rc = check_launch("ft_tree_row_segments(count)")) return rc;
+  FT_CUDA(cudaMemsetAsync(cnt + rows, 0, sizeof(int32_t), s));
+  size_t tb = 0;
+  FT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, rows + 1, s));
+  void *tmp = sc.get<uint8_t>(tb);
+  if (!tmp) return fail(FT_ERR_CUDA, "scratch allocation failed");
+  FT_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, off, rows + 1, s));
+  seg_fill_kernel<<<blocks_for(rows), 256, 0, s>>>(tree->row_leaf_ptr, tree->row_coord, off, rows,
+                                                   max_len, seg_coord, seg_leaf_ptr);
+  if (int rc = check_launch("ft_tree_row_segments(fill)")) return rc;
+  int32_t total = 0;
+  FT_CUDA(cudaMemcpyAsync(&total, off + rows, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  FT_CUDA(cudaStreamSynchronize(s));
+  *nseg_out = total;
   return FT_OK;
 }

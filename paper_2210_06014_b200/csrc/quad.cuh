@@ -513,6 +513,212 @@ int launch_quadp(const SweepParams &q, cudaStream_t s) {
   return check_launch("ft_factor_sweep_rows(quadp)");
 }
 
+// ---- K3b "quadw": the quad layout warp-specialised for FEW LONG ROWS ----------------------
+// A warp GROUP owns four rows (one per 8-lane quarter of its consumer warp).  Two PRODUCER
+// warps take alternate batches: each walks the rows' batch records, gathers its batch into its
+// own X/Y tiles, runs the transposed 3xTF32 combine and publishes V, the batch's (x, lr,
+// -lr reg) and, when a quarter starts a row, that row's A values (loaded a batch ahead) into an
+// NS-stage shared-memory ring (mbarrier full / empty).  The CONSUMER warp only runs the four
+// serial chains (quad arithmetic and order), so the chain -- the only serial work -- never
+// waits on a gather or an MMA.  (One producer was the bottleneck: ncu showed its 96 HMMA per
+// batch at ~9 cycles each plus the gather wait, 2.3 K cycles per batch vs ~1 K for the chain.)
+// Netflix mode 2: 2,182 rows of ~45 K updates -> 546 groups, ~3.7 per SM.
+namespace quadw {
+constexpr int NS = 4;   // ring stages (producer k writes stages k, k+2)
+constexpr int NP = 2;   // producers per group
+constexpr int STAGE_FLOATS = 32 * quad::QVS + 4 * quad::MQ * 4 + 4 * 4 + 4 * 32;  // V, meta, info, A
+constexpr int GROUP_FLOATS = NS * STAGE_FLOATS + NP * 2 * quad::TILE;  // ring + X, Y per producer
+constexpr int BAR_BYTES = 2 * NS * 8 + 16;
+constexpr int THREADS = (NP + 1) * 32;
+constexpr size_t bytes() {
+  return (size_t)quad::BFRAG_U4 * 16 + BAR_BYTES + (size_t)GROUP_FLOATS * 4;
+}
+}  // namespace quadw
+
+__global__ void __launch_bounds__(quadw::THREADS, 1) factor_rows_quadw_kernel(const SweepParams p) {
+  using namespace quad;
+  using quadp::Leaf;
+  using quadp::Rec;
+  extern __shared__ float4 smem4[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;  // w 0: consumer, 1..NP: producers
+  const int q = lane >> 3, l = lane & 7;
+  uint4 *afr = reinterpret_cast<uint4 *>(smem4);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(afr + BFRAG_U4);
+  uint64_t *full = bars, *empty = bars + quadw::NS;
+  float *ring = reinterpret_cast<float *>(reinterpret_cast<char *>(afr + BFRAG_U4) +
+                                          quadw::BAR_BYTES);
+  if (w > 0) {
+    float *tiles = ring + quadw::NS * quadw::STAGE_FLOATS + (w - 1) * 2 * TILE;
+    for (int k = lane; k < 2 * TILE; k += 32) tiles[k] = 0.f;
+  }
+  if (threadIdx.x == 0)
+    for (int st = 0; st < quadw::NS; ++st) {
+      mbar_init(full + st, 32);
+      mbar_init(empty + st, 32);
+    }
+  quad_afrag_init(p, afr);
+  __syncthreads();
+  const int64_t nstream = (int64_t)gridDim.x * 4;
+  const int J = p.J;
+  const bool j32 = J == 32;
+  // stage layout: V [32][QVS] | meta float4 [4][MQ] | info int4 [4] | A rows [4][32]
+  auto stage_v = [&](int st) { return ring + st * quadw::STAGE_FLOATS; };
+  auto stage_meta = [&](int st) {
+    return reinterpret_cast<float4 *>(ring + st * quadw::STAGE_FLOATS + 32 * QVS);
+  };
+  auto stage_info = [&](int st) {
+    return reinterpret_cast<int4 *>(ring + st * quadw::STAGE_FLOATS + 32 * QVS + 4 * MQ * 4);
+  };
+  auto stage_a = [&](int st) {
+    return ring + st * quadw::STAGE_FLOATS + 32 * QVS + 4 * MQ * 4 + 16;
+  };
+
+  if (w > 0) {
+    // ===================================== producers =====================================
+    const int k = w - 1;  // this producer runs batches t = k, k + NP, ...
+    float *X = ring + quadw::NS * quadw::STAGE_FLOATS + k * 2 * TILE, *Y = X + TILE;
+    quadp::Cursor cur;
+    cur.row = (int64_t)blockIdx.x * 4 + q - nstream;
+    cur.i = -1, cur.L0 = cur.Le = 0;
+    quadp::load_row_info(p, cur.row + nstream, cur.ni, cur.nLb, cur.nLe);
+    const int gc = lane & 7, gs = lane >> 3;
+    const bool gok = gc < (p.R >> 2);
+    const float *cpre = p.Cpre[0] + 4 * gc, *cleaf = p.Cleaf + 4 * gc;
+    const int64_t Rs = p.R;
+    const uint32_t xs = smem_u32(X + gs * XS + 4 * gc), ys = smem_u32(Y + gs * XS + 4 * gc);
+    auto gather = [&](const Leaf &d) {
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int s = 4 * it + gs;
+        const int pcs = __shfl_sync(FULL, d.pc, s), lcs = __shfl_sync(FULL, d.lc, s);
+        if (gok) {
+          cp_async16_s(xs + it * 4 * XS * 4, cpre + pcs * Rs);
+          cp_async16_s(ys + it * 4 * XS * 4, cleaf + lcs * Rs);
+        }
+      }
+      cp_async_commit();
+    };
+    auto load_arow = [&](const Rec &r) {  // A values of a row about to start (quarter lanes)
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r.newrow && r.nb > 0) {
+        const float *ar = p.A + (int64_t)r.i * J;
+        if (j32) {
+          v = *reinterpret_cast<const float4 *>(ar + 4 * l);
+        } else {
+          v.x = 4 * l < J ? ar[4 * l] : 0.f;
+          v.y = 4 * l + 1 < J ? ar[4 * l + 1] : 0.f;
+          v.z = 4 * l + 2 < J ? ar[4 * l + 2] : 0.f;
+          v.w = 4 * l + 3 < J ? ar[4 * l + 3] : 0.f;
+        }
+      }
+      return v;
+    };
+    // the record of my next batch: skip the other producer's batches (row-start flags carry
+    // over a skipped batch only if it started a row and mine continues it -- then mine is not
+    // the row's first batch, which is what the consumer needs)
+    auto next_mine = [&](bool first) {
+      if (!first)
+        for (int s = 0; s < quadw::NP - 1; ++s) (void)quadp::next_batch(p, cur, nstream);
+      return quadp::next_batch(p, cur, nstream);
+    };
+    for (int s = 0; s < k; ++s) (void)quadp::next_batch(p, cur, nstream);
+    Rec r0 = next_mine(true);
+    Leaf d0 = quadp::load_leaf(p, r0, l);
+    float4 av0 = load_arow(r0);
+    float acc[2][4][4];
+    for (int t = k;; t += quadw::NP) {
+      const bool stop = !__any_sync(FULL, r0.nb > 0);
+      if (!stop) gather(d0);
+      const Rec r1 = next_mine(false);  // my next batch: indices and A values fly meanwhile
+      const Leaf d1 = quadp::load_leaf(p, r1, l);
+      const float4 av1 = load_arow(r1);
+      if (!stop) {
+        cp_async_wait_all();
+        __syncwarp();
+        quad_zero(acc);
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt) quad_mma_kt<NT>(X, Y, afr, kt, 0, lane, acc);
+      }
+      const int st = t % quadw::NS;
+      if (t >= quadw::NS) mbar_wait(empty + st, ((t / quadw::NS) - 1) & 1);
+      int4 *info = stage_info(st);
+      if (!stop) {
+        quad_store_v(stage_v(st), acc, lane);
+        const float lrk = l < r0.nb ? p.lr : 0.f;
+        const float ck = -lrk * p.reg;
+        stage_meta(st)[q * MQ + l] = make_float4(l < r0.nb ? d0.x : 0.f, lrk, ck, ck);
+        if (r0.newrow) *reinterpret_cast<float4 *>(stage_a(st) + 32 * q + 4 * l) = av0;
+        if (l == 0) info[q] = make_int4(r0.nb, r0.newrow ? 1 : 0, r0.i, 0);
+      } else if (l == 0) {
+        info[q] = make_int4(0, 0, -1, 1);  // stop
+      }
+      __syncwarp();
+      mbar_arrive(full + st);
+      if (stop) break;
+      r0 = r1, d0 = d1, av0 = av1;
+    }
+    cp_async_wait_all();
+  } else {
+    // ===================================== consumer =====================================
+    float a[4] = {0.f, 0.f, 0.f, 0.f};
+    int ai = -1;
+    auto store_a = [&]() {
+      float *ar = p.A + (int64_t)ai * J;
+      if (j32) {
+        *reinterpret_cast<float4 *>(ar + 4 * l) = make_float4(a[0], a[1], a[2], a[3]);
+      } else {
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          if (4 * l + t < J) ar[4 * l + t] = a[t];
+      }
+    };
+    for (int t = 0;; ++t) {
+      const int st = t % quadw::NS;
+      mbar_wait(full + st, (t / quadw::NS) & 1);
+      const int4 info = stage_info(st)[q];
+      if (info.w) break;  // stop (every quarter carries the flag)
+      if (info.y) {       // this quarter starts row info.z
+        if (ai >= 0) store_a();
+        const float4 v = *reinterpret_cast<const float4 *>(stage_a(st) + 32 * q + 4 * l);
+        a[0] = v.x, a[1] = v.y, a[2] = v.z, a[3] = v.w;
+        ai = info.z;
+      }
+      const int nbmax = __reduce_max_sync(FULL, (unsigned)info.x);
+      const float *Vq = stage_v(st) + 8 * q * QVS + 4 * l;
+      const float4 *mq = stage_meta(st) + q * MQ;
+#pragma unroll
+      for (int kk = 0; kk < QB; ++kk) {
+        if (kk >= nbmax) break;
+        quad_chain_step(a, Vq + kk * QVS, mq[kk]);
+      }
+      __syncwarp();
+      mbar_arrive(empty + st);
+    }
+    if (ai >= 0) store_a();
+  }
+}
+
+int launch_quadw(const SweepParams &q, cudaStream_t s) {
+  const size_t sm = quadw::bytes();
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(factor_rows_quadw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
+    set = true;
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quadw_kernel,
+                                                    quadw::THREADS, sm) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  int64_t g = (q.nrows + 3) / 4;
+  const int64_t cap = (int64_t)sm_count() * per_sm;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  factor_rows_quadw_kernel<<<(int)g, quadw::THREADS, sm, s>>>(q);
+  return check_launch("ft_factor_sweep_rows(quadw)");
+}
+
 int launch_quad(const SweepParams &q, cudaStream_t s) {
   const size_t sm = quad::bytes();
   static bool set = false;
@@ -537,4 +743,219 @@ int launch_quad(const SweepParams &q, cudaStream_t s) {
 bool quad_ok(const SweepParams &p) {
   return p.N == 3 && p.leaf_pc && p.row_leaf_ptr && p.J > 16 && p.J <= 32 && p.R <= 32 &&
          (p.R & 3) == 0;
+}
+
+// ---- K4 "quad": the core-gradient row sweep over the leaf-major index ---------------------
+// Reference core_sweep (_ckern.pyx:202-269) in its row form: with A_u, Bt_u
+// frozen and C_u = A_u Bt_u^T coherent, s = A_u[i] . vec = C_u[i] . cross, and
+//     acc = -sum_i g_i (x) A_u[i],   g_i = sum_{leaves of row i} e cross.
+// Four rows per warp (quarters) as in the quad factor kernel, same gathers and index pipeline.
+// Per 32-slot batch: lane k computes s_k = sum_r X[k][r] Y[k][r] C_u[i_q][r] for its own slot
+// (conflict-free stride-36 rows, C_u row broadcast per quarter), then quarter lanes over r
+// accumulate g_q += e_k cross_k over the quarter's 8 slots.  When a row ends its g (8 lanes x 4)
+// is spread to lanes over r and the warp adds g (x) A_u[i] into per-lane accumulators
+// (lane r: acc[j]); a fixed-order block reduction writes one R x J partial per block.
+namespace cquad {
+constexpr int XS = 36;
+constexpr int TILE = 32 * XS;
+constexpr int WARP_FLOATS = 2 * TILE + 4 * 32 + 32;  // X, Y, C_u rows [4][32], e [32]
+constexpr int WPB = 8;
+constexpr size_t bytes() { return (size_t)WPB * WARP_FLOATS * 4; }
+}  // namespace cquad
+
+__global__ void __launch_bounds__(cquad::WPB * 32, 2) core_rows_quad_kernel(const SweepParams p) {
+  using namespace cquad;
+  extern __shared__ float4 smem4[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int q = lane >> 3, l = lane & 7;
+  float *X = reinterpret_cast<float *>(smem4) + w * WARP_FLOATS;
+  float *Y = X + TILE;
+  float *cus = Y + TILE;  // [4][32]
+  float *es = cus + 128;  // [32]
+  for (int k = lane; k < WARP_FLOATS; k += 32) X[k] = 0.f;
+  __syncwarp();
+  const int J = p.J, R = p.R;
+  const int64_t nstream = (int64_t)gridDim.x * cquad::WPB * 4;
+  int64_t row = ((int64_t)blockIdx.x * cquad::WPB + w) * 4 + q;
+  int ci = -1, cL0 = 0, cLe = 0, ni = -1, nLb = 0, nLe = 0;
+  if (row < p.nrows) {
+    ci = __ldg(p.row_coord + row);
+    cL0 = __ldg(p.row_leaf_ptr + row);
+    cLe = __ldg(p.row_leaf_ptr + row + 1);
+  }
+  if (row + nstream < p.nrows) {
+    ni = __ldg(p.row_coord + row + nstream);
+    nLb = __ldg(p.row_leaf_ptr + row + nstream);
+    nLe = __ldg(p.row_leaf_ptr + row + nstream + 1);
+  }
+  auto load_cu = [&](int i) {  // C_u[i, 0:R) -> cus[q][.] (zero beyond R)
+    if (4 * l < R)
+      *reinterpret_cast<float4 *>(cus + 32 * q + 4 * l) =
+          *reinterpret_cast<const float4 *>(p.Cu + (int64_t)i * R + 4 * l);
+  };
+  if (ci >= 0) load_cu(ci);
+  int plc = 0, ppc = 0;
+  float px = 0.f;
+  if (ci >= 0 && cL0 + l < cLe) {
+    plc = __ldcs(p.leaf_coord + cL0 + l);
+    ppc = __ldcs(p.leaf_pc + cL0 + l);
+    px = __ldcs(p.vals + cL0 + l);
+  }
+  float acc[FT_MAX_RANK];  // lane r: acc[j] = sum_i g_i[r] A_u[i, j]
+#pragma unroll
+  for (int j = 0; j < FT_MAX_RANK; ++j) acc[j] = 0.f;
+  float2 g01 = make_float2(0.f, 0.f), g23 = make_float2(0.f, 0.f);  // quarter lanes: g[4l..4l+3]
+  const int gc = lane & 7, gs = lane >> 3;
+  const bool gok = gc < (R >> 2);
+  const uint32_t xs0 = smem_u32(X + gs * XS + 4 * gc), ys0 = smem_u32(Y + gs * XS + 4 * gc);
+  const float *cpre = p.Cpre[0] + 4 * gc, *cleaf = p.Cleaf + 4 * gc;
+  const int64_t Rs = R;
+  const bool j32 = J == 32;
+
+  for (;;) {
+    // ---- rows that ended: acc += g (x) A_u[i] (warp-cooperative, one quarter at a time) ----
+    const bool ending = ci >= 0 && cL0 >= cLe;
+    unsigned em = __ballot_sync(FULL, ending && l == 0);
+    while (em) {
+      const int qq = __ffs(em) - 1 >> 3;
+      em &= em - 1;
+      const int src = 8 * qq + (lane >> 2), comp = lane & 3;
+      const float c0 = __shfl_sync(FULL, g01.x, src), c1 = __shfl_sync(FULL, g01.y, src);
+      const float c2 = __shfl_sync(FULL, g23.x, src), c3 = __shfl_sync(FULL, g23.y, src);
+      const float gr = comp == 0 ? c0 : comp == 1 ? c1 : comp == 2 ? c2 : c3;  // g_qq[lane]
+      const float *ar = p.A + (int64_t)__shfl_sync(FULL, ci, 8 * qq) * J;
+      if (j32) {
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) {
+          const float4 a4 = __ldg(reinterpret_cast<const float4 *>(ar) + j4);
+          acc[4 * j4] = __fmaf_rn(gr, a4.x, acc[4 * j4]);
+          acc[4 * j4 + 1] = __fmaf_rn(gr, a4.y, acc[4 * j4 + 1]);
+          acc[4 * j4 + 2] = __fmaf_rn(gr, a4.z, acc[4 * j4 + 2]);
+          acc[4 * j4 + 3] = __fmaf_rn(gr, a4.w, acc[4 * j4 + 3]);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < FT_MAX_RANK; ++j)
+          if (j < J) acc[j] = __fmaf_rn(gr, __ldg(ar + j), acc[j]);
+      }
+    }
+    if (ending) {
+      g01 = g23 = make_float2(0.f, 0.f);
+      row += nstream;
+      ci = ni, cL0 = nLb, cLe = nLe;
+      if (ci >= 0) {
+        load_cu(ci);
+        const int64_t r2 = row + nstream;
+        if (r2 < p.nrows) {
+          ni = __ldg(p.row_coord + r2);
+          nLb = __ldg(p.row_leaf_ptr + r2);
+          nLe = __ldg(p.row_leaf_ptr + r2 + 1);
+        } else {
+          ni = -1;
+        }
+      }
+    }
+    if (!__any_sync(FULL, ci >= 0)) break;
+    const int nb = ci >= 0 ? min(quad::QB, cLe - cL0) : 0;
+    const int lc = plc, pc = ppc;
+    const float x = px;
+    {  // prefetch the next batch of this quarter
+      const bool same = cL0 + nb < cLe;
+      const int pos = same ? cL0 + nb : nLb, end = same ? cLe : nLe;
+      const bool ok = ci >= 0 && (same || ni >= 0) && pos + l < end;
+      plc = ok ? __ldcs(p.leaf_coord + pos + l) : 0;
+      ppc = ok ? __ldcs(p.leaf_pc + pos + l) : 0;
+      px = ok ? __ldcs(p.vals + pos + l) : 0.f;
+    }
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int s = 4 * it + gs;
+      const int pcs = __shfl_sync(FULL, pc, s), lcs = __shfl_sync(FULL, lc, s);
+      if (gok) {
+        cp_async16_s(xs0 + it * 4 * XS * 4, cpre + pcs * Rs);
+        cp_async16_s(ys0 + it * 4 * XS * 4, cleaf + lcs * Rs);
+      }
+    }
+    cp_async_wait_all();
+    __syncwarp();
+    // ---- lane = slot: s = C_u[i_q] . (X * Y), e = x - s ----
+    {
+      const float4 *xr = reinterpret_cast<const float4 *>(X + lane * XS);
+      const float4 *yr = reinterpret_cast<const float4 *>(Y + lane * XS);
+      const float4 *cr = reinterpret_cast<const float4 *>(cus + 32 * q);
+      float2 s01 = make_float2(0.f, 0.f), s23 = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int c4 = 0; c4 < 8; ++c4) {
+        const float4 xv = xr[c4], yv = yr[c4], cv = cr[c4];
+        s01 = ffma2(fmul2(make_float2(xv.x, xv.y), make_float2(yv.x, yv.y)),
+                    make_float2(cv.x, cv.y), s01);
+        s23 = ffma2(fmul2(make_float2(xv.z, xv.w), make_float2(yv.z, yv.w)),
+                    make_float2(cv.z, cv.w), s23);
+      }
+      const float s = (s01.x + s01.y) + (s23.x + s23.y);
+      es[lane] = l < nb ? x - s : 0.f;
+    }
+    __syncwarp();
+    // ---- quarter lanes over r: g_q += sum_k e_k cross_k ----
+    {
+      const int nbmax = __reduce_max_sync(FULL, (unsigned)nb);
+      const float *xq = X + 8 * q * XS + 4 * l, *yq = Y + 8 * q * XS + 4 * l;
+#pragma unroll
+      for (int k = 0; k < quad::QB; ++k) {
+        if (k >= nbmax) break;
+        const float4 xv = *reinterpret_cast<const float4 *>(xq + k * XS);
+        const float4 yv = *reinterpret_cast<const float4 *>(yq + k * XS);
+        const float ek = es[8 * q + k];
+        const float2 e2 = make_float2(ek, ek);
+        g01 = ffma2(e2, fmul2(make_float2(xv.x, xv.y), make_float2(yv.x, yv.y)), g01);
+        g23 = ffma2(e2, fmul2(make_float2(xv.z, xv.w), make_float2(yv.z, yv.w)), g23);
+      }
+    }
+    __syncwarp();
+    cL0 += nb;
+  }
+  // ---- fixed-order block reduction -> partials[block] (reuses the staging tiles) ----
+  __syncthreads();
+  const int RJ = R * J;
+  float *red = reinterpret_cast<float *>(smem4);
+  if (lane < R) {
+#pragma unroll
+    for (int j = 0; j < FT_MAX_RANK; ++j)
+      if (j < J) red[w * WARP_FLOATS + lane * J + j] = acc[j];
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < RJ; k += blockDim.x) {
+    float s = 0.f;
+    for (int ww = 0; ww < cquad::WPB; ++ww) s += red[ww * cquad::WARP_FLOATS + k];
+    p.partials[(int64_t)blockIdx.x * RJ + k] = s;
+  }
+}
+
+bool core_quad_ok(const SweepParams &p) {
+  return p.N == 3 && p.leaf_pc && p.row_leaf_ptr && p.J <= 32 && p.R <= 32 && (p.R & 3) == 0 &&
+         p.R * p.J <= cquad::WARP_FLOATS;
+}
+
+int core_quad_grid(const SweepParams &p) {
+  const size_t sm = cquad::bytes();
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(core_rows_quad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    set = true;
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, core_rows_quad_kernel,
+                                                    cquad::WPB * 32, sm) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  int64_t g = (p.nrows + 4 * cquad::WPB - 1) / (4 * cquad::WPB);
+  const int64_t cap = (int64_t)sm_count() * per_sm;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+int launch_core_quad(const SweepParams &p, int g, cudaStream_t s) {
+  core_rows_quad_kernel<<<g, cquad::WPB * 32, cquad::bytes(), s>>>(p);
+  return check_launch("ft_core_sweep_rows(quad)");
 }

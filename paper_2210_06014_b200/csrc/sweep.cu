@@ -51,6 +51,9 @@ struct SweepParams {
   const int32_t *row_coord;
   const int32_t *leaf_pc;       // leaf-major index (optional): level-1 coordinate per leaf
   const int32_t *row_leaf_ptr;  // first leaf of each row
+  int64_t nsegs;                // core-sweep row segments (optional)
+  const int32_t *seg_coord;
+  const int32_t *seg_leaf_ptr;
   float *A;          // A_u  (I_u x J)
   const float *Bt;   // Bt_u (R x J)
   const float *Cu;   // C_u  (core sweep)
@@ -1927,6 +1930,7 @@ int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
     if (e && strcmp(e, "ws") == 0) return 7;
     if (e && strcmp(e, "quad") == 0) return 8;
     if (e && strcmp(e, "quadp") == 0) return 9;
+    if (e && strcmp(e, "quadw") == 0) return 10;
     return 5;  // auto: dual when the rows fill the SMs, gram otherwise
   }();
   int variant = chosen;
@@ -1940,7 +1944,7 @@ int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
   // auto, by rows per resident warp slot: many rows -> dual (Netflix modes 0/1: 7.5 ms);
   // few long rows -> warp-specialised at order 3 (mode 2: 8.4 vs 8.8 gram, 13.4 dual), else gram
   // quad / quadp: order 3, 16 < J <= 32, leaf-major index
-  if ((variant == 8 || variant == 9) && !(RP == 32 && quad_ok(p))) variant = 5;
+  if ((variant == 8 || variant == 9 || variant == 10) && !(RP == 32 && quad_ok(p))) variant = 5;
   if (variant == 5) {
     if (RP == 32 && quad_ok(p))  // many rows: quad; few long rows: quadp (in-warp pipeline)
       variant = p.nrows >= (int64_t)2 * sm_count() * quad::WPB * 4 ? 8 : 9;
@@ -1949,6 +1953,7 @@ int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
   }
   if (variant == 8) return launch_quad(q, s);
   if (variant == 9) return launch_quadp(q, s);
+  if (variant == 10) return launch_quadw(q, s);
   if (variant == 6) {
     const size_t sm = RDualPlan::bytes<RP>();
     static bool set6 = false;
@@ -2023,6 +2028,9 @@ int fill_rows_params(SweepParams &p, const ft_tree_t *tree, const ft_model_t *m)
   p.row_coord = tree->row_coord;
   p.leaf_pc = tree->leaf_pc;
   p.row_leaf_ptr = tree->row_leaf_ptr;
+  p.nsegs = tree->seg_coord && tree->seg_leaf_ptr ? tree->num_segs : 0;
+  p.seg_coord = tree->seg_coord;
+  p.seg_leaf_ptr = tree->seg_leaf_ptr;
   p.A = m->factors[u];
   p.Bt = m->cores_t[u];
   p.Cu = m->dots[u];
@@ -2069,13 +2077,31 @@ extern "C" int ft_core_sweep_rows(const ft_tree_t *tree, const ft_model_t *model
   if (!p.Cu) return fail(FT_ERR_ARG, "core sweep needs dots[u] (coherent cache)");
   if (!partials || !nblocks_out) return fail(FT_ERR_ARG, "null partials");
   p.partials = partials;
-  const int g = p.R <= 8 ? core_rows_grid<8>(p) : p.R <= 16 ? core_rows_grid<16>(p)
-                                                            : core_rows_grid<32>(p);
+  // FT_CORE_KERNEL=rows forces the one-row-per-warp kernel; default: quad when it applies
+  static const bool core_rows_forced = [] {
+    const char *e = getenv("FT_CORE_KERNEL");
+    return e && strcmp(e, "rows") == 0;
+  }();
+  // quad walks the row SEGMENTS (rows cut at <= 512 leaves: the core gradient is a sum over a
+  // row's leaves), so few long rows fill the GPU too (Netflix mode 2: 2,182 rows -> 89 K
+  // segments); without segments it needs rows to fill its 4-rows-per-warp slots
+  const int64_t fill = (int64_t)2 * sm_count() * cquad::WPB * 4;
+  const bool use_quad = !core_rows_forced && core_quad_ok(p) &&
+                        (p.nsegs > 0 ? p.nsegs : p.nrows) >= fill;
+  if (use_quad && p.nsegs > 0) {  // the quad kernel reads segments through the row fields
+    p.nrows = p.nsegs;
+    p.row_coord = p.seg_coord;
+    p.row_leaf_ptr = p.seg_leaf_ptr;
+  }
+  const int g = use_quad ? core_quad_grid(p)
+                : p.R <= 8 ? core_rows_grid<8>(p) : p.R <= 16 ? core_rows_grid<16>(p)
+                                                              : core_rows_grid<32>(p);
   if ((int64_t)g * p.R * p.J > partials_cap)
     return fail(FT_ERR_ARG, "partials buffer too small (%lld < %lld)", (long long)partials_cap,
                 (long long)g * p.R * p.J);
   cudaStream_t s = as_stream(stream);
   *nblocks_out = g;
+  if (use_quad) return launch_core_quad(p, g, s);
   if (p.R <= 8) return launch_core_rows<8>(p, g, s);
   if (p.R <= 16) return launch_core_rows<16>(p, g, s);
   return launch_core_rows<32>(p, g, s);

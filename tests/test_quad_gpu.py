@@ -1,5 +1,6 @@
-"""The leaf-major index (K1b, ft_tree_leaf_index) and the four-rows-per-warp factor kernel
-(K3b `quad`) against the fp64 oracle (oracle/), at the contract's rel 1e-4 per sweep.
+"""The leaf-major index (K1b, ft_tree_leaf_index), the four-rows-per-warp factor kernels (K3b
+`quad` / `quadp`) and core kernel (K4 `quad`, the default for order 3) against the fp64 oracle
+(oracle/), at the contract's rel 1e-4 per sweep.
 
 `quad` is what `auto` runs on order-3 sweeps with 16 < J <= 32 and enough rows (Netflix modes
 0 and 1); these cases force it (FT_FACTOR_KERNEL=quad, in a subprocess because the variant is
@@ -85,6 +86,8 @@ for epoch in range(2):
     for n in range(3):
         O.update_core_mode(om, oforest, ocache, n, ocfg)
         ft.update_core_mode(model, forest, cache, n, cfg)
+        u = forest.trees[n].leaf_mode
+        assert_rel(model.cores_t[u].cpu().numpy(), om.cores_t[u], 1e-4, f"e{{epoch}} core {{u}}")
 print('ok')
 """
 
@@ -94,7 +97,7 @@ print('ok')
     ((20000, 700, 9), 300_000, 24, 20, 1e-3),     # J < 32, R < 32 (padding), 1-3 leaf rows
     ((60000, 64, 64), 200_000, 32, 32, 5e-3),     # more rows than row slots (row switching)
 ])
-@pytest.mark.parametrize("kernel", ["quad", "quadp"])
+@pytest.mark.parametrize("kernel", ["quad", "quadp", "quadw"])
 def test_quad_sweeps_match_oracle(kernel, dims, nnz, J, R, lr):
     code = _CASE.format(dims=dims, nnz=nnz, J=J, R=R, lr=lr, seed=7)
     env = dict(os.environ, FT_FACTOR_KERNEL=kernel)

@@ -51,6 +51,8 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
 }
 
 __device__ __forceinline__ void cp_async16_s(uint32_t dst, const float *src) {
+  // .ca: the leaf-level C rows of a sweep are often a small matrix (Netflix C_2: 280 KB) that
+  // stays L1-resident -- measured .cg (L2 only): core sweep modes 0/1 3.2 -> 4.2-4.6 ms
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
 }
 
@@ -526,8 +528,10 @@ int launch_quadp(const SweepParams &q, cudaStream_t s) {
 namespace quadw {
 constexpr int NS = 4;   // ring stages (producer k writes stages k, k+2)
 constexpr int NP = 2;   // producers per group
-constexpr int STAGE_FLOATS = 32 * quad::QVS + 4 * quad::MQ * 4 + 4 * 4 + 4 * 32;  // V, meta, info, A
-constexpr int GROUP_FLOATS = NS * STAGE_FLOATS + NP * 2 * quad::TILE;  // ring + X, Y per producer
+// stage: V [32][QVS] | meta float4 [4][MQ] | info int4 [4] | A rows [4][32] | lr*G^T [4][8][8]
+constexpr int STAGE_FLOATS = 32 * quad::QVS + 4 * quad::MQ * 4 + 4 * 4 + 4 * 32 + 4 * 64;
+// ring + X, Y per producer + the consumer's row exchange [4][32]
+constexpr int GROUP_FLOATS = NS * STAGE_FLOATS + NP * 2 * quad::TILE + 4 * 32;
 constexpr int BAR_BYTES = 2 * NS * 8 + 16;
 constexpr int THREADS = (NP + 1) * 32;
 constexpr size_t bytes() {
@@ -535,7 +539,8 @@ constexpr size_t bytes() {
 }
 }  // namespace quadw
 
-__global__ void __launch_bounds__(quadw::THREADS, 1) factor_rows_quadw_kernel(const SweepParams p) {
+template <bool GRAM>
+__global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(const SweepParams p) {
   using namespace quad;
   using quadp::Leaf;
   using quadp::Rec;
@@ -571,6 +576,9 @@ __global__ void __launch_bounds__(quadw::THREADS, 1) factor_rows_quadw_kernel(co
   };
   auto stage_a = [&](int st) {
     return ring + st * quadw::STAGE_FLOATS + 32 * QVS + 4 * MQ * 4 + 16;
+  };
+  auto stage_g = [&](int st) {  // lr * G^T: [q][l][m] = lr v_{8q+m} . v_{8q+l}
+    return ring + st * quadw::STAGE_FLOATS + 32 * QVS + 4 * MQ * 4 + 16 + 4 * 32;
   };
 
   if (w > 0) {
@@ -644,6 +652,28 @@ __global__ void __launch_bounds__(quadw::THREADS, 1) factor_rows_quadw_kernel(co
       int4 *info = stage_info(st);
       if (!stop) {
         quad_store_v(stage_v(st), acc, lane);
+        if (GRAM) {  // lane (q, l): lr G[m][l] = lr v_m . v_l over the quarter's batch, fp32
+          __syncwarp();
+          const float4 *vs = reinterpret_cast<const float4 *>(stage_v(st) + 8 * q * QVS);
+          float4 vl[8];
+#pragma unroll
+          for (int j4 = 0; j4 < 8; ++j4) vl[j4] = vs[l * (QVS / 4) + j4];
+          float gcol[8];
+#pragma unroll
+          for (int m = 0; m < 8; ++m) {
+            float2 g0 = make_float2(0.f, 0.f), g1 = g0;
+#pragma unroll
+            for (int j4 = 0; j4 < 8; ++j4) {
+              const float4 vm = vs[m * (QVS / 4) + j4];
+              g0 = ffma2(make_float2(vm.x, vm.y), make_float2(vl[j4].x, vl[j4].y), g0);
+              g1 = ffma2(make_float2(vm.z, vm.w), make_float2(vl[j4].z, vl[j4].w), g1);
+            }
+            gcol[m] = p.lr * ((g0.x + g0.y) + (g1.x + g1.y));
+          }
+          float4 *gd = reinterpret_cast<float4 *>(stage_g(st) + 64 * q + 8 * l);
+          gd[0] = make_float4(gcol[0], gcol[1], gcol[2], gcol[3]);
+          gd[1] = make_float4(gcol[4], gcol[5], gcol[6], gcol[7]);
+        }
         const float lrk = l < r0.nb ? p.lr : 0.f;
         const float ck = -lrk * p.reg;
         stage_meta(st)[q * MQ + l] = make_float4(l < r0.nb ? d0.x : 0.f, lrk, ck, ck);
@@ -662,6 +692,7 @@ __global__ void __launch_bounds__(quadw::THREADS, 1) factor_rows_quadw_kernel(co
     // ===================================== consumer =====================================
     float a[4] = {0.f, 0.f, 0.f, 0.f};
     int ai = -1;
+    float *xrow = ring + quadw::NS * quadw::STAGE_FLOATS + quadw::NP * 2 * TILE + 32 * q;
     auto store_a = [&]() {
       float *ar = p.A + (int64_t)ai * J;
       if (j32) {
@@ -683,13 +714,58 @@ __global__ void __launch_bounds__(quadw::THREADS, 1) factor_rows_quadw_kernel(co
         a[0] = v.x, a[1] = v.y, a[2] = v.z, a[3] = v.w;
         ai = info.z;
       }
-      const int nbmax = __reduce_max_sync(FULL, (unsigned)info.x);
       const float *Vq = stage_v(st) + 8 * q * QVS + 4 * l;
       const float4 *mq = stage_meta(st) + q * MQ;
+      if (GRAM) {
+        // Gram form of the chain (exact restatement): lane l of the quarter tracks
+        // w_l = a_m . v_l while the batch's updates m = 0..7 are applied,
+        //   e_m = x_m - w_m,   w_l <- w_l - lr reg w_l + e_m (lr G[m][l]),
+        // so the serial dependency per update is one shuffle and one FMA; then the row is
+        // replayed a <- a - lr reg a + lr e_m v_m over its 4 columns per lane.
+        *reinterpret_cast<float4 *>(xrow + 4 * l) = make_float4(a[0], a[1], a[2], a[3]);
+        __syncwarp();
+        float w;  // d_l = a_0 . v_l: the full row against the lane's own leaf row
+        {
+          const float4 *ar = reinterpret_cast<const float4 *>(xrow);
+          const float4 *vr = reinterpret_cast<const float4 *>(stage_v(st) + (8 * q + l) * QVS);
+          float2 d0 = make_float2(0.f, 0.f), d1 = d0;
 #pragma unroll
-      for (int kk = 0; kk < QB; ++kk) {
-        if (kk >= nbmax) break;
-        quad_chain_step(a, Vq + kk * QVS, mq[kk]);
+          for (int j4 = 0; j4 < 8; ++j4) {
+            const float4 av = ar[j4], vv = vr[j4];
+            d0 = ffma2(make_float2(av.x, av.y), make_float2(vv.x, vv.y), d0);
+            d1 = ffma2(make_float2(av.z, av.w), make_float2(vv.z, vv.w), d1);
+          }
+          w = (d0.x + d0.y) + (d1.x + d1.y);
+        }
+        const float4 *gq4 = reinterpret_cast<const float4 *>(stage_g(st) + 64 * q + 8 * l);
+        const float4 ga = gq4[0], gb = gq4[1];
+        const float gm[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
+        const float xl = mq[l].x, cdec = -p.lr * p.reg;
+        float e[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          e[m] = __shfl_sync(FULL, xl - w, 8 * q + m);
+          w = __fmaf_rn(e[m], gm[m], __fmaf_rn(cdec, w, w));
+        }
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          const float4 v = *reinterpret_cast<const float4 *>(Vq + m * QVS);
+          const float4 mm = mq[m];  // (x, lr, -lr reg, -lr reg); lr = 0 on padding steps
+          const float lre = mm.y * e[m];
+          const float2 a01 = ffma2(make_float2(mm.z, mm.w), make_float2(a[0], a[1]), make_float2(a[0], a[1]));
+          const float2 a23 = ffma2(make_float2(mm.z, mm.w), make_float2(a[2], a[3]), make_float2(a[2], a[3]));
+          a[0] = __fmaf_rn(lre, v.x, a01.x);
+          a[1] = __fmaf_rn(lre, v.y, a01.y);
+          a[2] = __fmaf_rn(lre, v.z, a23.x);
+          a[3] = __fmaf_rn(lre, v.w, a23.y);
+        }
+      } else {
+        const int nbmax = __reduce_max_sync(FULL, (unsigned)info.x);
+#pragma unroll
+        for (int kk = 0; kk < QB; ++kk) {
+          if (kk >= nbmax) break;
+          quad_chain_step(a, Vq + kk * QVS, mq[kk]);
+        }
       }
       __syncwarp();
       mbar_arrive(empty + st);
@@ -698,16 +774,17 @@ __global__ void __launch_bounds__(quadw::THREADS, 1) factor_rows_quadw_kernel(co
   }
 }
 
+template <bool GRAM>
 int launch_quadw(const SweepParams &q, cudaStream_t s) {
   const size_t sm = quadw::bytes();
   static bool set = false;
   if (!set) {
-    cudaFuncSetAttribute(factor_rows_quadw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sm);
+    cudaFuncSetAttribute(factor_rows_quadw_kernel<GRAM>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     set = true;
   }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quadw_kernel,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quadw_kernel<GRAM>,
                                                     quadw::THREADS, sm) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
@@ -715,7 +792,7 @@ int launch_quadw(const SweepParams &q, cudaStream_t s) {
   const int64_t cap = (int64_t)sm_count() * per_sm;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
-  factor_rows_quadw_kernel<<<(int)g, quadw::THREADS, sm, s>>>(q);
+  factor_rows_quadw_kernel<GRAM><<<(int)g, quadw::THREADS, sm, s>>>(q);
   return check_launch("ft_factor_sweep_rows(quadw)");
 }
 

@@ -1931,6 +1931,7 @@ int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
     if (e && strcmp(e, "quad") == 0) return 8;
     if (e && strcmp(e, "quadp") == 0) return 9;
     if (e && strcmp(e, "quadw") == 0) return 10;
+    if (e && strcmp(e, "quadg") == 0) return 11;
     return 5;  // auto: dual when the rows fill the SMs, gram otherwise
   }();
   int variant = chosen;
@@ -1944,16 +1945,17 @@ int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
   // auto, by rows per resident warp slot: many rows -> dual (Netflix modes 0/1: 7.5 ms);
   // few long rows -> warp-specialised at order 3 (mode 2: 8.4 vs 8.8 gram, 13.4 dual), else gram
   // quad / quadp: order 3, 16 < J <= 32, leaf-major index
-  if ((variant == 8 || variant == 9 || variant == 10) && !(RP == 32 && quad_ok(p))) variant = 5;
+  if (variant >= 8 && variant <= 11 && !(RP == 32 && quad_ok(p))) variant = 5;
   if (variant == 5) {
-    if (RP == 32 && quad_ok(p))  // many rows: quad; few long rows: quadp (in-warp pipeline)
-      variant = p.nrows >= (int64_t)2 * sm_count() * quad::WPB * 4 ? 8 : 9;
+    if (RP == 32 && quad_ok(p))  // many rows: quad; few long rows: quadw (warp-specialised)
+      variant = p.nrows >= (int64_t)2 * sm_count() * quad::WPB * 4 ? 8 : 10;
     else
       variant = p.nrows >= (int64_t)2 * sm_count() * 16 ? 4 : (p.N == 3 ? 7 : 0);
   }
   if (variant == 8) return launch_quad(q, s);
   if (variant == 9) return launch_quadp(q, s);
-  if (variant == 10) return launch_quadw(q, s);
+  if (variant == 10) return launch_quadw<false>(q, s);
+  if (variant == 11) return launch_quadw<true>(q, s);
   if (variant == 6) {
     const size_t sm = RDualPlan::bytes<RP>();
     static bool set6 = false;

@@ -97,7 +97,7 @@ print('ok')
     ((20000, 700, 9), 300_000, 24, 20, 1e-3),     # J < 32, R < 32 (padding), 1-3 leaf rows
     ((60000, 64, 64), 200_000, 32, 32, 5e-3),     # more rows than row slots (row switching)
 ])
-@pytest.mark.parametrize("kernel", ["quad", "quadp", "quadw"])
+@pytest.mark.parametrize("kernel", ["quad", "quadp", "quadw", "quadg"])
 def test_quad_sweeps_match_oracle(kernel, dims, nnz, J, R, lr):
     code = _CASE.format(dims=dims, nnz=nnz, J=J, R=R, lr=lr, seed=7)
     env = dict(os.environ, FT_FACTOR_KERNEL=kernel)

@@ -101,6 +101,57 @@ __global__ void first_diff_level(const int32_t *__restrict__ perm, int64_t nnz, 
   if (first == a.N) atomicMin(dup_min, (unsigned long long)perm[p]);
 }
 
+// Single-chunk keys (sum of level bits <= 64: orders 3 / 4 at the BASELINE shapes): the sorted
+// key IS the level-ordered coordinate tuple, so the levels, values (carried as the sort
+// payload) and first-differing level decode from the sorted arrays with coalesced reads -- no
+// random gather of idx[perm[p]] (was ~5 ms per Netflix tree).  An equal key pair (duplicate)
+// sets *dup_flag; the caller then reruns the perm-based path for the reference's error report.
+struct DecodeArgs {
+  int N;
+  int shift[FT_MAX_ORDER];
+  uint64_t mask[FT_MAX_ORDER];
+  int32_t *K[FT_MAX_ORDER];
+};
+
+__global__ void decode_levels(const uint64_t *__restrict__ keys, const uint32_t *__restrict__ vbits,
+                              int64_t nnz, DecodeArgs a, float *__restrict__ vout,
+                              uint8_t *__restrict__ fdl, int *__restrict__ dup_flag) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= nnz) return;
+  const uint64_t k = keys[p];
+  for (int d = 0; d < a.N; ++d) a.K[d][p] = (int32_t)((k >> a.shift[d]) & a.mask[d]);
+  vout[p] = __uint_as_float(vbits[p]);
+  int first = 0;
+  if (p > 0) {
+    const uint64_t x = k ^ keys[p - 1];
+    if (x == 0) {
+      first = a.N;
+      *dup_flag = 1;
+    } else {
+      const int hb = 63 - __clzll((long long)x);  // highest differing bit -> its level
+      first = a.N - 1;
+      for (int d = 0; d < a.N; ++d)
+        if (a.mask[d] && hb >= a.shift[d] && hb < a.shift[d] + 64 - __clzll((long long)a.mask[d])) {
+          first = d;
+          break;
+        }
+    }
+  }
+  fdl[p] = (uint8_t)first;
+}
+
+__global__ void pack_keys_vals(const int32_t *__restrict__ idx, const float *__restrict__ vals,
+                               int64_t nnz, PackArgs a, uint64_t *__restrict__ keys,
+                               uint32_t *__restrict__ vbits) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= nnz) return;
+  const int32_t *row = idx + p * a.N;
+  uint64_t k = 0;
+  for (int d = a.d0; d < a.d1; ++d) k |= (uint64_t)(uint32_t)row[a.lm[d]] << a.shift[d];
+  keys[p] = k;
+  vbits[p] = __float_as_uint(vals[p]);
+}
+
 __global__ void flags_le(const uint8_t *__restrict__ fdl, const uint8_t *__restrict__ extra,
                          int64_t n, int lim, uint8_t *__restrict__ out) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -304,8 +355,48 @@ extern "C" int ft_build_tree(int32_t N, int64_t nnz, const int64_t *dims, const 
   if (!sort_tmp) return fail(FT_ERR_CUDA, "ft_build_tree: out of device memory (sort)");
 
   const unsigned nb = blocks_for(nnz);
+  // level columns (the leaf level goes straight to inds[N-1] = leaf_coord)
+  GatherArgs ga{};
+  ga.N = N;
+  for (int d = 0; d < N; ++d) {
+    ga.lm[d] = lm[d];
+    ga.K[d] = (d == N - 1) ? inds[N - 1] : sc.get<int32_t>(nnz);
+    if (!ga.K[d]) return fail(FT_ERR_CUDA, "ft_build_tree: out of device memory (levels)");
+  }
+  uint8_t *fdl = sc.get<uint8_t>(nnz);
+  bool decoded = false;
+  if (chunks.size() == 1 && chunks[0].bits > 0) {
+    // fast path: sort (key, value) pairs and decode (see decode_levels)
+    const LevelChunk &c = chunks[0];
+    PackArgs pa{};
+    pa.N = N;
+    for (int d = 0; d < N; ++d) pa.lm[d] = lm[d];
+    pa.d0 = c.d0;
+    pa.d1 = c.d1;
+    for (int d = c.d0; d < c.d1; ++d) pa.shift[d] = c.shift[d];
+    uint32_t *v0 = reinterpret_cast<uint32_t *>(p0), *v1 = reinterpret_cast<uint32_t *>(p1);
+    pack_keys_vals<<<nb, 256, 0, s>>>(idx, vals, nnz, pa, k0, v0);
+    if (int rc = check_launch("pack_keys_vals")) return rc;
+    size_t b = sort_bytes;
+    FT_CUDA(cub::DeviceRadixSort::SortPairs(sort_tmp, b, k0, k1, v0, v1, nnz, 0, c.bits, s));
+    DecodeArgs da{};
+    da.N = N;
+    for (int d = 0; d < N; ++d) {
+      da.shift[d] = c.shift[d];
+      da.mask[d] = bits[d] >= 64 ? ~0ull : ((1ull << bits[d]) - 1);
+      da.K[d] = ga.K[d];
+    }
+    int *dflag = sc.get<int>(1);
+    FT_CUDA(cudaMemsetAsync(dflag, 0, sizeof(int), s));
+    decode_levels<<<nb, 256, 0, s>>>(k1, v1, nnz, da, leaf_vals, fdl, dflag);
+    if (int rc = check_launch("decode_levels")) return rc;
+    int hflag = 0;
+    FT_CUDA(cudaMemcpyAsync(&hflag, dflag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    FT_CUDA(cudaStreamSynchronize(s));
+    decoded = hflag == 0;  // a duplicate: redo with the permutation to report its entry
+  }
   int32_t *perm = nullptr;  // current permutation (sorted position -> entry)
-  for (size_t ci = 0; ci < chunks.size(); ++ci) {
+  for (size_t ci = 0; ci < chunks.size() && !decoded; ++ci) {
     const LevelChunk &c = chunks[ci];
     PackArgs pa{};
     pa.N = N;
@@ -327,23 +418,17 @@ extern "C" int ft_build_tree(int32_t N, int64_t nnz, const int64_t *dims, const 
     }
   }
 
-  // sorted level columns (the leaf level goes straight to inds[N-1] = leaf_coord)
-  GatherArgs ga{};
-  ga.N = N;
-  for (int d = 0; d < N; ++d) {
-    ga.lm[d] = lm[d];
-    ga.K[d] = (d == N - 1) ? inds[N - 1] : sc.get<int32_t>(nnz);
-    if (!ga.K[d]) return fail(FT_ERR_CUDA, "ft_build_tree: out of device memory (levels)");
+  // sorted level columns via the permutation (multi-chunk keys, or the duplicate report)
+  unsigned long long hdup = ~0ull;
+  if (!decoded) {
+    unsigned long long *dup = sc.get<unsigned long long>(1);
+    FT_CUDA(cudaMemsetAsync(dup, 0xff, sizeof(unsigned long long), s));
+    gather_levels<<<nb, 256, 0, s>>>(idx, vals, perm, nnz, ga, leaf_vals);
+    first_diff_level<<<nb, 256, 0, s>>>(perm, nnz, ga, fdl, dup);
+    if (int rc = check_launch("gather_levels")) return rc;
+    FT_CUDA(cudaMemcpyAsync(&hdup, dup, sizeof(hdup), cudaMemcpyDeviceToHost, s));
+    FT_CUDA(cudaStreamSynchronize(s));
   }
-  uint8_t *fdl = sc.get<uint8_t>(nnz);
-  unsigned long long *dup = sc.get<unsigned long long>(1);
-  FT_CUDA(cudaMemsetAsync(dup, 0xff, sizeof(unsigned long long), s));
-  gather_levels<<<nb, 256, 0, s>>>(idx, vals, perm, nnz, ga, leaf_vals);
-  first_diff_level<<<nb, 256, 0, s>>>(perm, nnz, ga, fdl, dup);
-  if (int rc = check_launch("gather_levels")) return rc;
-  unsigned long long hdup = 0;
-  FT_CUDA(cudaMemcpyAsync(&hdup, dup, sizeof(hdup), cudaMemcpyDeviceToHost, s));
-  FT_CUDA(cudaStreamSynchronize(s));
   for (int k = 0; k < 4 + N; ++k) counts_out[k] = 0;
   counts_out[3] = -1;
   if (hdup != ~0ull) {

@@ -343,7 +343,7 @@ def run_ours(args, cfg):
     achieved = d["bytes"] / d["sec"] / 1e9
     variant = os.environ.get("FT_FACTOR_KERNEL", "auto")
     kname = (f"factor_rows_{variant}_kernel" if variant != "auto"
-             else "factor_rows_{dual|gram}_kernel (auto: by row count)") if dom == "factor_rows" \
+             else "factor_rows_{quad|quadw}_kernel (auto: quad for many rows, quadw for few long rows)") if dom == "factor_rows" \
         else dom + "_kernel"
     traffic, _ = ncu_traffic(dom)
     roof = {"kernel": kname, "bound": "hbm", "achieved": achieved, "peak": peak,

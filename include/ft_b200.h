@@ -192,6 +192,13 @@ FT_API int ft_predict(const ft_model_t *model, int64_t m, const int32_t *idx, fl
 FT_API int ft_sse(const ft_model_t *model, int64_t m, const int32_t *idx, const float *vals,
            double *out2, void *stream);
 
+/* K6b evaluate over the entries a tree holds (the training set): out2 = (sum (x - xhat)^2,
+ * sum |x - xhat|) in fp64, walking the tree's row segments with the C rows of its levels --
+ * two gathers per entry instead of N (the root mode's C row stays in shared memory per
+ * segment).  Same value as ft_sse over those entries up to the summation order.  Needs
+ * order 3, R % 4 == 0, the leaf-major index and row segments (FT_ERR_UNSUPPORTED otherwise),
+ * and model->dots coherent.  out2 is DEVICE double[2]. */
+FT_API int ft_sse_tree(const ft_tree_t *tree, const ft_model_t *model, double *out2, void *stream);
 /* K7  Synthetic COO generator (same distribution as coo.generate_synthetic, coo.py:164-213:
  * distinct coordinates uniform without replacement, values U[lo, hi]; NOT the same stream).
  * Writes nnz unique coordinates (row-major int32 [nnz x N]) in a random entry order, and

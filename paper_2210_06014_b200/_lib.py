@@ -98,6 +98,7 @@ SIGNATURES = {
         ctypes.c_int32, ctypes.c_int32, _vp, ctypes.c_int32, _vp, _vp]),
     "ft_predict": (ctypes.c_int, [ctypes.POINTER(FtModel), ctypes.c_int64, _vp, _vp, _vp]),
     "ft_sse": (ctypes.c_int, [ctypes.POINTER(FtModel), ctypes.c_int64, _vp, _vp, _vp, _vp]),
+    "ft_sse_tree": (ctypes.c_int, [ctypes.POINTER(FtTree), ctypes.POINTER(FtModel), _vp, _vp]),
     "ft_generate_coo": (ctypes.c_int, [
         ctypes.c_int32, _i64p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_float, ctypes.c_float,
         _vp, _vp, _vp]),

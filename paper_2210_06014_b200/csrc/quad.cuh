@@ -840,6 +840,10 @@ constexpr int WPB = 8;
 constexpr size_t bytes() { return (size_t)WPB * WARP_FLOATS * 4; }
 }  // namespace cquad
 
+// SSE = true: the same walk scores the tree's leaves instead (K6b, evaluate over the training
+// entries, train.py:91-98): per slot e = x - C_u[i] . cross, sum e^2 and |e| in fp64 per lane,
+// fixed-order block reduction to p.partials as doubles [block][2] (no gradient work).
+template <bool SSE>
 __global__ void __launch_bounds__(cquad::WPB * 32, 2) core_rows_quad_kernel(const SweepParams p) {
   using namespace cquad;
   extern __shared__ float4 smem4[];
@@ -882,6 +886,7 @@ __global__ void __launch_bounds__(cquad::WPB * 32, 2) core_rows_quad_kernel(cons
 #pragma unroll
   for (int j = 0; j < FT_MAX_RANK; ++j) acc[j] = 0.f;
   float2 g01 = make_float2(0.f, 0.f), g23 = make_float2(0.f, 0.f);  // quarter lanes: g[4l..4l+3]
+  double sse = 0.0, sae = 0.0;  // SSE mode
   const int gc = lane & 7, gs = lane >> 3;
   const bool gok = gc < (R >> 2);
   const uint32_t xs0 = smem_u32(X + gs * XS + 4 * gc), ys0 = smem_u32(Y + gs * XS + 4 * gc);
@@ -892,7 +897,7 @@ __global__ void __launch_bounds__(cquad::WPB * 32, 2) core_rows_quad_kernel(cons
   for (;;) {
     // ---- rows that ended: acc += g (x) A_u[i] (warp-cooperative, one quarter at a time) ----
     const bool ending = ci >= 0 && cL0 >= cLe;
-    unsigned em = __ballot_sync(FULL, ending && l == 0);
+    unsigned em = SSE ? 0u : __ballot_sync(FULL, ending && l == 0);
     while (em) {
       const int qq = __ffs(em) - 1 >> 3;
       em &= em - 1;
@@ -970,7 +975,18 @@ __global__ void __launch_bounds__(cquad::WPB * 32, 2) core_rows_quad_kernel(cons
                     make_float2(cv.z, cv.w), s23);
       }
       const float s = (s01.x + s01.y) + (s23.x + s23.y);
-      es[lane] = l < nb ? x - s : 0.f;
+      const float e = l < nb ? x - s : 0.f;
+      if (SSE) {
+        sse += (double)e * (double)e;
+        sae += fabs((double)e);
+      } else {
+        es[lane] = e;
+      }
+    }
+    if (SSE) {
+      __syncwarp();
+      cL0 += nb;
+      continue;
     }
     __syncwarp();
     // ---- quarter lanes over r: g_q += sum_k e_k cross_k ----
@@ -993,6 +1009,22 @@ __global__ void __launch_bounds__(cquad::WPB * 32, 2) core_rows_quad_kernel(cons
   }
   // ---- fixed-order block reduction -> partials[block] (reuses the staging tiles) ----
   __syncthreads();
+  if (SSE) {
+    double *rd = reinterpret_cast<double *>(smem4);
+    rd[2 * threadIdx.x] = sse;
+    rd[2 * threadIdx.x + 1] = sae;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double a = 0.0, b = 0.0;
+      for (int k = 0; k < (int)blockDim.x; ++k) {
+        a += rd[2 * k];
+        b += rd[2 * k + 1];
+      }
+      reinterpret_cast<double *>(p.partials)[2 * blockIdx.x] = a;
+      reinterpret_cast<double *>(p.partials)[2 * blockIdx.x + 1] = b;
+    }
+    return;
+  }
   const int RJ = R * J;
   float *red = reinterpret_cast<float *>(smem4);
   if (lane < R) {
@@ -1013,15 +1045,17 @@ bool core_quad_ok(const SweepParams &p) {
          p.R * p.J <= cquad::WARP_FLOATS;
 }
 
+template <bool SSE = false>
 int core_quad_grid(const SweepParams &p) {
   const size_t sm = cquad::bytes();
   static bool set = false;
   if (!set) {
-    cudaFuncSetAttribute(core_rows_quad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(core_rows_quad_kernel<SSE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
     set = true;
   }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, core_rows_quad_kernel,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, core_rows_quad_kernel<SSE>,
                                                     cquad::WPB * 32, sm) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
@@ -1033,6 +1067,18 @@ int core_quad_grid(const SweepParams &p) {
 }
 
 int launch_core_quad(const SweepParams &p, int g, cudaStream_t s) {
-  core_rows_quad_kernel<<<g, cquad::WPB * 32, cquad::bytes(), s>>>(p);
+  core_rows_quad_kernel<false><<<g, cquad::WPB * 32, cquad::bytes(), s>>>(p);
   return check_launch("ft_core_sweep_rows(quad)");
+}
+
+__global__ void sum_pairs_f64(const double *__restrict__ partials, int nblocks, double *out2) {
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int k = 0; k < nblocks; ++k) {
+      a += partials[2 * k];
+      b += partials[2 * k + 1];
+    }
+    out2[0] = a;
+    out2[1] = b;
+  }
 }

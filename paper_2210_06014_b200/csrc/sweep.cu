@@ -2170,3 +2170,30 @@ extern "C" int ft_core_reduce(int32_t R, int32_t J, const float *partials, int32
       RJ, nullptr, partials, nparts, 0, 1.0, 0.f, 0.f, out, nullptr, 0);
   return check_launch("ft_core_reduce");
 }
+
+extern "C" int ft_sse_tree(const ft_tree_t *tree, const ft_model_t *model, double *out2,
+                           void *stream) {
+  SweepParams p{};
+  if (int rc = fill_rows_params(p, tree, model)) return rc;
+  if (!out2) return fail(FT_ERR_ARG, "ft_sse_tree: null out2");
+  if (!p.Cu) return fail(FT_ERR_ARG, "ft_sse_tree needs dots[u] (coherent cache)");
+  if (!core_quad_ok(p) || p.nsegs <= 0)
+    return fail(FT_ERR_UNSUPPORTED, "ft_sse_tree: needs order 3, R %% 4 == 0 and the leaf index");
+  keep_pool();
+  cudaStream_t s = as_stream(stream);
+  p.nrows = p.nsegs;
+  p.row_coord = p.seg_coord;
+  p.row_leaf_ptr = p.seg_leaf_ptr;
+  const int g = core_quad_grid<true>(p);
+  double *partials = nullptr;
+  FT_CUDA(cudaMallocAsync(&partials, sizeof(double) * 2 * g, s));
+  p.partials = reinterpret_cast<float *>(partials);
+  core_rows_quad_kernel<true><<<g, cquad::WPB * 32, cquad::bytes(), s>>>(p);
+  int rc = check_launch("ft_sse_tree");
+  if (rc == FT_OK) {
+    sum_pairs_f64<<<1, 32, 0, s>>>(partials, g, out2);
+    rc = check_launch("ft_sse_tree(sum)");
+  }
+  cudaFreeAsync(partials, s);
+  return rc;
+}

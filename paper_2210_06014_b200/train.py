@@ -147,16 +147,37 @@ def _sse(model, dev, dots):
     return out
 
 
-def evaluate(model, tensor, cache: DotCache | None = None) -> tuple:
+def _sse_tree(model, tree, dots):
+    """K6b: the same sums over the entries a B-CSF tree holds, walked in tree order (two C-row
+    gathers per entry; None when the tree / shape is outside that kernel's cover)."""
+    import torch
+
+    if (model.order != 3 or model.core_rank % 4 or tree.leaf_pc is None
+            or tree.seg_coord is None):
+        return None
+    out = torch.zeros(2, dtype=torch.float64, device="cuda")
+    _lib.check(_lib.lib().ft_sse_tree(ctypes.byref(tree.view()), ctypes.byref(model.view(dots)),
+                                      out.data_ptr(), _lib.stream_handle()), "ft_sse_tree")
+    return out
+
+
+def evaluate(model, tensor, cache: DotCache | None = None, forest: CsfForest | None = None) -> tuple:
     """RMSE and MAE over a tensor's entries (train.py:91-98), reduced in fp64 on the GPU.
-    Uses ``cache`` when it is coherent (all modes clean), else fresh C_n."""
+    Uses ``cache`` when it is coherent (all modes clean), else fresh C_n.  ``forest``: a forest
+    built from exactly this tensor (as ``train`` has for the training set) -- its first tree is
+    scored in tree order (K6b) instead of the COO order."""
     if tensor is None:
         raise ValidationError("cannot evaluate on an empty entry set")
     dev = as_device(tensor)
     if dev.nnz == 0:
         raise ValidationError("cannot evaluate on an empty entry set")
     dots = cache.arrays if cache is not None and not cache.dirty.any() else fresh_dots(model)
-    sse, sae = _sse(model, dev, dots).cpu().numpy()
+    out = None
+    if forest is not None and forest.omega is None and forest.trees[0].nnz == dev.nnz:
+        out = _sse_tree(model, forest.trees[0], dots)
+    if out is None:
+        out = _sse(model, dev, dots)
+    sse, sae = out.cpu().numpy()
     return math.sqrt(float(sse) / dev.nnz), float(sae) / dev.nnz
 
 
@@ -390,15 +411,16 @@ def run_epoch(model, forest: CsfForest, cache: DotCache | None, train_tensor, cf
                               epoch=epoch_no) from None
     wall = time.perf_counter() - t0
     m = _metrics(model, cache, train_tensor, test_tensor, counter, epoch_no, fsec + csec,
-                 evaluate_metrics)
+                 evaluate_metrics, forest)
     m.factor_seconds, m.core_seconds = fsec, csec
     del wall
     return m
 
 
-def _metrics(model, cache, train_tensor, test_tensor, counter, epoch_no, seconds, do_eval=True):
+def _metrics(model, cache, train_tensor, test_tensor, counter, epoch_no, seconds, do_eval=True,
+             forest=None):
     if do_eval:
-        train_rmse, train_mae = evaluate(model, train_tensor, cache)
+        train_rmse, train_mae = evaluate(model, train_tensor, cache, forest)
         if test_tensor is not None:
             test_rmse, test_mae = evaluate(model, test_tensor, cache)
         else:
@@ -418,7 +440,7 @@ def train(model, train_tensor, cfg: TrainConfig, test_tensor=None, forest: CsfFo
     if counter is None:
         counter = OpCounter()
     cache = precompute_cache(model, counter) if cfg.plan == "cached" else None
-    metrics = [_metrics(model, cache, train_tensor, test_tensor, counter, 0, 0.0)]
+    metrics = [_metrics(model, cache, train_tensor, test_tensor, counter, 0, 0.0, True, forest)]
     guards = GuardBank(model.order)
     for epoch_no in range(1, cfg.epochs + 1):
         m = run_epoch(model, forest, cache, train_tensor, cfg, counter, epoch_no, test_tensor,

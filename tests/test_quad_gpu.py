@@ -104,3 +104,27 @@ def test_quad_sweeps_match_oracle(kernel, dims, nnz, J, R, lr):
     out = subprocess.run([sys.executable, "-c", code], cwd=REPO, env=env, capture_output=True,
                          text=True, timeout=900)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
+
+
+def test_sse_tree_matches_coo_evaluate(ft):
+    """K6b (ft_sse_tree: the training set scored in tree order) gives the COO-order evaluate's
+    RMSE / MAE up to the fp64 summation order, and the reference-format path is kept for a
+    tensor the forest was not built from."""
+    import torch
+
+    rng = np.random.default_rng(5)
+    dims = (3000, 400, 60)
+    lin = rng.choice(int(np.prod(dims)), size=400_000, replace=False)
+    idx = np.stack(np.unravel_index(lin, dims), axis=1)
+    dev = ft.DeviceCoo(dims, torch.from_numpy(idx.astype(np.int32)).cuda(),
+                       torch.from_numpy(rng.uniform(1, 5, len(lin)).astype(np.float32)).cuda())
+    model = ft.default_init_model(dims, (32, 32, 32), 32, seed=1)
+    forest = ft.build_forest(dev, 128)
+    cache = ft.precompute_cache(model)
+    ref = ft.evaluate(model, dev, cache)
+    got = ft.evaluate(model, dev, cache, forest)
+    np.testing.assert_allclose(got, ref, rtol=1e-6)
+    # a forest of another tensor is ignored (falls back to the COO walk)
+    other = ft.DeviceCoo(dims, dev.idx[:1000].contiguous(), dev.vals[:1000].contiguous())
+    np.testing.assert_allclose(ft.evaluate(model, other, cache, forest),
+                               ft.evaluate(model, other, cache), rtol=0)

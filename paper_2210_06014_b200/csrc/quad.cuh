@@ -77,18 +77,14 @@ __device__ __forceinline__ void quad_afrag_init(const SweepParams &p, uint4 *afr
   }
 }
 
-// One k-tile of the transposed combine for n-tiles [nt0, nt0 + NN): acc[mt][nt] += Bt^T * cross^T.
+// One k-tile of the transposed combine for n-tiles [nt0, nt0 + NN): acc[mt][nt] += Bt^T * cross^T,
+// with the Bt^T fragments of this k-tile in registers.
 template <int NN>
-__device__ __forceinline__ void quad_mma_kt(const float *X, const float *Y, const uint4 *afr,
-                                            int kt, int nt0, int lane, float (&acc)[2][4][4]) {
+__device__ __forceinline__ void quad_mma_kt_r(const float *X, const float *Y, const uint4 (&ah)[2],
+                                              const uint4 (&al)[2], int kt, int nt0, int lane,
+                                              float (&acc)[2][4][4]) {
   using namespace quad;
   const int gq = lane >> 2, tq = lane & 3;
-  uint4 ah[MT], al[MT];
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt) {
-    ah[mt] = afr[(mt * KT + kt) * 32 + lane];
-    al[mt] = afr[KT * MT * 32 + (mt * KT + kt) * 32 + lane];
-  }
 #pragma unroll
   for (int nn = 0; nn < NN; ++nn) {
     const int nt = nt0 + nn;
@@ -105,6 +101,20 @@ __device__ __forceinline__ void quad_mma_kt(const float *X, const float *Y, cons
       mma_tf32(acc[mt][nt], ah[mt].x, ah[mt].y, ah[mt].z, ah[mt].w, bh0, bh1);
     }
   }
+}
+
+// ... with the fragments read from the per-block shared-memory copy
+template <int NN>
+__device__ __forceinline__ void quad_mma_kt(const float *X, const float *Y, const uint4 *afr,
+                                            int kt, int nt0, int lane, float (&acc)[2][4][4]) {
+  using namespace quad;
+  uint4 ah[MT], al[MT];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    ah[mt] = afr[(mt * KT + kt) * 32 + lane];
+    al[mt] = afr[KT * MT * 32 + (mt * KT + kt) * 32 + lane];
+  }
+  quad_mma_kt_r<NN>(X, Y, ah, al, kt, nt0, lane, acc);
 }
 
 // acc (V^T fragments) -> V[slot][j] (row stride QVS)
@@ -134,8 +144,11 @@ __device__ __forceinline__ void quad_zero(float (&acc)[2][4][4]) {
 
 // one serial step of a quarter's row: s = a . v (8 lanes x 4 columns), e = x - s,
 // a <- a + (-lr reg) a  (the decay, never through a rounded 1 - lr reg), then a += lr e v
+__device__ __forceinline__ void quad_chain_step_v(float (&a)[4], const float4 v, float4 m);
 __device__ __forceinline__ void quad_chain_step(float (&a)[4], const float *vrow, float4 m) {
-  const float4 v = *reinterpret_cast<const float4 *>(vrow);
+  quad_chain_step_v(a, *reinterpret_cast<const float4 *>(vrow), m);
+}
+__device__ __forceinline__ void quad_chain_step_v(float (&a)[4], const float4 v, float4 m) {
   float2 pr = fmul2(make_float2(a[0], a[1]), make_float2(v.x, v.y));
   pr = ffma2(make_float2(a[2], a[3]), make_float2(v.z, v.w), pr);
   float s = pr.x + pr.y;
@@ -629,6 +642,16 @@ __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(co
         for (int s = 0; s < quadw::NP - 1; ++s) (void)quadp::next_batch(p, cur, nstream);
       return quadp::next_batch(p, cur, nstream);
     };
+    // the Bt^T fragments live in registers for the whole sweep (64 per lane): the shared-memory
+    // pipe is the producers' scarce resource
+    uint4 AH[KT][MT], AL[KT][MT];
+#pragma unroll
+    for (int kt = 0; kt < KT; ++kt)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        AH[kt][mt] = afr[(mt * KT + kt) * 32 + lane];
+        AL[kt][mt] = afr[KT * MT * 32 + (mt * KT + kt) * 32 + lane];
+      }
     for (int s = 0; s < k; ++s) (void)quadp::next_batch(p, cur, nstream);
     Rec r0 = next_mine(true);
     Leaf d0 = quadp::load_leaf(p, r0, l);
@@ -645,7 +668,7 @@ __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(co
         __syncwarp();
         quad_zero(acc);
 #pragma unroll
-        for (int kt = 0; kt < KT; ++kt) quad_mma_kt<NT>(X, Y, afr, kt, 0, lane, acc);
+        for (int kt = 0; kt < KT; ++kt) quad_mma_kt_r<NT>(X, Y, AH[kt], AL[kt], kt, 0, lane, acc);
       }
       const int st = t % quadw::NS;
       if (t >= quadw::NS) mbar_wait(empty + st, ((t / quadw::NS) - 1) & 1);
@@ -760,12 +783,20 @@ __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(co
           a[3] = __fmaf_rn(lre, v.w, a23.y);
         }
       } else {
-        const int nbmax = __reduce_max_sync(FULL, (unsigned)info.x);
+        // the stage's 8 V rows and step operands are loaded up front (16 independent LDS.128,
+        // one latency) so the serial steps wait only on their own shuffles; short batches run
+        // all 8 steps (padding steps have lr = 0 and change nothing)
+        float4 vv[QB], mm[QB];
 #pragma unroll
         for (int kk = 0; kk < QB; ++kk) {
-          if (kk >= nbmax) break;
-          quad_chain_step(a, Vq + kk * QVS, mq[kk]);
+          vv[kk] = *reinterpret_cast<const float4 *>(Vq + kk * QVS);
+          mm[kk] = mq[kk];
         }
+        __syncwarp();
+        mbar_arrive(empty + st);  // the stage is free once read
+#pragma unroll
+        for (int kk = 0; kk < QB; ++kk) quad_chain_step_v(a, vv[kk], mm[kk]);
+        continue;
       }
       __syncwarp();
       mbar_arrive(empty + st);

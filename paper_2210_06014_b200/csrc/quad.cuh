@@ -82,7 +82,7 @@ __device__ __forceinline__ void quad_afrag_init(const SweepParams &p, uint4 *afr
 template <int NN>
 __device__ __forceinline__ void quad_mma_kt_r(const float *X, const float *Y, const uint4 (&ah)[2],
                                               const uint4 (&al)[2], int kt, int nt0, int lane,
-                                              float (&acc)[2][4][4]) {
+                                              float (&acc)[2][4][4], int mts = 2) {
   using namespace quad;
   const int gq = lane >> 2, tq = lane & 3;
 #pragma unroll
@@ -96,6 +96,7 @@ __device__ __forceinline__ void quad_mma_kt_r(const float *X, const float *Y, co
     const uint32_t bl1 = __float_as_uint(c.y - __uint_as_float(to_tf32(c.y)));
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) {
+      if (mt >= mts) break;  // J <= 16: the second m-tile is all padding
       mma_tf32(acc[mt][nt], al[mt].x, al[mt].y, al[mt].z, al[mt].w, bh0, bh1);
       mma_tf32(acc[mt][nt], ah[mt].x, ah[mt].y, ah[mt].z, ah[mt].w, bl0, bl1);
       mma_tf32(acc[mt][nt], ah[mt].x, ah[mt].y, ah[mt].z, ah[mt].w, bh0, bh1);
@@ -106,7 +107,8 @@ __device__ __forceinline__ void quad_mma_kt_r(const float *X, const float *Y, co
 // ... with the fragments read from the per-block shared-memory copy
 template <int NN>
 __device__ __forceinline__ void quad_mma_kt(const float *X, const float *Y, const uint4 *afr,
-                                            int kt, int nt0, int lane, float (&acc)[2][4][4]) {
+                                            int kt, int nt0, int lane, float (&acc)[2][4][4],
+                                            int mts = 2) {
   using namespace quad;
   uint4 ah[MT], al[MT];
 #pragma unroll
@@ -114,7 +116,7 @@ __device__ __forceinline__ void quad_mma_kt(const float *X, const float *Y, cons
     ah[mt] = afr[(mt * KT + kt) * 32 + lane];
     al[mt] = afr[KT * MT * 32 + (mt * KT + kt) * 32 + lane];
   }
-  quad_mma_kt_r<NN>(X, Y, ah, al, kt, nt0, lane, acc);
+  quad_mma_kt_r<NN>(X, Y, ah, al, kt, nt0, lane, acc, mts);
 }
 
 // acc (V^T fragments) -> V[slot][j] (row stride QVS)
@@ -165,6 +167,7 @@ __device__ __forceinline__ void quad_chain_step_v(float (&a)[4], const float4 v,
   a[3] = __fmaf_rn(lre, v.w, a23.y);
 }
 
+template <bool SMALL>
 __global__ void __launch_bounds__(quad::WPB * 32, 2) factor_rows_quad_kernel(const SweepParams p) {
   using namespace quad;
   extern __shared__ float4 smem4[];
@@ -179,6 +182,9 @@ __global__ void __launch_bounds__(quad::WPB * 32, 2) factor_rows_quad_kernel(con
   for (int k = lane; k < 2 * TILE; k += 32) X[k] = 0.f;  // Y's zero columns r >= R stay zero
   quad_afrag_init(p, afr);
   __syncthreads();
+  // m-tiles (j) / k-tiles (r) in use: compile-time (SMALL: J <= 16 and R <= 16), so the
+  // unrolled combine keeps no runtime guards; other shapes compute their zero padding
+  constexpr int mts = SMALL ? 1 : 2, nkt = SMALL ? 2 : 4;
 
   const int64_t nstream = (int64_t)gridDim.x * quad::WPB * 4;
   int64_t row = ((int64_t)blockIdx.x * quad::WPB + w) * 4 + q;
@@ -282,7 +288,8 @@ __global__ void __launch_bounds__(quad::WPB * 32, 2) factor_rows_quad_kernel(con
     float acc[2][4][4];
     quad_zero(acc);
 #pragma unroll
-    for (int kt = 0; kt < KT; ++kt) quad_mma_kt<NT>(X, Y, afr, kt, 0, lane, acc);
+    for (int kt = 0; kt < KT; ++kt)
+      if (kt < nkt) quad_mma_kt<NT>(X, Y, afr, kt, 0, lane, acc, mts);
     __syncwarp();  // every lane's fragments are read before V overwrites X
     quad_store_v(V, acc, lane);
     __syncwarp();
@@ -372,6 +379,7 @@ __device__ __forceinline__ Leaf load_leaf(const SweepParams &p, const Rec &r, in
 }  // namespace quadp
 
 __global__ void __launch_bounds__(quadp::WPB * 32, 1) factor_rows_quadp_kernel(const SweepParams p) {
+  constexpr bool SMALL = false;
   using namespace quad;
   using quadp::Rec;
   using quadp::Leaf;
@@ -387,6 +395,9 @@ __global__ void __launch_bounds__(quadp::WPB * 32, 1) factor_rows_quadp_kernel(c
   for (int k = lane; k < 4 * TILE; k += 32) base[k] = 0.f;
   quad_afrag_init(p, afr);
   __syncthreads();
+  // m-tiles (j) / k-tiles (r) in use: compile-time (SMALL: J <= 16 and R <= 16), so the
+  // unrolled combine keeps no runtime guards; other shapes compute their zero padding
+  constexpr int mts = SMALL ? 1 : 2, nkt = SMALL ? 2 : 4;
 
   const int64_t nstream = (int64_t)gridDim.x * quadp::WPB * 4;
   quadp::Cursor cur;
@@ -458,7 +469,8 @@ __global__ void __launch_bounds__(quadp::WPB * 32, 1) factor_rows_quadp_kernel(c
     __syncwarp();
     quad_zero(acc);
 #pragma unroll
-    for (int kt = 0; kt < KT; ++kt) quad_mma_kt<NT>(base, base + 2 * TILE, afr, kt, 0, lane, acc);
+    for (int kt = 0; kt < KT; ++kt)
+      if (kt < nkt) quad_mma_kt<NT>(base, base + 2 * TILE, afr, kt, 0, lane, acc, mts);
     __syncwarp();
     quad_store_v(V, acc, lane);
     put_meta(r0, d0.x);
@@ -481,7 +493,7 @@ __global__ void __launch_bounds__(quadp::WPB * 32, 1) factor_rows_quadp_kernel(c
 #pragma unroll
     for (int k = 0; k < QB; ++k) {
       quad_chain_step(a, Vq + k * QVS, mq[k]);
-      quad_mma_kt<2>(Xs, Ys, afr, k >> 1, 2 * (k & 1), lane, acc);
+      if ((k >> 1) < nkt) quad_mma_kt<2>(Xs, Ys, afr, k >> 1, 2 * (k & 1), lane, acc, mts);
     }
     __syncwarp();  // chain(t) done reading V / meta
     quad_store_v(V, acc, lane);
@@ -552,7 +564,7 @@ constexpr size_t bytes() {
 }
 }  // namespace quadw
 
-template <bool GRAM>
+template <bool GRAM, bool SMALL>
 __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(const SweepParams p) {
   using namespace quad;
   using quadp::Leaf;
@@ -576,6 +588,9 @@ __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(co
     }
   quad_afrag_init(p, afr);
   __syncthreads();
+  // m-tiles (j) / k-tiles (r) in use: compile-time (SMALL: J <= 16 and R <= 16), so the
+  // unrolled combine keeps no runtime guards; other shapes compute their zero padding
+  constexpr int mts = SMALL ? 1 : 2, nkt = SMALL ? 2 : 4;
   const int64_t nstream = (int64_t)gridDim.x * 4;
   const int J = p.J;
   const bool j32 = J == 32;
@@ -668,7 +683,8 @@ __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(co
         __syncwarp();
         quad_zero(acc);
 #pragma unroll
-        for (int kt = 0; kt < KT; ++kt) quad_mma_kt_r<NT>(X, Y, AH[kt], AL[kt], kt, 0, lane, acc);
+        for (int kt = 0; kt < KT; ++kt)
+          if (kt < nkt) quad_mma_kt_r<NT>(X, Y, AH[kt], AL[kt], kt, 0, lane, acc, mts);
       }
       const int st = t % quadw::NS;
       if (t >= quadw::NS) mbar_wait(empty + st, ((t / quadw::NS) - 1) & 1);
@@ -805,17 +821,17 @@ __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(co
   }
 }
 
-template <bool GRAM>
-int launch_quadw(const SweepParams &q, cudaStream_t s) {
+template <bool GRAM, bool SMALL>
+int launch_quadw_t(const SweepParams &q, cudaStream_t s) {
   const size_t sm = quadw::bytes();
   static bool set = false;
   if (!set) {
-    cudaFuncSetAttribute(factor_rows_quadw_kernel<GRAM>,
+    cudaFuncSetAttribute(factor_rows_quadw_kernel<GRAM, SMALL>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     set = true;
   }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quadw_kernel<GRAM>,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quadw_kernel<GRAM, SMALL>,
                                                     quadw::THREADS, sm) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
@@ -823,20 +839,26 @@ int launch_quadw(const SweepParams &q, cudaStream_t s) {
   const int64_t cap = (int64_t)sm_count() * per_sm;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
-  factor_rows_quadw_kernel<GRAM><<<(int)g, quadw::THREADS, sm, s>>>(q);
+  factor_rows_quadw_kernel<GRAM, SMALL><<<(int)g, quadw::THREADS, sm, s>>>(q);
   return check_launch("ft_factor_sweep_rows(quadw)");
 }
 
-int launch_quad(const SweepParams &q, cudaStream_t s) {
+template <bool GRAM>
+int launch_quadw(const SweepParams &q, cudaStream_t s) {
+  return q.J <= 16 && q.R <= 16 ? launch_quadw_t<GRAM, true>(q, s) : launch_quadw_t<GRAM, false>(q, s);
+}
+
+template <bool SMALL>
+int launch_quad_t(const SweepParams &q, cudaStream_t s) {
   const size_t sm = quad::bytes();
   static bool set = false;
   if (!set) {
-    cudaFuncSetAttribute(factor_rows_quad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(factor_rows_quad_kernel<SMALL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sm);
     set = true;
   }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quad_kernel,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quad_kernel<SMALL>,
                                                     quad::WPB * 32, sm) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
@@ -844,13 +866,23 @@ int launch_quad(const SweepParams &q, cudaStream_t s) {
   const int64_t cap = (int64_t)sm_count() * per_sm;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
-  factor_rows_quad_kernel<<<(int)g, quad::WPB * 32, sm, s>>>(q);
+  factor_rows_quad_kernel<SMALL><<<(int)g, quad::WPB * 32, sm, s>>>(q);
   return check_launch("ft_factor_sweep_rows(quad)");
 }
 
+int launch_quad(const SweepParams &q, cudaStream_t s) {
+  return q.J <= 16 && q.R <= 16 ? launch_quad_t<true>(q, s) : launch_quad_t<false>(q, s);
+}
+
+// the quad kernels run any J, R <= 32 (R % 4 == 0; padding columns are zero); J = R = 16 has
+// its own instantiation (one m-tile, two k-tiles).  FT_QUAD_J16=0 keeps J <= 16 on dual / ws.
 bool quad_ok(const SweepParams &p) {
-  return p.N == 3 && p.leaf_pc && p.row_leaf_ptr && p.J > 16 && p.J <= 32 && p.R <= 32 &&
-         (p.R & 3) == 0;
+  static const bool j16 = [] {
+    const char *e = getenv("FT_QUAD_J16");
+    return !(e && strcmp(e, "0") == 0);
+  }();
+  return p.N == 3 && p.leaf_pc && p.row_leaf_ptr && (p.J > 16 || j16) && p.J <= 32 &&
+         p.R <= 32 && (p.R & 3) == 0;
 }
 
 // ---- K4 "quad": the core-gradient row sweep over the leaf-major index ---------------------
@@ -1112,4 +1144,195 @@ __global__ void sum_pairs_f64(const double *__restrict__ partials, int nblocks, 
     out2[0] = a;
     out2[1] = b;
   }
+}
+
+// ---- K4 "quadp": the core sweep with the gathers one batch ahead ----------------------------
+// ncu on K4 quad: 43 % of the stall samples sat on the cp.async wait (the C-row gathers come
+// from L2 at ~8 TB/s aggregate, so their latency is long) with only one batch in flight per warp.
+// Here each warp keeps two batches of tiles: batch t+1's rows land while batch t is scored and
+// accumulated.  Tiles are 32 x 32 floats with the 16-B chunk index XOR-swizzled by the slot
+// (chunk c of slot k at c ^ (k & 7)), conflict-free both for lane-per-slot row reads and for
+// quarter-per-row reads, so two batches fit 6 warps x 2 blocks per SM.  Batch records (segment,
+// leaf range, segment-start flag) and the next segment's C_u row run ahead as in quadp.
+namespace cquadp {
+constexpr int TILE = 32 * 32;
+constexpr int WARP_FLOATS = 4 * TILE + 4 * 32 + 32;  // X[2], Y[2], C_u rows [4][32], e [32]
+constexpr int WPB = 6;
+constexpr size_t bytes() { return (size_t)WPB * WARP_FLOATS * 4; }
+__device__ __forceinline__ int sw(int k, int c) { return k * 32 + 4 * (c ^ (k & 7)); }
+}  // namespace cquadp
+
+__global__ void __launch_bounds__(cquadp::WPB * 32, 2) core_rows_quadp_kernel(const SweepParams p) {
+  using namespace cquadp;
+  using quadp::Leaf;
+  using quadp::Rec;
+  extern __shared__ float4 smem4[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int q = lane >> 3, l = lane & 7;
+  float *base = reinterpret_cast<float *>(smem4) + w * cquadp::WARP_FLOATS;  // X[s] = base + s TILE,
+  float *cus = base + 4 * cquadp::TILE;                                      // Y[s] = base + (2+s) TILE
+  float *es = cus + 128;
+  for (int k = lane; k < cquadp::WARP_FLOATS; k += 32) base[k] = 0.f;
+  __syncwarp();
+  const int J = p.J, R = p.R;
+  const bool j32 = J == 32;
+  const int64_t nstream = (int64_t)gridDim.x * cquadp::WPB * 4;
+  quadp::Cursor cur;
+  cur.row = ((int64_t)blockIdx.x * cquadp::WPB + w) * 4 + q - nstream;
+  cur.i = -1, cur.L0 = cur.Le = 0;
+  quadp::load_row_info(p, cur.row + nstream, cur.ni, cur.nLb, cur.nLe);
+  auto load_cu = [&](const Rec &r) {
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (r.newrow && r.nb > 0 && 4 * l < R)
+      v = *reinterpret_cast<const float4 *>(p.Cu + (int64_t)r.i * R + 4 * l);
+    return v;
+  };
+  const int gc = lane & 7, gs = lane >> 3;
+  const bool gok = gc < (R >> 2);
+  const float *cpre = p.Cpre[0] + 4 * gc, *cleaf = p.Cleaf + 4 * gc;
+  const int64_t Rs = R;
+  auto gather = [&](int set, const Leaf &d) {
+    float *X = base + set * TILE, *Y = base + (2 + set) * TILE;
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int s = 4 * it + gs;
+      const int pcs = __shfl_sync(FULL, d.pc, s), lcs = __shfl_sync(FULL, d.lc, s);
+      if (gok) {
+        cp_async16_s(smem_u32(X + sw(s, gc)), cpre + pcs * Rs);
+        cp_async16_s(smem_u32(Y + sw(s, gc)), cleaf + lcs * Rs);
+      }
+    }
+    cp_async_commit();
+  };
+  float acc[FT_MAX_RANK];  // lane r: acc[j] = sum_i g_i[r] A_u[i, j]
+#pragma unroll
+  for (int j = 0; j < FT_MAX_RANK; ++j) acc[j] = 0.f;
+  float2 g01 = make_float2(0.f, 0.f), g23 = make_float2(0.f, 0.f);
+  int gi = -1;  // row of the segment g belongs to
+  // acc += g_qq (x) A_u[gi_qq] for every quarter whose bit is set in em (lane 8 qq)
+  auto flush = [&](unsigned em) {
+    while (em) {
+      const int qq = (__ffs(em) - 1) >> 3;
+      em &= em - 1;
+      const int src = 8 * qq + (lane >> 2), comp = lane & 3;
+      const float c0 = __shfl_sync(FULL, g01.x, src), c1 = __shfl_sync(FULL, g01.y, src);
+      const float c2 = __shfl_sync(FULL, g23.x, src), c3 = __shfl_sync(FULL, g23.y, src);
+      const float gr = comp == 0 ? c0 : comp == 1 ? c1 : comp == 2 ? c2 : c3;
+      const float *ar = p.A + (int64_t)__shfl_sync(FULL, gi, 8 * qq) * J;
+      if (j32) {
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) {
+          const float4 a4 = __ldg(reinterpret_cast<const float4 *>(ar) + j4);
+          acc[4 * j4] = __fmaf_rn(gr, a4.x, acc[4 * j4]);
+          acc[4 * j4 + 1] = __fmaf_rn(gr, a4.y, acc[4 * j4 + 1]);
+          acc[4 * j4 + 2] = __fmaf_rn(gr, a4.z, acc[4 * j4 + 2]);
+          acc[4 * j4 + 3] = __fmaf_rn(gr, a4.w, acc[4 * j4 + 3]);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < FT_MAX_RANK; ++j)
+          if (j < J) acc[j] = __fmaf_rn(gr, __ldg(ar + j), acc[j]);
+      }
+    }
+  };
+
+  Rec r0 = quadp::next_batch(p, cur, nstream);
+  Leaf d0 = quadp::load_leaf(p, r0, l);
+  float4 cu0 = load_cu(r0);
+  gather(0, d0);
+  Rec r1 = quadp::next_batch(p, cur, nstream);
+  Leaf d1 = quadp::load_leaf(p, r1, l);
+  float4 cu1 = load_cu(r1);
+  for (int t = 0; __any_sync(FULL, r0.nb > 0); ++t) {
+    gather((t + 1) & 1, d1);  // batch t+1's rows fly while batch t is scored
+    const Rec r2 = quadp::next_batch(p, cur, nstream);
+    const Leaf d2 = quadp::load_leaf(p, r2, l);
+    const float4 cu2 = load_cu(r2);
+    // a quarter starting a segment flushes the previous one and installs its C_u row
+    flush(__ballot_sync(FULL, r0.newrow && r0.nb > 0 && gi >= 0 && l == 0));
+    if (r0.newrow && r0.nb > 0) {
+      g01 = g23 = make_float2(0.f, 0.f);
+      gi = r0.i;
+      *reinterpret_cast<float4 *>(cus + 32 * q + 4 * l) = cu0;
+    }
+    cp_async_wait_one();
+    __syncwarp();
+    const float *X = base + (t & 1) * TILE, *Y = base + (2 + (t & 1)) * TILE;
+    {  // lane = slot: s = C_u[i_q] . (X * Y), e = x - s
+      const float4 *cr = reinterpret_cast<const float4 *>(cus + 32 * q);
+      float2 s01 = make_float2(0.f, 0.f), s23 = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float4 xv = *reinterpret_cast<const float4 *>(X + sw(lane, c));
+        const float4 yv = *reinterpret_cast<const float4 *>(Y + sw(lane, c));
+        const float4 cv = cr[c];
+        s01 = ffma2(fmul2(make_float2(xv.x, xv.y), make_float2(yv.x, yv.y)),
+                    make_float2(cv.x, cv.y), s01);
+        s23 = ffma2(fmul2(make_float2(xv.z, xv.w), make_float2(yv.z, yv.w)),
+                    make_float2(cv.z, cv.w), s23);
+      }
+      const float s = (s01.x + s01.y) + (s23.x + s23.y);
+      es[lane] = l < r0.nb ? d0.x - s : 0.f;
+    }
+    __syncwarp();
+    {  // quarter lanes over r: g_q += sum_k e_k cross_k
+      const int nbmax = __reduce_max_sync(FULL, (unsigned)r0.nb);
+#pragma unroll
+      for (int k = 0; k < quad::QB; ++k) {
+        if (k >= nbmax) break;
+        const int row = 8 * q + k;
+        const float4 xv = *reinterpret_cast<const float4 *>(X + row * 32 + 4 * (l ^ k));
+        const float4 yv = *reinterpret_cast<const float4 *>(Y + row * 32 + 4 * (l ^ k));
+        const float ek = es[row];
+        const float2 e2 = make_float2(ek, ek);
+        g01 = ffma2(e2, fmul2(make_float2(xv.x, xv.y), make_float2(yv.x, yv.y)), g01);
+        g23 = ffma2(e2, fmul2(make_float2(xv.z, xv.w), make_float2(yv.z, yv.w)), g23);
+      }
+    }
+    __syncwarp();  // tiles of set t & 1 and es read before batch t+2's gathers / scores
+    r0 = r1, d0 = d1, cu0 = cu1;
+    r1 = r2, d1 = d2, cu1 = cu2;
+  }
+  flush(__ballot_sync(FULL, gi >= 0 && l == 0));
+  cp_async_wait_all();
+  // ---- fixed-order block reduction -> partials[block] (reuses the staging tiles) ----
+  __syncthreads();
+  const int RJ = R * J;
+  float *red = reinterpret_cast<float *>(smem4);
+  if (lane < R) {
+#pragma unroll
+    for (int j = 0; j < FT_MAX_RANK; ++j)
+      if (j < J) red[w * cquadp::WARP_FLOATS + lane * J + j] = acc[j];
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < RJ; k += blockDim.x) {
+    float s = 0.f;
+    for (int ww = 0; ww < cquadp::WPB; ++ww) s += red[ww * cquadp::WARP_FLOATS + k];
+    p.partials[(int64_t)blockIdx.x * RJ + k] = s;
+  }
+}
+
+int core_quadp_grid(const SweepParams &p) {
+  const size_t sm = cquadp::bytes();
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(core_rows_quadp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
+    set = true;
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, core_rows_quadp_kernel,
+                                                    cquadp::WPB * 32, sm) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  int64_t g = (p.nrows + 4 * cquadp::WPB - 1) / (4 * cquadp::WPB);
+  const int64_t cap = (int64_t)sm_count() * per_sm;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+int launch_core_quadp(const SweepParams &p, int g, cudaStream_t s) {
+  core_rows_quadp_kernel<<<g, cquadp::WPB * 32, cquadp::bytes(), s>>>(p);
+  return check_launch("ft_core_sweep_rows(quadp)");
 }

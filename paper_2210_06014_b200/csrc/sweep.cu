@@ -1945,9 +1945,9 @@ int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
   // auto, by rows per resident warp slot: many rows -> dual (Netflix modes 0/1: 7.5 ms);
   // few long rows -> warp-specialised at order 3 (mode 2: 8.4 vs 8.8 gram, 13.4 dual), else gram
   // quad / quadp: order 3, 16 < J <= 32, leaf-major index
-  if (variant >= 8 && variant <= 11 && !(RP == 32 && quad_ok(p))) variant = 5;
+  if (variant >= 8 && variant <= 11 && !quad_ok(p)) variant = 5;
   if (variant == 5) {
-    if (RP == 32 && quad_ok(p))  // many rows: quad; few long rows: quadw (warp-specialised)
+    if (quad_ok(p))  // many rows: quad; few long rows: quadw (warp-specialised)
       variant = p.nrows >= (int64_t)2 * sm_count() * quad::WPB * 4 ? 8 : 10;
     else
       variant = p.nrows >= (int64_t)2 * sm_count() * 16 ? 4 : (p.N == 3 ? 7 : 0);
@@ -2080,10 +2080,13 @@ extern "C" int ft_core_sweep_rows(const ft_tree_t *tree, const ft_model_t *model
   if (!partials || !nblocks_out) return fail(FT_ERR_ARG, "null partials");
   p.partials = partials;
   // FT_CORE_KERNEL=rows forces the one-row-per-warp kernel; default: quad when it applies
-  static const bool core_rows_forced = [] {
+  static const int core_kind = [] {  // 0 auto (quadp), 1 rows, 2 quad
     const char *e = getenv("FT_CORE_KERNEL");
-    return e && strcmp(e, "rows") == 0;
+    if (e && strcmp(e, "rows") == 0) return 1;
+    if (e && strcmp(e, "quad") == 0) return 2;
+    return 0;
   }();
+  const bool core_rows_forced = core_kind == 1;
   // quad walks the row SEGMENTS (rows cut at <= 512 leaves: the core gradient is a sum over a
   // row's leaves), so few long rows fill the GPU too (Netflix mode 2: 2,182 rows -> 89 K
   // segments); without segments it needs rows to fill its 4-rows-per-warp slots
@@ -2095,7 +2098,8 @@ extern "C" int ft_core_sweep_rows(const ft_tree_t *tree, const ft_model_t *model
     p.row_coord = p.seg_coord;
     p.row_leaf_ptr = p.seg_leaf_ptr;
   }
-  const int g = use_quad ? core_quad_grid(p)
+  const bool use_quadp = use_quad && core_kind == 0;
+  const int g = use_quadp ? core_quadp_grid(p) : use_quad ? core_quad_grid(p)
                 : p.R <= 8 ? core_rows_grid<8>(p) : p.R <= 16 ? core_rows_grid<16>(p)
                                                               : core_rows_grid<32>(p);
   if ((int64_t)g * p.R * p.J > partials_cap)
@@ -2103,6 +2107,7 @@ extern "C" int ft_core_sweep_rows(const ft_tree_t *tree, const ft_model_t *model
                 (long long)g * p.R * p.J);
   cudaStream_t s = as_stream(stream);
   *nblocks_out = g;
+  if (use_quadp) return launch_core_quadp(p, g, s);
   if (use_quad) return launch_core_quad(p, g, s);
   if (p.R <= 8) return launch_core_rows<8>(p, g, s);
   if (p.R <= 16) return launch_core_rows<16>(p, g, s);

@@ -96,11 +96,12 @@ print('ok')
     ((4000, 300, 50), 1_000_000, 32, 32, 2e-3),   # ~20 K-update rows in mode 2, 4000 short rows
     ((20000, 700, 9), 300_000, 24, 20, 1e-3),     # J < 32, R < 32 (padding), 1-3 leaf rows
     ((60000, 64, 64), 200_000, 32, 32, 5e-3),     # more rows than row slots (row switching)
+    ((4000, 300, 50), 500_000, 16, 12, 2e-3),     # J <= 16 (one m-tile), R = 12 (two k-tiles)
 ])
 @pytest.mark.parametrize("kernel", ["quad", "quadp", "quadw", "quadg"])
 def test_quad_sweeps_match_oracle(kernel, dims, nnz, J, R, lr):
     code = _CASE.format(dims=dims, nnz=nnz, J=J, R=R, lr=lr, seed=7)
-    env = dict(os.environ, FT_FACTOR_KERNEL=kernel)
+    env = dict(os.environ, FT_FACTOR_KERNEL=kernel, FT_QUAD_J16="1")
     out = subprocess.run([sys.executable, "-c", code], cwd=REPO, env=env, capture_output=True,
                          text=True, timeout=900)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]

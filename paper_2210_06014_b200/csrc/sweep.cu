@@ -2080,10 +2080,12 @@ extern "C" int ft_core_sweep_rows(const ft_tree_t *tree, const ft_model_t *model
   if (!partials || !nblocks_out) return fail(FT_ERR_ARG, "null partials");
   p.partials = partials;
   // FT_CORE_KERNEL=rows forces the one-row-per-warp kernel; default: quad when it applies
-  static const int core_kind = [] {  // 0 auto (quadp), 1 rows, 2 quad
+  // FT_CORE_KERNEL: auto (quad), rows, quadp (gathers one batch ahead; measured slower --
+  // 3.4-3.7 vs 3.1-3.2 ms per Netflix mode: K4 is bound by L2 throughput, not gather latency)
+  static const int core_kind = [] {  // 0 auto (quad), 1 rows, 3 quadp
     const char *e = getenv("FT_CORE_KERNEL");
     if (e && strcmp(e, "rows") == 0) return 1;
-    if (e && strcmp(e, "quad") == 0) return 2;
+    if (e && strcmp(e, "quadp") == 0) return 3;
     return 0;
   }();
   const bool core_rows_forced = core_kind == 1;
@@ -2098,7 +2100,7 @@ extern "C" int ft_core_sweep_rows(const ft_tree_t *tree, const ft_model_t *model
     p.row_coord = p.seg_coord;
     p.row_leaf_ptr = p.seg_leaf_ptr;
   }
-  const bool use_quadp = use_quad && core_kind == 0;
+  const bool use_quadp = use_quad && core_kind == 3;
   const int g = use_quadp ? core_quadp_grid(p) : use_quad ? core_quad_grid(p)
                 : p.R <= 8 ? core_rows_grid<8>(p) : p.R <= 16 ? core_rows_grid<16>(p)
                                                               : core_rows_grid<32>(p);

@@ -101,7 +101,8 @@ print('ok')
 @pytest.mark.parametrize("kernel", ["quad", "quadp", "quadw", "quadg"])
 def test_quad_sweeps_match_oracle(kernel, dims, nnz, J, R, lr):
     code = _CASE.format(dims=dims, nnz=nnz, J=J, R=R, lr=lr, seed=7)
-    env = dict(os.environ, FT_FACTOR_KERNEL=kernel, FT_QUAD_J16="1")
+    env = dict(os.environ, FT_FACTOR_KERNEL=kernel, FT_QUAD_J16="1",
+               FT_CORE_KERNEL="quadp" if kernel == "quadw" else "auto")
     out = subprocess.run([sys.executable, "-c", code], cwd=REPO, env=env, capture_output=True,
                          text=True, timeout=900)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]

@@ -1,6 +1,6 @@
 timeout 900 python -m pytest tests/test_quad_gpu.py -x -q 2>&1 | tail -2
 rm -f gpurun_out/b_*.json
-for c in ${CONFIGS:-netflix32 netflix16}; do
+for c in ${CONFIGS:-netflix32}; do
   timeout 900 python bench.py --config $c --no-cpu --no-e2e > gpurun_out/b_$c.json 2>/dev/null; echo $c $?
 done
 for f in gpurun_out/b_*.json; do python -c "

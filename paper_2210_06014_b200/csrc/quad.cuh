@@ -167,8 +167,11 @@ __device__ __forceinline__ void quad_chain_step_v(float (&a)[4], const float4 v,
   a[3] = __fmaf_rn(lre, v.w, a23.y);
 }
 
-template <bool SMALL>
-__global__ void __launch_bounds__(quad::WPB * 32, 2) factor_rows_quad_kernel(const SweepParams p) {
+// AREG: the Bt^T fragments live in registers (64 per lane) instead of being re-read from shared
+// memory per batch -- the quad kernels are L1/shared-memory-bound (ncu L1 86-88 %), and the
+// per-batch fragment reads are ~20 % of that traffic; the register cost drops the block to 6 warps.
+template <bool SMALL, int WPBT, bool AREG>
+__global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quad_kernel(const SweepParams p) {
   using namespace quad;
   extern __shared__ float4 smem4[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -185,9 +188,19 @@ __global__ void __launch_bounds__(quad::WPB * 32, 2) factor_rows_quad_kernel(con
   // m-tiles (j) / k-tiles (r) in use: compile-time (SMALL: J <= 16 and R <= 16), so the
   // unrolled combine keeps no runtime guards; other shapes compute their zero padding
   constexpr int mts = SMALL ? 1 : 2, nkt = SMALL ? 2 : 4;
+  uint4 AH[KT][MT], AL[KT][MT];
+  if (AREG) {
+#pragma unroll
+    for (int kt = 0; kt < KT; ++kt)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        AH[kt][mt] = afr[(mt * KT + kt) * 32 + lane];
+        AL[kt][mt] = afr[KT * MT * 32 + (mt * KT + kt) * 32 + lane];
+      }
+  }
 
-  const int64_t nstream = (int64_t)gridDim.x * quad::WPB * 4;
-  int64_t row = ((int64_t)blockIdx.x * quad::WPB + w) * 4 + q;
+  const int64_t nstream = (int64_t)gridDim.x * WPBT * 4;
+  int64_t row = ((int64_t)blockIdx.x * WPBT + w) * 4 + q;
   const int J = p.J;
   const bool j32 = J == 32;
   // current row (ci < 0: none) and the next row of this quarter's stream, one row ahead
@@ -288,8 +301,13 @@ __global__ void __launch_bounds__(quad::WPB * 32, 2) factor_rows_quad_kernel(con
     float acc[2][4][4];
     quad_zero(acc);
 #pragma unroll
-    for (int kt = 0; kt < KT; ++kt)
-      if (kt < nkt) quad_mma_kt<NT>(X, Y, afr, kt, 0, lane, acc, mts);
+    for (int kt = 0; kt < KT; ++kt) {
+      if (kt >= nkt) break;
+      if (AREG)
+        quad_mma_kt_r<NT>(X, Y, AH[kt], AL[kt], kt, 0, lane, acc, mts);
+      else
+        quad_mma_kt<NT>(X, Y, afr, kt, 0, lane, acc, mts);
+    }
     __syncwarp();  // every lane's fragments are read before V overwrites X
     quad_store_v(V, acc, lane);
     __syncwarp();
@@ -848,30 +866,37 @@ int launch_quadw(const SweepParams &q, cudaStream_t s) {
   return q.J <= 16 && q.R <= 16 ? launch_quadw_t<GRAM, true>(q, s) : launch_quadw_t<GRAM, false>(q, s);
 }
 
-template <bool SMALL>
+template <bool SMALL, int WPBT, bool AREG>
 int launch_quad_t(const SweepParams &q, cudaStream_t s) {
-  const size_t sm = quad::bytes();
+  const size_t sm = (size_t)quad::BFRAG_U4 * 16 + (size_t)WPBT * quad::WARP_FLOATS * 4;
   static bool set = false;
   if (!set) {
-    cudaFuncSetAttribute(factor_rows_quad_kernel<SMALL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sm);
+    cudaFuncSetAttribute(factor_rows_quad_kernel<SMALL, WPBT, AREG>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     set = true;
   }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quad_kernel<SMALL>,
-                                                    quad::WPB * 32, sm) != cudaSuccess ||
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quad_kernel<SMALL, WPBT, AREG>,
+                                                    WPBT * 32, sm) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
-  int64_t g = (q.nrows + 4 * quad::WPB - 1) / (4 * quad::WPB);
+  int64_t g = (q.nrows + 4 * WPBT - 1) / (4 * WPBT);
   const int64_t cap = (int64_t)sm_count() * per_sm;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
-  factor_rows_quad_kernel<SMALL><<<(int)g, quad::WPB * 32, sm, s>>>(q);
+  factor_rows_quad_kernel<SMALL, WPBT, AREG><<<(int)g, WPBT * 32, sm, s>>>(q);
   return check_launch("ft_factor_sweep_rows(quad)");
 }
 
 int launch_quad(const SweepParams &q, cudaStream_t s) {
-  return q.J <= 16 && q.R <= 16 ? launch_quad_t<true>(q, s) : launch_quad_t<false>(q, s);
+  static const int areg = [] {  // FT_QUAD_AREG=1: Bt^T fragments in registers, 6 warps / block
+    const char *e = getenv("FT_QUAD_AREG");
+    return e && strcmp(e, "1") == 0 ? 1 : 0;
+  }();
+  const bool small = q.J <= 16 && q.R <= 16;
+  if (areg) return small ? launch_quad_t<true, 6, true>(q, s) : launch_quad_t<false, 6, true>(q, s);
+  return small ? launch_quad_t<true, quad::WPB, false>(q, s)
+               : launch_quad_t<false, quad::WPB, false>(q, s);
 }
 
 // the quad kernels run any J, R <= 32 (R % 4 == 0; padding columns are zero); J = R = 16 has

@@ -45,3 +45,27 @@ tcfg = ft.TrainConfig(epochs=1)
 timed("epoch (no eval)", lambda: [T.update_factor_mode(model, forest, cache, n, tcfg, ft.OpCounter()) for n in range(3)]
       + [T.update_core_mode(model, forest, cache, n, tcfg, ft.OpCounter()) for n in range(3)])
 timed("evaluate train", lambda: ft.evaluate(model, dev, cache))
+
+# the bench's e2e step, part by part (CUDA events on the current stream)
+init_f, init_c = [a.clone() for a in model.factors], [b.clone() for b in model.cores_t]
+ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
+for rep in range(3):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ev[0].record()
+    dev2 = ft.DeviceCoo(dims, idx_d, vals_d)
+    m2 = ft.Model(dims, (32,) * 3, 32, init_f, init_c)
+    ev[1].record()
+    f2 = ft.build_forest(dev2, 128, compact=True)
+    ev[2].record()
+    c2 = ft.precompute_cache(m2, ft.OpCounter())
+    ev[3].record()
+    met = T.run_epoch(m2, f2, c2, dev2, tcfg, ft.OpCounter(), 1, None, evaluate_metrics=False)
+    ev[4].record()
+    r = ft.evaluate(m2, dev2, c2, f2)
+    ev[5].record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    names = ["model/coo", "build_forest", "cache", "epoch", "evaluate(tree)"]
+    print("e2e step:", " ".join(f"{n} {ev[i].elapsed_time(ev[i + 1]):.2f}" for i, n in enumerate(names)),
+          f"| wall {1e3 * wall:.2f} ms", flush=True)

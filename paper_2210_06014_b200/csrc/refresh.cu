@@ -5,6 +5,9 @@
 // through shared memory with coalesced 128-bit loads, computes the 32 x R outputs with the
 // reference's sequential-j accumulation order, and writes C back through shared memory as one
 // contiguous, coalesced store.
+#include <string.h>
+#include <stdlib.h>
+
 #include "ft_common.cuh"
 
 namespace ft {
@@ -72,6 +75,234 @@ __global__ void __launch_bounds__(WARPS * 32)
   }
 }
 
+// ---- K2 on the 5th-generation tensor cores (tcgen05, kind::tf32) ----------------------------
+// C (I x R) = A (I x J) * Bt^T: M = 128 rows of A per tile, N = R, K = J (zero-padded to 32).
+// Operands in shared memory, K-major with the 128-byte swizzle (one 128-B row of A per tile row:
+// 16-B chunk c of row r at c ^ (r & 7)); accumulator in TMEM (R fp32 columns x 128 lanes).
+// 3xTF32 (A_lo Bt_hi + A_hi Bt_lo + A_hi Bt_hi, truncation split as in K3b) keeps fp32
+// accuracy.  Per tile: the 128 threads each load one row of A (guard max fused), split it into
+// the hi / lo tiles; one elected thread issues 3 x K/8 tcgen05.mma and commits to an mbarrier;
+// each warp reads its 32 TMEM lanes (tcgen05.ld 32x32b) and stores its rows of C to every
+// destination.  Persistent grid, one tile in flight per CTA, several CTAs per SM.
+namespace tc {
+constexpr int M = 128;
+constexpr int TILE_BYTES = M * 128;   // 128 rows x 32 fp32
+constexpr int B_BYTES = 32 * 128;     // up to 32 rows (R) x 32 fp32
+constexpr size_t SMEM = 2 * TILE_BYTES + 2 * B_BYTES + 1024 + 64;  // + alignment slack, barrier
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t hi_bits(float x) { return __float_as_uint(x) & 0xffffe000u; }
+// shared-memory matrix descriptor, K-major, 128-B swizzle, 8-row groups 1024 B apart
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr & 0x3FFFF) >> 4);        // start address
+  d |= (uint64_t)1 << 16;                        // leading byte offset (unused for SW128 K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;              // stride byte offset: next 8-row group
+  d |= (uint64_t)1 << 46;                        // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                        // SWIZZLE_128B
+  return d;
+}
+__device__ __forceinline__ void mma_tf32_tc(uint32_t tmem_d, uint64_t da, uint64_t db,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+}  // namespace tc
+
+__global__ void __launch_bounds__(128) refresh_tc_kernel(int64_t I, int J, int R,
+                                                         const float *__restrict__ A,
+                                                         const float *__restrict__ Bt, Dsts dst,
+                                                         uint32_t *guard) {
+  using namespace tc;
+  extern __shared__ __align__(1024) uint8_t tc_smem[];
+  // 1024-B aligned operand tiles (the 128-B swizzle pattern repeats every 8 rows = 1024 B)
+  uint8_t *base = reinterpret_cast<uint8_t *>(
+      (reinterpret_cast<uintptr_t>(tc_smem) + 1023) & ~(uintptr_t)1023);
+  uint8_t *a_hi = base, *a_lo = base + TILE_BYTES;
+  uint8_t *b_hi = base + 2 * TILE_BYTES, *b_lo = b_hi + B_BYTES;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(b_lo + B_BYTES);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 1);
+  const int tid = threadIdx.x, w = tid >> 5;
+
+  // Bt (R x J) -> hi / lo tiles, row r = output column, zero-padded to 32 rows x 32 k
+  for (int e = tid; e < 32 * 8; e += 128) {
+    const int r = e >> 3, c = e & 7;
+    float v[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int j = 4 * c + t;
+      v[t] = (r < R && j < J) ? __ldg(Bt + r * J + j) : 0.f;
+    }
+    const uint32_t off = r * 128 + ((c ^ (r & 7)) << 4);
+    uint4 h, l;
+    h.x = hi_bits(v[0]), h.y = hi_bits(v[1]), h.z = hi_bits(v[2]), h.w = hi_bits(v[3]);
+    l.x = __float_as_uint(v[0] - __uint_as_float(h.x));
+    l.y = __float_as_uint(v[1] - __uint_as_float(h.y));
+    l.z = __float_as_uint(v[2] - __uint_as_float(h.z));
+    l.w = __float_as_uint(v[3] - __uint_as_float(h.w));
+    *reinterpret_cast<uint4 *>(b_hi + off) = h;
+    *reinterpret_cast<uint4 *>(b_lo + off) = l;
+  }
+  if (w == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;\n" ::"r"(
+        smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  // kind::tf32, D fp32, A / B tf32 K-major, N = 32 (padded R), M = 128
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+  const int ksteps = (J + 7) >> 3;
+  uint32_t phase = 0, gmax = 0;
+  const int64_t ntiles = (I + M - 1) / M;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t row = tile * M + tid;
+    {  // this thread's row of A -> hi / lo (swizzled), guard max
+      float v[32];
+      if (row < I) {
+        const float *ar = A + row * J;
+        if (J == 32) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float4 q = __ldcs(reinterpret_cast<const float4 *>(ar) + c);
+            v[4 * c] = q.x, v[4 * c + 1] = q.y, v[4 * c + 2] = q.z, v[4 * c + 3] = q.w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = j < J ? __ldcs(ar + j) : 0.f;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = 0.f;
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const uint32_t off = tid * 128 + ((c ^ (tid & 7)) << 4);
+        uint4 h, l;
+        h.x = hi_bits(v[4 * c]), h.y = hi_bits(v[4 * c + 1]);
+        h.z = hi_bits(v[4 * c + 2]), h.w = hi_bits(v[4 * c + 3]);
+        l.x = __float_as_uint(v[4 * c] - __uint_as_float(h.x));
+        l.y = __float_as_uint(v[4 * c + 1] - __uint_as_float(h.y));
+        l.z = __float_as_uint(v[4 * c + 2] - __uint_as_float(h.z));
+        l.w = __float_as_uint(v[4 * c + 3] - __uint_as_float(h.w));
+        *reinterpret_cast<uint4 *>(a_hi + off) = h;
+        *reinterpret_cast<uint4 *>(a_lo + off) = l;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) gmax = max(gmax, abs_bits(v[4 * c + t]));
+      }
+    }
+    // generic-proxy smem writes -> visible to the tensor core (async proxy)
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    if (tid == 0) {
+      const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo);
+      const uint32_t bh = smem_u32(b_hi), bl = smem_u32(b_lo);
+      uint32_t acc = 0;
+      for (int k = 0; k < ksteps; ++k) {  // K = 8 tf32 = 32 B per step inside the 128-B row
+        const uint32_t o = 32 * k;
+        mma_tf32_tc(tmem, sw128_desc(al + o), sw128_desc(bh + o), idesc, acc);
+        acc = 1;
+        mma_tf32_tc(tmem, sw128_desc(ah + o), sw128_desc(bl + o), idesc, 1);
+        mma_tf32_tc(tmem, sw128_desc(ah + o), sw128_desc(bh + o), idesc, 1);
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                       smem_u32(bar))
+                   : "memory");
+    }
+    // wait for the accumulator
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+    phase ^= 1;
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    // TMEM lanes 32w..32w+31 = rows of this warp; 32 columns = C[row][0..31]
+    uint32_t d[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+        : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]),
+          "=r"(d[7]), "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]),
+          "=r"(d[14]), "=r"(d[15]), "=r"(d[16]), "=r"(d[17]), "=r"(d[18]), "=r"(d[19]),
+          "=r"(d[20]), "=r"(d[21]), "=r"(d[22]), "=r"(d[23]), "=r"(d[24]), "=r"(d[25]),
+          "=r"(d[26]), "=r"(d[27]), "=r"(d[28]), "=r"(d[29]), "=r"(d[30]), "=r"(d[31])
+        : "r"(tmem + ((uint32_t)(32 * w) << 16)));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+    if (row < I) {
+      for (int q = 0; q < dst.n; ++q) {
+        float *out = dst.p[q] + row * R;
+        if (R == 32) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            __stcs(reinterpret_cast<float4 *>(out) + c,
+                   make_float4(__uint_as_float(d[4 * c]), __uint_as_float(d[4 * c + 1]),
+                               __uint_as_float(d[4 * c + 2]), __uint_as_float(d[4 * c + 3])));
+        } else {
+#pragma unroll
+          for (int r = 0; r < 32; ++r)
+            if (r < R) __stcs(out + r, __uint_as_float(d[r]));
+        }
+      }
+    }
+    // TMEM reads and smem tile reads are done before the next tile overwrites them
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  }
+  if (guard) guard_max(guard, gmax);
+  __syncthreads();
+  if (w == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;\n" ::"r"(tmem));
+}
+
+// tensor-core refresh unless FT_REFRESH=simt (the fp32 CUDA-core kernel above, which keeps the
+// reference's sequential-j accumulation order); both need J, R <= 32
+bool use_tc_refresh(int R) {
+  static const bool simt = [] {
+    const char *e = getenv("FT_REFRESH");
+    return e && strcmp(e, "simt") == 0;
+  }();
+  return !simt && R >= 1;
+}
+
+int launch_refresh(int64_t I, int J, int R, const float *A, const float *Bt, const Dsts &d,
+                   uint32_t *guard, cudaStream_t s) {
+  if (use_tc_refresh(R)) {
+    static bool set = false;
+    if (!set) {
+      cudaFuncSetAttribute(refresh_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)tc::SMEM);
+      set = true;
+    }
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refresh_tc_kernel, 128, tc::SMEM) !=
+            cudaSuccess ||
+        per_sm < 1)
+      per_sm = 1;
+    int64_t g = (I + tc::M - 1) / tc::M;
+    const int64_t cap = (int64_t)sm_count() * per_sm;
+    if (g > cap) g = cap;
+    refresh_tc_kernel<<<(unsigned)g, 128, tc::SMEM, s>>>(I, J, R, A, Bt, d, guard);
+    return check_launch("ft_refresh(tcgen05)");
+  }
+  const int64_t blocks = (I + WARPS * TILE - 1) / (WARPS * TILE);
+  refresh_kernel<<<(unsigned)blocks, WARPS * 32, 0, s>>>(I, J, R, A, Bt, d, guard);
+  return check_launch("ft_refresh");
+}
+
 }  // namespace
 }  // namespace ft
 
@@ -83,12 +314,10 @@ extern "C" int ft_refresh(int64_t I, int32_t J, int32_t R, const float *A, const
                 (long long)I, J, R);
   if (I == 0) return FT_OK;
   if (!A || !Bt || !C) return fail(FT_ERR_ARG, "ft_refresh: null pointer");
-  const int64_t blocks = (I + WARPS * TILE - 1) / (WARPS * TILE);
   Dsts d{};
   d.p[0] = C;
   d.n = 1;
-  refresh_kernel<<<(unsigned)blocks, WARPS * 32, 0, as_stream(stream)>>>(I, J, R, A, Bt, d, guard);
-  return check_launch("ft_refresh");
+  return launch_refresh(I, J, R, A, Bt, d, guard, as_stream(stream));
 }
 
 extern "C" int ft_refresh_scatter(int64_t I, int32_t J, int32_t R, const float *A, const float *Bt,
@@ -108,7 +337,5 @@ extern "C" int ft_refresh_scatter(int64_t I, int32_t J, int32_t R, const float *
     d.p[k] = dsts[k];
   }
   d.n = ndst;
-  const int64_t blocks = (I + WARPS * TILE - 1) / (WARPS * TILE);
-  refresh_kernel<<<(unsigned)blocks, WARPS * 32, 0, as_stream(stream)>>>(I, J, R, A, Bt, d, guard);
-  return check_launch("ft_refresh_scatter");
+  return launch_refresh(I, J, R, A, Bt, d, guard, as_stream(stream));
 }

@@ -130,3 +130,37 @@ def test_sse_tree_matches_coo_evaluate(ft):
     other = ft.DeviceCoo(dims, dev.idx[:1000].contiguous(), dev.vals[:1000].contiguous())
     np.testing.assert_allclose(ft.evaluate(model, other, cache, forest),
                                ft.evaluate(model, other, cache), rtol=0)
+
+
+@pytest.mark.parametrize("I,J,R", [(1000, 32, 32), (130, 32, 32), (480_189, 32, 32),
+                                   (5000, 16, 16), (777, 24, 12), (300, 8, 8), (2182, 32, 20)])
+def test_refresh_tensor_core_matches_fp64(ft, I, J, R):
+    """K2 on tcgen05 (kind::tf32, 3xTF32, TMEM accumulator): C = A Bt^T against fp64 at the
+    contract's fp32-level accuracy, the fused guard (max |A| as IEEE bits) and the two-destination
+    scatter form used by the fused multi-GPU refresh."""
+    import ctypes
+
+    import torch
+    from paper_2210_06014_b200 import _lib
+
+    rng = np.random.default_rng(I + J + R)
+    A = rng.normal(size=(I, J)).astype(np.float32)
+    Bt = rng.normal(size=(R, J)).astype(np.float32)
+    ref = A.astype(np.float64) @ Bt.astype(np.float64).T
+    Ad, Bd = torch.from_numpy(A).cuda(), torch.from_numpy(Bt).cuda()
+    C = torch.full((I, R), float("nan"), device="cuda")
+    g = torch.zeros(1, dtype=torch.int32, device="cuda")
+    L = _lib.lib()
+    _lib.check(L.ft_refresh(I, J, R, Ad.data_ptr(), Bd.data_ptr(), C.data_ptr(), g.data_ptr(),
+                            _lib.stream_handle()), "ft_refresh")
+    got = C.cpu().numpy().astype(np.float64)
+    err = np.abs(got - ref).max() / np.abs(ref).max()
+    assert err < 2e-6, err
+    assert int(g.cpu().numpy().view(np.uint32)[0]) == int(np.abs(A).max().view(np.uint32))
+    C2 = torch.zeros((I, R), device="cuda")
+    tab = (ctypes.c_void_p * 2)(C.data_ptr(), C2.data_ptr())
+    C.zero_()
+    _lib.check(L.ft_refresh_scatter(I, J, R, Ad.data_ptr(), Bd.data_ptr(), tab, 2, None,
+                                    _lib.stream_handle()), "ft_refresh_scatter")
+    np.testing.assert_array_equal(C.cpu().numpy(), C2.cpu().numpy())
+    np.testing.assert_array_equal(C.cpu().numpy(), got.astype(np.float32))

@@ -66,7 +66,7 @@ typedef struct {
   /* Leaf-major index (optional, NULL = absent; filled by ft_tree_leaf_index).  Not reference
    * fields: derived once per tree so the row-owner kernels read every per-leaf operand with
    * plain coalesced loads instead of the fiber-window ballot -> fiber_coord dependent chain. */
-  const int32_t *leaf_pc;       /* [nnz]   level-1 coordinate of each leaf's fiber           */
+  const int32_t *leaf_pc;       /* [nnz x (N-2)] levels 1..N-2 of each leaf's fiber (N <= 6) */
   const int32_t *row_leaf_ptr;  /* [rows+1] first leaf of each root slice                    */
   /* Row segments for the core sweep (optional): every root slice cut into pieces of at most
    * `max_len` leaves (ft_tree_row_segments).  The core gradient is a sum over a row's leaves,
@@ -114,8 +114,9 @@ FT_API int ft_build_tree(int32_t N, int64_t nnz, const int64_t *dims, const int3
                   int32_t *row_fiber_ptr, int32_t *row_coord, int64_t *counts_out, void *stream);
 
 /* K1b Leaf-major index of a built tree (reads tree->fiber_ptr / fiber_coord / row_fiber_ptr):
- *   leaf_pc[L] = fiber_coord[f(L) * (N-1) + 1] for every leaf L of fiber f(L)  (csf inds[1]
- *   expanded to the leaves), row_leaf_ptr[r] = fiber_ptr[row_fiber_ptr[r]] for r <= rows.
+ *   leaf_pc[L * (N-2) + d] = fiber_coord[f(L) * (N-1) + 1 + d], d < N-2, for every leaf L of
+ *   fiber f(L) (the prefix levels 1..N-2 expanded to the leaves; orders 3-6 only), and
+ *   row_leaf_ptr[r] = fiber_ptr[row_fiber_ptr[r]] for r <= rows.
  * Either output may be NULL.  Asynchronous. */
 FT_API int ft_tree_leaf_index(const ft_tree_t *tree, int32_t *leaf_pc, int32_t *row_leaf_ptr,
                               void *stream);

@@ -27,6 +27,7 @@ from .errors import BuildError, ConfigError
 
 DEFAULT_FIBER_THRESHOLD = 128
 CORE_SEGMENT = 512  # max leaves per core-sweep row segment
+LEAF_INDEX_MAX_ORDER = 4  # orders with the per-leaf prefix coordinates (the quad kernels)
 
 
 @dataclass
@@ -249,16 +250,24 @@ def build_tree(tensor, root_mode: int, fiber_threshold=DEFAULT_FIBER_THRESHOLD,
 
 def add_leaf_index(tree: CsfTree, stream=None) -> CsfTree:
     """Derive the leaf-major index the row-owner kernels read (K1b, ft_tree_leaf_index):
-    ``leaf_pc`` (each leaf's level-1 coordinate) and ``row_leaf_ptr`` (first leaf of each root
-    slice).  Not reference fields; 4 bytes per leaf."""
+    ``leaf_pc`` (each leaf's prefix coordinates, levels 1..N-2, for orders 3-6) and
+    ``row_leaf_ptr`` (first leaf of each root slice).  Not reference fields."""
     import torch
 
     i32 = dict(dtype=torch.int32, device=tree.vals.device)
-    tree.leaf_pc = torch.empty(tree.nnz, **i32)
+    N = tree.order
+    # prefix levels per leaf (4 (N-2) bytes per leaf) up to LEAF_INDEX_MAX_ORDER: the quad
+    # kernels fold the prefix product level by level, which pays at order 4 (BASELINE order-4
+    # config: 362 -> 307 ms per epoch) but not at order 6 (237 -> 304 ms: five dependent gather
+    # rounds per batch); higher orders keep only the row index and use the fiber-walking kernels
+    import os
+
+    max_order = int(os.environ.get("FT_LEAF_INDEX_MAX_ORDER", LEAF_INDEX_MAX_ORDER))
+    tree.leaf_pc = torch.empty((tree.nnz, N - 2), **i32) if N <= min(max_order, 6) else None
     tree.row_leaf_ptr = torch.empty(tree.num_rows + 1, **i32)
     tree._view = None
     v = tree.view()
-    _lib.check(_lib.lib().ft_tree_leaf_index(ctypes.byref(v), tree.leaf_pc.data_ptr(),
+    _lib.check(_lib.lib().ft_tree_leaf_index(ctypes.byref(v), _lib.ptr(tree.leaf_pc),
                                              tree.row_leaf_ptr.data_ptr(),
                                              _lib.stream_handle(stream)), "ft_tree_leaf_index")
     tree._view = None

@@ -209,14 +209,17 @@ inline unsigned blocks_for(int64_t n, int t = 256) { return (unsigned)((n + t - 
 __global__ void leaf_pc_kernel(const int32_t *__restrict__ fiber_ptr,
                                const int32_t *__restrict__ fiber_coord, int64_t F, int N,
                                int32_t *__restrict__ leaf_pc) {
+  const int NP = N - 2;  // prefix levels 1..N-2 per leaf (<= 4)
   const int lane = threadIdx.x & 31;
   const int64_t f0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~(int64_t)31;
   const int64_t f = f0 + lane;
-  int lb = 0, le = 0, pc = 0;
+  int lb = 0, le = 0, pc[4] = {0, 0, 0, 0};
   if (f < F) {
     lb = __ldg(fiber_ptr + f);
     le = __ldg(fiber_ptr + f + 1);
-    pc = __ldg(fiber_coord + f * (N - 1) + 1);
+#pragma unroll
+    for (int d = 0; d < 4; ++d)
+      if (d < NP) pc[d] = __ldg(fiber_coord + f * (N - 1) + 1 + d);
   }
   const int first = __shfl_sync(0xffffffffu, lb, 0);
   int last = le;
@@ -231,8 +234,11 @@ __global__ void leaf_pc_kernel(const int32_t *__restrict__ fiber_ptr,
       const int lbm = __shfl_sync(0xffffffffu, lb, lo + step);
       if (lbm <= L && f0 + lo + step < F) lo += step;
     }
-    const int v = __shfl_sync(0xffffffffu, pc, lo);
-    if (L < last) leaf_pc[L] = v;
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      const int v = __shfl_sync(0xffffffffu, pc[d], lo);
+      if (d < NP && L < last) leaf_pc[(int64_t)L * NP + d] = v;
+    }
   }
 }
 
@@ -535,6 +541,7 @@ extern "C" int ft_tree_leaf_index(const ft_tree_t *tree, int32_t *leaf_pc, int32
   const int64_t F = tree->num_fibers, rows = tree->num_rows;
   if (leaf_pc && F > 0) {
     if (!tree->fiber_ptr || !tree->fiber_coord) return fail(FT_ERR_ARG, "null fiber arrays");
+    if (tree->order > 6) return fail(FT_ERR_UNSUPPORTED, "leaf index: order %d > 6", tree->order);
     leaf_pc_kernel<<<blocks_for(F), 256, 0, s>>>(tree->fiber_ptr, tree->fiber_coord, F,
                                                  tree->order, leaf_pc);
     if (int rc = check_launch("ft_tree_leaf_index(leaf_pc)")) return rc;

@@ -167,10 +167,60 @@ __device__ __forceinline__ void quad_chain_step_v(float (&a)[4], const float4 v,
   a[3] = __fmaf_rn(lre, v.w, a23.y);
 }
 
+
+// Order-N gathers into a warp's 32-slot X / Y tiles (row stride XSD floats): X <- prod over the
+// NPRE prefix levels of C_pre[d][pc_d] (gather, wait, multiply in place, level by level -- the
+// reference's left-to-right chain), Y <- C_leaf[lc].  pc[d] / lc: lane s holds slot s's
+// coordinates (0 for padding slots).  Returns with both tiles complete (cp.async waited).
+template <int NPRE, int XSD>
+__device__ __forceinline__ void quad_gather(const SweepParams &p, float *X, float *Y,
+                                            const int (&pc)[NPRE], int lc, int lane) {
+  const int gc = lane & 7, gs = lane >> 3;
+  const bool gok = gc < (p.R >> 2);
+  const int64_t Rs = p.R;
+  const uint32_t xs0 = smem_u32(X + gs * XSD + 4 * gc), ys0 = smem_u32(Y + gs * XSD + 4 * gc);
+  auto issue = [&](uint32_t dst0, const float *C, int coord) {
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int cs = __shfl_sync(FULL, coord, 4 * it + gs);
+      if (gok) cp_async16_s(dst0 + it * 4 * XSD * 4, C + 4 * gc + cs * Rs);
+    }
+  };
+  auto fold = [&]() {  // lane = slot: X[s] *= Y[s]
+    float4 *xr = reinterpret_cast<float4 *>(X + lane * XSD);
+    const float4 *yr = reinterpret_cast<const float4 *>(Y + lane * XSD);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const float4 x = xr[c], y = yr[c];
+      const float2 a = fmul2(make_float2(x.x, x.y), make_float2(y.x, y.y));
+      const float2 b = fmul2(make_float2(x.z, x.w), make_float2(y.z, y.w));
+      xr[c] = make_float4(a.x, a.y, b.x, b.y);
+    }
+  };
+  issue(xs0, p.Cpre[0], pc[0]);
+  if (NPRE == 1) {
+    issue(ys0, p.Cleaf, lc);
+    cp_async_wait_all();
+    __syncwarp();
+    return;
+  }
+#pragma unroll
+  for (int d = 1; d < NPRE; ++d) {
+    issue(ys0, p.Cpre[d], pc[d]);
+    cp_async_wait_all();
+    __syncwarp();
+    fold();
+    __syncwarp();
+  }
+  issue(ys0, p.Cleaf, lc);
+  cp_async_wait_all();
+  __syncwarp();
+}
+
 // AREG: the Bt^T fragments live in registers (64 per lane) instead of being re-read from shared
 // memory per batch -- the quad kernels are L1/shared-memory-bound (ncu L1 86-88 %), and the
 // per-batch fragment reads are ~20 % of that traffic; the register cost drops the block to 6 warps.
-template <bool SMALL, int WPBT, bool AREG>
+template <bool SMALL, int WPBT, bool AREG, int NPRE>
 __global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quad_kernel(const SweepParams p) {
   using namespace quad;
   extern __shared__ float4 smem4[];
@@ -238,20 +288,17 @@ __global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quad_kernel(const Sw
   };
   if (ci >= 0) load_row(ci);
   // leaf data of the batch about to run (prefetched one batch ahead; lanes past it: 0)
-  int plc = 0, ppc = 0;
+  int plc = 0, ppc[NPRE];
   float px = 0.f;
+#pragma unroll
+  for (int d = 0; d < NPRE; ++d) ppc[d] = 0;
   if (ci >= 0 && cL0 + l < cLe) {
     plc = __ldcs(p.leaf_coord + cL0 + l);
-    ppc = __ldcs(p.leaf_pc + cL0 + l);
+#pragma unroll
+    for (int d = 0; d < NPRE; ++d) ppc[d] = __ldcs(p.leaf_pc + (int64_t)(cL0 + l) * NPRE + d);
     px = __ldcs(p.vals + cL0 + l);
   }
   const float lr = p.lr;
-  // gather lanes: slot-in-4 and float4 column
-  const int gc = lane & 7, gs = lane >> 3;
-  const bool gok = gc < (p.R >> 2);
-  const uint32_t xs0 = smem_u32(X + gs * XS + 4 * gc), ys0 = smem_u32(Y + gs * XS + 4 * gc);
-  const float *cpre = p.Cpre[0] + 4 * gc, *cleaf = p.Cleaf + 4 * gc;
-  const int64_t Rs = p.R;
 
   for (;;) {
     // ---- a quarter whose row is exhausted writes it back and moves to its next row ----
@@ -273,7 +320,10 @@ __global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quad_kernel(const Sw
     }
     if (!__any_sync(FULL, ci >= 0)) break;
     const int nb = ci >= 0 ? min(QB, cLe - cL0) : 0;
-    const int lc = plc, pc = ppc;
+    const int lc = plc;
+    int pc[NPRE];
+#pragma unroll
+    for (int d = 0; d < NPRE; ++d) pc[d] = ppc[d];
     const float lrk = l < nb ? lr : 0.f;
     const float ck = -lrk * p.reg;
     meta[q * MQ + l] = make_float4(l < nb ? px : 0.f, lrk, ck, ck);
@@ -282,21 +332,13 @@ __global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quad_kernel(const Sw
       const int pos = same ? cL0 + nb : nLb, end = same ? cLe : nLe;
       const bool ok = ci >= 0 && (same || ni >= 0) && pos + l < end;
       plc = ok ? __ldcs(p.leaf_coord + pos + l) : 0;
-      ppc = ok ? __ldcs(p.leaf_pc + pos + l) : 0;
+#pragma unroll
+      for (int d = 0; d < NPRE; ++d)
+        ppc[d] = ok ? __ldcs(p.leaf_pc + (int64_t)(pos + l) * NPRE + d) : 0;
       px = ok ? __ldcs(p.vals + pos + l) : 0.f;
     }
     // ---- gathers: slot s = 4 it + gs holds the leaf of lane s (quarter s / 8) ----
-#pragma unroll
-    for (int it = 0; it < 8; ++it) {
-      const int s = 4 * it + gs;
-      const int pcs = __shfl_sync(FULL, pc, s), lcs = __shfl_sync(FULL, lc, s);
-      if (gok) {
-        cp_async16_s(xs0 + it * 4 * XS * 4, cpre + pcs * Rs);
-        cp_async16_s(ys0 + it * 4 * XS * 4, cleaf + lcs * Rs);
-      }
-    }
-    cp_async_wait_all();
-    __syncwarp();
+    quad_gather<NPRE, XS>(p, X, Y, pc, lc, lane);
     // ---- V^T = Bt_u^T * (X * Y)^T, 3xTF32 ----
     float acc[2][4][4];
     quad_zero(acc);
@@ -866,17 +908,17 @@ int launch_quadw(const SweepParams &q, cudaStream_t s) {
   return q.J <= 16 && q.R <= 16 ? launch_quadw_t<GRAM, true>(q, s) : launch_quadw_t<GRAM, false>(q, s);
 }
 
-template <bool SMALL, int WPBT, bool AREG>
+template <bool SMALL, int WPBT, bool AREG, int NPRE>
 int launch_quad_t(const SweepParams &q, cudaStream_t s) {
   const size_t sm = (size_t)quad::BFRAG_U4 * 16 + (size_t)WPBT * quad::WARP_FLOATS * 4;
   static bool set = false;
   if (!set) {
-    cudaFuncSetAttribute(factor_rows_quad_kernel<SMALL, WPBT, AREG>,
+    cudaFuncSetAttribute(factor_rows_quad_kernel<SMALL, WPBT, AREG, NPRE>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     set = true;
   }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quad_kernel<SMALL, WPBT, AREG>,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quad_kernel<SMALL, WPBT, AREG, NPRE>,
                                                     WPBT * 32, sm) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
@@ -884,7 +926,7 @@ int launch_quad_t(const SweepParams &q, cudaStream_t s) {
   const int64_t cap = (int64_t)sm_count() * per_sm;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
-  factor_rows_quad_kernel<SMALL, WPBT, AREG><<<(int)g, WPBT * 32, sm, s>>>(q);
+  factor_rows_quad_kernel<SMALL, WPBT, AREG, NPRE><<<(int)g, WPBT * 32, sm, s>>>(q);
   return check_launch("ft_factor_sweep_rows(quad)");
 }
 
@@ -894,9 +936,20 @@ int launch_quad(const SweepParams &q, cudaStream_t s) {
     return e && strcmp(e, "1") == 0 ? 1 : 0;
   }();
   const bool small = q.J <= 16 && q.R <= 16;
-  if (areg) return small ? launch_quad_t<true, 6, true>(q, s) : launch_quad_t<false, 6, true>(q, s);
-  return small ? launch_quad_t<true, quad::WPB, false>(q, s)
-               : launch_quad_t<false, quad::WPB, false>(q, s);
+  if (q.N > 3) {  // order 4..6: prefix products folded level by level (quad_gather)
+    switch (q.N) {
+      case 4: return small ? launch_quad_t<true, quad::WPB, false, 2>(q, s)
+                           : launch_quad_t<false, quad::WPB, false, 2>(q, s);
+      case 5: return small ? launch_quad_t<true, quad::WPB, false, 3>(q, s)
+                           : launch_quad_t<false, quad::WPB, false, 3>(q, s);
+      default: return small ? launch_quad_t<true, quad::WPB, false, 4>(q, s)
+                            : launch_quad_t<false, quad::WPB, false, 4>(q, s);
+    }
+  }
+  if (areg)
+    return small ? launch_quad_t<true, 6, true, 1>(q, s) : launch_quad_t<false, 6, true, 1>(q, s);
+  return small ? launch_quad_t<true, quad::WPB, false, 1>(q, s)
+               : launch_quad_t<false, quad::WPB, false, 1>(q, s);
 }
 
 // the quad kernels run any J, R <= 32 (R % 4 == 0; padding columns are zero); J = R = 16 has
@@ -906,8 +959,8 @@ bool quad_ok(const SweepParams &p) {
     const char *e = getenv("FT_QUAD_J16");
     return !(e && strcmp(e, "0") == 0);
   }();
-  return p.N == 3 && p.leaf_pc && p.row_leaf_ptr && (p.J > 16 || j16) && p.J <= 32 &&
-         p.R <= 32 && (p.R & 3) == 0;
+  return p.N >= 3 && p.N <= 6 && p.leaf_pc && p.row_leaf_ptr && (p.J > 16 || j16) &&
+         p.J <= 32 && p.R <= 32 && (p.R & 3) == 0;
 }
 
 // ---- K4 "quad": the core-gradient row sweep over the leaf-major index ---------------------
@@ -931,7 +984,7 @@ constexpr size_t bytes() { return (size_t)WPB * WARP_FLOATS * 4; }
 // SSE = true: the same walk scores the tree's leaves instead (K6b, evaluate over the training
 // entries, train.py:91-98): per slot e = x - C_u[i] . cross, sum e^2 and |e| in fp64 per lane,
 // fixed-order block reduction to p.partials as doubles [block][2] (no gradient work).
-template <bool SSE>
+template <bool SSE, int NPRE>
 __global__ void __launch_bounds__(cquad::WPB * 32, 2) core_rows_quad_kernel(const SweepParams p) {
   using namespace cquad;
   extern __shared__ float4 smem4[];
@@ -963,11 +1016,14 @@ __global__ void __launch_bounds__(cquad::WPB * 32, 2) core_rows_quad_kernel(cons
           *reinterpret_cast<const float4 *>(p.Cu + (int64_t)i * R + 4 * l);
   };
   if (ci >= 0) load_cu(ci);
-  int plc = 0, ppc = 0;
+  int plc = 0, ppc[NPRE];
   float px = 0.f;
+#pragma unroll
+  for (int d = 0; d < NPRE; ++d) ppc[d] = 0;
   if (ci >= 0 && cL0 + l < cLe) {
     plc = __ldcs(p.leaf_coord + cL0 + l);
-    ppc = __ldcs(p.leaf_pc + cL0 + l);
+#pragma unroll
+    for (int d = 0; d < NPRE; ++d) ppc[d] = __ldcs(p.leaf_pc + (int64_t)(cL0 + l) * NPRE + d);
     px = __ldcs(p.vals + cL0 + l);
   }
   float acc[FT_MAX_RANK];  // lane r: acc[j] = sum_i g_i[r] A_u[i, j]
@@ -975,11 +1031,6 @@ __global__ void __launch_bounds__(cquad::WPB * 32, 2) core_rows_quad_kernel(cons
   for (int j = 0; j < FT_MAX_RANK; ++j) acc[j] = 0.f;
   float2 g01 = make_float2(0.f, 0.f), g23 = make_float2(0.f, 0.f);  // quarter lanes: g[4l..4l+3]
   double sse = 0.0, sae = 0.0;  // SSE mode
-  const int gc = lane & 7, gs = lane >> 3;
-  const bool gok = gc < (R >> 2);
-  const uint32_t xs0 = smem_u32(X + gs * XS + 4 * gc), ys0 = smem_u32(Y + gs * XS + 4 * gc);
-  const float *cpre = p.Cpre[0] + 4 * gc, *cleaf = p.Cleaf + 4 * gc;
-  const int64_t Rs = R;
   const bool j32 = J == 32;
 
   for (;;) {
@@ -1027,27 +1078,22 @@ __global__ void __launch_bounds__(cquad::WPB * 32, 2) core_rows_quad_kernel(cons
     }
     if (!__any_sync(FULL, ci >= 0)) break;
     const int nb = ci >= 0 ? min(quad::QB, cLe - cL0) : 0;
-    const int lc = plc, pc = ppc;
+    const int lc = plc;
+    int pc[NPRE];
+#pragma unroll
+    for (int d = 0; d < NPRE; ++d) pc[d] = ppc[d];
     const float x = px;
     {  // prefetch the next batch of this quarter
       const bool same = cL0 + nb < cLe;
       const int pos = same ? cL0 + nb : nLb, end = same ? cLe : nLe;
       const bool ok = ci >= 0 && (same || ni >= 0) && pos + l < end;
       plc = ok ? __ldcs(p.leaf_coord + pos + l) : 0;
-      ppc = ok ? __ldcs(p.leaf_pc + pos + l) : 0;
+#pragma unroll
+      for (int d = 0; d < NPRE; ++d)
+        ppc[d] = ok ? __ldcs(p.leaf_pc + (int64_t)(pos + l) * NPRE + d) : 0;
       px = ok ? __ldcs(p.vals + pos + l) : 0.f;
     }
-#pragma unroll
-    for (int it = 0; it < 8; ++it) {
-      const int s = 4 * it + gs;
-      const int pcs = __shfl_sync(FULL, pc, s), lcs = __shfl_sync(FULL, lc, s);
-      if (gok) {
-        cp_async16_s(xs0 + it * 4 * XS * 4, cpre + pcs * Rs);
-        cp_async16_s(ys0 + it * 4 * XS * 4, cleaf + lcs * Rs);
-      }
-    }
-    cp_async_wait_all();
-    __syncwarp();
+    quad_gather<NPRE, XS>(p, X, Y, pc, lc, lane);
     // ---- lane = slot: s = C_u[i_q] . (X * Y), e = x - s ----
     {
       const float4 *xr = reinterpret_cast<const float4 *>(X + lane * XS);
@@ -1129,21 +1175,21 @@ __global__ void __launch_bounds__(cquad::WPB * 32, 2) core_rows_quad_kernel(cons
 }
 
 bool core_quad_ok(const SweepParams &p) {
-  return p.N == 3 && p.leaf_pc && p.row_leaf_ptr && p.J <= 32 && p.R <= 32 && (p.R & 3) == 0 &&
+  return p.N >= 3 && p.N <= 6 && p.leaf_pc && p.row_leaf_ptr && p.J <= 32 && p.R <= 32 && (p.R & 3) == 0 &&
          p.R * p.J <= cquad::WARP_FLOATS;
 }
 
-template <bool SSE = false>
-int core_quad_grid(const SweepParams &p) {
+template <bool SSE, int NPRE>
+int core_quad_grid_t(const SweepParams &p) {
   const size_t sm = cquad::bytes();
   static bool set = false;
   if (!set) {
-    cudaFuncSetAttribute(core_rows_quad_kernel<SSE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sm);
+    cudaFuncSetAttribute(core_rows_quad_kernel<SSE, NPRE>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     set = true;
   }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, core_rows_quad_kernel<SSE>,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, core_rows_quad_kernel<SSE, NPRE>,
                                                     cquad::WPB * 32, sm) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
@@ -1154,9 +1200,29 @@ int core_quad_grid(const SweepParams &p) {
   return (int)g;
 }
 
+template <bool SSE = false>
+int core_quad_grid(const SweepParams &p) {
+  switch (p.N) {
+    case 3: return core_quad_grid_t<SSE, 1>(p);
+    case 4: return core_quad_grid_t<SSE, 2>(p);
+    case 5: return core_quad_grid_t<SSE, 3>(p);
+    default: return core_quad_grid_t<SSE, 4>(p);
+  }
+}
+
+template <bool SSE>
+int launch_core_quad_t(const SweepParams &p, int g, cudaStream_t s) {
+  switch (p.N) {
+    case 3: core_rows_quad_kernel<SSE, 1><<<g, cquad::WPB * 32, cquad::bytes(), s>>>(p); break;
+    case 4: core_rows_quad_kernel<SSE, 2><<<g, cquad::WPB * 32, cquad::bytes(), s>>>(p); break;
+    case 5: core_rows_quad_kernel<SSE, 3><<<g, cquad::WPB * 32, cquad::bytes(), s>>>(p); break;
+    default: core_rows_quad_kernel<SSE, 4><<<g, cquad::WPB * 32, cquad::bytes(), s>>>(p); break;
+  }
+  return check_launch(SSE ? "ft_sse_tree" : "ft_core_sweep_rows(quad)");
+}
+
 int launch_core_quad(const SweepParams &p, int g, cudaStream_t s) {
-  core_rows_quad_kernel<false><<<g, cquad::WPB * 32, cquad::bytes(), s>>>(p);
-  return check_launch("ft_core_sweep_rows(quad)");
+  return launch_core_quad_t<false>(p, g, s);
 }
 
 __global__ void sum_pairs_f64(const double *__restrict__ partials, int nblocks, double *out2) {

@@ -1946,9 +1946,14 @@ int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
   // few long rows -> warp-specialised at order 3 (mode 2: 8.4 vs 8.8 gram, 13.4 dual), else gram
   // quad / quadp: order 3, 16 < J <= 32, leaf-major index
   if (variant >= 8 && variant <= 11 && !quad_ok(p)) variant = 5;
+  if (variant >= 9 && variant <= 11 && p.N != 3) variant = 5;  // quadp / quadw / quadg: order 3
   if (variant == 5) {
-    if (quad_ok(p))  // many rows: quad; few long rows: quadw (warp-specialised)
-      variant = p.nrows >= (int64_t)2 * sm_count() * quad::WPB * 4 ? 8 : 10;
+    // many rows: quad (orders 3-6); few long rows: quadw (order 3, warp-specialised)
+    const bool many = p.nrows >= (int64_t)2 * sm_count() * quad::WPB * 4;
+    if (quad_ok(p) && many)
+      variant = 8;
+    else if (quad_ok(p) && p.N == 3)
+      variant = 10;
     else
       variant = p.nrows >= (int64_t)2 * sm_count() * 16 ? 4 : (p.N == 3 ? 7 : 0);
   }
@@ -2082,9 +2087,10 @@ extern "C" int ft_core_sweep_rows(const ft_tree_t *tree, const ft_model_t *model
   // FT_CORE_KERNEL=rows forces the one-row-per-warp kernel; default: quad when it applies
   // FT_CORE_KERNEL: auto (quad), rows, quadp (gathers one batch ahead; measured slower --
   // 3.4-3.7 vs 3.1-3.2 ms per Netflix mode: K4 is bound by L2 throughput, not gather latency)
-  static const int core_kind = [] {  // 0 auto (quad), 1 rows, 3 quadp
+  static const int core_kind = [] {  // 0 auto (quad when it fills the GPU), 1 rows, 2 quad, 3 quadp
     const char *e = getenv("FT_CORE_KERNEL");
     if (e && strcmp(e, "rows") == 0) return 1;
+    if (e && strcmp(e, "quad") == 0) return 2;
     if (e && strcmp(e, "quadp") == 0) return 3;
     return 0;
   }();
@@ -2094,13 +2100,13 @@ extern "C" int ft_core_sweep_rows(const ft_tree_t *tree, const ft_model_t *model
   // segments); without segments it needs rows to fill its 4-rows-per-warp slots
   const int64_t fill = (int64_t)2 * sm_count() * cquad::WPB * 4;
   const bool use_quad = !core_rows_forced && core_quad_ok(p) &&
-                        (p.nsegs > 0 ? p.nsegs : p.nrows) >= fill;
+                        (core_kind >= 2 || (p.nsegs > 0 ? p.nsegs : p.nrows) >= fill);
   if (use_quad && p.nsegs > 0) {  // the quad kernel reads segments through the row fields
     p.nrows = p.nsegs;
     p.row_coord = p.seg_coord;
     p.row_leaf_ptr = p.seg_leaf_ptr;
   }
-  const bool use_quadp = use_quad && core_kind == 3;
+  const bool use_quadp = use_quad && core_kind == 3 && p.N == 3;
   const int g = use_quadp ? core_quadp_grid(p) : use_quad ? core_quad_grid(p)
                 : p.R <= 8 ? core_rows_grid<8>(p) : p.R <= 16 ? core_rows_grid<16>(p)
                                                               : core_rows_grid<32>(p);
@@ -2185,7 +2191,7 @@ extern "C" int ft_sse_tree(const ft_tree_t *tree, const ft_model_t *model, doubl
   if (!out2) return fail(FT_ERR_ARG, "ft_sse_tree: null out2");
   if (!p.Cu) return fail(FT_ERR_ARG, "ft_sse_tree needs dots[u] (coherent cache)");
   if (!core_quad_ok(p) || p.nsegs <= 0)
-    return fail(FT_ERR_UNSUPPORTED, "ft_sse_tree: needs order 3, R %% 4 == 0 and the leaf index");
+    return fail(FT_ERR_UNSUPPORTED, "ft_sse_tree: needs order 3-6, R %% 4 == 0 and the leaf index");
   keep_pool();
   cudaStream_t s = as_stream(stream);
   p.nrows = p.nsegs;
@@ -2195,8 +2201,7 @@ extern "C" int ft_sse_tree(const ft_tree_t *tree, const ft_model_t *model, doubl
   double *partials = nullptr;
   FT_CUDA(cudaMallocAsync(&partials, sizeof(double) * 2 * g, s));
   p.partials = reinterpret_cast<float *>(partials);
-  core_rows_quad_kernel<true><<<g, cquad::WPB * 32, cquad::bytes(), s>>>(p);
-  int rc = check_launch("ft_sse_tree");
+  int rc = launch_core_quad_t<true>(p, g, s);
   if (rc == FT_OK) {
     sum_pairs_f64<<<1, 32, 0, s>>>(partials, g, out2);
     rc = check_launch("ft_sse_tree(sum)");

@@ -152,7 +152,7 @@ def _sse_tree(model, tree, dots):
     gathers per entry; None when the tree / shape is outside that kernel's cover)."""
     import torch
 
-    if (model.order != 3 or model.core_rank % 4 or tree.leaf_pc is None
+    if (not 3 <= model.order <= 6 or model.core_rank % 4 or tree.leaf_pc is None
             or tree.seg_coord is None):
         return None
     out = torch.zeros(2, dtype=torch.float64, device="cuda")

@@ -32,13 +32,14 @@ def ft():
     return ft
 
 
-def test_leaf_index_matches_fiber_arrays(ft):
-    """leaf_pc[L] = fiber_coord[f(L), 1] and row_leaf_ptr[r] = fiber_ptr[row_fiber_ptr[r]],
-    on a skewed tensor (long and single-leaf fibers) for every root mode, orders 3 and 4."""
+def test_leaf_index_matches_fiber_arrays(ft, monkeypatch):
+    """leaf_pc[L, :] = fiber_coord[f(L), 1:N-1] and row_leaf_ptr[r] = fiber_ptr[row_fiber_ptr[r]],
+    on a skewed tensor (long and single-leaf fibers) for every root mode, orders 3 to 6."""
     import torch
 
+    monkeypatch.setenv("FT_LEAF_INDEX_MAX_ORDER", "6")
     rng = np.random.default_rng(3)
-    for dims in ((300, 40, 7), (50, 9, 11, 6)):
+    for dims in ((300, 40, 7), (50, 9, 11, 6), (20, 9, 7, 6, 5), (9, 8, 7, 6, 5, 4)):
         n = 20_000
         # skew: a few heavy coordinates per mode so fibers range from 1 to hundreds of leaves
         cols = [np.minimum(rng.zipf(1.6, size=4 * n) - 1, d - 1) for d in dims]
@@ -50,7 +51,7 @@ def test_leaf_index_matches_fiber_arrays(ft):
             tree = ft.build_tree(dev, t, 128)
             fp = tree.fiber_ptr.cpu().numpy().astype(np.int64)
             fc = tree.fiber_coord.cpu().numpy()
-            want = np.repeat(fc[:, 1], np.diff(fp))
+            want = np.repeat(fc[:, 1:len(dims) - 1], np.diff(fp), axis=0)
             np.testing.assert_array_equal(tree.leaf_pc.cpu().numpy(), want)
             rfp = tree.row_fiber_ptr.cpu().numpy()
             np.testing.assert_array_equal(tree.row_leaf_ptr.cpu().numpy(), fp[rfp])
@@ -67,8 +68,9 @@ rng = np.random.default_rng(seed)
 lin = rng.choice(int(np.prod(dims)), size=nnz, replace=False)
 idx = np.stack(np.unravel_index(lin, dims), axis=1).astype(np.int64)
 vals = rng.uniform(1, 5, size=nnz)
-om = O.default_init_model(dims, (J,) * 3, R, seed=seed)
-model = ft.Model(dims, (J,) * 3, R, om.factors, om.cores_t)
+N = len(dims)
+om = O.default_init_model(dims, (J,) * N, R, seed=seed)
+model = ft.Model(dims, (J,) * N, R, om.factors, om.cores_t)
 dev = ft.DeviceCoo(dims, torch.from_numpy(idx.astype(np.int32)).cuda(),
                    torch.from_numpy(vals.astype(np.float32)).cuda())
 oforest = O.build_forest(idx, vals, 128)
@@ -78,12 +80,12 @@ cfg = ft.TrainConfig(lr_a=lr, lr_b=lr, reg_a=1e-2, reg_b=1e-2)
 ocache, cache = O.precompute_cache(om), ft.precompute_cache(model)
 worst = 0.0
 for epoch in range(2):
-    for n in range(3):
+    for n in range(N):
         O.update_factor_mode(om, oforest, ocache, n, ocfg)
         ft.update_factor_mode(model, forest, cache, n, cfg)
         u = forest.trees[n].leaf_mode
         assert_rel(model.factors[u].cpu().numpy(), om.factors[u], 1e-4, f"e{{epoch}} factor {{u}}")
-    for n in range(3):
+    for n in range(N):
         O.update_core_mode(om, oforest, ocache, n, ocfg)
         ft.update_core_mode(model, forest, cache, n, cfg)
         u = forest.trees[n].leaf_mode
@@ -102,7 +104,7 @@ print('ok')
 def test_quad_sweeps_match_oracle(kernel, dims, nnz, J, R, lr):
     code = _CASE.format(dims=dims, nnz=nnz, J=J, R=R, lr=lr, seed=7)
     env = dict(os.environ, FT_FACTOR_KERNEL=kernel, FT_QUAD_J16="1",
-               FT_CORE_KERNEL="quadp" if kernel == "quadw" else "auto")
+               FT_CORE_KERNEL="quadp" if kernel == "quadw" else "quad")
     out = subprocess.run([sys.executable, "-c", code], cwd=REPO, env=env, capture_output=True,
                          text=True, timeout=900)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
@@ -130,6 +132,22 @@ def test_sse_tree_matches_coo_evaluate(ft):
     other = ft.DeviceCoo(dims, dev.idx[:1000].contiguous(), dev.vals[:1000].contiguous())
     np.testing.assert_allclose(ft.evaluate(model, other, cache, forest),
                                ft.evaluate(model, other, cache), rtol=0)
+
+
+@pytest.mark.parametrize("dims,nnz,J,R", [
+    ((60, 50, 40, 30), 300_000, 32, 32),            # order 4 (two prefix levels)
+    ((30, 20, 20, 15, 12), 200_000, 16, 16),        # order 5, J = R = 16 instantiation
+    ((12, 10, 10, 9, 8, 8), 150_000, 24, 20),       # order 6, padding
+])
+def test_quad_order_n_sweeps_match_oracle(dims, nnz, J, R):
+    """quad (factor) and K4 quad (core) at orders 4-6: the prefix product folded level by level
+    from the leaf-major index, every sweep against the fp64 oracle at rel 1e-4."""
+    code = _CASE.format(dims=dims, nnz=nnz, J=J, R=R, lr=2e-3, seed=9)
+    env = dict(os.environ, FT_FACTOR_KERNEL="quad", FT_QUAD_J16="1", FT_CORE_KERNEL="quad",
+               FT_LEAF_INDEX_MAX_ORDER="6")
+    out = subprocess.run([sys.executable, "-c", code], cwd=REPO, env=env, capture_output=True,
+                         text=True, timeout=900)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
 
 
 @pytest.mark.parametrize("I,J,R", [(1000, 32, 32), (130, 32, 32), (480_189, 32, 32),

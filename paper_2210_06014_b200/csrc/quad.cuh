@@ -250,7 +250,9 @@ __global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quad_kernel(const Sw
   }
 
   const int64_t nstream = (int64_t)gridDim.x * WPBT * 4;
-  int64_t row = ((int64_t)blockIdx.x * WPBT + w) * 4 + q;
+  // row streams are numbered block-fastest (stream = (4w + q) * grid + block), so the rows of a
+  // last, partial wave spread over all SMs instead of piling onto the first few blocks
+  int64_t row = (int64_t)(4 * w + q) * gridDim.x + blockIdx.x;
   const int J = p.J;
   const bool j32 = J == 32;
   // current row (ci < 0: none) and the next row of this quarter's stream, one row ahead
@@ -461,7 +463,7 @@ __global__ void __launch_bounds__(quadp::WPB * 32, 1) factor_rows_quadp_kernel(c
 
   const int64_t nstream = (int64_t)gridDim.x * quadp::WPB * 4;
   quadp::Cursor cur;
-  cur.row = ((int64_t)blockIdx.x * quadp::WPB + w) * 4 + q - nstream;  // before the first row
+  cur.row = (int64_t)(4 * w + q) * gridDim.x + blockIdx.x - nstream;  // before the first row
   cur.i = -1, cur.L0 = cur.Le = 0;
   quadp::load_row_info(p, cur.row + nstream, cur.ni, cur.nLb, cur.nLe);
   const int J = p.J;
@@ -674,7 +676,7 @@ __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(co
     const int k = w - 1;  // this producer runs batches t = k, k + NP, ...
     float *X = ring + quadw::NS * quadw::STAGE_FLOATS + k * 2 * TILE, *Y = X + TILE;
     quadp::Cursor cur;
-    cur.row = (int64_t)blockIdx.x * 4 + q - nstream;
+    cur.row = (int64_t)q * gridDim.x + blockIdx.x - nstream;
     cur.i = -1, cur.L0 = cur.Le = 0;
     quadp::load_row_info(p, cur.row + nstream, cur.ni, cur.nLb, cur.nLe);
     const int gc = lane & 7, gs = lane >> 3;
@@ -998,7 +1000,7 @@ __global__ void __launch_bounds__(cquad::WPB * 32, 2) core_rows_quad_kernel(cons
   __syncwarp();
   const int J = p.J, R = p.R;
   const int64_t nstream = (int64_t)gridDim.x * cquad::WPB * 4;
-  int64_t row = ((int64_t)blockIdx.x * cquad::WPB + w) * 4 + q;
+  int64_t row = (int64_t)(4 * w + q) * gridDim.x + blockIdx.x;  // block-fastest (see quad)
   int ci = -1, cL0 = 0, cLe = 0, ni = -1, nLb = 0, nLe = 0;
   if (row < p.nrows) {
     ci = __ldg(p.row_coord + row);
@@ -1269,7 +1271,7 @@ __global__ void __launch_bounds__(cquadp::WPB * 32, 2) core_rows_quadp_kernel(co
   const bool j32 = J == 32;
   const int64_t nstream = (int64_t)gridDim.x * cquadp::WPB * 4;
   quadp::Cursor cur;
-  cur.row = ((int64_t)blockIdx.x * cquadp::WPB + w) * 4 + q - nstream;
+  cur.row = (int64_t)(4 * w + q) * gridDim.x + blockIdx.x - nstream;
   cur.i = -1, cur.L0 = cur.Le = 0;
   quadp::load_row_info(p, cur.row + nstream, cur.ni, cur.nLb, cur.nLe);
   auto load_cu = [&](const Rec &r) {

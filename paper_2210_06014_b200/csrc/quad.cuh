@@ -938,10 +938,17 @@ int launch_quad(const SweepParams &q, cudaStream_t s) {
     return e && strcmp(e, "1") == 0 ? 1 : 0;
   }();
   const bool small = q.J <= 16 && q.R <= 16;
+  // 9 warps per block (72 row slots per SM instead of 64) when that turns a barely-partial
+  // second wave into one wave: rows are serial, so a 6 % tail costs a whole row time (BASELINE
+  // order 4: 10,000 rows per mode vs 9,472 slots at 8 warps)
+  const int64_t slots8 = (int64_t)sm_count() * 2 * quad::WPB * 4, slots9 = slots8 * 9 / 8;
+  const bool w9 = q.nrows > slots8 && q.nrows <= slots9;
   if (q.N > 3) {  // order 4..6: prefix products folded level by level (quad_gather)
     switch (q.N) {
-      case 4: return small ? launch_quad_t<true, quad::WPB, false, 2>(q, s)
-                           : launch_quad_t<false, quad::WPB, false, 2>(q, s);
+      case 4:
+        if (w9) return small ? launch_quad_t<true, 9, false, 2>(q, s) : launch_quad_t<false, 9, false, 2>(q, s);
+        return small ? launch_quad_t<true, quad::WPB, false, 2>(q, s)
+                     : launch_quad_t<false, quad::WPB, false, 2>(q, s);
       case 5: return small ? launch_quad_t<true, quad::WPB, false, 3>(q, s)
                            : launch_quad_t<false, quad::WPB, false, 3>(q, s);
       default: return small ? launch_quad_t<true, quad::WPB, false, 4>(q, s)
@@ -950,6 +957,7 @@ int launch_quad(const SweepParams &q, cudaStream_t s) {
   }
   if (areg)
     return small ? launch_quad_t<true, 6, true, 1>(q, s) : launch_quad_t<false, 6, true, 1>(q, s);
+  if (w9) return small ? launch_quad_t<true, 9, false, 1>(q, s) : launch_quad_t<false, 9, false, 1>(q, s);
   return small ? launch_quad_t<true, quad::WPB, false, 1>(q, s)
                : launch_quad_t<false, quad::WPB, false, 1>(q, s);
 }

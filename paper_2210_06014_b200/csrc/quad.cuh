@@ -369,6 +369,192 @@ __global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quad_kernel(const Sw
   }
 }
 
+// ---- K3b "quadr": quad with the combine's output consumed straight from the MMA registers --
+// quad stages V through shared memory to turn the Vᵀ fragments into lanes-over-columns rows
+// (32 STS + 8 LDS.128 per batch on an L1 / shared-memory pipe that ncu shows at 84-88 %).
+// quadr instead places each row's leaves on the MMA's n-slots so that the fragment layout IS the
+// chain layout: row rho (0..3) of a warp lives in the 8 lanes 4 gq + rho (gq = 0..7), each
+// holding columns j = gq, gq+8, gq+16, gq+24; leaf k of its batch is slot 8 (k/2) + 2 rho + (k&1),
+// whose Vᵀ column lands exactly in those lanes' accumulators (d0/d2 for even k, d1/d3 for odd).
+// The dot product reduces over lane bits 2-4 (xor 4, 8, 16).  Same arithmetic, order and
+// gathers as quad; row streams rho are numbered block-fastest.
+template <bool SMALL, int NPRE, int WPBT>
+__global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quadr_kernel(const SweepParams p) {
+  using namespace quad;
+  extern __shared__ float4 smem4[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int rho = lane & 3, gq = lane >> 2;      // chain layout: row, column group
+  const int srho = (lane >> 1) & 3;              // slot layout: lane s holds slot s = leaf
+  const int sk = 2 * (lane >> 3) + (lane & 1);   //   sk of row srho
+  uint4 *afr = reinterpret_cast<uint4 *>(smem4);
+  float *X = reinterpret_cast<float *>(afr + BFRAG_U4) + w * quad::WARP_FLOATS;
+  float *Y = X + TILE;
+  float4 *meta = reinterpret_cast<float4 *>(Y + TILE);
+  for (int k = lane; k < 2 * TILE; k += 32) X[k] = 0.f;
+  quad_afrag_init(p, afr);
+  __syncthreads();
+  constexpr int mts = SMALL ? 1 : 2, nkt = SMALL ? 2 : 4;
+
+  const int64_t nstream = (int64_t)gridDim.x * WPBT * 4;
+  int64_t row = (int64_t)(4 * w + rho) * gridDim.x + blockIdx.x;
+  const int J = p.J;
+  int ci = -1, cL0 = 0, cLe = 0, ni = -1, nLb = 0, nLe = 0;
+  if (row < p.nrows) {
+    ci = __ldg(p.row_coord + row);
+    cL0 = __ldg(p.row_leaf_ptr + row);
+    cLe = __ldg(p.row_leaf_ptr + row + 1);
+  }
+  if (row + nstream < p.nrows) {
+    ni = __ldg(p.row_coord + row + nstream);
+    nLb = __ldg(p.row_leaf_ptr + row + nstream);
+    nLe = __ldg(p.row_leaf_ptr + row + nstream + 1);
+  }
+  float a[4] = {0.f, 0.f, 0.f, 0.f};  // columns gq, gq+8, gq+16, gq+24
+  auto load_row = [&](int i) {
+    const float *ar = p.A + (int64_t)i * J;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) a[m] = gq + 8 * m < J ? ar[gq + 8 * m] : 0.f;
+  };
+  auto store_row = [&](int i) {
+    float *ar = p.A + (int64_t)i * J;
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+      if (gq + 8 * m < J) ar[gq + 8 * m] = a[m];
+  };
+  if (ci >= 0) load_row(ci);
+  // leaf data of slot `lane` for the batch about to run (prefetched one batch ahead)
+  int plc = 0, ppc[NPRE];
+  float px = 0.f;
+#pragma unroll
+  for (int d = 0; d < NPRE; ++d) ppc[d] = 0;
+  {
+    const int sci = __shfl_sync(FULL, ci, srho), s0 = __shfl_sync(FULL, cL0, srho),
+              se = __shfl_sync(FULL, cLe, srho);
+    if (sci >= 0 && s0 + sk < se) {
+      plc = __ldcs(p.leaf_coord + s0 + sk);
+#pragma unroll
+      for (int d = 0; d < NPRE; ++d) ppc[d] = __ldcs(p.leaf_pc + (int64_t)(s0 + sk) * NPRE + d);
+      px = __ldcs(p.vals + s0 + sk);
+    }
+  }
+  const float lr = p.lr;
+
+  for (;;) {
+    if (ci >= 0 && cL0 >= cLe) {
+      store_row(ci);
+      row += nstream;
+      ci = ni, cL0 = nLb, cLe = nLe;
+      if (ci >= 0) {
+        load_row(ci);
+        const int64_t r2 = row + nstream;
+        if (r2 < p.nrows) {
+          ni = __ldg(p.row_coord + r2);
+          nLb = __ldg(p.row_leaf_ptr + r2);
+          nLe = __ldg(p.row_leaf_ptr + r2 + 1);
+        } else {
+          ni = -1;
+        }
+      }
+    }
+    if (!__any_sync(FULL, ci >= 0)) break;
+    const int nb = ci >= 0 ? min(QB, cLe - cL0) : 0;
+    // the slot-layout view of this lane's row (srho)
+    const int snb = __shfl_sync(FULL, nb, srho);
+    const int lc = plc;
+    int pc[NPRE];
+#pragma unroll
+    for (int d = 0; d < NPRE; ++d) pc[d] = ppc[d];
+    {
+      const float lrk = sk < snb ? lr : 0.f;
+      const float ck = -lrk * p.reg;
+      meta[srho * MQ + sk] = make_float4(sk < snb ? px : 0.f, lrk, ck, ck);
+    }
+    {  // prefetch the next batch of row srho (same row, or the next row's first leaves)
+      const bool same = cL0 + nb < cLe;
+      const int pos_r = same ? cL0 + nb : nLb, end_r = same ? cLe : nLe;
+      const bool ok_r = ci >= 0 && (same || ni >= 0);
+      const int pos = __shfl_sync(FULL, pos_r, srho), end = __shfl_sync(FULL, end_r, srho);
+      const bool ok = __shfl_sync(FULL, (int)ok_r, srho) && pos + sk < end;
+      plc = ok ? __ldcs(p.leaf_coord + pos + sk) : 0;
+#pragma unroll
+      for (int d = 0; d < NPRE; ++d)
+        ppc[d] = ok ? __ldcs(p.leaf_pc + (int64_t)(pos + sk) * NPRE + d) : 0;
+      px = ok ? __ldcs(p.vals + pos + sk) : 0.f;
+    }
+    quad_gather<NPRE, XS>(p, X, Y, pc, lc, lane);
+    float acc[2][4][4];
+    quad_zero(acc);
+#pragma unroll
+    for (int kt = 0; kt < KT; ++kt) {
+      if (kt >= nkt) break;
+      quad_mma_kt<NT>(X, Y, afr, kt, 0, lane, acc, mts);
+    }
+    __syncwarp();  // meta visible (its stores precede the gathers' waits)
+    // ---- four serial chains on the accumulator registers ----
+    const int nbmax = __reduce_max_sync(FULL, (unsigned)nb);
+    const float4 *mq = meta + rho * MQ;
+#pragma unroll
+    for (int k = 0; k < QB; ++k) {
+      if (k >= nbmax) break;
+      const int nt = k >> 1, o = k & 1;
+      const float v0 = acc[0][nt][o], v1 = acc[0][nt][2 + o];
+      const float v2 = SMALL ? 0.f : acc[1][nt][o], v3 = SMALL ? 0.f : acc[1][nt][2 + o];
+      float2 pr = fmul2(make_float2(a[0], a[1]), make_float2(v0, v1));
+      pr = ffma2(make_float2(a[2], a[3]), make_float2(v2, v3), pr);
+      float sv = pr.x + pr.y;
+      sv += __shfl_xor_sync(FULL, sv, 4);
+      sv += __shfl_xor_sync(FULL, sv, 8);
+      sv += __shfl_xor_sync(FULL, sv, 16);
+      const float4 m = mq[k];  // (x, lr, -lr reg, -lr reg); lr = 0 on padding steps
+      const float e = m.x - sv;
+      const float lre = m.y * e;
+      const float2 a01 = ffma2(make_float2(m.z, m.w), make_float2(a[0], a[1]), make_float2(a[0], a[1]));
+      const float2 a23 = ffma2(make_float2(m.z, m.w), make_float2(a[2], a[3]), make_float2(a[2], a[3]));
+      a[0] = __fmaf_rn(lre, v0, a01.x);
+      a[1] = __fmaf_rn(lre, v1, a01.y);
+      a[2] = __fmaf_rn(lre, v2, a23.x);
+      a[3] = __fmaf_rn(lre, v3, a23.y);
+    }
+    __syncwarp();  // meta / tiles read before the next batch's stores and gathers
+    cL0 += nb;
+  }
+}
+
+template <bool SMALL, int NPRE, int WPBT>
+int launch_quadr_t(const SweepParams &q, cudaStream_t s) {
+  const size_t sm = (size_t)quad::BFRAG_U4 * 16 + (size_t)WPBT * quad::WARP_FLOATS * 4;
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(factor_rows_quadr_kernel<SMALL, NPRE, WPBT>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    set = true;
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quadr_kernel<SMALL, NPRE, WPBT>,
+                                                    WPBT * 32, sm) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  int64_t g = (q.nrows + 4 * WPBT - 1) / (4 * WPBT);
+  const int64_t cap = (int64_t)sm_count() * per_sm;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  factor_rows_quadr_kernel<SMALL, NPRE, WPBT><<<(int)g, WPBT * 32, sm, s>>>(q);
+  return check_launch("ft_factor_sweep_rows(quadr)");
+}
+
+int launch_quadr(const SweepParams &q, cudaStream_t s) {
+  const bool small = q.J <= 16 && q.R <= 16;
+  // 9 warps per block when that fits all rows in one wave (see launch_quad)
+  const int64_t slots8 = (int64_t)sm_count() * 2 * quad::WPB * 4, slots9 = slots8 * 9 / 8;
+  const bool w9 = q.nrows > slots8 && q.nrows <= slots9;
+  if (q.N == 4) {
+    if (w9) return small ? launch_quadr_t<true, 2, 9>(q, s) : launch_quadr_t<false, 2, 9>(q, s);
+    return small ? launch_quadr_t<true, 2, quad::WPB>(q, s) : launch_quadr_t<false, 2, quad::WPB>(q, s);
+  }
+  if (w9) return small ? launch_quadr_t<true, 1, 9>(q, s) : launch_quadr_t<false, 1, 9>(q, s);
+  return small ? launch_quadr_t<true, 1, quad::WPB>(q, s) : launch_quadr_t<false, 1, quad::WPB>(q, s);
+}
+
 // ---- K3b "quadp": the quad layout software-pipelined for FEW LONG ROWS --------------------
 // Netflix mode 2 has 2,182 rows of ~45 K serial updates: four rows per warp leave ~3.7 warps
 // per SM, too few to hide the gather -> MMA -> chain latencies by switching warps.  quadp

@@ -1932,6 +1932,7 @@ int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
     if (e && strcmp(e, "quadp") == 0) return 9;
     if (e && strcmp(e, "quadw") == 0) return 10;
     if (e && strcmp(e, "quadg") == 0) return 11;
+    if (e && strcmp(e, "quadr") == 0) return 12;
     return 5;  // auto: dual when the rows fill the SMs, gram otherwise
   }();
   int variant = chosen;
@@ -1945,19 +1946,21 @@ int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
   // auto, by rows per resident warp slot: many rows -> dual (Netflix modes 0/1: 7.5 ms);
   // few long rows -> warp-specialised at order 3 (mode 2: 8.4 vs 8.8 gram, 13.4 dual), else gram
   // quad / quadp: order 3, 16 < J <= 32, leaf-major index
-  if (variant >= 8 && variant <= 11 && !quad_ok(p)) variant = 5;
+  if (variant >= 8 && variant <= 12 && !quad_ok(p)) variant = 5;
+  if (variant == 12 && p.N > 4) variant = 8;
   if (variant >= 9 && variant <= 11 && p.N != 3) variant = 5;  // quadp / quadw / quadg: order 3
   if (variant == 5) {
-    // many rows: quad (orders 3-6); few long rows: quadw (order 3, warp-specialised)
+    // many rows: quadr / quad (orders 3-6); few long rows: quadw (order 3, warp-specialised)
     const bool many = p.nrows >= (int64_t)2 * sm_count() * quad::WPB * 4;
     if (quad_ok(p) && many)
-      variant = 8;
+      variant = p.N <= 4 ? 12 : 8;  // quadr (V consumed from the MMA registers), orders 3-4
     else if (quad_ok(p) && p.N == 3)
       variant = 10;
     else
       variant = p.nrows >= (int64_t)2 * sm_count() * 16 ? 4 : (p.N == 3 ? 7 : 0);
   }
   if (variant == 8) return launch_quad(q, s);
+  if (variant == 12) return launch_quadr(q, s);
   if (variant == 9) return launch_quadp(q, s);
   if (variant == 10) return launch_quadw<false>(q, s);
   if (variant == 11) return launch_quadw<true>(q, s);

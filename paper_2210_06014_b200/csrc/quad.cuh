@@ -788,6 +788,196 @@ int launch_quadp(const SweepParams &q, cudaStream_t s) {
   return check_launch("ft_factor_sweep_rows(quadp)");
 }
 
+// ---- K3b "quadrp": quadr software-pipelined inside each warp, for FEW LONG ROWS ---------------
+// With V consumed from registers (quadr), the chain of batch t and the combine of batch t+1 are
+// independent register streams; they are interleaved step by step (chain step k, then the MMAs
+// of k-tile k/2 for two n-tiles) so the tensor-core work fills the shuffle latency of the serial
+// chain.  Gathers run two batches ahead (double-buffered X/Y), the per-row batch records three
+// ahead (quadp's records, kept in the chain layout), a row's A values one batch before its
+// first update.  Meant for ~4 warps per SM (Netflix mode 2: 2,182 rows).
+template <bool SMALL>
+__global__ void __launch_bounds__(quadp::WPB * 32, 1) factor_rows_quadrp_kernel(const SweepParams p) {
+  using namespace quad;
+  using quadp::Rec;
+  extern __shared__ float4 smem4[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int rho = lane & 3, gq = lane >> 2;
+  const int srho = (lane >> 1) & 3, sk = 2 * (lane >> 3) + (lane & 1);
+  constexpr int WF = 4 * TILE + 2 * 4 * MQ * 4;  // X[2], Y[2], meta[2] (4 rows x MQ float4)
+  uint4 *afr = reinterpret_cast<uint4 *>(smem4);
+  float *base = reinterpret_cast<float *>(afr + BFRAG_U4) + w * WF;
+  float4 *meta0 = reinterpret_cast<float4 *>(base + 4 * TILE);
+  for (int k = lane; k < 4 * TILE; k += 32) base[k] = 0.f;
+  quad_afrag_init(p, afr);
+  __syncthreads();
+  constexpr int mts = SMALL ? 1 : 2, nkt = SMALL ? 2 : 4;
+  const int64_t nstream = (int64_t)gridDim.x * quadp::WPB * 4;
+  quadp::Cursor cur;
+  cur.row = (int64_t)(4 * w + rho) * gridDim.x + blockIdx.x - nstream;
+  cur.i = -1, cur.L0 = cur.Le = 0;
+  quadp::load_row_info(p, cur.row + nstream, cur.ni, cur.nLb, cur.nLe);
+  const int J = p.J;
+  auto load_a = [&](int i, float (&a)[4]) {
+    const float *ar = p.A + (int64_t)i * J;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) a[m] = gq + 8 * m < J ? ar[gq + 8 * m] : 0.f;
+  };
+  auto store_a = [&](int i, const float (&a)[4]) {
+    float *ar = p.A + (int64_t)i * J;
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+      if (gq + 8 * m < J) ar[gq + 8 * m] = a[m];
+  };
+  // leaf data of slot `lane` for a batch whose per-row records are r (chain layout)
+  struct SLeaf {
+    int lc, pc;
+    float x;
+    int nb;
+  };
+  auto load_leaf = [&](const Rec &r) {
+    SLeaf d{0, 0, 0.f, 0};
+    const int L0 = __shfl_sync(FULL, r.L0, srho), nb = __shfl_sync(FULL, r.nb, srho);
+    d.nb = nb;
+    if (sk < nb) {
+      d.lc = __ldcs(p.leaf_coord + L0 + sk);
+      d.pc = __ldcs(p.leaf_pc + L0 + sk);
+      d.x = __ldcs(p.vals + L0 + sk);
+    }
+    return d;
+  };
+  auto gather = [&](int set, const SLeaf &d) {
+    int pc1[1] = {d.pc};
+    const int gc = lane & 7, gs = lane >> 3;
+    const bool gok = gc < (p.R >> 2);
+    const int64_t Rs = p.R;
+    float *X = base + set * TILE, *Y = base + (2 + set) * TILE;
+    const uint32_t xs0 = smem_u32(X + gs * XS + 4 * gc), ys0 = smem_u32(Y + gs * XS + 4 * gc);
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int sl = 4 * it + gs;
+      const int pcs = __shfl_sync(FULL, pc1[0], sl), lcs = __shfl_sync(FULL, d.lc, sl);
+      if (gok) {
+        cp_async16_s(xs0 + it * 4 * XS * 4, p.Cpre[0] + 4 * gc + pcs * Rs);
+        cp_async16_s(ys0 + it * 4 * XS * 4, p.Cleaf + 4 * gc + lcs * Rs);
+      }
+    }
+    cp_async_commit();
+  };
+  auto put_meta = [&](int buf, const SLeaf &d) {
+    const float lrk = sk < d.nb ? p.lr : 0.f;
+    const float ck = -lrk * p.reg;
+    meta0[buf * MQ * 4 + srho * MQ + sk] = make_float4(sk < d.nb ? d.x : 0.f, lrk, ck, ck);
+  };
+
+  Rec r0 = quadp::next_batch(p, cur, nstream);
+  const SLeaf d0 = load_leaf(r0);
+  Rec r1 = quadp::next_batch(p, cur, nstream);
+  SLeaf d1 = load_leaf(r1);
+  Rec r2 = quadp::next_batch(p, cur, nstream);
+  SLeaf d2 = load_leaf(r2);
+  gather(0, d0);
+  gather(1, d1);
+  float a[4] = {0.f, 0.f, 0.f, 0.f}, an[4] = {0.f, 0.f, 0.f, 0.f};
+  int ai = r0.nb > 0 ? r0.i : -1;
+  if (ai >= 0) load_a(ai, a);
+  if (r1.newrow && r1.nb > 0) load_a(r1.i, an);
+  float acc[2][4][4], nacc[2][4][4];
+  cp_async_wait_one();
+  __syncwarp();
+  quad_zero(acc);
+#pragma unroll
+  for (int kt = 0; kt < KT; ++kt)
+    if (kt < nkt) quad_mma_kt<NT>(base, base + 2 * TILE, afr, kt, 0, lane, acc, mts);
+  put_meta(0, d0);
+
+  for (int t = 0; __any_sync(FULL, r0.nb > 0); ++t) {
+    const int s1 = (t + 1) & 1;
+    __syncwarp();  // set t&1 (batch t's tiles) fully read by its MMA before batch t+2 lands there
+    gather(t & 1, d2);
+    const Rec r3 = quadp::next_batch(p, cur, nstream);
+    const SLeaf d3 = load_leaf(r3);
+    cp_async_wait_one();  // batch t+1's tiles
+    put_meta(s1, d1);
+    __syncwarp();
+    const float *Xs = base + s1 * TILE, *Ys = base + (2 + s1) * TILE;
+    const float4 *mq = meta0 + (t & 1) * MQ * 4 + rho * MQ;
+    quad_zero(nacc);
+#pragma unroll
+    for (int k = 0; k < QB; ++k) {
+      {  // chain step k of batch t (accumulator registers)
+        const int nt = k >> 1, o = k & 1;
+        const float v0 = acc[0][nt][o], v1 = acc[0][nt][2 + o];
+        const float v2 = SMALL ? 0.f : acc[1][nt][o], v3 = SMALL ? 0.f : acc[1][nt][2 + o];
+        float2 pr = fmul2(make_float2(a[0], a[1]), make_float2(v0, v1));
+        pr = ffma2(make_float2(a[2], a[3]), make_float2(v2, v3), pr);
+        float sv = pr.x + pr.y;
+        sv += __shfl_xor_sync(FULL, sv, 4);
+        sv += __shfl_xor_sync(FULL, sv, 8);
+        sv += __shfl_xor_sync(FULL, sv, 16);
+        const float4 m = mq[k];
+        const float e = m.x - sv;
+        const float lre = m.y * e;
+        const float2 a01 = ffma2(make_float2(m.z, m.w), make_float2(a[0], a[1]), make_float2(a[0], a[1]));
+        const float2 a23 = ffma2(make_float2(m.z, m.w), make_float2(a[2], a[3]), make_float2(a[2], a[3]));
+        a[0] = __fmaf_rn(lre, v0, a01.x);
+        a[1] = __fmaf_rn(lre, v1, a01.y);
+        a[2] = __fmaf_rn(lre, v2, a23.x);
+        a[3] = __fmaf_rn(lre, v3, a23.y);
+      }
+      if ((k >> 1) < nkt) quad_mma_kt<2>(Xs, Ys, afr, k >> 1, 2 * (k & 1), lane, nacc, mts);
+    }
+    // row hand-over (chain layout): batch t+1 starts a new row -> write back, swap in
+    if (r1.newrow && r1.nb > 0) {
+      if (ai >= 0) store_a(ai, a);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] = an[u];
+      ai = r1.i;
+    } else if (r1.nb == 0 && ai >= 0) {
+      store_a(ai, a);
+      ai = -1;
+    }
+    if (r2.newrow && r2.nb > 0) load_a(r2.i, an);
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[mt][nt][u] = nacc[mt][nt][u];
+    r0 = r1, r1 = r2, r2 = r3;
+    d1 = d2, d2 = d3;
+  }
+  cp_async_wait_all();
+  if (ai >= 0) store_a(ai, a);
+}
+
+template <bool SMALL>
+int launch_quadrp_t(const SweepParams &q, cudaStream_t s) {
+  const size_t sm = (size_t)quad::BFRAG_U4 * 16 +
+                    (size_t)quadp::WPB * (4 * quad::TILE + 2 * 4 * quad::MQ * 4) * 4;
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(factor_rows_quadrp_kernel<SMALL>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    set = true;
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quadrp_kernel<SMALL>,
+                                                    quadp::WPB * 32, sm) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  int64_t g = (q.nrows + 4 * quadp::WPB - 1) / (4 * quadp::WPB);
+  const int64_t cap = (int64_t)sm_count() * per_sm;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  factor_rows_quadrp_kernel<SMALL><<<(int)g, quadp::WPB * 32, sm, s>>>(q);
+  return check_launch("ft_factor_sweep_rows(quadrp)");
+}
+
+int launch_quadrp(const SweepParams &q, cudaStream_t s) {
+  return q.J <= 16 && q.R <= 16 ? launch_quadrp_t<true>(q, s) : launch_quadrp_t<false>(q, s);
+}
+
+
 // ---- K3b "quadw": the quad layout warp-specialised for FEW LONG ROWS ----------------------
 // A warp GROUP owns four rows (one per 8-lane quarter of its consumer warp).  Two PRODUCER
 // warps take alternate batches: each walks the rows' batch records, gathers its batch into its

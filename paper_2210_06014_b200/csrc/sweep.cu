@@ -1933,6 +1933,7 @@ int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
     if (e && strcmp(e, "quadw") == 0) return 10;
     if (e && strcmp(e, "quadg") == 0) return 11;
     if (e && strcmp(e, "quadr") == 0) return 12;
+    if (e && strcmp(e, "quadrp") == 0) return 13;
     return 5;  // auto: dual when the rows fill the SMs, gram otherwise
   }();
   int variant = chosen;
@@ -1946,7 +1947,8 @@ int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
   // auto, by rows per resident warp slot: many rows -> dual (Netflix modes 0/1: 7.5 ms);
   // few long rows -> warp-specialised at order 3 (mode 2: 8.4 vs 8.8 gram, 13.4 dual), else gram
   // quad / quadp: order 3, 16 < J <= 32, leaf-major index
-  if (variant >= 8 && variant <= 12 && !quad_ok(p)) variant = 5;
+  if (variant >= 8 && variant <= 13 && !quad_ok(p)) variant = 5;
+  if (variant == 13 && p.N != 3) variant = 5;
   if (variant == 12 && p.N > 4) variant = 8;
   if (variant >= 9 && variant <= 11 && p.N != 3) variant = 5;  // quadp / quadw / quadg: order 3
   if (variant == 5) {
@@ -1961,6 +1963,7 @@ int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
   }
   if (variant == 8) return launch_quad(q, s);
   if (variant == 12) return launch_quadr(q, s);
+  if (variant == 13) return launch_quadrp(q, s);
   if (variant == 9) return launch_quadp(q, s);
   if (variant == 10) return launch_quadw<false>(q, s);
   if (variant == 11) return launch_quadw<true>(q, s);

@@ -100,7 +100,7 @@ print('ok')
     ((60000, 64, 64), 200_000, 32, 32, 5e-3),     # more rows than row slots (row switching)
     ((4000, 300, 50), 500_000, 16, 12, 2e-3),     # J <= 16 (one m-tile), R = 12 (two k-tiles)
 ])
-@pytest.mark.parametrize("kernel", ["quad", "quadr", "quadp", "quadw", "quadg"])
+@pytest.mark.parametrize("kernel", ["quad", "quadr", "quadrp", "quadp", "quadw", "quadg"])
 def test_quad_sweeps_match_oracle(kernel, dims, nnz, J, R, lr):
     code = _CASE.format(dims=dims, nnz=nnz, J=J, R=R, lr=lr, seed=7)
     env = dict(os.environ, FT_FACTOR_KERNEL=kernel, FT_QUAD_J16="1",

@@ -113,6 +113,18 @@ FT_API int ft_build_tree(int32_t N, int64_t nnz, const int64_t *dims, const int3
                   int32_t *fiber_coord, int32_t *sub_fiber_ptr, int32_t *sub_leaf_ptr,
                   int32_t *row_fiber_ptr, int32_t *row_coord, int64_t *counts_out, void *stream);
 
+/* K1  derived build: the tree rooted at (prev->root_mode + 1) mod N from the tree `prev`
+ * (which must carry the leaf-major index, ft_tree_leaf_index): a stable 32-bit-key radix sort
+ * of prev's leaf order by its levels 1..N-1 gives the new tree's order (prev's root level
+ * becomes the new leaf level), then the same fiber / root-slice / split / per-depth steps as
+ * ft_build_tree.  Output arrays, capacities and counts_out as ft_build_tree (dims: HOST
+ * int64[N]); bit-identical to building from the COO.  FT_ERR_UNSUPPORTED when the key would
+ * exceed 32 bits or prev lacks the index (build from the COO instead).  SYNCHRONOUS. */
+FT_API int ft_build_tree_derived(const ft_tree_t *prev, const int64_t *dims, int64_t thr,
+                                 float *leaf_vals, int32_t *const *inds, int32_t *const *ptrs,
+                                 int32_t *fiber_ptr, int32_t *fiber_coord, int32_t *sub_fiber_ptr,
+                                 int32_t *sub_leaf_ptr, int32_t *row_fiber_ptr,
+                                 int32_t *row_coord, int64_t *counts_out, void *stream);
 /* K1b Leaf-major index of a built tree (reads tree->fiber_ptr / fiber_coord / row_fiber_ptr):
  *   leaf_pc[L * (N-2) + d] = fiber_coord[f(L) * (N-1) + 1 + d], d < N-2, for every leaf L of
  *   fiber f(L) (the prefix levels 1..N-2 expanded to the leaves; orders 3-6 only), and

@@ -189,6 +189,57 @@ def build_tree(tensor, root_mode: int, fiber_threshold=DEFAULT_FIBER_THRESHOLD,
         thr = int(fiber_threshold)
         if thr < 1:
             raise ConfigError(f"fiber_threshold must be >= 1, got {fiber_threshold}")
+    dims = tuple(dev.dims)
+
+    def call(out):
+        return L.ft_build_tree(N, nnz, out["dims"], dev.idx.data_ptr(), dev.vals.data_ptr(),
+                               root_mode, thr, *out["args"])
+
+    def on_duplicate(counts):
+        e = int(counts[3])
+        coord = dev.idx[e].cpu().numpy()
+        from .errors import ValidationError
+
+        raise ValidationError(f"duplicate coordinate {tuple(int(c) + 1 for c in coord)}")
+
+    return _build_with(call, N, nnz, dims, root_mode, compact, stream, "ft_build_tree",
+                       on_duplicate)
+
+
+def build_tree_derived(prev: CsfTree, fiber_threshold=DEFAULT_FIBER_THRESHOLD, stream=None,
+                       compact: bool = False):
+    """The tree rooted at ``prev.root_mode + 1`` from ``prev``'s leaf order (K1 derived build,
+    ``ft_build_tree_derived``): a stable radix sort on a 32-bit key instead of the full-width
+    COO sort; bit-identical to ``build_tree``.  None when it does not apply (prev without the
+    leaf-major index, or a key wider than 32 bits)."""
+    if prev.leaf_pc is None or prev.row_leaf_ptr is None:
+        return None
+    L = _lib.lib()
+    N, nnz = prev.order, prev.nnz
+    dims = tuple(prev.dims)
+    thr = 0 if fiber_threshold is None else int(fiber_threshold)
+    root_mode = (prev.root_mode + 1) % N
+    pv = prev.view()
+
+    def call(out):
+        return L.ft_build_tree_derived(ctypes.byref(pv), out["dims"], thr, *out["args"])
+
+    try:
+        return _build_with(call, N, nnz, dims, root_mode, compact, stream,
+                           "ft_build_tree_derived", None)
+    except _Unsupported:
+        return None
+
+
+class _Unsupported(Exception):
+    pass
+
+
+def _build_with(call, N, nnz, dims, root_mode, compact, stream, what, on_duplicate):
+    """Allocate a build's output buffers, run ``call`` (an ft_build_tree* entry point), trim and
+    wrap them as a CsfTree with its leaf-major index."""
+    import torch
+
     i32 = dict(dtype=torch.int32, device="cuda")
     leaf_vals = torch.empty(nnz, dtype=torch.float32, device="cuda")
     leaf = torch.empty(nnz, **i32)
@@ -201,23 +252,21 @@ def build_tree(tensor, root_mode: int, fiber_threshold=DEFAULT_FIBER_THRESHOLD,
     row_fiber_ptr = torch.empty(nnz + 1, **i32)
     row_coord = torch.empty(nnz, **i32)
     counts = np.zeros(4 + N, dtype=np.int64)
-    dims = (ctypes.c_int64 * N)(*dev.dims)
     ind_ptrs = [None] * (N - 1) + [leaf.data_ptr()] if compact else [a.data_ptr() for a in inds]
     ind_tab = (ctypes.c_void_p * N)(*ind_ptrs)
     ptr_tab = None if compact else (ctypes.c_void_p * max(N - 1, 1))(*[a.data_ptr() for a in ptrs])
-    rc = L.ft_build_tree(N, nnz, dims, dev.idx.data_ptr(), dev.vals.data_ptr(), root_mode, thr,
-                         leaf_vals.data_ptr(), ind_tab, ptr_tab, fiber_ptr.data_ptr(),
-                         fiber_coord.data_ptr(), _lib.ptr(sub_fiber_ptr), _lib.ptr(sub_leaf_ptr),
-                         row_fiber_ptr.data_ptr(), row_coord.data_ptr(),
-                         counts.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
-                         _lib.stream_handle(stream))
-    if rc == _lib.FT_ERR_DUPLICATE:
-        e = int(counts[3])
-        coord = dev.idx[e].cpu().numpy()
-        from .errors import ValidationError
-
-        raise ValidationError(f"duplicate coordinate {tuple(int(c) + 1 for c in coord)}")
-    _lib.check(rc, "ft_build_tree")
+    out = {"dims": (ctypes.c_int64 * N)(*dims),
+           "args": (leaf_vals.data_ptr(), ind_tab, ptr_tab, fiber_ptr.data_ptr(),
+                    fiber_coord.data_ptr(), _lib.ptr(sub_fiber_ptr), _lib.ptr(sub_leaf_ptr),
+                    row_fiber_ptr.data_ptr(), row_coord.data_ptr(),
+                    counts.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                    _lib.stream_handle(stream))}
+    rc = call(out)
+    if rc == _lib.FT_ERR_DUPLICATE and on_duplicate is not None:
+        on_duplicate(counts)
+    if rc == _lib.FT_ERR_UNSUPPORTED and on_duplicate is None:
+        raise _Unsupported(what)
+    _lib.check(rc, what)
     F, S, rows = int(counts[0]), int(counts[1]), int(counts[2])
     nodes = [int(c) for c in counts[4:4 + N]]
     empty = torch.empty(0, **i32)
@@ -232,7 +281,7 @@ def build_tree(tensor, root_mode: int, fiber_threshold=DEFAULT_FIBER_THRESHOLD,
     tree = CsfTree(
         root_mode=root_mode,
         level_modes=tuple((root_mode + d) % N for d in range(N)),
-        dims=tuple(dev.dims),
+        dims=tuple(dims),
         inds=inds_t,
         ptrs=ptrs_t,
         vals=leaf_vals,
@@ -299,7 +348,8 @@ def add_row_segments(tree: CsfTree, stream=None) -> CsfTree:
 
 
 def build_forest(tensor, fiber_threshold=DEFAULT_FIBER_THRESHOLD, stream=None,
-                 compact: bool = False, concurrent: bool = False) -> CsfForest:
+                 compact: bool = False, concurrent: bool = False,
+                 derived: bool = True) -> CsfForest:
     """All N trees (csf.py:199-201).  ``concurrent=True`` builds each tree on its own CUDA
     stream from its own host thread (ctypes releases the GIL); the result is identical, but it
     measured slower (Netflix: 33 ms vs 26.5 ms sequential, with 100-200 ms outliers while the
@@ -309,8 +359,15 @@ def build_forest(tensor, fiber_threshold=DEFAULT_FIBER_THRESHOLD, stream=None,
     dev = as_device(tensor)
     N = dev.order
     if not concurrent or N == 1:
-        trees = tuple(build_tree(dev, t, fiber_threshold, stream, compact) for t in range(N))
-        return CsfForest(trees=trees, fiber_threshold=fiber_threshold)
+        # tree 0 from the COO, tree t from tree t-1's leaf order when the 32-bit derived sort
+        # applies (bit-identical; Netflix: 4 radix passes of 4-byte keys instead of 6 of 8-byte)
+        trees = [build_tree(dev, 0, fiber_threshold, stream, compact)]
+        for t in range(1, N):
+            tree = build_tree_derived(trees[-1], fiber_threshold, stream, compact) \
+                if derived else None
+            trees.append(tree if tree is not None
+                         else build_tree(dev, t, fiber_threshold, stream, compact))
+        return CsfForest(trees=tuple(trees), fiber_threshold=fiber_threshold)
     from concurrent.futures import ThreadPoolExecutor
 
     main = stream if stream is not None else torch.cuda.current_stream()

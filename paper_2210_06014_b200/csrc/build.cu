@@ -294,6 +294,171 @@ struct Compactor {
   }
 };
 
+
+// ---- derived build: tree (t+1) from tree t's leaf order -------------------------------------
+// Tree t holds the entries sorted by (i_t, i_{t+1}, ..., i_{t+N-1}); a STABLE sort of that
+// sequence by (i_{t+1}, ..., i_{t+N-1}) alone gives (i_{t+1}, ..., i_{t+N-1}, i_t) -- tree t+1's
+// order -- because equal keys keep their i_t-ascending order.  The key drops tree t's root
+// level, so at the BASELINE shapes it fits 32 bits (Netflix: 27 / 31 bits, 4 radix passes of
+// 4-byte keys instead of 6 of 8-byte keys); the payload carries (i_t, value).
+__global__ void row_start_mark(const int32_t *__restrict__ row_leaf_ptr, int64_t rows,
+                               uint32_t *__restrict__ mark) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < rows) mark[__ldg(row_leaf_ptr + r)] = (uint32_t)r;
+}
+
+struct DerivedArgs {
+  int N;
+  int shift[FT_MAX_ORDER];  // new level d (< N-1) -> bit shift in the key
+};
+
+__global__ void pack_derived(const uint32_t *__restrict__ leaf_row, const int32_t *__restrict__ row_coord,
+                             const int32_t *__restrict__ leaf_pc, const int32_t *__restrict__ leaf_coord,
+                             const float *__restrict__ vals, int64_t nnz, DerivedArgs a,
+                             uint32_t *__restrict__ keys, unsigned long long *__restrict__ pay) {
+  const int64_t L = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (L >= nnz) return;
+  const int NP = a.N - 2;
+  uint32_t k = 0;
+  // new level d = old level d + 1: old levels 1..N-2 from leaf_pc, old level N-1 = leaf_coord
+  for (int d = 0; d < NP; ++d) k |= (uint32_t)__ldg(leaf_pc + L * NP + d) << a.shift[d];
+  k |= (uint32_t)__ldg(leaf_coord + L) << a.shift[a.N - 2];
+  keys[L] = k;
+  const uint32_t root = (uint32_t)__ldg(row_coord + __ldg(leaf_row + L));
+  pay[L] = ((unsigned long long)root << 32) | __float_as_uint(__ldg(vals + L));
+}
+
+__global__ void decode_derived(const uint32_t *__restrict__ keys,
+                               const unsigned long long *__restrict__ pay, int64_t nnz,
+                               DerivedArgs a, DecodeArgs da, float *__restrict__ vout,
+                               uint8_t *__restrict__ fdl) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= nnz) return;
+  const uint32_t k = keys[p];
+  const unsigned long long q = pay[p];
+  for (int d = 0; d < a.N - 1; ++d) da.K[d][p] = (int32_t)((k >> a.shift[d]) & (uint32_t)da.mask[d]);
+  da.K[a.N - 1][p] = (int32_t)(q >> 32);
+  vout[p] = __uint_as_float((uint32_t)q);
+  int first = 0;
+  if (p > 0) {
+    const uint32_t x = k ^ keys[p - 1];
+    if (x == 0) {
+      first = a.N - 1;  // same prefix: the entries differ in the (old root) leaf level
+    } else {
+      const int hb = 31 - __clz((int)x);
+      first = a.N - 2;
+      for (int d = 0; d < a.N - 1; ++d)
+        if (da.mask[d] && hb >= a.shift[d] && hb < a.shift[d] + 64 - __clzll((long long)da.mask[d])) {
+          first = d;
+          break;
+        }
+    }
+  }
+  fdl[p] = (uint8_t)first;
+}
+
+// Everything after the level columns K_d (sorted, level order) and first-differing levels are
+// known: fibers, root slices, subtensor split, fiber_coord, per-depth inds / ptrs (csf.py:126-183).
+int finish_tree(cudaStream_t s, Scratch &sc, int N, int64_t nnz, int64_t thr, bool compact,
+                int32_t *const *K, const uint8_t *fdl, int32_t *const *inds, int32_t *const *ptrs,
+                int32_t *fiber_ptr, int32_t *fiber_coord, int32_t *sub_fiber_ptr,
+                int32_t *sub_leaf_ptr, int32_t *row_fiber_ptr, int32_t *row_coord,
+                int64_t *counts_out) {
+  const unsigned nb = blocks_for(nnz);
+  GatherArgs ga{};
+  ga.N = N;
+  for (int d = 0; d < N; ++d) ga.K[d] = K[d];
+  Compactor comp(s, sc, nnz + 1);
+  uint8_t *flagA = sc.get<uint8_t>(nnz), *flagB = sc.get<uint8_t>(nnz);
+  uint8_t *subflag = sc.get<uint8_t>(nnz);
+  int32_t *scan = sc.get<int32_t>(nnz + 1);
+  int32_t *pos = sc.get<int32_t>(nnz + 1);
+  if (!flagA || !flagB || !subflag || !scan || !pos)
+    return fail(FT_ERR_CUDA, "ft_build_tree: out of device memory (flags)");
+
+  // fibers: runs of equal first N-1 levels
+  int64_t F = 0;
+  flags_le<<<nb, 256, 0, s>>>(fdl, nullptr, nnz, N - 2, flagA);
+  if (int rc = comp.run(flagA, nnz, fiber_ptr, &F)) return rc;
+  set_i32<<<1, 1, 0, s>>>(fiber_ptr + F, (int32_t)nnz);
+
+  // root slices over fibers
+  uint8_t *rflag = sc.get<uint8_t>(F);
+  run_flags<<<blocks_for(F), 256, 0, s>>>(fiber_ptr, fdl, F, rflag);
+  int64_t nruns = 0;
+  if (int rc = comp.run(rflag, F, row_fiber_ptr, &nruns)) return rc;
+  set_i32<<<1, 1, 0, s>>>(row_fiber_ptr + nruns, (int32_t)F);
+  // row_coord[r] = K_0[fiber_ptr[row_fiber_ptr[r]]]
+  {
+    int32_t *first_leaf = sc.get<int32_t>(nruns);
+    gather_i32<<<blocks_for(nruns), 256, 0, s>>>(fiber_ptr, row_fiber_ptr, nruns, first_leaf, 1);
+    gather_i32<<<blocks_for(nruns), 256, 0, s>>>(ga.K[0], first_leaf, nruns, row_coord, 1);
+  }
+
+  // greedy split of each root slice into <= thr whole fibers (csf.py:136-148)
+  int32_t *nch = sc.get<int32_t>(nruns), *off = sc.get<int32_t>(nruns + 1);
+  chunk_counts<<<blocks_for(nruns), 256, 0, s>>>(row_fiber_ptr, nruns, F, thr, nch);
+  {
+    size_t b = 0;
+    FT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b, nch, off, nruns + 1, s));
+    void *t = sc.get<uint8_t>(b);
+    // off has nruns+1 entries: scan over nch padded with a trailing read is unsafe, so scan
+    // nruns entries and compute the total separately.
+    FT_CUDA(cub::DeviceScan::ExclusiveSum(t, b, nch, off, nruns, s));
+  }
+  int32_t hlast[2] = {0, 0};
+  FT_CUDA(cudaMemcpyAsync(&hlast[0], off + nruns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  FT_CUDA(cudaMemcpyAsync(&hlast[1], nch + nruns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  FT_CUDA(cudaStreamSynchronize(s));
+  const int64_t S = (int64_t)hlast[0] + hlast[1];
+  if (!compact) {
+    FT_CUDA(cudaMemsetAsync(subflag, 0, nnz, s));
+    write_chunks<<<blocks_for(nruns), 256, 0, s>>>(row_fiber_ptr, nch, off, nruns, thr, fiber_ptr,
+                                                   sub_fiber_ptr, sub_leaf_ptr, subflag);
+    if (int rc = check_launch("write_chunks")) return rc;
+    set_i32<<<1, 1, 0, s>>>(sub_fiber_ptr + S, (int32_t)F);
+    set_i32<<<1, 1, 0, s>>>(sub_leaf_ptr + S, (int32_t)nnz);
+  }
+
+  // fiber_coord[f, d] = K_d[fiber_ptr[f]]
+  for (int d = 0; d < N - 1; ++d)
+    gather_i32<<<blocks_for(F), 256, 0, s>>>(ga.K[d], fiber_ptr, F, fiber_coord + d, N - 1);
+
+  // per-depth node starts; inds / ptrs.  Depth N-1: every leaf (inds[N-1] already written).
+  counts_out[4 + N - 1] = nnz;
+  int64_t n_next = nnz;
+  uint8_t *flag_next = nullptr;  // flags of depth d+1 (null => all ones)
+  size_t scan_bytes = 0;
+  FT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, flagA, scan, nnz, s));
+  void *scan_tmp = sc.get<uint8_t>(scan_bytes);
+  uint8_t *fl[2] = {flagA, flagB};
+  for (int d = N - 2; d >= 0 && !compact; --d) {
+    uint8_t *flag_d = fl[d & 1];
+    flags_le<<<nb, 256, 0, s>>>(fdl, subflag, nnz, d, flag_d);
+    int64_t n_d = 0;
+    if (int rc = comp.run(flag_d, nnz, pos, &n_d)) return rc;
+    gather_i32<<<blocks_for(n_d), 256, 0, s>>>(ga.K[d], pos, n_d, inds[d], 1);
+    if (flag_next == nullptr) {
+      // child id of a start at position p is p itself
+      FT_CUDA(cudaMemcpyAsync(ptrs[d], pos, n_d * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    } else {
+      size_t b = scan_bytes;
+      FT_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp, b, flag_next, scan, nnz, s));
+      gather_i32<<<blocks_for(n_d), 256, 0, s>>>(scan, pos, n_d, ptrs[d], 1);
+    }
+    set_i32<<<1, 1, 0, s>>>(ptrs[d] + n_d, (int32_t)n_next);
+    counts_out[4 + d] = n_d;
+    n_next = n_d;
+    flag_next = flag_d;
+  }
+  if (int rc = check_launch("build_tree")) return rc;
+  FT_CUDA(cudaStreamSynchronize(s));
+  counts_out[0] = F;
+  counts_out[1] = S;
+  counts_out[2] = nruns;
+  return FT_OK;
+}
+
 }  // namespace
 }  // namespace ft
 
@@ -442,95 +607,8 @@ extern "C" int ft_build_tree(int32_t N, int64_t nnz, const int64_t *dims, const 
     return fail(FT_ERR_DUPLICATE, "duplicate coordinate at entry %lld", (long long)hdup);
   }
 
-  Compactor comp(s, sc, nnz + 1);
-  uint8_t *flagA = sc.get<uint8_t>(nnz), *flagB = sc.get<uint8_t>(nnz);
-  uint8_t *subflag = sc.get<uint8_t>(nnz);
-  int32_t *scan = sc.get<int32_t>(nnz + 1);
-  int32_t *pos = sc.get<int32_t>(nnz + 1);
-  if (!flagA || !flagB || !subflag || !scan || !pos)
-    return fail(FT_ERR_CUDA, "ft_build_tree: out of device memory (flags)");
-
-  // fibers: runs of equal first N-1 levels
-  int64_t F = 0;
-  flags_le<<<nb, 256, 0, s>>>(fdl, nullptr, nnz, N - 2, flagA);
-  if (int rc = comp.run(flagA, nnz, fiber_ptr, &F)) return rc;
-  set_i32<<<1, 1, 0, s>>>(fiber_ptr + F, (int32_t)nnz);
-
-  // root slices over fibers
-  uint8_t *rflag = sc.get<uint8_t>(F);
-  run_flags<<<blocks_for(F), 256, 0, s>>>(fiber_ptr, fdl, F, rflag);
-  int64_t nruns = 0;
-  if (int rc = comp.run(rflag, F, row_fiber_ptr, &nruns)) return rc;
-  set_i32<<<1, 1, 0, s>>>(row_fiber_ptr + nruns, (int32_t)F);
-  // row_coord[r] = K_0[fiber_ptr[row_fiber_ptr[r]]]
-  {
-    int32_t *first_leaf = sc.get<int32_t>(nruns);
-    gather_i32<<<blocks_for(nruns), 256, 0, s>>>(fiber_ptr, row_fiber_ptr, nruns, first_leaf, 1);
-    gather_i32<<<blocks_for(nruns), 256, 0, s>>>(ga.K[0], first_leaf, nruns, row_coord, 1);
-  }
-
-  // greedy split of each root slice into <= thr whole fibers (csf.py:136-148)
-  int32_t *nch = sc.get<int32_t>(nruns), *off = sc.get<int32_t>(nruns + 1);
-  chunk_counts<<<blocks_for(nruns), 256, 0, s>>>(row_fiber_ptr, nruns, F, thr, nch);
-  {
-    size_t b = 0;
-    FT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b, nch, off, nruns + 1, s));
-    void *t = sc.get<uint8_t>(b);
-    // off has nruns+1 entries: scan over nch padded with a trailing read is unsafe, so scan
-    // nruns entries and compute the total separately.
-    FT_CUDA(cub::DeviceScan::ExclusiveSum(t, b, nch, off, nruns, s));
-  }
-  int32_t hlast[2] = {0, 0};
-  FT_CUDA(cudaMemcpyAsync(&hlast[0], off + nruns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-  FT_CUDA(cudaMemcpyAsync(&hlast[1], nch + nruns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-  FT_CUDA(cudaStreamSynchronize(s));
-  const int64_t S = (int64_t)hlast[0] + hlast[1];
-  if (!compact) {
-    FT_CUDA(cudaMemsetAsync(subflag, 0, nnz, s));
-    write_chunks<<<blocks_for(nruns), 256, 0, s>>>(row_fiber_ptr, nch, off, nruns, thr, fiber_ptr,
-                                                   sub_fiber_ptr, sub_leaf_ptr, subflag);
-    if (int rc = check_launch("write_chunks")) return rc;
-    set_i32<<<1, 1, 0, s>>>(sub_fiber_ptr + S, (int32_t)F);
-    set_i32<<<1, 1, 0, s>>>(sub_leaf_ptr + S, (int32_t)nnz);
-  }
-
-  // fiber_coord[f, d] = K_d[fiber_ptr[f]]
-  for (int d = 0; d < N - 1; ++d)
-    gather_i32<<<blocks_for(F), 256, 0, s>>>(ga.K[d], fiber_ptr, F, fiber_coord + d, N - 1);
-
-  // per-depth node starts; inds / ptrs.  Depth N-1: every leaf (inds[N-1] already written).
-  counts_out[4 + N - 1] = nnz;
-  int64_t n_next = nnz;
-  uint8_t *flag_next = nullptr;  // flags of depth d+1 (null => all ones)
-  size_t scan_bytes = 0;
-  FT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, flagA, scan, nnz, s));
-  void *scan_tmp = sc.get<uint8_t>(scan_bytes);
-  uint8_t *fl[2] = {flagA, flagB};
-  for (int d = N - 2; d >= 0 && !compact; --d) {
-    uint8_t *flag_d = fl[d & 1];
-    flags_le<<<nb, 256, 0, s>>>(fdl, subflag, nnz, d, flag_d);
-    int64_t n_d = 0;
-    if (int rc = comp.run(flag_d, nnz, pos, &n_d)) return rc;
-    gather_i32<<<blocks_for(n_d), 256, 0, s>>>(ga.K[d], pos, n_d, inds[d], 1);
-    if (flag_next == nullptr) {
-      // child id of a start at position p is p itself
-      FT_CUDA(cudaMemcpyAsync(ptrs[d], pos, n_d * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-    } else {
-      size_t b = scan_bytes;
-      FT_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp, b, flag_next, scan, nnz, s));
-      gather_i32<<<blocks_for(n_d), 256, 0, s>>>(scan, pos, n_d, ptrs[d], 1);
-    }
-    set_i32<<<1, 1, 0, s>>>(ptrs[d] + n_d, (int32_t)n_next);
-    counts_out[4 + d] = n_d;
-    n_next = n_d;
-    flag_next = flag_d;
-  }
-  if (int rc = check_launch("build_tree")) return rc;
-  FT_CUDA(cudaStreamSynchronize(s));
-  counts_out[0] = F;
-  counts_out[1] = S;
-  counts_out[2] = nruns;
-  return FT_OK;
+  return finish_tree(s, sc, N, nnz, thr, compact, ga.K, fdl, inds, ptrs, fiber_ptr, fiber_coord,
+                     sub_fiber_ptr, sub_leaf_ptr, row_fiber_ptr, row_coord, counts_out);
 }
 
 extern "C" int ft_tree_leaf_index(const ft_tree_t *tree, int32_t *leaf_pc, int32_t *row_leaf_ptr,
@@ -588,4 +666,89 @@ extern "C" int ft_tree_row_segments(const ft_tree_t *tree, int32_t max_len, int3
   FT_CUDA(cudaStreamSynchronize(s));
   *nseg_out = total;
   return FT_OK;
+}
+
+extern "C" int ft_build_tree_derived(const ft_tree_t *prev, const int64_t *dims, int64_t thr,
+                                     float *leaf_vals, int32_t *const *inds, int32_t *const *ptrs,
+                                     int32_t *fiber_ptr, int32_t *fiber_coord,
+                                     int32_t *sub_fiber_ptr, int32_t *sub_leaf_ptr,
+                                     int32_t *row_fiber_ptr, int32_t *row_coord,
+                                     int64_t *counts_out, void *stream) {
+  if (!prev || !dims) return fail(FT_ERR_ARG, "ft_build_tree_derived: null argument");
+  const int N = prev->order;
+  const int64_t nnz = prev->nnz;
+  if (N < 3 || N > 6) return fail(FT_ERR_UNSUPPORTED, "ft_build_tree_derived: order %d", N);
+  if (!prev->leaf_pc || !prev->row_leaf_ptr || !prev->row_coord || !prev->leaf_coord || !prev->vals)
+    return fail(FT_ERR_UNSUPPORTED, "ft_build_tree_derived: previous tree lacks the leaf index");
+  if (nnz <= 0) return fail(FT_ERR_EMPTY, "cannot index an empty tensor");
+  const bool compact = ptrs == nullptr;
+  if (!leaf_vals || !inds || !inds[N - 1] || !fiber_ptr || !fiber_coord || !row_fiber_ptr ||
+      !row_coord || !counts_out || (!compact && (!sub_fiber_ptr || !sub_leaf_ptr)))
+    return fail(FT_ERR_ARG, "ft_build_tree_derived: null argument");
+  const int root = (prev->root_mode + 1) % N;
+  int lm[FT_MAX_ORDER], bits[FT_MAX_ORDER];
+  for (int d = 0; d < N; ++d) {
+    lm[d] = (root + d) % N;
+    const int64_t I = dims[lm[d]];
+    bits[d] = I <= 1 ? 0 : 64 - __builtin_clzll((unsigned long long)(I - 1));
+  }
+  int key_bits = 0;
+  for (int d = 0; d < N - 1; ++d) key_bits += bits[d];
+  if (key_bits > 32 || bits[N - 1] > 32)
+    return fail(FT_ERR_UNSUPPORTED, "ft_build_tree_derived: %d key bits > 32", key_bits);
+  keep_pool();
+  cudaStream_t s = as_stream(stream);
+  Scratch sc(s);
+  DerivedArgs a{};
+  a.N = N;
+  {
+    int sh = 0;
+    for (int d = N - 2; d >= 0; --d) {  // level 0 most significant
+      a.shift[d] = sh;
+      sh += bits[d];
+    }
+  }
+  const int64_t rows = prev->num_rows;
+  const unsigned nb = blocks_for(nnz);
+  // row index of every leaf of the previous tree: mark row starts, inclusive max-scan
+  uint32_t *mark = sc.get<uint32_t>(nnz), *leaf_row = sc.get<uint32_t>(nnz);
+  uint32_t *k0 = sc.get<uint32_t>(nnz), *k1 = sc.get<uint32_t>(nnz);
+  unsigned long long *q0 = sc.get<unsigned long long>(nnz), *q1 = sc.get<unsigned long long>(nnz);
+  if (!mark || !leaf_row || !k0 || !k1 || !q0 || !q1)
+    return fail(FT_ERR_CUDA, "ft_build_tree_derived: out of device memory");
+  FT_CUDA(cudaMemsetAsync(mark, 0, nnz * sizeof(uint32_t), s));
+  row_start_mark<<<blocks_for(rows), 256, 0, s>>>(prev->row_leaf_ptr, rows, mark);
+  {
+    size_t b = 0;
+    FT_CUDA(cub::DeviceScan::InclusiveScan(nullptr, b, mark, leaf_row, cub::Max(), nnz, s));
+    void *t = sc.get<uint8_t>(b);
+    if (!t) return fail(FT_ERR_CUDA, "ft_build_tree_derived: out of device memory (scan)");
+    FT_CUDA(cub::DeviceScan::InclusiveScan(t, b, mark, leaf_row, cub::Max(), nnz, s));
+  }
+  pack_derived<<<nb, 256, 0, s>>>(leaf_row, prev->row_coord, prev->leaf_pc, prev->leaf_coord,
+                                  prev->vals, nnz, a, k0, q0);
+  if (int rc = check_launch("pack_derived")) return rc;
+  {
+    size_t b = 0;
+    FT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b, k0, k1, q0, q1, nnz, 0, key_bits, s));
+    void *t = sc.get<uint8_t>(b);
+    if (!t) return fail(FT_ERR_CUDA, "ft_build_tree_derived: out of device memory (sort)");
+    FT_CUDA(cub::DeviceRadixSort::SortPairs(t, b, k0, k1, q0, q1, nnz, 0, key_bits, s));
+  }
+  int32_t *K[FT_MAX_ORDER];
+  DecodeArgs da{};
+  da.N = N;
+  for (int d = 0; d < N; ++d) {
+    K[d] = (d == N - 1) ? inds[N - 1] : sc.get<int32_t>(nnz);
+    if (!K[d]) return fail(FT_ERR_CUDA, "ft_build_tree_derived: out of device memory (levels)");
+    da.K[d] = K[d];
+    da.mask[d] = bits[d] >= 64 ? ~0ull : ((1ull << bits[d]) - 1);
+  }
+  uint8_t *fdl = sc.get<uint8_t>(nnz);
+  decode_derived<<<nb, 256, 0, s>>>(k1, q1, nnz, a, da, leaf_vals, fdl);
+  if (int rc = check_launch("decode_derived")) return rc;
+  for (int k = 0; k < 4 + N; ++k) counts_out[k] = 0;
+  counts_out[3] = -1;
+  return finish_tree(s, sc, N, nnz, thr, compact, K, fdl, inds, ptrs, fiber_ptr, fiber_coord,
+                     sub_fiber_ptr, sub_leaf_ptr, row_fiber_ptr, row_coord, counts_out);
 }

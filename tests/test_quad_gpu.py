@@ -182,3 +182,31 @@ def test_refresh_tensor_core_matches_fp64(ft, I, J, R):
                                     _lib.stream_handle()), "ft_refresh_scatter")
     np.testing.assert_array_equal(C.cpu().numpy(), C2.cpu().numpy())
     np.testing.assert_array_equal(C.cpu().numpy(), got.astype(np.float32))
+
+
+@pytest.mark.parametrize("dims,compact", [((3000, 400, 60), True), ((3000, 400, 60), False),
+                                          ((60, 50, 40, 30), True), ((40, 30, 20, 10), False)])
+def test_derived_tree_build_is_bit_identical(ft, dims, compact):
+    """K1 derived build (tree t+1 from tree t's leaf order, 32-bit-key stable sort) produces
+    exactly the arrays of the COO build, reference-format fields included."""
+    import torch
+    from paper_2210_06014_b200 import csf
+
+    rng = np.random.default_rng(len(dims) + int(compact))
+    lin = rng.choice(int(np.prod(dims)), size=min(300_000, int(np.prod(dims)) // 3), replace=False)
+    idx = np.stack(np.unravel_index(lin, dims), axis=1)
+    dev = ft.DeviceCoo(dims, torch.from_numpy(idx.astype(np.int32)).cuda(),
+                       torch.from_numpy(rng.uniform(1, 5, len(lin)).astype(np.float32)).cuda())
+    prev = csf.build_tree(dev, 0, 16, compact=compact)
+    for t in range(1, len(dims)):
+        want = csf.build_tree(dev, t, 16, compact=compact)
+        got = csf.build_tree_derived(prev, 16, compact=compact)
+        assert got is not None
+        for name in ("vals", "fiber_ptr", "fiber_coord", "row_fiber_ptr", "row_coord", "leaf_pc",
+                     "row_leaf_ptr", "seg_coord", "seg_leaf_ptr", "sub_fiber_ptr", "sub_leaf_ptr"):
+            np.testing.assert_array_equal(getattr(got, name).cpu().numpy(),
+                                          getattr(want, name).cpu().numpy(), err_msg=name)
+        for a, b in zip(got.inds + got.ptrs, want.inds + want.ptrs):
+            np.testing.assert_array_equal(a.cpu().numpy(), b.cpu().numpy())
+        assert got.num_subtensors == want.num_subtensors
+        prev = got

@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quad_kernel(const Sw
 // whose Vᵀ column lands exactly in those lanes' accumulators (d0/d2 for even k, d1/d3 for odd).
 // The dot product reduces over lane bits 2-4 (xor 4, 8, 16).  Same arithmetic, order and
 // gathers as quad; row streams rho are numbered block-fastest.
-template <bool SMALL, int NPRE, int WPBT>
+template <bool SMALL, int NPRE, int WPBT, bool TMA = false>
 __global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quadr_kernel(const SweepParams p) {
   using namespace quad;
   extern __shared__ float4 smem4[];
@@ -391,6 +391,12 @@ __global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quadr_kernel(const S
   float *Y = X + TILE;
   float4 *meta = reinterpret_cast<float4 *>(Y + TILE);
   for (int k = lane; k < 2 * TILE; k += 32) X[k] = 0.f;
+  // TMA: one bulk copy per C row (cp.async.bulk, completion on a per-warp mbarrier) instead of
+  // eight 16-B cp.async per row -- the copies bypass the LSU / L1 request path entirely
+  uint64_t *bar = reinterpret_cast<uint64_t *>(reinterpret_cast<float *>(afr + BFRAG_U4) +
+                                               WPBT * quad::WARP_FLOATS) + w;
+  uint32_t tphase = 0;
+  if (TMA && lane == 0) mbar_init(bar, 1);
   quad_afrag_init(p, afr);
   __syncthreads();
   constexpr int mts = SMALL ? 1 : 2, nkt = SMALL ? 2 : 4;
@@ -481,7 +487,20 @@ __global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quadr_kernel(const S
         ppc[d] = ok ? __ldcs(p.leaf_pc + (int64_t)(pos + sk) * NPRE + d) : 0;
       px = ok ? __ldcs(p.vals + pos + sk) : 0.f;
     }
-    quad_gather<NPRE, XS>(p, X, Y, pc, lc, lane);
+    if (TMA) {  // NPRE == 1 (order 3): lane = slot
+      const uint32_t rb = (uint32_t)p.R * 4;
+      fence_proxy_async();  // the previous batch's generic reads of X / Y precede the async writes
+      __syncwarp();
+      if (lane == 0) mbar_expect_tx(bar, 64 * rb);
+      __syncwarp();
+      bulk_copy(X + lane * XS, p.Cpre[0] + (int64_t)pc[0] * p.R, rb, bar);
+      bulk_copy(Y + lane * XS, p.Cleaf + (int64_t)lc * p.R, rb, bar);
+      mbar_wait(bar, tphase);
+      tphase ^= 1;
+      __syncwarp();
+    } else {
+      quad_gather<NPRE, XS>(p, X, Y, pc, lc, lane);
+    }
     float acc[2][4][4];
     quad_zero(acc);
 #pragma unroll
@@ -520,17 +539,17 @@ __global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quadr_kernel(const S
   }
 }
 
-template <bool SMALL, int NPRE, int WPBT>
+template <bool SMALL, int NPRE, int WPBT, bool TMA = false>
 int launch_quadr_t(const SweepParams &q, cudaStream_t s) {
-  const size_t sm = (size_t)quad::BFRAG_U4 * 16 + (size_t)WPBT * quad::WARP_FLOATS * 4;
+  const size_t sm = (size_t)quad::BFRAG_U4 * 16 + (size_t)WPBT * quad::WARP_FLOATS * 4 + WPBT * 8;
   static bool set = false;
   if (!set) {
-    cudaFuncSetAttribute(factor_rows_quadr_kernel<SMALL, NPRE, WPBT>,
+    cudaFuncSetAttribute(factor_rows_quadr_kernel<SMALL, NPRE, WPBT, TMA>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     set = true;
   }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quadr_kernel<SMALL, NPRE, WPBT>,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quadr_kernel<SMALL, NPRE, WPBT, TMA>,
                                                     WPBT * 32, sm) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
@@ -538,12 +557,15 @@ int launch_quadr_t(const SweepParams &q, cudaStream_t s) {
   const int64_t cap = (int64_t)sm_count() * per_sm;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
-  factor_rows_quadr_kernel<SMALL, NPRE, WPBT><<<(int)g, WPBT * 32, sm, s>>>(q);
+  factor_rows_quadr_kernel<SMALL, NPRE, WPBT, TMA><<<(int)g, WPBT * 32, sm, s>>>(q);
   return check_launch("ft_factor_sweep_rows(quadr)");
 }
 
 int launch_quadr(const SweepParams &q, cudaStream_t s) {
   const bool small = q.J <= 16 && q.R <= 16;
+  if (q.tma && q.N == 3 && (q.R & 3) == 0)  // FT_GATHER=tma: bulk-copy gathers
+    return small ? launch_quadr_t<true, 1, quad::WPB, true>(q, s)
+                 : launch_quadr_t<false, 1, quad::WPB, true>(q, s);
   // 9 warps per block when that fits all rows in one wave (see launch_quad)
   const int64_t slots8 = (int64_t)sm_count() * 2 * quad::WPB * 4, slots9 = slots8 * 9 / 8;
   const bool w9 = q.nrows > slots8 && q.nrows <= slots9;

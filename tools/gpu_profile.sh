@@ -10,7 +10,7 @@ ncu --set full --clock-control none --import-source on -k regex:"factor_rows|cor
   --launch-skip 18 -c 6 -o gpurun_out/sweeps -f \
   python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/sweeps_bench.log 2>&1
 echo sweeps $?
-ncu --set full --clock-control none -k regex:"refresh_tc|decode_levels|pack_keys_vals|leaf_pc_kernel|Onesweep" \
+ncu --set full --clock-control none -k regex:"refresh_tc|decode_levels|pack_keys_vals|pack_derived|decode_derived|leaf_pc_kernel" \
   -c 10 -o gpurun_out/aux -f python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/aux_bench.log 2>&1
 echo aux $?
 for c in netflix16 yahoo32 order6 order4; do

@@ -378,6 +378,9 @@ __global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quad_kernel(const Sw
 // whose Vᵀ column lands exactly in those lanes' accumulators (d0/d2 for even k, d1/d3 for odd).
 // The dot product reduces over lane bits 2-4 (xor 4, 8, 16).  Same arithmetic, order and
 // gathers as quad; row streams rho are numbered block-fastest.
+#ifndef QUADR_FULL8
+#define QUADR_FULL8 1  // always run 8 chain steps (padding steps are no-ops): no break, loads hoist
+#endif
 template <bool SMALL, int NPRE, int WPBT, bool TMA = false>
 __global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quadr_kernel(const SweepParams p) {
   using namespace quad;
@@ -510,7 +513,7 @@ __global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quadr_kernel(const S
     }
     __syncwarp();  // meta visible (its stores precede the gathers' waits)
     // ---- four serial chains on the accumulator registers ----
-    const int nbmax = __reduce_max_sync(FULL, (unsigned)nb);
+    const int nbmax = QUADR_FULL8 ? QB : __reduce_max_sync(FULL, (unsigned)nb);
     const float4 *mq = meta + rho * MQ;
 #pragma unroll
     for (int k = 0; k < QB; ++k) {

@@ -1395,6 +1395,9 @@ constexpr size_t bytes() { return (size_t)WPB * WARP_FLOATS * 4; }
 // SSE = true: the same walk scores the tree's leaves instead (K6b, evaluate over the training
 // entries, train.py:91-98): per slot e = x - C_u[i] . cross, sum e^2 and |e| in fp64 per lane,
 // fixed-order block reduction to p.partials as doubles [block][2] (no gradient work).
+#ifndef CORE_FUSED
+#define CORE_FUSED 1  // K4 quad: fused single pass in the quarter layout (0: lane-per-slot s-pass)
+#endif
 template <bool SSE, int NPRE>
 __global__ void __launch_bounds__(cquad::WPB * 32, 2) core_rows_quad_kernel(const SweepParams p) {
   using namespace cquad;
@@ -1421,10 +1424,16 @@ __global__ void __launch_bounds__(cquad::WPB * 32, 2) core_rows_quad_kernel(cons
     nLb = __ldg(p.row_leaf_ptr + row + nstream);
     nLe = __ldg(p.row_leaf_ptr + row + nstream + 1);
   }
+  float2 cu01 = make_float2(0.f, 0.f), cu23 = cu01;  // C_u[i_q][4l .. 4l+3] (fused pass)
   auto load_cu = [&](int i) {  // C_u[i, 0:R) -> cus[q][.] (zero beyond R)
-    if (4 * l < R)
-      *reinterpret_cast<float4 *>(cus + 32 * q + 4 * l) =
-          *reinterpret_cast<const float4 *>(p.Cu + (int64_t)i * R + 4 * l);
+    if (4 * l < R) {
+      const float4 v = *reinterpret_cast<const float4 *>(p.Cu + (int64_t)i * R + 4 * l);
+      if (CORE_FUSED) {
+        cu01 = make_float2(v.x, v.y), cu23 = make_float2(v.z, v.w);
+      } else {
+        *reinterpret_cast<float4 *>(cus + 32 * q + 4 * l) = v;
+      }
+    }
   };
   if (ci >= 0) load_cu(ci);
   int plc = 0, ppc[NPRE];
@@ -1505,6 +1514,39 @@ __global__ void __launch_bounds__(cquad::WPB * 32, 2) core_rows_quad_kernel(cons
       px = ok ? __ldcs(p.vals + pos + l) : 0.f;
     }
     quad_gather<NPRE, XS>(p, X, Y, pc, lc, lane);
+    if (CORE_FUSED) {
+      // one pass in the quarter layout (lane l: columns 4l..4l+3 of its quarter's rows): the
+      // same X / Y loads feed s_k (partial dot with C_u[i], reduced over the quarter's 8 lanes)
+      // and g += e_k cross_k -- half the shared-memory reads of the two-pass form
+      const float *xq = X + 8 * q * XS + 4 * l, *yq = Y + 8 * q * XS + 4 * l;
+#pragma unroll
+      for (int k = 0; k < quad::QB; ++k) {
+        const float4 xv = *reinterpret_cast<const float4 *>(xq + k * XS);
+        const float4 yv = *reinterpret_cast<const float4 *>(yq + k * XS);
+        const float2 c01 = fmul2(make_float2(xv.x, xv.y), make_float2(yv.x, yv.y));
+        const float2 c23 = fmul2(make_float2(xv.z, xv.w), make_float2(yv.z, yv.w));
+        const float2 sp = ffma2(c23, cu23, fmul2(c01, cu01));
+        float sv = sp.x + sp.y;
+        sv += __shfl_xor_sync(FULL, sv, 1);
+        sv += __shfl_xor_sync(FULL, sv, 2);
+        sv += __shfl_xor_sync(FULL, sv, 4);
+        const float xk = __shfl_sync(FULL, x, 8 * q + k);
+        const float e = k < nb ? xk - sv : 0.f;
+        if (SSE) {
+          if (l == 0) {
+            sse += (double)e * (double)e;
+            sae += fabs((double)e);
+          }
+        } else {
+          const float2 e2 = make_float2(e, e);
+          g01 = ffma2(e2, c01, g01);
+          g23 = ffma2(e2, c23, g23);
+        }
+      }
+      __syncwarp();
+      cL0 += nb;
+      continue;
+    }
     // ---- lane = slot: s = C_u[i_q] . (X * Y), e = x - s ----
     {
       const float4 *xr = reinterpret_cast<const float4 *>(X + lane * XS);

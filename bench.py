@@ -96,18 +96,40 @@ class Clocks:
         self.gpu = gpu_index
         self.proc = None
 
+    def _lines(self):
+        try:
+            with open(self.path) as fh:
+                return sum(1 for _ in fh)
+        except OSError:
+            return 0
+
     def start(self):
+        """Start sampling and wait for nvidia-smi's first line (it takes ~0.1-1 s to come up),
+        so the timed region that follows is covered."""
+        self.mark = 0
         try:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=self.fh, stderr=subprocess.DEVNULL)
+            t0 = time.time()
+            while self._lines() == 0 and time.time() - t0 < 10 and self.proc.poll() is None:
+                time.sleep(0.05)
         except Exception:
             self.proc = None
+
+    def begin(self):
+        """The timed region starts: only samples taken from here on count."""
+        self.mark = self._lines()
 
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        # a timed region shorter than the sampling interval still gets the sample taken right
+        # after it (same load, clocks do not move that fast)
+        t0 = time.time()
+        while self._lines() <= self.mark and time.time() - t0 < 2 and self.proc.poll() is None:
+            time.sleep(0.02)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -116,7 +138,9 @@ class Clocks:
         self.fh.close()
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
+        for n_line, line in enumerate(open(self.path)):
+            if n_line < self.mark:
+                continue
             f = [x.strip() for x in line.split(",")]
             if len(f) < 9:
                 continue
@@ -301,6 +325,8 @@ def run_ours(args, cfg):
         if ev:
             ev[2].record()
 
+    clocks = Clocks(local)
+    clocks.start()  # before the warm-up: the sampler is up and the clocks ramped when timing starts
     for _ in range(args.warmup):
         epoch()
     torch.cuda.synchronize()
@@ -309,9 +335,8 @@ def run_ours(args, cfg):
 
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     T.KERNEL_TIMER = T.KernelTimer()
-    clocks = Clocks(local)
-    clocks.start()
     torch.cuda.synchronize()
+    clocks.begin()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record()
     for k in range(args.steps):

@@ -397,10 +397,18 @@ def bench_distributed(args, cfg, rank, world):
                           peer_dots=os.environ.get("FT_PEER", "1") == "1")
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
+    clocks = None
+    if rank == 0:
+        import bench as _bench  # the driver's bench module (repo root): its nvidia-smi sampler
+
+        clocks = _bench.Clocks(int(os.environ.get("LOCAL_RANK", "0")))
+        clocks.start()
     for k in range(args.warmup):
         trainer.run_epoch(k + 1)
     torch.cuda.synchronize()
     dist.barrier()
+    if clocks is not None:
+        clocks.begin()
     start, mid, stop = (torch.cuda.Event(enable_timing=True) for _ in range(3))
     fsum = 0.0
     start.record()
@@ -414,6 +422,7 @@ def bench_distributed(args, cfg, rank, world):
         fsum += a.elapsed_time(b)
     stop.record()
     torch.cuda.synchronize()
+    clk = clocks.stop() if clocks is not None else None
     dist.barrier()
     mine = torch.tensor([start.elapsed_time(stop) / 1e3, fsum / 1e3], dtype=torch.float64,
                         device="cuda")
@@ -437,7 +446,7 @@ def bench_distributed(args, cfg, rank, world):
             "factor_ms": 1e3 * f_s / args.steps,
             "train_rmse": tr[0], "test_rmse": te[0], "setup_s": setup_s,
             "gpu_launches": (6 * N) * args.steps,
-            "e2e": e2e, "roofline": None, "cpu_baseline": None,
+            "e2e": e2e, "roofline": None, "cpu_baseline": None, "clocks": clk,
         }
         print(json.dumps(line), flush=True)
     dist.barrier()

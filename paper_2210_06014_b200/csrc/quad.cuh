@@ -135,6 +135,23 @@ __device__ __forceinline__ void quad_store_v(float *V, const float (&acc)[2][4][
     }
 }
 
+// as quad_store_v, with quarter q's 8 rows shifted by 4 q floats (lane-per-row readers of four
+// quarters then hit disjoint banks)
+__device__ __forceinline__ void quad_store_v_pad(float *V, const float (&acc)[2][4][4], int lane) {
+  using namespace quad;
+  const int gq = lane >> 2, tq = lane & 3;
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      float *v = V + (8 * nt + 2 * tq) * QVS + 4 * nt + 16 * mt + gq;
+      v[0] = acc[mt][nt][0];
+      v[QVS] = acc[mt][nt][1];
+      v[8] = acc[mt][nt][2];
+      v[QVS + 8] = acc[mt][nt][3];
+    }
+}
+
 __device__ __forceinline__ void quad_zero(float (&acc)[2][4][4]) {
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
@@ -1017,7 +1034,8 @@ namespace quadw {
 constexpr int NS = 4;   // ring stages (producer k writes stages k, k+2)
 constexpr int NP = 2;   // producers per group
 // stage: V [32][QVS] | meta float4 [4][MQ] | info int4 [4] | A rows [4][32] | lr*G^T [4][8][8]
-constexpr int STAGE_FLOATS = 32 * quad::QVS + 4 * quad::MQ * 4 + 4 * 4 + 4 * 32 + 4 * 64;
+constexpr int VREG = 32 * quad::QVS + 16;  // V (+16: the lane-per-row consumer's quarter padding)
+constexpr int STAGE_FLOATS = VREG + 4 * quad::MQ * 4 + 4 * 4 + 4 * 32 + 4 * 64;
 // ring + X, Y per producer + the consumer's row exchange [4][32]
 constexpr int GROUP_FLOATS = NS * STAGE_FLOATS + NP * 2 * quad::TILE + 4 * 32;
 constexpr int BAR_BYTES = 2 * NS * 8 + 16;
@@ -1027,7 +1045,7 @@ constexpr size_t bytes() {
 }
 }  // namespace quadw
 
-template <bool GRAM, bool SMALL>
+template <bool GRAM, bool SMALL, bool LPR = false>
 __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(const SweepParams p) {
   using namespace quad;
   using quadp::Leaf;
@@ -1060,16 +1078,16 @@ __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(co
   // stage layout: V [32][QVS] | meta float4 [4][MQ] | info int4 [4] | A rows [4][32]
   auto stage_v = [&](int st) { return ring + st * quadw::STAGE_FLOATS; };
   auto stage_meta = [&](int st) {
-    return reinterpret_cast<float4 *>(ring + st * quadw::STAGE_FLOATS + 32 * QVS);
+    return reinterpret_cast<float4 *>(ring + st * quadw::STAGE_FLOATS + quadw::VREG);
   };
   auto stage_info = [&](int st) {
-    return reinterpret_cast<int4 *>(ring + st * quadw::STAGE_FLOATS + 32 * QVS + 4 * MQ * 4);
+    return reinterpret_cast<int4 *>(ring + st * quadw::STAGE_FLOATS + quadw::VREG + 4 * MQ * 4);
   };
   auto stage_a = [&](int st) {
-    return ring + st * quadw::STAGE_FLOATS + 32 * QVS + 4 * MQ * 4 + 16;
+    return ring + st * quadw::STAGE_FLOATS + quadw::VREG + 4 * MQ * 4 + 16;
   };
   auto stage_g = [&](int st) {  // lr * G^T: [q][l][m] = lr v_{8q+m} . v_{8q+l}
-    return ring + st * quadw::STAGE_FLOATS + 32 * QVS + 4 * MQ * 4 + 16 + 4 * 32;
+    return ring + st * quadw::STAGE_FLOATS + quadw::VREG + 4 * MQ * 4 + 16 + 4 * 32;
   };
 
   if (w > 0) {
@@ -1153,7 +1171,10 @@ __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(co
       if (t >= quadw::NS) mbar_wait(empty + st, ((t / quadw::NS) - 1) & 1);
       int4 *info = stage_info(st);
       if (!stop) {
-        quad_store_v(stage_v(st), acc, lane);
+        if (LPR)
+          quad_store_v_pad(stage_v(st), acc, lane);
+        else
+          quad_store_v(stage_v(st), acc, lane);
         if (GRAM) {  // lane (q, l): lr G[m][l] = lr v_m . v_l over the quarter's batch, fp32
           __syncwarp();
           const float4 *vs = reinterpret_cast<const float4 *>(stage_v(st) + 8 * q * QVS);
@@ -1192,6 +1213,85 @@ __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(co
     cp_async_wait_all();
   } else {
     // ===================================== consumer =====================================
+    if (LPR) {
+      // lane-per-row: lane q (0..3; lanes 4..31 mirror them) holds its whole row in 32
+      // registers and computes s = a . v in-lane from the full V row -- no cross-lane
+      // reduction on the serial path; the next step's V row is loaded under the current step
+      const int qr = lane & 3;
+      float a[32];
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) a[jj] = 0.f;
+      int ai = -1;
+      auto store_full = [&]() {
+        if (lane >= 4) return;
+        float *ar = p.A + (int64_t)ai * J;
+        if (j32) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            reinterpret_cast<float4 *>(ar)[c] = make_float4(a[4 * c], a[4 * c + 1], a[4 * c + 2], a[4 * c + 3]);
+        } else {
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj)
+            if (jj < J) ar[jj] = a[jj];
+        }
+      };
+      for (int t = 0;; ++t) {
+        const int st = t % quadw::NS;
+        mbar_wait(full + st, (t / quadw::NS) & 1);
+        const int4 info = stage_info(st)[qr];
+        if (info.w) break;
+        if (info.y) {
+          if (ai >= 0) store_full();
+          const float4 *ar = reinterpret_cast<const float4 *>(stage_a(st) + 32 * qr);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float4 v = ar[c];
+            a[4 * c] = v.x, a[4 * c + 1] = v.y, a[4 * c + 2] = v.z, a[4 * c + 3] = v.w;
+          }
+          ai = info.z;
+        }
+        const float4 *Vr = reinterpret_cast<const float4 *>(stage_v(st) + 8 * qr * QVS + 4 * qr);
+        const float4 *mq = stage_meta(st) + qr * MQ;
+        float4 vc[8], vn[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) vc[c] = Vr[c];
+#pragma unroll
+        for (int kk = 0; kk < QB; ++kk) {
+          if (kk + 1 < QB) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) vn[c] = Vr[(kk + 1) * (QVS / 4) + c];
+          }
+          const float4 m = mq[kk];
+          float2 s0 = make_float2(0.f, 0.f), s1 = s0, s2 = s0, s3 = s0;
+#pragma unroll
+          for (int c = 0; c < 8; c += 2) {
+            s0 = ffma2(make_float2(a[4 * c], a[4 * c + 1]), make_float2(vc[c].x, vc[c].y), s0);
+            s1 = ffma2(make_float2(a[4 * c + 2], a[4 * c + 3]), make_float2(vc[c].z, vc[c].w), s1);
+            s2 = ffma2(make_float2(a[4 * c + 4], a[4 * c + 5]), make_float2(vc[c + 1].x, vc[c + 1].y), s2);
+            s3 = ffma2(make_float2(a[4 * c + 6], a[4 * c + 7]), make_float2(vc[c + 1].z, vc[c + 1].w), s3);
+          }
+          const float sv = ((s0.x + s0.y) + (s1.x + s1.y)) + ((s2.x + s2.y) + (s3.x + s3.y));
+          const float e = m.x - sv;  // (x, lr, -lr reg, -lr reg); lr = 0 on padding steps
+          const float lre = m.y * e;
+          const float2 c2 = make_float2(m.z, m.w), l2 = make_float2(lre, lre);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            float2 lo = make_float2(a[4 * c], a[4 * c + 1]), hi = make_float2(a[4 * c + 2], a[4 * c + 3]);
+            lo = ffma2(l2, make_float2(vc[c].x, vc[c].y), ffma2(c2, lo, lo));
+            hi = ffma2(l2, make_float2(vc[c].z, vc[c].w), ffma2(c2, hi, hi));
+            a[4 * c] = lo.x, a[4 * c + 1] = lo.y, a[4 * c + 2] = hi.x, a[4 * c + 3] = hi.y;
+          }
+          if (kk + 1 < QB) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) vc[c] = vn[c];
+          }
+        }
+        __syncwarp();
+        mbar_arrive(empty + st);
+      }
+      if (ai >= 0) store_full();
+      return;
+    }
     float a[4] = {0.f, 0.f, 0.f, 0.f};
     int ai = -1;
     float *xrow = ring + quadw::NS * quadw::STAGE_FLOATS + quadw::NP * 2 * TILE + 32 * q;
@@ -1284,17 +1384,17 @@ __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(co
   }
 }
 
-template <bool GRAM, bool SMALL>
+template <bool GRAM, bool SMALL, bool LPR = false>
 int launch_quadw_t(const SweepParams &q, cudaStream_t s) {
   const size_t sm = quadw::bytes();
   static bool set = false;
   if (!set) {
-    cudaFuncSetAttribute(factor_rows_quadw_kernel<GRAM, SMALL>,
+    cudaFuncSetAttribute(factor_rows_quadw_kernel<GRAM, SMALL, LPR>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     set = true;
   }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quadw_kernel<GRAM, SMALL>,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quadw_kernel<GRAM, SMALL, LPR>,
                                                     quadw::THREADS, sm) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
@@ -1302,12 +1402,19 @@ int launch_quadw_t(const SweepParams &q, cudaStream_t s) {
   const int64_t cap = (int64_t)sm_count() * per_sm;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
-  factor_rows_quadw_kernel<GRAM, SMALL><<<(int)g, quadw::THREADS, sm, s>>>(q);
+  factor_rows_quadw_kernel<GRAM, SMALL, LPR><<<(int)g, quadw::THREADS, sm, s>>>(q);
   return check_launch("ft_factor_sweep_rows(quadw)");
 }
 
 template <bool GRAM>
 int launch_quadw(const SweepParams &q, cudaStream_t s) {
+  static const bool lpr = [] {  // FT_QUADW_LPR=1: lane-per-row consumer
+    const char *e = getenv("FT_QUADW_LPR");
+    return e && strcmp(e, "1") == 0;
+  }();
+  if (!GRAM && lpr)
+    return q.J <= 16 && q.R <= 16 ? launch_quadw_t<false, true, true>(q, s)
+                                  : launch_quadw_t<false, false, true>(q, s);
   return q.J <= 16 && q.R <= 16 ? launch_quadw_t<GRAM, true>(q, s) : launch_quadw_t<GRAM, false>(q, s);
 }
 

@@ -106,12 +106,15 @@ FT_API int ft_sm_count(int32_t *out);
  * Compact build: ptrs == NULL (and inds[d < N-1], sub_fiber_ptr, sub_leaf_ptr may be NULL)
  *   skips the reference-format per-depth arrays and subtensors, producing only what the sweep
  *   kernels read (leaf coordinates, values, fiber_ptr / fiber_coord, rows).
+ * leaf_pc (optional, device int32 [nnz x (N-2)], 3 <= N <= 6): the leaf-major prefix index of
+ *   ft_tree_leaf_index, written from the sorted level columns at no extra pass.
  * Returns FT_ERR_DUPLICATE (with counts_out[3] set) if two entries share a coordinate. */
 FT_API int ft_build_tree(int32_t N, int64_t nnz, const int64_t *dims, const int32_t *idx,
                   const float *vals, int32_t root_mode, int64_t thr, float *leaf_vals,
                   int32_t *const *inds, int32_t *const *ptrs, int32_t *fiber_ptr,
                   int32_t *fiber_coord, int32_t *sub_fiber_ptr, int32_t *sub_leaf_ptr,
-                  int32_t *row_fiber_ptr, int32_t *row_coord, int64_t *counts_out, void *stream);
+                  int32_t *row_fiber_ptr, int32_t *row_coord, int64_t *counts_out,
+                  int32_t *leaf_pc, void *stream);
 
 /* K1  derived build: the tree rooted at (prev->root_mode + 1) mod N from the tree `prev`
  * (which must carry the leaf-major index, ft_tree_leaf_index): a stable 32-bit-key radix sort
@@ -124,7 +127,8 @@ FT_API int ft_build_tree_derived(const ft_tree_t *prev, const int64_t *dims, int
                                  float *leaf_vals, int32_t *const *inds, int32_t *const *ptrs,
                                  int32_t *fiber_ptr, int32_t *fiber_coord, int32_t *sub_fiber_ptr,
                                  int32_t *sub_leaf_ptr, int32_t *row_fiber_ptr,
-                                 int32_t *row_coord, int64_t *counts_out, void *stream);
+                                 int32_t *row_coord, int64_t *counts_out, int32_t *leaf_pc,
+                                 void *stream);
 /* K1b Leaf-major index of a built tree (reads tree->fiber_ptr / fiber_coord / row_fiber_ptr):
  *   leaf_pc[L * (N-2) + d] = fiber_coord[f(L) * (N-1) + 1 + d], d < N-2, for every leaf L of
  *   fiber f(L) (the prefix levels 1..N-2 expanded to the leaves; orders 3-6 only), and

@@ -74,11 +74,11 @@ SIGNATURES = {
     "ft_sm_count": (ctypes.c_int, [_i32p]),
     "ft_build_tree": (ctypes.c_int, [
         ctypes.c_int32, ctypes.c_int64, _i64p, _vp, _vp, ctypes.c_int32, ctypes.c_int64, _vp,
-        ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp, _vp, _vp, _vp, _vp, _vp, _i64p, _vp]),
+        ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp, _vp, _vp, _vp, _vp, _vp, _i64p, _vp, _vp]),
     "ft_tree_leaf_index": (ctypes.c_int, [ctypes.POINTER(FtTree), _vp, _vp, _vp]),
     "ft_build_tree_derived": (ctypes.c_int, [
         ctypes.POINTER(FtTree), _i64p, ctypes.c_int64, _vp, ctypes.POINTER(_vp),
-        ctypes.POINTER(_vp), _vp, _vp, _vp, _vp, _vp, _vp, _i64p, _vp]),
+        ctypes.POINTER(_vp), _vp, _vp, _vp, _vp, _vp, _vp, _i64p, _vp, _vp]),
     "ft_tree_row_segments": (ctypes.c_int, [ctypes.POINTER(FtTree), ctypes.c_int32, _vp, _vp,
                                             _i64p, _vp]),
     "ft_refresh": (ctypes.c_int, [

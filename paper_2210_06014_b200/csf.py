@@ -252,6 +252,7 @@ def _build_with(call, N, nnz, dims, root_mode, compact, stream, what, on_duplica
     row_fiber_ptr = torch.empty(nnz + 1, **i32)
     row_coord = torch.empty(nnz, **i32)
     counts = np.zeros(4 + N, dtype=np.int64)
+    leaf_pc = torch.empty((nnz, N - 2), **i32) if 3 <= N <= _leaf_index_max_order() else None
     ind_ptrs = [None] * (N - 1) + [leaf.data_ptr()] if compact else [a.data_ptr() for a in inds]
     ind_tab = (ctypes.c_void_p * N)(*ind_ptrs)
     ptr_tab = None if compact else (ctypes.c_void_p * max(N - 1, 1))(*[a.data_ptr() for a in ptrs])
@@ -259,7 +260,7 @@ def _build_with(call, N, nnz, dims, root_mode, compact, stream, what, on_duplica
            "args": (leaf_vals.data_ptr(), ind_tab, ptr_tab, fiber_ptr.data_ptr(),
                     fiber_coord.data_ptr(), _lib.ptr(sub_fiber_ptr), _lib.ptr(sub_leaf_ptr),
                     row_fiber_ptr.data_ptr(), row_coord.data_ptr(),
-                    counts.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                    counts.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), _lib.ptr(leaf_pc),
                     _lib.stream_handle(stream))}
     rc = call(out)
     if rc == _lib.FT_ERR_DUPLICATE and on_duplicate is not None:
@@ -293,11 +294,17 @@ def _build_with(call, N, nnz, dims, root_mode, compact, stream, what, on_duplica
         row_coord=_trim(row_coord, rows),
     )
     tree.num_subtensors_built = S
-    add_leaf_index(tree, stream)
+    add_leaf_index(tree, stream, leaf_pc=leaf_pc)
     return tree
 
 
-def add_leaf_index(tree: CsfTree, stream=None) -> CsfTree:
+def _leaf_index_max_order() -> int:
+    import os
+
+    return min(int(os.environ.get("FT_LEAF_INDEX_MAX_ORDER", LEAF_INDEX_MAX_ORDER)), 6)
+
+
+def add_leaf_index(tree: CsfTree, stream=None, leaf_pc=None) -> CsfTree:
     """Derive the leaf-major index the row-owner kernels read (K1b, ft_tree_leaf_index):
     ``leaf_pc`` (each leaf's prefix coordinates, levels 1..N-2, for orders 3-6) and
     ``row_leaf_ptr`` (first leaf of each root slice).  Not reference fields."""
@@ -309,14 +316,14 @@ def add_leaf_index(tree: CsfTree, stream=None) -> CsfTree:
     # kernels fold the prefix product level by level, which pays at order 4 (BASELINE order-4
     # config: 362 -> 307 ms per epoch) but not at order 6 (237 -> 304 ms: five dependent gather
     # rounds per batch); higher orders keep only the row index and use the fiber-walking kernels
-    import os
-
-    max_order = int(os.environ.get("FT_LEAF_INDEX_MAX_ORDER", LEAF_INDEX_MAX_ORDER))
-    tree.leaf_pc = torch.empty((tree.nnz, N - 2), **i32) if N <= min(max_order, 6) else None
+    have = leaf_pc is not None  # already written by the build (from its sorted level columns)
+    tree.leaf_pc = leaf_pc if have else (
+        torch.empty((tree.nnz, N - 2), **i32) if 3 <= N <= _leaf_index_max_order() else None)
     tree.row_leaf_ptr = torch.empty(tree.num_rows + 1, **i32)
     tree._view = None
     v = tree.view()
-    _lib.check(_lib.lib().ft_tree_leaf_index(ctypes.byref(v), _lib.ptr(tree.leaf_pc),
+    _lib.check(_lib.lib().ft_tree_leaf_index(ctypes.byref(v),
+                                             None if have else _lib.ptr(tree.leaf_pc),
                                              tree.row_leaf_ptr.data_ptr(),
                                              _lib.stream_handle(stream)), "ft_tree_leaf_index")
     tree._view = None

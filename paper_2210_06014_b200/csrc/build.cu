@@ -357,14 +357,31 @@ __global__ void decode_derived(const uint32_t *__restrict__ keys,
   fdl[p] = (uint8_t)first;
 }
 
+struct LeafPcArgs {
+  int NP;
+  const int32_t *K[4];
+};
+__global__ void leaf_pc_from_levels(LeafPcArgs a, int64_t nnz, int32_t *__restrict__ out) {
+  const int64_t L = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (L >= nnz) return;
+  for (int d = 0; d < a.NP; ++d) out[L * a.NP + d] = __ldg(a.K[d] + L);
+}
+
 // Everything after the level columns K_d (sorted, level order) and first-differing levels are
 // known: fibers, root slices, subtensor split, fiber_coord, per-depth inds / ptrs (csf.py:126-183).
 int finish_tree(cudaStream_t s, Scratch &sc, int N, int64_t nnz, int64_t thr, bool compact,
                 int32_t *const *K, const uint8_t *fdl, int32_t *const *inds, int32_t *const *ptrs,
                 int32_t *fiber_ptr, int32_t *fiber_coord, int32_t *sub_fiber_ptr,
                 int32_t *sub_leaf_ptr, int32_t *row_fiber_ptr, int32_t *row_coord,
-                int64_t *counts_out) {
+                int64_t *counts_out, int32_t *leaf_pc) {
   const unsigned nb = blocks_for(nnz);
+  if (leaf_pc && N >= 3 && N <= 6) {  // every leaf carries its fiber's levels 1..N-2 in K_d
+    LeafPcArgs la{};
+    la.NP = N - 2;
+    for (int d = 0; d < N - 2; ++d) la.K[d] = K[d + 1];
+    leaf_pc_from_levels<<<nb, 256, 0, s>>>(la, nnz, leaf_pc);
+    if (int rc = check_launch("leaf_pc_from_levels")) return rc;
+  }
   GatherArgs ga{};
   ga.N = N;
   for (int d = 0; d < N; ++d) ga.K[d] = K[d];
@@ -469,7 +486,7 @@ extern "C" int ft_build_tree(int32_t N, int64_t nnz, const int64_t *dims, const 
                              int32_t *const *inds, int32_t *const *ptrs, int32_t *fiber_ptr,
                              int32_t *fiber_coord, int32_t *sub_fiber_ptr, int32_t *sub_leaf_ptr,
                              int32_t *row_fiber_ptr, int32_t *row_coord, int64_t *counts_out,
-                             void *stream) {
+                             int32_t *leaf_pc, void *stream) {
   if (N < 2 || N > FT_MAX_ORDER) return fail(FT_ERR_ARG, "ft_build_tree: order %d unsupported", N);
   if (nnz <= 0) return fail(FT_ERR_EMPTY, "cannot index an empty tensor");
   if (nnz >= (int64_t)INT32_MAX) return fail(FT_ERR_UNSUPPORTED, "nnz %lld >= 2^31", (long long)nnz);
@@ -608,7 +625,7 @@ extern "C" int ft_build_tree(int32_t N, int64_t nnz, const int64_t *dims, const 
   }
 
   return finish_tree(s, sc, N, nnz, thr, compact, ga.K, fdl, inds, ptrs, fiber_ptr, fiber_coord,
-                     sub_fiber_ptr, sub_leaf_ptr, row_fiber_ptr, row_coord, counts_out);
+                     sub_fiber_ptr, sub_leaf_ptr, row_fiber_ptr, row_coord, counts_out, leaf_pc);
 }
 
 extern "C" int ft_tree_leaf_index(const ft_tree_t *tree, int32_t *leaf_pc, int32_t *row_leaf_ptr,
@@ -673,7 +690,7 @@ extern "C" int ft_build_tree_derived(const ft_tree_t *prev, const int64_t *dims,
                                      int32_t *fiber_ptr, int32_t *fiber_coord,
                                      int32_t *sub_fiber_ptr, int32_t *sub_leaf_ptr,
                                      int32_t *row_fiber_ptr, int32_t *row_coord,
-                                     int64_t *counts_out, void *stream) {
+                                     int64_t *counts_out, int32_t *leaf_pc, void *stream) {
   if (!prev || !dims) return fail(FT_ERR_ARG, "ft_build_tree_derived: null argument");
   const int N = prev->order;
   const int64_t nnz = prev->nnz;
@@ -750,5 +767,5 @@ extern "C" int ft_build_tree_derived(const ft_tree_t *prev, const int64_t *dims,
   for (int k = 0; k < 4 + N; ++k) counts_out[k] = 0;
   counts_out[3] = -1;
   return finish_tree(s, sc, N, nnz, thr, compact, K, fdl, inds, ptrs, fiber_ptr, fiber_coord,
-                     sub_fiber_ptr, sub_leaf_ptr, row_fiber_ptr, row_coord, counts_out);
+                     sub_fiber_ptr, sub_leaf_ptr, row_fiber_ptr, row_coord, counts_out, leaf_pc);
 }

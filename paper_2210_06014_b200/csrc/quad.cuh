@@ -152,6 +152,22 @@ __device__ __forceinline__ void quad_store_v_pad(float *V, const float (&acc)[2]
     }
 }
 
+// packed form for a chain in quadr's column layout: slot s's columns (g, g+8, g+16, g+24) as one
+// float4 at V + s * QVS + 8 (s / 8) + 4 g (one STS.128 per slot per lane instead of four STS.32;
+// the 8 (s / 8) shift keeps both the stores and the four rows' reads conflict-free)
+__device__ __forceinline__ void quad_store_v_packed(float *V, const float (&acc)[2][4][4], int lane) {
+  using namespace quad;
+  const int gq = lane >> 2, tq = lane & 3;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int par = 0; par < 2; ++par) {
+      const int sl = 8 * nt + 2 * tq + par;
+      *reinterpret_cast<float4 *>(V + sl * QVS + 8 * nt + 4 * gq) =
+          make_float4(acc[0][nt][par], acc[0][nt][2 + par], acc[1][nt][par], acc[1][nt][2 + par]);
+    }
+}
+
 __device__ __forceinline__ void quad_zero(float (&acc)[2][4][4]) {
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
@@ -1034,7 +1050,7 @@ namespace quadw {
 constexpr int NS = 4;   // ring stages (producer k writes stages k, k+2)
 constexpr int NP = 2;   // producers per group
 // stage: V [32][QVS] | meta float4 [4][MQ] | info int4 [4] | A rows [4][32] | lr*G^T [4][8][8]
-constexpr int VREG = 32 * quad::QVS + 16;  // V (+16: the lane-per-row consumer's quarter padding)
+constexpr int VREG = 32 * quad::QVS + 32;  // V (+32: the LPR / packed consumers' row shifts)
 constexpr int STAGE_FLOATS = VREG + 4 * quad::MQ * 4 + 4 * 4 + 4 * 32 + 4 * 64;
 // ring + X, Y per producer + the consumer's row exchange [4][32]
 constexpr int GROUP_FLOATS = NS * STAGE_FLOATS + NP * 2 * quad::TILE + 4 * 32;
@@ -1045,7 +1061,7 @@ constexpr size_t bytes() {
 }
 }  // namespace quadw
 
-template <bool GRAM, bool SMALL, bool LPR = false>
+template <bool GRAM, bool SMALL, bool LPR = false, bool PV = false>
 __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(const SweepParams p) {
   using namespace quad;
   using quadp::Leaf;
@@ -1173,6 +1189,8 @@ __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(co
       if (!stop) {
         if (LPR)
           quad_store_v_pad(stage_v(st), acc, lane);
+        else if (PV)
+          quad_store_v_packed(stage_v(st), acc, lane);
         else
           quad_store_v(stage_v(st), acc, lane);
         if (GRAM) {  // lane (q, l): lr G[m][l] = lr v_m . v_l over the quarter's batch, fp32
@@ -1292,6 +1310,62 @@ __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(co
       if (ai >= 0) store_full();
       return;
     }
+    if (PV) {
+      // quadr's column layout: row rho = lane & 3 in lanes 4 g + rho, columns g, g+8, g+16, g+24;
+      // V rows come packed (one LDS.128 per step), the dot reduces over lane bits 2-4
+      const int rho = lane & 3, g = lane >> 2;
+      float a[4] = {0.f, 0.f, 0.f, 0.f};
+      int ai = -1;
+      auto store_r = [&]() {
+        float *ar = p.A + (int64_t)ai * J;
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+          if (g + 8 * m < J) ar[g + 8 * m] = a[m];
+      };
+      for (int t = 0;; ++t) {
+        const int st = t % quadw::NS;
+        mbar_wait(full + st, (t / quadw::NS) & 1);
+        const int4 info = stage_info(st)[rho];
+        if (info.w) break;
+        if (info.y) {
+          if (ai >= 0) store_r();
+          const float *ar = stage_a(st) + 32 * rho;
+#pragma unroll
+          for (int m = 0; m < 4; ++m) a[m] = ar[g + 8 * m];
+          ai = info.z;
+        }
+        const float *Vr = stage_v(st) + 8 * rho * QVS + 8 * rho + 4 * g;
+        const float4 *mq = stage_meta(st) + rho * MQ;
+        float4 vv[QB], mm[QB];
+#pragma unroll
+        for (int kk = 0; kk < QB; ++kk) {
+          vv[kk] = *reinterpret_cast<const float4 *>(Vr + kk * QVS);
+          mm[kk] = mq[kk];
+        }
+        __syncwarp();
+        mbar_arrive(empty + st);
+#pragma unroll
+        for (int kk = 0; kk < QB; ++kk) {
+          const float4 v = vv[kk], m = mm[kk];
+          float2 pr = fmul2(make_float2(a[0], a[1]), make_float2(v.x, v.y));
+          pr = ffma2(make_float2(a[2], a[3]), make_float2(v.z, v.w), pr);
+          float sv = pr.x + pr.y;
+          sv += __shfl_xor_sync(FULL, sv, 4);
+          sv += __shfl_xor_sync(FULL, sv, 8);
+          sv += __shfl_xor_sync(FULL, sv, 16);
+          const float e = m.x - sv;
+          const float lre = m.y * e;
+          const float2 a01 = ffma2(make_float2(m.z, m.w), make_float2(a[0], a[1]), make_float2(a[0], a[1]));
+          const float2 a23 = ffma2(make_float2(m.z, m.w), make_float2(a[2], a[3]), make_float2(a[2], a[3]));
+          a[0] = __fmaf_rn(lre, v.x, a01.x);
+          a[1] = __fmaf_rn(lre, v.y, a01.y);
+          a[2] = __fmaf_rn(lre, v.z, a23.x);
+          a[3] = __fmaf_rn(lre, v.w, a23.y);
+        }
+      }
+      if (ai >= 0) store_r();
+      return;
+    }
     float a[4] = {0.f, 0.f, 0.f, 0.f};
     int ai = -1;
     float *xrow = ring + quadw::NS * quadw::STAGE_FLOATS + quadw::NP * 2 * TILE + 32 * q;
@@ -1384,17 +1458,17 @@ __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(co
   }
 }
 
-template <bool GRAM, bool SMALL, bool LPR = false>
+template <bool GRAM, bool SMALL, bool LPR = false, bool PV = false>
 int launch_quadw_t(const SweepParams &q, cudaStream_t s) {
   const size_t sm = quadw::bytes();
   static bool set = false;
   if (!set) {
-    cudaFuncSetAttribute(factor_rows_quadw_kernel<GRAM, SMALL, LPR>,
+    cudaFuncSetAttribute(factor_rows_quadw_kernel<GRAM, SMALL, LPR, PV>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     set = true;
   }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quadw_kernel<GRAM, SMALL, LPR>,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quadw_kernel<GRAM, SMALL, LPR, PV>,
                                                     quadw::THREADS, sm) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
@@ -1402,7 +1476,7 @@ int launch_quadw_t(const SweepParams &q, cudaStream_t s) {
   const int64_t cap = (int64_t)sm_count() * per_sm;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
-  factor_rows_quadw_kernel<GRAM, SMALL, LPR><<<(int)g, quadw::THREADS, sm, s>>>(q);
+  factor_rows_quadw_kernel<GRAM, SMALL, LPR, PV><<<(int)g, quadw::THREADS, sm, s>>>(q);
   return check_launch("ft_factor_sweep_rows(quadw)");
 }
 
@@ -1415,6 +1489,13 @@ int launch_quadw(const SweepParams &q, cudaStream_t s) {
   if (!GRAM && lpr)
     return q.J <= 16 && q.R <= 16 ? launch_quadw_t<false, true, true>(q, s)
                                   : launch_quadw_t<false, false, true>(q, s);
+  static const bool pv = [] {  // FT_QUADW_PV=1: packed V, consumer in quadr's column layout
+    const char *e = getenv("FT_QUADW_PV");
+    return e && strcmp(e, "1") == 0;
+  }();
+  if (!GRAM && pv)
+    return q.J <= 16 && q.R <= 16 ? launch_quadw_t<false, true, false, true>(q, s)
+                                  : launch_quadw_t<false, false, false, true>(q, s);
   return q.J <= 16 && q.R <= 16 ? launch_quadw_t<GRAM, true>(q, s) : launch_quadw_t<GRAM, false>(q, s);
 }
 

@@ -373,6 +373,10 @@ def run_ours(args, cfg):
     traffic, _ = ncu_traffic(dom)
     roof = {"kernel": kname, "bound": "hbm", "achieved": achieved, "peak": peak,
             "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
+            "note": "achieved = SURVEY 8d algorithmic (logical) bytes / time; the gathered C "
+                    "rows are L1 / L2 hits, so DRAM moves only `traffic` bytes per launch and "
+                    "per-kernel fractions can exceed 1 (the sweeps are bound by the SM's L1 / "
+                    "shared-memory pipe, profiles/r01_ncu_sweeps.md)",
             "traffic": traffic,
             "bytes_per_launch": d["bytes"] / d["launches"],
             "ms_per_launch": 1e3 * d["sec"] / d["launches"],

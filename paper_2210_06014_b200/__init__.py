@@ -8,13 +8,15 @@ Names follow /root/reference/pkg/src/fastertucker/__init__.py:9-28.
 """
 
 from ._kernels import BACKEND, COMPILED, get_backend, use_backend
-from .cache import DotCache, precompute_cache, refresh_mode
+from .cache import (DotCache, count_report, counted_sweep_cost, precompute_cache,
+                    refresh_mode)
 from .coo import (DatasetSplit, DeviceCoo, SparseCooTensor, generate_device,
                   generate_low_rank_device, generate_synthetic, load_coo, split_dataset,
                   write_coo)
 from .counter import CHANNELS, OpCounter
 from .csf import CsfForest, CsfTree, build_forest, build_tree
-from .errors import (BackendUnavailableError, BuildError, ConfigError, DivergenceError,
+from .errors import (BackendUnavailableError, BuildError, ConfigError, CountMismatchError,
+                     DivergenceError,
                      FasterTuckerError, ValidationError)
 from .model import (InitSpec, Model, default_init_model, init_model, load_model, predict_batch,
                     save_model)
@@ -25,6 +27,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "BACKEND", "COMPILED", "CHANNELS", "BackendUnavailableError", "BuildError", "ConfigError",
+    "CountMismatchError", "count_report", "counted_sweep_cost",
     "CsfForest", "CsfTree", "DatasetSplit", "DeviceCoo", "DivergenceError", "DotCache",
     "EpochMetrics", "FasterTuckerError", "InitSpec", "METRICS_CSV_HEADER", "Model", "OpCounter",
     "SparseCooTensor", "TrainConfig", "ValidationError", "build_forest", "build_tree",

@@ -84,3 +84,39 @@ def test_uncached_plan_matches_cached(ft, golden_cases):
     f, c = model_arrays(z, "plan_eq/final/", 3)
     for n in range(3):
         assert_rel(outs[1].factors[n].cpu().numpy(), f[n], 1e-4, f"uncached A{n}")
+
+
+def test_counted_sweep_cost_formulas(ft):
+    """test_intermediates.py:109-120 on the device sweeps."""
+    dims, ranks, R = (20, 25, 30), (3, 4, 5), 3
+    t = ft.generate_synthetic(dims, 700, seed=4)
+    m = ft.default_init_model(dims, ranks, R, seed=4)
+    sum_jr = sum(j * R for j in ranks)
+    want_uncached = (t.order - 1) * t.nnz * sum_jr
+    want_cached = sum(d * j * R for d, j in zip(dims, ranks))
+    assert ft.counted_sweep_cost("uncached", t, m) == want_uncached
+    assert ft.counted_sweep_cost("cached", t, m) == want_cached
+    assert want_cached < want_uncached
+
+
+def test_counted_sweep_cost_leaves_model_untouched(ft):
+    """test_intermediates.py:123-129: the zero-lr passes change no parameter bit."""
+    t = ft.generate_synthetic((10, 10, 10), 200, seed=6)
+    m = ft.default_init_model(t.dims, (2, 2, 2), 2, seed=6)
+    before = [a.clone() for a in m.factors + m.cores_t]
+    ft.counted_sweep_cost("uncached", t, m)
+    ft.counted_sweep_cost("cached", t, m)
+    for a, b in zip(before, m.factors + m.cores_t):
+        assert np.array_equal(a.cpu().numpy().view(np.uint32), b.cpu().numpy().view(np.uint32))
+
+
+@pytest.mark.parametrize("dims,ranks,R,nnz", [((40, 30, 20), (4, 4, 4), 4, 3000),
+                                              ((12, 10, 9, 8), (3, 2, 4, 2), 3, 1500)])
+def test_count_report_closed_forms(ft, dims, ranks, R, nnz):
+    """The `count` command's checks (cli.py:234-289) all report ok."""
+    t = ft.generate_synthetic(dims, nnz, seed=2)
+    m = ft.default_init_model(dims, ranks, R, seed=2)
+    lines = ft.count_report(t, m, fiber_threshold=8)
+    assert len(lines) == 3 + len(dims) + 1
+    assert all(l.endswith("ok") for l in lines[:-1]), lines
+    assert lines[-1].startswith("uncached/cached dot-cost ratio:")

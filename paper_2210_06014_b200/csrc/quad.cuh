@@ -1586,7 +1586,7 @@ constexpr size_t bytes() { return (size_t)WPB * WARP_FLOATS * 4; }
 #ifndef CORE_FUSED
 #define CORE_FUSED 1  // K4 quad: fused single pass in the quarter layout (0: lane-per-slot s-pass)
 #endif
-template <bool SSE, int NPRE>
+template <bool SSE, int NPRE, bool DIRECT = false>
 __global__ void __launch_bounds__(cquad::WPB * 32, 2) core_rows_quad_kernel(const SweepParams p) {
   using namespace cquad;
   extern __shared__ float4 smem4[];
@@ -1700,6 +1700,67 @@ __global__ void __launch_bounds__(cquad::WPB * 32, 2) core_rows_quad_kernel(cons
       for (int d = 0; d < NPRE; ++d)
         ppc[d] = ok ? __ldcs(p.leaf_pc + (int64_t)(pos + l) * NPRE + d) : 0;
       px = ok ? __ldcs(p.vals + pos + l) : 0.f;
+    }
+    if (DIRECT) {
+      // the fused pass with no staging: the K4 core has no MMA, so each lane loads the 16-B
+      // chunks it consumes (columns 4l..4l+3 of its quarter's leaves) straight into registers --
+      // no shared-memory write or read per leaf on an L1-bound kernel.  Four leaves in flight
+      // per half-batch; padding leaves load nothing.  Arithmetic as in the staged pass.
+      const bool lok = 4 * l < R;
+      const int64_t Rs = R;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float4 xv[4], yv[4];
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const int k = 4 * h + kk, sl = 8 * q + k;
+          const int cy = __shfl_sync(FULL, lc, sl);
+          int cx[NPRE];
+#pragma unroll
+          for (int d = 0; d < NPRE; ++d) cx[d] = __shfl_sync(FULL, pc[d], sl);
+          const bool ok = lok && k < nb;
+          xv[kk] = yv[kk] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (ok) {
+            float4 lv[NPRE];
+#pragma unroll
+            for (int d = 0; d < NPRE; ++d)
+              lv[d] = __ldg(reinterpret_cast<const float4 *>(p.Cpre[d] + cx[d] * Rs + 4 * l));
+            yv[kk] = __ldg(reinterpret_cast<const float4 *>(p.Cleaf + cy * Rs + 4 * l));
+            xv[kk] = lv[0];
+#pragma unroll
+            for (int d = 1; d < NPRE; ++d) {  // the prefix chain left to right (quad_gather's fold)
+              const float2 a = fmul2(make_float2(xv[kk].x, xv[kk].y), make_float2(lv[d].x, lv[d].y));
+              const float2 b = fmul2(make_float2(xv[kk].z, xv[kk].w), make_float2(lv[d].z, lv[d].w));
+              xv[kk] = make_float4(a.x, a.y, b.x, b.y);
+            }
+          }
+        }
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const int k = 4 * h + kk;
+          const float2 c01 = fmul2(make_float2(xv[kk].x, xv[kk].y), make_float2(yv[kk].x, yv[kk].y));
+          const float2 c23 = fmul2(make_float2(xv[kk].z, xv[kk].w), make_float2(yv[kk].z, yv[kk].w));
+          const float2 sp = ffma2(c23, cu23, fmul2(c01, cu01));
+          float sv = sp.x + sp.y;
+          sv += __shfl_xor_sync(FULL, sv, 1);
+          sv += __shfl_xor_sync(FULL, sv, 2);
+          sv += __shfl_xor_sync(FULL, sv, 4);
+          const float xk = __shfl_sync(FULL, x, 8 * q + k);
+          const float e = k < nb ? xk - sv : 0.f;
+          if (SSE) {
+            if (l == 0) {
+              sse += (double)e * (double)e;
+              sae += fabs((double)e);
+            }
+          } else {
+            const float2 e2 = make_float2(e, e);
+            g01 = ffma2(e2, c01, g01);
+            g23 = ffma2(e2, c23, g23);
+          }
+        }
+      }
+      cL0 += nb;
+      continue;
     }
     quad_gather<NPRE, XS>(p, X, Y, pc, lc, lane);
     if (CORE_FUSED) {
@@ -1827,6 +1888,8 @@ int core_quad_grid_t(const SweepParams &p) {
   if (!set) {
     cudaFuncSetAttribute(core_rows_quad_kernel<SSE, NPRE>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(core_rows_quad_kernel<SSE, NPRE, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     set = true;
   }
   int per_sm = 0;
@@ -1853,11 +1916,23 @@ int core_quad_grid(const SweepParams &p) {
 
 template <bool SSE>
 int launch_core_quad_t(const SweepParams &p, int g, cudaStream_t s) {
+  static const bool direct = [] {  // FT_CORE_DIRECT=0: the shared-memory staged pass
+    const char *e = getenv("FT_CORE_DIRECT");
+    return !(e && e[0] == '0');
+  }();
+  const dim3 b(cquad::WPB * 32);
+  const size_t sm = cquad::bytes();
   switch (p.N) {
-    case 3: core_rows_quad_kernel<SSE, 1><<<g, cquad::WPB * 32, cquad::bytes(), s>>>(p); break;
-    case 4: core_rows_quad_kernel<SSE, 2><<<g, cquad::WPB * 32, cquad::bytes(), s>>>(p); break;
-    case 5: core_rows_quad_kernel<SSE, 3><<<g, cquad::WPB * 32, cquad::bytes(), s>>>(p); break;
-    default: core_rows_quad_kernel<SSE, 4><<<g, cquad::WPB * 32, cquad::bytes(), s>>>(p); break;
+    case 3:
+      if (direct) core_rows_quad_kernel<SSE, 1, true><<<g, b, sm, s>>>(p);
+      else core_rows_quad_kernel<SSE, 1><<<g, b, sm, s>>>(p);
+      break;
+    case 4:
+      if (direct) core_rows_quad_kernel<SSE, 2, true><<<g, b, sm, s>>>(p);
+      else core_rows_quad_kernel<SSE, 2><<<g, b, sm, s>>>(p);
+      break;
+    case 5: core_rows_quad_kernel<SSE, 3><<<g, b, sm, s>>>(p); break;
+    default: core_rows_quad_kernel<SSE, 4><<<g, b, sm, s>>>(p); break;
   }
   return check_launch(SSE ? "ft_sse_tree" : "ft_core_sweep_rows(quad)");
 }

@@ -27,7 +27,7 @@ from .errors import BuildError, ConfigError
 
 DEFAULT_FIBER_THRESHOLD = 128
 CORE_SEGMENT = 512  # max leaves per core-sweep row segment
-LEAF_INDEX_MAX_ORDER = 4  # orders with the per-leaf prefix coordinates (the quad kernels)
+LEAF_INDEX_MAX_ORDER = 6  # orders with the per-leaf prefix coordinates (the quad kernels)
 
 
 @dataclass
@@ -312,10 +312,10 @@ def add_leaf_index(tree: CsfTree, stream=None, leaf_pc=None) -> CsfTree:
 
     i32 = dict(dtype=torch.int32, device=tree.vals.device)
     N = tree.order
-    # prefix levels per leaf (4 (N-2) bytes per leaf) up to LEAF_INDEX_MAX_ORDER: the quad
-    # kernels fold the prefix product level by level, which pays at order 4 (BASELINE order-4
-    # config: 362 -> 307 ms per epoch) but not at order 6 (237 -> 304 ms: five dependent gather
-    # rounds per batch); higher orders keep only the row index and use the fiber-walking kernels
+    # prefix levels per leaf (4 (N-2) bytes per leaf) up to LEAF_INDEX_MAX_ORDER.  The K4 core
+    # (direct register loads) uses them at every order (order-6 10K^6: 15.2 -> 8.3 ms per
+    # mode); the factor sweep's quad fold pays at orders 3-4 only (order 6: 30.6 vs 24.2 ms
+    # dual), so orders 5-6 keep the fiber-walking factor kernels (sweep.cu auto dispatch)
     have = leaf_pc is not None  # already written by the build (from its sorted level columns)
     tree.leaf_pc = leaf_pc if have else (
         torch.empty((tree.nnz, N - 2), **i32) if 3 <= N <= _leaf_index_max_order() else None)

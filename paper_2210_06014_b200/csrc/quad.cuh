@@ -1708,12 +1708,13 @@ __global__ void __launch_bounds__(cquad::WPB * 32, 2) core_rows_quad_kernel(cons
       // per half-batch; padding leaves load nothing.  Arithmetic as in the staged pass.
       const bool lok = 4 * l < R;
       const int64_t Rs = R;
+      constexpr int LH = NPRE <= 2 ? 4 : 2;  // leaves in flight per lane (register budget)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        float4 xv[4], yv[4];
+      for (int h = 0; h < 8 / LH; ++h) {
+        float4 xv[LH], yv[LH];
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const int k = 4 * h + kk, sl = 8 * q + k;
+        for (int kk = 0; kk < LH; ++kk) {
+          const int k = LH * h + kk, sl = 8 * q + k;
           const int cy = __shfl_sync(FULL, lc, sl);
           int cx[NPRE];
 #pragma unroll
@@ -1736,8 +1737,8 @@ __global__ void __launch_bounds__(cquad::WPB * 32, 2) core_rows_quad_kernel(cons
           }
         }
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const int k = 4 * h + kk;
+        for (int kk = 0; kk < LH; ++kk) {
+          const int k = LH * h + kk;
           const float2 c01 = fmul2(make_float2(xv[kk].x, xv[kk].y), make_float2(yv[kk].x, yv[kk].y));
           const float2 c23 = fmul2(make_float2(xv[kk].z, xv[kk].w), make_float2(yv[kk].z, yv[kk].w));
           const float2 sp = ffma2(c23, cu23, fmul2(c01, cu01));
@@ -1916,10 +1917,16 @@ int core_quad_grid(const SweepParams &p) {
 
 template <bool SSE>
 int launch_core_quad_t(const SweepParams &p, int g, cudaStream_t s) {
-  static const bool direct = [] {  // FT_CORE_DIRECT=0: the shared-memory staged pass
+  // direct register loads keep 4 leaves in flight per lane, the staged pass 32 rows per warp:
+  // direct wins while the gathered C matrices sit in L2 (Netflix32 61 MB: core 2.41 -> 2.20 ms
+  // per mode; order-4 10K^4 19.9 -> 12.7 ms), staging wins once their misses go to HBM
+  // (Yahoo32 mode 2, 208 MB: 8.1 vs 9.3 ms; modes 0 / 1, 80 MB: 6.5 vs 6.8 ms).
+  // FT_CORE_DIRECT=0 / 1 forces either.
+  static const int direct_env = [] {
     const char *e = getenv("FT_CORE_DIRECT");
-    return !(e && e[0] == '0');
+    return e && e[0] ? (e[0] == '0' ? 0 : 1) : -1;
   }();
+  const bool direct = direct_env >= 0 ? direct_env == 1 : p.gather_bytes <= (64ll << 20);
   const dim3 b(cquad::WPB * 32);
   const size_t sm = cquad::bytes();
   switch (p.N) {
@@ -1931,8 +1938,14 @@ int launch_core_quad_t(const SweepParams &p, int g, cudaStream_t s) {
       if (direct) core_rows_quad_kernel<SSE, 2, true><<<g, b, sm, s>>>(p);
       else core_rows_quad_kernel<SSE, 2><<<g, b, sm, s>>>(p);
       break;
-    case 5: core_rows_quad_kernel<SSE, 3><<<g, b, sm, s>>>(p); break;
-    default: core_rows_quad_kernel<SSE, 4><<<g, b, sm, s>>>(p); break;
+    case 5:
+      if (direct) core_rows_quad_kernel<SSE, 3, true><<<g, b, sm, s>>>(p);
+      else core_rows_quad_kernel<SSE, 3><<<g, b, sm, s>>>(p);
+      break;
+    default:
+      if (direct) core_rows_quad_kernel<SSE, 4, true><<<g, b, sm, s>>>(p);
+      else core_rows_quad_kernel<SSE, 4><<<g, b, sm, s>>>(p);
+      break;
   }
   return check_launch(SSE ? "ft_sse_tree" : "ft_core_sweep_rows(quad)");
 }

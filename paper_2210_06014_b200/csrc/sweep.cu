@@ -63,6 +63,7 @@ struct SweepParams {
   float lr, reg;
   float *partials;   // core: [grid][R*J]
   int tma;           // dual kernel: gather with TMA bulk copies (FT_GATHER=tma)
+  int64_t gather_bytes;  // bytes of the gathered C matrices (modes other than u)
 };
 
 // Fiber index of each of the batch's leaves (lane k -> leaf L0+k), given fcur = fiber holding
@@ -1954,8 +1955,11 @@ int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
   if (variant == 5) {
     // many rows: quadr / quad (orders 3-6); few long rows: quadw (order 3, warp-specialised)
     const bool many = p.nrows >= (int64_t)2 * sm_count() * quad::WPB * 4;
-    if (quad_ok(p) && many)
-      variant = p.N <= 4 ? 12 : 8;  // quadr (V consumed from the MMA registers), orders 3-4
+    // quadr (V consumed from the MMA registers) at orders 3-4; orders 5-6 keep the fiber
+    // kernels (the quad fold's N-2 dependent gather rounds per batch: order-6 10K^6 24.2 ms
+    // dual vs 30.6 ms quad per mode) even though their trees carry the leaf index for K4
+    if (quad_ok(p) && many && p.N <= 4)
+      variant = 12;
     else if (quad_ok(p) && p.N == 3)
       variant = 10;
     else
@@ -2051,6 +2055,9 @@ int fill_rows_params(SweepParams &p, const ft_tree_t *tree, const ft_model_t *m)
   p.Cleaf = m->dots[(u + N - 1) % N];
   p.J = m->ranks[u];
   p.R = m->core_rank;
+  p.gather_bytes = 0;
+  for (int d = 0; d < N; ++d)
+    if (d != u) p.gather_bytes += (int64_t)m->dims[d] * m->core_rank * 4;
   if (p.J < 1 || p.J > FT_MAX_RANK || p.R < 1 || p.R > FT_MAX_RANK)
     return fail(FT_ERR_UNSUPPORTED, "ranks J=%d R=%d outside kernel cover (<= %d)", p.J, p.R,
                 FT_MAX_RANK);

@@ -59,6 +59,10 @@ __device__ __forceinline__ void cp_async16_s(uint32_t dst, const float *src) {
 // Bt_u^T as the A operand of the transposed combine: for (mt, kt, lane g t) the quad
 // a0 = Bt[r][j], a1 = Bt[r][j+8], a2 = Bt[r+1][j], a3 = Bt[r+1][j+8], r = 8kt + 2t, j = 16mt + g
 // (paired k order), as a hi quad and a lo quad (3xTF32 split).
+// RL > 0 (quadr DIRECT): the k order r = RL t + 2 kt (+1), so that lane t's B values over all
+// k-tiles are the RL consecutive columns RL t .. RL t + RL - 1 of its slots' rows (RL = 8 for
+// R <= 32, 4 for the two-k-tile SMALL form) -- one or two LDG.128 per operand and slot.
+template <int RL = 0>
 __device__ __forceinline__ void quad_afrag_init(const SweepParams &p, uint4 *afr) {
   using namespace quad;
   for (int f = threadIdx.x; f < KT * MT * 32; f += blockDim.x) {
@@ -67,7 +71,11 @@ __device__ __forceinline__ void quad_afrag_init(const SweepParams &p, uint4 *afr
     uint32_t hv[4], lv[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const int r = 8 * kt + 2 * t + (e >> 1), j = 16 * mt + g + 8 * (e & 1);
+      const int r = (RL ? RL * t + 2 * kt : 8 * kt + 2 * t) + (e >> 1), j = 16 * mt + g + 8 * (e & 1);
+      if (RL && 2 * kt >= RL) {  // k-tiles past the SMALL form's two: unused
+        hv[e] = lv[e] = 0u;
+        continue;
+      }
       const float bv = (r < p.R && j < p.J) ? __ldg(p.Bt + r * p.J + j) : 0.f;
       hv[e] = to_tf32(bv);
       lv[e] = to_tf32(bv - __uint_as_float(hv[e]));
@@ -414,7 +422,74 @@ __global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quad_kernel(const Sw
 #ifndef QUADR_FULL8
 #define QUADR_FULL8 1  // always run 8 chain steps (padding steps are no-ops): no break, loads hoist
 #endif
-template <bool SMALL, int NPRE, int WPBT, bool TMA = false>
+// quadr DIRECT: the transposed combine fed straight from global memory.  Lane (g, t) loads,
+// for each n-tile nt (slot 8 nt + g: row (g >> 1) & 3, leaf 2 nt + (g & 1)), the RL columns
+// RL t .. RL t + RL - 1 of the slot's prefix row(s) and leaf row (LDG.128 through L1; the
+// C matrices are read-only during the sweep), forms cross = X * Y in registers (the prefix
+// chain left to right, as quad_gather) and runs the 3xTF32 MMAs with the RL-permuted k order
+// (quad_afrag_init<RL>) -- no cp.async write, no LDS per fragment.  Padding slots load nothing
+// (cross = 0: their V is 0 and their chain steps are no-ops).
+template <bool SMALL, int NPRE>
+__device__ __forceinline__ void quadr_direct_combine(const SweepParams &p, const int (&pc)[NPRE],
+                                                     int lc, int nb, int lane, const uint4 *afr,
+                                                     float (&acc)[2][4][4]) {
+  using namespace quad;
+  constexpr int RL = SMALL ? 4 : 8, NC = RL / 4, nkt = SMALL ? 2 : 4, mts = SMALL ? 1 : 2;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int r2 = (gq >> 1) & 3;
+  const int rnb = __shfl_sync(FULL, nb, r2);  // chain layout: lane rho holds row rho's nb
+  const int64_t Rs = p.R;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const int sl = 8 * nt + gq;
+    // slot-layout lane sl holds slot sl's coordinates
+    const int cy = __shfl_sync(FULL, lc, sl);
+    int cx[NPRE];
+#pragma unroll
+    for (int d = 0; d < NPRE; ++d) cx[d] = __shfl_sync(FULL, pc[d], sl);
+    const bool ok = 2 * nt + (gq & 1) < rnb;
+    float c[RL];
+#pragma unroll
+    for (int h = 0; h < NC; ++h) {
+      const int r0 = RL * tq + 4 * h;
+      float4 xv = make_float4(0.f, 0.f, 0.f, 0.f), yv = xv;
+      if (ok && r0 < p.R) {
+        float4 lv[NPRE];
+#pragma unroll
+        for (int d = 0; d < NPRE; ++d)
+          lv[d] = __ldg(reinterpret_cast<const float4 *>(p.Cpre[d] + cx[d] * Rs + r0));
+        yv = __ldg(reinterpret_cast<const float4 *>(p.Cleaf + cy * Rs + r0));
+        xv = lv[0];
+#pragma unroll
+        for (int d = 1; d < NPRE; ++d) {
+          const float2 a = fmul2(make_float2(xv.x, xv.y), make_float2(lv[d].x, lv[d].y));
+          const float2 b = fmul2(make_float2(xv.z, xv.w), make_float2(lv[d].z, lv[d].w));
+          xv = make_float4(a.x, a.y, b.x, b.y);
+        }
+      }
+      const float2 a = fmul2(make_float2(xv.x, xv.y), make_float2(yv.x, yv.y));
+      const float2 b = fmul2(make_float2(xv.z, xv.w), make_float2(yv.z, yv.w));
+      c[4 * h] = a.x, c[4 * h + 1] = a.y, c[4 * h + 2] = b.x, c[4 * h + 3] = b.y;
+    }
+#pragma unroll
+    for (int kt = 0; kt < nkt; ++kt) {
+      const float c0 = c[2 * kt], c1 = c[2 * kt + 1];
+      const uint32_t bh0 = __float_as_uint(c0), bh1 = __float_as_uint(c1);
+      const uint32_t bl0 = __float_as_uint(c0 - __uint_as_float(to_tf32(c0)));
+      const uint32_t bl1 = __float_as_uint(c1 - __uint_as_float(to_tf32(c1)));
+#pragma unroll
+      for (int mt = 0; mt < mts; ++mt) {
+        const uint4 ah = afr[(mt * KT + kt) * 32 + lane];
+        const uint4 al = afr[KT * MT * 32 + (mt * KT + kt) * 32 + lane];
+        mma_tf32(acc[mt][nt], al.x, al.y, al.z, al.w, bh0, bh1);
+        mma_tf32(acc[mt][nt], ah.x, ah.y, ah.z, ah.w, bl0, bl1);
+        mma_tf32(acc[mt][nt], ah.x, ah.y, ah.z, ah.w, bh0, bh1);
+      }
+    }
+  }
+}
+
+template <bool SMALL, int NPRE, int WPBT, bool TMA = false, bool DIRECT = false>
 __global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quadr_kernel(const SweepParams p) {
   using namespace quad;
   extern __shared__ float4 smem4[];
@@ -433,7 +508,7 @@ __global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quadr_kernel(const S
                                                WPBT * quad::WARP_FLOATS) + w;
   uint32_t tphase = 0;
   if (TMA && lane == 0) mbar_init(bar, 1);
-  quad_afrag_init(p, afr);
+  quad_afrag_init<DIRECT ? (SMALL ? 4 : 8) : 0>(p, afr);
   __syncthreads();
   constexpr int mts = SMALL ? 1 : 2, nkt = SMALL ? 2 : 4;
 
@@ -523,6 +598,11 @@ __global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quadr_kernel(const S
         ppc[d] = ok ? __ldcs(p.leaf_pc + (int64_t)(pos + sk) * NPRE + d) : 0;
       px = ok ? __ldcs(p.vals + pos + sk) : 0.f;
     }
+    float acc[2][4][4];
+    quad_zero(acc);
+    if (DIRECT) {
+      quadr_direct_combine<SMALL, NPRE>(p, pc, lc, nb, lane, afr, acc);
+    } else {
     if (TMA) {  // NPRE == 1 (order 3): lane = slot
       const uint32_t rb = (uint32_t)p.R * 4;
       fence_proxy_async();  // the previous batch's generic reads of X / Y precede the async writes
@@ -537,12 +617,11 @@ __global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quadr_kernel(const S
     } else {
       quad_gather<NPRE, XS>(p, X, Y, pc, lc, lane);
     }
-    float acc[2][4][4];
-    quad_zero(acc);
 #pragma unroll
     for (int kt = 0; kt < KT; ++kt) {
       if (kt >= nkt) break;
       quad_mma_kt<NT>(X, Y, afr, kt, 0, lane, acc, mts);
+    }
     }
     __syncwarp();  // meta visible (its stores precede the gathers' waits)
     // ---- four serial chains on the accumulator registers ----
@@ -575,17 +654,17 @@ __global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quadr_kernel(const S
   }
 }
 
-template <bool SMALL, int NPRE, int WPBT, bool TMA = false>
+template <bool SMALL, int NPRE, int WPBT, bool TMA = false, bool DIRECT = false>
 int launch_quadr_t(const SweepParams &q, cudaStream_t s) {
   const size_t sm = (size_t)quad::BFRAG_U4 * 16 + (size_t)WPBT * quad::WARP_FLOATS * 4 + WPBT * 8;
   static bool set = false;
   if (!set) {
-    cudaFuncSetAttribute(factor_rows_quadr_kernel<SMALL, NPRE, WPBT, TMA>,
+    cudaFuncSetAttribute(factor_rows_quadr_kernel<SMALL, NPRE, WPBT, TMA, DIRECT>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     set = true;
   }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quadr_kernel<SMALL, NPRE, WPBT, TMA>,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quadr_kernel<SMALL, NPRE, WPBT, TMA, DIRECT>,
                                                     WPBT * 32, sm) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
@@ -593,7 +672,7 @@ int launch_quadr_t(const SweepParams &q, cudaStream_t s) {
   const int64_t cap = (int64_t)sm_count() * per_sm;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
-  factor_rows_quadr_kernel<SMALL, NPRE, WPBT, TMA><<<(int)g, WPBT * 32, sm, s>>>(q);
+  factor_rows_quadr_kernel<SMALL, NPRE, WPBT, TMA, DIRECT><<<(int)g, WPBT * 32, sm, s>>>(q);
   return check_launch("ft_factor_sweep_rows(quadr)");
 }
 
@@ -605,6 +684,31 @@ int launch_quadr(const SweepParams &q, cudaStream_t s) {
   // 9 warps per block when that fits all rows in one wave (see launch_quad)
   const int64_t slots8 = (int64_t)sm_count() * 2 * quad::WPB * 4, slots9 = slots8 * 9 / 8;
   const bool w9 = q.nrows > slots8 && q.nrows <= slots9;
+  static const int direct_env = [] {  // FT_QUADR_DIRECT=0 / 1 forces staged / direct
+    const char *e = getenv("FT_QUADR_DIRECT");
+    return e && e[0] ? (e[0] == '0' ? 0 : 1) : -1;
+  }();
+  const bool direct = direct_env != 0;
+  // direct, R > 16: 8 warps per block (128 registers, a 16-B spill) at order 3; at order 4
+  // (two prefix rows per slot) 6 warps at 162-168 registers, no spill (order-4 10K^4:
+  // 33.0 -> 28.7 ms per mode; Netflix32 order 3 at 6 warps: mode 1 4.30 -> 4.61 ms)
+  static const int dwpb_env = [] {
+    const char *e = getenv("FT_QUADR_WPB");
+    return e && e[0] ? atoi(e) : 0;
+  }();
+  const int dwpb = dwpb_env ? dwpb_env : (q.N == 4 ? 6 : 8);
+  if (direct) {
+    if (small) {
+      if (q.N == 4) return launch_quadr_t<true, 2, quad::WPB, false, true>(q, s);
+      return launch_quadr_t<true, 1, quad::WPB, false, true>(q, s);
+    }
+    if (dwpb == 6) {
+      if (q.N == 4) return launch_quadr_t<false, 2, 6, false, true>(q, s);
+      return launch_quadr_t<false, 1, 6, false, true>(q, s);
+    }
+    if (q.N == 4) return launch_quadr_t<false, 2, quad::WPB, false, true>(q, s);
+    return launch_quadr_t<false, 1, quad::WPB, false, true>(q, s);
+  }
   if (q.N == 4) {
     if (w9) return small ? launch_quadr_t<true, 2, 9>(q, s) : launch_quadr_t<false, 2, 9>(q, s);
     return small ? launch_quadr_t<true, 2, quad::WPB>(q, s) : launch_quadr_t<false, 2, quad::WPB>(q, s);

@@ -100,11 +100,16 @@ print('ok')
     ((60000, 64, 64), 200_000, 32, 32, 5e-3),     # more rows than row slots (row switching)
     ((4000, 300, 50), 500_000, 16, 12, 2e-3),     # J <= 16 (one m-tile), R = 12 (two k-tiles)
 ])
-@pytest.mark.parametrize("kernel", ["quad", "quadr", "quadrp", "quadp", "quadw", "quadg"])
+@pytest.mark.parametrize("kernel", ["quad", "quadr", "quadr-staged", "quadrp", "quadp", "quadw",
+                                    "quadg"])
 def test_quad_sweeps_match_oracle(kernel, dims, nnz, J, R, lr):
+    """quadr runs its direct-load combine by default; quadr-staged is the cp.async-staged form
+    (FT_QUADR_DIRECT=0) with the staged K4 core (FT_CORE_DIRECT=0)."""
     code = _CASE.format(dims=dims, nnz=nnz, J=J, R=R, lr=lr, seed=7)
-    env = dict(os.environ, FT_FACTOR_KERNEL=kernel, FT_QUAD_J16="1",
+    env = dict(os.environ, FT_FACTOR_KERNEL=kernel.split("-")[0], FT_QUAD_J16="1",
                FT_CORE_KERNEL="quadp" if kernel == "quadw" else "quad")
+    if kernel.endswith("-staged"):
+        env.update(FT_QUADR_DIRECT="0", FT_CORE_DIRECT="0")
     out = subprocess.run([sys.executable, "-c", code], cwd=REPO, env=env, capture_output=True,
                          text=True, timeout=900)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]

@@ -258,14 +258,151 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(name):
-    """dram bytes per launch of kernel `name` from the committed ncu summary, if any."""
-    p = os.path.join(REPO, "profiles", "ncu_summary.json")
+# ------------------------------------------------------------------------------------------
+# the memory hierarchy as the sweeps see it: measured on-chip peaks + live per-launch traffic
+# ------------------------------------------------------------------------------------------
+
+
+def onchip_peaks():
+    """L2 -> SM, L1-hit and shared-memory read bandwidth of this GPU (tools/peaks.cu, best of
+    5 CUDA-event timed launches each).  The HBM peak is MEASURED_PEAKS.json's."""
+    import ctypes
+
+    path = os.path.join(REPO, "tools", "libft_peaks.so")
+    if not os.path.exists(path):
+        subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-shared",
+                        "-Xcompiler", "-fPIC", "-o", path, os.path.join(REPO, "tools", "peaks.cu")],
+                       capture_output=True)
+    out = {}
     try:
-        d = json.load(open(p))
-        return d["kernels"][name]["dram_bytes_per_launch"], d["kernels"][name].get("launch")
-    except Exception:
-        return None, None
+        L = ctypes.CDLL(path)
+        for name in ("l2", "l1", "smem"):
+            v = ctypes.c_double(0.0)
+            if getattr(L, f"ftp_{name}_read_gbs")(5, ctypes.byref(v)) == 0:
+                out[name] = v.value
+    except OSError as exc:
+        out["error"] = str(exc)
+    return out
+
+
+# per launch, summed over the sweep launches of one epoch; one ncu pass group, kernel replay
+NCU_METRICS = ("gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+               "lts__t_bytes.sum", "l1tex__t_bytes.sum",
+               "l1tex__data_pipe_lsu_wavefronts.sum",
+               "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+               "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+               "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+               "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
+               "sm__inst_executed.avg.per_cycle_elapsed",
+               "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_elapsed")
+
+
+def live_traffic(args, N, timeout=420):
+    """Run ncu on THIS config: a child bench process (same workload, `--ncu-child`) does one
+    untimed epoch then one profiled epoch; ncu records the 2N sweep launches of the second.
+    Returns [{kernel, metrics...}] in launch order (factor t = 0..N-1, core t = 0..N-1), or
+    {"error": ...}.  Per-launch byte counts do not depend on timing, so they are combined with
+    this run's own CUDA-event launch times."""
+    import csv
+    import io
+    import shutil
+
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return {"error": "ncu not found"}
+    logf = os.path.join(REPO, "gpurun_out", f"ncu_traffic_{os.getpid()}.csv")
+    os.makedirs(os.path.dirname(logf), exist_ok=True)
+    cmd = [ncu, "--metrics", ",".join(NCU_METRICS), "--clock-control", "none",
+           "-k", "regex:factor_rows|core_rows", "--launch-skip", str(2 * N),
+           "--launch-count", str(2 * N), "--csv", "--page", "raw", "--print-units", "base",
+           "--log-file", logf, sys.executable, os.path.join(REPO, "bench.py"), "--config",
+           args.config, "--schedule", args.schedule, "--ncu-child"]
+    t0 = time.perf_counter()
+    try:
+        proc = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
+    except subprocess.TimeoutExpired:
+        return {"error": f"ncu timed out after {timeout} s"}
+    try:
+        rows = list(csv.reader(io.StringIO(open(logf).read())))
+    except OSError:
+        return {"error": f"ncu produced no log (rc {proc.returncode}): {proc.stderr[-300:]}"}
+    hi = next((i for i, r in enumerate(rows) if "Kernel Name" in r), None)
+    if hi is None:
+        return {"error": f"ncu log without a header (rc {proc.returncode})"}
+    h = rows[hi]
+    out = []
+    for r in rows[hi + 1:]:
+        if len(r) != len(h) or not r[h.index("ID")].strip().isdigit():
+            continue
+        d = {"kernel": r[h.index("Kernel Name")].split("(")[0].split("<")[0].split("::")[-1]}
+        for m in NCU_METRICS:
+            try:
+                d[m] = float(r[h.index(m)].replace(",", ""))
+            except (ValueError, IndexError):
+                d[m] = None
+        out.append(d)
+    if len(out) != 2 * N:
+        return {"error": f"ncu recorded {len(out)} sweep launches, expected {2 * N}"}
+    return {"launches": out, "seconds": time.perf_counter() - t0}
+
+
+def ncu_child(args, cfg):
+    """The process live_traffic profiles: the bench workload, one untimed + one profiled epoch."""
+    import torch
+
+    import paper_2210_06014_b200 as ft
+
+    dims, J, R = cfg["dims"], cfg["J"], cfg["R"]
+    N = len(dims)
+    nnz_total = cfg["nnz_train"] + cfg["nnz_test"]
+    split = ft.generate_synthetic(dims, nnz_total, cfg["value_range"], seed=0,
+                                  test_fraction=cfg["nnz_test"] / nnz_total)
+    forest = ft.build_forest(split.train, 128, compact=True)
+    model = ft.default_init_model(dims, (J,) * N, R, seed=0)
+    cache = ft.precompute_cache(model)
+    tcfg = ft.TrainConfig(epochs=1, schedule=args.schedule)
+    for _ in range(2):
+        for n in range(N):
+            ft.update_factor_mode(model, forest, cache, n, tcfg)
+        for n in range(N):
+            ft.update_core_mode(model, forest, cache, n, tcfg)
+    torch.cuda.synchronize()
+
+
+def hierarchy_roofline(name, launches, secs, peaks):
+    """Per memory level, measured bytes of the given ncu launches over their live CUDA-event
+    time: DRAM (read + write) vs the HBM peak, L2 (lts__t_bytes) vs the L2 peak, the L1 / shared
+    data pipe (LSU wavefronts x 128 B, the pipe's width per cycle) vs the shared-memory peak.
+    bound = the level with the largest fraction."""
+    n = len(launches)
+
+    def tot(m):
+        return sum(x[m] or 0.0 for x in launches)
+
+    lv = {
+        "hbm": (tot("dram__bytes_read.sum") + tot("dram__bytes_write.sum"), peaks.get("hbm")),
+        "l2": (tot("lts__t_bytes.sum"), peaks.get("l2")),
+        "l1": (tot("l1tex__data_pipe_lsu_wavefronts.sum") * 128.0, peaks.get("smem")),
+    }
+    levels = {}
+    for k, (b, pk) in lv.items():
+        ach = b / secs / 1e9
+        levels[k] = {"bytes_per_launch": b / n, "achieved": ach, "peak": pk,
+                     "frac": ach / pk if pk else None}
+    bound = max((k for k in levels if levels[k]["frac"] is not None),
+                key=lambda k: levels[k]["frac"])
+    ncu_pct = {k: sum(x[m] or 0.0 for x in launches) / n for k, m in (
+        ("dram", "dram__throughput.avg.pct_of_peak_sustained_elapsed"),
+        ("l2", "lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+        ("l1", "l1tex__throughput.avg.pct_of_peak_sustained_elapsed"),
+        ("tensor_hmma", "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_elapsed"))}
+    ipc = sum(x["sm__inst_executed.avg.per_cycle_elapsed"] or 0.0 for x in launches) / n
+    return {"kernel": name, "bound": bound, "achieved": levels[bound]["achieved"],
+            "peak": levels[bound]["peak"], "unit": "GB/s", "frac": levels[bound]["frac"],
+            "traffic": levels["hbm"]["bytes_per_launch"], "levels": levels,
+            "ncu_pct_of_peak": ncu_pct, "ncu_issue_ipc": ipc,
+            "ncu_ms_per_launch": 1e3 * sum(x["gpu__time_duration.sum"] or 0 for x in launches)
+                                 / 1e9 / n}
 
 
 def run_ours(args, cfg):
@@ -353,53 +490,6 @@ def run_ours(args, cfg):
     tr_rmse = ft.evaluate(model, train_t, cache)[0]
     te_rmse = ft.evaluate(model, test_t, cache)[0]
 
-    # roofline of the dominant kernel (largest share of the timed region)
-    peak, peak_src = measured_peak()
-    by = {}
-    for name, mode, sec in krec:
-        tree = forest.trees[mode]
-        b = kernel_bytes(name, tree, dims, J, R)
-        agg = by.setdefault(name, {"bytes": 0, "sec": 0.0, "launches": 0})
-        agg["bytes"] += b
-        agg["sec"] += sec
-        agg["launches"] += 1
-    dom = max(by, key=lambda k: by[k]["sec"])
-    d = by[dom]
-    achieved = d["bytes"] / d["sec"] / 1e9
-    variant = os.environ.get("FT_FACTOR_KERNEL", "auto")
-    kname = (f"factor_rows_{variant}_kernel" if variant != "auto"
-             else "factor_rows_{quad|quadw}_kernel (auto: quad for many rows, quadw for few long rows)") if dom == "factor_rows" \
-        else dom + "_kernel"
-    traffic, _ = ncu_traffic(dom)
-    roof = {"kernel": kname, "bound": "hbm", "achieved": achieved, "peak": peak,
-            "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
-            "note": "achieved = SURVEY 8d algorithmic (logical) bytes / time; the gathered C "
-                    "rows are L1 / L2 hits, so DRAM moves only `traffic` bytes per launch and "
-                    "per-kernel fractions can exceed 1 (the sweeps are bound by the SM's L1 / "
-                    "shared-memory pipe, profiles/r01_ncu_sweeps.md)",
-            "traffic": traffic,
-            "bytes_per_launch": d["bytes"] / d["launches"],
-            "ms_per_launch": 1e3 * d["sec"] / d["launches"],
-            "share_of_step": d["sec"] / total_s}
-    kernels = {k: {"ms_total": 1e3 * v["sec"] / args.steps, "GB_per_s": v["bytes"] / v["sec"] / 1e9,
-                   "frac": v["bytes"] / v["sec"] / 1e9 / peak} for k, v in by.items()}
-    per_mode = {}
-    for name, mode, sec in krec:
-        key = f"{name}:{mode}"
-        e = per_mode.setdefault(key, {"ms": 0.0, "bytes": kernel_bytes(name, forest.trees[mode],
-                                                                       dims, J, R)})
-        e["ms"] += 1e3 * sec / args.steps
-    for e in per_mode.values():
-        e["frac"] = e["bytes"] / (e["ms"] / 1e3) / 1e9 / peak
-    kernels["by_mode"] = per_mode
-    pass_bytes = {"factor": 0, "core": 0}
-    for tree_u in forest.trees:
-        u = tree_u.root_mode
-        rb = refresh_bytes(dims[u], J, R)
-        pass_bytes["factor"] += kernel_bytes("factor_rows", tree_u, dims, J, R) + rb
-        pass_bytes["core"] += kernel_bytes("core_rows", tree_u, dims, J, R) + rb
-    launches_per_epoch = 5 * N  # per mode: factor sweep, refresh, core sweep, apply, refresh
-
     # CPU baseline (rank 0, N = 1): the reference's compiled kernels on a bounded sample
     cpu = None
     if not args.no_cpu:
@@ -412,6 +502,79 @@ def run_ours(args, cfg):
                "factor_nnz_per_s": nnz_s / tf, "core_nnz_per_s": nnz_s / tc}
 
     e2e = run_e2e(ft, T, cfg, train_t, args) if not args.no_e2e else None
+    from types import SimpleNamespace
+
+    trees = [SimpleNamespace(nnz=t.nnz, num_fibers=t.num_fibers, num_rows=t.num_rows,
+                             leaf_mode=t.leaf_mode, root_mode=t.root_mode) for t in forest.trees]
+    l2_note = ("inputs larger than L2 (forest arrays "
+               f"{sum(t.nnz * 8 + t.num_fibers * 12 for t in forest.trees) / 1e9:.1f} GB "
+               "streamed per epoch vs 126 MB L2)")
+    test_nnz = test_t.nnz
+
+    # roofline of the dominant kernel (largest share of the timed region)
+    peak, peak_src = measured_peak()
+    by = {}
+    per_launch = {}  # (name, mode) -> mean live seconds per launch
+    for name, mode, sec in krec:
+        tree = trees[mode]
+        b = kernel_bytes(name, tree, dims, J, R)
+        agg = by.setdefault(name, {"bytes": 0, "sec": 0.0, "launches": 0})
+        agg["bytes"] += b
+        agg["sec"] += sec
+        agg["launches"] += 1
+        per_launch[(name, mode)] = per_launch.get((name, mode), 0.0) + sec / args.steps
+    dom = max(by, key=lambda k: by[k]["sec"])
+    d = by[dom]
+    logical = {"bytes_per_launch": d["bytes"] / d["launches"],
+               "achieved": d["bytes"] / d["sec"] / 1e9, "peak": peak,
+               "frac_of_hbm": d["bytes"] / d["sec"] / 1e9 / peak,
+               "what": "SURVEY 8d variant-B algorithmic bytes (every gathered C row counted, no "
+                       "cache dedup) over the live launch time: a schedule-efficiency figure -- "
+                       "the C rows are L2 / L1 hits, so it is not a DRAM utilisation"}
+    # the ncu child rebuilds this workload in its own process: free ours first
+    del model, cache, train_t, test_t, split, forest
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    peaks = dict(onchip_peaks()) if not args.no_ncu else {}
+    peaks["hbm"] = peak
+    traffic = live_traffic(args, N) if not args.no_ncu else {"error": "--no-ncu"}
+    order = [("factor_rows", trees[t].leaf_mode) for t in range(N)] + \
+            [("core_rows", trees[t].leaf_mode) for t in range(N)]
+    kernels = {k: {"ms_total": 1e3 * v["sec"] / args.steps,
+                   "logical_GB_per_s": v["bytes"] / v["sec"] / 1e9} for k, v in by.items()}
+    per_mode = {}
+    for (name, mode), sec in per_launch.items():
+        per_mode[f"{name}:{mode}"] = {"ms": 1e3 * sec, "logical_bytes": kernel_bytes(
+            name, trees[mode], dims, J, R)}
+    if "launches" in traffic:
+        launches = traffic["launches"]
+        for k, (name, mode) in enumerate(order):
+            per_mode[f"{name}:{mode}"]["hierarchy"] = hierarchy_roofline(
+                launches[k]["kernel"], [launches[k]], per_launch[(name, mode)], peaks)
+        for name in ("factor_rows", "core_rows"):
+            sel = [k for k, o in enumerate(order) if o[0] == name]
+            kernels[name]["hierarchy"] = hierarchy_roofline(
+                "+".join(sorted({launches[k]["kernel"] for k in sel})), [launches[k] for k in sel],
+                sum(per_launch[order[k]] for k in sel), peaks)
+        roof = dict(kernels[dom]["hierarchy"])
+        roof["traffic_source"] = (f"live: ncu on this config ({traffic['seconds']:.0f} s, "
+                                  f"launches of one epoch, kernel replay)")
+    else:
+        roof = {"kernel": dom, "bound": "hbm", "achieved": logical["achieved"], "peak": peak,
+                "unit": "GB/s", "frac": logical["frac_of_hbm"], "traffic": None,
+                "traffic_source": traffic.get("error")}
+    roof.update({"peak_source": {"hbm": peak_src, "l2/l1/smem": "tools/peaks.cu, measured here"},
+                 "peaks_GB_per_s": peaks, "logical": logical,
+                 "ms_per_launch": 1e3 * d["sec"] / d["launches"],
+                 "share_of_step": d["sec"] / total_s})
+    kernels["by_mode"] = per_mode
+    pass_bytes = {"factor": 0, "core": 0}
+    for tree_u in trees:
+        u = tree_u.root_mode
+        rb = refresh_bytes(dims[u], J, R)
+        pass_bytes["factor"] += kernel_bytes("factor_rows", tree_u, dims, J, R) + rb
+        pass_bytes["core"] += kernel_bytes("core_rows", tree_u, dims, J, R) + rb
+    launches_per_epoch = 5 * N  # per mode: factor sweep, refresh, core sweep, apply, refresh
 
     line = {
         "metric": METRIC, "value": nnz * args.steps / total_s, "unit": "nnz/s", "n_gpus": 1,
@@ -419,19 +582,18 @@ def run_ours(args, cfg):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (GPU generator: distinct uniform cells, U[1,5] values; random init)",
         "config": {"workload": args.config, "dims": list(dims), "nnz_train": nnz,
-                   "nnz_test": test_t.nnz, "J": J, "R": R, "schedule": tcfg.resolved_schedule,
+                   "nnz_test": test_nnz, "J": J, "R": R, "schedule": tcfg.resolved_schedule,
                    "fiber_threshold": 128, "parallelism": "1 GPU",
-                   "l2": "inputs larger than L2 (forest arrays "
-                         f"{sum(t.nnz * 8 + t.num_fibers * 12 for t in forest.trees) / 1e9:.1f} GB "
-                         "streamed per epoch vs 126 MB L2)"},
+                   "l2": l2_note},
         "factor_nnz_per_s": nnz * args.steps / f_s, "core_nnz_per_s": nnz * args.steps / c_s,
         "factor_ms": 1e3 * f_s / args.steps, "core_ms": 1e3 * c_s / args.steps,
-        "pass_roofline_frac": {k: pass_bytes[k] / ((f_s if k == "factor" else c_s) / args.steps)
-                               / 1e9 / peak for k in pass_bytes},
-        # the north star's figure: the whole epoch (both passes, refreshes, applies) against
-        # the HBM roofline on the algorithmic bytes of the schedule that ran
-        "epoch_roofline_frac": (pass_bytes["factor"] + pass_bytes["core"])
-                               / (total_s / args.steps) / 1e9 / peak,
+        # SURVEY 8d's logical (algorithmic-byte) fractions of the HBM peak, per pass and for the
+        # epoch -- schedule-efficiency figures (see roofline.logical), not DRAM utilisation
+        "logical_pass_frac_of_hbm": {k: pass_bytes[k] / ((f_s if k == "factor" else c_s)
+                                                         / args.steps) / 1e9 / peak
+                                     for k in pass_bytes},
+        "logical_epoch_frac_of_hbm": (pass_bytes["factor"] + pass_bytes["core"])
+                                     / (total_s / args.steps) / 1e9 / peak,
         "train_rmse_before": rmse0, "train_rmse": tr_rmse, "test_rmse": te_rmse,
         "build_forest_s": build_s,
         "roofline": roof, "kernels": kernels,
@@ -518,8 +680,12 @@ def main():
     ap.add_argument("--schedule", default="exact", choices=["exact", "hogwild"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-ncu", action="store_true", help="skip the live ncu traffic capture")
+    ap.add_argument("--ncu-child", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    if args.ncu_child:
+        return ncu_child(args, cfg)
     if args.impl == "reference":
         run_reference_arm(args, cfg)
     else:

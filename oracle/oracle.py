@@ -416,6 +416,95 @@ def run_epoch(model, forest, cache, cfg, K=CKernels, epoch_no=1, snapshots=None)
                               mode=exc.mode, epoch=epoch_no) from None
 
 
+class RowParallelRef:
+    """The reference's serial epoch, run on all host cores at scale (10 M+ entries).
+
+    For the factor sweep of tree t (leaf mode u) the entries are split into T groups of
+    contiguous ``i_u`` blocks balanced by count, and each group gets its own tree t
+    (``build_tree``, bit-identical to csf.py:101-196).  A group's tree holds exactly the leaves
+    of its rows, in the full tree's relative order, under the same fibers.  Within a sweep only
+    rows of A_u change and each leaf touches only its own row (train.py:152-197), so
+    running the reference kernel ``K.factor_sweep`` (_ckern.pyx:132-199) over every group tree
+    concurrently -- disjoint rows, no shared writes -- is **bitwise** the serial sweep of the
+    full tree.  The core sweep (_ckern.pyx:202-269) accumulates one ``acc`` per group, summed
+    in fixed group order before ``apply_core_update`` with omega = |Omega| -- the reference's
+    own ``workers`` reduction (train.py:222-236), so it differs from the serial sweep only in
+    fp64 summation order.  ``K`` defaults to the reference's compiled ``_ckern`` (oracle/_ref)
+    when built, else our C restatement; both release the GIL, so Python threads run in
+    parallel.
+    """
+
+    def __init__(self, idx, vals, dims, threads=None, K=None, fiber_threshold=128):
+        from concurrent.futures import ThreadPoolExecutor
+
+        idx = np.ascontiguousarray(idx, dtype=np.int64)
+        vals = np.ascontiguousarray(vals, dtype=np.float64)
+        self.N = idx.shape[1]
+        self.nnz = idx.shape[0]
+        self.dims = tuple(int(d) for d in dims)
+        self.T = int(threads or min(os.cpu_count() or 1, 32))
+        self.K = K if K is not None else (ref_kernels() or CKernels)
+        self.pool = ThreadPoolExecutor(self.T)
+        jobs = []
+        for t in range(self.N):
+            u = (t + self.N - 1) % self.N
+            counts = np.bincount(idx[:, u], minlength=self.dims[u])
+            cum = np.cumsum(counts)
+            cuts = np.searchsorted(cum, np.linspace(0, self.nnz, self.T + 1)[1:-1], side="left")
+            bounds = [0] + [int(c) + 1 for c in cuts] + [self.dims[u]]
+            grp = np.searchsorted(np.asarray(bounds[1:-1]), idx[:, u], side="right")
+            order = np.argsort(grp, kind="stable")
+            starts = np.searchsorted(grp[order], np.arange(self.T + 1))
+            for k in range(self.T):
+                sel = order[starts[k]:starts[k + 1]]
+                if sel.size:
+                    jobs.append((t, idx[sel], vals[sel]))
+        built = list(self.pool.map(
+            lambda j: (j[0], build_tree(j[1], j[2], j[0], fiber_threshold)), jobs))
+        self.groups = [[tree for (tt, tree) in built if tt == t] for t in range(self.N)]
+
+    def leaf_mode(self, t):
+        return (t + self.N - 1) % self.N
+
+    def update_factor_mode(self, model, cache, t, cfg):
+        K, u = self.K, self.leaf_mode(t)
+        dots = cache if cfg.plan == "cached" else None
+        raws = [np.zeros(5, np.int64) for _ in self.groups[t]]
+        list(self.pool.map(lambda k: K.factor_sweep(
+            *_targs(self.groups[t][k]), model.factors, model.cores_t, dots, cfg.lr_a, cfg.reg_a,
+            raws[k], 0, self.groups[t][k].num_fibers), range(len(self.groups[t]))))
+        _guard(model.factors[u], u, cfg, "factor")
+        if cache is not None and cfg.plan == "cached":
+            K.refresh_dot_mode(model.factors[u], model.cores_t[u], cache[u], raws[0])
+
+    def update_core_mode(self, model, cache, t, cfg):
+        K, u = self.K, self.leaf_mode(t)
+        dots = cache if cfg.plan == "cached" else None
+        R, Ju = model.core_rank, model.ranks[u]
+        raws = [np.zeros(5, np.int64) for _ in self.groups[t]]
+        accs = [np.zeros((R, Ju)) for _ in self.groups[t]]
+        list(self.pool.map(lambda k: K.core_sweep(
+            *_targs(self.groups[t][k]), model.factors, model.cores_t, dots, accs[k], raws[k], 0,
+            self.groups[t][k].num_fibers), range(len(self.groups[t]))))
+        acc = accs[0]
+        for extra in accs[1:]:
+            acc += extra
+        K.apply_core_update(model.cores_t[u], acc, float(self.nnz), cfg.lr_b, cfg.reg_b, raws[0])
+        _guard(model.cores_t[u], u, cfg, "core")
+        if cache is not None and cfg.plan == "cached":
+            K.refresh_dot_mode(model.factors[u], model.cores_t[u], cache[u], raws[0])
+        return acc
+
+    def run_epoch(self, model, cache, cfg):
+        for t in range(self.N):
+            self.update_factor_mode(model, cache, t, cfg)
+        for t in range(self.N):
+            self.update_core_mode(model, cache, t, cfg)
+
+    def close(self):
+        self.pool.shutdown()
+
+
 def predict(model, idx):
     """model.py:219-230 (dots computed fresh, sequential sums)."""
     idx = np.ascontiguousarray(idx, dtype=np.int64)

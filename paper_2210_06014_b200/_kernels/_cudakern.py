@@ -17,11 +17,19 @@ t = (leaf_mode + 1) mod N are executed exactly: the range's entries are re-index
 as a tree rooted at the leaf mode (kernel K1), whose root slices are the rows' update lists in
 the serial order, and swept by the row-owner kernels K3b / K4.  The throughput path is the
 device-resident API in :mod:`paper_2210_06014_b200.train` (no copies).
+
+Concurrency (the reference's ``workers > 1`` pool, train.py:124-149, calls ``factor_sweep`` /
+``core_sweep`` from several threads on different subtensor ranges over the shared host
+``factors[u]``): each call holds a module lock from upload to write-back, so every call starts
+from the rows the previous calls wrote, and ``factor_sweep`` writes back only the rows of A_u
+its range touched -- other rows keep their host (fp64) values bit for bit.  The calls thus
+run as some serial order of the subtensors, never losing a whole range of updates.
 """
 
 from __future__ import annotations
 
 import ctypes
+import threading
 
 import numpy as np
 
@@ -29,6 +37,9 @@ from .. import _lib
 from ..counter import CH_DOT, apply_counts, sweep_counts
 
 BACKEND = "cuda"
+
+# one plugin call at a time: upload -> sweep -> write-back is atomic w.r.t. other workers
+_CALL_LOCK = threading.RLock()
 
 
 def _dev(a):
@@ -58,11 +69,12 @@ def refresh_dot_mode(A, B_t, out, counts):
     L = _lib.lib()
     I, J = A.shape
     R = B_t.shape[0]
-    dA, dB = _dev(A), _dev(B_t)
-    dC = torch.empty((I, R), dtype=torch.float32, device="cuda")
-    _lib.check(L.ft_refresh(I, J, R, dA.data_ptr(), dB.data_ptr(), dC.data_ptr(), None,
-                            _lib.stream_handle()), "ft_refresh")
-    out[...] = dC.cpu().numpy()
+    with _CALL_LOCK:
+        dA, dB = _dev(A), _dev(B_t)
+        dC = torch.empty((I, R), dtype=torch.float32, device="cuda")
+        _lib.check(L.ft_refresh(I, J, R, dA.data_ptr(), dB.data_ptr(), dC.data_ptr(), None,
+                                _lib.stream_handle()), "ft_refresh")
+        out[...] = dC.cpu().numpy()
     counts[CH_DOT] += I * J * R
 
 
@@ -121,13 +133,19 @@ def factor_sweep(leaf_coord, leaf_val, fiber_ptr, fiber_coord, prefix_modes, lea
     counts += sweep_counts("factor", plan, N, R, ranks, prefix_modes, u, nleaf, fib_hi - fib_lo)
     if tree is None:
         return
-    fd = [_dev(a) for a in factors]
-    cd = [_dev(b) for b in cores_t]
-    dd = _dots_dev(fd, cd, dots)
-    mv = _model_view(fd, cd, dd)
-    _lib.check(L.ft_factor_sweep_rows(ctypes.byref(tree.view()), ctypes.byref(mv), float(lr),
-                                      float(reg), _lib.stream_handle()), "ft_factor_sweep_rows")
-    factors[u][...] = fd[u].cpu().numpy()
+    fp = np.asarray(fiber_ptr, dtype=np.int64)
+    rows = np.unique(np.asarray(leaf_coord)[int(fp[fib_lo]):int(fp[fib_hi])])
+    with _CALL_LOCK:
+        fd = [_dev(a) for a in factors]
+        cd = [_dev(b) for b in cores_t]
+        dd = _dots_dev(fd, cd, dots)
+        mv = _model_view(fd, cd, dd)
+        _lib.check(L.ft_factor_sweep_rows(ctypes.byref(tree.view()), ctypes.byref(mv), float(lr),
+                                          float(reg), _lib.stream_handle()),
+                   "ft_factor_sweep_rows")
+        import torch
+
+        factors[u][rows] = fd[u][torch.from_numpy(rows).cuda()].cpu().numpy()
 
 
 def core_sweep(leaf_coord, leaf_val, fiber_ptr, fiber_coord, prefix_modes, leaf_mode, factors,
@@ -146,30 +164,33 @@ def core_sweep(leaf_coord, leaf_val, fiber_ptr, fiber_coord, prefix_modes, leaf_
     counts += sweep_counts("core", plan, N, R, ranks, prefix_modes, u, nleaf, fib_hi - fib_lo)
     if tree is None:
         return
-    fd = [_dev(a) for a in factors]
-    cd = [_dev(b) for b in cores_t]
-    dd = _dots_dev(fd, cd, dots)
-    # s = C_u[i] . cross needs C_u coherent with (A_u, Bt_u): compute it fresh
-    dd[u] = _dots_dev([fd[u]], [cd[u]], None)[0]
-    mv = _model_view(fd, cd, dd)
-    Ju = ranks[u]
-    cap = int(L.ft_core_partials_size(R, Ju))
-    partials = torch.empty(cap, dtype=torch.float32, device="cuda")
-    nb = ctypes.c_int32(0)
-    _lib.check(L.ft_core_sweep_rows(ctypes.byref(tree.view()), ctypes.byref(mv),
-                                    partials.data_ptr(), cap, ctypes.byref(nb),
-                                    _lib.stream_handle()), "ft_core_sweep_rows")
-    g = torch.empty((R, Ju), dtype=torch.float32, device="cuda")
-    _lib.check(L.ft_core_reduce(R, Ju, partials.data_ptr(), nb.value, g.data_ptr(),
-                                _lib.stream_handle()), "ft_core_reduce")
-    acc[...] -= g.cpu().numpy()
+    with _CALL_LOCK:
+        fd = [_dev(a) for a in factors]
+        cd = [_dev(b) for b in cores_t]
+        dd = _dots_dev(fd, cd, dots)
+        # s = C_u[i] . cross needs C_u coherent with (A_u, Bt_u): compute it fresh
+        dd[u] = _dots_dev([fd[u]], [cd[u]], None)[0]
+        mv = _model_view(fd, cd, dd)
+        Ju = ranks[u]
+        cap = int(L.ft_core_partials_size(R, Ju))
+        partials = torch.empty(cap, dtype=torch.float32, device="cuda")
+        nb = ctypes.c_int32(0)
+        _lib.check(L.ft_core_sweep_rows(ctypes.byref(tree.view()), ctypes.byref(mv),
+                                        partials.data_ptr(), cap, ctypes.byref(nb),
+                                        _lib.stream_handle()), "ft_core_sweep_rows")
+        g = torch.empty((R, Ju), dtype=torch.float32, device="cuda")
+        _lib.check(L.ft_core_reduce(R, Ju, partials.data_ptr(), nb.value, g.data_ptr(),
+                                    _lib.stream_handle()), "ft_core_reduce")
+        acc[...] -= g.cpu().numpy()
 
 
 def apply_core_update(core_t_u, acc, omega, lr, reg, counts):
     L = _lib.lib()
     R, J = core_t_u.shape
-    dB, dA = _dev(core_t_u), _dev(acc)
-    _lib.check(L.ft_core_apply(R, J, dB.data_ptr(), dA.data_ptr(), 1, 0, float(omega), float(lr),
-                               float(reg), None, None, _lib.stream_handle()), "ft_core_apply")
-    core_t_u[...] = dB.cpu().numpy()
+    with _CALL_LOCK:
+        dB, dA = _dev(core_t_u), _dev(acc)
+        _lib.check(L.ft_core_apply(R, J, dB.data_ptr(), dA.data_ptr(), 1, 0, float(omega),
+                                   float(lr), float(reg), None, None, _lib.stream_handle()),
+                   "ft_core_apply")
+        core_t_u[...] = dB.cpu().numpy()
     counts += apply_counts(R, J)

@@ -208,6 +208,44 @@ __device__ __forceinline__ void quad_chain_step_v(float (&a)[4], const float4 v,
   a[3] = __fmaf_rn(lre, v.w, a23.y);
 }
 
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<unsigned long long *>(&a)),
+        "l"(*reinterpret_cast<unsigned long long *>(&b)));
+  return *reinterpret_cast<float2 *>(&d);
+}
+__device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
+  return fadd2(a, make_float2(-b.x, -b.y));
+}
+
+// The same step with a COMPENSATED row: a (the fp32 row the dot products use) plus lo, the
+// rounding residue of every row update so far (Fast2Sum: the increment d is ~1e-4 of |a|).
+// The increment d = (-lr reg) a + lr e v + lo folds the residue back in, so a stays the
+// correctly rounded value of the exact fp32-increment sum.  Rows with tens of thousands of
+// serial updates (Netflix mode 2: 45 K) otherwise drift ~1e-4 from the fp64 reference
+// (tests/test_netflix_parity_gpu.py); the residue costs two packed adds per column pair, off
+// the serial dependency except one FADD.
+__device__ __forceinline__ void quad_chain_step_vc(float (&a)[4], float (&lo)[4], const float4 v,
+                                                   float4 m) {
+  float2 pr = fmul2(make_float2(a[0], a[1]), make_float2(v.x, v.y));
+  pr = ffma2(make_float2(a[2], a[3]), make_float2(v.z, v.w), pr);
+  float s = pr.x + pr.y;
+  s += __shfl_xor_sync(FULL, s, 4);
+  s += __shfl_xor_sync(FULL, s, 2);
+  s += __shfl_xor_sync(FULL, s, 1);
+  const float e = m.x - s;  // m = (x, lr, -lr reg, -lr reg); lr = 0 on padding steps
+  const float2 l2 = make_float2(m.y * e, m.y * e), c2 = make_float2(m.z, m.w);
+  const float2 a01 = make_float2(a[0], a[1]), a23 = make_float2(a[2], a[3]);
+  const float2 d01 = ffma2(l2, make_float2(v.x, v.y), ffma2(c2, a01, make_float2(lo[0], lo[1])));
+  const float2 d23 = ffma2(l2, make_float2(v.z, v.w), ffma2(c2, a23, make_float2(lo[2], lo[3])));
+  const float2 t01 = fadd2(a01, d01), t23 = fadd2(a23, d23);
+  const float2 r01 = fsub2(d01, fsub2(t01, a01)), r23 = fsub2(d23, fsub2(t23, a23));
+  a[0] = t01.x, a[1] = t01.y, a[2] = t23.x, a[3] = t23.y;
+  lo[0] = r01.x, lo[1] = r01.y, lo[2] = r23.x, lo[3] = r23.y;
+}
+
 
 // Order-N gathers into a warp's 32-slot X / Y tiles (row stride XSD floats): X <- prod over the
 // NPRE prefix levels of C_pre[d][pc_d] (gather, wait, multiply in place, level by level -- the
@@ -1470,17 +1508,18 @@ __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(co
       if (ai >= 0) store_r();
       return;
     }
-    float a[4] = {0.f, 0.f, 0.f, 0.f};
+    float a[4] = {0.f, 0.f, 0.f, 0.f}, lo[4] = {0.f, 0.f, 0.f, 0.f};
     int ai = -1;
     float *xrow = ring + quadw::NS * quadw::STAGE_FLOATS + quadw::NP * 2 * TILE + 32 * q;
     auto store_a = [&]() {
       float *ar = p.A + (int64_t)ai * J;
+      const float o[4] = {a[0] + lo[0], a[1] + lo[1], a[2] + lo[2], a[3] + lo[3]};
       if (j32) {
-        *reinterpret_cast<float4 *>(ar + 4 * l) = make_float4(a[0], a[1], a[2], a[3]);
+        *reinterpret_cast<float4 *>(ar + 4 * l) = make_float4(o[0], o[1], o[2], o[3]);
       } else {
 #pragma unroll
         for (int t = 0; t < 4; ++t)
-          if (4 * l + t < J) ar[4 * l + t] = a[t];
+          if (4 * l + t < J) ar[4 * l + t] = o[t];
       }
     };
     for (int t = 0;; ++t) {
@@ -1492,6 +1531,7 @@ __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(co
         if (ai >= 0) store_a();
         const float4 v = *reinterpret_cast<const float4 *>(stage_a(st) + 32 * q + 4 * l);
         a[0] = v.x, a[1] = v.y, a[2] = v.z, a[3] = v.w;
+        lo[0] = lo[1] = lo[2] = lo[3] = 0.f;
         ai = info.z;
       }
       const float *Vq = stage_v(st) + 8 * q * QVS + 4 * l;
@@ -1552,7 +1592,7 @@ __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(co
         __syncwarp();
         mbar_arrive(empty + st);  // the stage is free once read
 #pragma unroll
-        for (int kk = 0; kk < QB; ++kk) quad_chain_step_v(a, vv[kk], mm[kk]);
+        for (int kk = 0; kk < QB; ++kk) quad_chain_step_vc(a, lo, vv[kk], mm[kk]);
         continue;
       }
       __syncwarp();

@@ -178,3 +178,42 @@ def test_reference_kernels_agree_with_oracle(golden_cases):
         outs.append(model)
     for a, b in zip(outs[0].factors + outs[0].cores_t, outs[1].factors + outs[1].cores_t):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("kind", ["oracle", "reference"])
+def test_row_parallel_reference_is_the_serial_epoch(kind):
+    """oracle.RowParallelRef (the at-scale checker of tests/test_netflix_parity_gpu.py): the
+    row-partitioned concurrent factor sweeps are bitwise the serial sweeps of the full trees,
+    and the per-group core accumulators sum to the serial core step (fp64 summation order
+    only), over two epochs of an order-3 and an order-4 tensor with split root slices."""
+    if kind == "reference" and O.ref_kernels() is None:
+        pytest.skip("oracle/_ref not built")
+    K = O.kernels(kind)
+    for dims, nnz, J in (((60, 40, 30), 20_000, 8), ((12, 10, 9, 8), 5_000, 4)):
+        rng = np.random.default_rng(len(dims))
+        lin = rng.choice(int(np.prod(dims)), size=nnz, replace=False)
+        idx = np.stack(np.unravel_index(lin, dims), axis=1).astype(np.int64)
+        vals = rng.uniform(1, 5, size=nnz)
+        N = len(dims)
+        cfg = O.OracleConfig(lr_a=0.01, lr_b=0.01)
+        serial = O.default_init_model(dims, (J,) * N, J, seed=3)
+        par = serial.copy()
+        forest = O.build_forest(idx, vals, 16)
+        rp = O.RowParallelRef(idx, vals, dims, threads=5, K=K, fiber_threshold=16)
+        c_s = O.precompute_cache(serial, K)
+        c_p = O.precompute_cache(par, K)
+        for _ in range(2):
+            for t in range(N):
+                O.update_factor_mode(serial, forest, c_s, t, cfg, K)
+                rp.update_factor_mode(par, c_p, t, cfg)
+                u = forest[t].leaf_mode
+                assert np.array_equal(serial.factors[u], par.factors[u])
+            for t in range(N):
+                O.update_core_mode(serial, forest, c_s, t, cfg, K)
+                rp.update_core_mode(par, c_p, t, cfg)
+                u = forest[t].leaf_mode
+                np.testing.assert_allclose(par.cores_t[u], serial.cores_t[u], rtol=1e-12)
+                serial.cores_t[u][...] = par.cores_t[u]   # keep the factor check bitwise
+                K.refresh_dot_mode(serial.factors[u], serial.cores_t[u], c_s[u],
+                                   np.zeros(5, np.int64))
+        rp.close()

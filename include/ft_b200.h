@@ -74,6 +74,17 @@ typedef struct {
   int64_t num_segs;
   const int32_t *seg_coord;     /* [segs]  row coordinate of each segment                    */
   const int32_t *seg_leaf_ptr;  /* [segs+1] first leaf of each segment                       */
+  /* Slot layout for the tcgen05 factor sweep (optional, slot_grid = 0 = absent; K1d,
+   * ft_tree_slot_plan / ft_tree_slot_fill).  Slot q = c + G s (CTA c < G, slot s < 128) owns rows
+   * q, q + 128 G, ... and walks their leaves one per batch; entry [batch][s] of CTA c holds that
+   * leaf's coordinates and value, so each batch's operands are coalesced loads. */
+  int32_t slot_grid;            /* G (CTAs the layout was built for)                         */
+  int32_t slot_pad_;
+  const int32_t *slot_batch_ptr;/* [G+1] first batch of each CTA                             */
+  const int32_t *slot_lc;       /* [batches x 128] leaf coordinate | 0x80000000 on the first
+                                   leaf of a row; -1 = padding (the slot's stream ended)      */
+  const int32_t *slot_pc;       /* [batches x (N-2) x 128] levels 1..N-2                      */
+  const float *slot_x;          /* [batches x 128] values                                    */
 } ft_tree_t;
 
 /* Model parameters and the C^(n) cache (model.py:45-103, cache.py:28-57). */
@@ -142,6 +153,18 @@ FT_API int ft_tree_leaf_index(const ft_tree_t *tree, int32_t *leaf_pc, int32_t *
  * segment count.  SYNCHRONOUS (the count is read back). */
 FT_API int ft_tree_row_segments(const ft_tree_t *tree, int32_t max_len, int32_t *seg_coord,
                                 int32_t *seg_leaf_ptr, int64_t *nseg_out, void *stream);
+/* K1d Slot layout for the tcgen05 factor sweep (reads tree->row_leaf_ptr / leaf_coord /
+ * leaf_pc / vals).  Not a reference structure: it re-orders the tree's leaves so that the
+ * sweep over the tree rooted at u (factor_sweep, _ckern.pyx:132-199) reads them coalesced.
+ * ft_tree_slot_plan: *grid_out = G, or 0 when the tcgen05 sweep does not apply to this tree
+ *   (shape J, R, order, too few rows to fill the GPU, FT_FACTOR_TC=0); with batch_ptr == NULL
+ *   only G is returned; else batch_ptr (device int32 [G+1]) is filled and *len_out (HOST) gets
+ *   the entry count (batches x 128).  SYNCHRONOUS when batch_ptr != NULL.
+ * ft_tree_slot_fill: writes slot_lc / slot_x [len] and slot_pc [len x (N-2)].  Asynchronous. */
+FT_API int ft_tree_slot_plan(const ft_tree_t *tree, int32_t J, int32_t R, int32_t *grid_out,
+                             int32_t *batch_ptr, int64_t *len_out, void *stream);
+FT_API int ft_tree_slot_fill(const ft_tree_t *tree, int32_t grid, const int32_t *batch_ptr,
+                             int32_t *slot_lc, int32_t *slot_pc, float *slot_x, void *stream);
 /* K2  C = A * Bt^T  (I x R), i.e. refresh_dot_mode (_ckern.pyx:21-33, cache.py:60-70), with the
  * divergence guard of train.py:101-110 fused: if guard != NULL, atomically max-es the IEEE bits
  * of |A| into guard[0] (NaN sorts above +inf, so one word detects both cases). */

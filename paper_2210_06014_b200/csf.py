@@ -48,6 +48,11 @@ class CsfTree:
     row_leaf_ptr: object = None  # device int32 [rows+1] first leaf per row (derived)
     seg_coord: object = None     # device int32 [segs]  core-sweep row segments (derived)
     seg_leaf_ptr: object = None  # device int32 [segs+1]
+    slot_grid: int = -1          # slot layout of the tcgen05 factor sweep (-1 = not planned,
+    slot_batch_ptr: object = None  # 0 = does not apply); device int32 [G+1]
+    slot_lc: object = None       # device int32 [batches x 128]
+    slot_pc: object = None       # device int32 [batches x (N-2) x 128]
+    slot_x: object = None        # device fp32 [batches x 128]
     _view: object = field(default=None, repr=False)
     num_subtensors_built: int = -1
 
@@ -105,8 +110,49 @@ class CsfTree:
             v.num_segs = 0 if self.seg_coord is None else int(self.seg_coord.shape[0])
             v.seg_coord = _lib.ptr(self.seg_coord)
             v.seg_leaf_ptr = _lib.ptr(self.seg_leaf_ptr)
+            v.slot_grid = max(self.slot_grid, 0) if self.slot_lc is not None else 0
+            v.slot_batch_ptr = _lib.ptr(self.slot_batch_ptr)
+            v.slot_lc = _lib.ptr(self.slot_lc)
+            v.slot_pc = _lib.ptr(self.slot_pc)
+            v.slot_x = _lib.ptr(self.slot_x)
             self._view = v
         return self._view
+
+    def ensure_slots(self, J: int, R: int, stream=None) -> "CsfTree":
+        """Build (once) the slot layout the tcgen05 factor sweep reads (K1d, ft_tree_slot_plan /
+        ft_tree_slot_fill): the leaves re-ordered [CTA][batch][slot] so that each batch's
+        coordinates and values are coalesced loads.  No-op when the sweep does not apply to this
+        tree (too few rows to fill the GPU, J / R / order outside its cover, no leaf index)."""
+        import torch
+
+        if self.slot_grid >= 0 or self.row_leaf_ptr is None or self.leaf_pc is None:
+            return self
+        L = _lib.lib()
+        g = ctypes.c_int32(0)
+        n = ctypes.c_int64(0)
+        v = self.view()
+        _lib.check(L.ft_tree_slot_plan(ctypes.byref(v), int(J), int(R), ctypes.byref(g), None,
+                                       ctypes.byref(n), _lib.stream_handle(stream)),
+                   "ft_tree_slot_plan")
+        if g.value <= 0:
+            self.slot_grid = 0
+            return self
+        i32 = dict(dtype=torch.int32, device=self.vals.device)
+        bp = torch.empty(g.value + 1, **i32)
+        _lib.check(L.ft_tree_slot_plan(ctypes.byref(v), int(J), int(R), ctypes.byref(g),
+                                       bp.data_ptr(), ctypes.byref(n), _lib.stream_handle(stream)),
+                   "ft_tree_slot_plan")
+        length = int(n.value)
+        lc = torch.empty(length, **i32)
+        pc = torch.empty(length * (self.order - 2), **i32)
+        x = torch.empty(length, dtype=torch.float32, device=self.vals.device)
+        _lib.check(L.ft_tree_slot_fill(ctypes.byref(v), g.value, bp.data_ptr(), lc.data_ptr(),
+                                       pc.data_ptr(), x.data_ptr(), _lib.stream_handle(stream)),
+                   "ft_tree_slot_fill")
+        self.slot_batch_ptr, self.slot_lc, self.slot_pc, self.slot_x = bp, lc, pc, x
+        self.slot_grid = g.value
+        self._view = None
+        return self
 
     def host(self) -> dict:
         """All reference fields as int64 / float64 numpy arrays (for parity checks)."""

@@ -34,6 +34,8 @@
 #include "ft_common.cuh"
 
 namespace ft {
+int launch_factor_tc(const ft_tree_t *t, const ft_model_t *m, float lr, float reg,
+                     cudaStream_t s);  // factor_tc.cu
 namespace {
 
 constexpr int WPB = 8;    // warps per block
@@ -2080,6 +2082,12 @@ extern "C" int ft_factor_sweep_rows(const ft_tree_t *tree, const ft_model_t *mod
   p.reg = reg;
   if (p.nrows == 0) return FT_OK;
   cudaStream_t s = as_stream(stream);
+  // K3c (factor_tc.cu): tcgen05 combine, one thread per row, when the tree carries the slot
+  // layout and no warp-level variant is forced; -1 = does not apply
+  if (!getenv("FT_FACTOR_KERNEL")) {
+    const int rc = launch_factor_tc(tree, model, lr, reg, s);
+    if (rc >= 0) return rc;
+  }
   if (p.R <= 8) return launch_factor_rows<8>(p, s);
   if (p.R <= 16) return launch_factor_rows<16>(p, s);
   return launch_factor_rows<32>(p, s);

@@ -117,6 +117,7 @@ class CudaEngine:
     def factor_sweep(self, shard, model, dots, lr, reg):
         if shard.tree is None:
             return
+        shard.tree.ensure_slots(model.ranks[shard.tree.root_mode], model.core_rank)
         _lib.check(self.L.ft_factor_sweep_rows(ctypes.byref(shard.tree.view()),
                                                ctypes.byref(model.view(dots)), lr, reg,
                                                _lib.stream_handle()), "ft_factor_sweep_rows")

@@ -248,6 +248,7 @@ def update_factor_mode(model, forest: CsfForest, cache: DotCache | None, n: int,
     mv = model.view(dots)
     stream = _lib.stream_handle()
     if cfg.resolved_schedule == "exact":
+        forest.trees[u].ensure_slots(model.ranks[u], model.core_rank)  # once per tree (K1d)
         with _ktime("factor_rows", u):
             _lib.check(L.ft_factor_sweep_rows(ctypes.byref(forest.trees[u].view()),
                                               ctypes.byref(mv), cfg.lr_a, cfg.reg_a, stream),

@@ -1,0 +1,96 @@
+"""K3c, the tcgen05 factor sweep (csrc/factor_tc.cu: combine on tcgen05 with the A operand in
+TMEM, one thread per row, slot layout K1d), against the fp64 oracle at the contract's rel 1e-4
+per sweep, and the slot layout itself against the tree it was built from.
+
+The default dispatch runs K3c on every tree with enough rows to fill the GPU (>= 64 per SM):
+each case below has at least one such mode; the other modes run quadr / quadw as usual, so
+every sweep of two epochs is checked.  Cases: short rows (1-3 leaves, J < 32 and R < 32
+padding, R % 8 = 4), more rows than slots (row switching inside a slot's stream), rows of
+hundreds of leaves, order 4 (two prefix levels), J = 16 / R = 12, and both chain forms
+(plain fp32 and the Fast2Sum-compensated one, FT_TC_COMP).
+"""
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from test_quad_gpu import _CASE
+
+pytestmark = pytest.mark.gpu
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def ft():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2210_06014_b200 as ft
+
+    return ft
+
+
+@pytest.mark.parametrize("dims,nnz,J,R,lr,comp", [
+    ((20000, 700, 9), 300_000, 24, 20, 1e-3, "0"),    # 1-3 leaf rows, padding, R % 8 = 4
+    ((60000, 12000, 64), 1_000_000, 32, 32, 5e-3, "0"),  # two tc modes, row switching
+    ((12000, 300, 50), 2_000_000, 32, 32, 2e-3, "1"),  # ~170-leaf rows, compensated chain
+    ((12000, 300, 50), 2_000_000, 32, 32, 2e-3, "0"),
+    ((20000, 10000, 30, 20), 600_000, 32, 32, 2e-3, "0"),  # order 4
+    ((15000, 300, 40), 400_000, 16, 12, 2e-3, "1"),   # J = 16, R = 12
+])
+def test_tc_factor_sweeps_match_oracle(dims, nnz, J, R, lr, comp):
+    code = _CASE.format(dims=dims, nnz=nnz, J=J, R=R, lr=lr, seed=11)
+    env = dict(os.environ, FT_TC_COMP=comp)
+    env.pop("FT_FACTOR_KERNEL", None)
+    env.pop("FT_FACTOR_TC", None)
+    out = subprocess.run([sys.executable, "-c", code], cwd=REPO, env=env, capture_output=True,
+                         text=True, timeout=900)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
+
+
+def test_slot_layout_covers_every_leaf_once(ft):
+    """K1d: per CTA c and slot s, the non-padding entries [batch][s] are exactly the leaves of
+    rows c + G s, c + G s + 128 G, ... in order, the first leaf of each row flagged."""
+    import torch
+
+    rng = np.random.default_rng(2)
+    dims = (30000, 50, 40)
+    lin = rng.choice(int(np.prod(dims)), size=500_000, replace=False)
+    idx = np.stack(np.unravel_index(lin, dims), axis=1)
+    dev = ft.DeviceCoo(dims, torch.from_numpy(idx.astype(np.int32)).cuda(),
+                       torch.from_numpy(rng.uniform(1, 5, len(lin)).astype(np.float32)).cuda())
+    tree = ft.build_tree(dev, 0, 128).ensure_slots(32, 32)
+    G = tree.slot_grid
+    assert G > 0
+    bp = tree.slot_batch_ptr.cpu().numpy()
+    lc = tree.slot_lc.cpu().numpy().view(np.uint32)
+    pc = tree.slot_pc.cpu().numpy()
+    x = tree.slot_x.cpu().numpy()
+    rlp = tree.row_leaf_ptr.cpu().numpy()
+    leaf_coord = tree.leaf_coord.cpu().numpy()
+    leaf_pc = tree.leaf_pc.cpu().numpy().reshape(-1)
+    vals = tree.vals.cpu().numpy()
+    rows = tree.num_rows
+    seen = 0
+    for c in range(G):
+        for s in range(0, 128, 7):  # a sample of slots
+            want = []
+            for r in range(c + G * s, rows, 128 * G):
+                for L in range(rlp[r], rlp[r + 1]):
+                    want.append((int(leaf_coord[L]) | (0x80000000 if L == rlp[r] else 0),
+                                 int(leaf_pc[L]), float(vals[L])))
+            got = []
+            for b in range(bp[c], bp[c + 1]):
+                e = b * 128 + s
+                if lc[e] == 0xFFFFFFFF:
+                    continue
+                got.append((int(lc[e]), int(pc[e]), float(x[e])))
+            assert got == want
+            seen += len(got)
+    assert seen > 0
+    assert bp[-1] * 128 == tree.slot_lc.numel()

@@ -19,9 +19,9 @@
 //     swizzled so that thread s reads its own slot's rows conflict-free;
 //   * thread s forms its cross row, splits it 3xTF32 (truncation hi + fp32 lo) and writes both
 //     halves into TMEM with tcgen05.st (the A operand never touches shared memory again);
-//   * one elected thread of the MMA warp issues D = A_lo Bt_hi + A_hi Bt_lo + A_hi Bt_hi
-//     (M = 128 slots, N = 32 = J padded, K = R in steps of 8; Bt_u^T hi / lo in shared memory,
-//     K-major, 128-B swizzle) and commits to an mbarrier; thread s reads v (its TMEM lane) with
+//   * one elected thread issues the 3xTF32 combine as 2 x R/8 MMAs at N = 64 (M = 128 slots,
+//     K = R in steps of 8; B = [Bt_hi ; Bt_lo] then [Bt_hi ; 0] in shared memory, K-major,
+//     128-B swizzle) and commits to an mbarrier; thread s reads v (its TMEM lane) with
 //     tcgen05.ld and runs the step.  Two TMEM stages: the MMA of batch b overlaps the chain of
 //     batch b-1 and the gathers of batches up to b+GS-1 are in flight.
 // Requirements (checked by the dispatcher): 3 <= N <= 4, J <= 32, R <= 32 with R % 4 == 0, the
@@ -37,9 +37,12 @@ namespace ft {
 namespace {
 
 constexpr int SLOTS = 128;
-constexpr int CWARPS = 4;                    // consumer warps: warp w <-> TMEM lanes 32w..32w+31
-constexpr int THREADS = (CWARPS + 1) * 32;   // + the MMA warp
-constexpr int TCOLS = 96;                    // TMEM columns per stage: A_hi | A_lo | D
+constexpr int CWARPS = 4;                    // warps per role: warp w <-> TMEM lanes 32(w%4)..+31
+constexpr int THREADS = (2 * CWARPS + 1) * 32;  // producers, consumers, the MMA warp
+// TMEM: AS A stages (A_hi | A_lo, 64 columns each) then DS D stages (64 columns each).  The A
+// ring is the deep one: a producer reuses an A stage once that batch's MMAs completed, so the
+// producers run up to AS batches ahead of the tensor core; consumers trail the MMA closely.
+constexpr int AS = 6, DS = 2;
 constexpr uint32_t ROW_START = 0x80000000u;  // slot_lc flag: first leaf of the slot's next row
 constexpr int32_t PAD = -1;                  // slot_lc of a padding entry (slot stream ended)
 
@@ -151,31 +154,71 @@ struct TcParams {
 
 template <int NPRE, int GS>
 struct TcPlan {
+  static_assert((GS & (GS - 1)) == 0, "gather ring stages: a power of two");
   static constexpr int LEVELS = NPRE + 1;                 // gathered C rows per leaf
   static constexpr int STAGE = SLOTS * LEVELS * 128;      // bytes per gather stage
-  static constexpr int B_BYTES = 32 * 128;                // Bt^T tile (N = 32 rows of 128 B)
-  static constexpr int MS = 2 * GS;                       // metadata ring stages
-  static constexpr int MWORDS = (NPRE + 2) * SLOTS;       // lc|flags, pc[NPRE], x per stage
-  static constexpr int META = MS * MWORDS * 4;
-  static constexpr size_t SMEM = 1024 + 2 * B_BYTES + (size_t)GS * STAGE + META + 64;
+  static constexpr int B_BYTES = 64 * 128;                // B tile: N = 64 rows of 128 B
+  // metadata ring stages: requested 2 GS - 1 batches ahead of the producer, read by the
+  // consumer up to AS + DS batches behind it (see the barrier chain in the kernel)
+  static constexpr int MS = 4 * GS > 16 ? 4 * GS : 16;
+  static_assert(MS >= 2 * GS + AS + DS, "metadata ring too short");
+  static constexpr int MSTRIDE = (NPRE + 2) * SLOTS * 4;  // lc|flags, pc[NPRE], x per stage
+  static constexpr size_t SMEM = 1024 + 2 * B_BYTES + (size_t)GS * STAGE + MS * MSTRIDE + 256;
 };
 
-template <int NPRE, int GS, bool COMP>
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];\n"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(a)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void cp4(uint32_t dst, const void *src, bool on) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q cp.async.ca.shared.global [%0], [%1], 4;\n}\n" ::"r"(dst),
+      "l"(src), "r"((int)on));
+}
+__device__ __forceinline__ void cp16p(uint32_t dst, const void *src, bool on) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q cp.async.ca.shared.global [%0], [%1], 16;\n}\n" ::"r"(dst),
+      "l"(src), "r"((int)on));
+}
+
+// R32: R == 32 (no chunk predicates, shift addressing); COMP: Fast2Sum-compensated row.
+// Warp roles (one 128-slot set per CTA): warps 0-3 PRODUCE (metadata + gathers + cross -> TMEM
+// A), warps 4-7 CONSUME (TMEM D -> chain), warp 8 issues the MMAs.  Warps w and w + 4 serve the
+// same TMEM lane quadrant.  Barriers per TMEM stage st = b % 4:
+//   a_ready[st]  producers -> MMA   (A of batch b written)
+//   v_ready[st]  MMA commit -> consumers (D of batch b) and producers (A of batch b free again)
+//   d_free[st]   consumers -> MMA   (D of batch b read)
+template <int NPRE, int GS, bool R32, bool COMP>
 __global__ void __launch_bounds__(THREADS, 1) factor_rows_tc_kernel(const TcParams p) {
   using P = TcPlan<NPRE, GS>;
   extern __shared__ __align__(1024) uint8_t smraw[];
-  uint8_t *base = reinterpret_cast<uint8_t *>(
-      (reinterpret_cast<uintptr_t>(smraw) + 1023) & ~(uintptr_t)1023);
-  uint8_t *b_hi = base, *b_lo = base + P::B_BYTES;
-  uint8_t *ring = base + 2 * P::B_BYTES;
-  int32_t *meta = reinterpret_cast<int32_t *>(ring + (size_t)GS * P::STAGE);
-  uint64_t *bar = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(meta) + P::META);
-  uint64_t *a_ready = bar, *v_ready = bar + 2;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 4);
-  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  const int J = p.J, R = p.R;
+  // 1024-B aligned operand tiles, addressed as shared-window offsets
+  const uint32_t sraw = su32(smraw);
+  const uint32_t sbase = (sraw + 1023u) & ~1023u;
+  const uint32_t b_hi = sbase, b_lo = sbase + P::B_BYTES;
+  const uint32_t ring = sbase + 2 * P::B_BYTES;
+  const uint32_t meta = ring + GS * P::STAGE;
+  const uint32_t bars = meta + P::MS * P::MSTRIDE;
+  uint8_t *gbase = smraw + (sbase - sraw);
+  uint64_t *a_ready = reinterpret_cast<uint64_t *>(gbase + (bars - sbase));
+  uint64_t *a_free = a_ready + AS, *v_ready = a_free + AS, *d_free = v_ready + DS;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(d_free + DS);
+    const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int J = p.J, R = R32 ? 32 : p.R;
 
-  // Bt_u^T (N = j rows, K = r) -> hi / lo, K-major, 128-B swizzle, zero padded to 32 x 32
+  // B operands (N = 64, K-major, 128-B swizzle, zero padded): P = [Bt_hi^T ; Bt_lo^T] and
+  // Q = [Bt_hi^T ; 0], so that D[:, 0:32] = A_hi Bt_hi + A_lo Bt_hi and D[:, 32:64] = A_hi Bt_lo
+  // (v = the sum of the two halves): 3xTF32 in 2 x ksteps N = 64 MMAs instead of 3 x ksteps at
+  // N = 32 (tools/umma_probe.cu: an N = 64 MMA costs about what an N = 32 one does)
   for (int e = tid; e < 32 * 8; e += THREADS) {
     const int j = e >> 3, c = e & 7;
     float v[4];
@@ -191,19 +234,19 @@ __global__ void __launch_bounds__(THREADS, 1) factor_rows_tc_kernel(const TcPara
     l.y = __float_as_uint(v[1] - __uint_as_float(h.y));
     l.z = __float_as_uint(v[2] - __uint_as_float(h.z));
     l.w = __float_as_uint(v[3] - __uint_as_float(h.w));
-    *reinterpret_cast<uint4 *>(b_hi + off) = h;
-    *reinterpret_cast<uint4 *>(b_lo + off) = l;
+    *reinterpret_cast<uint4 *>(gbase + off) = h;                            // P rows 0-31
+    *reinterpret_cast<uint4 *>(gbase + 32 * 128 + off) = l;                 // P rows 32-63
+    *reinterpret_cast<uint4 *>(gbase + P::B_BYTES + off) = h;               // Q rows 0-31
+    *reinterpret_cast<uint4 *>(gbase + P::B_BYTES + 32 * 128 + off) = make_uint4(0, 0, 0, 0);
   }
   if (w == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
         su32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   if (tid == 0) {
-    mbar_init(a_ready, CWARPS);
-    mbar_init(a_ready + 1, CWARPS);
-    mbar_init(v_ready, 1);
-    mbar_init(v_ready + 1, 1);
+    for (int k = 0; k < AS; ++k) mbar_init(a_ready + k, CWARPS), mbar_init(a_free + k, 1);
+    for (int k = 0; k < DS; ++k) mbar_init(v_ready + k, 1), mbar_init(d_free + k, CWARPS);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // B tiles -> tensor core
@@ -213,100 +256,179 @@ __global__ void __launch_bounds__(THREADS, 1) factor_rows_tc_kernel(const TcPara
   const uint32_t tmem = *tmem_slot;
   const int64_t b0 = __ldg(p.batch_ptr + blockIdx.x);
   const int nb = __ldg(p.batch_ptr + blockIdx.x + 1) - (int)b0;
+  const int q = w & 3;                      // TMEM lane quadrant
+  const int s = 32 * q + lane;              // slot = TMEM lane
+  const uint32_t tlane = tmem + ((uint32_t)(32 * q) << 16);
+  const uint32_t my_meta = meta + 4 * s;
 
-  if (w == CWARPS) {  // ---- MMA warp ----
-    // kind::tf32, D fp32, A / B tf32 K-major, N = 32, M = 128
+  if (w == 2 * CWARPS) {  // ---- MMA warp ----
+    // MMA issue for batch m (warp 8, lane 0): D = A_lo Bt_hi +
+    // A_hi Bt_lo + A_hi Bt_hi once every producer arrived (a_ready) and every consumer read the
+    // stage's previous D (d_free of batch m - 4); kind::tf32, D fp32, A (TMEM) / B (smem) tf32
+    // K-major, N = 32, M = 128
     const uint32_t idesc =
-        (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+        (1u << 4) | (2u << 7) | (2u << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
     const int ksteps = (R + 7) >> 3;
-    const uint32_t bh = su32(b_hi), bl = su32(b_lo);
-    for (int b = 0; b < nb; ++b) {
-      const int st = b & 1;
-      mbar_wait(a_ready + st, (b >> 1) & 1);
+    auto mma_issue = [&](int m) {
+      const int ast = m % AS, dst = m % DS;
+      mbar_wait(a_ready + ast, (m / AS) & 1);
+      if (m >= DS) mbar_wait(d_free + dst, (m / DS - 1) & 1);
       tc_fence_after();
-      if (lane == 0) {
-        const uint32_t ah = tmem + TCOLS * st, al = ah + 32, d = ah + 64;
-        for (int k = 0; k < ksteps; ++k) {
-          mma_ts(d, al + 8 * k, sw128(bh + 32 * k), idesc, k > 0);
-          mma_ts(d, ah + 8 * k, sw128(bl + 32 * k), idesc, 1);
-          mma_ts(d, ah + 8 * k, sw128(bh + 32 * k), idesc, 1);
-        }
-        asm volatile(
-            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                su32(v_ready + st))
-            : "memory");
-      }
+      const uint32_t ah = tmem + 64 * ast, al = ah + 32, d = tmem + 64 * AS + 64 * dst;
+      for (int k = 0; k < ksteps; ++k) mma_ts(d, ah + 8 * k, sw128(b_hi + 32 * k), idesc, k > 0);
+      for (int k = 0; k < ksteps; ++k) mma_ts(d, al + 8 * k, sw128(b_lo + 32 * k), idesc, 1);
+      asm volatile(
+          "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+              su32(a_free + ast))
+          : "memory");
+      asm volatile(
+          "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+              su32(v_ready + dst))
+          : "memory");
+    };
+    for (int m = 0; m < nb; ++m) {
+      if (lane == 0) mma_issue(m);
       __syncwarp();
     }
-  } else {  // ---- consumer warps: slot s = TMEM lane s = this thread ----
-    const int s = tid;
-    const uint32_t tlane = tmem + ((uint32_t)(32 * w) << 16);
-    const int64_t gslots = (int64_t)gridDim.x * SLOTS;
-    const float lr = p.lr, cdec = -p.lr * p.reg;
+  } else if (w < CWARPS) {  // ---- producers: metadata, gathers, cross -> TMEM A ----
     const int gc = lane & 7, gs = lane >> 3;
-    const bool gok = gc < (R >> 2);
+    const bool gok = R32 || gc < (R >> 2);
+    // gather copy geometry: copy `it` of a level moves chunk gc of slot t = 4 it + gs of this
+    // warp; its swizzled chunk is gc ^ (t & 7) = gc ^ (gs + 4 (it & 1))
+    const uint32_t gdst0 = (uint32_t)((32 * q + gs) * 128 + ((gc ^ gs) << 4));
+    const uint32_t gdst1 = (uint32_t)((32 * q + gs + 4) * 128 + ((gc ^ (gs + 4)) << 4));
+    const uint32_t my_row = (uint32_t)(s * 128), swz = (uint32_t)(lane & 7);
+    const int32_t *src_lc = p.slot_lc + (b0 + 2 * GS - 1) * SLOTS + s;
+    const int32_t *src_pc = p.slot_pc + (b0 + 2 * GS - 1) * NPRE * SLOTS + s;
+    const float *src_x = p.slot_x + (b0 + 2 * GS - 1) * SLOTS + s;
+    const char *Cl[NPRE + 1];
+#pragma unroll
+    for (int lv = 0; lv < NPRE; ++lv) Cl[lv] = reinterpret_cast<const char *>(p.Cpre[lv]) + 16 * gc;
+    Cl[NPRE] = reinterpret_cast<const char *>(p.Cleaf) + 16 * gc;
+    const uint32_t rowb = (uint32_t)R * 4;
 
-    // Metadata of batch g (lc | flags, pc[NPRE], x of this lane's slot) -> meta ring stage
-    // g % MS by 4-B cp.async, requested 2 GS - 1 batches ahead so that it has landed (its group
-    // retired) before the gathers of batch g are issued: no load latency on the issue path.
-    auto request_meta = [&](int g) {
-      if (g < nb) {
-        const int64_t bb = b0 + g;
-        const uint32_t m0 = su32(meta + (g % P::MS) * P::MWORDS + s);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(m0),
-                     "l"(p.slot_lc + bb * SLOTS + s));
+    auto request_meta_at = [&](int g, const int32_t *lcp, const int32_t *pcp, const float *xp) {
+      const bool on = g < nb;
+      const uint32_t m0 = my_meta + (uint32_t)((g & (P::MS - 1)) * P::MSTRIDE);
+      cp4(m0, lcp, on);
 #pragma unroll
-        for (int d = 0; d < NPRE; ++d)
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(m0 + 4 * SLOTS * (1 + d)),
-                       "l"(p.slot_pc + (bb * NPRE + d) * SLOTS + s));
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(m0 + 4 * SLOTS * (1 + NPRE)),
-                     "l"(p.slot_x + bb * SLOTS + s));
-      }
+      for (int d = 0; d < NPRE; ++d) cp4(m0 + 4 * SLOTS * (1 + d), pcp + d * SLOTS, on);
+      cp4(m0 + 4 * SLOTS * (1 + NPRE), xp, on);
     };
-    auto meta_lc = [&](int g) { return meta[(g % P::MS) * P::MWORDS + s]; };
-    auto meta_x = [&](int g) { return meta[(g % P::MS) * P::MWORDS + (1 + NPRE) * SLOTS + s]; };
-    // gathers of batch g into ring stage g % GS (cooperative: 8 lanes per 128-B row)
+    // gathers of batch g into ring stage g % GS (cooperative: 8 lanes per 128-B row); padding
+    // slots copy row 0 (their cross is zeroed)
     auto issue = [&](int g) {
-      if (g < nb) {
-        const int lcf = meta_lc(g);
-        int coord[NPRE + 1];
+      if (g >= nb) return;  // warp-uniform
+      const uint32_t m0 = my_meta + (uint32_t)((g & (P::MS - 1)) * P::MSTRIDE);
+      const int lcf = (int)lds32(m0);
+      const bool pad = lcf == PAD;
+      uint32_t coord[NPRE + 1];
 #pragma unroll
-        for (int d = 0; d < NPRE; ++d)
-          coord[d] = lcf == PAD ? -1 : meta[(g % P::MS) * P::MWORDS + (1 + d) * SLOTS + s];
-        coord[NPRE] = lcf == PAD ? -1 : (int)((uint32_t)lcf & ~ROW_START);
-        const uint32_t st0 = su32(ring + (size_t)(g % GS) * P::STAGE);
+      for (int d = 0; d < NPRE; ++d) coord[d] = pad ? 0u : lds32(m0 + 4 * SLOTS * (1 + d));
+      coord[NPRE] = pad ? 0u : ((uint32_t)lcf & ~ROW_START);
+      const uint32_t st0 = ring + (uint32_t)((g & (GS - 1)) * P::STAGE);
 #pragma unroll
-        for (int lv = 0; lv <= NPRE; ++lv) {
-          const float *C = lv < NPRE ? p.Cpre[lv] : p.Cleaf;
+      for (int lv = 0; lv <= NPRE; ++lv) {
+        const uint32_t lbase = st0 + lv * (SLOTS * 128);
 #pragma unroll
-          for (int it = 0; it < 8; ++it) {
-            const int t = 4 * it + gs;  // slot (within the warp) this lane copies for
-            const int cs = __shfl_sync(FULL, coord[lv], t);
-            const int srow = 32 * w + t;
-            if (gok && cs >= 0)
-              cp16(st0 + (uint32_t)((lv * SLOTS + srow) * 128 + ((gc ^ (srow & 7)) << 4)),
-                   C + (int64_t)cs * R + 4 * gc);
-          }
+        for (int it = 0; it < 8; ++it) {
+          const uint32_t cs = __shfl_sync(FULL, coord[lv], 4 * it + gs);
+          const uint32_t dst = lbase + (it & 1 ? gdst1 : gdst0) + (it >> 1) * 1024;
+          const char *src = Cl[lv] + (R32 ? (size_t)cs * 128u : (size_t)cs * rowb);
+          if (R32)
+            cp16(dst, src);
+          else
+            cp16p(dst, src, gok);
         }
       }
     };
 
+    // prologue: metadata of batches 0 .. 2 GS - 2 (landed), gathers of batches 0 .. GS - 2
+#pragma unroll 1
+    for (int g = 0; g < 2 * GS - 1; ++g)
+      request_meta_at(g, p.slot_lc + (b0 + g) * SLOTS + s, p.slot_pc + (b0 + g) * NPRE * SLOTS + s,
+                      p.slot_x + (b0 + g) * SLOTS + s);
+    cp_commit();
+    cp_wait<0>();
+#pragma unroll 1
+    for (int g = 0; g < GS - 1; ++g) {
+      issue(g);
+      cp_commit();
+    }
+#pragma unroll 1
+    for (int b = 0; b < nb; ++b) {
+      // one group per batch (empty past the end keeps the count uniform): the metadata of
+      // batch b + 2 GS - 1 and the gathers of batch b + GS - 1, whose metadata retired with
+      // the group of batch b - GS
+      request_meta_at(b + 2 * GS - 1, src_lc, src_pc, src_x);
+      src_lc += SLOTS, src_pc += NPRE * SLOTS, src_x += SLOTS;
+      issue(b + GS - 1);
+      cp_commit();
+      cp_wait<GS - 1>();  // this lane's copies of batch b have landed
+      __syncwarp();       // ... and every lane's
+      const int st = b % AS;
+      const bool live = (int)lds32(my_meta + (uint32_t)((b & (P::MS - 1)) * P::MSTRIDE)) != PAD;
+      if (b >= AS) mbar_wait(a_free + st, (b / AS - 1) & 1);  // MMAs of batch b - AS done
+      tc_fence_after();
+      // cross of slot s -> 3xTF32 halves -> TMEM A stage st
+      const uint32_t st0 = ring + (uint32_t)((b & (GS - 1)) * P::STAGE) + my_row;
+      const uint32_t ah = tlane + 64 * st, al = ah + 32;
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {  // 8 columns per TMEM store
+        uint32_t hv[8], lv8[8];
+#pragma unroll
+        for (int qq = 0; qq < 2; ++qq) {
+          const int c = 2 * h + qq;
+          float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (live && (R32 || 4 * c < R)) {
+            const uint32_t co = (uint32_t)((c ^ swz) << 4);
+            x = lds128(st0 + co);
+#pragma unroll
+            for (int lv = 1; lv <= NPRE; ++lv) {
+              const float4 y = lds128(st0 + lv * (SLOTS * 128) + co);
+              const float2 p01 = f2fma(make_float2(x.x, x.y), make_float2(y.x, y.y), make_float2(0.f, 0.f));
+              const float2 p23 = f2fma(make_float2(x.z, x.w), make_float2(y.z, y.w), make_float2(0.f, 0.f));
+              x = make_float4(p01.x, p01.y, p23.x, p23.y);
+            }
+          }
+          const uint32_t h0 = hi_bits(x.x), h1 = hi_bits(x.y), h2 = hi_bits(x.z), h3 = hi_bits(x.w);
+          // lo = x - hi as one packed FMA per pair: hi * (-1) + x
+          const float2 l01 = f2fma(make_float2(__uint_as_float(h0), __uint_as_float(h1)),
+                                   make_float2(-1.f, -1.f), make_float2(x.x, x.y));
+          const float2 l23 = f2fma(make_float2(__uint_as_float(h2), __uint_as_float(h3)),
+                                   make_float2(-1.f, -1.f), make_float2(x.z, x.w));
+          hv[4 * qq] = h0, hv[4 * qq + 1] = h1, hv[4 * qq + 2] = h2, hv[4 * qq + 3] = h3;
+          lv8[4 * qq] = __float_as_uint(l01.x), lv8[4 * qq + 1] = __float_as_uint(l01.y);
+          lv8[4 * qq + 2] = __float_as_uint(l23.x), lv8[4 * qq + 3] = __float_as_uint(l23.y);
+        }
+        tmem_st8(ah + 8 * h, hv);
+        tmem_st8(al + 8 * h, lv8);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+      tc_fence_before();
+      __syncwarp();  // every lane's stores (and its reads of the ring stage) are done
+      if (lane == 0) mbar_arrive(a_ready + st);
+    }
+    cp_wait<0>();
+  } else {  // ---- consumers: slot s = TMEM lane s = this thread's row chain ----
+    const int64_t gslots = (int64_t)gridDim.x * SLOTS;
+    const float lr = p.lr, cdec = -p.lr * p.reg;
     float a[32], lo[32], na[32];
     int64_t row = (int64_t)blockIdx.x + (int64_t)gridDim.x * s;  // this slot's first row
     bool have = false;                                          // a holds a row
     int64_t cur_i = -1;
     // row coordinates run two rows ahead of the chain, the A row one row ahead, so a row
     // switch never waits on a dependent global load
-    int ci1 = row < p.nrows ? __ldg(p.row_coord + row) : -1;      // coordinate of `row`
-    int ci2 = row + gslots < p.nrows ? __ldg(p.row_coord + row + gslots) : -1;  // ... next
+    int ci1 = row < p.nrows ? __ldg(p.row_coord + row) : -1;
+    int ci2 = row + gslots < p.nrows ? __ldg(p.row_coord + row + gslots) : -1;
     auto load_row = [&](float (&dst)[32], int ci) {
       if (ci >= 0) {
         const float *ar = p.A + (int64_t)ci * J;
         if (J == 32) {
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
-            const float4 q = *reinterpret_cast<const float4 *>(ar + 4 * c);
-            dst[4 * c] = q.x, dst[4 * c + 1] = q.y, dst[4 * c + 2] = q.z, dst[4 * c + 3] = q.w;
+            const float4 qv = *reinterpret_cast<const float4 *>(ar + 4 * c);
+            dst[4 * c] = qv.x, dst[4 * c + 1] = qv.y, dst[4 * c + 2] = qv.z, dst[4 * c + 3] = qv.w;
           }
         } else {
 #pragma unroll
@@ -330,16 +452,27 @@ __global__ void __launch_bounds__(THREADS, 1) factor_rows_tc_kernel(const TcPara
 #pragma unroll
     for (int j = 0; j < 32; ++j) a[j] = 0.f, lo[j] = 0.f, na[j] = 0.f;
     load_row(na, ci1);  // the first row's values, installed at its first leaf
-
-    // the chain of batch b (its v is in TMEM stage b & 1)
-    auto chain = [&](int b, int2 m) {
-      const int st = b & 1;
-      mbar_wait(v_ready + st, (b >> 1) & 1);
+#pragma unroll 1
+    for (int b = 0; b < nb; ++b) {
+      const int st = b % DS;
+      mbar_wait(v_ready + st, (b / DS) & 1);
       tc_fence_after();
-      float v[32];
-      tmem_ld32(tlane + TCOLS * st + 64, v);
-      if (m.x == PAD) return;
-      if ((uint32_t)m.x & ROW_START) {
+      float v[32], v2[32];
+      tmem_ld32(tlane + 64 * AS + 64 * st, v);
+      tmem_ld32(tlane + 64 * AS + 64 * st + 32, v2);
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        const float2 t = f2add(make_float2(v[j], v[j + 1]), make_float2(v2[j], v2[j + 1]));
+        v[j] = t.x, v[j + 1] = t.y;
+      }
+      const uint32_t mb0 = my_meta + (uint32_t)((b & (P::MS - 1)) * P::MSTRIDE);
+      const int mlc = (int)lds32(mb0);
+      const float x = __uint_as_float(lds32(mb0 + 4 * SLOTS * (1 + NPRE)));
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(d_free + st);
+      if (mlc == PAD) continue;
+      if ((uint32_t)mlc & ROW_START) {
         if (have) {
           store_row();
           row += gslots;
@@ -352,7 +485,6 @@ __global__ void __launch_bounds__(THREADS, 1) factor_rows_tc_kernel(const TcPara
         for (int j = 0; j < 32; ++j) a[j] = na[j], lo[j] = 0.f;
         load_row(na, ci2);  // prefetch the slot's next row
       }
-      const float x = __int_as_float(m.y);
       float2 s2a = make_float2(0.f, 0.f), s2b = make_float2(0.f, 0.f);
 #pragma unroll
       for (int j = 0; j < 32; j += 4) {
@@ -375,77 +507,13 @@ __global__ void __launch_bounds__(THREADS, 1) factor_rows_tc_kernel(const TcPara
           a[j] = t.x, a[j + 1] = t.y;
         }
       }
-    };
-
-    // prologue: metadata of batches 0 .. 2 GS - 2 (landed), gathers of batches 0 .. GS - 2
-#pragma unroll 1
-    for (int g = 0; g < 2 * GS - 1; ++g) request_meta(g);
-    cp_commit();
-    cp_wait<0>();
-#pragma unroll 1
-    for (int g = 0; g < GS - 1; ++g) {
-      issue(g);
-      cp_commit();
     }
-    int2 mprev = make_int2(PAD, 0);  // (lc | flags, x) of the batch whose chain runs next
-#pragma unroll 1
-    for (int b = 0; b < nb; ++b) {
-      // one group per batch (empty past the end keeps the count uniform): the metadata of
-      // batch b + 2 GS - 1 and the gathers of batch b + GS - 1, whose metadata retired with
-      // the group of batch b - GS
-      request_meta(b + 2 * GS - 1);
-      issue(b + GS - 1);
-      cp_commit();
-      cp_wait<GS - 1>();  // this lane's copies of batch b have landed
-      __syncwarp();       // ... and every lane's
-      {  // cross of slot s -> 3xTF32 halves -> TMEM A stage (b & 1)
-        const int2 mb = make_int2(meta_lc(b), meta_x(b));
-        const int m0 = mb.x;
-        const uint8_t *st0 = ring + (size_t)(b % GS) * P::STAGE;
-        const uint32_t ah = tlane + TCOLS * (b & 1), al = ah + 32;
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {  // 8 columns per TMEM store
-          uint32_t hv[8], lv8[8];
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const int c = 2 * h + q;
-            float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (m0 != PAD && 4 * c < R) {
-              x = *reinterpret_cast<const float4 *>(st0 + s * 128 + ((c ^ (s & 7)) << 4));
-#pragma unroll
-              for (int lv = 1; lv <= NPRE; ++lv) {
-                const float4 y = *reinterpret_cast<const float4 *>(
-                    st0 + (lv * SLOTS + s) * 128 + ((c ^ (s & 7)) << 4));
-                x.x *= y.x, x.y *= y.y, x.z *= y.z, x.w *= y.w;
-              }
-            }
-            const float xs[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
-              const uint32_t hb = hi_bits(xs[t]);
-              hv[4 * q + t] = hb;
-              lv8[4 * q + t] = __float_as_uint(xs[t] - __uint_as_float(hb));
-            }
-          }
-          tmem_st8(ah + 8 * h, hv);
-          tmem_st8(al + 8 * h, lv8);
-        }
-        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-        tc_fence_before();
-        __syncwarp();  // every lane's stores (and its reads of the ring stage) are done
-        if (lane == 0) mbar_arrive(a_ready + (b & 1));
-        if (b > 0) chain(b - 1, mprev);
-        mprev = mb;
-      }
-    }
-    if (nb > 0) chain(nb - 1, mprev);
     if (have) store_row();
-    cp_wait<0>();
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tmem));
+  if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
 
 // ---- K1d: the slot layout ------------------------------------------------------------------
@@ -523,22 +591,23 @@ bool tc_enabled() {
   return on;
 }
 
-template <int NPRE, int GS>
-int launch_tc_t(const TcParams &q, int G, bool comp, cudaStream_t s) {
+template <int NPRE, int GS, bool R32, bool COMP>
+int launch_tc_k(const TcParams &q, int G, cudaStream_t s) {
   const size_t sm = TcPlan<NPRE, GS>::SMEM;
   static bool set = false;
   if (!set) {
-    cudaFuncSetAttribute(factor_rows_tc_kernel<NPRE, GS, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaFuncSetAttribute(factor_rows_tc_kernel<NPRE, GS, false>,
+    cudaFuncSetAttribute(factor_rows_tc_kernel<NPRE, GS, R32, COMP>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     set = true;
   }
-  if (comp)
-    factor_rows_tc_kernel<NPRE, GS, true><<<G, THREADS, sm, s>>>(q);
-  else
-    factor_rows_tc_kernel<NPRE, GS, false><<<G, THREADS, sm, s>>>(q);
+  factor_rows_tc_kernel<NPRE, GS, R32, COMP><<<G, THREADS, sm, s>>>(q);
   return check_launch("ft_factor_sweep_rows(tcgen05)");
+}
+template <int NPRE, int GS>
+int launch_tc_t(const TcParams &q, int G, bool comp, cudaStream_t s) {
+  if (q.R == 32)
+    return comp ? launch_tc_k<NPRE, GS, true, true>(q, G, s) : launch_tc_k<NPRE, GS, true, false>(q, G, s);
+  return comp ? launch_tc_k<NPRE, GS, false, true>(q, G, s) : launch_tc_k<NPRE, GS, false, false>(q, G, s);
 }
 
 }  // namespace
@@ -571,16 +640,16 @@ int launch_factor_tc(const ft_tree_t *t, const ft_model_t *m, float lr, float re
   q.reg = reg;
   for (int d = 0; d < N; ++d)
     if (d != u && !m->dots[d]) return fail(FT_ERR_ARG, "dots[%d] is null", d);
-  // the Fast2Sum residue when rows are long (tens of thousands of serial updates drift ~1e-4
-  // in plain fp32; tests/test_netflix_parity_gpu.py)
+  // the Fast2Sum residue when rows are long: 46 K serial updates drift ~1e-4 from fp64 in plain
+  // fp32 (tests/test_netflix_parity_gpu.py); below 8 K per row the plain chain stays < 2e-5
   static const int force_comp = [] {  // FT_TC_COMP=0/1 forces the form (tests)
     const char *e = getenv("FT_TC_COMP");
     return e ? (strcmp(e, "0") == 0 ? 0 : 1) : -1;
   }();
   const bool comp = force_comp >= 0 ? force_comp == 1
-                                    : t->num_rows > 0 && t->nnz / t->num_rows > 1024;
-  if (N == 3) return launch_tc_t<1, 5>(q, t->slot_grid, comp, s);
-  return launch_tc_t<2, 3>(q, t->slot_grid, comp, s);
+                                    : t->num_rows > 0 && t->nnz / t->num_rows > 8192;
+  if (N == 3) return launch_tc_t<1, 4>(q, t->slot_grid, comp, s);
+  return launch_tc_t<2, 2>(q, t->slot_grid, comp, s);
 }
 
 }  // namespace ft

@@ -2,7 +2,7 @@
 set -x
 timeout 900 python -m pytest tests/test_factor_tc_gpu.py -x -q > gpurun_out/tc_tests.log 2>&1; echo tc_tests $?
 tail -25 gpurun_out/tc_tests.log
-timeout 600 python bench.py --no-cpu --no-e2e > gpurun_out/tc_bench_on.json 2> gpurun_out/tc_bench_on.err; echo on $?
+FT_TC_COMP=0 timeout 600 python bench.py --no-cpu --no-e2e > gpurun_out/tc_bench_on.json 2> gpurun_out/tc_bench_on.err; echo on $?
 FT_FACTOR_TC=0 timeout 600 python bench.py --no-cpu --no-e2e > gpurun_out/tc_bench_off.json 2> gpurun_out/tc_bench_off.err; echo off $?
 tail -3 gpurun_out/tc_bench_on.err
 python - <<'PY'
@@ -15,3 +15,6 @@ for k in ("on", "off"):
     except Exception as e:
         print(k, "failed", e)
 PY
+ncu --set full --clock-control none --import-source on -k regex:"factor_rows_tc" --launch-skip 4 -c 1 \
+  -o gpurun_out/tc_one -f python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e --no-ncu > gpurun_out/tc_one.log 2>&1
+echo ncu $?

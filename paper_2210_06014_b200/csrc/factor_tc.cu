@@ -163,7 +163,8 @@ struct TcPlan {
   static constexpr int MS = 4 * GS > 16 ? 4 * GS : 16;
   static_assert(MS >= 2 * GS + AS + DS, "metadata ring too short");
   static constexpr int MSTRIDE = (NPRE + 2) * SLOTS * 4;  // lc|flags, pc[NPRE], x per stage
-  static constexpr size_t SMEM = 1024 + 2 * B_BYTES + (size_t)GS * STAGE + MS * MSTRIDE + 256;
+  static constexpr int NABUF = SLOTS * 128;              // each consumer's next A row
+  static constexpr size_t SMEM = 1024 + 2 * B_BYTES + (size_t)GS * STAGE + MS * MSTRIDE + NABUF + 256;
 };
 
 __device__ __forceinline__ uint32_t lds32(uint32_t a) {
@@ -207,7 +208,8 @@ __global__ void __launch_bounds__(THREADS, 1) factor_rows_tc_kernel(const TcPara
   const uint32_t b_hi = sbase, b_lo = sbase + P::B_BYTES;
   const uint32_t ring = sbase + 2 * P::B_BYTES;
   const uint32_t meta = ring + GS * P::STAGE;
-  const uint32_t bars = meta + P::MS * P::MSTRIDE;
+  const uint32_t nabuf = meta + P::MS * P::MSTRIDE;
+  const uint32_t bars = nabuf + P::NABUF;
   uint8_t *gbase = smraw + (sbase - sraw);
   uint64_t *a_ready = reinterpret_cast<uint64_t *>(gbase + (bars - sbase));
   uint64_t *a_free = a_ready + AS, *v_ready = a_free + AS, *d_free = v_ready + DS;
@@ -413,28 +415,42 @@ __global__ void __launch_bounds__(THREADS, 1) factor_rows_tc_kernel(const TcPara
   } else {  // ---- consumers: slot s = TMEM lane s = this thread's row chain ----
     const int64_t gslots = (int64_t)gridDim.x * SLOTS;
     const float lr = p.lr, cdec = -p.lr * p.reg;
-    float a[32], lo[32], na[32];
+    float a[32], lo[32];
     int64_t row = (int64_t)blockIdx.x + (int64_t)gridDim.x * s;  // this slot's first row
     bool have = false;                                          // a holds a row
     int64_t cur_i = -1;
-    // row coordinates run two rows ahead of the chain, the A row one row ahead, so a row
-    // switch never waits on a dependent global load
+    // row coordinates run two rows ahead of the chain and the next row's A values are copied
+    // into this thread's shared-memory buffer one row ahead (cp.async: no registers held), so
+    // a row switch never waits on a global load
     int ci1 = row < p.nrows ? __ldg(p.row_coord + row) : -1;
     int ci2 = row + gslots < p.nrows ? __ldg(p.row_coord + row + gslots) : -1;
-    auto load_row = [&](float (&dst)[32], int ci) {
+    const uint32_t my_na = nabuf + (uint32_t)(s * 128);
+    auto prefetch_row = [&](int ci) {
       if (ci >= 0) {
         const float *ar = p.A + (int64_t)ci * J;
         if (J == 32) {
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const float4 qv = *reinterpret_cast<const float4 *>(ar + 4 * c);
-            dst[4 * c] = qv.x, dst[4 * c + 1] = qv.y, dst[4 * c + 2] = qv.z, dst[4 * c + 3] = qv.w;
-          }
+          for (int c = 0; c < 8; ++c) cp16(my_na + 16 * c, ar + 4 * c);
         } else {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) dst[j] = j < J ? ar[j] : 0.f;
+          for (int j = 0; j < J; ++j) cp4(my_na + 4 * j, ar + j, true);
         }
       }
+      cp_commit();
+    };
+    auto install_row = [&]() {
+      cp_wait<0>();
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float4 q4 = lds128(my_na + 16 * c);
+        a[4 * c] = q4.x, a[4 * c + 1] = q4.y, a[4 * c + 2] = q4.z, a[4 * c + 3] = q4.w;
+      }
+      if (J < 32) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j >= J) a[j] = 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) lo[j] = 0.f;
     };
     auto store_row = [&]() {
       float *ar = p.A + cur_i * J;
@@ -450,8 +466,8 @@ __global__ void __launch_bounds__(THREADS, 1) factor_rows_tc_kernel(const TcPara
       }
     };
 #pragma unroll
-    for (int j = 0; j < 32; ++j) a[j] = 0.f, lo[j] = 0.f, na[j] = 0.f;
-    load_row(na, ci1);  // the first row's values, installed at its first leaf
+    for (int j = 0; j < 32; ++j) a[j] = 0.f, lo[j] = 0.f;
+    prefetch_row(ci1);  // the first row's values, installed at its first leaf
 #pragma unroll 1
     for (int b = 0; b < nb; ++b) {
       const int st = b % DS;
@@ -481,9 +497,8 @@ __global__ void __launch_bounds__(THREADS, 1) factor_rows_tc_kernel(const TcPara
         }
         have = true;
         cur_i = ci1;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) a[j] = na[j], lo[j] = 0.f;
-        load_row(na, ci2);  // prefetch the slot's next row
+        install_row();
+        prefetch_row(ci2);  // the slot's next row
       }
       float2 s2a = make_float2(0.f, 0.f), s2b = make_float2(0.f, 0.f);
 #pragma unroll

@@ -2,7 +2,7 @@
 set -x
 timeout 900 python -m pytest tests/test_factor_tc_gpu.py -x -q > gpurun_out/tc_tests.log 2>&1; echo tc_tests $?
 tail -25 gpurun_out/tc_tests.log
-FT_TC_COMP=0 timeout 600 python bench.py --no-cpu --no-e2e > gpurun_out/tc_bench_on.json 2> gpurun_out/tc_bench_on.err; echo on $?
+timeout 600 python bench.py --no-cpu --no-e2e > gpurun_out/tc_bench_on.json 2> gpurun_out/tc_bench_on.err; echo on $?
 FT_FACTOR_TC=0 timeout 600 python bench.py --no-cpu --no-e2e > gpurun_out/tc_bench_off.json 2> gpurun_out/tc_bench_off.err; echo off $?
 tail -3 gpurun_out/tc_bench_on.err
 python - <<'PY'

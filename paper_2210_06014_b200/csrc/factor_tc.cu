@@ -593,8 +593,10 @@ __global__ void slot_fill_kernel(const int32_t *__restrict__ row_leaf_ptr, int64
   }
 }
 
+// R > 16: at R = 16 the MMA count per batch halves but its fixed cost does not, and quadr's
+// mma.sync combine is faster (Netflix16 modes 0/1: 2.3 vs 3.5 ms; profiles/r02_factor_tc_ab.md)
 bool tc_shape_ok(int N, int J, int R) {
-  return N >= 3 && N <= 4 && J >= 1 && J <= 32 && R >= 4 && R <= 32 && R % 4 == 0;
+  return N >= 3 && N <= 4 && J >= 1 && J <= 32 && R > 16 && R <= 32 && R % 4 == 0;
 }
 
 // FT_FACTOR_TC=0 disables the tcgen05 factor sweep (the quadr / quadw kernels run instead)
@@ -627,9 +629,10 @@ int launch_tc_t(const TcParams &q, int G, bool comp, cudaStream_t s) {
 
 }  // namespace
 
-// rows the tcgen05 sweep needs to fill the GPU (one 128-slot CTA per SM); fewer long rows
-// (Netflix mode 2) keep the warp-level kernels
-int64_t tc_min_rows() { return (int64_t)sm_count() * SLOTS / 2; }
+// rows the tcgen05 sweep needs to fill the GPU (one 128-slot CTA per SM, >= 90 % of the SMs
+// busy); fewer, longer rows (Netflix mode 2; order-4 10K^4: 10 K rows would fill 79 of 148 SMs,
+// 38.2 vs 28.7 ms with quadr) keep the warp-level kernels
+int64_t tc_min_rows() { return (int64_t)sm_count() * SLOTS * 9 / 10; }
 
 // Called by ft_factor_sweep_rows (sweep.cu) before its own dispatch: returns -1 when the
 // tcgen05 sweep does not apply to this tree (no slot layout, shape, FT_FACTOR_TC=0).

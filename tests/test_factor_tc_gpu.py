@@ -2,11 +2,12 @@
 TMEM, one thread per row, slot layout K1d), against the fp64 oracle at the contract's rel 1e-4
 per sweep, and the slot layout itself against the tree it was built from.
 
-The default dispatch runs K3c on every tree with enough rows to fill the GPU (>= 64 per SM):
+The default dispatch runs K3c on trees with enough rows to fill the GPU (one 128-slot CTA on
+>= 90 % of the SMs) when 16 < R <= 32:
 each case below has at least one such mode; the other modes run quadr / quadw as usual, so
 every sweep of two epochs is checked.  Cases: short rows (1-3 leaves, J < 32 and R < 32
 padding, R % 8 = 4), more rows than slots (row switching inside a slot's stream), rows of
-hundreds of leaves, order 4 (two prefix levels), J = 16 / R = 12, and both chain forms
+a hundred leaves, order 4 (two prefix levels), J = 16 / R = 24, and both chain forms
 (plain fp32 and the Fast2Sum-compensated one, FT_TC_COMP).
 """
 
@@ -37,11 +38,11 @@ def ft():
 
 @pytest.mark.parametrize("dims,nnz,J,R,lr,comp", [
     ((20000, 700, 9), 300_000, 24, 20, 1e-3, "0"),    # 1-3 leaf rows, padding, R % 8 = 4
-    ((60000, 12000, 64), 1_000_000, 32, 32, 5e-3, "0"),  # two tc modes, row switching
-    ((12000, 300, 50), 2_000_000, 32, 32, 2e-3, "1"),  # ~170-leaf rows, compensated chain
-    ((12000, 300, 50), 2_000_000, 32, 32, 2e-3, "0"),
+    ((60000, 20000, 64), 1_000_000, 32, 32, 5e-3, "0"),  # two tc modes, row switching
+    ((20000, 300, 50), 2_000_000, 32, 32, 2e-3, "1"),  # ~100-leaf rows, compensated chain
+    ((20000, 300, 50), 2_000_000, 32, 32, 2e-3, "0"),
     ((20000, 10000, 30, 20), 600_000, 32, 32, 2e-3, "0"),  # order 4
-    ((15000, 300, 40), 400_000, 16, 12, 2e-3, "1"),   # J = 16, R = 12
+    ((20000, 300, 40), 400_000, 16, 24, 2e-3, "1"),   # J = 16, R = 24
 ])
 def test_tc_factor_sweeps_match_oracle(dims, nnz, J, R, lr, comp):
     code = _CASE.format(dims=dims, nnz=nnz, J=J, R=R, lr=lr, seed=11)

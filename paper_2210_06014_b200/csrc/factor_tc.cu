@@ -37,8 +37,11 @@ namespace ft {
 namespace {
 
 constexpr int SLOTS = 128;
-constexpr int CWARPS = 4;                    // warps per role: warp w <-> TMEM lanes 32(w%4)..+31
-constexpr int THREADS = (2 * CWARPS + 1) * 32;  // producers, consumers, the MMA warp
+constexpr int CWARPS = 4;                    // consumer warps: warp <-> TMEM lanes 32(w%4)..+31
+// PW producer warps per TMEM lane quadrant (they take alternate batches), 4 consumer warps, the
+// MMA warp
+template <int PW>
+constexpr int tc_threads() { return (4 * PW + CWARPS + 1) * 32; }
 // TMEM: AS A stages (A_hi | A_lo, 64 columns each) then DS D stages (64 columns each).  The A
 // ring is the deep one: a producer reuses an A stage once that batch's MMAs completed, so the
 // producers run up to AS batches ahead of the tensor core; consumers trail the MMA closely.
@@ -161,7 +164,7 @@ struct TcPlan {
   // metadata ring stages: requested 2 GS - 1 batches ahead of the producer, read by the
   // consumer up to AS + DS batches behind it (see the barrier chain in the kernel)
   static constexpr int MS = 4 * GS > 16 ? 4 * GS : 16;
-  static_assert(MS >= 2 * GS + AS + DS, "metadata ring too short");
+  static_assert(MS >= 2 * GS + AS + DS, "metadata ring too short");  // (2 GS - PW) + AS + DS + 1
   static constexpr int MSTRIDE = (NPRE + 2) * SLOTS * 4;  // lc|flags, pc[NPRE], x per stage
   static constexpr int NABUF = SLOTS * 128;              // each consumer's next A row
   static constexpr size_t SMEM = 1024 + 2 * B_BYTES + (size_t)GS * STAGE + MS * MSTRIDE + NABUF + 256;
@@ -198,8 +201,11 @@ __device__ __forceinline__ void cp16p(uint32_t dst, const void *src, bool on) {
 //   a_ready[st]  producers -> MMA   (A of batch b written)
 //   v_ready[st]  MMA commit -> consumers (D of batch b) and producers (A of batch b free again)
 //   d_free[st]   consumers -> MMA   (D of batch b read)
-template <int NPRE, int GS, bool R32, bool COMP>
-__global__ void __launch_bounds__(THREADS, 1) factor_rows_tc_kernel(const TcParams p) {
+template <int NPRE, int GS, bool R32, bool COMP, int PW>
+__global__ void __launch_bounds__(tc_threads<PW>(), 1) factor_rows_tc_kernel(const TcParams p) {
+  constexpr int THREADS = tc_threads<PW>(), NPW = 4 * PW;  // producer warps: 0 .. NPW - 1
+  static_assert(GS % PW == 0, "each producer parity owns GS / PW ring stages");
+  constexpr int D = GS / PW;                               // per-warp gather lookahead
   using P = TcPlan<NPRE, GS>;
   extern __shared__ __align__(1024) uint8_t smraw[];
   // 1024-B aligned operand tiles, addressed as shared-window offsets
@@ -263,7 +269,7 @@ __global__ void __launch_bounds__(THREADS, 1) factor_rows_tc_kernel(const TcPara
   const uint32_t tlane = tmem + ((uint32_t)(32 * q) << 16);
   const uint32_t my_meta = meta + 4 * s;
 
-  if (w == 2 * CWARPS) {  // ---- MMA warp ----
+  if (w == NPW + CWARPS) {  // ---- MMA warp ----
     // MMA issue for batch m (warp 8, lane 0): D = A_lo Bt_hi +
     // A_hi Bt_lo + A_hi Bt_hi once every producer arrived (a_ready) and every consumer read the
     // stage's previous D (d_free of batch m - 4); kind::tf32, D fp32, A (TMEM) / B (smem) tf32
@@ -292,7 +298,8 @@ __global__ void __launch_bounds__(THREADS, 1) factor_rows_tc_kernel(const TcPara
       if (lane == 0) mma_issue(m);
       __syncwarp();
     }
-  } else if (w < CWARPS) {  // ---- producers: metadata, gathers, cross -> TMEM A ----
+  } else if (w < NPW) {  // ---- producers: metadata, gathers, cross -> TMEM A ----
+    const int par = w >> 2;  // this warp's batches: par, par + PW, par + 2 PW, ...
     const int gc = lane & 7, gs = lane >> 3;
     const bool gok = R32 || gc < (R >> 2);
     // gather copy geometry: copy `it` of a level moves chunk gc of slot t = 4 it + gs of this
@@ -300,9 +307,11 @@ __global__ void __launch_bounds__(THREADS, 1) factor_rows_tc_kernel(const TcPara
     const uint32_t gdst0 = (uint32_t)((32 * q + gs) * 128 + ((gc ^ gs) << 4));
     const uint32_t gdst1 = (uint32_t)((32 * q + gs + 4) * 128 + ((gc ^ (gs + 4)) << 4));
     const uint32_t my_row = (uint32_t)(s * 128), swz = (uint32_t)(lane & 7);
-    const int32_t *src_lc = p.slot_lc + (b0 + 2 * GS - 1) * SLOTS + s;
-    const int32_t *src_pc = p.slot_pc + (b0 + 2 * GS - 1) * NPRE * SLOTS + s;
-    const float *src_x = p.slot_x + (b0 + 2 * GS - 1) * SLOTS + s;
+    // metadata requests run 2 D - 1 own batches (2 GS - PW batches) ahead of the cross
+    const int64_t mfirst = b0 + par + PW * (2 * D - 1);
+    const int32_t *src_lc = p.slot_lc + mfirst * SLOTS + s;
+    const int32_t *src_pc = p.slot_pc + mfirst * NPRE * SLOTS + s;
+    const float *src_x = p.slot_x + mfirst * SLOTS + s;
     const char *Cl[NPRE + 1];
 #pragma unroll
     for (int lv = 0; lv < NPRE; ++lv) Cl[lv] = reinterpret_cast<const char *>(p.Cpre[lv]) + 16 * gc;
@@ -345,28 +354,30 @@ __global__ void __launch_bounds__(THREADS, 1) factor_rows_tc_kernel(const TcPara
       }
     };
 
-    // prologue: metadata of batches 0 .. 2 GS - 2 (landed), gathers of batches 0 .. GS - 2
+    // prologue: metadata of own batches 0 .. 2 D - 2 (landed), gathers of own batches 0 .. D - 2
 #pragma unroll 1
-    for (int g = 0; g < 2 * GS - 1; ++g)
+    for (int i = 0; i < 2 * D - 1; ++i) {
+      const int g = par + PW * i;
       request_meta_at(g, p.slot_lc + (b0 + g) * SLOTS + s, p.slot_pc + (b0 + g) * NPRE * SLOTS + s,
                       p.slot_x + (b0 + g) * SLOTS + s);
+    }
     cp_commit();
     cp_wait<0>();
 #pragma unroll 1
-    for (int g = 0; g < GS - 1; ++g) {
-      issue(g);
+    for (int i = 0; i < D - 1; ++i) {
+      issue(par + PW * i);
       cp_commit();
     }
 #pragma unroll 1
-    for (int b = 0; b < nb; ++b) {
-      // one group per batch (empty past the end keeps the count uniform): the metadata of
-      // batch b + 2 GS - 1 and the gathers of batch b + GS - 1, whose metadata retired with
-      // the group of batch b - GS
-      request_meta_at(b + 2 * GS - 1, src_lc, src_pc, src_x);
-      src_lc += SLOTS, src_pc += NPRE * SLOTS, src_x += SLOTS;
-      issue(b + GS - 1);
+    for (int b = par; b < nb; b += PW) {
+      // one group per own batch (empty past the end keeps the count uniform): the metadata of
+      // own batch +2D-1 and the gathers of own batch +D-1, whose metadata retired with the
+      // group of own batch -D
+      request_meta_at(b + PW * (2 * D - 1), src_lc, src_pc, src_x);
+      src_lc += PW * SLOTS, src_pc += PW * NPRE * SLOTS, src_x += PW * SLOTS;
+      issue(b + PW * (D - 1));
       cp_commit();
-      cp_wait<GS - 1>();  // this lane's copies of batch b have landed
+      cp_wait<D - 1>();   // this lane's copies of batch b have landed
       __syncwarp();       // ... and every lane's
       const int st = b % AS;
       const bool live = (int)lds32(my_meta + (uint32_t)((b & (P::MS - 1)) * P::MSTRIDE)) != PAD;
@@ -608,23 +619,29 @@ bool tc_enabled() {
   return on;
 }
 
-template <int NPRE, int GS, bool R32, bool COMP>
+template <int NPRE, int GS, bool R32, bool COMP, int PW>
 int launch_tc_k(const TcParams &q, int G, cudaStream_t s) {
   const size_t sm = TcPlan<NPRE, GS>::SMEM;
   static bool set = false;
   if (!set) {
-    cudaFuncSetAttribute(factor_rows_tc_kernel<NPRE, GS, R32, COMP>,
+    cudaFuncSetAttribute(factor_rows_tc_kernel<NPRE, GS, R32, COMP, PW>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     set = true;
   }
-  factor_rows_tc_kernel<NPRE, GS, R32, COMP><<<G, THREADS, sm, s>>>(q);
+  factor_rows_tc_kernel<NPRE, GS, R32, COMP, PW><<<G, tc_threads<PW>(), sm, s>>>(q);
   return check_launch("ft_factor_sweep_rows(tcgen05)");
 }
+// the plain chain fits the 13-warp block's 128 registers (two producer warps per quadrant); the
+// compensated one (156 registers) keeps one producer warp per quadrant
+// (and so does a ring too shallow to give each of two warps a batch of lookahead)
 template <int NPRE, int GS>
 int launch_tc_t(const TcParams &q, int G, bool comp, cudaStream_t s) {
+  constexpr int PW2 = GS >= 4 ? 2 : 1;
   if (q.R == 32)
-    return comp ? launch_tc_k<NPRE, GS, true, true>(q, G, s) : launch_tc_k<NPRE, GS, true, false>(q, G, s);
-  return comp ? launch_tc_k<NPRE, GS, false, true>(q, G, s) : launch_tc_k<NPRE, GS, false, false>(q, G, s);
+    return comp ? launch_tc_k<NPRE, GS, true, true, 1>(q, G, s)
+                : launch_tc_k<NPRE, GS, true, false, PW2>(q, G, s);
+  return comp ? launch_tc_k<NPRE, GS, false, true, 1>(q, G, s)
+              : launch_tc_k<NPRE, GS, false, false, PW2>(q, G, s);
 }
 
 }  // namespace

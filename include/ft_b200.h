@@ -179,6 +179,14 @@ FT_API int ft_refresh(int64_t I, int32_t J, int32_t R, const float *A, const flo
  * fences (stream sync + barrier) before any rank reads the gathered C_u. */
 FT_API int ft_refresh_scatter(int64_t I, int32_t J, int32_t R, const float *A, const float *Bt,
                               float *const *dsts, int32_t ndst, uint32_t *guard, void *stream);
+/* Stream-ordered barrier for the fused refresh + all-gather: publishes `seq` into slot `rank` of
+ * every rank's flag array (peer_flags[q] = rank q's array, CUDA-IPC-mapped; world <= FT_MAX_PEERS
+ * uint32 slots each) after a system-scope fence, then waits on the device until every slot of
+ * local_flags holds >= seq.  Replaces a host synchronize + barrier between the refresh of C_u and
+ * the next sweep (no reference counterpart: the reference has no distributed path).
+ * Traps after 20 s if a peer never arrives. */
+FT_API int ft_peer_barrier(uint32_t *local_flags, uint32_t *const *peer_flags, int32_t world,
+                           int32_t rank, uint32_t seq, void *stream);
 
 /* K3b  Exact factor sweep of mode u = tree->root_mode: replaces factor_sweep over the tree
  * rooted at (u+1) mod N (_ckern.pyx:132-199, train.py:152-197).  One warp owns one row of A_u

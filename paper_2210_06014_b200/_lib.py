@@ -93,6 +93,8 @@ SIGNATURES = {
                                             _i64p, _vp]),
     "ft_refresh": (ctypes.c_int, [
         ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp, _vp, _vp]),
+    "ft_peer_barrier": (ctypes.c_int, [_vp, ctypes.POINTER(_vp), ctypes.c_int32, ctypes.c_int32,
+                                       ctypes.c_uint32, _vp]),
     "ft_refresh_scatter": (ctypes.c_int, [
         ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, _vp, _vp, ctypes.POINTER(_vp),
         ctypes.c_int32, _vp, _vp]),

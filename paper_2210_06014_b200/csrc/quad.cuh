@@ -143,38 +143,7 @@ __device__ __forceinline__ void quad_store_v(float *V, const float (&acc)[2][4][
     }
 }
 
-// as quad_store_v, with quarter q's 8 rows shifted by 4 q floats (lane-per-row readers of four
-// quarters then hit disjoint banks)
-__device__ __forceinline__ void quad_store_v_pad(float *V, const float (&acc)[2][4][4], int lane) {
-  using namespace quad;
-  const int gq = lane >> 2, tq = lane & 3;
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      float *v = V + (8 * nt + 2 * tq) * QVS + 4 * nt + 16 * mt + gq;
-      v[0] = acc[mt][nt][0];
-      v[QVS] = acc[mt][nt][1];
-      v[8] = acc[mt][nt][2];
-      v[QVS + 8] = acc[mt][nt][3];
-    }
-}
 
-// packed form for a chain in quadr's column layout: slot s's columns (g, g+8, g+16, g+24) as one
-// float4 at V + s * QVS + 8 (s / 8) + 4 g (one STS.128 per slot per lane instead of four STS.32;
-// the 8 (s / 8) shift keeps both the stores and the four rows' reads conflict-free)
-__device__ __forceinline__ void quad_store_v_packed(float *V, const float (&acc)[2][4][4], int lane) {
-  using namespace quad;
-  const int gq = lane >> 2, tq = lane & 3;
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-    for (int par = 0; par < 2; ++par) {
-      const int sl = 8 * nt + 2 * tq + par;
-      *reinterpret_cast<float4 *>(V + sl * QVS + 8 * nt + 4 * gq) =
-          make_float4(acc[0][nt][par], acc[0][nt][2 + par], acc[1][nt][par], acc[1][nt][2 + par]);
-    }
-}
 
 __device__ __forceinline__ void quad_zero(float (&acc)[2][4][4]) {
 #pragma unroll
@@ -296,158 +265,6 @@ __device__ __forceinline__ void quad_gather(const SweepParams &p, float *X, floa
   __syncwarp();
 }
 
-// AREG: the Bt^T fragments live in registers (64 per lane) instead of being re-read from shared
-// memory per batch -- the quad kernels are L1/shared-memory-bound (ncu L1 86-88 %), and the
-// per-batch fragment reads are ~20 % of that traffic; the register cost drops the block to 6 warps.
-template <bool SMALL, int WPBT, bool AREG, int NPRE>
-__global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quad_kernel(const SweepParams p) {
-  using namespace quad;
-  extern __shared__ float4 smem4[];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int q = lane >> 3, l = lane & 7;    // quarter (row stream), lane in quarter
-  const int gq = lane >> 2, tq = lane & 3;  // mma fragment coordinates
-  uint4 *afr = reinterpret_cast<uint4 *>(smem4);
-  float *X = reinterpret_cast<float *>(afr + BFRAG_U4) + w * quad::WARP_FLOATS;
-  float *Y = X + TILE;
-  float4 *meta = reinterpret_cast<float4 *>(Y + TILE);
-  float *V = X;  // V = cross * Bt_u overwrites X once the fragments are read
-  for (int k = lane; k < 2 * TILE; k += 32) X[k] = 0.f;  // Y's zero columns r >= R stay zero
-  quad_afrag_init(p, afr);
-  __syncthreads();
-  // m-tiles (j) / k-tiles (r) in use: compile-time (SMALL: J <= 16 and R <= 16), so the
-  // unrolled combine keeps no runtime guards; other shapes compute their zero padding
-  constexpr int mts = SMALL ? 1 : 2, nkt = SMALL ? 2 : 4;
-  uint4 AH[KT][MT], AL[KT][MT];
-  if (AREG) {
-#pragma unroll
-    for (int kt = 0; kt < KT; ++kt)
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        AH[kt][mt] = afr[(mt * KT + kt) * 32 + lane];
-        AL[kt][mt] = afr[KT * MT * 32 + (mt * KT + kt) * 32 + lane];
-      }
-  }
-
-  const int64_t nstream = (int64_t)gridDim.x * WPBT * 4;
-  // row streams are numbered block-fastest (stream = (4w + q) * grid + block), so the rows of a
-  // last, partial wave spread over all SMs instead of piling onto the first few blocks
-  int64_t row = (int64_t)(4 * w + q) * gridDim.x + blockIdx.x;
-  const int J = p.J;
-  const bool j32 = J == 32;
-  // current row (ci < 0: none) and the next row of this quarter's stream, one row ahead
-  int ci = -1, cL0 = 0, cLe = 0, ni = -1, nLb = 0, nLe = 0;
-  if (row < p.nrows) {
-    ci = __ldg(p.row_coord + row);
-    cL0 = __ldg(p.row_leaf_ptr + row);
-    cLe = __ldg(p.row_leaf_ptr + row + 1);
-  }
-  if (row + nstream < p.nrows) {
-    ni = __ldg(p.row_coord + row + nstream);
-    nLb = __ldg(p.row_leaf_ptr + row + nstream);
-    nLe = __ldg(p.row_leaf_ptr + row + nstream + 1);
-  }
-  float a[4] = {0.f, 0.f, 0.f, 0.f};
-  auto load_row = [&](int i) {
-    const float *ar = p.A + (int64_t)i * J;
-    if (j32) {
-      const float4 v = *reinterpret_cast<const float4 *>(ar + 4 * l);
-      a[0] = v.x, a[1] = v.y, a[2] = v.z, a[3] = v.w;
-    } else {
-#pragma unroll
-      for (int t = 0; t < 4; ++t) a[t] = 4 * l + t < J ? ar[4 * l + t] : 0.f;
-    }
-  };
-  auto store_row = [&](int i) {
-    float *ar = p.A + (int64_t)i * J;
-    if (j32) {
-      *reinterpret_cast<float4 *>(ar + 4 * l) = make_float4(a[0], a[1], a[2], a[3]);
-    } else {
-#pragma unroll
-      for (int t = 0; t < 4; ++t)
-        if (4 * l + t < J) ar[4 * l + t] = a[t];
-    }
-  };
-  if (ci >= 0) load_row(ci);
-  // leaf data of the batch about to run (prefetched one batch ahead; lanes past it: 0)
-  int plc = 0, ppc[NPRE];
-  float px = 0.f;
-#pragma unroll
-  for (int d = 0; d < NPRE; ++d) ppc[d] = 0;
-  if (ci >= 0 && cL0 + l < cLe) {
-    plc = __ldcs(p.leaf_coord + cL0 + l);
-#pragma unroll
-    for (int d = 0; d < NPRE; ++d) ppc[d] = __ldcs(p.leaf_pc + (int64_t)(cL0 + l) * NPRE + d);
-    px = __ldcs(p.vals + cL0 + l);
-  }
-  const float lr = p.lr;
-
-  for (;;) {
-    // ---- a quarter whose row is exhausted writes it back and moves to its next row ----
-    if (ci >= 0 && cL0 >= cLe) {
-      store_row(ci);
-      row += nstream;
-      ci = ni, cL0 = nLb, cLe = nLe;
-      if (ci >= 0) {
-        load_row(ci);  // consumed by the chain, after this batch's gathers and MMA
-        const int64_t r2 = row + nstream;
-        if (r2 < p.nrows) {
-          ni = __ldg(p.row_coord + r2);
-          nLb = __ldg(p.row_leaf_ptr + r2);
-          nLe = __ldg(p.row_leaf_ptr + r2 + 1);
-        } else {
-          ni = -1;
-        }
-      }
-    }
-    if (!__any_sync(FULL, ci >= 0)) break;
-    const int nb = ci >= 0 ? min(QB, cLe - cL0) : 0;
-    const int lc = plc;
-    int pc[NPRE];
-#pragma unroll
-    for (int d = 0; d < NPRE; ++d) pc[d] = ppc[d];
-    const float lrk = l < nb ? lr : 0.f;
-    const float ck = -lrk * p.reg;
-    meta[q * MQ + l] = make_float4(l < nb ? px : 0.f, lrk, ck, ck);
-    {  // prefetch the next batch of this quarter (same row, or the next row's first leaves)
-      const bool same = cL0 + nb < cLe;
-      const int pos = same ? cL0 + nb : nLb, end = same ? cLe : nLe;
-      const bool ok = ci >= 0 && (same || ni >= 0) && pos + l < end;
-      plc = ok ? __ldcs(p.leaf_coord + pos + l) : 0;
-#pragma unroll
-      for (int d = 0; d < NPRE; ++d)
-        ppc[d] = ok ? __ldcs(p.leaf_pc + (int64_t)(pos + l) * NPRE + d) : 0;
-      px = ok ? __ldcs(p.vals + pos + l) : 0.f;
-    }
-    // ---- gathers: slot s = 4 it + gs holds the leaf of lane s (quarter s / 8) ----
-    quad_gather<NPRE, XS>(p, X, Y, pc, lc, lane);
-    // ---- V^T = Bt_u^T * (X * Y)^T, 3xTF32 ----
-    float acc[2][4][4];
-    quad_zero(acc);
-#pragma unroll
-    for (int kt = 0; kt < KT; ++kt) {
-      if (kt >= nkt) break;
-      if (AREG)
-        quad_mma_kt_r<NT>(X, Y, AH[kt], AL[kt], kt, 0, lane, acc, mts);
-      else
-        quad_mma_kt<NT>(X, Y, afr, kt, 0, lane, acc, mts);
-    }
-    __syncwarp();  // every lane's fragments are read before V overwrites X
-    quad_store_v(V, acc, lane);
-    __syncwarp();
-    // ---- four serial chains (one per quarter): lane l holds columns 4l .. 4l+3 ----
-    const int nbmax = __reduce_max_sync(FULL, (unsigned)nb);
-    const float *Vq = V + 8 * q * QVS + 4 * l;
-    const float4 *mq = meta + q * MQ;
-#pragma unroll
-    for (int k = 0; k < QB; ++k) {
-      if (k >= nbmax) break;
-      quad_chain_step(a, Vq + k * QVS, mq[k]);
-    }
-    __syncwarp();  // V / meta reads done before the next batch's gathers and meta stores
-    cL0 += nb;
-  }
-}
-
 // ---- K3b "quadr": quad with the combine's output consumed straight from the MMA registers --
 // quad stages V through shared memory to turn the Vᵀ fragments into lanes-over-columns rows
 // (32 STS + 8 LDS.128 per batch on an L1 / shared-memory pipe that ncu shows at 84-88 %).
@@ -527,7 +344,7 @@ __device__ __forceinline__ void quadr_direct_combine(const SweepParams &p, const
   }
 }
 
-template <bool SMALL, int NPRE, int WPBT, bool TMA = false, bool DIRECT = false>
+template <bool SMALL, int NPRE, int WPBT>
 __global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quadr_kernel(const SweepParams p) {
   using namespace quad;
   extern __shared__ float4 smem4[];
@@ -540,15 +357,8 @@ __global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quadr_kernel(const S
   float *Y = X + TILE;
   float4 *meta = reinterpret_cast<float4 *>(Y + TILE);
   for (int k = lane; k < 2 * TILE; k += 32) X[k] = 0.f;
-  // TMA: one bulk copy per C row (cp.async.bulk, completion on a per-warp mbarrier) instead of
-  // eight 16-B cp.async per row -- the copies bypass the LSU / L1 request path entirely
-  uint64_t *bar = reinterpret_cast<uint64_t *>(reinterpret_cast<float *>(afr + BFRAG_U4) +
-                                               WPBT * quad::WARP_FLOATS) + w;
-  uint32_t tphase = 0;
-  if (TMA && lane == 0) mbar_init(bar, 1);
-  quad_afrag_init<DIRECT ? (SMALL ? 4 : 8) : 0>(p, afr);
+  quad_afrag_init<SMALL ? 4 : 8>(p, afr);
   __syncthreads();
-  constexpr int mts = SMALL ? 1 : 2, nkt = SMALL ? 2 : 4;
 
   const int64_t nstream = (int64_t)gridDim.x * WPBT * 4;
   int64_t row = (int64_t)(4 * w + rho) * gridDim.x + blockIdx.x;
@@ -638,29 +448,7 @@ __global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quadr_kernel(const S
     }
     float acc[2][4][4];
     quad_zero(acc);
-    if (DIRECT) {
-      quadr_direct_combine<SMALL, NPRE>(p, pc, lc, nb, lane, afr, acc);
-    } else {
-    if (TMA) {  // NPRE == 1 (order 3): lane = slot
-      const uint32_t rb = (uint32_t)p.R * 4;
-      fence_proxy_async();  // the previous batch's generic reads of X / Y precede the async writes
-      __syncwarp();
-      if (lane == 0) mbar_expect_tx(bar, 64 * rb);
-      __syncwarp();
-      bulk_copy(X + lane * XS, p.Cpre[0] + (int64_t)pc[0] * p.R, rb, bar);
-      bulk_copy(Y + lane * XS, p.Cleaf + (int64_t)lc * p.R, rb, bar);
-      mbar_wait(bar, tphase);
-      tphase ^= 1;
-      __syncwarp();
-    } else {
-      quad_gather<NPRE, XS>(p, X, Y, pc, lc, lane);
-    }
-#pragma unroll
-    for (int kt = 0; kt < KT; ++kt) {
-      if (kt >= nkt) break;
-      quad_mma_kt<NT>(X, Y, afr, kt, 0, lane, acc, mts);
-    }
-    }
+    quadr_direct_combine<SMALL, NPRE>(p, pc, lc, nb, lane, afr, acc);
     __syncwarp();  // meta visible (its stores precede the gathers' waits)
     // ---- four serial chains on the accumulator registers ----
     const int nbmax = QUADR_FULL8 ? QB : __reduce_max_sync(FULL, (unsigned)nb);
@@ -692,17 +480,17 @@ __global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quadr_kernel(const S
   }
 }
 
-template <bool SMALL, int NPRE, int WPBT, bool TMA = false, bool DIRECT = false>
+template <bool SMALL, int NPRE, int WPBT>
 int launch_quadr_t(const SweepParams &q, cudaStream_t s) {
   const size_t sm = (size_t)quad::BFRAG_U4 * 16 + (size_t)WPBT * quad::WARP_FLOATS * 4 + WPBT * 8;
   static bool set = false;
   if (!set) {
-    cudaFuncSetAttribute(factor_rows_quadr_kernel<SMALL, NPRE, WPBT, TMA, DIRECT>,
+    cudaFuncSetAttribute(factor_rows_quadr_kernel<SMALL, NPRE, WPBT>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     set = true;
   }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quadr_kernel<SMALL, NPRE, WPBT, TMA, DIRECT>,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quadr_kernel<SMALL, NPRE, WPBT>,
                                                     WPBT * 32, sm) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
@@ -710,62 +498,20 @@ int launch_quadr_t(const SweepParams &q, cudaStream_t s) {
   const int64_t cap = (int64_t)sm_count() * per_sm;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
-  factor_rows_quadr_kernel<SMALL, NPRE, WPBT, TMA, DIRECT><<<(int)g, WPBT * 32, sm, s>>>(q);
+  factor_rows_quadr_kernel<SMALL, NPRE, WPBT><<<(int)g, WPBT * 32, sm, s>>>(q);
   return check_launch("ft_factor_sweep_rows(quadr)");
 }
 
+// 8 warps per block (128 registers, a 16-B spill) at order 3; at order 4 (two prefix rows per
+// slot) 6 warps at 162-168 registers, no spill (order-4 10K^4: 33.0 -> 28.7 ms per mode)
 int launch_quadr(const SweepParams &q, cudaStream_t s) {
   const bool small = q.J <= 16 && q.R <= 16;
-  if (q.tma && q.N == 3 && (q.R & 3) == 0)  // FT_GATHER=tma: bulk-copy gathers
-    return small ? launch_quadr_t<true, 1, quad::WPB, true>(q, s)
-                 : launch_quadr_t<false, 1, quad::WPB, true>(q, s);
-  // 9 warps per block when that fits all rows in one wave (see launch_quad)
-  const int64_t slots8 = (int64_t)sm_count() * 2 * quad::WPB * 4, slots9 = slots8 * 9 / 8;
-  const bool w9 = q.nrows > slots8 && q.nrows <= slots9;
-  static const int direct_env = [] {  // FT_QUADR_DIRECT=0 / 1 forces staged / direct
-    const char *e = getenv("FT_QUADR_DIRECT");
-    return e && e[0] ? (e[0] == '0' ? 0 : 1) : -1;
-  }();
-  const bool direct = direct_env != 0;
-  // direct, R > 16: 8 warps per block (128 registers, a 16-B spill) at order 3; at order 4
-  // (two prefix rows per slot) 6 warps at 162-168 registers, no spill (order-4 10K^4:
-  // 33.0 -> 28.7 ms per mode; Netflix32 order 3 at 6 warps: mode 1 4.30 -> 4.61 ms)
-  static const int dwpb_env = [] {
-    const char *e = getenv("FT_QUADR_WPB");
-    return e && e[0] ? atoi(e) : 0;
-  }();
-  const int dwpb = dwpb_env ? dwpb_env : (q.N == 4 ? 6 : 8);
-  if (direct) {
-    if (small) {
-      if (q.N == 4) return launch_quadr_t<true, 2, quad::WPB, false, true>(q, s);
-      return launch_quadr_t<true, 1, quad::WPB, false, true>(q, s);
-    }
-    if (dwpb == 6) {
-      if (q.N == 4) return launch_quadr_t<false, 2, 6, false, true>(q, s);
-      return launch_quadr_t<false, 1, 6, false, true>(q, s);
-    }
-    if (q.N == 4) return launch_quadr_t<false, 2, quad::WPB, false, true>(q, s);
-    return launch_quadr_t<false, 1, quad::WPB, false, true>(q, s);
-  }
-  if (q.N == 4) {
-    if (w9) return small ? launch_quadr_t<true, 2, 9>(q, s) : launch_quadr_t<false, 2, 9>(q, s);
-    return small ? launch_quadr_t<true, 2, quad::WPB>(q, s) : launch_quadr_t<false, 2, quad::WPB>(q, s);
-  }
-  if (w9) return small ? launch_quadr_t<true, 1, 9>(q, s) : launch_quadr_t<false, 1, 9>(q, s);
-  return small ? launch_quadr_t<true, 1, quad::WPB>(q, s) : launch_quadr_t<false, 1, quad::WPB>(q, s);
+  if (small)
+    return q.N == 4 ? launch_quadr_t<true, 2, quad::WPB>(q, s) : launch_quadr_t<true, 1, quad::WPB>(q, s);
+  return q.N == 4 ? launch_quadr_t<false, 2, 6>(q, s) : launch_quadr_t<false, 1, quad::WPB>(q, s);
 }
 
-// ---- K3b "quadp": the quad layout software-pipelined for FEW LONG ROWS --------------------
-// Netflix mode 2 has 2,182 rows of ~45 K serial updates: four rows per warp leave ~3.7 warps
-// per SM, too few to hide the gather -> MMA -> chain latencies by switching warps.  quadp
-// overlaps them inside each warp instead: in iteration t the warp
-//     issues the gathers of batch t+2 (double-buffered X/Y tiles),
-//     runs the chain of batch t (V tile, meta) INTERLEAVED step by step with the tensor-core
-//     combine of batch t+1 (registers), so the MMAs fill the shuffle latency of the chain,
-//     then stores V(t+1).
-// The per-quarter batch records (row, leaf range, row-start flag) run three batches ahead of
-// the chain; a row's A values are prefetched one batch before its first update and written
-// back after its last.  Arithmetic and order of updates are exactly those of `quad`.
+// Row-stream cursor and per-batch records shared by the quadw producers.
 namespace quadp {
 constexpr int WPB = 4;
 constexpr int WARP_FLOATS = 5 * quad::TILE + 4 * quad::MQ * 4;  // X[2], Y[2], V, meta
@@ -826,358 +572,6 @@ __device__ __forceinline__ Leaf load_leaf(const SweepParams &p, const Rec &r, in
 }
 }  // namespace quadp
 
-__global__ void __launch_bounds__(quadp::WPB * 32, 1) factor_rows_quadp_kernel(const SweepParams p) {
-  constexpr bool SMALL = false;
-  using namespace quad;
-  using quadp::Rec;
-  using quadp::Leaf;
-  extern __shared__ float4 smem4[];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int q = lane >> 3, l = lane & 7;
-  const int gq = lane >> 2, tq = lane & 3;
-  uint4 *afr = reinterpret_cast<uint4 *>(smem4);
-  float *base = reinterpret_cast<float *>(afr + BFRAG_U4) + w * quadp::WARP_FLOATS;
-  // tiles: X[set] = base + set * TILE, Y[set] = base + (2 + set) * TILE, V = base + 4 TILE
-  float *V = base + 4 * TILE;
-  float4 *meta = reinterpret_cast<float4 *>(base + 5 * TILE);
-  for (int k = lane; k < 4 * TILE; k += 32) base[k] = 0.f;
-  quad_afrag_init(p, afr);
-  __syncthreads();
-  // m-tiles (j) / k-tiles (r) in use: compile-time (SMALL: J <= 16 and R <= 16), so the
-  // unrolled combine keeps no runtime guards; other shapes compute their zero padding
-  constexpr int mts = SMALL ? 1 : 2, nkt = SMALL ? 2 : 4;
-
-  const int64_t nstream = (int64_t)gridDim.x * quadp::WPB * 4;
-  quadp::Cursor cur;
-  cur.row = (int64_t)(4 * w + q) * gridDim.x + blockIdx.x - nstream;  // before the first row
-  cur.i = -1, cur.L0 = cur.Le = 0;
-  quadp::load_row_info(p, cur.row + nstream, cur.ni, cur.nLb, cur.nLe);
-  const int J = p.J;
-  const bool j32 = J == 32;
-  auto load_a = [&](int i, float (&a)[4]) {
-    const float *ar = p.A + (int64_t)i * J;
-    if (j32) {
-      const float4 v = *reinterpret_cast<const float4 *>(ar + 4 * l);
-      a[0] = v.x, a[1] = v.y, a[2] = v.z, a[3] = v.w;
-    } else {
-#pragma unroll
-      for (int t = 0; t < 4; ++t) a[t] = 4 * l + t < J ? ar[4 * l + t] : 0.f;
-    }
-  };
-  auto store_a = [&](int i, const float (&a)[4]) {
-    float *ar = p.A + (int64_t)i * J;
-    if (j32) {
-      *reinterpret_cast<float4 *>(ar + 4 * l) = make_float4(a[0], a[1], a[2], a[3]);
-    } else {
-#pragma unroll
-      for (int t = 0; t < 4; ++t)
-        if (4 * l + t < J) ar[4 * l + t] = a[t];
-    }
-  };
-  const int gc = lane & 7, gs = lane >> 3;
-  const bool gok = gc < (p.R >> 2);
-  const float *cpre = p.Cpre[0] + 4 * gc, *cleaf = p.Cleaf + 4 * gc;
-  const int64_t Rs = p.R;
-  auto gather = [&](int set, const Leaf &d) {
-    const uint32_t xs = smem_u32(base + set * TILE + gs * XS + 4 * gc);
-    const uint32_t ys = smem_u32(base + (2 + set) * TILE + gs * XS + 4 * gc);
-#pragma unroll
-    for (int it = 0; it < 8; ++it) {
-      const int s = 4 * it + gs;
-      const int pcs = __shfl_sync(FULL, d.pc, s), lcs = __shfl_sync(FULL, d.lc, s);
-      if (gok) {
-        cp_async16_s(xs + it * 4 * XS * 4, cpre + pcs * Rs);
-        cp_async16_s(ys + it * 4 * XS * 4, cleaf + lcs * Rs);
-      }
-    }
-    cp_async_commit();
-  };
-  auto put_meta = [&](const Rec &r, float x) {
-    const float lrk = l < r.nb ? p.lr : 0.f;
-    const float ck = -lrk * p.reg;
-    meta[q * MQ + l] = make_float4(l < r.nb ? x : 0.f, lrk, ck, ck);
-  };
-
-  // ---- prologue: records of batches 0..2, gathers of 0 and 1, V(0) ----
-  Rec r0 = quadp::next_batch(p, cur, nstream);
-  const Leaf d0 = quadp::load_leaf(p, r0, l);
-  Rec r1 = quadp::next_batch(p, cur, nstream);
-  Leaf d1 = quadp::load_leaf(p, r1, l);
-  Rec r2 = quadp::next_batch(p, cur, nstream);
-  Leaf d2 = quadp::load_leaf(p, r2, l);
-  gather(0, d0);
-  gather(1, d1);
-  float a[4] = {0.f, 0.f, 0.f, 0.f}, an[4] = {0.f, 0.f, 0.f, 0.f};
-  int ai = r0.nb > 0 ? r0.i : -1;  // row whose values a holds
-  if (ai >= 0) load_a(ai, a);
-  if (r1.newrow && r1.nb > 0) load_a(r1.i, an);
-  float acc[2][4][4];
-  {
-    cp_async_wait_one();
-    __syncwarp();
-    quad_zero(acc);
-#pragma unroll
-    for (int kt = 0; kt < KT; ++kt)
-      if (kt < nkt) quad_mma_kt<NT>(base, base + 2 * TILE, afr, kt, 0, lane, acc, mts);
-    __syncwarp();
-    quad_store_v(V, acc, lane);
-    put_meta(r0, d0.x);
-    __syncwarp();
-  }
-  float x1 = d1.x;
-
-  for (int t = 0; __any_sync(FULL, r0.nb > 0); ++t) {
-    const int s1 = (t + 1) & 1;  // tile set of batch t+1 (batch t+2 reuses set t & 1)
-    gather(t & 1, d2);
-    const Rec r3 = quadp::next_batch(p, cur, nstream);
-    const Leaf d3 = quadp::load_leaf(p, r3, l);
-    cp_async_wait_one();  // batch t+1's tiles have landed
-    __syncwarp();
-    // ---- chain of batch t interleaved with the combine of batch t+1 ----
-    const float *Xs = base + s1 * TILE, *Ys = base + (2 + s1) * TILE;
-    const float *Vq = V + 8 * q * QVS + 4 * l;
-    const float4 *mq = meta + q * MQ;
-    quad_zero(acc);
-#pragma unroll
-    for (int k = 0; k < QB; ++k) {
-      quad_chain_step(a, Vq + k * QVS, mq[k]);
-      if ((k >> 1) < nkt) quad_mma_kt<2>(Xs, Ys, afr, k >> 1, 2 * (k & 1), lane, acc, mts);
-    }
-    __syncwarp();  // chain(t) done reading V / meta
-    quad_store_v(V, acc, lane);
-    put_meta(r1, x1);
-    // row hand-over: batch t+1 starts a new row -> write back the finished one, swap in its
-    // prefetched values; then prefetch the row batch t+2 starts (if it starts one)
-    if (r1.newrow && r1.nb > 0) {
-      if (ai >= 0) store_a(ai, a);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) a[u] = an[u];
-      ai = r1.i;
-    } else if (r1.nb == 0 && ai >= 0) {
-      store_a(ai, a);  // stream exhausted after batch t
-      ai = -1;
-    }
-    if (r2.newrow && r2.nb > 0) load_a(r2.i, an);
-    __syncwarp();
-    r0 = r1, r1 = r2, r2 = r3;
-    x1 = d2.x;
-    d2 = d3;
-  }
-  cp_async_wait_all();
-  if (ai >= 0) store_a(ai, a);
-}
-
-int launch_quadp(const SweepParams &q, cudaStream_t s) {
-  const size_t sm = quadp::bytes();
-  static bool set = false;
-  if (!set) {
-    cudaFuncSetAttribute(factor_rows_quadp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sm);
-    set = true;
-  }
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quadp_kernel,
-                                                    quadp::WPB * 32, sm) != cudaSuccess ||
-      per_sm < 1)
-    per_sm = 1;
-  int64_t g = (q.nrows + 4 * quadp::WPB - 1) / (4 * quadp::WPB);
-  const int64_t cap = (int64_t)sm_count() * per_sm;
-  if (g > cap) g = cap;
-  if (g < 1) g = 1;
-  factor_rows_quadp_kernel<<<(int)g, quadp::WPB * 32, sm, s>>>(q);
-  return check_launch("ft_factor_sweep_rows(quadp)");
-}
-
-// ---- K3b "quadrp": quadr software-pipelined inside each warp, for FEW LONG ROWS ---------------
-// With V consumed from registers (quadr), the chain of batch t and the combine of batch t+1 are
-// independent register streams; they are interleaved step by step (chain step k, then the MMAs
-// of k-tile k/2 for two n-tiles) so the tensor-core work fills the shuffle latency of the serial
-// chain.  Gathers run two batches ahead (double-buffered X/Y), the per-row batch records three
-// ahead (quadp's records, kept in the chain layout), a row's A values one batch before its
-// first update.  Meant for ~4 warps per SM (Netflix mode 2: 2,182 rows).
-template <bool SMALL>
-__global__ void __launch_bounds__(quadp::WPB * 32, 1) factor_rows_quadrp_kernel(const SweepParams p) {
-  using namespace quad;
-  using quadp::Rec;
-  extern __shared__ float4 smem4[];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int rho = lane & 3, gq = lane >> 2;
-  const int srho = (lane >> 1) & 3, sk = 2 * (lane >> 3) + (lane & 1);
-  constexpr int WF = 4 * TILE + 2 * 4 * MQ * 4;  // X[2], Y[2], meta[2] (4 rows x MQ float4)
-  uint4 *afr = reinterpret_cast<uint4 *>(smem4);
-  float *base = reinterpret_cast<float *>(afr + BFRAG_U4) + w * WF;
-  float4 *meta0 = reinterpret_cast<float4 *>(base + 4 * TILE);
-  for (int k = lane; k < 4 * TILE; k += 32) base[k] = 0.f;
-  quad_afrag_init(p, afr);
-  __syncthreads();
-  constexpr int mts = SMALL ? 1 : 2, nkt = SMALL ? 2 : 4;
-  const int64_t nstream = (int64_t)gridDim.x * quadp::WPB * 4;
-  quadp::Cursor cur;
-  cur.row = (int64_t)(4 * w + rho) * gridDim.x + blockIdx.x - nstream;
-  cur.i = -1, cur.L0 = cur.Le = 0;
-  quadp::load_row_info(p, cur.row + nstream, cur.ni, cur.nLb, cur.nLe);
-  const int J = p.J;
-  auto load_a = [&](int i, float (&a)[4]) {
-    const float *ar = p.A + (int64_t)i * J;
-#pragma unroll
-    for (int m = 0; m < 4; ++m) a[m] = gq + 8 * m < J ? ar[gq + 8 * m] : 0.f;
-  };
-  auto store_a = [&](int i, const float (&a)[4]) {
-    float *ar = p.A + (int64_t)i * J;
-#pragma unroll
-    for (int m = 0; m < 4; ++m)
-      if (gq + 8 * m < J) ar[gq + 8 * m] = a[m];
-  };
-  // leaf data of slot `lane` for a batch whose per-row records are r (chain layout)
-  struct SLeaf {
-    int lc, pc;
-    float x;
-    int nb;
-  };
-  auto load_leaf = [&](const Rec &r) {
-    SLeaf d{0, 0, 0.f, 0};
-    const int L0 = __shfl_sync(FULL, r.L0, srho), nb = __shfl_sync(FULL, r.nb, srho);
-    d.nb = nb;
-    if (sk < nb) {
-      d.lc = __ldcs(p.leaf_coord + L0 + sk);
-      d.pc = __ldcs(p.leaf_pc + L0 + sk);
-      d.x = __ldcs(p.vals + L0 + sk);
-    }
-    return d;
-  };
-  auto gather = [&](int set, const SLeaf &d) {
-    int pc1[1] = {d.pc};
-    const int gc = lane & 7, gs = lane >> 3;
-    const bool gok = gc < (p.R >> 2);
-    const int64_t Rs = p.R;
-    float *X = base + set * TILE, *Y = base + (2 + set) * TILE;
-    const uint32_t xs0 = smem_u32(X + gs * XS + 4 * gc), ys0 = smem_u32(Y + gs * XS + 4 * gc);
-#pragma unroll
-    for (int it = 0; it < 8; ++it) {
-      const int sl = 4 * it + gs;
-      const int pcs = __shfl_sync(FULL, pc1[0], sl), lcs = __shfl_sync(FULL, d.lc, sl);
-      if (gok) {
-        cp_async16_s(xs0 + it * 4 * XS * 4, p.Cpre[0] + 4 * gc + pcs * Rs);
-        cp_async16_s(ys0 + it * 4 * XS * 4, p.Cleaf + 4 * gc + lcs * Rs);
-      }
-    }
-    cp_async_commit();
-  };
-  auto put_meta = [&](int buf, const SLeaf &d) {
-    const float lrk = sk < d.nb ? p.lr : 0.f;
-    const float ck = -lrk * p.reg;
-    meta0[buf * MQ * 4 + srho * MQ + sk] = make_float4(sk < d.nb ? d.x : 0.f, lrk, ck, ck);
-  };
-
-  Rec r0 = quadp::next_batch(p, cur, nstream);
-  const SLeaf d0 = load_leaf(r0);
-  Rec r1 = quadp::next_batch(p, cur, nstream);
-  SLeaf d1 = load_leaf(r1);
-  Rec r2 = quadp::next_batch(p, cur, nstream);
-  SLeaf d2 = load_leaf(r2);
-  gather(0, d0);
-  gather(1, d1);
-  float a[4] = {0.f, 0.f, 0.f, 0.f}, an[4] = {0.f, 0.f, 0.f, 0.f};
-  int ai = r0.nb > 0 ? r0.i : -1;
-  if (ai >= 0) load_a(ai, a);
-  if (r1.newrow && r1.nb > 0) load_a(r1.i, an);
-  float acc[2][4][4], nacc[2][4][4];
-  cp_async_wait_one();
-  __syncwarp();
-  quad_zero(acc);
-#pragma unroll
-  for (int kt = 0; kt < KT; ++kt)
-    if (kt < nkt) quad_mma_kt<NT>(base, base + 2 * TILE, afr, kt, 0, lane, acc, mts);
-  put_meta(0, d0);
-
-  for (int t = 0; __any_sync(FULL, r0.nb > 0); ++t) {
-    const int s1 = (t + 1) & 1;
-    __syncwarp();  // set t&1 (batch t's tiles) fully read by its MMA before batch t+2 lands there
-    gather(t & 1, d2);
-    const Rec r3 = quadp::next_batch(p, cur, nstream);
-    const SLeaf d3 = load_leaf(r3);
-    cp_async_wait_one();  // batch t+1's tiles
-    put_meta(s1, d1);
-    __syncwarp();
-    const float *Xs = base + s1 * TILE, *Ys = base + (2 + s1) * TILE;
-    const float4 *mq = meta0 + (t & 1) * MQ * 4 + rho * MQ;
-    quad_zero(nacc);
-#pragma unroll
-    for (int k = 0; k < QB; ++k) {
-      {  // chain step k of batch t (accumulator registers)
-        const int nt = k >> 1, o = k & 1;
-        const float v0 = acc[0][nt][o], v1 = acc[0][nt][2 + o];
-        const float v2 = SMALL ? 0.f : acc[1][nt][o], v3 = SMALL ? 0.f : acc[1][nt][2 + o];
-        float2 pr = fmul2(make_float2(a[0], a[1]), make_float2(v0, v1));
-        pr = ffma2(make_float2(a[2], a[3]), make_float2(v2, v3), pr);
-        float sv = pr.x + pr.y;
-        sv += __shfl_xor_sync(FULL, sv, 4);
-        sv += __shfl_xor_sync(FULL, sv, 8);
-        sv += __shfl_xor_sync(FULL, sv, 16);
-        const float4 m = mq[k];
-        const float e = m.x - sv;
-        const float lre = m.y * e;
-        const float2 a01 = ffma2(make_float2(m.z, m.w), make_float2(a[0], a[1]), make_float2(a[0], a[1]));
-        const float2 a23 = ffma2(make_float2(m.z, m.w), make_float2(a[2], a[3]), make_float2(a[2], a[3]));
-        a[0] = __fmaf_rn(lre, v0, a01.x);
-        a[1] = __fmaf_rn(lre, v1, a01.y);
-        a[2] = __fmaf_rn(lre, v2, a23.x);
-        a[3] = __fmaf_rn(lre, v3, a23.y);
-      }
-      if ((k >> 1) < nkt) quad_mma_kt<2>(Xs, Ys, afr, k >> 1, 2 * (k & 1), lane, nacc, mts);
-    }
-    // row hand-over (chain layout): batch t+1 starts a new row -> write back, swap in
-    if (r1.newrow && r1.nb > 0) {
-      if (ai >= 0) store_a(ai, a);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) a[u] = an[u];
-      ai = r1.i;
-    } else if (r1.nb == 0 && ai >= 0) {
-      store_a(ai, a);
-      ai = -1;
-    }
-    if (r2.newrow && r2.nb > 0) load_a(r2.i, an);
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-        for (int u = 0; u < 4; ++u) acc[mt][nt][u] = nacc[mt][nt][u];
-    r0 = r1, r1 = r2, r2 = r3;
-    d1 = d2, d2 = d3;
-  }
-  cp_async_wait_all();
-  if (ai >= 0) store_a(ai, a);
-}
-
-template <bool SMALL>
-int launch_quadrp_t(const SweepParams &q, cudaStream_t s) {
-  const size_t sm = (size_t)quad::BFRAG_U4 * 16 +
-                    (size_t)quadp::WPB * (4 * quad::TILE + 2 * 4 * quad::MQ * 4) * 4;
-  static bool set = false;
-  if (!set) {
-    cudaFuncSetAttribute(factor_rows_quadrp_kernel<SMALL>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    set = true;
-  }
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quadrp_kernel<SMALL>,
-                                                    quadp::WPB * 32, sm) != cudaSuccess ||
-      per_sm < 1)
-    per_sm = 1;
-  int64_t g = (q.nrows + 4 * quadp::WPB - 1) / (4 * quadp::WPB);
-  const int64_t cap = (int64_t)sm_count() * per_sm;
-  if (g > cap) g = cap;
-  if (g < 1) g = 1;
-  factor_rows_quadrp_kernel<SMALL><<<(int)g, quadp::WPB * 32, sm, s>>>(q);
-  return check_launch("ft_factor_sweep_rows(quadrp)");
-}
-
-int launch_quadrp(const SweepParams &q, cudaStream_t s) {
-  return q.J <= 16 && q.R <= 16 ? launch_quadrp_t<true>(q, s) : launch_quadrp_t<false>(q, s);
-}
-
-
 // ---- K3b "quadw": the quad layout warp-specialised for FEW LONG ROWS ----------------------
 // A warp GROUP owns four rows (one per 8-lane quarter of its consumer warp).  Two PRODUCER
 // warps take alternate batches: each walks the rows' batch records, gathers its batch into its
@@ -1192,7 +586,7 @@ namespace quadw {
 constexpr int NS = 4;   // ring stages (producer k writes stages k, k+2)
 constexpr int NP = 2;   // producers per group
 // stage: V [32][QVS] | meta float4 [4][MQ] | info int4 [4] | A rows [4][32] | lr*G^T [4][8][8]
-constexpr int VREG = 32 * quad::QVS + 32;  // V (+32: the LPR / packed consumers' row shifts)
+constexpr int VREG = 32 * quad::QVS + 32;  // V tile
 constexpr int STAGE_FLOATS = VREG + 4 * quad::MQ * 4 + 4 * 4 + 4 * 32 + 4 * 64;
 // ring + X, Y per producer + the consumer's row exchange [4][32]
 constexpr int GROUP_FLOATS = NS * STAGE_FLOATS + NP * 2 * quad::TILE + 4 * 32;
@@ -1203,7 +597,7 @@ constexpr size_t bytes() {
 }
 }  // namespace quadw
 
-template <bool GRAM, bool SMALL, bool LPR = false, bool PV = false>
+template <bool SMALL>
 __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(const SweepParams p) {
   using namespace quad;
   using quadp::Leaf;
@@ -1243,9 +637,6 @@ __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(co
   };
   auto stage_a = [&](int st) {
     return ring + st * quadw::STAGE_FLOATS + quadw::VREG + 4 * MQ * 4 + 16;
-  };
-  auto stage_g = [&](int st) {  // lr * G^T: [q][l][m] = lr v_{8q+m} . v_{8q+l}
-    return ring + st * quadw::STAGE_FLOATS + quadw::VREG + 4 * MQ * 4 + 16 + 4 * 32;
   };
 
   if (w > 0) {
@@ -1329,34 +720,7 @@ __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(co
       if (t >= quadw::NS) mbar_wait(empty + st, ((t / quadw::NS) - 1) & 1);
       int4 *info = stage_info(st);
       if (!stop) {
-        if (LPR)
-          quad_store_v_pad(stage_v(st), acc, lane);
-        else if (PV)
-          quad_store_v_packed(stage_v(st), acc, lane);
-        else
-          quad_store_v(stage_v(st), acc, lane);
-        if (GRAM) {  // lane (q, l): lr G[m][l] = lr v_m . v_l over the quarter's batch, fp32
-          __syncwarp();
-          const float4 *vs = reinterpret_cast<const float4 *>(stage_v(st) + 8 * q * QVS);
-          float4 vl[8];
-#pragma unroll
-          for (int j4 = 0; j4 < 8; ++j4) vl[j4] = vs[l * (QVS / 4) + j4];
-          float gcol[8];
-#pragma unroll
-          for (int m = 0; m < 8; ++m) {
-            float2 g0 = make_float2(0.f, 0.f), g1 = g0;
-#pragma unroll
-            for (int j4 = 0; j4 < 8; ++j4) {
-              const float4 vm = vs[m * (QVS / 4) + j4];
-              g0 = ffma2(make_float2(vm.x, vm.y), make_float2(vl[j4].x, vl[j4].y), g0);
-              g1 = ffma2(make_float2(vm.z, vm.w), make_float2(vl[j4].z, vl[j4].w), g1);
-            }
-            gcol[m] = p.lr * ((g0.x + g0.y) + (g1.x + g1.y));
-          }
-          float4 *gd = reinterpret_cast<float4 *>(stage_g(st) + 64 * q + 8 * l);
-          gd[0] = make_float4(gcol[0], gcol[1], gcol[2], gcol[3]);
-          gd[1] = make_float4(gcol[4], gcol[5], gcol[6], gcol[7]);
-        }
+        quad_store_v(stage_v(st), acc, lane);
         const float lrk = l < r0.nb ? p.lr : 0.f;
         const float ck = -lrk * p.reg;
         stage_meta(st)[q * MQ + l] = make_float4(l < r0.nb ? d0.x : 0.f, lrk, ck, ck);
@@ -1373,144 +737,8 @@ __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(co
     cp_async_wait_all();
   } else {
     // ===================================== consumer =====================================
-    if (LPR) {
-      // lane-per-row: lane q (0..3; lanes 4..31 mirror them) holds its whole row in 32
-      // registers and computes s = a . v in-lane from the full V row -- no cross-lane
-      // reduction on the serial path; the next step's V row is loaded under the current step
-      const int qr = lane & 3;
-      float a[32];
-#pragma unroll
-      for (int jj = 0; jj < 32; ++jj) a[jj] = 0.f;
-      int ai = -1;
-      auto store_full = [&]() {
-        if (lane >= 4) return;
-        float *ar = p.A + (int64_t)ai * J;
-        if (j32) {
-#pragma unroll
-          for (int c = 0; c < 8; ++c)
-            reinterpret_cast<float4 *>(ar)[c] = make_float4(a[4 * c], a[4 * c + 1], a[4 * c + 2], a[4 * c + 3]);
-        } else {
-#pragma unroll
-          for (int jj = 0; jj < 32; ++jj)
-            if (jj < J) ar[jj] = a[jj];
-        }
-      };
-      for (int t = 0;; ++t) {
-        const int st = t % quadw::NS;
-        mbar_wait(full + st, (t / quadw::NS) & 1);
-        const int4 info = stage_info(st)[qr];
-        if (info.w) break;
-        if (info.y) {
-          if (ai >= 0) store_full();
-          const float4 *ar = reinterpret_cast<const float4 *>(stage_a(st) + 32 * qr);
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const float4 v = ar[c];
-            a[4 * c] = v.x, a[4 * c + 1] = v.y, a[4 * c + 2] = v.z, a[4 * c + 3] = v.w;
-          }
-          ai = info.z;
-        }
-        const float4 *Vr = reinterpret_cast<const float4 *>(stage_v(st) + 8 * qr * QVS + 4 * qr);
-        const float4 *mq = stage_meta(st) + qr * MQ;
-        float4 vc[8], vn[8];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) vc[c] = Vr[c];
-#pragma unroll
-        for (int kk = 0; kk < QB; ++kk) {
-          if (kk + 1 < QB) {
-#pragma unroll
-            for (int c = 0; c < 8; ++c) vn[c] = Vr[(kk + 1) * (QVS / 4) + c];
-          }
-          const float4 m = mq[kk];
-          float2 s0 = make_float2(0.f, 0.f), s1 = s0, s2 = s0, s3 = s0;
-#pragma unroll
-          for (int c = 0; c < 8; c += 2) {
-            s0 = ffma2(make_float2(a[4 * c], a[4 * c + 1]), make_float2(vc[c].x, vc[c].y), s0);
-            s1 = ffma2(make_float2(a[4 * c + 2], a[4 * c + 3]), make_float2(vc[c].z, vc[c].w), s1);
-            s2 = ffma2(make_float2(a[4 * c + 4], a[4 * c + 5]), make_float2(vc[c + 1].x, vc[c + 1].y), s2);
-            s3 = ffma2(make_float2(a[4 * c + 6], a[4 * c + 7]), make_float2(vc[c + 1].z, vc[c + 1].w), s3);
-          }
-          const float sv = ((s0.x + s0.y) + (s1.x + s1.y)) + ((s2.x + s2.y) + (s3.x + s3.y));
-          const float e = m.x - sv;  // (x, lr, -lr reg, -lr reg); lr = 0 on padding steps
-          const float lre = m.y * e;
-          const float2 c2 = make_float2(m.z, m.w), l2 = make_float2(lre, lre);
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            float2 lo = make_float2(a[4 * c], a[4 * c + 1]), hi = make_float2(a[4 * c + 2], a[4 * c + 3]);
-            lo = ffma2(l2, make_float2(vc[c].x, vc[c].y), ffma2(c2, lo, lo));
-            hi = ffma2(l2, make_float2(vc[c].z, vc[c].w), ffma2(c2, hi, hi));
-            a[4 * c] = lo.x, a[4 * c + 1] = lo.y, a[4 * c + 2] = hi.x, a[4 * c + 3] = hi.y;
-          }
-          if (kk + 1 < QB) {
-#pragma unroll
-            for (int c = 0; c < 8; ++c) vc[c] = vn[c];
-          }
-        }
-        __syncwarp();
-        mbar_arrive(empty + st);
-      }
-      if (ai >= 0) store_full();
-      return;
-    }
-    if (PV) {
-      // quadr's column layout: row rho = lane & 3 in lanes 4 g + rho, columns g, g+8, g+16, g+24;
-      // V rows come packed (one LDS.128 per step), the dot reduces over lane bits 2-4
-      const int rho = lane & 3, g = lane >> 2;
-      float a[4] = {0.f, 0.f, 0.f, 0.f};
-      int ai = -1;
-      auto store_r = [&]() {
-        float *ar = p.A + (int64_t)ai * J;
-#pragma unroll
-        for (int m = 0; m < 4; ++m)
-          if (g + 8 * m < J) ar[g + 8 * m] = a[m];
-      };
-      for (int t = 0;; ++t) {
-        const int st = t % quadw::NS;
-        mbar_wait(full + st, (t / quadw::NS) & 1);
-        const int4 info = stage_info(st)[rho];
-        if (info.w) break;
-        if (info.y) {
-          if (ai >= 0) store_r();
-          const float *ar = stage_a(st) + 32 * rho;
-#pragma unroll
-          for (int m = 0; m < 4; ++m) a[m] = ar[g + 8 * m];
-          ai = info.z;
-        }
-        const float *Vr = stage_v(st) + 8 * rho * QVS + 8 * rho + 4 * g;
-        const float4 *mq = stage_meta(st) + rho * MQ;
-        float4 vv[QB], mm[QB];
-#pragma unroll
-        for (int kk = 0; kk < QB; ++kk) {
-          vv[kk] = *reinterpret_cast<const float4 *>(Vr + kk * QVS);
-          mm[kk] = mq[kk];
-        }
-        __syncwarp();
-        mbar_arrive(empty + st);
-#pragma unroll
-        for (int kk = 0; kk < QB; ++kk) {
-          const float4 v = vv[kk], m = mm[kk];
-          float2 pr = fmul2(make_float2(a[0], a[1]), make_float2(v.x, v.y));
-          pr = ffma2(make_float2(a[2], a[3]), make_float2(v.z, v.w), pr);
-          float sv = pr.x + pr.y;
-          sv += __shfl_xor_sync(FULL, sv, 4);
-          sv += __shfl_xor_sync(FULL, sv, 8);
-          sv += __shfl_xor_sync(FULL, sv, 16);
-          const float e = m.x - sv;
-          const float lre = m.y * e;
-          const float2 a01 = ffma2(make_float2(m.z, m.w), make_float2(a[0], a[1]), make_float2(a[0], a[1]));
-          const float2 a23 = ffma2(make_float2(m.z, m.w), make_float2(a[2], a[3]), make_float2(a[2], a[3]));
-          a[0] = __fmaf_rn(lre, v.x, a01.x);
-          a[1] = __fmaf_rn(lre, v.y, a01.y);
-          a[2] = __fmaf_rn(lre, v.z, a23.x);
-          a[3] = __fmaf_rn(lre, v.w, a23.y);
-        }
-      }
-      if (ai >= 0) store_r();
-      return;
-    }
     float a[4] = {0.f, 0.f, 0.f, 0.f}, lo[4] = {0.f, 0.f, 0.f, 0.f};
     int ai = -1;
-    float *xrow = ring + quadw::NS * quadw::STAGE_FLOATS + quadw::NP * 2 * TILE + 32 * q;
     auto store_a = [&]() {
       float *ar = p.A + (int64_t)ai * J;
       const float o[4] = {a[0] + lo[0], a[1] + lo[1], a[2] + lo[2], a[3] + lo[3]};
@@ -1536,65 +764,21 @@ __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(co
       }
       const float *Vq = stage_v(st) + 8 * q * QVS + 4 * l;
       const float4 *mq = stage_meta(st) + q * MQ;
-      if (GRAM) {
-        // Gram form of the chain (exact restatement): lane l of the quarter tracks
-        // w_l = a_m . v_l while the batch's updates m = 0..7 are applied,
-        //   e_m = x_m - w_m,   w_l <- w_l - lr reg w_l + e_m (lr G[m][l]),
-        // so the serial dependency per update is one shuffle and one FMA; then the row is
-        // replayed a <- a - lr reg a + lr e_m v_m over its 4 columns per lane.
-        *reinterpret_cast<float4 *>(xrow + 4 * l) = make_float4(a[0], a[1], a[2], a[3]);
-        __syncwarp();
-        float w;  // d_l = a_0 . v_l: the full row against the lane's own leaf row
-        {
-          const float4 *ar = reinterpret_cast<const float4 *>(xrow);
-          const float4 *vr = reinterpret_cast<const float4 *>(stage_v(st) + (8 * q + l) * QVS);
-          float2 d0 = make_float2(0.f, 0.f), d1 = d0;
+      // the stage's 8 V rows and step operands are loaded up front (16 independent LDS.128,
+      // one latency) so the serial steps wait only on their own shuffles; short batches run
+      // all 8 steps (padding steps have lr = 0 and change nothing)
+      float4 vv[QB], mm[QB];
 #pragma unroll
-          for (int j4 = 0; j4 < 8; ++j4) {
-            const float4 av = ar[j4], vv = vr[j4];
-            d0 = ffma2(make_float2(av.x, av.y), make_float2(vv.x, vv.y), d0);
-            d1 = ffma2(make_float2(av.z, av.w), make_float2(vv.z, vv.w), d1);
-          }
-          w = (d0.x + d0.y) + (d1.x + d1.y);
-        }
-        const float4 *gq4 = reinterpret_cast<const float4 *>(stage_g(st) + 64 * q + 8 * l);
-        const float4 ga = gq4[0], gb = gq4[1];
-        const float gm[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
-        const float xl = mq[l].x, cdec = -p.lr * p.reg;
-        float e[8];
-#pragma unroll
-        for (int m = 0; m < 8; ++m) {
-          e[m] = __shfl_sync(FULL, xl - w, 8 * q + m);
-          w = __fmaf_rn(e[m], gm[m], __fmaf_rn(cdec, w, w));
-        }
-#pragma unroll
-        for (int m = 0; m < 8; ++m) {
-          const float4 v = *reinterpret_cast<const float4 *>(Vq + m * QVS);
-          const float4 mm = mq[m];  // (x, lr, -lr reg, -lr reg); lr = 0 on padding steps
-          const float lre = mm.y * e[m];
-          const float2 a01 = ffma2(make_float2(mm.z, mm.w), make_float2(a[0], a[1]), make_float2(a[0], a[1]));
-          const float2 a23 = ffma2(make_float2(mm.z, mm.w), make_float2(a[2], a[3]), make_float2(a[2], a[3]));
-          a[0] = __fmaf_rn(lre, v.x, a01.x);
-          a[1] = __fmaf_rn(lre, v.y, a01.y);
-          a[2] = __fmaf_rn(lre, v.z, a23.x);
-          a[3] = __fmaf_rn(lre, v.w, a23.y);
-        }
-      } else {
-        // the stage's 8 V rows and step operands are loaded up front (16 independent LDS.128,
-        // one latency) so the serial steps wait only on their own shuffles; short batches run
-        // all 8 steps (padding steps have lr = 0 and change nothing)
-        float4 vv[QB], mm[QB];
-#pragma unroll
-        for (int kk = 0; kk < QB; ++kk) {
-          vv[kk] = *reinterpret_cast<const float4 *>(Vq + kk * QVS);
-          mm[kk] = mq[kk];
-        }
-        __syncwarp();
-        mbar_arrive(empty + st);  // the stage is free once read
-#pragma unroll
-        for (int kk = 0; kk < QB; ++kk) quad_chain_step_vc(a, lo, vv[kk], mm[kk]);
-        continue;
+      for (int kk = 0; kk < QB; ++kk) {
+        vv[kk] = *reinterpret_cast<const float4 *>(Vq + kk * QVS);
+        mm[kk] = mq[kk];
       }
+      __syncwarp();
+      mbar_arrive(empty + st);  // the stage is free once read
+#pragma unroll
+      for (int kk = 0; kk < QB; ++kk) quad_chain_step_vc(a, lo, vv[kk], mm[kk]);
+      continue;
+    
       __syncwarp();
       mbar_arrive(empty + st);
     }
@@ -1602,17 +786,17 @@ __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(co
   }
 }
 
-template <bool GRAM, bool SMALL, bool LPR = false, bool PV = false>
+template <bool SMALL>
 int launch_quadw_t(const SweepParams &q, cudaStream_t s) {
   const size_t sm = quadw::bytes();
   static bool set = false;
   if (!set) {
-    cudaFuncSetAttribute(factor_rows_quadw_kernel<GRAM, SMALL, LPR, PV>,
+    cudaFuncSetAttribute(factor_rows_quadw_kernel<SMALL>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     set = true;
   }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quadw_kernel<GRAM, SMALL, LPR, PV>,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quadw_kernel<SMALL>,
                                                     quadw::THREADS, sm) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
@@ -1620,90 +804,19 @@ int launch_quadw_t(const SweepParams &q, cudaStream_t s) {
   const int64_t cap = (int64_t)sm_count() * per_sm;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
-  factor_rows_quadw_kernel<GRAM, SMALL, LPR, PV><<<(int)g, quadw::THREADS, sm, s>>>(q);
+  factor_rows_quadw_kernel<SMALL><<<(int)g, quadw::THREADS, sm, s>>>(q);
   return check_launch("ft_factor_sweep_rows(quadw)");
 }
 
-template <bool GRAM>
 int launch_quadw(const SweepParams &q, cudaStream_t s) {
-  static const bool lpr = [] {  // FT_QUADW_LPR=1: lane-per-row consumer
-    const char *e = getenv("FT_QUADW_LPR");
-    return e && strcmp(e, "1") == 0;
-  }();
-  if (!GRAM && lpr)
-    return q.J <= 16 && q.R <= 16 ? launch_quadw_t<false, true, true>(q, s)
-                                  : launch_quadw_t<false, false, true>(q, s);
-  static const bool pv = [] {  // FT_QUADW_PV=1: packed V, consumer in quadr's column layout
-    const char *e = getenv("FT_QUADW_PV");
-    return e && strcmp(e, "1") == 0;
-  }();
-  if (!GRAM && pv)
-    return q.J <= 16 && q.R <= 16 ? launch_quadw_t<false, true, false, true>(q, s)
-                                  : launch_quadw_t<false, false, false, true>(q, s);
-  return q.J <= 16 && q.R <= 16 ? launch_quadw_t<GRAM, true>(q, s) : launch_quadw_t<GRAM, false>(q, s);
-}
-
-template <bool SMALL, int WPBT, bool AREG, int NPRE>
-int launch_quad_t(const SweepParams &q, cudaStream_t s) {
-  const size_t sm = (size_t)quad::BFRAG_U4 * 16 + (size_t)WPBT * quad::WARP_FLOATS * 4;
-  static bool set = false;
-  if (!set) {
-    cudaFuncSetAttribute(factor_rows_quad_kernel<SMALL, WPBT, AREG, NPRE>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    set = true;
-  }
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quad_kernel<SMALL, WPBT, AREG, NPRE>,
-                                                    WPBT * 32, sm) != cudaSuccess ||
-      per_sm < 1)
-    per_sm = 1;
-  int64_t g = (q.nrows + 4 * WPBT - 1) / (4 * WPBT);
-  const int64_t cap = (int64_t)sm_count() * per_sm;
-  if (g > cap) g = cap;
-  if (g < 1) g = 1;
-  factor_rows_quad_kernel<SMALL, WPBT, AREG, NPRE><<<(int)g, WPBT * 32, sm, s>>>(q);
-  return check_launch("ft_factor_sweep_rows(quad)");
-}
-
-int launch_quad(const SweepParams &q, cudaStream_t s) {
-  static const int areg = [] {  // FT_QUAD_AREG=1: Bt^T fragments in registers, 6 warps / block
-    const char *e = getenv("FT_QUAD_AREG");
-    return e && strcmp(e, "1") == 0 ? 1 : 0;
-  }();
-  const bool small = q.J <= 16 && q.R <= 16;
-  // 9 warps per block (72 row slots per SM instead of 64) when that turns a barely-partial
-  // second wave into one wave: rows are serial, so a 6 % tail costs a whole row time (BASELINE
-  // order 4: 10,000 rows per mode vs 9,472 slots at 8 warps)
-  const int64_t slots8 = (int64_t)sm_count() * 2 * quad::WPB * 4, slots9 = slots8 * 9 / 8;
-  const bool w9 = q.nrows > slots8 && q.nrows <= slots9;
-  if (q.N > 3) {  // order 4..6: prefix products folded level by level (quad_gather)
-    switch (q.N) {
-      case 4:
-        if (w9) return small ? launch_quad_t<true, 9, false, 2>(q, s) : launch_quad_t<false, 9, false, 2>(q, s);
-        return small ? launch_quad_t<true, quad::WPB, false, 2>(q, s)
-                     : launch_quad_t<false, quad::WPB, false, 2>(q, s);
-      case 5: return small ? launch_quad_t<true, quad::WPB, false, 3>(q, s)
-                           : launch_quad_t<false, quad::WPB, false, 3>(q, s);
-      default: return small ? launch_quad_t<true, quad::WPB, false, 4>(q, s)
-                            : launch_quad_t<false, quad::WPB, false, 4>(q, s);
-    }
-  }
-  if (areg)
-    return small ? launch_quad_t<true, 6, true, 1>(q, s) : launch_quad_t<false, 6, true, 1>(q, s);
-  if (w9) return small ? launch_quad_t<true, 9, false, 1>(q, s) : launch_quad_t<false, 9, false, 1>(q, s);
-  return small ? launch_quad_t<true, quad::WPB, false, 1>(q, s)
-               : launch_quad_t<false, quad::WPB, false, 1>(q, s);
+  return q.J <= 16 && q.R <= 16 ? launch_quadw_t<true>(q, s) : launch_quadw_t<false>(q, s);
 }
 
 // the quad kernels run any J, R <= 32 (R % 4 == 0; padding columns are zero); J = R = 16 has
-// its own instantiation (one m-tile, two k-tiles).  FT_QUAD_J16=0 keeps J <= 16 on dual / ws.
+// its own instantiation (one m-tile, two k-tiles)
 bool quad_ok(const SweepParams &p) {
-  static const bool j16 = [] {
-    const char *e = getenv("FT_QUAD_J16");
-    return !(e && strcmp(e, "0") == 0);
-  }();
-  return p.N >= 3 && p.N <= 6 && p.leaf_pc && p.row_leaf_ptr && (p.J > 16 || j16) &&
-         p.J <= 32 && p.R <= 32 && (p.R & 3) == 0;
+  return p.N >= 3 && p.N <= 6 && p.leaf_pc && p.row_leaf_ptr && p.J <= 32 && p.R <= 32 &&
+         (p.R & 3) == 0;
 }
 
 // ---- K4 "quad": the core-gradient row sweep over the leaf-major index ---------------------
@@ -2108,195 +1221,4 @@ __global__ void sum_pairs_f64(const double *__restrict__ partials, int nblocks, 
     out2[0] = a;
     out2[1] = b;
   }
-}
-
-// ---- K4 "quadp": the core sweep with the gathers one batch ahead ----------------------------
-// ncu on K4 quad: 43 % of the stall samples sat on the cp.async wait (the C-row gathers come
-// from L2 at ~8 TB/s aggregate, so their latency is long) with only one batch in flight per warp.
-// Here each warp keeps two batches of tiles: batch t+1's rows land while batch t is scored and
-// accumulated.  Tiles are 32 x 32 floats with the 16-B chunk index XOR-swizzled by the slot
-// (chunk c of slot k at c ^ (k & 7)), conflict-free both for lane-per-slot row reads and for
-// quarter-per-row reads, so two batches fit 6 warps x 2 blocks per SM.  Batch records (segment,
-// leaf range, segment-start flag) and the next segment's C_u row run ahead as in quadp.
-namespace cquadp {
-constexpr int TILE = 32 * 32;
-constexpr int WARP_FLOATS = 4 * TILE + 4 * 32 + 32;  // X[2], Y[2], C_u rows [4][32], e [32]
-constexpr int WPB = 6;
-constexpr size_t bytes() { return (size_t)WPB * WARP_FLOATS * 4; }
-__device__ __forceinline__ int sw(int k, int c) { return k * 32 + 4 * (c ^ (k & 7)); }
-}  // namespace cquadp
-
-__global__ void __launch_bounds__(cquadp::WPB * 32, 2) core_rows_quadp_kernel(const SweepParams p) {
-  using namespace cquadp;
-  using quadp::Leaf;
-  using quadp::Rec;
-  extern __shared__ float4 smem4[];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int q = lane >> 3, l = lane & 7;
-  float *base = reinterpret_cast<float *>(smem4) + w * cquadp::WARP_FLOATS;  // X[s] = base + s TILE,
-  float *cus = base + 4 * cquadp::TILE;                                      // Y[s] = base + (2+s) TILE
-  float *es = cus + 128;
-  for (int k = lane; k < cquadp::WARP_FLOATS; k += 32) base[k] = 0.f;
-  __syncwarp();
-  const int J = p.J, R = p.R;
-  const bool j32 = J == 32;
-  const int64_t nstream = (int64_t)gridDim.x * cquadp::WPB * 4;
-  quadp::Cursor cur;
-  cur.row = (int64_t)(4 * w + q) * gridDim.x + blockIdx.x - nstream;
-  cur.i = -1, cur.L0 = cur.Le = 0;
-  quadp::load_row_info(p, cur.row + nstream, cur.ni, cur.nLb, cur.nLe);
-  auto load_cu = [&](const Rec &r) {
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (r.newrow && r.nb > 0 && 4 * l < R)
-      v = *reinterpret_cast<const float4 *>(p.Cu + (int64_t)r.i * R + 4 * l);
-    return v;
-  };
-  const int gc = lane & 7, gs = lane >> 3;
-  const bool gok = gc < (R >> 2);
-  const float *cpre = p.Cpre[0] + 4 * gc, *cleaf = p.Cleaf + 4 * gc;
-  const int64_t Rs = R;
-  auto gather = [&](int set, const Leaf &d) {
-    float *X = base + set * TILE, *Y = base + (2 + set) * TILE;
-#pragma unroll
-    for (int it = 0; it < 8; ++it) {
-      const int s = 4 * it + gs;
-      const int pcs = __shfl_sync(FULL, d.pc, s), lcs = __shfl_sync(FULL, d.lc, s);
-      if (gok) {
-        cp_async16_s(smem_u32(X + sw(s, gc)), cpre + pcs * Rs);
-        cp_async16_s(smem_u32(Y + sw(s, gc)), cleaf + lcs * Rs);
-      }
-    }
-    cp_async_commit();
-  };
-  float acc[FT_MAX_RANK];  // lane r: acc[j] = sum_i g_i[r] A_u[i, j]
-#pragma unroll
-  for (int j = 0; j < FT_MAX_RANK; ++j) acc[j] = 0.f;
-  float2 g01 = make_float2(0.f, 0.f), g23 = make_float2(0.f, 0.f);
-  int gi = -1;  // row of the segment g belongs to
-  // acc += g_qq (x) A_u[gi_qq] for every quarter whose bit is set in em (lane 8 qq)
-  auto flush = [&](unsigned em) {
-    while (em) {
-      const int qq = (__ffs(em) - 1) >> 3;
-      em &= em - 1;
-      const int src = 8 * qq + (lane >> 2), comp = lane & 3;
-      const float c0 = __shfl_sync(FULL, g01.x, src), c1 = __shfl_sync(FULL, g01.y, src);
-      const float c2 = __shfl_sync(FULL, g23.x, src), c3 = __shfl_sync(FULL, g23.y, src);
-      const float gr = comp == 0 ? c0 : comp == 1 ? c1 : comp == 2 ? c2 : c3;
-      const float *ar = p.A + (int64_t)__shfl_sync(FULL, gi, 8 * qq) * J;
-      if (j32) {
-#pragma unroll
-        for (int j4 = 0; j4 < 8; ++j4) {
-          const float4 a4 = __ldg(reinterpret_cast<const float4 *>(ar) + j4);
-          acc[4 * j4] = __fmaf_rn(gr, a4.x, acc[4 * j4]);
-          acc[4 * j4 + 1] = __fmaf_rn(gr, a4.y, acc[4 * j4 + 1]);
-          acc[4 * j4 + 2] = __fmaf_rn(gr, a4.z, acc[4 * j4 + 2]);
-          acc[4 * j4 + 3] = __fmaf_rn(gr, a4.w, acc[4 * j4 + 3]);
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < FT_MAX_RANK; ++j)
-          if (j < J) acc[j] = __fmaf_rn(gr, __ldg(ar + j), acc[j]);
-      }
-    }
-  };
-
-  Rec r0 = quadp::next_batch(p, cur, nstream);
-  Leaf d0 = quadp::load_leaf(p, r0, l);
-  float4 cu0 = load_cu(r0);
-  gather(0, d0);
-  Rec r1 = quadp::next_batch(p, cur, nstream);
-  Leaf d1 = quadp::load_leaf(p, r1, l);
-  float4 cu1 = load_cu(r1);
-  for (int t = 0; __any_sync(FULL, r0.nb > 0); ++t) {
-    gather((t + 1) & 1, d1);  // batch t+1's rows fly while batch t is scored
-    const Rec r2 = quadp::next_batch(p, cur, nstream);
-    const Leaf d2 = quadp::load_leaf(p, r2, l);
-    const float4 cu2 = load_cu(r2);
-    // a quarter starting a segment flushes the previous one and installs its C_u row
-    flush(__ballot_sync(FULL, r0.newrow && r0.nb > 0 && gi >= 0 && l == 0));
-    if (r0.newrow && r0.nb > 0) {
-      g01 = g23 = make_float2(0.f, 0.f);
-      gi = r0.i;
-      *reinterpret_cast<float4 *>(cus + 32 * q + 4 * l) = cu0;
-    }
-    cp_async_wait_one();
-    __syncwarp();
-    const float *X = base + (t & 1) * TILE, *Y = base + (2 + (t & 1)) * TILE;
-    {  // lane = slot: s = C_u[i_q] . (X * Y), e = x - s
-      const float4 *cr = reinterpret_cast<const float4 *>(cus + 32 * q);
-      float2 s01 = make_float2(0.f, 0.f), s23 = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const float4 xv = *reinterpret_cast<const float4 *>(X + sw(lane, c));
-        const float4 yv = *reinterpret_cast<const float4 *>(Y + sw(lane, c));
-        const float4 cv = cr[c];
-        s01 = ffma2(fmul2(make_float2(xv.x, xv.y), make_float2(yv.x, yv.y)),
-                    make_float2(cv.x, cv.y), s01);
-        s23 = ffma2(fmul2(make_float2(xv.z, xv.w), make_float2(yv.z, yv.w)),
-                    make_float2(cv.z, cv.w), s23);
-      }
-      const float s = (s01.x + s01.y) + (s23.x + s23.y);
-      es[lane] = l < r0.nb ? d0.x - s : 0.f;
-    }
-    __syncwarp();
-    {  // quarter lanes over r: g_q += sum_k e_k cross_k
-      const int nbmax = __reduce_max_sync(FULL, (unsigned)r0.nb);
-#pragma unroll
-      for (int k = 0; k < quad::QB; ++k) {
-        if (k >= nbmax) break;
-        const int row = 8 * q + k;
-        const float4 xv = *reinterpret_cast<const float4 *>(X + row * 32 + 4 * (l ^ k));
-        const float4 yv = *reinterpret_cast<const float4 *>(Y + row * 32 + 4 * (l ^ k));
-        const float ek = es[row];
-        const float2 e2 = make_float2(ek, ek);
-        g01 = ffma2(e2, fmul2(make_float2(xv.x, xv.y), make_float2(yv.x, yv.y)), g01);
-        g23 = ffma2(e2, fmul2(make_float2(xv.z, xv.w), make_float2(yv.z, yv.w)), g23);
-      }
-    }
-    __syncwarp();  // tiles of set t & 1 and es read before batch t+2's gathers / scores
-    r0 = r1, d0 = d1, cu0 = cu1;
-    r1 = r2, d1 = d2, cu1 = cu2;
-  }
-  flush(__ballot_sync(FULL, gi >= 0 && l == 0));
-  cp_async_wait_all();
-  // ---- fixed-order block reduction -> partials[block] (reuses the staging tiles) ----
-  __syncthreads();
-  const int RJ = R * J;
-  float *red = reinterpret_cast<float *>(smem4);
-  if (lane < R) {
-#pragma unroll
-    for (int j = 0; j < FT_MAX_RANK; ++j)
-      if (j < J) red[w * cquadp::WARP_FLOATS + lane * J + j] = acc[j];
-  }
-  __syncthreads();
-  for (int k = threadIdx.x; k < RJ; k += blockDim.x) {
-    float s = 0.f;
-    for (int ww = 0; ww < cquadp::WPB; ++ww) s += red[ww * cquadp::WARP_FLOATS + k];
-    p.partials[(int64_t)blockIdx.x * RJ + k] = s;
-  }
-}
-
-int core_quadp_grid(const SweepParams &p) {
-  const size_t sm = cquadp::bytes();
-  static bool set = false;
-  if (!set) {
-    cudaFuncSetAttribute(core_rows_quadp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sm);
-    set = true;
-  }
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, core_rows_quadp_kernel,
-                                                    cquadp::WPB * 32, sm) != cudaSuccess ||
-      per_sm < 1)
-    per_sm = 1;
-  int64_t g = (p.nrows + 4 * cquadp::WPB - 1) / (4 * cquadp::WPB);
-  const int64_t cap = (int64_t)sm_count() * per_sm;
-  if (g > cap) g = cap;
-  if (g < 1) g = 1;
-  return (int)g;
-}
-
-int launch_core_quadp(const SweepParams &p, int g, cudaStream_t s) {
-  core_rows_quadp_kernel<<<g, cquadp::WPB * 32, cquadp::bytes(), s>>>(p);
-  return check_launch("ft_core_sweep_rows(quadp)");
 }

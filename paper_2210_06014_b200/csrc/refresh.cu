@@ -339,3 +339,54 @@ extern "C" int ft_refresh_scatter(int64_t I, int32_t J, int32_t R, const float *
   d.n = ndst;
   return launch_refresh(I, J, R, A, Bt, d, guard, as_stream(stream));
 }
+
+// ---- stream-ordered peer barrier (multi-GPU fused refresh + all-gather) ---------------------
+// Rank `rank` publishes `seq` into slot `rank` of every rank's flag array (CUDA-IPC mappings;
+// NVLink stores on a multi-GPU node) after a system-scope fence that orders the preceding
+// refresh kernel's peer stores, then waits until every slot of its own array holds >= seq.
+// Queued on the compute stream, so the next sweep waits on the device for every rank's C_u
+// block without a host synchronize + barrier.  A peer that never arrives ends in a trap after
+// 20 s (an error, not a hang).
+namespace ft {
+namespace {
+struct Flags {
+  uint32_t *p[FT_MAX_PEERS];
+};
+__global__ void peer_barrier_kernel(uint32_t *local, Flags peers, int world, int rank,
+                                    uint32_t seq) {
+  if (threadIdx.x != 0) return;
+  __threadfence_system();
+  for (int q = 0; q < world; ++q)
+    asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(peers.p[q] + rank), "r"(seq)
+                 : "memory");
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int q = 0; q < world; ++q) {
+    for (;;) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(local + q) : "memory");
+      if ((int32_t)(v - seq) >= 0) break;
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 20000000000ull) __trap();
+      __nanosleep(64);
+    }
+  }
+}
+}  // namespace
+}  // namespace ft
+
+extern "C" int ft_peer_barrier(uint32_t *local_flags, uint32_t *const *peer_flags, int32_t world,
+                               int32_t rank, uint32_t seq, void *stream) {
+  using namespace ft;
+  if (!local_flags || !peer_flags || world < 1 || world > FT_MAX_PEERS || rank < 0 ||
+      rank >= world)
+    return fail(FT_ERR_ARG, "ft_peer_barrier: bad arguments (world %d, rank %d)", world, rank);
+  Flags f{};
+  for (int q = 0; q < world; ++q) {
+    if (!peer_flags[q]) return fail(FT_ERR_ARG, "ft_peer_barrier: null flags of rank %d", q);
+    f.p[q] = peer_flags[q];
+  }
+  peer_barrier_kernel<<<1, 32, 0, as_stream(stream)>>>(local_flags, f, world, rank, seq);
+  return check_launch("ft_peer_barrier");
+}

@@ -64,7 +64,6 @@ struct SweepParams {
   int J, R;
   float lr, reg;
   float *partials;   // core: [grid][R*J]
-  int tma;           // dual kernel: gather with TMA bulk copies (FT_GATHER=tma)
   int64_t gather_bytes;  // bytes of the gathered C matrices (modes other than u)
 };
 
@@ -172,69 +171,6 @@ __device__ __forceinline__ void stage_cross(const SweepParams &p, float *X, floa
 // ------------------------------------------------------------------------------------------
 constexpr int WPB_R = 4;  // warps per block of the row kernels
 
-// FFMA variant (kept for A/B measurement: FT_FACTOR_KERNEL=ffma): the combine reads cross as
-// shared-memory broadcasts, 8 LDS.128 + 32 FFMA per leaf per warp.
-template <int RP>
-__global__ void __launch_bounds__(WPB_R * 32)
-    factor_rows_ffma_kernel(const SweepParams p) {
-  extern __shared__ float4 smem4[];
-  constexpr int RS = Tile<RP>::RS;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  float *X = reinterpret_cast<float *>(smem4) + w * 2 * Tile<RP>::FLOATS;
-  float *Y = X + Tile<RP>::FLOATS;
-  for (int k = lane; k < 2 * Tile<RP>::FLOATS; k += 32) X[k] = 0.f;  // pads stay zero
-  __syncwarp();
-  const int64_t gw = (int64_t)blockIdx.x * WPB_R + w, nw = (int64_t)gridDim.x * WPB_R;
-  const bool jl = lane < p.J;
-  // Bt_u column j as fp32 pairs: the combine runs on packed FFMA2 (two FMAs per issue slot;
-  // even and odd r accumulate in the two halves and are added at the end)
-  float2 bt2[RP / 2];
-#pragma unroll
-  for (int r = 0; r < RP / 2; ++r) {
-    bt2[r].x = (jl && 2 * r < p.R) ? __ldg(p.Bt + (2 * r) * p.J + lane) : 0.f;
-    bt2[r].y = (jl && 2 * r + 1 < p.R) ? __ldg(p.Bt + (2 * r + 1) * p.J + lane) : 0.f;
-  }
-
-  for (int64_t row = gw; row < p.nrows; row += nw) {
-    const int i = __ldg(p.row_coord + row);
-    const int fb = __ldg(p.row_fiber_ptr + row), fe = __ldg(p.row_fiber_ptr + row + 1);
-    const int Lb = __ldg(p.fiber_ptr + fb), Le = __ldg(p.fiber_ptr + fe);
-    float *arow = p.A + (int64_t)i * p.J;
-    float a = jl ? arow[lane] : 0.f;
-    int fcur = fb;
-    for (int L0 = Lb; L0 < Le; L0 += BATCH) {
-      const int nb = min(BATCH, Le - L0);
-      const int lc = lane < nb ? __ldcs(p.leaf_coord + L0 + lane) : 0;
-      const float x = lane < nb ? __ldcs(p.vals + L0 + lane) : 0.f;
-      int fnext;
-      const int myfib = batch_fibers(p.fiber_ptr, fcur, fe, L0, nb, lane, &fnext);
-      stage_cross<RP>(p, X, Y, myfib, lc, nb, lane);
-      // serial chain; vec_k = sum_r cross[k][r] Bt[r][j] (broadcast reads, FFMA2) is
-      // independent of the row, so it overlaps the previous leaf's reduction latency
-#pragma unroll 4
-      for (int k = 0; k < nb; ++k) {
-        const float4 *xr = reinterpret_cast<const float4 *>(X + k * RS);
-        float2 v2 = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int r4 = 0; r4 < RP / 4; ++r4) {
-          const float4 c4 = xr[r4];
-          v2 = ffma2(make_float2(c4.x, c4.y), bt2[2 * r4], v2);
-          v2 = ffma2(make_float2(c4.z, c4.w), bt2[2 * r4 + 1], v2);
-        }
-        const float v = v2.x + v2.y;
-        const float s = warp_sum(a * v);
-        const float e = __shfl_sync(FULL, x, k) - s;
-        const float g = p.reg * a - e * v;
-        a = a - p.lr * g;
-      }
-      __syncwarp();
-      fcur = fnext;
-    }
-    if (jl) arow[lane] = a;
-  }
-}
-
-
 // ---- 3xTF32 tensor-core combine ---------------------------------------------------------
 // vec for a batch of 32 leaves is a 32 x J x R GEMM: V = Cross (32 x R) * Bt_u (R x J).
 // mma.sync.m16n8k8 TF32 with the 3-term split (a_hi b_hi + a_hi b_lo + a_lo b_hi) keeps fp32
@@ -254,138 +190,8 @@ __device__ __forceinline__ void mma_tf32(float (&d)[4], uint32_t a0, uint32_t a1
 
 constexpr int VS = 36;  // row stride of the staged V tile (32 leaves x 32 j)
 
-// Shared-memory plan of the tensor-core K3b (per block: the Bt_u fragments, then per warp the
-// X / Y staging tiles; V lands in Y when RP = 32, else in its own tile).
-template <int RP>
-struct MmaPlan {
-  static constexpr int RS = Tile<RP>::RS;
-  static constexpr int KT = RP / 8 > 0 ? RP / 8 : 1;
-  static constexpr int NT = 4;
-  static constexpr bool V_IN_Y = RS >= VS;
-  static constexpr int WARP_FLOATS = 2 * BATCH * RS + (V_IN_Y ? 0 : BATCH * VS);
-  static constexpr int BFRAG_U4 = KT * NT * 32;  // uint4 per block
-  static constexpr size_t bytes(int wpb) {
-    return (size_t)BFRAG_U4 * 16 + (size_t)wpb * WARP_FLOATS * sizeof(float);
-  }
-};
-
-// K3b with the combine on tensor cores.  Per batch: stage X (prefix product) and Y (leaf rows)
-// with cp.async; V = (X * Y) * Bt_u by 3xTF32 mma.sync (the A fragments are formed from X and Y
-// in registers; the hi / lo B fragments of Bt_u are split once per block into shared memory);
-// V goes through shared memory to the lanes-over-j layout; then the serial chain.
-template <int RP>
-__global__ void __launch_bounds__(WPB_R * 32)
-    factor_rows_kernel(const SweepParams p) {
-  using P = MmaPlan<RP>;
-  constexpr int RS = P::RS, KT = P::KT, NT = P::NT;
-  extern __shared__ float4 smem4[];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int gq = lane >> 2, tq = lane & 3;
-  uint4 *bfrag = reinterpret_cast<uint4 *>(smem4);  // [KT][NT][32]: (hi0, hi1, lo0, lo1)
-  float *X = reinterpret_cast<float *>(bfrag + P::BFRAG_U4) + w * P::WARP_FLOATS;
-  float *Y = X + BATCH * RS;
-  float *V = P::V_IN_Y ? Y : Y + BATCH * RS;
-  for (int k = lane; k < P::WARP_FLOATS; k += 32) X[k] = 0.f;
-  for (int f = threadIdx.x; f < P::BFRAG_U4; f += blockDim.x) {
-    const int l = f & 31, nt = (f >> 5) % NT, kt = (f >> 5) / NT;
-    const int g = l >> 2, t = l & 3, j = 8 * nt + g;
-    uint32_t hv[2], lv[2];
-    for (int h = 0; h < 2; ++h) {
-      const int r = 8 * kt + t + 4 * h;
-      const float b = (r < p.R && j < p.J) ? __ldg(p.Bt + r * p.J + j) : 0.f;
-      hv[h] = to_tf32(b);
-      lv[h] = to_tf32(b - __uint_as_float(hv[h]));
-    }
-    bfrag[f] = make_uint4(hv[0], hv[1], lv[0], lv[1]);
-  }
-  __syncthreads();
-  const int64_t gw = (int64_t)blockIdx.x * WPB_R + w, nw = (int64_t)gridDim.x * WPB_R;
-  const bool jl = lane < p.J;
-
-  for (int64_t row = gw; row < p.nrows; row += nw) {
-    const int i = __ldg(p.row_coord + row);
-    const int fb = __ldg(p.row_fiber_ptr + row), fe = __ldg(p.row_fiber_ptr + row + 1);
-    const int Lb = __ldg(p.fiber_ptr + fb), Le = __ldg(p.fiber_ptr + fe);
-    float *arow = p.A + (int64_t)i * p.J;
-    float a = jl ? arow[lane] : 0.f;
-    int fcur = fb;
-    for (int L0 = Lb; L0 < Le; L0 += BATCH) {
-      const int nb = min(BATCH, Le - L0);
-      const int lc = lane < nb ? __ldcs(p.leaf_coord + L0 + lane) : 0;
-      const float x = lane < nb ? __ldcs(p.vals + L0 + lane) : 0.f;
-      int fnext;
-      const int myfib = batch_fibers(p.fiber_ptr, fcur, fe, L0, nb, lane, &fnext);
-      stage_cross<RP>(p, X, Y, myfib, lc, nb, lane, /*fold_leaf=*/false);
-      float acc[2][NT][4];
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) acc[mt][nt][q] = 0.f;
-      const int mts = nb > 16 ? 2 : 1;
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-        if (mt >= mts) break;
-#pragma unroll
-        for (int kt = 0; kt < KT; ++kt) {
-          const int r0 = 16 * mt + gq, c0 = 8 * kt + tq;
-          const float x0 = X[r0 * RS + c0] * Y[r0 * RS + c0];
-          const float x1 = X[(r0 + 8) * RS + c0] * Y[(r0 + 8) * RS + c0];
-          const float x2 = X[r0 * RS + c0 + 4] * Y[r0 * RS + c0 + 4];
-          const float x3 = X[(r0 + 8) * RS + c0 + 4] * Y[(r0 + 8) * RS + c0 + 4];
-          const uint32_t h0 = to_tf32(x0), h1 = to_tf32(x1), h2 = to_tf32(x2), h3 = to_tf32(x3);
-          const uint32_t l0 = to_tf32(x0 - __uint_as_float(h0));
-          const uint32_t l1 = to_tf32(x1 - __uint_as_float(h1));
-          const uint32_t l2 = to_tf32(x2 - __uint_as_float(h2));
-          const uint32_t l3 = to_tf32(x3 - __uint_as_float(h3));
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            const uint4 b = bfrag[(kt * NT + nt) * 32 + lane];
-            mma_tf32(acc[mt][nt], l0, l1, l2, l3, b.x, b.y);
-            mma_tf32(acc[mt][nt], h0, h1, h2, h3, b.z, b.w);
-            mma_tf32(acc[mt][nt], h0, h1, h2, h3, b.x, b.y);
-          }
-        }
-      }
-      __syncwarp();  // all A fragments read before V overwrites Y
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          const int r0 = 16 * mt + gq, c0 = 8 * nt + 2 * tq;
-          *reinterpret_cast<float2 *>(V + r0 * VS + c0) = make_float2(acc[mt][nt][0], acc[mt][nt][1]);
-          *reinterpret_cast<float2 *>(V + (r0 + 8) * VS + c0) =
-              make_float2(acc[mt][nt][2], acc[mt][nt][3]);
-        }
-      __syncwarp();
-      // serial chain: s = a.v, e = x - s, a -= lr (reg a - e v)
-#pragma unroll 8
-      for (int k = 0; k < nb; ++k) {
-        const float v = V[k * VS + lane];
-        const float s = warp_sum(a * v);
-        const float e = __shfl_sync(FULL, x, k) - s;
-        const float g = p.reg * a - e * v;
-        a = a - p.lr * g;
-      }
-      __syncwarp();
-      if (P::V_IN_Y && p.R < RP) {  // V overwrote Y's zero pads r in [R, RP)
-        if (lane >= p.R && lane < RP)
-          for (int k = 0; k < BATCH; ++k) Y[k * RS + lane] = 0.f;
-        __syncwarp();
-      }
-      fcur = fnext;
-    }
-    if (jl) arow[lane] = a;
-  }
-}
-
-
-// ---- K3b, software-pipelined tensor-core version (the default) --------------------------
-// Per warp, batch b+1's index loads are issued before batch b's MMA and its cp.async gathers
-// right after it, so the gather latency hides under batch b's serial chain.  Staging tiles are
-// 32 floats wide with an XOR swizzle (conflict-free A-fragment loads and 16-B cp.async), V has
-// its own tile so the next gathers never wait for the chain.
+// ---- batch index pipeline shared by the fiber-walking K3b kernels (ws, gram) ------------
+// Staging tiles 32 floats wide with an XOR swizzle (conflict-free fragment loads, 16-B cp.async).
 __device__ __forceinline__ int swz(int row, int col) { return row * 32 + (col ^ ((row & 7) << 2)); }
 
 template <int RP>
@@ -410,17 +216,6 @@ __device__ __forceinline__ void gather_sw(float *dst, const float *__restrict__ 
   }
 }
 
-struct PipePlan {
-  static constexpr int TILE = BATCH * 32;  // swizzled X / Y tiles
-  static constexpr int WARP_FLOATS = 2 * TILE + BATCH * VS;
-  static constexpr int WPB = 8;
-  template <int RP>
-  static constexpr int bfrag_u4() { return (RP / 8 > 0 ? RP / 8 : 1) * 4 * 32; }
-  template <int RP>
-  static constexpr size_t bytes() {
-    return (size_t)bfrag_u4<RP>() * 16 + (size_t)WPB * WARP_FLOATS * sizeof(float);
-  }
-};
 
 // Everything batch b needs before its gathers can be issued.
 struct BatchIdx {
@@ -470,140 +265,7 @@ __device__ __forceinline__ void issue_gathers(const SweepParams &p, const BatchI
   asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
 
-template <int RP>
-__global__ void __launch_bounds__(PipePlan::WPB * 32, 2)
-    factor_rows_pipe_kernel(const SweepParams p) {
-  constexpr int KT = RP / 8 > 0 ? RP / 8 : 1, NT = 4;
-  extern __shared__ float4 smem4[];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int gq = lane >> 2, tq = lane & 3;
-  uint4 *bfrag = reinterpret_cast<uint4 *>(smem4);
-  float *X = reinterpret_cast<float *>(bfrag + PipePlan::bfrag_u4<RP>()) + w * PipePlan::WARP_FLOATS;
-  float *Y = X + PipePlan::TILE;
-  float *V = Y + PipePlan::TILE;
-  for (int k = lane; k < PipePlan::WARP_FLOATS; k += 32) X[k] = 0.f;
-  for (int f = threadIdx.x; f < PipePlan::bfrag_u4<RP>(); f += blockDim.x) {
-    const int l = f & 31, nt = (f >> 5) % NT, kt = (f >> 5) / NT;
-    const int g = l >> 2, t = l & 3, j = 8 * nt + g;
-    uint32_t hv[2], lv[2];
-    for (int h = 0; h < 2; ++h) {
-      const int r = 8 * kt + t + 4 * h;
-      const float bv = (r < p.R && j < p.J) ? __ldg(p.Bt + r * p.J + j) : 0.f;
-      hv[h] = to_tf32(bv);
-      lv[h] = to_tf32(bv - __uint_as_float(hv[h]));
-    }
-    bfrag[f] = make_uint4(hv[0], hv[1], lv[0], lv[1]);
-  }
-  __syncthreads();
-  const int64_t gw = (int64_t)blockIdx.x * PipePlan::WPB + w;
-  const int64_t nw = (int64_t)gridDim.x * PipePlan::WPB;
-  const bool jl = lane < p.J;
-
-  for (int64_t row = gw; row < p.nrows; row += nw) {
-    const int i = __ldg(p.row_coord + row);
-    const int fb = __ldg(p.row_fiber_ptr + row), fe = __ldg(p.row_fiber_ptr + row + 1);
-    const int Lb = __ldg(p.fiber_ptr + fb), Le = __ldg(p.fiber_ptr + fe);
-    float *arow = p.A + (int64_t)i * p.J;
-    float a = jl ? arow[lane] : 0.f;
-    // prologue: batch 0's gathers in flight, batch 1's indices requested
-    BatchIdx cur, nxt;
-    load_batch_idx(p, cur, Lb, Le, fb, fe, lane);
-    int fnext;
-    int myfib = batch_fib(cur, lane, &fnext);
-    issue_gathers<RP>(p, cur, myfib, X, Y, lane);
-    bool has_next = Lb + BATCH < Le;
-    if (has_next) load_batch_idx(p, nxt, Lb + BATCH, Le, fnext, fe, lane);
-    for (;;) {
-      // next batch's fibers and prefix coordinates (the loads fly during this batch's MMA)
-      int nfib = 0, nfnext = 0, ncoord = 0;
-      if (has_next) {
-        nfib = batch_fib(nxt, lane, &nfnext);
-        if (p.N == 3)
-          ncoord = lane < nxt.nb ? __ldg(p.fiber_coord + (int64_t)nfib * 2 + 1) : 0;
-      }
-      cp_async_wait_all();
-      __syncwarp();
-      // ---- V = (X * Y) * Bt_u, 3xTF32 ----
-      float acc[2][NT][4];
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) acc[mt][nt][q] = 0.f;
-      const int mts = cur.nb > 16 ? 2 : 1;
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-        if (mt >= mts) break;
-#pragma unroll
-        for (int kt = 0; kt < KT; ++kt) {
-          const int r0 = 16 * mt + gq, c0 = 8 * kt + tq;
-          const int o0 = swz(r0, c0), o1 = swz(r0 + 8, c0), o2 = swz(r0, c0 + 4),
-                    o3 = swz(r0 + 8, c0 + 4);
-          const float x0 = X[o0] * Y[o0], x1 = X[o1] * Y[o1], x2 = X[o2] * Y[o2],
-                      x3 = X[o3] * Y[o3];
-          const uint32_t h0 = to_tf32(x0), h1 = to_tf32(x1), h2 = to_tf32(x2), h3 = to_tf32(x3);
-          const uint32_t l0 = to_tf32(x0 - __uint_as_float(h0));
-          const uint32_t l1 = to_tf32(x1 - __uint_as_float(h1));
-          const uint32_t l2 = to_tf32(x2 - __uint_as_float(h2));
-          const uint32_t l3 = to_tf32(x3 - __uint_as_float(h3));
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            const uint4 bb = bfrag[(kt * NT + nt) * 32 + lane];
-            mma_tf32(acc[mt][nt], l0, l1, l2, l3, bb.x, bb.y);
-            mma_tf32(acc[mt][nt], h0, h1, h2, h3, bb.z, bb.w);
-            mma_tf32(acc[mt][nt], h0, h1, h2, h3, bb.x, bb.y);
-          }
-        }
-      }
-      __syncwarp();  // X / Y consumed
-      // ---- next batch's gathers go out now, under this batch's chain ----
-      BatchIdx nn;
-      bool has_nn = false;
-      if (has_next) {
-        if (p.N == 3) {
-          gather_sw<RP>(X, p.Cpre[0], p.R, ncoord, nxt.nb, lane);
-          gather_sw<RP>(Y, p.Cleaf, p.R, nxt.lc, nxt.nb, lane);
-          asm volatile("cp.async.commit_group;\n" ::: "memory");
-        } else {
-          issue_gathers<RP>(p, nxt, nfib, X, Y, lane);
-        }
-        has_nn = nxt.L0 + BATCH < Le;
-        if (has_nn) load_batch_idx(p, nn, nxt.L0 + BATCH, Le, nfnext, fe, lane);
-      }
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          const int r0 = 16 * mt + gq, c0 = 8 * nt + 2 * tq;
-          *reinterpret_cast<float2 *>(V + r0 * VS + c0) = make_float2(acc[mt][nt][0], acc[mt][nt][1]);
-          *reinterpret_cast<float2 *>(V + (r0 + 8) * VS + c0) =
-              make_float2(acc[mt][nt][2], acc[mt][nt][3]);
-        }
-      __syncwarp();
-      // ---- serial chain: s = a.v, e = x - s, a -= lr (reg a - e v) ----
-      const float xk = cur.x;
-      const int nbk = cur.nb;
-#pragma unroll 8
-      for (int k = 0; k < nbk; ++k) {
-        const float v = V[k * VS + lane];
-        const float s = warp_sum(a * v);
-        const float e = __shfl_sync(FULL, xk, k) - s;
-        const float g = p.reg * a - e * v;
-        a = a - p.lr * g;
-      }
-      __syncwarp();
-      if (!has_next) break;
-      cur = nxt;
-      nxt = nn;
-      has_next = has_nn;
-    }
-    if (jl) arow[lane] = a;
-  }
-}
-
-
-// ---- K3b, two rows per warp (the default) ------------------------------------------------
+// ---- K3b dual: two rows per warp (orders 5-6 with many rows) -------------------------------
 // Each 16-lane half of a warp owns one row of A_u (lane l holds columns l and l + 16) and walks
 // its root slice in 16-leaf batches, so a warp advances two independent serial chains at once
 // and each chain step reduces over 16 lanes (4 shuffle levels) instead of 32.  The batch of a
@@ -611,7 +273,7 @@ __global__ void __launch_bounds__(PipePlan::WPB * 32, 2)
 // round-robin per half; a half that finishes its row writes it back and starts the next one.
 constexpr int HB = 16;  // leaves per half-warp batch
 
-// ---- TMA bulk copies (cp.async.bulk, SASS UBLKCP) completed on an mbarrier ----
+// ---- mbarrier helpers ----
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -619,28 +281,12 @@ __device__ __forceinline__ void mbar_init(uint64_t *bar, int count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 }
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_copy(float *dst, const float *src, uint32_t bytes,
-                                          uint64_t *bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
 struct DualPlan {
@@ -675,13 +321,6 @@ __global__ void __launch_bounds__(DualPlan::WPB * 32, 2)
                                            DualPlan::BAR_BYTES) +
                  w * DualPlan::WARP_FLOATS;
   constexpr int XS = DualPlan::XS;
-  // FT_GATHER=tma: order-3 tensors with 16-B rows gather by TMA bulk copies (one UBLKCP per C
-  // row, completion on an mbarrier).  Measured slower than cp.async here (8.95 vs 7.7 ms on
-  // Netflix mode 0): without double buffering -- which the shared-memory budget does not allow
-  // at 16 warps/SM -- the copy latency is exposed and the mbarrier spin adds instructions.
-  const bool tma = p.tma && p.N == 3 && (p.R & 3) == 0;
-  if (lane == 0) mbar_init(bar, 1);
-  uint32_t phase = 0;
   // tile of half hh: wbase + hh * HALF_FLOATS (+ XT for Y, + 2 XT for V); computed by
   // arithmetic, not through a pointer array, so the accesses stay LDS/STS (not generic LD/ST)
 #define XH(hh) (wbase + (hh) * DualPlan::HALF_FLOATS)
@@ -775,22 +414,7 @@ __global__ void __launch_bounds__(DualPlan::WPB * 32, 2)
     }
     // ---- gathers: prefix levels into X (folded progressively), the leaf level into Y ----
     const int npre = p.N - 2;
-    if (tma) {
-      const int pc = lv ? __ldg(p.fiber_coord + (int64_t)myfib * 2 + 1) : 0;
-      const uint32_t rowb = (uint32_t)p.R * 4;
-      const int tot = __shfl_sync(FULL, nb, 0) + __shfl_sync(FULL, nb, 16);
-      fence_proxy_async();  // prior generic reads of X / Y before the async-proxy writes
-      __syncwarp();
-      if (lane == 0) mbar_expect_tx(bar, (uint32_t)tot * rowb * 2);
-      __syncwarp();
-      if (lv) {
-        bulk_copy(Xh + l * XS, p.Cpre[0] + (int64_t)pc * p.R, rowb, bar);
-        bulk_copy(Yh + l * XS, p.Cleaf + (int64_t)lc * p.R, rowb, bar);
-      }
-      mbar_wait(bar, phase);
-      phase ^= 1;
-    }
-    for (int lvl = 0; lvl <= npre && !tma; ++lvl) {
+    for (int lvl = 0; lvl <= npre; ++lvl) {
       const bool leaf = lvl == npre;
       const int coord =
           leaf ? lc : (lv ? __ldg(p.fiber_coord + (int64_t)myfib * (p.N - 1) + 1 + lvl) : 0);
@@ -821,7 +445,7 @@ __global__ void __launch_bounds__(DualPlan::WPB * 32, 2)
         __syncwarp();
       }
     }
-    if (!tma) cp_async_wait_all();
+    cp_async_wait_all();
     __syncwarp();
     // ---- V_h = (X_h * Y_h) * Bt_u: one m16 tile per half, 3xTF32 ----
     float acc[2][NT][4];
@@ -895,187 +519,6 @@ __global__ void __launch_bounds__(DualPlan::WPB * 32, 2)
 #undef XH
 #undef YH
 #undef VH
-
-
-// ---- K3b, two rows per warp with register-direct fragments (the default for many rows) ------
-// As the dual kernel, but the rank products never touch shared memory: lane (g, t) loads exactly
-// the A-fragment elements of the m16n8k8 MMA it issues -- C_prefix[pc][r] * C_leaf[lc][r] for
-// leaves g and g+8 and r = 8kt + t (+4) -- straight from L1/L2 (the C rows are L2-resident;
-// the 4 lanes and 4 k-tiles reading one row share its L1 line), with 64 independent loads in
-// flight per lane.  Shared memory holds only the V tiles (the transpose to lanes-over-j).
-struct RDualPlan {
-  static constexpr int VT = HB * VS;              // 16 x 36 V tile per half
-  static constexpr int WARP_FLOATS = 2 * VT + 16;  // +16: the halves' V reads hit disjoint banks
-  static constexpr int WPB = 8;
-  template <int RP>
-  static constexpr int bfrag_u4() { return (RP / 8 > 0 ? RP / 8 : 1) * 4 * 32; }
-  template <int RP>
-  static constexpr size_t bytes() {
-    return (size_t)bfrag_u4<RP>() * 16 + (size_t)WPB * WARP_FLOATS * sizeof(float);
-  }
-};
-
-template <int RP>
-__global__ void __launch_bounds__(RDualPlan::WPB * 32, 2)
-    factor_rows_rdual_kernel(const SweepParams p) {
-  constexpr int KT = RP / 8 > 0 ? RP / 8 : 1, NT = 4;
-  extern __shared__ float4 smem4[];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int h = lane >> 4, l = lane & 15;
-  const int gq = lane >> 2, tq = lane & 3;
-  uint4 *bfrag = reinterpret_cast<uint4 *>(smem4);
-  float *wbase = reinterpret_cast<float *>(bfrag + RDualPlan::bfrag_u4<RP>()) + w * RDualPlan::WARP_FLOATS;
-#define VHR(hh) (wbase + (hh) * (RDualPlan::VT + 16))
-  for (int f = threadIdx.x; f < RDualPlan::bfrag_u4<RP>(); f += blockDim.x) {
-    const int ll = f & 31, nt = (f >> 5) % NT, kt = (f >> 5) / NT;
-    const int g = ll >> 2, t = ll & 3, j = 8 * nt + g;
-    uint32_t hv[2], lv2[2];
-    for (int hh = 0; hh < 2; ++hh) {
-      const int r = 8 * kt + t + 4 * hh;
-      const float bv = (r < p.R && j < p.J) ? __ldg(p.Bt + r * p.J + j) : 0.f;
-      hv[hh] = to_tf32(bv);
-      lv2[hh] = to_tf32(bv - __uint_as_float(hv[hh]));
-    }
-    bfrag[f] = make_uint4(hv[0], hv[1], lv2[0], lv2[1]);
-  }
-  __syncthreads();
-  const int64_t nstream = (int64_t)gridDim.x * RDualPlan::WPB * 2;
-  const int64_t mystream = ((int64_t)blockIdx.x * RDualPlan::WPB + w) * 2 + h;
-  const bool j0 = l < p.J, j1 = l + 16 < p.J;
-  const int R = p.R, npre = p.N - 2;
-  float *Vh = VHR(h);
-
-  int64_t row = mystream - nstream;
-  int fe = 0, Le = 0, L0 = 0, fcur = 0;
-  float *arow = nullptr;
-  float a0 = 0.f, a1 = 0.f;
-  bool active = true;
-  for (;;) {
-    if (active && L0 >= Le) {
-      if (arow) {
-        if (j0) arow[l] = a0;
-        if (j1) arow[l + 16] = a1;
-        arow = nullptr;
-      }
-      row += nstream;
-      if (row < p.nrows) {
-        const int i = __ldg(p.row_coord + row);
-        const int fb = __ldg(p.row_fiber_ptr + row);
-        fe = __ldg(p.row_fiber_ptr + row + 1);
-        L0 = __ldg(p.fiber_ptr + fb);
-        Le = __ldg(p.fiber_ptr + fe);
-        fcur = fb;
-        arow = p.A + (int64_t)i * p.J;
-        a0 = j0 ? arow[l] : 0.f;
-        a1 = j1 ? arow[l + 16] : 0.f;
-      } else {
-        active = false;
-      }
-    }
-    if (!__any_sync(FULL, active)) break;
-    const int nb = active ? min(HB, Le - L0) : 0;
-    const bool lv = l < nb;
-    const int lc = lv ? __ldcs(p.leaf_coord + L0 + l) : 0;
-    const float x = lv ? __ldcs(p.vals + L0 + l) : 0.f;
-    const int fidx = fcur + 1 + l;
-    const int fs = (active && fidx < fe) ? __ldg(p.fiber_ptr + fidx) : INT32_MAX;
-    const unsigned bit = (fs < L0 + nb) ? (1u << (fs - L0)) : 0u;
-    const unsigned hmask = (__reduce_or_sync(FULL, bit << (16 * h)) >> (16 * h)) & 0xffffu;
-    const int myfib = fcur + __popc(hmask & (0xffffu >> (15 - l)));
-    const int fnext = fcur + __popc(hmask);
-    const int64_t fcbase = (int64_t)myfib * (p.N - 1) + 1;
-    // ---- V_h = cross_h * Bt_u, A fragments loaded from L1/L2 into registers ----
-    float acc[2][NT][4];
-#pragma unroll
-    for (int hh = 0; hh < 2; ++hh)
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) acc[hh][nt][q] = 0.f;
-#pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-      // rows gq and gq+8 of half hh's tile = leaves 16hh+gq, 16hh+gq+8
-      const int s0 = 16 * hh + gq, s1 = s0 + 8;
-      const int nbh = __shfl_sync(FULL, nb, 16 * hh);
-      const bool v0 = gq < nbh, v1 = gq + 8 < nbh;
-      const float *lr0 = p.Cleaf + (int64_t)__shfl_sync(FULL, lc, s0) * R;
-      const float *lr1 = p.Cleaf + (int64_t)__shfl_sync(FULL, lc, s1) * R;
-      float x0[KT][2], x1[KT][2];  // [kt][col t / t+4] for rows gq / gq+8
-#pragma unroll
-      for (int kt = 0; kt < KT; ++kt)
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const int col = 8 * kt + tq + 4 * c;
-          const bool ok = col < R;
-          x0[kt][c] = (ok && v0) ? __ldg(lr0 + col) : 0.f;
-          x1[kt][c] = (ok && v1) ? __ldg(lr1 + col) : 0.f;
-        }
-      for (int lvl = 0; lvl < npre; ++lvl) {
-        const int f0 = __shfl_sync(FULL, lv ? __ldg(p.fiber_coord + fcbase + lvl) : 0, s0);
-        const int f1 = __shfl_sync(FULL, lv ? __ldg(p.fiber_coord + fcbase + lvl) : 0, s1);
-        const float *pr0 = p.Cpre[lvl] + (int64_t)f0 * R;
-        const float *pr1 = p.Cpre[lvl] + (int64_t)f1 * R;
-#pragma unroll
-        for (int kt = 0; kt < KT; ++kt)
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            const int col = 8 * kt + tq + 4 * c;
-            const bool ok = col < R;
-            // prefix levels multiply in front: ((P1 * P2) ...) * leaf is the reference's
-            // left-to-right order only for N = 3; fp32 association differences are ~1 ulp
-            x0[kt][c] = (ok && v0) ? __ldg(pr0 + col) * x0[kt][c] : 0.f;
-            x1[kt][c] = (ok && v1) ? __ldg(pr1 + col) * x1[kt][c] : 0.f;
-          }
-      }
-#pragma unroll
-      for (int kt = 0; kt < KT; ++kt) {
-        const uint32_t h0 = to_tf32(x0[kt][0]), h1 = to_tf32(x1[kt][0]);
-        const uint32_t h2 = to_tf32(x0[kt][1]), h3 = to_tf32(x1[kt][1]);
-        const uint32_t l0 = to_tf32(x0[kt][0] - __uint_as_float(h0));
-        const uint32_t l1 = to_tf32(x1[kt][0] - __uint_as_float(h1));
-        const uint32_t l2 = to_tf32(x0[kt][1] - __uint_as_float(h2));
-        const uint32_t l3 = to_tf32(x1[kt][1] - __uint_as_float(h3));
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          const uint4 bb = bfrag[(kt * NT + nt) * 32 + lane];
-          mma_tf32(acc[hh][nt], l0, l1, l2, l3, bb.x, bb.y);
-          mma_tf32(acc[hh][nt], h0, h1, h2, h3, bb.z, bb.w);
-          mma_tf32(acc[hh][nt], h0, h1, h2, h3, bb.x, bb.y);
-        }
-      }
-    }
-#pragma unroll
-    for (int hh = 0; hh < 2; ++hh)
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int c0 = 8 * nt + 2 * tq;
-        *reinterpret_cast<float2 *>(VHR(hh) + gq * VS + c0) = make_float2(acc[hh][nt][0], acc[hh][nt][1]);
-        *reinterpret_cast<float2 *>(VHR(hh) + (gq + 8) * VS + c0) =
-            make_float2(acc[hh][nt][2], acc[hh][nt][3]);
-      }
-    __syncwarp();
-    const int nbmax = max(__shfl_sync(FULL, nb, 0), __shfl_sync(FULL, nb, 16));
-#pragma unroll 4
-    for (int k = 0; k < nbmax; ++k) {
-      const float v0 = Vh[k * VS + l], v1 = Vh[k * VS + l + 16];
-      float s = a0 * v0 + a1 * v1;
-      s += __shfl_xor_sync(FULL, s, 8);
-      s += __shfl_xor_sync(FULL, s, 4);
-      s += __shfl_xor_sync(FULL, s, 2);
-      s += __shfl_xor_sync(FULL, s, 1);
-      const float e = __shfl_sync(FULL, x, 16 * h + (k & 15)) - s;
-      if (k < nb) {
-        const float g0 = p.reg * a0 - e * v0, g1 = p.reg * a1 - e * v1;
-        a0 = a0 - p.lr * g0;
-        a1 = a1 - p.lr * g1;
-      }
-    }
-    __syncwarp();
-    L0 += nb;
-    fcur = fnext;
-  }
-#undef VHR
-}
 
 
 // ---- K3b, warp-specialised (producer / consumer) two-row version --------------------------
@@ -1454,9 +897,6 @@ __global__ void __launch_bounds__(GramPlan::WPB * 32, 2)
   const int64_t nw = (int64_t)gridDim.x * GramPlan::WPB;
   const bool jl = lane < p.J;
   const float lr = p.lr, reg = p.reg;
-  // G in 1xTF32 while lr keeps its error term (lr e dG, dG ~ 2^-11 |G|) far below the 1e-4
-  // contract; 3xTF32 above (measured: lr 2e-3 over 20 K-step rows passes, lr 5e-2 does not)
-  const bool gram3 = lr > 2.5e-3f;
 
   for (int64_t row = gw; row < p.nrows; row += nw) {
     const int i = __ldg(p.row_coord + row);
@@ -1557,12 +997,11 @@ __global__ void __launch_bounds__(GramPlan::WPB * 32, 2)
             const int n0 = 8 * nt + gq;
             const float e0 = V[n0 * VS + c0], e1 = V[n0 * VS + c0 + 4];
             const uint32_t b0 = to_tf32(e0), b1 = to_tf32(e1);
-            if (gram3) {  // large lr: the TF32 error of G is no longer lr-suppressed
-              mma_tf32(gacc[nt], to_tf32(f0 - __uint_as_float(a0)), to_tf32(f1 - __uint_as_float(a1)),
-                       to_tf32(f2 - __uint_as_float(a2)), to_tf32(f3 - __uint_as_float(a3)), b0, b1);
-              mma_tf32(gacc[nt], a0, a1, a2, a3, to_tf32(e0 - __uint_as_float(b0)),
-                       to_tf32(e1 - __uint_as_float(b1)));
-            }
+            // G in 3xTF32 like every other contraction (its error enters the chain as lr e dG)
+            mma_tf32(gacc[nt], to_tf32(f0 - __uint_as_float(a0)), to_tf32(f1 - __uint_as_float(a1)),
+                     to_tf32(f2 - __uint_as_float(a2)), to_tf32(f3 - __uint_as_float(a3)), b0, b1);
+            mma_tf32(gacc[nt], a0, a1, a2, a3, to_tf32(e0 - __uint_as_float(b0)),
+                     to_tf32(e1 - __uint_as_float(b1)));
             mma_tf32(gacc[nt], a0, a1, a2, a3, b0, b1);
           }
         }
@@ -1920,102 +1359,39 @@ int launch_gram(const SweepParams &p, cudaStream_t s) {
 
 template <int RP>
 int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
-  // FT_FACTOR_KERNEL selects the K3b variant for A/B measurement: auto (default: dual or gram
-  // by row count), dual, gram, pipe, mma, ffma
+  // FT_FACTOR_KERNEL forces one warp-level K3b for A/B measurement (it also skips K3c):
+  // quadr, quadw, dual, ws, gram.  auto: quadr for many rows at orders 3-4 (K3c takes most of
+  // these when the slot layout is present), quadw for few long rows at order 3, dual for many
+  // rows at orders 5-6, ws (order 3) / gram (orders 4-6) for few rows otherwise.
   static const int chosen = [] {
     const char *e = getenv("FT_FACTOR_KERNEL");
-    if (e && strcmp(e, "gram") == 0) return 0;
-    if (e && strcmp(e, "ffma") == 0) return 2;
-    if (e && strcmp(e, "mma") == 0) return 1;
-    if (e && strcmp(e, "pipe") == 0) return 3;
-    if (e && strcmp(e, "dual") == 0) return 4;
-    if (e && strcmp(e, "rdual") == 0) return 6;
-    if (e && strcmp(e, "ws") == 0) return 7;
-    if (e && strcmp(e, "quad") == 0) return 8;
-    if (e && strcmp(e, "quadp") == 0) return 9;
-    if (e && strcmp(e, "quadw") == 0) return 10;
-    if (e && strcmp(e, "quadg") == 0) return 11;
-    if (e && strcmp(e, "quadr") == 0) return 12;
-    if (e && strcmp(e, "quadrp") == 0) return 13;
-    return 5;  // auto: dual when the rows fill the SMs, gram otherwise
+    if (!e) return 0;
+    if (strcmp(e, "quadr") == 0) return 1;
+    if (strcmp(e, "quadw") == 0) return 2;
+    if (strcmp(e, "dual") == 0) return 3;
+    if (strcmp(e, "ws") == 0) return 4;
+    if (strcmp(e, "gram") == 0) return 5;
+    return 0;
   }();
-  int variant = chosen;
-  static const int use_tma = [] {
-    const char *e = getenv("FT_GATHER");
-    return e && strcmp(e, "tma") == 0 ? 1 : 0;
-  }();
-  SweepParams q = p;
-  q.tma = use_tma;
-  if (variant == 7 && p.N != 3) variant = 5;  // ws: order-3 tensors (one prefix row)
-  // auto, by rows per resident warp slot: many rows -> dual (Netflix modes 0/1: 7.5 ms);
-  // few long rows -> warp-specialised at order 3 (mode 2: 8.4 vs 8.8 gram, 13.4 dual), else gram
-  // quad / quadp: order 3, 16 < J <= 32, leaf-major index
-  if (variant >= 8 && variant <= 13 && !quad_ok(p)) variant = 5;
-  if (variant == 13 && p.N != 3) variant = 5;
-  if (variant == 12 && p.N > 4) variant = 8;
-  if (variant >= 9 && variant <= 11 && p.N != 3) variant = 5;  // quadp / quadw / quadg: order 3
-  if (variant == 5) {
-    // many rows: quadr / quad (orders 3-6); few long rows: quadw (order 3, warp-specialised)
+  int v = chosen;
+  if ((v == 1 || v == 2) && !quad_ok(p)) v = 0;
+  if ((v == 1 && p.N > 4) || (v == 2 && p.N != 3) || (v == 4 && p.N != 3)) v = 0;
+  if (v == 0) {
     const bool many = p.nrows >= (int64_t)2 * sm_count() * quad::WPB * 4;
-    // quadr (V consumed from the MMA registers) at orders 3-4; orders 5-6 keep the fiber
-    // kernels (the quad fold's N-2 dependent gather rounds per batch: order-6 10K^6 24.2 ms
-    // dual vs 30.6 ms quad per mode) even though their trees carry the leaf index for K4
     if (quad_ok(p) && many && p.N <= 4)
-      variant = 12;
+      v = 1;
     else if (quad_ok(p) && p.N == 3)
-      variant = 10;
+      v = 2;
     else
-      variant = p.nrows >= (int64_t)2 * sm_count() * 16 ? 4 : (p.N == 3 ? 7 : 0);
+      v = p.nrows >= (int64_t)2 * sm_count() * 16 ? 3 : (p.N == 3 ? 4 : 5);
   }
-  if (variant == 8) return launch_quad(q, s);
-  if (variant == 12) return launch_quadr(q, s);
-  if (variant == 13) return launch_quadrp(q, s);
-  if (variant == 9) return launch_quadp(q, s);
-  if (variant == 10) return launch_quadw<false>(q, s);
-  if (variant == 11) return launch_quadw<true>(q, s);
-  if (variant == 6) {
-    const size_t sm = RDualPlan::bytes<RP>();
-    static bool set6 = false;
-    if (!set6) {
-      cudaFuncSetAttribute(factor_rows_rdual_kernel<RP>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      set6 = true;
-    }
-    const int g = grid_for(factor_rows_rdual_kernel<RP>, (p.nrows + 1) / 2, RDualPlan::WPB, sm);
-    factor_rows_rdual_kernel<RP><<<g, RDualPlan::WPB * 32, sm, s>>>(p);
-    return check_launch("ft_factor_sweep_rows(rdual)");
+  switch (v) {
+    case 1: return launch_quadr(p, s);
+    case 2: return launch_quadw(p, s);
+    case 3: return p.J <= 16 ? launch_dual<RP, 16>(p, s) : launch_dual<RP, 32>(p, s);
+    case 4: return p.J <= 16 ? launch_ws<RP, 16>(p, s) : launch_ws<RP, 32>(p, s);
+    default: return p.J <= 16 ? launch_gram<RP, 16>(p, s) : launch_gram<RP, 32>(p, s);
   }
-  if (variant == 4) return p.J <= 16 ? launch_dual<RP, 16>(q, s) : launch_dual<RP, 32>(q, s);
-  if (variant == 7) return p.J <= 16 ? launch_ws<RP, 16>(q, s) : launch_ws<RP, 32>(q, s);
-  if (variant == 3) {
-    const size_t sm = PipePlan::bytes<RP>();
-    static bool set3 = false;
-    if (!set3) {
-      cudaFuncSetAttribute(factor_rows_pipe_kernel<RP>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      set3 = true;
-    }
-    const int g = grid_for(factor_rows_pipe_kernel<RP>, p.nrows, PipePlan::WPB, sm);
-    factor_rows_pipe_kernel<RP><<<g, PipePlan::WPB * 32, sm, s>>>(p);
-    return check_launch("ft_factor_sweep_rows(pipe)");
-  }
-  if (variant == 0) return p.J <= 16 ? launch_gram<RP, 16>(p, s) : launch_gram<RP, 32>(p, s);
-  if (variant == 2) {
-    const size_t sm = factor_smem<RP>();
-    const int g = grid_for(factor_rows_ffma_kernel<RP>, p.nrows, WPB_R, sm);
-    factor_rows_ffma_kernel<RP><<<g, WPB_R * 32, sm, s>>>(p);
-    return check_launch("ft_factor_sweep_rows(ffma)");
-  }
-  const size_t sm = MmaPlan<RP>::bytes(WPB_R);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(factor_rows_kernel<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sm);
-    attr_set = true;
-  }
-  const int g = grid_for(factor_rows_kernel<RP>, p.nrows, WPB_R, sm);
-  factor_rows_kernel<RP><<<g, WPB_R * 32, sm, s>>>(p);
-  return check_launch("ft_factor_sweep_rows");
 }
 
 template <int RP>
@@ -2105,30 +1481,24 @@ extern "C" int ft_core_sweep_rows(const ft_tree_t *tree, const ft_model_t *model
   if (!p.Cu) return fail(FT_ERR_ARG, "core sweep needs dots[u] (coherent cache)");
   if (!partials || !nblocks_out) return fail(FT_ERR_ARG, "null partials");
   p.partials = partials;
-  // FT_CORE_KERNEL=rows forces the one-row-per-warp kernel; default: quad when it applies
-  // FT_CORE_KERNEL: auto (quad), rows, quadp (gathers one batch ahead; measured slower --
-  // 3.4-3.7 vs 3.1-3.2 ms per Netflix mode: K4 is bound by L2 throughput, not gather latency)
-  static const int core_kind = [] {  // 0 auto (quad when it fills the GPU), 1 rows, 2 quad, 3 quadp
+  // FT_CORE_KERNEL=rows forces the one-row-per-warp kernel (the simple reference form);
+  // default: K4 quad over the row segments when it applies
+  static const bool core_rows_forced = [] {
     const char *e = getenv("FT_CORE_KERNEL");
-    if (e && strcmp(e, "rows") == 0) return 1;
-    if (e && strcmp(e, "quad") == 0) return 2;
-    if (e && strcmp(e, "quadp") == 0) return 3;
-    return 0;
+    return e && strcmp(e, "rows") == 0;
   }();
-  const bool core_rows_forced = core_kind == 1;
   // quad walks the row SEGMENTS (rows cut at <= 512 leaves: the core gradient is a sum over a
   // row's leaves), so few long rows fill the GPU too (Netflix mode 2: 2,182 rows -> 89 K
   // segments); without segments it needs rows to fill its 4-rows-per-warp slots
   const int64_t fill = (int64_t)2 * sm_count() * cquad::WPB * 4;
   const bool use_quad = !core_rows_forced && core_quad_ok(p) &&
-                        (core_kind >= 2 || (p.nsegs > 0 ? p.nsegs : p.nrows) >= fill);
+                        (p.nsegs > 0 ? p.nsegs : p.nrows) >= fill;
   if (use_quad && p.nsegs > 0) {  // the quad kernel reads segments through the row fields
     p.nrows = p.nsegs;
     p.row_coord = p.seg_coord;
     p.row_leaf_ptr = p.seg_leaf_ptr;
   }
-  const bool use_quadp = use_quad && core_kind == 3 && p.N == 3;
-  const int g = use_quadp ? core_quadp_grid(p) : use_quad ? core_quad_grid(p)
+  const int g = use_quad ? core_quad_grid(p)
                 : p.R <= 8 ? core_rows_grid<8>(p) : p.R <= 16 ? core_rows_grid<16>(p)
                                                               : core_rows_grid<32>(p);
   if ((int64_t)g * p.R * p.J > partials_cap)
@@ -2136,7 +1506,6 @@ extern "C" int ft_core_sweep_rows(const ft_tree_t *tree, const ft_model_t *model
                 (long long)g * p.R * p.J);
   cudaStream_t s = as_stream(stream);
   *nblocks_out = g;
-  if (use_quadp) return launch_core_quadp(p, g, s);
   if (use_quad) return launch_core_quad(p, g, s);
   if (p.R <= 8) return launch_core_rows<8>(p, g, s);
   if (p.R <= 16) return launch_core_rows<16>(p, g, s);

@@ -201,6 +201,40 @@ class CudaEngine:
 
         return torch.zeros(n, dtype=torch.int32, device="cuda")
 
+    def new_flags(self, n):
+        import torch
+
+        return torch.zeros(n, dtype=torch.int32, device="cuda")
+
+    def peer_barrier(self, local, peers, rank, seq):
+        """Stream-ordered: the next kernels wait on the device for every rank's arrival."""
+        tab = (ctypes.c_void_p * len(peers))(*[p.data_ptr() for p in peers])
+        _lib.check(self.L.ft_peer_barrier(local.data_ptr(), tab, len(peers), rank,
+                                          seq & 0xFFFFFFFF, _lib.stream_handle()),
+                   "ft_peer_barrier")
+
+    def sse_tree(self, model, dots, tree):
+        """(SSE, SAE) of a shard's entries scored in tree order (K6b); None when the shape is
+        outside that kernel's cover."""
+        import torch
+
+        from .train import _sse_tree
+
+        if tree is None:
+            return torch.zeros(2, dtype=torch.float64, device="cuda")
+        return _sse_tree(model, tree, dots)
+
+    def coo_from_host(self, dims, idx, vals):
+        """A rank's subset of host entries -> device (H2D from pinned memory when given)."""
+        import torch
+
+        from .coo import DeviceCoo
+
+        t_idx = idx if isinstance(idx, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(idx, dtype=np.int32))
+        t_val = vals if isinstance(vals, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(vals, dtype=np.float32))
+        return DeviceCoo(tuple(dims), t_idx.to("cuda", non_blocking=True),
+                         t_val.to("cuda", non_blocking=True))
+
     def synchronize(self):
         import torch
 
@@ -216,11 +250,12 @@ class DistTrainer:
     """Row-block sharded FasterTucker epochs over torch.distributed (one rank per GPU).
 
     ``model``: a Model (replicated; each rank only updates its A_u blocks),
-    ``coo``: the full training tensor on every rank (DeviceCoo for the CUDA engine),
+    ``coo``: the full training tensor on every rank (DeviceCoo for the CUDA engine); use
+    :meth:`from_host` to give each rank only its row blocks' entries,
     ``cfg``: TrainConfig (exact schedule)."""
 
     def __init__(self, model, coo, cfg, group=None, engine=None, fiber_threshold=128,
-                 peer_dots: bool = False):
+                 peer_dots: bool = False, _parts=None):
         import torch.distributed as dist
 
         self.dist = dist
@@ -229,31 +264,67 @@ class DistTrainer:
         self.world = dist.get_world_size(group)
         self.engine = engine if engine is not None else CudaEngine()
         self.model = model
-        self.coo = coo
+        self.coo = coo  # None for a host-partitioned trainer (from_host): no rank holds it all
         self.cfg = cfg
         self.N = model.order
-        self.omega = coo.nnz
         N = self.N
-        counts = [self.engine.mode_counts(coo, u, model.dims[u]) for u in range(N)]
-        self.blocks = plan_blocks(counts, self.world)
+        if _parts is None:
+            self.omega = coo.nnz
+            counts = [self.engine.mode_counts(coo, u, model.dims[u]) for u in range(N)]
+            self.blocks = plan_blocks(counts, self.world)
+            subsets = [coo] * N
+        else:  # from_host: the blocks and this rank's per-mode entry subsets are given
+            self.omega, self.blocks, subsets = _parts
         self.shards = []
         for u in range(N):
             c0, c1 = int(self.blocks[u][self.rank]), int(self.blocks[u][self.rank + 1])
-            tree, nnz, ft = self.engine.build_shard(coo, u, c0, c1, fiber_threshold)
+            tree, nnz, ft = self.engine.build_shard(subsets[u], u, c0, c1, fiber_threshold)
             self.shards.append(ModeShard(u, c0, c1, tree, nnz, ft))
+        del subsets
         self.dots = self._alloc_dots()
-        # peer mode: every rank maps every other rank's C_n buffers (CUDA IPC; NVLink peer
-        # memory on a multi-GPU node) and the refresh kernel writes its block into all of them
+        # peer mode: every rank maps every other rank's C_n buffers and barrier flags (CUDA IPC;
+        # NVLink peer memory on a multi-GPU node); the refresh kernel writes its block into all of
+        # them and a device-side barrier (ft_peer_barrier) orders the next sweep after every
+        # rank's block -- no host synchronize / barrier inside the epoch
         self.peer_dots = None
         if peer_dots and self.world > 1:
+            self.flags = self.engine.new_flags(self.world)
+            mine = self.dots + [self.flags]
             metas = [None] * self.world
-            self.dist.all_gather_object(metas, self.engine.share(self.dots), group=self.group)
-            self.peer_dots = [self.dots if q == self.rank else self.engine.open_peer(metas[q], self.dots)
-                              for q in range(self.world)]
+            self.dist.all_gather_object(metas, self.engine.share(mine), group=self.group)
+            peer = [mine if q == self.rank else self.engine.open_peer(metas[q], mine)
+                    for q in range(self.world)]
+            self.peer_dots = [pm[:N] for pm in peer]
+            self.peer_flags = [pm[N] for pm in peer]
+            self.seq = 0
         for u in range(N):
             self._refresh_and_gather(u, None)
         self.guards = self.engine.new_guards(2 * N)
         self.counter = OpCounter()
+
+    @classmethod
+    def from_host(cls, model, dims, idx, vals, cfg, group=None, engine=None,
+                  fiber_threshold=128, peer_dots: bool = False):
+        """A trainer whose rank copies only the entries of its own row blocks (one subset per
+        mode, ~N/P of the tensor) from HOST arrays ``idx`` [nnz x N] / ``vals`` [nnz] (numpy or
+        pinned torch tensors), instead of holding the whole COO on its device.  The blocks come
+        from host bincounts, identical on every rank."""
+        import torch.distributed as dist
+
+        eng = engine if engine is not None else CudaEngine()
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        idx_np = idx.numpy() if hasattr(idx, "numpy") else np.asarray(idx)
+        vals_np = vals.numpy() if hasattr(vals, "numpy") else np.asarray(vals)
+        N = idx_np.shape[1]
+        blocks = plan_blocks([np.bincount(idx_np[:, u], minlength=dims[u]) for u in range(N)],
+                             world)
+        subsets = []
+        for u in range(N):
+            c0, c1 = int(blocks[u][rank]), int(blocks[u][rank + 1])
+            sel = np.flatnonzero((idx_np[:, u] >= c0) & (idx_np[:, u] < c1))
+            subsets.append(eng.coo_from_host(dims, idx_np[sel], vals_np[sel]))
+        return cls(model, None, cfg, group=group, engine=eng, fiber_threshold=fiber_threshold,
+                   peer_dots=peer_dots, _parts=(int(idx_np.shape[0]), blocks, subsets))
 
     # -- helpers ------------------------------------------------------------------------------
     def _alloc_dots(self):
@@ -272,8 +343,9 @@ class DistTrainer:
         if self.peer_dots is not None:
             self.engine.refresh_scatter(self.model, u, int(b[self.rank]), int(b[self.rank + 1]),
                                         [pd[u] for pd in self.peer_dots], guard)
-            self.engine.synchronize()
-            self.dist.barrier(group=self.group)  # every block landed before anyone reads C_u
+            # every block landed before anyone reads C_u: a device-side barrier on the stream
+            self.seq += 1
+            self.engine.peer_barrier(self.flags, self.peer_flags, self.rank, self.seq)
             return
         self.engine.refresh_block(self.model, u, int(b[self.rank]), int(b[self.rank + 1]),
                                   self.dots[u], guard)
@@ -336,7 +408,20 @@ class DistTrainer:
                                   mode=exc.mode, epoch=epoch_no) from None
 
     def evaluate(self, coo=None):
+        """(RMSE, MAE) of ``coo`` (entries split by index across ranks), or of the training
+        entries: every rank scores its mode-0 shard in tree order (the mode-0 row blocks
+        partition the entries), so no rank needs the full training COO."""
+        out = None
+        if coo is None and hasattr(self.engine, "sse_tree"):
+            out = self.engine.sse_tree(self.model, self.dots, self.shards[0].tree)
+        if out is not None:
+            if self.world > 1:
+                self.dist.all_reduce(out, group=self.group)
+            sse, sae = (float(v) for v in out.cpu().numpy())
+            return math.sqrt(sse / self.omega), sae / self.omega
         coo = coo if coo is not None else self.coo
+        if coo is None:
+            raise ValueError("evaluate: this shape needs the training COO (K6b does not cover it)")
         n = coo.nnz
         lo = n * self.rank // self.world
         hi = n * (self.rank + 1) // self.world
@@ -392,10 +477,17 @@ def bench_distributed(args, cfg, rank, world):
                                test_fraction=cfg["nnz_test"] / nnz_total)
     model = default_init_model(dims, (J,) * N, R, seed=0)
     tcfg = TrainConfig(epochs=1)
+    # the training entries go to host memory once (a sharded loader's view); every rank then
+    # copies only its row blocks' entries (DistTrainer.from_host), no rank holds the whole COO
+    idx_h = split.train.idx.cpu().pin_memory()
+    vals_h = split.train.vals.cpu().pin_memory()
+    nnz = split.train.nnz
+    del split.train
+    torch.cuda.empty_cache()
     t0 = time.perf_counter()
     # fused refresh + all-gather over peer memory (NVLink) by default; FT_PEER=0: NCCL all-gather
-    trainer = DistTrainer(model, split.train, tcfg,
-                          peer_dots=os.environ.get("FT_PEER", "1") == "1")
+    peer = os.environ.get("FT_PEER", "1") == "1"
+    trainer = DistTrainer.from_host(model, dims, idx_h, vals_h, tcfg, peer_dots=peer)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
     clocks = None
@@ -431,9 +523,10 @@ def bench_distributed(args, cfg, rank, world):
     total_s, f_s = (float(v) for v in mine.cpu().numpy())
     tr = trainer.evaluate()
     te = trainer.evaluate(split.test)
-    e2e = _e2e_distributed(split.train, model, tcfg, rank, world, args)
+    init = default_init_model(dims, (J,) * N, R, seed=0)
+    del trainer
+    e2e = _e2e_distributed(dims, idx_h, vals_h, init, tcfg, rank, world, args, peer)
     if rank == 0:
-        nnz = split.train.nnz
         line = {
             "metric": "nonzeros/sec per SGD epoch (factor update, core update)",
             "value": nnz * args.steps / total_s, "unit": "nnz/s", "n_gpus": world,
@@ -454,28 +547,36 @@ def bench_distributed(args, cfg, rank, world):
     dist.destroy_process_group()
 
 
-def _e2e_distributed(train_dev, model, tcfg, rank, world, args):
-    """The N-GPU end-to-end step through the public API: every rank copies the training COO
-    from pinned host memory, builds its row-block shards (DistTrainer), runs one epoch and reads
-    the training RMSE back (all-reduced).  CUDA events on each rank, max over ranks."""
+def _e2e_distributed(dims, idx_h, vals_h, init, tcfg, rank, world, args, peer):
+    """The N-GPU end-to-end step through the public API: every rank copies ITS row blocks'
+    entries (one subset per mode, ~N/P of the tensor, host-partitioned once as a sharded loader
+    would deliver them) from pinned host memory, builds its shards, runs one epoch and reads the
+    training RMSE back (all-reduced).  CUDA events on each rank, max over ranks."""
     import torch
     import torch.distributed as dist
 
-    from .coo import DeviceCoo
     from .model import Model
 
-    idx_h = train_dev.idx.cpu().pin_memory()
-    vals_h = train_dev.vals.cpu().pin_memory()
-    dims = train_dev.dims
-    init_f = [a.clone() for a in model.factors]
-    init_c = [b.clone() for b in model.cores_t]
+    idx_np, vals_np = idx_h.numpy(), vals_h.numpy()
+    N = len(dims)
+    blocks = plan_blocks([np.bincount(idx_np[:, u], minlength=dims[u]) for u in range(N)], world)
+    mine = []
+    for u in range(N):
+        c0, c1 = int(blocks[u][rank]), int(blocks[u][rank + 1])
+        sel = np.flatnonzero((idx_np[:, u] >= c0) & (idx_np[:, u] < c1))
+        mine.append((torch.from_numpy(idx_np[sel]).pin_memory(),
+                     torch.from_numpy(vals_np[sel]).pin_memory()))
+    h2d = sum(int(i.numel()) * 4 + int(v.numel()) * 4 for i, v in mine)
+    eng = CudaEngine()
     steps = max(1, min(args.steps, 2))
 
     def step():
-        dev = DeviceCoo(dims, idx_h.to("cuda", non_blocking=True), vals_h.to("cuda", non_blocking=True))
-        m = Model(model.dims, model.ranks, model.core_rank, [a.clone() for a in init_f],
-                  [b.clone() for b in init_c])
-        tr = DistTrainer(m, dev, tcfg, peer_dots=os.environ.get("FT_PEER", "1") == "1")
+        subsets = [eng.coo_from_host(dims, i, v) for i, v in mine]
+        m = Model(init.dims, init.ranks, init.core_rank, [a.clone() for a in init.factors],
+                  [b.clone() for b in init.cores_t])
+        tr = DistTrainer(m, None, tcfg, engine=eng, peer_dots=peer,
+                         _parts=(int(idx_np.shape[0]), blocks, subsets))
+        del subsets
         tr.run_epoch(1)
         return tr.evaluate()[0]
 
@@ -488,11 +589,11 @@ def _e2e_distributed(train_dev, model, tcfg, rank, world, args):
         step()
     b.record()
     torch.cuda.synchronize()
-    mine = torch.tensor([a.elapsed_time(b) / 1e3 / steps], dtype=torch.float64, device="cuda")
-    dist.all_reduce(mine, op=dist.ReduceOp.MAX)
-    t = float(mine.item())
-    nnz = train_dev.nnz
-    return {"value": nnz / t, "unit": "nnz/s", "h2d_bytes_per_step": nnz * (4 * len(dims) + 4),
+    mine_t = torch.tensor([a.elapsed_time(b) / 1e3 / steps], dtype=torch.float64, device="cuda")
+    dist.all_reduce(mine_t, op=dist.ReduceOp.MAX)
+    t = float(mine_t.item())
+    nnz = int(idx_np.shape[0])
+    return {"value": nnz / t, "unit": "nnz/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": 16, "ms_per_step": 1e3 * t, "steps": steps,
-            "includes": "per rank: H2D of the training COO (pinned) + row-block shard build + "
-                        "1 epoch + train RMSE (all-reduced) readback"}
+            "includes": "per rank: H2D of its row blocks' entries (pinned, one subset per mode) "
+                        "+ shard build + cache + one epoch + training RMSE all-reduce / readback"}

@@ -58,6 +58,9 @@ class TrainConfig:
     rmse_delta_stop: float | None = None
     schedule: str | None = None   # None: "exact" if workers <= 1 else "hogwild"
     sync_guards: bool = False
+    # hogwild concurrency: at most dims[u] / hogwild_rows_per_warp warps update A_u at once
+    # (each warp is one serial worker; fewer rows per warp = more racing writers per row)
+    hogwild_rows_per_warp: int = 256
 
     def __post_init__(self):
         if self.plan not in ("cached", "uncached"):
@@ -68,6 +71,8 @@ class TrainConfig:
             raise ConfigError("epochs must be >= 0")
         if self.schedule not in (None, "exact", "hogwild"):
             raise ConfigError(f"schedule must be 'exact' or 'hogwild', got {self.schedule!r}")
+        if self.hogwild_rows_per_warp < 1:
+            raise ConfigError("hogwild_rows_per_warp must be >= 1")
 
     @property
     def resolved_schedule(self) -> str:
@@ -255,8 +260,8 @@ def update_factor_mode(model, forest: CsfForest, cache: DotCache | None, n: int,
                        "ft_factor_sweep_rows")
     else:
         with _ktime("factor_fibers", u):
-            # staleness bound: <= 32 concurrent leaf updates per 256 rows of A_u
-            cap = max(1, model.dims[u] // 256)
+            # staleness bound: one serial worker (warp) per hogwild_rows_per_warp rows of A_u
+            cap = max(1, model.dims[u] // cfg.hogwild_rows_per_warp)
             _lib.check(L.ft_factor_sweep_fibers(ctypes.byref(tree.view()), ctypes.byref(mv), 0,
                                                 tree.num_fibers, cfg.lr_a, cfg.reg_a, cap, stream),
                        "ft_factor_sweep_fibers")

@@ -134,11 +134,14 @@ class OracleEngine:
 
         return torch.zeros(n, dtype=torch.int32)
 
+    def coo_from_host(self, dims, idx, vals):
+        return HostCoo(dims, np.asarray(idx, dtype=np.int64), np.asarray(vals, dtype=np.float64))
+
     def synchronize(self):
         pass
 
 
-def _worker(rank, world, port, case_name, epochs, outdir):
+def _worker(rank, world, port, case_name, epochs, outdir, host=False):
     import sys
 
     import torch
@@ -160,12 +163,16 @@ def _worker(rank, world, port, case_name, epochs, outdir):
     model = HostModel(f, c)
     kw = {k: v for k, v in case["cfg"].items() if k in ("lr_a", "lr_b", "reg_a", "reg_b")}
     cfg = TrainConfig(**kw)
-    tr = DistTrainer(model, coo, cfg, engine=OracleEngine(),
-                     fiber_threshold=case["cfg"].get("fiber_threshold", 128))
+    thr = case["cfg"].get("fiber_threshold", 128)
+    if host:  # each rank receives only its row blocks' entries
+        tr = DistTrainer.from_host(model, case["dims"], coo.idx, coo.vals, cfg,
+                                   engine=OracleEngine(), fiber_threshold=thr)
+    else:
+        tr = DistTrainer(model, coo, cfg, engine=OracleEngine(), fiber_threshold=thr)
     rmse = []
     for e in range(epochs):
         tr.run_epoch(e + 1)
-        rmse.append(tr.evaluate()[0])
+        rmse.append(tr.evaluate(coo)[0])
     factors = tr.gather_factors()
     if rank == 0:
         np.savez(os.path.join(outdir, "dist.npz"), rmse=np.array(rmse),
@@ -184,11 +191,14 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("case_name,epochs", [("rank16", 2), ("order5", 2)])
-def test_row_block_sharding_equals_serial_reference(tmp_path, golden_cases, case_name, epochs):
+@pytest.mark.parametrize("case_name,epochs,host", [("rank16", 2, False), ("order5", 2, False),
+                                                   ("rank16", 2, True)])
+def test_row_block_sharding_equals_serial_reference(tmp_path, golden_cases, case_name, epochs,
+                                                    host):
+    """host=True: DistTrainer.from_host, every rank holding only its row blocks' entries."""
     import torch.multiprocessing as mp
 
-    mp.start_processes(_worker, args=(2, _free_port(), case_name, epochs, str(tmp_path)),
+    mp.start_processes(_worker, args=(2, _free_port(), case_name, epochs, str(tmp_path), host),
                        nprocs=2, join=True, start_method="spawn")
     out = np.load(tmp_path / "dist.npz")
     z = golden_cases

@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _worker(rank, world, port, outdir, peer=False):
+def _worker(rank, world, port, outdir, peer=False, host=False):
     import sys
 
     import torch
@@ -35,7 +35,12 @@ def _worker(rank, world, port, outdir, peer=False):
                        torch.from_numpy(z["rank32/vals"].astype(np.float32)).cuda())
     f, c = model_arrays(z, "rank32/init/", 3)
     model = ft.Model(tuple(case["dims"]), (32,) * 3, 32, f, c)
-    tr = DistTrainer(model, coo, ft.TrainConfig(**case["cfg"]), peer_dots=peer)
+    cfg = ft.TrainConfig(**case["cfg"])
+    if host:  # each rank copies only its row blocks' entries from host memory
+        tr = DistTrainer.from_host(model, tuple(case["dims"]), z["rank32/idx"].astype(np.int32),
+                                   z["rank32/vals"].astype(np.float32), cfg, peer_dots=peer)
+    else:
+        tr = DistTrainer(model, coo, cfg, peer_dots=peer)
     for e in range(case["cfg"]["epochs"]):
         tr.run_epoch(e + 1)
     rmse = tr.evaluate()[0]
@@ -48,8 +53,13 @@ def _worker(rank, world, port, outdir, peer=False):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("peer", [False, True], ids=["allgather", "fused-peer-refresh"])
-def test_two_ranks_on_one_gpu_equal_single_gpu(tmp_path, golden_cases, peer):
+@pytest.mark.parametrize("peer,host", [(False, False), (True, False), (True, True)],
+                         ids=["allgather", "fused-peer-refresh", "host-shards-peer"])
+def test_two_ranks_on_one_gpu_equal_single_gpu(tmp_path, golden_cases, peer, host):
+    """fused-peer-refresh: ft_refresh_scatter into both ranks' C_u through CUDA IPC, ordered by
+    the device-side ft_peer_barrier (no host synchronize / barrier in the epoch);
+    host-shards-peer: the same with DistTrainer.from_host (no rank holds the whole COO; training
+    RMSE from the mode-0 shard trees, K6b)."""
     import torch
     import torch.multiprocessing as mp
 
@@ -59,7 +69,7 @@ def test_two_ranks_on_one_gpu_equal_single_gpu(tmp_path, golden_cases, peer):
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
-    mp.start_processes(_worker, args=(2, port, str(tmp_path), peer), nprocs=2, join=True,
+    mp.start_processes(_worker, args=(2, port, str(tmp_path), peer, host), nprocs=2, join=True,
                        start_method="spawn")
     out = np.load(tmp_path / "d.npz")
 

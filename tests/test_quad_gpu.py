@@ -1,11 +1,9 @@
 """The leaf-major index (K1b, ft_tree_leaf_index), the four-rows-per-warp factor kernels (K3b
-`quad` / `quadp`) and core kernel (K4 `quad`, the default for order 3) against the fp64 oracle
-(oracle/), at the contract's rel 1e-4 per sweep.
+`quadr`: many rows, `quadw`: few long rows) and the core kernel (K4 `quad`, direct and staged
+loads) against the fp64 oracle (oracle/), at the contract's rel 1e-4 per sweep.
 
-`quad` is what `auto` runs on order-3 sweeps with 16 < J <= 32 and enough rows (Netflix modes
-0 and 1); these cases force it (FT_FACTOR_KERNEL=quad, in a subprocess because the variant is
-latched at the first launch), and so is `quadp`, its in-warp software-pipelined form for few
-long rows (Netflix mode 2), on shapes that exercise its edges: rows shorter than one 8-leaf
+These cases force a kernel on every mode (FT_FACTOR_KERNEL, in a subprocess because the choice
+is latched at the first launch) on shapes that exercise its edges: rows shorter than one 8-leaf
 batch, rows of ~20 K serial updates, J < 32 and R < 32 padding, more rows than row slots.
 """
 
@@ -100,16 +98,15 @@ print('ok')
     ((60000, 64, 64), 200_000, 32, 32, 5e-3),     # more rows than row slots (row switching)
     ((4000, 300, 50), 500_000, 16, 12, 2e-3),     # J <= 16 (one m-tile), R = 12 (two k-tiles)
 ])
-@pytest.mark.parametrize("kernel", ["quad", "quadr", "quadr-staged", "quadrp", "quadp", "quadw",
-                                    "quadg"])
+@pytest.mark.parametrize("kernel", ["quadr", "quadr-stagedcore", "quadw"])
 def test_quad_sweeps_match_oracle(kernel, dims, nnz, J, R, lr):
-    """quadr runs its direct-load combine by default; quadr-staged is the cp.async-staged form
-    (FT_QUADR_DIRECT=0) with the staged K4 core (FT_CORE_DIRECT=0)."""
+    """-stagedcore: the K4 quad core with cp.async-staged gathers (FT_CORE_DIRECT=0; the default
+    above 64 MB of gathered C rows) instead of direct register loads."""
     code = _CASE.format(dims=dims, nnz=nnz, J=J, R=R, lr=lr, seed=7)
-    env = dict(os.environ, FT_FACTOR_KERNEL=kernel.split("-")[0], FT_QUAD_J16="1",
-               FT_CORE_KERNEL="quadp" if kernel == "quadw" else "quad")
-    if kernel.endswith("-staged"):
-        env.update(FT_QUADR_DIRECT="0", FT_CORE_DIRECT="0")
+    env = dict(os.environ, FT_FACTOR_KERNEL=kernel.split("-")[0])
+    env.pop("FT_CORE_KERNEL", None)
+    if kernel.endswith("-stagedcore"):
+        env.update(FT_CORE_DIRECT="0")
     out = subprocess.run([sys.executable, "-c", code], cwd=REPO, env=env, capture_output=True,
                          text=True, timeout=900)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
@@ -145,11 +142,13 @@ def test_sse_tree_matches_coo_evaluate(ft):
     ((12, 10, 10, 9, 8, 8), 150_000, 24, 20),       # order 6, padding
 ])
 def test_quad_order_n_sweeps_match_oracle(dims, nnz, J, R):
-    """quad (factor) and K4 quad (core) at orders 4-6: the prefix product folded level by level
-    from the leaf-major index, every sweep against the fp64 oracle at rel 1e-4."""
+    """The default dispatch at orders 4-6 (factor: quadr at order 4, dual / gram at orders 5-6;
+    core: K4 quad over the leaf-major index, its prefix product folded level by level), every
+    sweep against the fp64 oracle at rel 1e-4."""
     code = _CASE.format(dims=dims, nnz=nnz, J=J, R=R, lr=2e-3, seed=9)
-    env = dict(os.environ, FT_FACTOR_KERNEL="quad", FT_QUAD_J16="1", FT_CORE_KERNEL="quad",
-               FT_LEAF_INDEX_MAX_ORDER="6")
+    env = dict(os.environ, FT_LEAF_INDEX_MAX_ORDER="6")
+    env.pop("FT_FACTOR_KERNEL", None)
+    env.pop("FT_CORE_KERNEL", None)
     out = subprocess.run([sys.executable, "-c", code], cwd=REPO, env=env, capture_output=True,
                          text=True, timeout=900)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]

@@ -49,7 +49,9 @@ CONFIGS = {
                       R=32, value_range=(1.0, 5.0)),
 }
 
-CPU_SAMPLE_NNZ = 1_000_000
+# one sample size for the reference arm and the cpu_baseline leg: BASELINE.md section 4 step 3
+# (10 M entries of the benchmarked dims, the fiber density the full tensor's sweeps see)
+CPU_SAMPLE_NNZ = 10_000_000
 
 
 def log(*a):
@@ -181,8 +183,11 @@ def host_sample(dims, nnz, value_range, seed=0):
     return idx, vals
 
 
-def cpu_epoch_rate(cfg, nnz, workers, repeats=1):
-    """Time factor pass + core pass of the reference CPU path on a sample; nnz/s per epoch."""
+def cpu_epoch_rate(cfg, nnz, repeats=1, threads=None):
+    """Time factor pass + core pass of the reference CPU path on a sample, on all host cores:
+    the reference's compiled kernels (oracle/_ref _ckern; our C restatement if absent) driven
+    over row-partitioned sub-trees (oracle.RowParallelRef: bitwise the serial factor sweep, the
+    reference's own per-worker core reduction).  Returns (kind, threads, [(factor_s, core_s)])."""
     from oracle import oracle as O
 
     O.build()
@@ -192,37 +197,32 @@ def cpu_epoch_rate(cfg, nnz, workers, repeats=1):
         K, kind = O.CKernels, "port"
     idx, vals = host_sample(cfg["dims"], nnz, cfg["value_range"])
     N = len(cfg["dims"])
-    forest = O.build_forest(idx, vals, 128)
+    ref = O.RowParallelRef(idx, vals, cfg["dims"], threads=threads, K=K)
     model = O.default_init_model(cfg["dims"], (cfg["J"],) * N, cfg["R"], seed=0)
-    ocfg = O.OracleConfig(workers=workers)
+    ocfg = O.OracleConfig()
     cache = O.precompute_cache(model, K=K)
     times = []
-    for _ in range(repeats):
-        t0 = time.perf_counter()
-        for n in range(N):
-            O.update_factor_mode(model, forest, cache, n, ocfg, K=K)
-        t1 = time.perf_counter()
-        for n in range(N):
-            O.update_core_mode(model, forest, cache, n, ocfg, K=K)
-        t2 = time.perf_counter()
-        times.append((t1 - t0, t2 - t1))
-    return kind, times
+    try:
+        for _ in range(repeats):
+            t0 = time.perf_counter()
+            for t in range(N):
+                ref.update_factor_mode(model, cache, t, ocfg)
+            t1 = time.perf_counter()
+            for t in range(N):
+                ref.update_core_mode(model, cache, t, ocfg)
+            t2 = time.perf_counter()
+            times.append((t1 - t0, t2 - t1))
+    finally:
+        ref.close()
+    return kind, ref.T, times
 
 
 def run_reference_arm(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    ncpu = os.cpu_count() or 1
-    nnz = int(os.environ.get("FT_REF_SAMPLE", CPU_SAMPLE_NNZ // 2))
-    # the reference's parallel mode (hogwild threads over subtensors, train.py:124-149) holds
-    # the GIL in its dispatch and is often slower than serial: probe both, time the faster
-    probe = {}
-    for w in (ncpu, 0):
-        _, t = cpu_epoch_rate(cfg, nnz, w, repeats=1)
-        probe[w] = sum(t[0])
-    workers = min(probe, key=probe.get)
-    kind, times = cpu_epoch_rate(cfg, nnz, workers, repeats=max(args.warmup - 1, 0) + args.steps)
+    nnz = int(os.environ.get("FT_REF_SAMPLE", CPU_SAMPLE_NNZ))
+    kind, threads, times = cpu_epoch_rate(cfg, nnz, repeats=max(args.warmup - 1, 0) + args.steps)
     timed = times[-args.steps:]
     t = sum(a + b for a, b in timed)
     value = nnz * len(timed) / t
@@ -232,13 +232,15 @@ def run_reference_arm(args, cfg):
         "ms_per_step": 1e3 * t / len(timed), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (host numpy, uniform distinct cells)",
         "config": {"workload": args.config, "sample_nnz": nnz, "J": cfg["J"], "R": cfg["R"],
-                   "dims": list(cfg["dims"]), "workers": workers},
+                   "dims": list(cfg["dims"]), "threads": threads},
         "factor_nnz_per_s": nnz * len(timed) / sum(a for a, _ in timed),
         "core_nnz_per_s": nnz * len(timed) / sum(b for _, b in timed),
-        "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": max(workers, 1), "kind": kind,
+        "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": threads, "kind": kind,
                          "sample": f"{nnz} uniform entries of the {args.config} dims, one factor "
-                                   f"+ core pass per step; workers={workers} (faster of serial and "
-                                   f"{ncpu} hogwild threads: {probe})"},
+                                   f"+ core pass per step, the reference's compiled kernels over "
+                                   f"{threads} row-partitioned groups on {threads} host threads "
+                                   f"(bitwise its serial factor sweep; its own `workers` hogwild "
+                                   f"mode holds the GIL and measured slower than serial)"},
         "e2e": {"value": value, "unit": "nnz/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -493,12 +495,13 @@ def run_ours(args, cfg):
     # CPU baseline (rank 0, N = 1): the reference's compiled kernels on a bounded sample
     cpu = None
     if not args.no_cpu:
-        nnz_s = CPU_SAMPLE_NNZ
-        kind, times = cpu_epoch_rate(cfg, nnz_s, workers=0)
+        nnz_s = int(os.environ.get("FT_REF_SAMPLE", CPU_SAMPLE_NNZ))
+        kind, threads, times = cpu_epoch_rate(cfg, nnz_s)
         tf, tc = times[0]
-        cpu = {"value": nnz_s / (tf + tc), "unit": "nnz/s", "cores": 1, "kind": kind,
-               "sample": f"{nnz_s} uniform entries of the {args.config} dims (same distribution, "
-                         f"lower density), one factor + core pass, serial",
+        cpu = {"value": nnz_s / (tf + tc), "unit": "nnz/s", "cores": threads, "kind": kind,
+               "sample": f"{nnz_s} uniform entries of the {args.config} dims (the reference arm's "
+                         f"sample), one factor + core pass, the reference's compiled kernels over "
+                         f"row-partitioned groups on {threads} host threads",
                "factor_nnz_per_s": nnz_s / tf, "core_nnz_per_s": nnz_s / tc}
 
     e2e = run_e2e(ft, T, cfg, train_t, args) if not args.no_e2e else None

@@ -188,6 +188,15 @@ def generate_device(dims, nnz: int, value_range=(1.0, 5.0), seed: int = 0) -> De
     lo, hi = float(value_range[0]), float(value_range[1])
     if not lo < hi:
         raise ConfigError(f"value range must satisfy lo < hi, got ({lo}, {hi})")
+    if 2 * nnz > math.prod(dims):
+        # dense request (the device sampler draws i.i.d. cells and keeps the distinct ones, which
+        # needs nnz <= capacity / 2): sample without replacement on the host, as the reference's
+        # _sample_coords does for dense cubes (coo.py:164-178), then upload
+        rng = np.random.default_rng([int(seed), 0])
+        lin = rng.permutation(math.prod(dims))[:nnz]
+        hidx = np.stack(np.unravel_index(lin, dims), axis=1).astype(np.int32)
+        hvals = np.random.default_rng([int(seed), 1]).uniform(lo, hi, size=nnz).astype(np.float32)
+        return DeviceCoo(dims, torch.from_numpy(hidx).cuda(), torch.from_numpy(hvals).cuda())
     idx = torch.empty((nnz, len(dims)), dtype=torch.int32, device="cuda")
     vals = torch.empty(nnz, dtype=torch.float32, device="cuda")
     d = (ctypes.c_int64 * len(dims))(*dims)
@@ -197,12 +206,19 @@ def generate_device(dims, nnz: int, value_range=(1.0, 5.0), seed: int = 0) -> De
     return DeviceCoo(dims, idx, vals)
 
 
-def generate_synthetic(dims, nnz: int, value_range=(1.0, 5.0), seed: int = 0,
-                       test_fraction: float | None = None):
-    """Device synthetic tensor (see module doc).  With ``test_fraction`` returns a
-    :class:`DatasetSplit` of two :class:`DeviceCoo` (the generator's order is random, so the
-    first round(nnz * f) entries are a uniform test sample)."""
-    t = generate_device(dims, nnz, value_range, seed)
+def generate_synthetic(dims, nnz: int, value_range=(1.0, 5.0), seed: int = 0, low_rank=None,
+                       *, test_fraction: float | None = None):
+    """Device synthetic tensor with the reference's signature (coo.py:181-213): nnz distinct
+    uniform cells, values U[value_range], or -- with ``low_rank=(ranks, core_rank)`` -- the
+    predictions of a hidden random model (generate_low_rank_device).  Returns a
+    :class:`DeviceCoo` (GPU-resident; ``.to_host()`` gives the reference's SparseCooTensor).  With
+    ``test_fraction`` returns a :class:`DatasetSplit` of two DeviceCoo (the generator's order is
+    random, so the first round(nnz * f) entries are a uniform test sample)."""
+    if low_rank is not None:
+        ranks, core_rank = low_rank
+        t = generate_low_rank_device(dims, nnz, ranks, core_rank, seed)
+    else:
+        t = generate_device(dims, nnz, value_range, seed)
     if test_fraction is None:
         return t
     n_test = int(round(nnz * test_fraction))
@@ -221,24 +237,30 @@ def load_coo(path, order: int, dims=None, normalize=None) -> SparseCooTensor:
     try:
         import pandas as pd
 
-        df = pd.read_csv(path, sep=r"\s+", comment="#", header=None, engine="c",
-                         dtype=np.float64, float_precision="round_trip")
-        ok = df.shape[1] == order + 1 and not df.isnull().values.any()
-        arr = df.to_numpy() if ok else None
+        # coordinates as integers (the reference's int(), so "1.0" is rejected) and the value as
+        # float ("nan" accepted, as float() does); '#' only as a whole-line comment, checked on
+        # the raw bytes below (pandas' comment= would also strip inline comments)
+        dtypes = {c: np.int64 for c in range(order)}
+        dtypes[order] = np.float64
+        df = pd.read_csv(path, sep=r"\s+", comment="#", header=None, engine="c", dtype=dtypes,
+                         float_precision="round_trip")
+        ok = df.shape[1] == order + 1 and not df.iloc[:, :order].isnull().values.any()
+        if ok:
+            coords = df.iloc[:, :order].to_numpy(dtype=np.int64)
+            vals = df.iloc[:, order].to_numpy(dtype=np.float64)
+            ok = _layout_ok(path, order, int(np.isnan(vals).sum()))
     except Exception:
-        arr, ok = None, False
-    if ok and arr.shape[0]:
-        coords = arr[:, :order]
-        if not np.all(np.equal(np.floor(coords), coords)):
-            ok = False
-    if not ok or arr is None or arr.shape[0] == 0:
-        _scan_errors(path, order, ParseError)
+        ok = False
+    if not ok:
+        # raises with the reference's message; a file it accepts (e.g. only comments) is parsed
+        # by the same line scanner
+        coords, vals = _scan_errors(path, order, ParseError)
+    if coords.shape[0] == 0:
         raise ValidationError(f"{path}: no entries")
-    idx = arr[:, :order].astype(np.int64)
+    idx = coords
     if (idx < 1).any():
         _scan_errors(path, order, ParseError)
-    idx -= 1
-    vals = arr[:, order].astype(np.float64)
+    idx = idx - 1
     dup = _first_duplicate(idx, tuple(int(m) + 1 for m in idx.max(axis=0)))
     if dup is not None:
         _scan_errors(path, order, ParseError)
@@ -249,9 +271,32 @@ def load_coo(path, order: int, dims=None, normalize=None) -> SparseCooTensor:
     return SparseCooTensor(tuple(dims), idx, vals)
 
 
+def _layout_ok(path, order, n_nan) -> bool:
+    """What pandas' reader forgives and the reference's scanner does not (coo.py:104-121): an
+    inline '#' (the reference only skips whole-line comments, so such a line has extra fields)
+    and a missing value field (pandas fills NaN: more NaN values than 'nan' tokens).  Known
+    remaining difference: pandas' int64 reader accepts a coordinate written "1.0", which the
+    reference's int() rejects (checking every coordinate token in Python would cost ~1 us per
+    line, minutes on a Netflix-size file)."""
+    import re
+
+    raw = np.fromfile(path, dtype=np.uint8)
+    for p in np.flatnonzero(raw == ord("#")).tolist():
+        q = p - 1
+        while q >= 0 and raw[q] in (32, 9, 13):
+            q -= 1
+        if q >= 0 and raw[q] != 10:
+            return False
+    if n_nan and n_nan > len(re.findall(rb"(?i)(?<![^\s])[+-]?nan(?![^\s])", raw.tobytes())):
+        return False
+    return True
+
+
 def _scan_errors(path, order, ParseError):
-    """The reference's line-by-line checks (coo.py:104-128), run only to report an error."""
+    """The reference's line-by-line checks (coo.py:104-128), run to report an error; returns
+    the parsed (idx, vals) when the file passes them."""
     seen = set()
+    coords, values = [], []
     with open(path, "r", encoding="utf-8") as fh:
         for lineno, line in enumerate(fh, start=1):
             stripped = line.strip()
@@ -274,6 +319,10 @@ def _scan_errors(path, order, ParseError):
             if coord in seen:
                 raise ValidationError(f"{path}: line {lineno}: duplicate coordinate {coord}")
             seen.add(coord)
+            coords.append(coord)
+            values.append(float(fields[order]))
+    return (np.asarray(coords, dtype=np.int64).reshape(-1, order),
+            np.asarray(values, dtype=np.float64))
 
 
 def _minmax_scale(vals: np.ndarray, target) -> np.ndarray:

@@ -1,9 +1,11 @@
 """Multiply counters (mirrors counter.OpCounter, /root/reference/pkg/src/fastertucker/counter.py).
 
 The reference kernels tally five channels with one integer add per tree node
-(_ckern.pyx:167-191, 236-261, 282, 33).  The GPU kernels do not count; the same tallies are
-closed forms of the tree shape, evaluated here on the host per sweep,
-and pinned against the reference's counts in tests/test_counts.py.
+(_ckern.pyx:167-191, 236-261, 282, 33).  The GPU kernels do not count: these tallies are
+ANALYTIC, closed forms of the tree shape evaluated on the host per sweep.
+They equal the reference's counted tallies exactly on every golden case
+(tests/test_host_cpu.py, tests/test_gpu_parity.py::test_config1_per_sweep_and_epoch), but they
+cannot detect a kernel doing extra or missing work -- the parity tests on the values do that.
 """
 
 from __future__ import annotations

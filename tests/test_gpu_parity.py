@@ -259,10 +259,11 @@ def test_predict_batch_matches_reference(ft, golden_cases):
     np.testing.assert_allclose(out, z["predict/out"], rtol=2e-5, atol=2e-5)
 
 
-def test_hogwild_rmse_within_one_percent(ft, golden_config1, golden_cases):
-    """Hogwild schedule (K3a, racing row updates): RMSE after E epochs within 1% of the
-    reference's serial trajectory (north star); the reference's own hogwild tolerance is 15%
-    (test_trainer.py:262-277)."""
+def test_hogwild_rmse_fidelity(ft, golden_config1, golden_cases):
+    """Hogwild schedule (K3a, racing row updates at the default, uncapped concurrency): RMSE
+    after E epochs within 1 % of the reference's serial trajectory on BASELINE config 1 (north
+    star), and within 2 % as the median of 3 runs on the reference's own hogwild fixture
+    (its test_trainer.py:262-277 allows 15 %)."""
     z = golden_config1
     train = _dev_coo(ft, z["train_idx"], z["train_vals"], (1000,) * 3)
     test = _dev_coo(ft, z["test_idx"], z["test_vals"], (1000,) * 3)
@@ -276,13 +277,13 @@ def test_hogwild_rmse_within_one_percent(ft, golden_config1, golden_cases):
     zc = golden_cases
     case = next(c for c in manifest(zc) if c["name"] == "hogwild")
     dev = _dev_coo(ft, zc["hogwild/idx"], zc["hogwild/vals"], tuple(case["dims"]))
-    model = _model(ft, zc, "hogwild/init/", 3)
-    cfg = ft.TrainConfig(**case["cfg"], schedule="hogwild")
-    rows = ft.train(model, dev, cfg)
     ref_rmse = zc["hogwild/metrics"][-1, 1]
-    # 20 rows per mode, lr 0.05: one warp of 32 in-flight leaves already overlaps rows; the
-    # reference's own hogwild bound for this fixture is 15% (test_trainer.py:262-277)
-    assert abs(rows[-1].train_rmse - ref_rmse) / ref_rmse < 0.05
+    gaps = []
+    for _ in range(3):  # racing updates: every run differs
+        model = _model(ft, zc, "hogwild/init/", 3)
+        rows = ft.train(model, dev, ft.TrainConfig(**case["cfg"], schedule="hogwild"))
+        gaps.append(abs(rows[-1].train_rmse - ref_rmse) / ref_rmse)
+    assert float(np.median(gaps)) < 0.02, gaps
 
 
 def test_exact_schedule_is_deterministic(ft, golden_cases):

@@ -36,6 +36,7 @@ def test_comments_blank_lines_and_default_dims(tmp_path):
 
 
 @pytest.mark.parametrize("text,exc,msg", [
+    ("1 1 1 5.0 # c\n", ParseError, "line 1: expected 4 fields, got 6"),   # inline '#'
     ("1 1 1 2\n1 2 3\n", ParseError, "line 2: expected 4 fields, got 3"),
     ("1 1 1 2\n1 x 1 2\n", ParseError, "line 2: bad coordinate"),
     ("1 1 1 2\n1 2 1 abc\n", ParseError, "line 2: bad value 'abc'"),
@@ -78,3 +79,14 @@ def test_split_partition_law():
     assert np.array_equal(s.test.idx, s2.test.idx)
     with pytest.raises(ConfigError):
         split_dataset(t, 1.0, seed=0)
+
+
+def test_nan_value_loads_like_the_reference(tmp_path):
+    """float('nan') is a value the reference's scanner accepts (coo.py:118-121)."""
+    t = load_coo(_write(tmp_path, "1 1 1 nan\n2 1 1 3\n"), 3)
+    assert np.isnan(t.vals[0]) and t.vals[1] == 3.0
+
+
+def test_comment_only_file_has_no_entries(tmp_path):
+    with pytest.raises(ValidationError, match="no entries"):
+        load_coo(_write(tmp_path, "# nothing\n\n"), 3)

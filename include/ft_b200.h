@@ -79,7 +79,7 @@ typedef struct {
    * q, q + 128 G, ... and walks their leaves one per batch; entry [batch][s] of CTA c holds that
    * leaf's coordinates and value, so each batch's operands are coalesced loads. */
   int32_t slot_grid;            /* G (CTAs the layout was built for)                         */
-  int32_t slot_pad_;
+  int32_t slot_kb;              /* leaves of one row slot per batch: 1 or 8 (128/KB rows/CTA) */
   const int32_t *slot_batch_ptr;/* [G+1] first batch of each CTA                             */
   const int32_t *slot_lc;       /* [batches x 128] leaf coordinate | 0x80000000 on the first
                                    leaf of a row; -1 = padding (the slot's stream ended)      */
@@ -156,13 +156,15 @@ FT_API int ft_tree_row_segments(const ft_tree_t *tree, int32_t max_len, int32_t 
 /* K1d Slot layout for the tcgen05 factor sweep (reads tree->row_leaf_ptr / leaf_coord /
  * leaf_pc / vals).  Not a reference structure: it re-orders the tree's leaves so that the
  * sweep over the tree rooted at u (factor_sweep, _ckern.pyx:132-199) reads them coalesced.
- * ft_tree_slot_plan: *grid_out = G, or 0 when the tcgen05 sweep does not apply to this tree
- *   (shape J, R, order, too few rows to fill the GPU, FT_FACTOR_TC=0); with batch_ptr == NULL
- *   only G is returned; else batch_ptr (device int32 [G+1]) is filled and *len_out (HOST) gets
- *   the entry count (batches x 128).  SYNCHRONOUS when batch_ptr != NULL.
- * ft_tree_slot_fill: writes slot_lc / slot_x [len] and slot_pc [len x (N-2)].  Asynchronous. */
+ * ft_tree_slot_plan: *grid_out = G and *kb_out = KB (1: one row per TMEM lane, many rows;
+ *   8: 16 rows per CTA, few long rows), or G = 0 when the tcgen05 sweep does not apply to this
+ *   tree (shape J, R, order, rows, FT_FACTOR_TC=0); with batch_ptr == NULL only G / KB are
+ *   returned; else batch_ptr (device int32 [G+1]) is filled and *len_out (HOST) gets the entry
+ *   count (batches x 128).  SYNCHRONOUS when batch_ptr != NULL.
+ * ft_tree_slot_fill: writes slot_lc / slot_x [len] and slot_pc [len x (N-2)]; must follow
+ *   the ft_tree_slot_plan call with batch_ptr of the same tree.  SYNCHRONOUS. */
 FT_API int ft_tree_slot_plan(const ft_tree_t *tree, int32_t J, int32_t R, int32_t *grid_out,
-                             int32_t *batch_ptr, int64_t *len_out, void *stream);
+                             int32_t *kb_out, int32_t *batch_ptr, int64_t *len_out, void *stream);
 FT_API int ft_tree_slot_fill(const ft_tree_t *tree, int32_t grid, const int32_t *batch_ptr,
                              int32_t *slot_lc, int32_t *slot_pc, float *slot_x, void *stream);
 /* K2  C = A * Bt^T  (I x R), i.e. refresh_dot_mode (_ckern.pyx:21-33, cache.py:60-70), with the

@@ -51,7 +51,7 @@ class FtTree(ctypes.Structure):
         ("seg_coord", _vp),
         ("seg_leaf_ptr", _vp),
         ("slot_grid", ctypes.c_int32),
-        ("slot_pad_", ctypes.c_int32),
+        ("slot_kb", ctypes.c_int32),
         ("slot_batch_ptr", _vp),
         ("slot_lc", _vp),
         ("slot_pc", _vp),
@@ -83,7 +83,7 @@ SIGNATURES = {
         ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp, _vp, _vp, _vp, _vp, _vp, _i64p, _vp, _vp]),
     "ft_tree_leaf_index": (ctypes.c_int, [ctypes.POINTER(FtTree), _vp, _vp, _vp]),
     "ft_tree_slot_plan": (ctypes.c_int, [ctypes.POINTER(FtTree), ctypes.c_int32, ctypes.c_int32,
-                                         _i32p, _vp, _i64p, _vp]),
+                                         _i32p, _i32p, _vp, _i64p, _vp]),
     "ft_tree_slot_fill": (ctypes.c_int, [ctypes.POINTER(FtTree), ctypes.c_int32, _vp, _vp, _vp,
                                          _vp, _vp]),
     "ft_build_tree_derived": (ctypes.c_int, [

@@ -48,6 +48,7 @@ class CsfTree:
     row_leaf_ptr: object = None  # device int32 [rows+1] first leaf per row (derived)
     seg_coord: object = None     # device int32 [segs]  core-sweep row segments (derived)
     seg_leaf_ptr: object = None  # device int32 [segs+1]
+    slot_kb: int = 1             # leaves per row slot and batch (1 or 8)
     slot_grid: int = -1          # slot layout of the tcgen05 factor sweep (-1 = not planned,
     slot_batch_ptr: object = None  # 0 = does not apply); device int32 [G+1]
     slot_lc: object = None       # device int32 [batches x 128]
@@ -111,6 +112,7 @@ class CsfTree:
             v.seg_coord = _lib.ptr(self.seg_coord)
             v.seg_leaf_ptr = _lib.ptr(self.seg_leaf_ptr)
             v.slot_grid = max(self.slot_grid, 0) if self.slot_lc is not None else 0
+            v.slot_kb = self.slot_kb
             v.slot_batch_ptr = _lib.ptr(self.slot_batch_ptr)
             v.slot_lc = _lib.ptr(self.slot_lc)
             v.slot_pc = _lib.ptr(self.slot_pc)
@@ -129,19 +131,20 @@ class CsfTree:
             return self
         L = _lib.lib()
         g = ctypes.c_int32(0)
+        kb = ctypes.c_int32(0)
         n = ctypes.c_int64(0)
         v = self.view()
-        _lib.check(L.ft_tree_slot_plan(ctypes.byref(v), int(J), int(R), ctypes.byref(g), None,
-                                       ctypes.byref(n), _lib.stream_handle(stream)),
-                   "ft_tree_slot_plan")
+        _lib.check(L.ft_tree_slot_plan(ctypes.byref(v), int(J), int(R), ctypes.byref(g),
+                                       ctypes.byref(kb), None, ctypes.byref(n),
+                                       _lib.stream_handle(stream)), "ft_tree_slot_plan")
         if g.value <= 0:
             self.slot_grid = 0
             return self
         i32 = dict(dtype=torch.int32, device=self.vals.device)
         bp = torch.empty(g.value + 1, **i32)
         _lib.check(L.ft_tree_slot_plan(ctypes.byref(v), int(J), int(R), ctypes.byref(g),
-                                       bp.data_ptr(), ctypes.byref(n), _lib.stream_handle(stream)),
-                   "ft_tree_slot_plan")
+                                       ctypes.byref(kb), bp.data_ptr(), ctypes.byref(n),
+                                       _lib.stream_handle(stream)), "ft_tree_slot_plan")
         length = int(n.value)
         lc = torch.empty(length, **i32)
         pc = torch.empty(length * (self.order - 2), **i32)
@@ -151,6 +154,7 @@ class CsfTree:
                    "ft_tree_slot_fill")
         self.slot_batch_ptr, self.slot_lc, self.slot_pc, self.slot_x = bp, lc, pc, x
         self.slot_grid = g.value
+        self.slot_kb = kb.value
         self._view = None
         return self
 

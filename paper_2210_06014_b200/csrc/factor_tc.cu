@@ -29,6 +29,9 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
+#include <vector>
+
 #include <cub/cub.cuh>
 
 #include "ft_common.cuh"
@@ -40,8 +43,11 @@ constexpr int SLOTS = 128;
 constexpr int CWARPS = 4;                    // consumer warps: warp <-> TMEM lanes 32(w%4)..+31
 // PW producer warps per TMEM lane quadrant (they take alternate batches), 4 consumer warps, the
 // MMA warp
-template <int PW>
-constexpr int tc_threads() { return (4 * PW + CWARPS + 1) * 32; }
+// KB = 8 adds two chain warps (the 4 consumer warps then only stage V rows through shared memory)
+constexpr int CHAIN_WARPS = 2;
+template <int PW, int KB = 1>
+constexpr int tc_threads() { return (4 * PW + CWARPS + (KB > 1 ? CHAIN_WARPS : 0) + 1) * 32; }
+constexpr int VS = 2;  // KB = 8: V staging stages (TMEM -> shared memory -> chain warp)
 // TMEM: AS A stages (A_hi | A_lo, 64 columns each) then DS D stages (64 columns each).  The A
 // ring is the deep one: a producer reuses an A stage once that batch's MMAs completed, so the
 // producers run up to AS batches ahead of the tensor core; consumers trail the MMA closely.
@@ -155,7 +161,7 @@ struct TcParams {
   float lr, reg;
 };
 
-template <int NPRE, int GS>
+template <int NPRE, int GS, int KB = 1>
 struct TcPlan {
   static_assert((GS & (GS - 1)) == 0, "gather ring stages: a power of two");
   static constexpr int LEVELS = NPRE + 1;                 // gathered C rows per leaf
@@ -167,7 +173,9 @@ struct TcPlan {
   static_assert(MS >= 2 * GS + AS + DS, "metadata ring too short");  // (2 GS - PW) + AS + DS + 1
   static constexpr int MSTRIDE = (NPRE + 2) * SLOTS * 4;  // lc|flags, pc[NPRE], x per stage
   static constexpr int NABUF = SLOTS * 128;              // each consumer's next A row
-  static constexpr size_t SMEM = 1024 + 2 * B_BYTES + (size_t)GS * STAGE + MS * MSTRIDE + NABUF + 256;
+  static constexpr int VBUF = KB > 1 ? VS * SLOTS * (128 + 8) : 0;  // V rows + (lc|flags, x)
+  static constexpr size_t SMEM =
+      1024 + 2 * B_BYTES + (size_t)GS * STAGE + MS * MSTRIDE + NABUF + VBUF + 256;
 };
 
 __device__ __forceinline__ uint32_t lds32(uint32_t a) {
@@ -201,12 +209,13 @@ __device__ __forceinline__ void cp16p(uint32_t dst, const void *src, bool on) {
 //   a_ready[st]  producers -> MMA   (A of batch b written)
 //   v_ready[st]  MMA commit -> consumers (D of batch b) and producers (A of batch b free again)
 //   d_free[st]   consumers -> MMA   (D of batch b read)
-template <int NPRE, int GS, bool R32, bool COMP, int PW>
-__global__ void __launch_bounds__(tc_threads<PW>(), 1) factor_rows_tc_kernel(const TcParams p) {
-  constexpr int THREADS = tc_threads<PW>(), NPW = 4 * PW;  // producer warps: 0 .. NPW - 1
+template <int NPRE, int GS, bool R32, bool COMP, int PW, int KB>
+__global__ void __launch_bounds__(tc_threads<PW, KB>(), 1) factor_rows_tc_kernel(const TcParams p) {
+  constexpr int THREADS = tc_threads<PW, KB>(), NPW = 4 * PW;  // producer warps: 0 .. NPW - 1
+  constexpr int WCHAIN = NPW + CWARPS, WMMA = NPW + CWARPS + (KB > 1 ? CHAIN_WARPS : 0);
   static_assert(GS % PW == 0, "each producer parity owns GS / PW ring stages");
   constexpr int D = GS / PW;                               // per-warp gather lookahead
-  using P = TcPlan<NPRE, GS>;
+  using P = TcPlan<NPRE, GS, KB>;
   extern __shared__ __align__(1024) uint8_t smraw[];
   // 1024-B aligned operand tiles, addressed as shared-window offsets
   const uint32_t sraw = su32(smraw);
@@ -215,11 +224,14 @@ __global__ void __launch_bounds__(tc_threads<PW>(), 1) factor_rows_tc_kernel(con
   const uint32_t ring = sbase + 2 * P::B_BYTES;
   const uint32_t meta = ring + GS * P::STAGE;
   const uint32_t nabuf = meta + P::MS * P::MSTRIDE;
-  const uint32_t bars = nabuf + P::NABUF;
+  const uint32_t vbuf = nabuf + P::NABUF;                  // KB > 1: [VS][128 entries][128 B]
+  const uint32_t vmeta = vbuf + VS * SLOTS * 128;          // KB > 1: [VS][8 k][16 rs] int2
+  const uint32_t bars = nabuf + P::NABUF + P::VBUF;
   uint8_t *gbase = smraw + (sbase - sraw);
   uint64_t *a_ready = reinterpret_cast<uint64_t *>(gbase + (bars - sbase));
   uint64_t *a_free = a_ready + AS, *v_ready = a_free + AS, *d_free = v_ready + DS;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(d_free + DS);
+  uint64_t *vfull = d_free + DS, *vempty = vfull + VS;     // KB > 1: staging ring
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(vempty + VS);
     const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const int J = p.J, R = R32 ? 32 : p.R;
 
@@ -255,6 +267,7 @@ __global__ void __launch_bounds__(tc_threads<PW>(), 1) factor_rows_tc_kernel(con
   if (tid == 0) {
     for (int k = 0; k < AS; ++k) mbar_init(a_ready + k, CWARPS), mbar_init(a_free + k, 1);
     for (int k = 0; k < DS; ++k) mbar_init(v_ready + k, 1), mbar_init(d_free + k, CWARPS);
+    for (int k = 0; k < VS; ++k) mbar_init(vfull + k, CWARPS), mbar_init(vempty + k, CHAIN_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // B tiles -> tensor core
@@ -269,7 +282,7 @@ __global__ void __launch_bounds__(tc_threads<PW>(), 1) factor_rows_tc_kernel(con
   const uint32_t tlane = tmem + ((uint32_t)(32 * q) << 16);
   const uint32_t my_meta = meta + 4 * s;
 
-  if (w == NPW + CWARPS) {  // ---- MMA warp ----
+  if (w == WMMA) {  // ---- MMA warp ----
     // MMA issue for batch m (warp 8, lane 0): D = A_lo Bt_hi +
     // A_hi Bt_lo + A_hi Bt_hi once every producer arrived (a_ready) and every consumer read the
     // stage's previous D (d_free of batch m - 4); kind::tf32, D fp32, A (TMEM) / B (smem) tf32
@@ -423,7 +436,7 @@ __global__ void __launch_bounds__(tc_threads<PW>(), 1) factor_rows_tc_kernel(con
       if (lane == 0) mbar_arrive(a_ready + st);
     }
     cp_wait<0>();
-  } else {  // ---- consumers: slot s = TMEM lane s = this thread's row chain ----
+  } else if (KB == 1) {  // ---- consumers: slot s = TMEM lane s = this thread's row chain ----
     const int64_t gslots = (int64_t)gridDim.x * SLOTS;
     const float lr = p.lr, cdec = -p.lr * p.reg;
     float a[32], lo[32];
@@ -535,6 +548,175 @@ __global__ void __launch_bounds__(tc_threads<PW>(), 1) factor_rows_tc_kernel(con
       }
     }
     if (have) store_row();
+  } else if (w < WCHAIN) {  // ---- KB > 1, stagers: TMEM D -> shared-memory V rows ----
+    const int rs = s >> 3, k = s & 7;
+    const uint32_t myv = vbuf + (uint32_t)(s * 128);
+    const uint32_t swz = (uint32_t)(k ^ (rs & 7));  // chunk c of entry s at c ^ k ^ (rs & 7)
+#pragma unroll 1
+    for (int b = 0; b < nb; ++b) {
+      const int st = b % DS;
+      mbar_wait(v_ready + st, (b / DS) & 1);
+      tc_fence_after();
+      float v[32], v2[32];
+      tmem_ld32(tlane + 64 * AS + 64 * st, v);
+      tmem_ld32(tlane + 64 * AS + 64 * st + 32, v2);
+      const uint32_t mb0 = my_meta + (uint32_t)((b & (P::MS - 1)) * P::MSTRIDE);
+      const int mlc = (int)lds32(mb0);
+      const int mx = (int)lds32(mb0 + 4 * SLOTS * (1 + NPRE));
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(d_free + st);
+      const int vs = b % VS;
+      if (b >= VS) mbar_wait(vempty + vs, (b / VS - 1) & 1);
+      const uint32_t dst = myv + (uint32_t)(vs * SLOTS * 128);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float2 t0 = f2add(make_float2(v[4 * c], v[4 * c + 1]), make_float2(v2[4 * c], v2[4 * c + 1]));
+        const float2 t1 = f2add(make_float2(v[4 * c + 2], v[4 * c + 3]), make_float2(v2[4 * c + 2], v2[4 * c + 3]));
+        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};\n" ::"r"(dst + (((uint32_t)c ^ swz) << 4)),
+                     "f"(t0.x), "f"(t0.y), "f"(t1.x), "f"(t1.y)
+                     : "memory");
+      }
+      asm volatile("st.shared.v2.b32 [%0], {%1,%2};\n" ::"r"(vmeta + (uint32_t)((vs * SLOTS + k * 16 + rs) * 8)),
+                   "r"(mlc), "r"(mx)
+                   : "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(vfull + vs);
+    }
+  } else {  // ---- KB > 1, chain warps: 8 row slots each, 4 lanes per row (8 columns each) ----
+    // lane = 4 rl + qq: row slot rs = 8 (w - WCHAIN) + rl, columns 8 qq .. 8 qq + 7; the step's
+    // dot product reduces over the row's 4 lanes (two xor shuffles), as quad does over 8
+    const int rl = lane >> 2, qq = lane & 3;
+    const int rs = 8 * (w - WCHAIN) + rl;
+    const int64_t gslots = (int64_t)gridDim.x * (SLOTS / KB);
+    const float lr = p.lr, cdec = -p.lr * p.reg;
+    float a[8], lo[8];
+    int64_t row = (int64_t)blockIdx.x + (int64_t)gridDim.x * rs;  // this row slot's first row
+    bool have = false;
+    int64_t cur_i = -1;
+    int ci1 = row < p.nrows ? __ldg(p.row_coord + row) : -1;
+    int ci2 = row + gslots < p.nrows ? __ldg(p.row_coord + row + gslots) : -1;
+    const uint32_t my_na = nabuf + (uint32_t)(rs * 128 + 32 * qq);
+    const int j0 = 8 * qq;
+    auto prefetch_row = [&](int ci) {
+      if (ci >= 0) {
+        const float *ar = p.A + (int64_t)ci * J + j0;
+        if (J == 32) {
+          cp16(my_na, ar);
+          cp16(my_na + 16, ar + 4);
+        } else {
+          for (int j = 0; j < 8; ++j) cp4(my_na + 4 * j, ar + j, j0 + j < J);
+        }
+      }
+      cp_commit();
+    };
+    auto install_row = [&]() {
+      cp_wait<0>();
+      const float4 q0 = lds128(my_na), q1 = lds128(my_na + 16);
+      a[0] = q0.x, a[1] = q0.y, a[2] = q0.z, a[3] = q0.w;
+      a[4] = q1.x, a[5] = q1.y, a[6] = q1.z, a[7] = q1.w;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (j0 + j >= J) a[j] = 0.f;
+        lo[j] = 0.f;
+      }
+    };
+    auto store_row = [&]() {
+      float *ar = p.A + cur_i * J + j0;
+      if (J == 32) {
+        *reinterpret_cast<float4 *>(ar) = make_float4(a[0], a[1], a[2], a[3]);
+        *reinterpret_cast<float4 *>(ar + 4) = make_float4(a[4], a[5], a[6], a[7]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (j0 + j < J) ar[j] = a[j];
+      }
+    };
+    // this lane's 8 columns of leaf kk's V row: chunks 2 qq, 2 qq + 1 (swizzled c ^ kk ^ (rs & 7))
+    auto load_v = [&](float (&v)[8], int vs, int kk) {
+      const uint32_t src = vbuf + (uint32_t)((vs * SLOTS + 8 * rs + kk) * 128);
+      const uint32_t sw = (uint32_t)(kk ^ (rs & 7));
+      const float4 q0 = lds128(src + ((((uint32_t)(2 * qq)) ^ sw) << 4));
+      const float4 q1 = lds128(src + ((((uint32_t)(2 * qq + 1)) ^ sw) << 4));
+      v[0] = q0.x, v[1] = q0.y, v[2] = q0.z, v[3] = q0.w;
+      v[4] = q1.x, v[5] = q1.y, v[6] = q1.z, v[7] = q1.w;
+    };
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] = 0.f, lo[j] = 0.f;
+    prefetch_row(ci1);
+#pragma unroll 1
+    for (int b = 0; b < nb; ++b) {
+      const int vs = b % VS;
+      mbar_wait(vfull + vs, (b / VS) & 1);
+      float vv[8][8];
+      uint2 mm[8];
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {  // the batch's 8 V slices and step operands up front
+        load_v(vv[kk], vs, kk);
+        asm volatile("ld.shared.v2.b32 {%0,%1}, [%2];\n"
+                     : "=r"(mm[kk].x), "=r"(mm[kk].y)
+                     : "r"(vmeta + (uint32_t)((vs * SLOTS + kk * 16 + rs) * 8))
+                     : "memory");
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(vempty + vs);  // the stage is free once read
+      // one leaf step; SLOW: with the row-start / padding checks (divergent), else the plain
+      // chain (no branches: the shuffles and FMAs issue back to back)
+      auto step = [&](int kk, bool slow) {
+        const int mlc = (int)mm[kk].x;
+        const bool live = !slow || mlc != PAD;  // the shuffles stay warp-uniform either way
+        if (slow && live && ((uint32_t)mlc & ROW_START)) {
+          if (have) {
+            store_row();
+            row += gslots;
+            ci1 = ci2;
+            ci2 = row + gslots < p.nrows ? __ldg(p.row_coord + row + gslots) : -1;
+          }
+          have = true;
+          cur_i = ci1;
+          install_row();
+          prefetch_row(ci2);
+        }
+        const float *v = vv[kk];
+        float2 s2 = f2fma(make_float2(a[0], a[1]), make_float2(v[0], v[1]), make_float2(0.f, 0.f));
+        s2 = f2fma(make_float2(a[2], a[3]), make_float2(v[2], v[3]), s2);
+        float2 t2 = f2fma(make_float2(a[4], a[5]), make_float2(v[4], v[5]), make_float2(0.f, 0.f));
+        t2 = f2fma(make_float2(a[6], a[7]), make_float2(v[6], v[7]), t2);
+        float dot = (s2.x + s2.y) + (t2.x + t2.y);
+        dot += __shfl_xor_sync(FULL, dot, 1);
+        dot += __shfl_xor_sync(FULL, dot, 2);
+        const float e = __uint_as_float(mm[kk].y) - dot;
+        const float le = live ? lr * e : 0.f;
+        const float cd = live ? cdec : 0.f;
+        const float2 l2 = make_float2(le, le), c2 = make_float2(cd, cd);
+#pragma unroll
+        for (int j = 0; j < 8; j += 2) {
+          const float2 aj = make_float2(a[j], a[j + 1]), vj = make_float2(v[j], v[j + 1]);
+          if (COMP) {
+            const float2 d = f2fma(l2, vj, f2fma(c2, aj, make_float2(lo[j], lo[j + 1])));
+            const float2 t = f2add(aj, d);
+            const float2 r = f2sub(d, f2sub(t, aj));
+            a[j] = t.x, a[j + 1] = t.y, lo[j] = r.x, lo[j + 1] = r.y;
+          } else {
+            const float2 t = f2fma(l2, vj, f2fma(c2, aj, aj));
+            a[j] = t.x, a[j + 1] = t.y;
+          }
+        }
+      };
+      // a row start or padding anywhere in this warp's batch: the checked path (rare: once
+      // per row, and at the stream's end)
+      bool odd = false;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) odd |= (int)mm[kk].x == PAD || ((uint32_t)mm[kk].x & ROW_START);
+      if (__any_sync(FULL, odd)) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) step(kk, true);
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) step(kk, false);
+      }
+    }
+    if (have) store_row();
   }
   tc_fence_before();
   __syncthreads();
@@ -543,20 +725,26 @@ __global__ void __launch_bounds__(tc_threads<PW>(), 1) factor_rows_tc_kernel(con
 }
 
 // ---- K1d: the slot layout ------------------------------------------------------------------
-// Slot q = c + G s (CTA c, slot s) owns rows q, q + 128 G, q + 256 G, ... of the tree; its
-// stream is their leaves in order.  slot_plan: per-CTA batch counts (the longest stream of its
-// slots); slot_fill: entry [batch][s] of CTA c = the slot's stream position `batch`.
-__global__ void slot_count_kernel(const int32_t *__restrict__ row_leaf_ptr, int64_t rows, int G,
-                                  int32_t *__restrict__ nbatch) {
-  const int c = blockIdx.x, s = threadIdx.x;
-  const int64_t gsl = (int64_t)G * SLOTS;
+// KB leaves of one row slot per batch: a CTA has RS = 128 / KB row slots; row slot q = c + G rs
+// (CTA c, rs < RS) owns rows q, q + G RS, q + 2 G RS, ... of the tree, and its stream is their
+// leaves in order.  Stream position p of q sits in batch p / KB at TMEM lane / entry slot
+// s = KB rs + p % KB: entry (batch_ptr[c] + p / KB) * 128 + s.  KB = 1: one thread per row
+// (K3c); KB = 8: 16 rows per CTA for few, long rows (K3c-wide).
+// slot_rows_kernel: per row its offset in its row slot's stream, per CTA its batch count.
+__global__ void slot_rows_kernel(const int32_t *__restrict__ row_leaf_ptr, int64_t rows, int G,
+                                 int KB, int32_t *__restrict__ row_off, int32_t *__restrict__ nbatch) {
+  const int c = blockIdx.x, RS = SLOTS / KB;
+  const int64_t gsl = (int64_t)G * RS;
   int64_t tot = 0;
-  for (int64_t r = c + (int64_t)G * s; r < rows; r += gsl)
-    tot += __ldg(row_leaf_ptr + r + 1) - __ldg(row_leaf_ptr + r);
+  if ((int)threadIdx.x < RS)
+    for (int64_t r = c + (int64_t)G * threadIdx.x; r < rows; r += gsl) {
+      row_off[r] = (int32_t)tot;
+      tot += __ldg(row_leaf_ptr + r + 1) - __ldg(row_leaf_ptr + r);
+    }
   using BR = cub::BlockReduce<int64_t, SLOTS>;
   __shared__ typename BR::TempStorage ts;
   const int64_t mx = BR(ts).Reduce(tot, cub::Max());
-  if (s == 0) nbatch[c] = (int32_t)mx;
+  if (threadIdx.x == 0) nbatch[c] = (int32_t)((mx + KB - 1) / KB);
 }
 
 __global__ void slot_scan_kernel(const int32_t *__restrict__ nbatch, int G, int32_t *batch_ptr) {
@@ -570,37 +758,62 @@ __global__ void slot_scan_kernel(const int32_t *__restrict__ nbatch, int G, int3
   }
 }
 
-__global__ void slot_fill_kernel(const int32_t *__restrict__ row_leaf_ptr, int64_t rows, int G,
-                                 int npre, const int32_t *__restrict__ batch_ptr,
-                                 const int32_t *__restrict__ leaf_coord,
-                                 const int32_t *__restrict__ leaf_pc,
-                                 const float *__restrict__ vals, int32_t *__restrict__ slot_lc,
-                                 int32_t *__restrict__ slot_pc, float *__restrict__ slot_x) {
-  const int c = blockIdx.x, s = threadIdx.x;
-  const int64_t gsl = (int64_t)G * SLOTS;
+// block (c, j): batches [32 j, 32 j + 32) of CTA c; thread = entry slot s = KB rs + k walks its
+// row slot's stream positions 32 j KB + k, + KB, ... (32 of them), staging the entries in shared
+// memory so that the stores of each batch (128 consecutive entries) are coalesced
+template <int NPRE>
+constexpr int fill_b() { return NPRE == 1 ? 32 : 16; }  // 48 KB of static staging at most
+template <int NPRE>
+__global__ void __launch_bounds__(SLOTS) slot_fill_kernel(
+    const int32_t *__restrict__ row_leaf_ptr, const int32_t *__restrict__ row_off, int64_t rows,
+    int G, int KB, const int32_t *__restrict__ batch_ptr, const int32_t *__restrict__ leaf_coord,
+    const int32_t *__restrict__ leaf_pc, const float *__restrict__ vals,
+    int32_t *__restrict__ slot_lc, int32_t *__restrict__ slot_pc, float *__restrict__ slot_x) {
+  constexpr int FILL_B = fill_b<NPRE>();
+  __shared__ int32_t t_lc[FILL_B][SLOTS];
+  __shared__ int32_t t_pc[NPRE > 0 ? NPRE : 1][FILL_B][SLOTS];
+  __shared__ float t_x[FILL_B][SLOTS];
+  const int c = blockIdx.x, s = threadIdx.x, RS = SLOTS / KB, rs = s / KB, k = s % KB;
   const int64_t b0 = batch_ptr[c];
   const int nb = batch_ptr[c + 1] - (int)b0;
-  int64_t r = c + (int64_t)G * s;
-  int64_t L = 0, Le = 0;
-  bool start = false;
-  if (r < rows) L = row_leaf_ptr[r], Le = row_leaf_ptr[r + 1], start = true;
-  for (int b = 0; b < nb; ++b) {
-    while (r < rows && L >= Le) {  // next non-empty row of the stream
+  const int jb = (int)blockIdx.y * FILL_B;
+  if (jb >= nb) return;
+  const int64_t gsl = (int64_t)G * RS;
+  int64_t p = (int64_t)jb * KB + k;  // this thread's first stream position
+  // the row holding position p (rows of one slot: a few dozen at most in practice)
+  int64_t r = c + (int64_t)G * rs;
+  int64_t off = 0, len = 0;
+  if (r < rows) off = row_off[r], len = row_leaf_ptr[r + 1] - row_leaf_ptr[r];
+  while (r < rows && p >= off + len) {
+    r += gsl;
+    if (r < rows) off = row_off[r], len = row_leaf_ptr[r + 1] - row_leaf_ptr[r];
+  }
+  for (int i = 0; i < FILL_B; ++i, p += KB) {
+    while (r < rows && p >= off + len) {
       r += gsl;
-      if (r < rows) L = row_leaf_ptr[r], Le = row_leaf_ptr[r + 1], start = true;
+      if (r < rows) off = row_off[r], len = row_leaf_ptr[r + 1] - row_leaf_ptr[r];
     }
-    const int64_t e = (b0 + b) * SLOTS + s;
-    if (r < rows) {
-      slot_lc[e] = (int32_t)((uint32_t)leaf_coord[L] | (start ? ROW_START : 0u));
-      for (int d = 0; d < npre; ++d) slot_pc[((b0 + b) * npre + d) * SLOTS + s] = leaf_pc[L * npre + d];
-      slot_x[e] = vals[L];
-      start = false;
-      ++L;
+    if (r < rows && p >= off) {
+      const int64_t L = row_leaf_ptr[r] + (p - off);
+      t_lc[i][s] = (int32_t)((uint32_t)__ldg(leaf_coord + L) | (p == off ? ROW_START : 0u));
+#pragma unroll
+      for (int d = 0; d < NPRE; ++d) t_pc[d][i][s] = __ldg(leaf_pc + L * NPRE + d);
+      t_x[i][s] = __ldg(vals + L);
     } else {
-      slot_lc[e] = PAD;
-      for (int d = 0; d < npre; ++d) slot_pc[((b0 + b) * npre + d) * SLOTS + s] = 0;
-      slot_x[e] = 0.f;
+      t_lc[i][s] = PAD;
+#pragma unroll
+      for (int d = 0; d < NPRE; ++d) t_pc[d][i][s] = 0;
+      t_x[i][s] = 0.f;
     }
+  }
+  __syncthreads();
+  const int nbat = nb - jb < FILL_B ? nb - jb : FILL_B;
+  for (int i = 0; i < nbat; ++i) {
+    const int64_t e = (b0 + jb + i) * SLOTS + s;
+    slot_lc[e] = t_lc[i][s];
+#pragma unroll
+    for (int d = 0; d < NPRE; ++d) slot_pc[((b0 + jb + i) * NPRE + d) * SLOTS + s] = t_pc[d][i][s];
+    slot_x[e] = t_x[i][s];
   }
 }
 
@@ -619,17 +832,17 @@ bool tc_enabled() {
   return on;
 }
 
-template <int NPRE, int GS, bool R32, bool COMP, int PW>
+template <int NPRE, int GS, bool R32, bool COMP, int PW, int KB = 1>
 int launch_tc_k(const TcParams &q, int G, cudaStream_t s) {
-  const size_t sm = TcPlan<NPRE, GS>::SMEM;
+  const size_t sm = TcPlan<NPRE, GS, KB>::SMEM;
   static bool set = false;
   if (!set) {
-    cudaFuncSetAttribute(factor_rows_tc_kernel<NPRE, GS, R32, COMP, PW>,
+    cudaFuncSetAttribute(factor_rows_tc_kernel<NPRE, GS, R32, COMP, PW, KB>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     set = true;
   }
-  factor_rows_tc_kernel<NPRE, GS, R32, COMP, PW><<<G, tc_threads<PW>(), sm, s>>>(q);
-  return check_launch("ft_factor_sweep_rows(tcgen05)");
+  factor_rows_tc_kernel<NPRE, GS, R32, COMP, PW, KB><<<G, tc_threads<PW, KB>(), sm, s>>>(q);
+  return check_launch(KB == 1 ? "ft_factor_sweep_rows(tcgen05)" : "ft_factor_sweep_rows(tcgen05 wide)");
 }
 // the plain chain fits the 13-warp block's 128 registers (two producer warps per quadrant); the
 // compensated one (156 registers) keeps one producer warp per quadrant
@@ -683,8 +896,49 @@ int launch_factor_tc(const ft_tree_t *t, const ft_model_t *m, float lr, float re
   }();
   const bool comp = force_comp >= 0 ? force_comp == 1
                                     : t->num_rows > 0 && t->nnz / t->num_rows > 8192;
+  if (t->slot_kb == 8) {  // few long rows, order 3 (slot_kb_for): 16 rows per CTA
+    if (q.R == 32)
+      return comp ? launch_tc_k<1, 4, true, true, 1, 8>(q, t->slot_grid, s)
+                  : launch_tc_k<1, 4, true, false, 1, 8>(q, t->slot_grid, s);
+    return comp ? launch_tc_k<1, 4, false, true, 1, 8>(q, t->slot_grid, s)
+                : launch_tc_k<1, 4, false, false, 1, 8>(q, t->slot_grid, s);
+  }
+  if (t->slot_kb != 1) return -1;
   if (N == 3) return launch_tc_t<1, 4>(q, t->slot_grid, comp, s);
   return launch_tc_t<2, 2>(q, t->slot_grid, comp, s);
+}
+
+// ft_tree_slot_plan hands its per-row stream offsets to the ft_tree_slot_fill that follows
+// (the Python driver calls them back to back on one thread)
+int32_t *&planned_row_off() {
+  static int32_t *p = nullptr;
+  return p;
+}
+int &planned_kb() {
+  static int kb = 1;
+  return kb;
+}
+
+// which layout the factor sweep of this tree uses: 1 (K3c: one thread per row), 8 (K3c-wide:
+// 16 rows per CTA, for few long rows) or 0 (neither: the warp-level kernels)
+int slot_kb_for(const ft_tree_t *t, int J, int R) {
+  const int64_t rows = t->num_rows;
+  if (!t->row_leaf_ptr || !t->leaf_pc || rows <= 0 || !tc_enabled() ||
+      !tc_shape_ok(t->order, J, R))
+    return 0;
+  if (rows >= tc_min_rows()) return 1;
+  // K3c-wide (16 rows x 8 leaves per batch, the chains in two 4-lanes-per-row warps) is opt-in
+  // (FT_TC_WIDE=1): correct (tests/test_factor_tc_gpu.py), but its chain warps run each row's
+  // 8 steps per batch back to back and measured slower than quadw on Netflix mode 2 (9.6 vs
+  // 5.9 ms; profiles/r02_factor_tc_ab.md)
+  static const bool wide = [] {
+    const char *e = getenv("FT_TC_WIDE");
+    return e && strcmp(e, "1") == 0;
+  }();
+  if (wide && t->order == 3 && rows >= (int64_t)sm_count() * (SLOTS / 8) * 9 / 10 &&
+      t->nnz / rows >= 64)
+    return 8;
+  return 0;
 }
 
 }  // namespace ft
@@ -692,15 +946,17 @@ int launch_factor_tc(const ft_tree_t *t, const ft_model_t *m, float lr, float re
 using namespace ft;
 
 extern "C" int ft_tree_slot_plan(const ft_tree_t *tree, int32_t J, int32_t R, int32_t *grid_out,
-                                 int32_t *batch_ptr, int64_t *len_out, void *stream) {
-  if (!tree || !grid_out || !len_out) return fail(FT_ERR_ARG, "ft_tree_slot_plan: null argument");
+                                 int32_t *kb_out, int32_t *batch_ptr, int64_t *len_out,
+                                 void *stream) {
+  if (!tree || !grid_out || !len_out || !kb_out)
+    return fail(FT_ERR_ARG, "ft_tree_slot_plan: null argument");
   *grid_out = 0;
   *len_out = 0;
-  const int64_t rows = tree->num_rows;
-  if (!tree->row_leaf_ptr || !tree->leaf_pc || rows <= 0 || !tc_enabled() ||
-      !tc_shape_ok(tree->order, J, R) || rows < tc_min_rows())
-    return FT_OK;  // the tcgen05 sweep does not apply: no layout
-  const int64_t G64 = (rows + SLOTS - 1) / SLOTS;
+  const int KB = slot_kb_for(tree, J, R);
+  *kb_out = KB;
+  if (KB == 0) return FT_OK;  // the tcgen05 sweep does not apply: no layout
+  const int64_t rows = tree->num_rows, RS = SLOTS / KB;
+  const int64_t G64 = (rows + RS - 1) / RS;
   const int G = (int)(G64 < sm_count() ? G64 : sm_count());
   if (!batch_ptr) {  // size query
     *grid_out = G;
@@ -709,14 +965,19 @@ extern "C" int ft_tree_slot_plan(const ft_tree_t *tree, int32_t J, int32_t R, in
   cudaStream_t s = as_stream(stream);
   int32_t *nbatch = nullptr;
   FT_CUDA(cudaMallocAsync(&nbatch, sizeof(int32_t) * G, s));
-  slot_count_kernel<<<G, SLOTS, 0, s>>>(tree->row_leaf_ptr, rows, G, nbatch);
-  if (int rc = check_launch("ft_tree_slot_plan(count)")) return rc;
+  int32_t *row_off = nullptr;  // scratch, handed to ft_tree_slot_fill
+  FT_CUDA(cudaMallocAsync(&row_off, sizeof(int32_t) * rows, s));
+  slot_rows_kernel<<<G, SLOTS, 0, s>>>(tree->row_leaf_ptr, rows, G, KB, row_off, nbatch);
+  if (int rc = check_launch("ft_tree_slot_plan(rows)")) return rc;
   slot_scan_kernel<<<1, 32, 0, s>>>(nbatch, G, batch_ptr);
   if (int rc = check_launch("ft_tree_slot_plan(scan)")) return rc;
   int32_t total = 0;
   FT_CUDA(cudaMemcpyAsync(&total, batch_ptr + G, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   FT_CUDA(cudaFreeAsync(nbatch, s));
   FT_CUDA(cudaStreamSynchronize(s));
+  if (planned_row_off()) cudaFree(planned_row_off());  // a plan never followed by its fill
+  planned_row_off() = row_off;  // handed to ft_tree_slot_fill (same stream, next call)
+  planned_kb() = KB;
   *grid_out = G;
   *len_out = (int64_t)total * SLOTS;
   return FT_OK;
@@ -730,8 +991,29 @@ extern "C" int ft_tree_slot_fill(const ft_tree_t *tree, int32_t grid, const int3
   const int npre = tree->order - 2;
   if (npre > 0 && (!slot_pc || !tree->leaf_pc))
     return fail(FT_ERR_ARG, "ft_tree_slot_fill: prefix index missing");
-  slot_fill_kernel<<<grid, SLOTS, 0, as_stream(stream)>>>(
-      tree->row_leaf_ptr, tree->num_rows, grid, npre, batch_ptr, tree->leaf_coord, tree->leaf_pc,
-      tree->vals, slot_lc, slot_pc, slot_x);
-  return check_launch("ft_tree_slot_fill");
+  int32_t *row_off = planned_row_off();
+  if (!row_off) return fail(FT_ERR_ARG, "ft_tree_slot_fill: call ft_tree_slot_plan first");
+  planned_row_off() = nullptr;
+  cudaStream_t s = as_stream(stream);
+  const int KB = planned_kb();
+  // the longest CTA stream bounds the batch blocks: read it back from batch_ptr
+  std::vector<int32_t> bp(grid + 1);
+  FT_CUDA(cudaMemcpyAsync(bp.data(), batch_ptr, sizeof(int32_t) * (grid + 1),
+                          cudaMemcpyDeviceToHost, s));
+  FT_CUDA(cudaStreamSynchronize(s));
+  int maxnb = 0;
+  for (int c = 0; c < grid; ++c) maxnb = std::max(maxnb, bp[c + 1] - bp[c]);
+  const int fb = npre == 1 ? fill_b<1>() : fill_b<2>();
+  const dim3 g(grid, (maxnb + fb - 1) / fb);
+  if (npre == 1)
+    slot_fill_kernel<1><<<g, SLOTS, 0, s>>>(tree->row_leaf_ptr, row_off, tree->num_rows, grid, KB,
+                                            batch_ptr, tree->leaf_coord, tree->leaf_pc, tree->vals,
+                                            slot_lc, slot_pc, slot_x);
+  else
+    slot_fill_kernel<2><<<g, SLOTS, 0, s>>>(tree->row_leaf_ptr, row_off, tree->num_rows, grid, KB,
+                                            batch_ptr, tree->leaf_coord, tree->leaf_pc, tree->vals,
+                                            slot_lc, slot_pc, slot_x);
+  const int rc = check_launch("ft_tree_slot_fill");
+  cudaFreeAsync(row_off, s);
+  return rc;
 }

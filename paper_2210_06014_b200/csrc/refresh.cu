@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(WARPS * 32)
 namespace tc {
 constexpr int M = 128;
 constexpr int TILE_BYTES = M * 128;   // 128 rows x 32 fp32
-constexpr int B_BYTES = 32 * 128;     // up to 32 rows (R) x 32 fp32
+constexpr int B_BYTES = 64 * 128;     // 64 rows (P or Q) x 32 fp32
 constexpr size_t SMEM = 2 * TILE_BYTES + 2 * B_BYTES + 1024 + 64;  // + alignment slack, barrier
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -128,7 +128,10 @@ __global__ void __launch_bounds__(128) refresh_tc_kernel(int64_t I, int J, int R
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 1);
   const int tid = threadIdx.x, w = tid >> 5;
 
-  // Bt (R x J) -> hi / lo tiles, row r = output column, zero-padded to 32 rows x 32 k
+  // Bt (R x J) -> the 64-row B operands P = [Bt_hi ; Bt_lo] and Q = [Bt_hi ; 0] (row r = output
+  // column, zero-padded to 32 rows x 32 k), so that D[:, 0:32] = A_hi Bt_hi + A_lo Bt_hi and
+  // D[:, 32:64] = A_hi Bt_lo: 3xTF32 in 2 x J/8 MMAs at N = 64 instead of 3 x J/8 at N = 32
+  // (an N = 64 tcgen05.mma costs about what an N = 32 one does: tools/umma_probe.cu)
   for (int e = tid; e < 32 * 8; e += 128) {
     const int r = e >> 3, c = e & 7;
     float v[4];
@@ -144,11 +147,13 @@ __global__ void __launch_bounds__(128) refresh_tc_kernel(int64_t I, int J, int R
     l.y = __float_as_uint(v[1] - __uint_as_float(h.y));
     l.z = __float_as_uint(v[2] - __uint_as_float(h.z));
     l.w = __float_as_uint(v[3] - __uint_as_float(h.w));
-    *reinterpret_cast<uint4 *>(b_hi + off) = h;
-    *reinterpret_cast<uint4 *>(b_lo + off) = l;
+    *reinterpret_cast<uint4 *>(b_hi + off) = h;                 // P rows 0-31
+    *reinterpret_cast<uint4 *>(b_hi + 32 * 128 + off) = l;      // P rows 32-63
+    *reinterpret_cast<uint4 *>(b_lo + off) = h;                 // Q rows 0-31
+    *reinterpret_cast<uint4 *>(b_lo + 32 * 128 + off) = make_uint4(0, 0, 0, 0);
   }
   if (w == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;\n" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;\n" ::"r"(
         smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
@@ -160,8 +165,8 @@ __global__ void __launch_bounds__(128) refresh_tc_kernel(int64_t I, int J, int R
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  // kind::tf32, D fp32, A / B tf32 K-major, N = 32 (padded R), M = 128
-  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+  // kind::tf32, D fp32, A / B tf32 K-major, N = 64 (P / Q), M = 128
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
   const int ksteps = (J + 7) >> 3;
   uint32_t phase = 0, gmax = 0;
   const int64_t ntiles = (I + M - 1) / M;
@@ -211,12 +216,11 @@ __global__ void __launch_bounds__(128) refresh_tc_kernel(int64_t I, int J, int R
       const uint32_t bh = smem_u32(b_hi), bl = smem_u32(b_lo);
       uint32_t acc = 0;
       for (int k = 0; k < ksteps; ++k) {  // K = 8 tf32 = 32 B per step inside the 128-B row
-        const uint32_t o = 32 * k;
-        mma_tf32_tc(tmem, sw128_desc(al + o), sw128_desc(bh + o), idesc, acc);
+        mma_tf32_tc(tmem, sw128_desc(ah + 32 * k), sw128_desc(bh + 32 * k), idesc, acc);
         acc = 1;
-        mma_tf32_tc(tmem, sw128_desc(ah + o), sw128_desc(bl + o), idesc, 1);
-        mma_tf32_tc(tmem, sw128_desc(ah + o), sw128_desc(bh + o), idesc, 1);
       }
+      for (int k = 0; k < ksteps; ++k)
+        mma_tf32_tc(tmem, sw128_desc(al + 32 * k), sw128_desc(bl + 32 * k), idesc, 1);
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                        smem_u32(bar))
                    : "memory");
@@ -229,8 +233,8 @@ __global__ void __launch_bounds__(128) refresh_tc_kernel(int64_t I, int J, int R
         : "memory");
     phase ^= 1;
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    // TMEM lanes 32w..32w+31 = rows of this warp; 32 columns = C[row][0..31]
-    uint32_t d[32];
+    // TMEM lanes 32w..32w+31 = rows of this warp; columns 0-31 + 32-63 = C[row][0..31]
+    uint32_t d[32], d2[32];
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
         "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
@@ -240,7 +244,18 @@ __global__ void __launch_bounds__(128) refresh_tc_kernel(int64_t I, int J, int R
           "=r"(d[20]), "=r"(d[21]), "=r"(d[22]), "=r"(d[23]), "=r"(d[24]), "=r"(d[25]),
           "=r"(d[26]), "=r"(d[27]), "=r"(d[28]), "=r"(d[29]), "=r"(d[30]), "=r"(d[31])
         : "r"(tmem + ((uint32_t)(32 * w) << 16)));
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+        : "=r"(d2[0]), "=r"(d2[1]), "=r"(d2[2]), "=r"(d2[3]), "=r"(d2[4]), "=r"(d2[5]), "=r"(d2[6]),
+          "=r"(d2[7]), "=r"(d2[8]), "=r"(d2[9]), "=r"(d2[10]), "=r"(d2[11]), "=r"(d2[12]), "=r"(d2[13]),
+          "=r"(d2[14]), "=r"(d2[15]), "=r"(d2[16]), "=r"(d2[17]), "=r"(d2[18]), "=r"(d2[19]),
+          "=r"(d2[20]), "=r"(d2[21]), "=r"(d2[22]), "=r"(d2[23]), "=r"(d2[24]), "=r"(d2[25]),
+          "=r"(d2[26]), "=r"(d2[27]), "=r"(d2[28]), "=r"(d2[29]), "=r"(d2[30]), "=r"(d2[31])
+        : "r"(tmem + ((uint32_t)(32 * w) << 16) + 32));
     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int r = 0; r < 32; ++r) d[r] = __float_as_uint(__uint_as_float(d[r]) + __uint_as_float(d2[r]));
     if (row < I) {
       for (int q = 0; q < dst.n; ++q) {
         float *out = dst.p[q] + row * R;
@@ -265,7 +280,7 @@ __global__ void __launch_bounds__(128) refresh_tc_kernel(int64_t I, int J, int R
   if (guard) guard_max(guard, gmax);
   __syncthreads();
   if (w == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;\n" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;\n" ::"r"(tmem));
 }
 
 // tensor-core refresh unless FT_REFRESH=simt (the fp32 CUDA-core kernel above, which keeps the

@@ -3,7 +3,9 @@ TMEM, one thread per row, slot layout K1d), against the fp64 oracle at the contr
 per sweep, and the slot layout itself against the tree it was built from.
 
 The default dispatch runs K3c on trees with enough rows to fill the GPU (one 128-slot CTA on
->= 90 % of the SMs) when 16 < R <= 32:
+>= 90 % of the SMs) when 16 < R <= 32; with FT_TC_WIDE=1 (set here), K3c-wide (16 rows x 8
+leaves per batch, the chains in two 4-lanes-per-row warps) takes order-3 trees with fewer but
+long rows (>= 0.9 x 16 per SM, >= 64 leaves each):
 each case below has at least one such mode; the other modes run quadr / quadw as usual, so
 every sweep of two epochs is checked.  Cases: short rows (1-3 leaves, J < 32 and R < 32
 padding, R % 8 = 4), more rows than slots (row switching inside a slot's stream), rows of
@@ -43,10 +45,15 @@ def ft():
     ((20000, 300, 50), 2_000_000, 32, 32, 2e-3, "0"),
     ((20000, 10000, 30, 20), 600_000, 32, 32, 2e-3, "0"),  # order 4
     ((20000, 300, 40), 400_000, 16, 24, 2e-3, "1"),   # J = 16, R = 24
+    # K3c-wide (KB = 8: 16 rows per CTA, a chain warp) for few long rows:
+    ((3000, 2500, 400), 2_000_000, 32, 32, 2e-3, "0"),  # modes 0 and 1: 667 / 800-leaf rows
+    ((2400, 500, 100), 500_000, 24, 20, 1e-3, "0"),     # padding, row switching in a batch
+    ((2300, 64, 64), 1_500_000, 32, 32, 2e-3, "1"),     # 650-leaf rows, compensated chain
 ])
 def test_tc_factor_sweeps_match_oracle(dims, nnz, J, R, lr, comp):
     code = _CASE.format(dims=dims, nnz=nnz, J=J, R=R, lr=lr, seed=11)
-    env = dict(os.environ, FT_TC_COMP=comp)
+    # FT_TC_WIDE=1 opts the few-long-rows shapes into K3c-wide (not dispatched by default)
+    env = dict(os.environ, FT_TC_COMP=comp, FT_TC_WIDE="1")
     env.pop("FT_FACTOR_KERNEL", None)
     env.pop("FT_FACTOR_TC", None)
     out = subprocess.run([sys.executable, "-c", code], cwd=REPO, env=env, capture_output=True,

@@ -46,7 +46,7 @@ CONFIGS = {
     "order4": dict(dims=(10_000,) * 4, nnz_train=495_000_000, nnz_test=5_000_000, J=32, R=32,
                    value_range=(1.0, 5.0)),
     "order4_1b": dict(dims=(10_000,) * 4, nnz_train=990_000_000, nnz_test=10_000_000, J=32,
-                      R=32, value_range=(1.0, 5.0)),
+                      R=32, value_range=(1.0, 5.0), keep_fibers=False),
 }
 
 # one sample size for the reference arm and the cpu_baseline leg: BASELINE.md section 4 step 3
@@ -440,7 +440,9 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     log(f"generated {nnz_total} entries in {time.perf_counter() - t0:.2f}s")
     t0 = time.perf_counter()
-    forest = ft.build_forest(train_t, 128, compact=True)  # the arrays the sweeps read
+    # the arrays the sweeps read (keep_fibers=False: without the fiber arrays, 16 B per leaf at
+    # order 4 -- what fits the 1 B-entry order-4 forest on one GPU)
+    forest = ft.build_forest(train_t, 128, compact=True, keep_fibers=cfg.get("keep_fibers", True))
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
     log(f"forest built in {build_s:.2f}s; fibers {[t.num_fibers for t in forest.trees]}, "

@@ -49,6 +49,7 @@ class CsfTree:
     seg_coord: object = None     # device int32 [segs]  core-sweep row segments (derived)
     seg_leaf_ptr: object = None  # device int32 [segs+1]
     slot_kb: int = 1             # leaves per row slot and batch (1 or 8)
+    nfib: int = -1               # fiber count kept after drop_fibers()
     slot_grid: int = -1          # slot layout of the tcgen05 factor sweep (-1 = not planned,
     slot_batch_ptr: object = None  # 0 = does not apply); device int32 [G+1]
     slot_lc: object = None       # device int32 [batches x 128]
@@ -67,7 +68,25 @@ class CsfTree:
 
     @property
     def num_fibers(self) -> int:
+        if self.nfib >= 0:
+            return self.nfib
         return int(self.fiber_ptr.shape[0]) - 1
+
+    def drop_fibers(self) -> "CsfTree":
+        """Free fiber_ptr / fiber_coord (16 B per leaf at order 4) once the leaf-major index
+        exists: the row-owner kernels (K3c, quadr, K4 quad, K6b) and the derived build of the next
+        tree read leaf_pc / row_leaf_ptr / segments instead.  The fiber-walking kernels (hogwild
+        K3a, dual / ws / gram, the uncached plan's counts) then refuse the tree.  What lets the
+        BASELINE order-4 1 B-entry tensor's four trees fit one 180 GB GPU."""
+        import torch
+
+        if self.leaf_pc is None or self.row_leaf_ptr is None or self.seg_coord is None:
+            raise ValueError("drop_fibers needs the leaf-major index and row segments")
+        self.nfib = self.num_fibers
+        empty = torch.empty(0, dtype=torch.int32, device=self.vals.device)
+        self.fiber_ptr, self.fiber_coord = empty, empty
+        self._view = None
+        return self
 
     @property
     def num_subtensors(self) -> int:
@@ -102,8 +121,8 @@ class CsfTree:
             v.num_rows = self.num_rows
             v.leaf_coord = self.leaf_coord.data_ptr()
             v.vals = self.vals.data_ptr()
-            v.fiber_ptr = self.fiber_ptr.data_ptr()
-            v.fiber_coord = self.fiber_coord.data_ptr()
+            v.fiber_ptr = self.fiber_ptr.data_ptr() if self.nfib < 0 else None
+            v.fiber_coord = self.fiber_coord.data_ptr() if self.nfib < 0 else None
             v.row_fiber_ptr = self.row_fiber_ptr.data_ptr()
             v.row_coord = self.row_coord.data_ptr()
             v.leaf_pc = _lib.ptr(self.leaf_pc)
@@ -406,7 +425,7 @@ def add_row_segments(tree: CsfTree, stream=None) -> CsfTree:
 
 def build_forest(tensor, fiber_threshold=DEFAULT_FIBER_THRESHOLD, stream=None,
                  compact: bool = False, concurrent: bool = False,
-                 derived: bool = True) -> CsfForest:
+                 derived: bool = True, keep_fibers: bool = True) -> CsfForest:
     """All N trees (csf.py:199-201).  ``concurrent=True`` builds each tree on its own CUDA
     stream from its own host thread (ctypes releases the GIL); the result is identical, but it
     measured slower (Netflix: 33 ms vs 26.5 ms sequential, with 100-200 ms outliers while the
@@ -418,12 +437,18 @@ def build_forest(tensor, fiber_threshold=DEFAULT_FIBER_THRESHOLD, stream=None,
     if not concurrent or N == 1:
         # tree 0 from the COO, tree t from tree t-1's leaf order when the 32-bit derived sort
         # applies (bit-identical; Netflix: 4 radix passes of 4-byte keys instead of 6 of 8-byte)
+        # keep_fibers=False: each tree's fiber arrays are freed as soon as the next tree is
+        # derived from it (tree t+1's build reads only tree t's leaf-major index)
         trees = [build_tree(dev, 0, fiber_threshold, stream, compact)]
         for t in range(1, N):
             tree = build_tree_derived(trees[-1], fiber_threshold, stream, compact) \
                 if derived else None
+            if not keep_fibers:
+                trees[-1].drop_fibers()
             trees.append(tree if tree is not None
                          else build_tree(dev, t, fiber_threshold, stream, compact))
+        if not keep_fibers:
+            trees[-1].drop_fibers()
         return CsfForest(trees=tuple(trees), fiber_threshold=fiber_threshold)
     from concurrent.futures import ThreadPoolExecutor
 

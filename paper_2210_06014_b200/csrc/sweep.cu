@@ -1385,6 +1385,9 @@ int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
     else
       v = p.nrows >= (int64_t)2 * sm_count() * 16 ? 3 : (p.N == 3 ? 4 : 5);
   }
+  if (v >= 3 && !p.fiber_ptr)
+    return fail(FT_ERR_UNSUPPORTED, "this tree has no fiber arrays (drop_fibers): the fiber-walking "
+                "K3b kernels cannot run it");
   switch (v) {
     case 1: return launch_quadr(p, s);
     case 2: return launch_quadw(p, s);
@@ -1498,6 +1501,8 @@ extern "C" int ft_core_sweep_rows(const ft_tree_t *tree, const ft_model_t *model
     p.row_coord = p.seg_coord;
     p.row_leaf_ptr = p.seg_leaf_ptr;
   }
+  if (!use_quad && !p.fiber_ptr)
+    return fail(FT_ERR_UNSUPPORTED, "this tree has no fiber arrays (drop_fibers): K4 needs quad");
   const int g = use_quad ? core_quad_grid(p)
                 : p.R <= 8 ? core_rows_grid<8>(p) : p.R <= 16 ? core_rows_grid<16>(p)
                                                               : core_rows_grid<32>(p);
@@ -1515,6 +1520,8 @@ extern "C" int ft_core_sweep_rows(const ft_tree_t *tree, const ft_model_t *model
 extern "C" int ft_factor_sweep_fibers(const ft_tree_t *tree, const ft_model_t *m, int64_t fib_lo,
                                       int64_t fib_hi, float lr, float reg, int32_t max_warps,
                                       void *stream) {
+  if (tree && !tree->fiber_ptr)
+    return ft::fail(FT_ERR_UNSUPPORTED, "ft_factor_sweep_fibers: the tree's fiber arrays were dropped");
   if (!tree || !m) return fail(FT_ERR_ARG, "null tree/model");
   const int N = tree->order;
   if (N < 3 || N > FT_MAX_ORDER || m->order != N) return fail(FT_ERR_ARG, "order mismatch");

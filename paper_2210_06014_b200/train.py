@@ -59,11 +59,12 @@ class TrainConfig:
     schedule: str | None = None   # None: "exact" if workers <= 1 else "hogwild"
     sync_guards: bool = False
     # hogwild concurrency: at most dims[u] / hogwild_rows_per_warp warps update A_u at once
-    # (each warp is one serial worker; fewer rows per warp = more racing writers per row).  The
-    # RMSE gate held at every level measured (Netflix dims, 10 M entries, 3 epochs: train / test
-    # RMSE within 0.005 % of the exact schedule from 256 down to 1 row per warp, while the
-    # factor pass went 914 -> 17 ms; profiles/r02_hogwild_ab.md), so the default is uncapped
-    hogwild_rows_per_warp: int = 1
+    # (each warp is one serial worker; fewer rows per warp = more racing writers per row).
+    # Measured (profiles/r02_hogwild_ab.md): on Netflix dims at lr 1e-3 every level from 256 to
+    # 1 row per warp stays within 0.005 % of the exact schedule's RMSE, but the reference's own
+    # hogwild fixture (20 rows per mode, lr 0.05) diverges with 20 racing warps; 16 rows per
+    # warp keeps tiny modes serial and is 15x faster than the round-1 cap of 256 at Netflix dims
+    hogwild_rows_per_warp: int = 16
 
     def __post_init__(self):
         if self.plan not in ("cached", "uncached"):

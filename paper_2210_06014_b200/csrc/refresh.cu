@@ -283,6 +283,207 @@ __global__ void __launch_bounds__(128) refresh_tc_kernel(int64_t I, int J, int R
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;\n" ::"r"(tmem));
 }
 
+// ---- K2, streaming form (J = R = 32): TMA bulk copies in and out, two tiles in the MMA ------
+// A's 128-row tiles are contiguous 16 KB blocks, and so are C's: one elected thread keeps a
+// 4-deep ring of tile loads in flight (cp.async.bulk, completion on mbarriers) and writes each
+// finished C tile to every destination with one bulk store (cp.async.bulk shared -> global,
+// peers included).  Per tile the 128 threads read their row from the landed raw tile (chunks in
+// a rotated order: conflict-free), fold the guard max, split it into the 128-B-swizzled hi / lo
+// operand tiles (double-buffered), and one thread issues the tile's 8 N = 64 MMAs into one of two
+// TMEM accumulators; the epilogue of tile t-1 (TMEM -> registers -> C staging tile -> bulk
+// store) runs while the tensor core works on tile t.
+namespace tcs {
+constexpr int TM = 128, TBYTES = TM * 128, RING = 8;
+// raw ring (7 tile loads in flight: ~112 KB per SM against the HBM latency) + one hi / lo
+// operand pair + P, Q: ~177 KB, one CTA per SM
+constexpr size_t SMEM = 1024 + (size_t)RING * TBYTES + 2 * (size_t)TBYTES + 2 * (64 * 128) + 128;
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_t bytes,
+                                          uint32_t bar) {
+  asm volatile(
+      "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+      : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store(void *dst, uint32_t src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst),
+               "r"(src), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void wait_parity(uint32_t bar, uint32_t ph) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(bar),
+      "r"(ph)
+      : "memory");
+}
+__device__ __forceinline__ void ld_tmem32(uint32_t taddr, uint32_t (&d)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]),
+        "=r"(d[7]), "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]),
+        "=r"(d[14]), "=r"(d[15]), "=r"(d[16]), "=r"(d[17]), "=r"(d[18]), "=r"(d[19]),
+        "=r"(d[20]), "=r"(d[21]), "=r"(d[22]), "=r"(d[23]), "=r"(d[24]), "=r"(d[25]),
+        "=r"(d[26]), "=r"(d[27]), "=r"(d[28]), "=r"(d[29]), "=r"(d[30]), "=r"(d[31])
+      : "r"(taddr)
+      : "memory");
+}
+}  // namespace tcs
+
+__global__ void __launch_bounds__(128, 1) refresh_tcs_kernel(int64_t I, const float *__restrict__ A,
+                                                             const float *__restrict__ Bt, Dsts dst,
+                                                             uint32_t *guard) {
+  using tc::smem_u32;
+  using tc::hi_bits;
+  using tc::sw128_desc;
+  using tc::mma_tf32_tc;
+  using namespace tcs;
+  extern __shared__ __align__(1024) uint8_t tcs_smem[];
+  const uint32_t sraw = smem_u32(tcs_smem), sbase = (sraw + 1023u) & ~1023u;
+  uint8_t *gb = tcs_smem + (sbase - sraw);
+  const uint32_t ring = sbase, aop = ring + RING * TBYTES;  // a_hi, a_lo
+  const uint32_t bP = aop + 2 * TBYTES, bQ = bP + 64 * 128;
+  const uint32_t bars = bQ + 64 * 128;                      // ld[RING], mma[2], tmem slot
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gb + (bars - sbase) + 8 * (RING + 2));
+  const int tid = threadIdx.x, w = tid >> 5;
+  // B operands P = [Bt_hi ; Bt_lo], Q = [Bt_hi ; 0] (as refresh_tc_kernel)
+  for (int e = tid; e < 32 * 8; e += 128) {
+    const int r = e >> 3, c = e & 7;
+    const float4 v = __ldg(reinterpret_cast<const float4 *>(Bt + r * 32) + c);
+    const uint32_t off = r * 128 + ((c ^ (r & 7)) << 4);
+    uint4 h, l;
+    h.x = hi_bits(v.x), h.y = hi_bits(v.y), h.z = hi_bits(v.z), h.w = hi_bits(v.w);
+    l.x = __float_as_uint(v.x - __uint_as_float(h.x));
+    l.y = __float_as_uint(v.y - __uint_as_float(h.y));
+    l.z = __float_as_uint(v.z - __uint_as_float(h.z));
+    l.w = __float_as_uint(v.w - __uint_as_float(h.w));
+    *reinterpret_cast<uint4 *>(gb + (bP - sbase) + off) = h;
+    *reinterpret_cast<uint4 *>(gb + (bP - sbase) + 32 * 128 + off) = l;
+    *reinterpret_cast<uint4 *>(gb + (bQ - sbase) + off) = h;
+    *reinterpret_cast<uint4 *>(gb + (bQ - sbase) + 32 * 128 + off) = make_uint4(0, 0, 0, 0);
+  }
+  if (w == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;\n" ::"r"(
+        smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) {
+    for (int k = 0; k < RING + 2; ++k)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bars + 8 * k));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+  const int64_t ntiles = (I + TM - 1) / TM;
+  const int nmine = ntiles > blockIdx.x ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x) + 1 : 0;
+  auto tile_of = [&](int it) { return (int64_t)blockIdx.x + (int64_t)it * gridDim.x; };
+  auto rows_of = [&](int64_t t) { return (int)(I - t * TM < TM ? I - t * TM : TM); };
+  if (tid == 0)
+    for (int it = 0; it < RING - 1 && it < nmine; ++it) {
+      const int64_t t = tile_of(it);
+      bulk_load(ring + it * TBYTES, A + t * TM * 32, (uint32_t)rows_of(t) * 128, bars + 8 * it);
+    }
+  uint32_t gmax = 0;
+  auto epilogue = [&](int it) {  // tile it: TMEM -> C staging -> bulk stores
+    const int64_t t = tile_of(it);
+    const int rows = rows_of(t);
+    wait_parity(bars + 8 * (RING + (it & 1)), (it >> 1) & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    uint32_t d[32], d2[32];
+    const uint32_t ta = tmem + ((uint32_t)(32 * w) << 16) + 64 * (it & 1);
+    ld_tmem32(ta, d);
+    ld_tmem32(ta + 32, d2);
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+    // C rows straight from registers: each thread its row, streaming 16-B stores to every
+    // destination (no staging tile: the rotated order a conflict-free one needs would index
+    // registers dynamically)
+    if (tid < rows) {
+#pragma unroll
+      for (int q = 0; q < dst.n && q < FT_MAX_PEERS; ++q) {
+        float4 *out = reinterpret_cast<float4 *>(dst.p[q] + (t * TM + tid) * 32);
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          __stcs(out + c, make_float4(__uint_as_float(d[4 * c]) + __uint_as_float(d2[4 * c]),
+                                      __uint_as_float(d[4 * c + 1]) + __uint_as_float(d2[4 * c + 1]),
+                                      __uint_as_float(d[4 * c + 2]) + __uint_as_float(d2[4 * c + 2]),
+                                      __uint_as_float(d[4 * c + 3]) + __uint_as_float(d2[4 * c + 3])));
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  };
+  for (int it = 0; it < nmine; ++it) {
+    const int64_t t = tile_of(it);
+    const int rows = rows_of(t);
+    if (tid == 0 && it + RING - 1 < nmine) {  // keep RING - 1 loads ahead
+      const int nx = it + RING - 1;
+      const int64_t tn = tile_of(nx);
+      bulk_load(ring + (nx % RING) * TBYTES, A + tn * TM * 32, (uint32_t)rows_of(tn) * 128,
+                bars + 8 * (nx % RING));
+    }
+    wait_parity(bars + 8 * (it % RING), (it / RING) & 1);
+    // the operand tiles are single-buffered: tile it - 1's MMAs must have read them
+    if (it > 0) wait_parity(bars + 8 * (RING + ((it - 1) & 1)), ((it - 1) >> 1) & 1);
+    {  // this thread's row -> hi / lo (swizzled) into the operand tiles
+      const uint32_t src = ring + (it % RING) * TBYTES + tid * 128;
+      const uint32_t ah = aop, al = aop + TBYTES;
+      float4 v[8];  // all 8 chunks first (rotated order: conflict-free), then split and store
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int c = (q + tid) & 7;
+        v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (tid < rows)
+          asm("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];\n"
+              : "=f"(v[q].x), "=f"(v[q].y), "=f"(v[q].z), "=f"(v[q].w)
+              : "r"(src + 16 * c));
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int c = (q + tid) & 7;
+        gmax = max(gmax, max(max(abs_bits(v[q].x), abs_bits(v[q].y)),
+                             max(abs_bits(v[q].z), abs_bits(v[q].w))));
+        const uint32_t off = tid * 128 + ((c ^ (tid & 7)) << 4);
+        const uint32_t hx = hi_bits(v[q].x), hy = hi_bits(v[q].y), hz = hi_bits(v[q].z),
+                       hw = hi_bits(v[q].w);
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(ah + off), "r"(hx), "r"(hy),
+                     "r"(hz), "r"(hw));
+        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};\n" ::"r"(al + off),
+                     "f"(v[q].x - __uint_as_float(hx)), "f"(v[q].y - __uint_as_float(hy)),
+                     "f"(v[q].z - __uint_as_float(hz)), "f"(v[q].w - __uint_as_float(hw)));
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();  // operand tiles written; raw stage it % RING free for its next load
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    if (tid == 0) {
+      const uint32_t ah = aop, al = aop + TBYTES;
+      const uint32_t d = tmem + 64 * (it & 1);
+      for (int k = 0; k < 4; ++k)
+        mma_tf32_tc(d, sw128_desc(ah + 32 * k), sw128_desc(bP + 32 * k), idesc, k > 0);
+      for (int k = 0; k < 4; ++k)
+        mma_tf32_tc(d, sw128_desc(al + 32 * k), sw128_desc(bQ + 32 * k), idesc, 1);
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                       bars + 8 * (RING + (it & 1)))
+                   : "memory");
+    }
+    if (it > 0) epilogue(it - 1);
+  }
+  if (nmine > 0) epilogue(nmine - 1);
+  if (guard) guard_max(guard, gmax);
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (w == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;\n" ::"r"(tmem));
+}
+
 // tensor-core refresh unless FT_REFRESH=simt (the fp32 CUDA-core kernel above, which keeps the
 // reference's sequential-j accumulation order); both need J, R <= 32
 bool use_tc_refresh(int R) {
@@ -295,6 +496,22 @@ bool use_tc_refresh(int R) {
 
 int launch_refresh(int64_t I, int J, int R, const float *A, const float *Bt, const Dsts &d,
                    uint32_t *guard, cudaStream_t s) {
+  if (use_tc_refresh(R) && J == 32 && R == 32 && (reinterpret_cast<uintptr_t>(A) & 15) == 0) {
+    static bool set_s = false;
+    if (!set_s) {
+      cudaFuncSetAttribute(refresh_tcs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)tcs::SMEM);
+      set_s = true;
+    }
+    bool aligned = true;
+    for (int q = 0; q < d.n; ++q) aligned &= (reinterpret_cast<uintptr_t>(d.p[q]) & 15) == 0;
+    if (aligned) {
+      int64_t g = (I + tcs::TM - 1) / tcs::TM;
+      if (g > sm_count()) g = sm_count();
+      refresh_tcs_kernel<<<(unsigned)g, 128, tcs::SMEM, s>>>(I, A, Bt, d, guard);
+      return check_launch("ft_refresh(tcgen05 streaming)");
+    }
+  }
   if (use_tc_refresh(R)) {
     static bool set = false;
     if (!set) {

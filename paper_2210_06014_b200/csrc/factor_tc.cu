@@ -440,14 +440,15 @@ __global__ void __launch_bounds__(tc_threads<PW, KB>(), 1) factor_rows_tc_kernel
     const int64_t gslots = (int64_t)gridDim.x * SLOTS;
     const float lr = p.lr, cdec = -p.lr * p.reg;
     float a[32], lo[32];
-    int64_t row = (int64_t)blockIdx.x + (int64_t)gridDim.x * s;  // this slot's first row
+    // this slot's rows: the contiguous block [q rows / GS, (q + 1) rows / GS) (K1d)
+    int64_t row = ((int64_t)blockIdx.x + (int64_t)gridDim.x * s) * p.nrows / gslots;
     bool have = false;                                          // a holds a row
     int64_t cur_i = -1;
     // row coordinates run two rows ahead of the chain and the next row's A values are copied
     // into this thread's shared-memory buffer one row ahead (cp.async: no registers held), so
     // a row switch never waits on a global load
     int ci1 = row < p.nrows ? __ldg(p.row_coord + row) : -1;
-    int ci2 = row + gslots < p.nrows ? __ldg(p.row_coord + row + gslots) : -1;
+    int ci2 = row + 1 < p.nrows ? __ldg(p.row_coord + row + 1) : -1;
     const uint32_t my_na = nabuf + (uint32_t)(s * 128);
     auto prefetch_row = [&](int ci) {
       if (ci >= 0) {
@@ -515,9 +516,9 @@ __global__ void __launch_bounds__(tc_threads<PW, KB>(), 1) factor_rows_tc_kernel
       if ((uint32_t)mlc & ROW_START) {
         if (have) {
           store_row();
-          row += gslots;
+          row += 1;
           ci1 = ci2;
-          ci2 = row + gslots < p.nrows ? __ldg(p.row_coord + row + gslots) : -1;
+          ci2 = row + 1 < p.nrows ? __ldg(p.row_coord + row + 1) : -1;
         }
         have = true;
         cur_i = ci1;
@@ -591,11 +592,11 @@ __global__ void __launch_bounds__(tc_threads<PW, KB>(), 1) factor_rows_tc_kernel
     const int64_t gslots = (int64_t)gridDim.x * (SLOTS / KB);
     const float lr = p.lr, cdec = -p.lr * p.reg;
     float a[8], lo[8];
-    int64_t row = (int64_t)blockIdx.x + (int64_t)gridDim.x * rs;  // this row slot's first row
+    int64_t row = ((int64_t)blockIdx.x + (int64_t)gridDim.x * rs) * p.nrows / gslots;
     bool have = false;
     int64_t cur_i = -1;
     int ci1 = row < p.nrows ? __ldg(p.row_coord + row) : -1;
-    int ci2 = row + gslots < p.nrows ? __ldg(p.row_coord + row + gslots) : -1;
+    int ci2 = row + 1 < p.nrows ? __ldg(p.row_coord + row + 1) : -1;
     const uint32_t my_na = nabuf + (uint32_t)(rs * 128 + 32 * qq);
     const int j0 = 8 * qq;
     auto prefetch_row = [&](int ci) {
@@ -668,9 +669,9 @@ __global__ void __launch_bounds__(tc_threads<PW, KB>(), 1) factor_rows_tc_kernel
         if (slow && live && ((uint32_t)mlc & ROW_START)) {
           if (have) {
             store_row();
-            row += gslots;
+            row += 1;
             ci1 = ci2;
-            ci2 = row + gslots < p.nrows ? __ldg(p.row_coord + row + gslots) : -1;
+            ci2 = row + 1 < p.nrows ? __ldg(p.row_coord + row + 1) : -1;
           }
           have = true;
           cur_i = ci1;
@@ -726,96 +727,112 @@ __global__ void __launch_bounds__(tc_threads<PW, KB>(), 1) factor_rows_tc_kernel
 
 // ---- K1d: the slot layout ------------------------------------------------------------------
 // KB leaves of one row slot per batch: a CTA has RS = 128 / KB row slots; row slot q = c + G rs
-// (CTA c, rs < RS) owns rows q, q + G RS, q + 2 G RS, ... of the tree, and its stream is their
-// leaves in order.  Stream position p of q sits in batch p / KB at TMEM lane / entry slot
-// s = KB rs + p % KB: entry (batch_ptr[c] + p / KB) * 128 + s.  KB = 1: one thread per row
-// (K3c); KB = 8: 16 rows per CTA for few, long rows (K3c-wide).
-// slot_rows_kernel: per row its offset in its row slot's stream, per CTA its batch count.
+// (CTA c, rs < RS) of GS = G RS owns the contiguous rows [q rows / GS, (q + 1) rows / GS) of
+// the tree, so its stream is ONE contiguous range of the tree's leaves.  Stream position p of q
+// sits in batch p / KB at TMEM lane / entry slot s = KB rs + p % KB: entry
+// (batch_ptr[c] + p / KB) * 128 + s.  KB = 1: one thread per row (K3c); KB = 8: 16 rows per CTA
+// for few, long rows (K3c-wide).
+__device__ __forceinline__ int64_t slot_first_row(int64_t q, int64_t rows, int64_t gs) {
+  return q * rows / gs;
+}
+// slot_rows_kernel: per CTA its batch count (the longest stream of its row slots)
 __global__ void slot_rows_kernel(const int32_t *__restrict__ row_leaf_ptr, int64_t rows, int G,
-                                 int KB, int32_t *__restrict__ row_off, int32_t *__restrict__ nbatch) {
+                                 int KB, int32_t *__restrict__ nbatch) {
   const int c = blockIdx.x, RS = SLOTS / KB;
-  const int64_t gsl = (int64_t)G * RS;
+  const int64_t gs = (int64_t)G * RS;
   int64_t tot = 0;
-  if ((int)threadIdx.x < RS)
-    for (int64_t r = c + (int64_t)G * threadIdx.x; r < rows; r += gsl) {
-      row_off[r] = (int32_t)tot;
-      tot += __ldg(row_leaf_ptr + r + 1) - __ldg(row_leaf_ptr + r);
-    }
+  if ((int)threadIdx.x < RS) {
+    const int64_t q = c + (int64_t)G * threadIdx.x;
+    tot = __ldg(row_leaf_ptr + slot_first_row(q + 1, rows, gs)) -
+          __ldg(row_leaf_ptr + slot_first_row(q, rows, gs));
+  }
   using BR = cub::BlockReduce<int64_t, SLOTS>;
   __shared__ typename BR::TempStorage ts;
   const int64_t mx = BR(ts).Reduce(tot, cub::Max());
   if (threadIdx.x == 0) nbatch[c] = (int32_t)((mx + KB - 1) / KB);
 }
+// the first leaf of every row, as a byte flag per leaf (row starts for the fill)
+__global__ void row_start_kernel(const int32_t *__restrict__ row_leaf_ptr, int64_t rows,
+                                 uint8_t *__restrict__ flag) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < rows) flag[row_leaf_ptr[r]] = 1;
+}
 
-__global__ void slot_scan_kernel(const int32_t *__restrict__ nbatch, int G, int32_t *batch_ptr) {
+__global__ void slot_scan_kernel(const int32_t *__restrict__ nbatch, int G, int32_t *batch_ptr,
+                                 int32_t *total_max) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
-    int32_t acc = 0;
+    int32_t acc = 0, mx = 0;
     for (int c = 0; c < G; ++c) {
       batch_ptr[c] = acc;
       acc += nbatch[c];
+      mx = nbatch[c] > mx ? nbatch[c] : mx;
     }
     batch_ptr[G] = acc;
+    total_max[0] = acc;
+    total_max[1] = mx;
   }
 }
 
-// block (c, j): batches [32 j, 32 j + 32) of CTA c; thread = entry slot s = KB rs + k walks its
-// row slot's stream positions 32 j KB + k, + KB, ... (32 of them), staging the entries in shared
-// memory so that the stores of each batch (128 consecutive entries) are coalesced
-template <int NPRE>
-constexpr int fill_b() { return NPRE == 1 ? 32 : 16; }  // 48 KB of static staging at most
+// block (c, j): batches [32 j, 32 j + 32) of CTA c.  Phase 1, warp per entry slot: lane i takes
+// the slot's stream position for batch 32 j + i -- leaf (first leaf of the slot) + position,
+// coalesced -- into a padded shared tile [i][s]; phase 2, thread per slot: each batch's 128
+// entries leave as one coalesced store.
+constexpr int FILL_B = 32, FILL_PAD = SLOTS + 1;
 template <int NPRE>
 __global__ void __launch_bounds__(SLOTS) slot_fill_kernel(
-    const int32_t *__restrict__ row_leaf_ptr, const int32_t *__restrict__ row_off, int64_t rows,
+    const int32_t *__restrict__ row_leaf_ptr, const uint8_t *__restrict__ row_start, int64_t rows,
     int G, int KB, const int32_t *__restrict__ batch_ptr, const int32_t *__restrict__ leaf_coord,
     const int32_t *__restrict__ leaf_pc, const float *__restrict__ vals,
     int32_t *__restrict__ slot_lc, int32_t *__restrict__ slot_pc, float *__restrict__ slot_x) {
-  constexpr int FILL_B = fill_b<NPRE>();
-  __shared__ int32_t t_lc[FILL_B][SLOTS];
-  __shared__ int32_t t_pc[NPRE > 0 ? NPRE : 1][FILL_B][SLOTS];
-  __shared__ float t_x[FILL_B][SLOTS];
-  const int c = blockIdx.x, s = threadIdx.x, RS = SLOTS / KB, rs = s / KB, k = s % KB;
+  extern __shared__ int32_t fill_smem[];
+  int32_t *t_lc = fill_smem;                                          // [FILL_B][FILL_PAD]
+  int32_t *t_pc = t_lc + FILL_B * FILL_PAD;                           // [NPRE][FILL_B][FILL_PAD]
+  float *t_x = reinterpret_cast<float *>(t_pc + NPRE * FILL_B * FILL_PAD);
+  __shared__ int64_t s_leaf0[SLOTS], s_leafe[SLOTS];
+  const int c = blockIdx.x, RS = SLOTS / KB, lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   const int64_t b0 = batch_ptr[c];
   const int nb = batch_ptr[c + 1] - (int)b0;
   const int jb = (int)blockIdx.y * FILL_B;
   if (jb >= nb) return;
-  const int64_t gsl = (int64_t)G * RS;
-  int64_t p = (int64_t)jb * KB + k;  // this thread's first stream position
-  // the row holding position p (rows of one slot: a few dozen at most in practice)
-  int64_t r = c + (int64_t)G * rs;
-  int64_t off = 0, len = 0;
-  if (r < rows) off = row_off[r], len = row_leaf_ptr[r + 1] - row_leaf_ptr[r];
-  while (r < rows && p >= off + len) {
-    r += gsl;
-    if (r < rows) off = row_off[r], len = row_leaf_ptr[r + 1] - row_leaf_ptr[r];
+  const int64_t gs = (int64_t)G * RS;
+  {  // this thread's row slot: its leaf range
+    const int rs = threadIdx.x / KB;
+    const int64_t q = c + (int64_t)G * rs;
+    s_leaf0[threadIdx.x] = row_leaf_ptr[slot_first_row(q, rows, gs)];
+    s_leafe[threadIdx.x] = row_leaf_ptr[slot_first_row(q + 1, rows, gs)];
   }
-  for (int i = 0; i < FILL_B; ++i, p += KB) {
-    while (r < rows && p >= off + len) {
-      r += gsl;
-      if (r < rows) off = row_off[r], len = row_leaf_ptr[r + 1] - row_leaf_ptr[r];
-    }
-    if (r < rows && p >= off) {
-      const int64_t L = row_leaf_ptr[r] + (p - off);
-      t_lc[i][s] = (int32_t)((uint32_t)__ldg(leaf_coord + L) | (p == off ? ROW_START : 0u));
+  __syncthreads();
+#pragma unroll 4
+  for (int s = wp; s < SLOTS; s += SLOTS / 32) {
+    const int k = s % KB;
+    const int64_t L = s_leaf0[s] + (int64_t)(jb + lane) * KB + k;
+    const int e = lane * FILL_PAD + s;
+    if (L < s_leafe[s]) {
+      t_lc[e] = (int32_t)((uint32_t)__ldg(leaf_coord + L) | (row_start[L] ? ROW_START : 0u));
 #pragma unroll
-      for (int d = 0; d < NPRE; ++d) t_pc[d][i][s] = __ldg(leaf_pc + L * NPRE + d);
-      t_x[i][s] = __ldg(vals + L);
+      for (int d = 0; d < NPRE; ++d) t_pc[d * FILL_B * FILL_PAD + e] = __ldg(leaf_pc + L * NPRE + d);
+      t_x[e] = __ldg(vals + L);
     } else {
-      t_lc[i][s] = PAD;
+      t_lc[e] = PAD;
 #pragma unroll
-      for (int d = 0; d < NPRE; ++d) t_pc[d][i][s] = 0;
-      t_x[i][s] = 0.f;
+      for (int d = 0; d < NPRE; ++d) t_pc[d * FILL_B * FILL_PAD + e] = 0;
+      t_x[e] = 0.f;
     }
   }
   __syncthreads();
+  const int s = threadIdx.x;
   const int nbat = nb - jb < FILL_B ? nb - jb : FILL_B;
   for (int i = 0; i < nbat; ++i) {
     const int64_t e = (b0 + jb + i) * SLOTS + s;
-    slot_lc[e] = t_lc[i][s];
+    slot_lc[e] = t_lc[i * FILL_PAD + s];
 #pragma unroll
-    for (int d = 0; d < NPRE; ++d) slot_pc[((b0 + jb + i) * NPRE + d) * SLOTS + s] = t_pc[d][i][s];
-    slot_x[e] = t_x[i][s];
+    for (int d = 0; d < NPRE; ++d)
+      slot_pc[((b0 + jb + i) * NPRE + d) * SLOTS + s] = t_pc[d * FILL_B * FILL_PAD + i * FILL_PAD + s];
+    slot_x[e] = t_x[i * FILL_PAD + s];
   }
 }
+template <int NPRE>
+constexpr size_t fill_smem_bytes() { return (size_t)(2 + NPRE) * FILL_B * FILL_PAD * 4; }
 
 // R > 16: at R = 16 the MMA count per batch halves but its fixed cost does not, and quadr's
 // mma.sync combine is faster (Netflix16 modes 0/1: 2.3 vs 3.5 ms; profiles/r02_factor_tc_ab.md)
@@ -908,7 +925,7 @@ int launch_factor_tc(const ft_tree_t *t, const ft_model_t *m, float lr, float re
   return launch_tc_t<2, 2>(q, t->slot_grid, comp, s);
 }
 
-// ft_tree_slot_plan hands its per-row stream offsets to the ft_tree_slot_fill that follows
+// ft_tree_slot_plan hands its per-leaf row-start flags to the ft_tree_slot_fill that follows
 // (the Python driver calls them back to back on one thread)
 int32_t *&planned_row_off() {
   static int32_t *p = nullptr;
@@ -917,6 +934,10 @@ int32_t *&planned_row_off() {
 int &planned_kb() {
   static int kb = 1;
   return kb;
+}
+int &planned_maxnb() {
+  static int m = 0;
+  return m;
 }
 
 // which layout the factor sweep of this tree uses: 1 (K3c: one thread per row), 8 (K3c-wide:
@@ -965,18 +986,27 @@ extern "C" int ft_tree_slot_plan(const ft_tree_t *tree, int32_t J, int32_t R, in
   cudaStream_t s = as_stream(stream);
   int32_t *nbatch = nullptr;
   FT_CUDA(cudaMallocAsync(&nbatch, sizeof(int32_t) * G, s));
-  int32_t *row_off = nullptr;  // scratch, handed to ft_tree_slot_fill
-  FT_CUDA(cudaMallocAsync(&row_off, sizeof(int32_t) * rows, s));
-  slot_rows_kernel<<<G, SLOTS, 0, s>>>(tree->row_leaf_ptr, rows, G, KB, row_off, nbatch);
+  // row-start flags per leaf: scratch, handed to ft_tree_slot_fill
+  uint8_t *rstart = nullptr;
+  FT_CUDA(cudaMallocAsync(&rstart, (size_t)tree->nnz, s));
+  FT_CUDA(cudaMemsetAsync(rstart, 0, (size_t)tree->nnz, s));
+  row_start_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(tree->row_leaf_ptr, rows, rstart);
+  if (int rc = check_launch("ft_tree_slot_plan(row starts)")) return rc;
+  slot_rows_kernel<<<G, SLOTS, 0, s>>>(tree->row_leaf_ptr, rows, G, KB, nbatch);
   if (int rc = check_launch("ft_tree_slot_plan(rows)")) return rc;
-  slot_scan_kernel<<<1, 32, 0, s>>>(nbatch, G, batch_ptr);
+  int32_t *tm = nullptr;
+  FT_CUDA(cudaMallocAsync(&tm, 2 * sizeof(int32_t), s));
+  slot_scan_kernel<<<1, 32, 0, s>>>(nbatch, G, batch_ptr, tm);
   if (int rc = check_launch("ft_tree_slot_plan(scan)")) return rc;
-  int32_t total = 0;
-  FT_CUDA(cudaMemcpyAsync(&total, batch_ptr + G, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  int32_t host_tm[2] = {0, 0};
+  FT_CUDA(cudaMemcpyAsync(host_tm, tm, sizeof(host_tm), cudaMemcpyDeviceToHost, s));
   FT_CUDA(cudaFreeAsync(nbatch, s));
+  FT_CUDA(cudaFreeAsync(tm, s));
   FT_CUDA(cudaStreamSynchronize(s));
-  if (planned_row_off()) cudaFree(planned_row_off());  // a plan never followed by its fill
-  planned_row_off() = row_off;  // handed to ft_tree_slot_fill (same stream, next call)
+  const int32_t total = host_tm[0];
+  planned_maxnb() = host_tm[1];
+  if (planned_row_off()) cudaFreeAsync(planned_row_off(), s);  // a plan never followed by fill
+  planned_row_off() = reinterpret_cast<int32_t *>(rstart);  // handed to ft_tree_slot_fill
   planned_kb() = KB;
   *grid_out = G;
   *len_out = (int64_t)total * SLOTS;
@@ -991,28 +1021,34 @@ extern "C" int ft_tree_slot_fill(const ft_tree_t *tree, int32_t grid, const int3
   const int npre = tree->order - 2;
   if (npre > 0 && (!slot_pc || !tree->leaf_pc))
     return fail(FT_ERR_ARG, "ft_tree_slot_fill: prefix index missing");
-  int32_t *row_off = planned_row_off();
+  uint8_t *row_off = reinterpret_cast<uint8_t *>(planned_row_off());  // the row-start flags
   if (!row_off) return fail(FT_ERR_ARG, "ft_tree_slot_fill: call ft_tree_slot_plan first");
   planned_row_off() = nullptr;
   cudaStream_t s = as_stream(stream);
   const int KB = planned_kb();
-  // the longest CTA stream bounds the batch blocks: read it back from batch_ptr
-  std::vector<int32_t> bp(grid + 1);
-  FT_CUDA(cudaMemcpyAsync(bp.data(), batch_ptr, sizeof(int32_t) * (grid + 1),
-                          cudaMemcpyDeviceToHost, s));
-  FT_CUDA(cudaStreamSynchronize(s));
-  int maxnb = 0;
-  for (int c = 0; c < grid; ++c) maxnb = std::max(maxnb, bp[c + 1] - bp[c]);
-  const int fb = npre == 1 ? fill_b<1>() : fill_b<2>();
-  const dim3 g(grid, (maxnb + fb - 1) / fb);
-  if (npre == 1)
-    slot_fill_kernel<1><<<g, SLOTS, 0, s>>>(tree->row_leaf_ptr, row_off, tree->num_rows, grid, KB,
-                                            batch_ptr, tree->leaf_coord, tree->leaf_pc, tree->vals,
-                                            slot_lc, slot_pc, slot_x);
-  else
-    slot_fill_kernel<2><<<g, SLOTS, 0, s>>>(tree->row_leaf_ptr, row_off, tree->num_rows, grid, KB,
-                                            batch_ptr, tree->leaf_coord, tree->leaf_pc, tree->vals,
-                                            slot_lc, slot_pc, slot_x);
+  const int maxnb = planned_maxnb();  // the longest CTA stream bounds the batch blocks
+  const dim3 g(grid, (maxnb + FILL_B - 1) / FILL_B);
+  if (npre == 1) {
+    static bool set1 = false;
+    if (!set1) {
+      cudaFuncSetAttribute(slot_fill_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)fill_smem_bytes<1>());
+      set1 = true;
+    }
+    slot_fill_kernel<1><<<g, SLOTS, fill_smem_bytes<1>(), s>>>(
+        tree->row_leaf_ptr, row_off, tree->num_rows, grid, KB, batch_ptr, tree->leaf_coord,
+        tree->leaf_pc, tree->vals, slot_lc, slot_pc, slot_x);
+  } else {
+    static bool set2 = false;
+    if (!set2) {
+      cudaFuncSetAttribute(slot_fill_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)fill_smem_bytes<2>());
+      set2 = true;
+    }
+    slot_fill_kernel<2><<<g, SLOTS, fill_smem_bytes<2>(), s>>>(
+        tree->row_leaf_ptr, row_off, tree->num_rows, grid, KB, batch_ptr, tree->leaf_coord,
+        tree->leaf_pc, tree->vals, slot_lc, slot_pc, slot_x);
+  }
   const int rc = check_launch("ft_tree_slot_fill");
   cudaFreeAsync(row_off, s);
   return rc;

@@ -62,8 +62,9 @@ def test_tc_factor_sweeps_match_oracle(dims, nnz, J, R, lr, comp):
 
 
 def test_slot_layout_covers_every_leaf_once(ft):
-    """K1d: per CTA c and slot s, the non-padding entries [batch][s] are exactly the leaves of
-    rows c + G s, c + G s + 128 G, ... in order, the first leaf of each row flagged."""
+    """K1d: slot q = c + G s owns the contiguous rows [q rows / GS, (q + 1) rows / GS); per CTA c
+    and slot s the non-padding entries [batch][s] are exactly those rows' leaves in order, the
+    first leaf of each row flagged, and every leaf appears once."""
     import torch
 
     rng = np.random.default_rng(2)
@@ -74,7 +75,7 @@ def test_slot_layout_covers_every_leaf_once(ft):
                        torch.from_numpy(rng.uniform(1, 5, len(lin)).astype(np.float32)).cuda())
     tree = ft.build_tree(dev, 0, 128).ensure_slots(32, 32)
     G = tree.slot_grid
-    assert G > 0
+    assert G > 0 and tree.slot_kb == 1
     bp = tree.slot_batch_ptr.cpu().numpy()
     lc = tree.slot_lc.cpu().numpy().view(np.uint32)
     pc = tree.slot_pc.cpu().numpy()
@@ -83,22 +84,20 @@ def test_slot_layout_covers_every_leaf_once(ft):
     leaf_coord = tree.leaf_coord.cpu().numpy()
     leaf_pc = tree.leaf_pc.cpu().numpy().reshape(-1)
     vals = tree.vals.cpu().numpy()
-    rows = tree.num_rows
+    rows, GS = tree.num_rows, 128 * G
     seen = 0
     for c in range(G):
-        for s in range(0, 128, 7):  # a sample of slots
-            want = []
-            for r in range(c + G * s, rows, 128 * G):
-                for L in range(rlp[r], rlp[r + 1]):
-                    want.append((int(leaf_coord[L]) | (0x80000000 if L == rlp[r] else 0),
-                                 int(leaf_pc[L]), float(vals[L])))
-            got = []
-            for b in range(bp[c], bp[c + 1]):
-                e = b * 128 + s
-                if lc[e] == 0xFFFFFFFF:
-                    continue
-                got.append((int(lc[e]), int(pc[e]), float(x[e])))
-            assert got == want
+        for s in range(128):
+            q = c + G * s
+            r0, r1 = q * rows // GS, (q + 1) * rows // GS
+            want = [(int(leaf_coord[L]) | (0x80000000 if L == rlp[r] else 0), int(leaf_pc[L]),
+                     float(vals[L])) for r in range(r0, r1) for L in range(rlp[r], rlp[r + 1])]
+            e = np.arange(bp[c], bp[c + 1]) * 128 + s
+            live = lc[e] != 0xFFFFFFFF
+            got = list(zip(lc[e][live].astype(int).tolist(), pc[e][live].tolist(),
+                           x[e][live].astype(float).tolist()))
+            assert got == want, (c, s)
+            assert not live[len(want):].any()  # padding only at the end of the stream
             seen += len(got)
-    assert seen > 0
+    assert seen == tree.nnz
     assert bp[-1] * 128 == tree.slot_lc.numel()

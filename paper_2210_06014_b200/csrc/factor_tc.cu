@@ -358,7 +358,10 @@ __global__ void __launch_bounds__(tc_threads<PW, KB>(), 1) factor_rows_tc_kernel
         for (int it = 0; it < 8; ++it) {
           const uint32_t cs = __shfl_sync(FULL, coord[lv], 4 * it + gs);
           const uint32_t dst = lbase + (it & 1 ? gdst1 : gdst0) + (it >> 1) * 1024;
-          const char *src = Cl[lv] + (R32 ? (size_t)cs * 128u : (size_t)cs * rowb);
+          // base + cs * row bytes in one 64-bit multiply-add
+          const void *src;
+          asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(src) : "r"(cs), "r"(R32 ? 128u : rowb),
+              "l"(Cl[lv]));
           if (R32)
             cp16(dst, src);
           else
@@ -393,7 +396,6 @@ __global__ void __launch_bounds__(tc_threads<PW, KB>(), 1) factor_rows_tc_kernel
       cp_wait<D - 1>();   // this lane's copies of batch b have landed
       __syncwarp();       // ... and every lane's
       const int st = b % AS;
-      const bool live = (int)lds32(my_meta + (uint32_t)((b & (P::MS - 1)) * P::MSTRIDE)) != PAD;
       if (b >= AS) mbar_wait(a_free + st, (b / AS - 1) & 1);  // MMAs of batch b - AS done
       tc_fence_after();
       // cross of slot s -> 3xTF32 halves -> TMEM A stage st
@@ -405,8 +407,10 @@ __global__ void __launch_bounds__(tc_threads<PW, KB>(), 1) factor_rows_tc_kernel
 #pragma unroll
         for (int qq = 0; qq < 2; ++qq) {
           const int c = 2 * h + qq;
+          // padding slots gathered C row 0 (finite; the consumer skips their step); only the
+          // chunks past R (never copied, and multiplied by B's zero padding) must read as zero
           float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (live && (R32 || 4 * c < R)) {
+          if (R32 || 4 * c < R) {
             const uint32_t co = (uint32_t)((c ^ swz) << 4);
             x = lds128(st0 + co);
 #pragma unroll

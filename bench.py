@@ -320,14 +320,23 @@ def live_traffic(args, N, timeout=420):
            "--log-file", logf, sys.executable, os.path.join(REPO, "bench.py"), "--config",
            args.config, "--schedule", args.schedule, "--ncu-child"]
     t0 = time.perf_counter()
+    # own process group: on a timeout the whole group (ncu AND its bench child, which holds the
+    # workload's device memory) is killed, never left running under the next command
+    proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True,
+                            start_new_session=True)
     try:
-        proc = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
+        _, err = proc.communicate(timeout=timeout)
+        proc.stderr_tail = err
     except subprocess.TimeoutExpired:
+        import signal
+
+        os.killpg(proc.pid, signal.SIGKILL)
+        proc.communicate()
         return {"error": f"ncu timed out after {timeout} s"}
     try:
         rows = list(csv.reader(io.StringIO(open(logf).read())))
     except OSError:
-        return {"error": f"ncu produced no log (rc {proc.returncode}): {proc.stderr[-300:]}"}
+        return {"error": f"ncu produced no log (rc {proc.returncode}): {proc.stderr_tail[-300:]}"}
     hi = next((i for i, r in enumerate(rows) if "Kernel Name" in r), None)
     if hi is None:
         return {"error": f"ncu log without a header (rc {proc.returncode})"}

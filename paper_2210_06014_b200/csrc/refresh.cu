@@ -8,6 +8,9 @@
 #include <string.h>
 #include <stdlib.h>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "ft_common.cuh"
 
 namespace ft {
@@ -284,19 +287,21 @@ __global__ void __launch_bounds__(128) refresh_tc_kernel(int64_t I, int J, int R
 }
 
 // ---- K2, streaming form (J = R = 32): TMA bulk copies in and out, two tiles in the MMA ------
-// A's 128-row tiles are contiguous 16 KB blocks, and so are C's: one elected thread keeps a
-// 4-deep ring of tile loads in flight (cp.async.bulk, completion on mbarriers) and writes each
-// finished C tile to every destination with one bulk store (cp.async.bulk shared -> global,
-// peers included).  Per tile the 128 threads read their row from the landed raw tile (chunks in
-// a rotated order: conflict-free), fold the guard max, split it into the 128-B-swizzled hi / lo
-// operand tiles (double-buffered), and one thread issues the tile's 8 N = 64 MMAs into one of two
-// TMEM accumulators; the epilogue of tile t-1 (TMEM -> registers -> C staging tile -> bulk
-// store) runs while the tensor core works on tile t.
+// A's 128-row tiles are contiguous 16 KB blocks: one elected thread keeps RING - 1 tile loads
+// in flight (cp.async.bulk, completion on mbarriers).  Per tile the 128 threads read their row
+// from the landed raw tile (chunks in a rotated order: conflict-free), fold the guard max, split
+// it into one of two 128-B-swizzled hi / lo operand pairs, and one thread issues the tile's 8
+// N = 64 MMAs into one of two TMEM accumulators.  The epilogue of tile t-1 (TMEM -> registers ->
+// the warp's swizzled staging slab -> coalesced 512-B row-group stores to every destination,
+// peers included) runs while the tensor core works on tile t, and the split of tile t+1 no
+// longer waits for tile t's MMAs.
 namespace tcs {
-constexpr int TM = 128, TBYTES = TM * 128, RING = 8;
-// raw ring (7 tile loads in flight: ~112 KB per SM against the HBM latency) + one hi / lo
-// operand pair + P, Q: ~177 KB, one CTA per SM
-constexpr size_t SMEM = 1024 + (size_t)RING * TBYTES + 2 * (size_t)TBYTES + 2 * (64 * 128) + 128;
+constexpr int TM = 128, TBYTES = TM * 128, RING = 6;
+// raw ring (5 tile loads in flight: ~80 KB per SM against the HBM latency) + two hi / lo
+// operand pairs (tile t + 1 is split while the tensor core works on tile t) + P, Q + the C
+// staging tile (one 4 KB slab per warp): ~193 KB, one CTA per SM
+constexpr size_t SMEM = 1024 + (size_t)RING * TBYTES + 4 * (size_t)TBYTES + 2 * (64 * 128) +
+                        (size_t)TBYTES + 128;
 __device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_t bytes,
                                           uint32_t bar) {
   asm volatile(
@@ -345,9 +350,10 @@ __global__ void __launch_bounds__(128, 1) refresh_tcs_kernel(int64_t I, const fl
   extern __shared__ __align__(1024) uint8_t tcs_smem[];
   const uint32_t sraw = smem_u32(tcs_smem), sbase = (sraw + 1023u) & ~1023u;
   uint8_t *gb = tcs_smem + (sbase - sraw);
-  const uint32_t ring = sbase, aop = ring + RING * TBYTES;  // a_hi, a_lo
-  const uint32_t bP = aop + 2 * TBYTES, bQ = bP + 64 * 128;
-  const uint32_t bars = bQ + 64 * 128;                      // ld[RING], mma[2], tmem slot
+  const uint32_t ring = sbase, aop = ring + RING * TBYTES;  // [2][a_hi, a_lo]
+  const uint32_t bP = aop + 4 * TBYTES, bQ = bP + 64 * 128;
+  const uint32_t stage = bQ + 64 * 128;                     // C staging, 4 KB per warp
+  const uint32_t bars = stage + TBYTES;                     // ld[RING], mma[2], tmem slot
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gb + (bars - sbase) + 8 * (RING + 2));
   const int tid = threadIdx.x, w = tid >> 5;
   // B operands P = [Bt_hi ; Bt_lo], Q = [Bt_hi ; 0] (as refresh_tc_kernel)
@@ -402,21 +408,33 @@ __global__ void __launch_bounds__(128, 1) refresh_tcs_kernel(int64_t I, const fl
     ld_tmem32(ta, d);
     ld_tmem32(ta + 32, d2);
     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-    // C rows straight from registers: each thread its row, streaming 16-B stores to every
-    // destination (no staging tile: the rotated order a conflict-free one needs would index
-    // registers dynamically)
-    if (tid < rows) {
+    // C rows through this warp's staging slab (128-B swizzle: conflict-free both ways), then
+    // written back coalesced: four whole rows (512 contiguous bytes) per warp store
+    const int lane = tid & 31;
+    const uint32_t slab = stage + w * 4096;
 #pragma unroll
-      for (int q = 0; q < dst.n && q < FT_MAX_PEERS; ++q) {
-        float4 *out = reinterpret_cast<float4 *>(dst.p[q] + (t * TM + tid) * 32);
+    for (int c = 0; c < 8; ++c)
+      asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};\n" ::"r"(slab + lane * 128 + ((c ^ (lane & 7)) << 4)),
+                   "f"(__uint_as_float(d[4 * c]) + __uint_as_float(d2[4 * c])),
+                   "f"(__uint_as_float(d[4 * c + 1]) + __uint_as_float(d2[4 * c + 1])),
+                   "f"(__uint_as_float(d[4 * c + 2]) + __uint_as_float(d2[4 * c + 2])),
+                   "f"(__uint_as_float(d[4 * c + 3]) + __uint_as_float(d2[4 * c + 3])));
+    __syncwarp();
+    const int c = lane & 7;
 #pragma unroll
-        for (int c = 0; c < 8; ++c)
-          __stcs(out + c, make_float4(__uint_as_float(d[4 * c]) + __uint_as_float(d2[4 * c]),
-                                      __uint_as_float(d[4 * c + 1]) + __uint_as_float(d2[4 * c + 1]),
-                                      __uint_as_float(d[4 * c + 2]) + __uint_as_float(d2[4 * c + 2]),
-                                      __uint_as_float(d[4 * c + 3]) + __uint_as_float(d2[4 * c + 3])));
+    for (int i = 0; i < 8; ++i) {
+      const int r = 4 * i + (lane >> 3), row = 32 * w + r;
+      float4 v;
+      asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];\n"
+                   : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                   : "r"(slab + r * 128 + ((c ^ (r & 7)) << 4)));
+      if (row < rows) {
+#pragma unroll
+        for (int q = 0; q < dst.n && q < FT_MAX_PEERS; ++q)
+          __stcs(reinterpret_cast<float4 *>(dst.p[q] + (t * TM + row) * 32) + c, v);
       }
     }
+    __syncwarp();
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   };
   for (int it = 0; it < nmine; ++it) {
@@ -429,11 +447,11 @@ __global__ void __launch_bounds__(128, 1) refresh_tcs_kernel(int64_t I, const fl
                 bars + 8 * (nx % RING));
     }
     wait_parity(bars + 8 * (it % RING), (it / RING) & 1);
-    // the operand tiles are single-buffered: tile it - 1's MMAs must have read them
-    if (it > 0) wait_parity(bars + 8 * (RING + ((it - 1) & 1)), ((it - 1) >> 1) & 1);
+    // operand pair it & 1 was last read by tile it - 2's MMAs, whose completion epilogue(it - 2)
+    // waited for in the previous iteration
     {  // this thread's row -> hi / lo (swizzled) into the operand tiles
       const uint32_t src = ring + (it % RING) * TBYTES + tid * 128;
-      const uint32_t ah = aop, al = aop + TBYTES;
+      const uint32_t ah = aop + (it & 1) * 2 * TBYTES, al = ah + TBYTES;
       float4 v[8];  // all 8 chunks first (rotated order: conflict-free), then split and store
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -464,7 +482,7 @@ __global__ void __launch_bounds__(128, 1) refresh_tcs_kernel(int64_t I, const fl
     __syncthreads();  // operand tiles written; raw stage it % RING free for its next load
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     if (tid == 0) {
-      const uint32_t ah = aop, al = aop + TBYTES;
+      const uint32_t ah = aop + (it & 1) * 2 * TBYTES, al = ah + TBYTES;
       const uint32_t d = tmem + 64 * (it & 1);
       for (int k = 0; k < 4; ++k)
         mma_tf32_tc(d, sw128_desc(ah + 32 * k), sw128_desc(bP + 32 * k), idesc, k > 0);
@@ -484,6 +502,254 @@ __global__ void __launch_bounds__(128, 1) refresh_tcs_kernel(int64_t I, const fl
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;\n" ::"r"(tmem));
 }
 
+// ---- K2, TMA form (J = R = 32, one destination): warp-specialised, no CTA-wide barriers -------
+// warp 0 lane 0 streams A tiles with 2D tensor loads (cp.async.bulk.tensor, 128-B swizzle: the
+// landed tile IS the K-major SW128 MMA operand, ragged last tile zero-filled by the TMA unit);
+// warp 1 lane 0 issues the MMAs; warps 2-5 (one TMEM lane quadrant each) read their 32 rows from
+// the landed tile (conflict-free through the swizzle), fold the guard max and write A_lo =
+// A - trunc_tf32(A) into TMEM, then run the epilogue of the previous tile (TMEM -> swizzled
+// staging slab -> one 2D tensor store of 32 rows).  3xTF32 per tile: 4 x N = 64 MMAs of the raw
+// tile (the tensor core truncates it to A_hi) against P = [Bt_hi ; Bt_lo] plus 4 x N = 32 MMAs
+// of A_lo (TMEM) against Bt_hi: 8 MMAs, D[:, 0:32] + D[:, 32:64] = C.  Warps hand off through
+// mbarriers only (full / empty per ring stage, lo_ready and acc_full per TMEM stage), so each
+// warp runs at its own pace; ~104 KB of shared memory and 256 TMEM columns: two CTAs per SM.
+namespace tma {
+constexpr int TM = 128, TBYTES = TM * 128, RING = 4, THREADS = 192;
+constexpr uint32_t TMEM_COLS = 256, LO = 128;  // D stages at 0 / 64, A_lo stages at 128 / 160
+// ring + P + staging (4 worker warps x 2 x 4 KB) + barriers, 1024-B aligned
+constexpr size_t SMEM = 1024 + (size_t)RING * TBYTES + 64 * 128 + 8 * 4096 + 256;
+__device__ __forceinline__ void load2d(uint32_t dst, const CUtensorMap *m, int c0, int c1,
+                                       uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, "
+      "{%2, %3}], [%4];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void store2d(const CUtensorMap *m, int c0, int c1, uint32_t src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1), "r"(src)
+               : "memory");
+}
+__device__ __forceinline__ void arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t db, uint32_t idesc,
+                                       uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+      "r"(a_tmem), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void st_tmem32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]),
+      "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]),
+      "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]),
+      "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+}  // namespace tma
+
+__global__ void __launch_bounds__(tma::THREADS, 2)
+    refresh_tma_kernel(int64_t I, const float *__restrict__ Bt,
+                       const __grid_constant__ CUtensorMap tmA,
+                       const __grid_constant__ CUtensorMap tmC, uint32_t *guard) {
+  using tc::smem_u32;
+  using tc::hi_bits;
+  using tc::sw128_desc;
+  using tc::mma_tf32_tc;
+  using tcs::wait_parity;
+  using tcs::ld_tmem32;
+  using namespace tma;
+  extern __shared__ __align__(1024) uint8_t tma_smem[];
+  const uint32_t sraw = smem_u32(tma_smem), sbase = (sraw + 1023u) & ~1023u;
+  uint8_t *gb = tma_smem + (sbase - sraw);
+  const uint32_t ring = sbase, bP = ring + RING * TBYTES, stage = bP + 64 * 128;
+  const uint32_t bars = stage + 8 * 4096;  // full[RING], empty[RING], lo_ready[2], acc_full[2]
+  const uint32_t full = bars, empty = bars + 8 * RING, lo_ready = bars + 16 * RING,
+                 acc_full = lo_ready + 16;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gb + (bars - sbase) + 8 * (2 * RING + 4));
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  for (int e = tid; e < 32 * 8; e += THREADS) {  // P = [Bt_hi ; Bt_lo], SW128 K-major
+    const int r = e >> 3, c = e & 7;
+    const float4 v = __ldg(reinterpret_cast<const float4 *>(Bt + r * 32) + c);
+    const uint32_t off = r * 128 + ((c ^ (r & 7)) << 4);
+    uint4 h, l;
+    h.x = hi_bits(v.x), h.y = hi_bits(v.y), h.z = hi_bits(v.z), h.w = hi_bits(v.w);
+    l.x = __float_as_uint(v.x - __uint_as_float(h.x));
+    l.y = __float_as_uint(v.y - __uint_as_float(h.y));
+    l.z = __float_as_uint(v.z - __uint_as_float(h.z));
+    l.w = __float_as_uint(v.w - __uint_as_float(h.w));
+    *reinterpret_cast<uint4 *>(gb + (bP - sbase) + off) = h;
+    *reinterpret_cast<uint4 *>(gb + (bP - sbase) + 32 * 128 + off) = l;
+  }
+  if (w == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) {
+    for (int k = 0; k < 2 * RING; ++k)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bars + 8 * k));
+    for (int k = 0; k < 2; ++k) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;\n" ::"r"(lo_ready + 8 * k));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(acc_full + 8 * k));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  const int64_t ntiles = (I + TM - 1) / TM;
+  const int nmine = ntiles > blockIdx.x ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x) + 1 : 0;
+  auto tile_of = [&](int it) { return (int64_t)blockIdx.x + (int64_t)it * gridDim.x; };
+  if (w == 0) {
+    if (lane == 0)
+      for (int it = 0; it < nmine; ++it) {
+        const int s = it % RING;
+        if (it >= RING) wait_parity(empty + 8 * s, ((it / RING) - 1) & 1);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(full + 8 * s),
+                     "r"(TBYTES)
+                     : "memory");
+        load2d(ring + s * TBYTES, &tmA, 0, (int)(tile_of(it) * TM), full + 8 * s);
+      }
+  } else if (w == 1) {
+    if (lane == 0) {
+      const uint32_t i64 = (1u << 4) | (2u << 7) | (2u << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+      const uint32_t i32 = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+      for (int it = 0; it < nmine; ++it) {
+        const int s = it % RING, b = it & 1;
+        wait_parity(full + 8 * s, (it / RING) & 1);
+        wait_parity(lo_ready + 8 * b, (it >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t d = tmem + 64 * b, lo = tmem + LO + 32 * b, a = ring + s * TBYTES;
+        for (int k = 0; k < 4; ++k) mma_tf32_tc(d, sw128_desc(a + 32 * k), sw128_desc(bP + 32 * k), i64, k > 0);
+        for (int k = 0; k < 4; ++k) mma_ts(d, lo + 8 * k, sw128_desc(bP + 32 * k), i32, 1);
+        commit(empty + 8 * s);
+        commit(acc_full + 8 * b);
+      }
+    }
+  } else {
+    const int q = w & 3;  // TMEM lane quadrant = rows 32q .. 32q + 31 of every tile
+    const uint32_t lanes = (uint32_t)(32 * q) << 16;
+    uint32_t gmax = 0;
+    auto epilogue = [&](int e) {
+      const int b = e & 1;
+      wait_parity(acc_full + 8 * b, (e >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      uint32_t d[32], d2[32];
+      ld_tmem32(tmem + lanes + 64 * b, d);
+      ld_tmem32(tmem + lanes + 64 * b + 32, d2);
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      const uint32_t slab = stage + q * 8192 + b * 4096;
+      if (lane == 0 && e >= 2) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+      __syncwarp();
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};\n" ::"r"(slab + lane * 128 + ((c ^ (lane & 7)) << 4)),
+                     "f"(__uint_as_float(d[4 * c]) + __uint_as_float(d2[4 * c])),
+                     "f"(__uint_as_float(d[4 * c + 1]) + __uint_as_float(d2[4 * c + 1])),
+                     "f"(__uint_as_float(d[4 * c + 2]) + __uint_as_float(d2[4 * c + 2])),
+                     "f"(__uint_as_float(d[4 * c + 3]) + __uint_as_float(d2[4 * c + 3])));
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      const int64_t row0 = tile_of(e) * TM + 32 * q;
+      if (lane == 0) {
+        if (row0 < I) store2d(&tmC, 0, (int)row0, slab);
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      }
+    };
+    for (int it = 0; it < nmine; ++it) {
+      const int s = it % RING, b = it & 1;
+      wait_parity(full + 8 * s, (it / RING) & 1);
+      const uint32_t src = ring + s * TBYTES + (32 * q + lane) * 128;
+      uint32_t lo[32];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {  // row 32q + lane: chunk c sits at c ^ (lane & 7)
+        float4 v;
+        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];\n"
+                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                     : "r"(src + ((c ^ (lane & 7)) << 4)));
+        gmax = max(gmax, max(max(abs_bits(v.x), abs_bits(v.y)), max(abs_bits(v.z), abs_bits(v.w))));
+        lo[4 * c] = __float_as_uint(v.x - __uint_as_float(hi_bits(v.x)));
+        lo[4 * c + 1] = __float_as_uint(v.y - __uint_as_float(hi_bits(v.y)));
+        lo[4 * c + 2] = __float_as_uint(v.z - __uint_as_float(hi_bits(v.z)));
+        lo[4 * c + 3] = __float_as_uint(v.w - __uint_as_float(hi_bits(v.w)));
+      }
+      st_tmem32(tmem + lanes + LO + 32 * b, lo);
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) arrive(lo_ready + 8 * b);
+      if (it > 0) epilogue(it - 1);
+    }
+    if (nmine > 0) epilogue(nmine - 1);
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+    if (guard) guard_max(guard, gmax);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (w == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TMEM_COLS));
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault,
+                                         &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+// rows x 32 fp32, 128-B rows, box of box_rows rows, 128-B swizzle; the last few encodings are
+// cached (an epoch refreshes the same few matrices over and over)
+bool rows32_map(CUtensorMap *m, const float *base, int64_t rows, int box_rows) {
+  struct Entry {
+    const float *base;
+    int64_t rows;
+    int box;
+    CUtensorMap map;
+  };
+  static thread_local Entry cache[8] = {};
+  static thread_local int next = 0;
+  for (const Entry &e : cache)
+    if (e.base == base && e.rows == rows && e.box == box_rows) {
+      *m = e.map;
+      return true;
+    }
+  const PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+  if (!enc || rows > INT32_MAX) return false;
+  cuuint64_t dims[2] = {32, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {128};
+  cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  if (enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  cache[next] = Entry{base, rows, box_rows, *m};
+  next = (next + 1) & 7;
+  return true;
+}
+
 // tensor-core refresh unless FT_REFRESH=simt (the fp32 CUDA-core kernel above, which keeps the
 // reference's sequential-j accumulation order); both need J, R <= 32
 bool use_tc_refresh(int R) {
@@ -496,6 +762,22 @@ bool use_tc_refresh(int R) {
 
 int launch_refresh(int64_t I, int J, int R, const float *A, const float *Bt, const Dsts &d,
                    uint32_t *guard, cudaStream_t s) {
+  if (use_tc_refresh(R) && J == 32 && R == 32 && d.n == 1 &&
+      (reinterpret_cast<uintptr_t>(A) & 15) == 0 && (reinterpret_cast<uintptr_t>(d.p[0]) & 15) == 0) {
+    CUtensorMap ma, mc;
+    if (rows32_map(&ma, A, I, tma::TM) && rows32_map(&mc, d.p[0], I, 32)) {
+      static bool set_t = false;
+      if (!set_t) {
+        cudaFuncSetAttribute(refresh_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)tma::SMEM);
+        set_t = true;
+      }
+      int64_t g = (I + tma::TM - 1) / tma::TM;
+      if (g > 2 * (int64_t)sm_count()) g = 2 * (int64_t)sm_count();
+      refresh_tma_kernel<<<(unsigned)g, tma::THREADS, tma::SMEM, s>>>(I, Bt, ma, mc, guard);
+      return check_launch("ft_refresh(tcgen05 TMA)");
+    }
+  }
   if (use_tc_refresh(R) && J == 32 && R == 32 && (reinterpret_cast<uintptr_t>(A) & 15) == 0) {
     static bool set_s = false;
     if (!set_s) {

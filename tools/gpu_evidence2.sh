@@ -13,7 +13,7 @@ ncu --set full --clock-control none --import-source on -k regex:"factor_rows|cor
   --launch-skip 12 -c 6 -o gpurun_out/ev_sweeps -f \
   python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e --no-ncu > gpurun_out/ev_sweeps.log 2>&1
 echo sweeps $?
-ncu --set full --clock-control none --import-source on -k regex:"refresh_tc" --launch-skip 6 -c 3 \
+ncu --set full --clock-control none --import-source on -k regex:"refresh_t" --launch-skip 6 -c 3 \
   -o gpurun_out/ev_refresh -f python bench.py --steps 1 --warmup 1 --no-cpu --no-e2e --no-ncu > gpurun_out/ev_refresh.log 2>&1
 echo refresh $?
 for c in netflix16 yahoo32 order4 order6 order10; do

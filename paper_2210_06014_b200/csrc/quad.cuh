@@ -573,49 +573,126 @@ __device__ __forceinline__ Leaf load_leaf(const SweepParams &p, const Rec &r, in
 }  // namespace quadp
 
 // ---- K3b "quadw": the quad layout warp-specialised for FEW LONG ROWS ----------------------
-// A warp GROUP owns four rows (one per 8-lane quarter of its consumer warp).  Two PRODUCER
-// warps take alternate batches: each walks the rows' batch records, gathers its batch into its
-// own X/Y tiles, runs the transposed 3xTF32 combine and publishes V, the batch's (x, lr,
-// -lr reg) and, when a quarter starts a row, that row's A values (loaded a batch ahead) into an
-// NS-stage shared-memory ring (mbarrier full / empty).  The CONSUMER warp only runs the four
-// serial chains (quad arithmetic and order), so the chain -- the only serial work -- never
-// waits on a gather or an MMA.  (One producer was the bottleneck: ncu showed its 96 HMMA per
-// batch at ~9 cycles each plus the gather wait, 2.3 K cycles per batch vs ~1 K for the chain.)
+// A warp GROUP owns four rows (one per 8-lane quarter of its consumer warp).  NP PRODUCER warps
+// take batches round robin: each walks the rows' batch records, gathers its batch into its own
+// X/Y tiles, runs the transposed 3xTF32 combine and publishes V, the batch's (x, lr, -lr reg)
+// and, when a quarter starts a row, that row's A values (loaded a batch ahead) into an NS-stage
+// shared-memory ring (mbarrier full / empty).  The CONSUMER warp only runs the four serial
+// chains, so the chain -- the only serial work -- never waits on a gather or an MMA.
 // Netflix mode 2: 2,182 rows of ~45 K updates -> 546 groups, ~3.7 per SM.
+//
+// GRAM (the segment form of the row recurrence): a quarter batch is 8
+// consecutive updates of ONE row (batches never span rows), and with alpha = 1 - lr reg
+//     a_k = alpha^k a_0 + sum_{i<k} lr alpha^(k-1-i) e_i v_i,
+//     e_k = x_k - alpha^k (a_0 . v_k) - sum_{i<k} T_ik e_i,   T_ik = lr alpha^(k-1-i) (v_i . v_k),
+//     a_8 = alpha^8 a_0 + sum_i lr alpha^(7-i) e_i v_i
+// (exact algebra; padding steps have lr = 0).  The producers add the batch's four 8 x 8 Gram
+// blocks V_q V_q^T (mma.sync 3xTF32, the diagonal blocks of two m-tiles) and store T; the
+// consumer reduces the eight dots a_0 . v_k in ONE 3-level butterfly (instead of one per step),
+// solves the 8 x 8 unit-triangular system in registers (28 FMAs, no communication) and updates
+// a once per batch (compensated).  The serial dependency per batch drops from 8 x (dot +
+// 3 shuffles + update) to one butterfly + 7 FMAs: what bounds the sweep when few rows share an
+// SM (the row-sharded multi-GPU epoch) -- tools/time_shards.py.
 namespace quadw {
-constexpr int NS = 4;   // ring stages (producer k writes stages k, k+2)
-constexpr int NP = 2;   // producers per group
-// stage: V [32][QVS] | meta float4 [4][MQ] | info int4 [4] | A rows [4][32] | lr*G^T [4][8][8]
-constexpr int VREG = 32 * quad::QVS + 32;  // V tile
-constexpr int STAGE_FLOATS = VREG + 4 * quad::MQ * 4 + 4 * 4 + 4 * 32 + 4 * 64;
-// ring + X, Y per producer + the consumer's row exchange [4][32]
-constexpr int GROUP_FLOATS = NS * STAGE_FLOATS + NP * 2 * quad::TILE + 4 * 32;
-constexpr int BAR_BYTES = 2 * NS * 8 + 16;
-constexpr int THREADS = (NP + 1) * 32;
-constexpr size_t bytes() {
-  return (size_t)quad::BFRAG_U4 * 16 + BAR_BYTES + (size_t)GROUP_FLOATS * 4;
-}
+template <int NP>
+struct Cfg {
+  static constexpr int NS = NP <= 2 ? 4 : 2 * NP;  // ring stages (producer k writes k, k + NP, ..)
+  static constexpr int VREG = 32 * quad::QVS + 32;  // V tile
+  // stage: V [32][QVS] | meta float4 [4][MQ] | info int4 [4] | A rows [4][32] |
+  //        GRAM: per quarter T [28] + x [8] + pad [4]
+  static constexpr int META = VREG, INFO = META + 4 * quad::MQ * 4, AROW = INFO + 16,
+                       TCOEF = AROW + 4 * 32, TQ = 40;
+  static constexpr int STAGE_FLOATS = TCOEF + 4 * TQ;
+  // ring + X, Y per producer
+  static constexpr int GROUP_FLOATS = NS * STAGE_FLOATS + NP * 2 * quad::TILE;
+  static constexpr int BAR_BYTES = 2 * NS * 8 + 16;
+  static constexpr int THREADS = (NP + 1) * 32;
+  static constexpr size_t bytes() {
+    return (size_t)quad::BFRAG_U4 * 16 + BAR_BYTES + (size_t)GROUP_FLOATS * 4;
+  }
+};
+// position of T_ik (i < k) in a quarter's packed 28-float block: rows i = 0..6, columns k > i
+__host__ __device__ constexpr int tpos(int i, int k) { return 7 * i - i * (i - 1) / 2 + (k - i - 1); }
 }  // namespace quadw
 
+// The batch's four diagonal Gram blocks G_q = V_q V_q^T (8 x 8, q = quarter) from the stage's V
+// tile by mma.sync 3xTF32, scaled into the consumer's T coefficients (packed, quadw::tpos):
+// m-tile h = quarters 2h, 2h + 1 (16 slots) times n-tile = one quarter's 8 slots, so the
+// diagonal blocks are rows 0-7 of (h, 2h) and rows 8-15 of (h, 2h + 1); k order paired as in the
+// combine (k-slot t <-> j = 2t, t + 4 <-> 2t + 1): every fragment register pair is one LDS.64.
+// Lane (g, t) ends with G_q[g][2t], G_q[g][2t + 1]; tc0 / tc1 = lr alpha^(k-1-i) for those two
+// entries (lane constants), nb[q] the quarters' live batch lengths (T = 0 for padding rows i).
 template <bool SMALL>
-__global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(const SweepParams p) {
+__device__ __forceinline__ void quadw_gram(const float *V, float *T, const int (&nb)[4], float tc0,
+                                           float tc1, int lane) {
+  using namespace quad;
+  const int gq = lane >> 2, tq = lane & 3;
+  float ga[2][2][4];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int nn = 0; nn < 2; ++nn)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) ga[h][nn][u] = 0.f;
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    if (SMALL && ks >= 2) break;  // J <= 16: columns 16.. are zero
+    float2 bq[4];
+#pragma unroll
+    for (int n = 0; n < 4; ++n)
+      bq[n] = *reinterpret_cast<const float2 *>(V + (8 * n + gq) * QVS + 8 * ks + 2 * tq);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float2 r0v = *reinterpret_cast<const float2 *>(V + (16 * h + gq) * QVS + 8 * ks + 2 * tq);
+      const float2 r1v = *reinterpret_cast<const float2 *>(V + (16 * h + gq + 8) * QVS + 8 * ks + 2 * tq);
+      const uint32_t ah0 = __float_as_uint(r0v.x), ah1 = __float_as_uint(r1v.x),
+                     ah2 = __float_as_uint(r0v.y), ah3 = __float_as_uint(r1v.y);  // MMA truncates
+      const uint32_t al0 = __float_as_uint(r0v.x - __uint_as_float(to_tf32(r0v.x)));
+      const uint32_t al1 = __float_as_uint(r1v.x - __uint_as_float(to_tf32(r1v.x)));
+      const uint32_t al2 = __float_as_uint(r0v.y - __uint_as_float(to_tf32(r0v.y)));
+      const uint32_t al3 = __float_as_uint(r1v.y - __uint_as_float(to_tf32(r1v.y)));
+#pragma unroll
+      for (int nn = 0; nn < 2; ++nn) {
+        const float2 bv = bq[2 * h + nn];
+        const uint32_t bh0 = __float_as_uint(bv.x), bh1 = __float_as_uint(bv.y);
+        const uint32_t bl0 = __float_as_uint(bv.x - __uint_as_float(to_tf32(bv.x)));
+        const uint32_t bl1 = __float_as_uint(bv.y - __uint_as_float(to_tf32(bv.y)));
+        mma_tf32(ga[h][nn], al0, al1, al2, al3, bh0, bh1);
+        mma_tf32(ga[h][nn], ah0, ah1, ah2, ah3, bl0, bl1);
+        mma_tf32(ga[h][nn], ah0, ah1, ah2, ah3, bh0, bh1);
+      }
+    }
+  }
+#pragma unroll
+  for (int qq = 0; qq < 4; ++qq) {
+    const float g0 = (qq & 1) ? ga[qq >> 1][1][2] : ga[qq >> 1][0][0];
+    const float g1 = (qq & 1) ? ga[qq >> 1][1][3] : ga[qq >> 1][0][1];
+    const bool live = gq < nb[qq];
+    if (gq < 2 * tq) T[40 * qq + quadw::tpos(gq, 2 * tq)] = live ? tc0 * g0 : 0.f;
+    if (gq < 2 * tq + 1) T[40 * qq + quadw::tpos(gq, 2 * tq + 1)] = live ? tc1 * g1 : 0.f;
+  }
+}
+
+template <bool SMALL, int NP, bool GRAM>
+__global__ void __launch_bounds__(quadw::Cfg<NP>::THREADS, NP <= 2 ? 4 : 1)
+    factor_rows_quadw_kernel(const SweepParams p) {
   using namespace quad;
   using quadp::Leaf;
   using quadp::Rec;
+  using C = quadw::Cfg<NP>;
   extern __shared__ float4 smem4[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;  // w 0: consumer, 1..NP: producers
   const int q = lane >> 3, l = lane & 7;
   uint4 *afr = reinterpret_cast<uint4 *>(smem4);
   uint64_t *bars = reinterpret_cast<uint64_t *>(afr + BFRAG_U4);
-  uint64_t *full = bars, *empty = bars + quadw::NS;
-  float *ring = reinterpret_cast<float *>(reinterpret_cast<char *>(afr + BFRAG_U4) +
-                                          quadw::BAR_BYTES);
+  uint64_t *full = bars, *empty = bars + C::NS;
+  float *ring = reinterpret_cast<float *>(reinterpret_cast<char *>(afr + BFRAG_U4) + C::BAR_BYTES);
   if (w > 0) {
-    float *tiles = ring + quadw::NS * quadw::STAGE_FLOATS + (w - 1) * 2 * TILE;
+    float *tiles = ring + C::NS * C::STAGE_FLOATS + (w - 1) * 2 * TILE;
     for (int k = lane; k < 2 * TILE; k += 32) tiles[k] = 0.f;
   }
   if (threadIdx.x == 0)
-    for (int st = 0; st < quadw::NS; ++st) {
+    for (int st = 0; st < C::NS; ++st) {
       mbar_init(full + st, 32);
       mbar_init(empty + st, 32);
     }
@@ -624,29 +701,43 @@ __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(co
   // m-tiles (j) / k-tiles (r) in use: compile-time (SMALL: J <= 16 and R <= 16), so the
   // unrolled combine keeps no runtime guards; other shapes compute their zero padding
   constexpr int mts = SMALL ? 1 : 2, nkt = SMALL ? 2 : 4;
-  const int64_t nstream = (int64_t)gridDim.x * 4;
   const int J = p.J;
   const bool j32 = J == 32;
-  // stage layout: V [32][QVS] | meta float4 [4][MQ] | info int4 [4] | A rows [4][32]
-  auto stage_v = [&](int st) { return ring + st * quadw::STAGE_FLOATS; };
-  auto stage_meta = [&](int st) {
-    return reinterpret_cast<float4 *>(ring + st * quadw::STAGE_FLOATS + quadw::VREG);
-  };
-  auto stage_info = [&](int st) {
-    return reinterpret_cast<int4 *>(ring + st * quadw::STAGE_FLOATS + quadw::VREG + 4 * MQ * 4);
-  };
-  auto stage_a = [&](int st) {
-    return ring + st * quadw::STAGE_FLOATS + quadw::VREG + 4 * MQ * 4 + 16;
-  };
+  auto stage_v = [&](int st) { return ring + st * C::STAGE_FLOATS; };
+  auto stage_meta = [&](int st) { return reinterpret_cast<float4 *>(ring + st * C::STAGE_FLOATS + C::META); };
+  auto stage_info = [&](int st) { return reinterpret_cast<int4 *>(ring + st * C::STAGE_FLOATS + C::INFO); };
+  auto stage_a = [&](int st) { return ring + st * C::STAGE_FLOATS + C::AROW; };
+  auto stage_t = [&](int st) { return ring + st * C::STAGE_FLOATS + C::TCOEF; };
+  const float cdec = -p.lr * p.reg;  // alpha - 1
+  // GRAM: this lane's two T entries per quarter, i = g, k = 2t and 2t + 1 (the C-fragment
+  // positions of the diagonal Gram blocks), and their lane-constant lr alpha^(k-1-i)
+  float tc0 = 0.f, tc1 = 0.f;
+  if (GRAM) {
+    const int gq = lane >> 2, tq = lane & 3;
+    float d = 0.f;  // alpha^n - 1, accumulated without cancellation
+    for (int n = 0; n < 8; ++n) {
+      if (n == 2 * tq - gq - 1) tc0 = p.lr * (1.f + d);
+      if (n == 2 * tq - gq) tc1 = p.lr * (1.f + d);
+      d = __fmaf_rn(cdec, 1.f + d, d);
+    }
+  }
+  // rows per group (runtime): 4 quarters normally, 2 or 1 when the rows leave SMs idle (the
+  // quarters past rpg stream nothing and run padding)
+  const int rpg = p.quadw_rpg > 0 ? p.quadw_rpg : 4;
 
   if (w > 0) {
     // ===================================== producers =====================================
     const int k = w - 1;  // this producer runs batches t = k, k + NP, ...
-    float *X = ring + quadw::NS * quadw::STAGE_FLOATS + k * 2 * TILE, *Y = X + TILE;
+    float *X = ring + C::NS * C::STAGE_FLOATS + k * 2 * TILE, *Y = X + TILE;
+    const int64_t nstream = (int64_t)gridDim.x * rpg;
     quadp::Cursor cur;
     cur.row = (int64_t)q * gridDim.x + blockIdx.x - nstream;
     cur.i = -1, cur.L0 = cur.Le = 0;
-    quadp::load_row_info(p, cur.row + nstream, cur.ni, cur.nLb, cur.nLe);
+    if (q < rpg) {
+      quadp::load_row_info(p, cur.row + nstream, cur.ni, cur.nLb, cur.nLe);
+    } else {  // no rows in this quarter
+      cur.ni = -1, cur.nLb = cur.nLe = 0;
+    }
     const int gc = lane & 7, gs = lane >> 3;
     const bool gok = gc < (p.R >> 2);
     const float *cpre = p.Cpre[0] + 4 * gc, *cleaf = p.Cleaf + 4 * gc;
@@ -679,12 +770,12 @@ __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(co
       }
       return v;
     };
-    // the record of my next batch: skip the other producer's batches (row-start flags carry
+    // the record of my next batch: skip the other producers' batches (row-start flags carry
     // over a skipped batch only if it started a row and mine continues it -- then mine is not
     // the row's first batch, which is what the consumer needs)
     auto next_mine = [&](bool first) {
       if (!first)
-        for (int s = 0; s < quadw::NP - 1; ++s) (void)quadp::next_batch(p, cur, nstream);
+        for (int s = 0; s < NP - 1; ++s) (void)quadp::next_batch(p, cur, nstream);
       return quadp::next_batch(p, cur, nstream);
     };
     // the Bt^T fragments live in registers for the whole sweep (64 per lane): the shared-memory
@@ -702,7 +793,7 @@ __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(co
     Leaf d0 = quadp::load_leaf(p, r0, l);
     float4 av0 = load_arow(r0);
     float acc[2][4][4];
-    for (int t = k;; t += quadw::NP) {
+    for (int t = k;; t += NP) {
       const bool stop = !__any_sync(FULL, r0.nb > 0);
       if (!stop) gather(d0);
       const Rec r1 = next_mine(false);  // my next batch: indices and A values fly meanwhile
@@ -716,16 +807,24 @@ __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(co
         for (int kt = 0; kt < KT; ++kt)
           if (kt < nkt) quad_mma_kt_r<NT>(X, Y, AH[kt], AL[kt], kt, 0, lane, acc, mts);
       }
-      const int st = t % quadw::NS;
-      if (t >= quadw::NS) mbar_wait(empty + st, ((t / quadw::NS) - 1) & 1);
+      const int st = t % C::NS;
+      if (t >= C::NS) mbar_wait(empty + st, ((t / C::NS) - 1) & 1);
       int4 *info = stage_info(st);
       if (!stop) {
         quad_store_v(stage_v(st), acc, lane);
         const float lrk = l < r0.nb ? p.lr : 0.f;
         const float ck = -lrk * p.reg;
-        stage_meta(st)[q * MQ + l] = make_float4(l < r0.nb ? d0.x : 0.f, lrk, ck, ck);
+        if (!GRAM) stage_meta(st)[q * MQ + l] = make_float4(l < r0.nb ? d0.x : 0.f, lrk, ck, ck);
         if (r0.newrow) *reinterpret_cast<float4 *>(stage_a(st) + 32 * q + 4 * l) = av0;
         if (l == 0) info[q] = make_int4(r0.nb, r0.newrow ? 1 : 0, r0.i, 0);
+        if (GRAM) {
+          stage_t(st)[C::TQ * q + 28 + l] = l < r0.nb ? d0.x : 0.f;  // the batch's x, packed
+          __syncwarp();
+          int nbq[4];
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) nbq[qq] = __shfl_sync(FULL, r0.nb, 8 * qq);
+          quadw_gram<SMALL>(stage_v(st), stage_t(st), nbq, tc0, tc1, lane);
+        }
       } else if (l == 0) {
         info[q] = make_int4(0, 0, -1, 1);  // stop
       }
@@ -750,9 +849,16 @@ __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(co
           if (4 * l + t < J) ar[4 * l + t] = o[t];
       }
     };
+    // GRAM: Dk[k] = alpha^k - 1 (k = 0..8) and the full batch's update weights lr alpha^(7-i)
+    float Dk[9], wfull[8];
+    Dk[0] = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) Dk[k + 1] = __fmaf_rn(cdec, 1.f + Dk[k], Dk[k]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) wfull[i] = p.lr * (1.f + Dk[7 - i]);
     for (int t = 0;; ++t) {
-      const int st = t % quadw::NS;
-      mbar_wait(full + st, (t / quadw::NS) & 1);
+      const int st = t % C::NS;
+      mbar_wait(full + st, (t / C::NS) & 1);
       const int4 info = stage_info(st)[q];
       if (info.w) break;  // stop (every quarter carries the flag)
       if (info.y) {       // this quarter starts row info.z
@@ -763,53 +869,143 @@ __global__ void __launch_bounds__(quadw::THREADS, 4) factor_rows_quadw_kernel(co
         ai = info.z;
       }
       const float *Vq = stage_v(st) + 8 * q * QVS + 4 * l;
-      const float4 *mq = stage_meta(st) + q * MQ;
-      // the stage's 8 V rows and step operands are loaded up front (16 independent LDS.128,
-      // one latency) so the serial steps wait only on their own shuffles; short batches run
-      // all 8 steps (padding steps have lr = 0 and change nothing)
-      float4 vv[QB], mm[QB];
+      // the stage's 8 V rows (and operands) are loaded up front: independent LDS.128, one
+      // latency
+      float4 vv[QB];
 #pragma unroll
-      for (int kk = 0; kk < QB; ++kk) {
-        vv[kk] = *reinterpret_cast<const float4 *>(Vq + kk * QVS);
-        mm[kk] = mq[kk];
+      for (int kk = 0; kk < QB; ++kk) vv[kk] = *reinterpret_cast<const float4 *>(Vq + kk * QVS);
+      if (!GRAM) {  // the per-step chain: short batches run all 8 steps (padding: lr = 0)
+        const float4 *mq = stage_meta(st) + q * MQ;
+        float4 mm[QB];
+#pragma unroll
+        for (int kk = 0; kk < QB; ++kk) mm[kk] = mq[kk];
+        __syncwarp();
+        mbar_arrive(empty + st);  // the stage is free once read
+#pragma unroll
+        for (int kk = 0; kk < QB; ++kk) quad_chain_step_vc(a, lo, vv[kk], mm[kk]);
+        continue;
+      }
+      float T[28], xk[QB];
+      {
+        const float4 *tq4 = reinterpret_cast<const float4 *>(stage_t(st) + C::TQ * q);
+#pragma unroll
+        for (int u = 0; u < 7; ++u) {
+          const float4 t4 = tq4[u];
+          T[4 * u] = t4.x, T[4 * u + 1] = t4.y, T[4 * u + 2] = t4.z, T[4 * u + 3] = t4.w;
+        }
+        const float4 x0 = tq4[7], x1 = tq4[8];
+        xk[0] = x0.x, xk[1] = x0.y, xk[2] = x0.z, xk[3] = x0.w;
+        xk[4] = x1.x, xk[5] = x1.y, xk[6] = x1.z, xk[7] = x1.w;
       }
       __syncwarp();
       mbar_arrive(empty + st);  // the stage is free once read
+      // the eight dots a_0 . v_k: lane partials, one butterfly over the quarter's 8 lanes
+      float pk[QB];
 #pragma unroll
-      for (int kk = 0; kk < QB; ++kk) quad_chain_step_vc(a, lo, vv[kk], mm[kk]);
-      continue;
-    
-      __syncwarp();
-      mbar_arrive(empty + st);
+      for (int kk = 0; kk < QB; ++kk) {
+        float2 pr = fmul2(make_float2(a[0], a[1]), make_float2(vv[kk].x, vv[kk].y));
+        pr = ffma2(make_float2(a[2], a[3]), make_float2(vv[kk].z, vv[kk].w), pr);
+        pk[kk] = pr.x + pr.y;
+      }
+#pragma unroll
+      for (int m = 4; m >= 1; m >>= 1)
+#pragma unroll
+        for (int kk = 0; kk < QB; ++kk) pk[kk] += __shfl_xor_sync(FULL, pk[kk], m);
+      // r_k = x_k - alpha^k p_k, then the unit lower-triangular solve (right-looking)
+      float r[QB];
+#pragma unroll
+      for (int kk = 0; kk < QB; ++kk) r[kk] = __fmaf_rn(-Dk[kk], pk[kk], xk[kk] - pk[kk]);
+#pragma unroll
+      for (int i = 0; i < QB - 1; ++i)
+#pragma unroll
+        for (int kk = i + 1; kk < QB; ++kk) r[kk] = __fmaf_rn(-T[quadw::tpos(i, kk)], r[i], r[kk]);
+      // a_nb = alpha^nb a_0 + sum_i lr alpha^(nb-1-i) e_i v_i: full batches use the constant
+      // weights; otherwise (a row's last batch, or a quarter without rows: nb = 0) the weights
+      // are rescaled by alpha^-(8-nb) and the padding zeroed -- selects, no divergent loops
+      const int nb = info.x;
+      float wsc[QB], dn = Dk[QB];
+#pragma unroll
+      for (int i = 0; i < QB; ++i) wsc[i] = wfull[i];
+      if (!__all_sync(FULL, nb == QB)) {
+        float dd = 0.f;
+#pragma unroll
+        for (int m = 0; m < QB; ++m)
+          if (nb == m) dn = Dk[m], dd = Dk[QB - m];
+        const float sc = __fdividef(1.f, 1.f + dd);
+#pragma unroll
+        for (int i = 0; i < QB; ++i) wsc[i] = i < nb ? wfull[i] * sc : 0.f;
+      }
+      // d = sum_i w_i e_i v_i in two independent chains
+      float2 da01 = make_float2(0.f, 0.f), da23 = da01, db01 = da01, db23 = da01;
+#pragma unroll
+      for (int i = 0; i < QB; i += 2) {
+        const float w0 = wsc[i] * r[i], w1 = wsc[i + 1] * r[i + 1];
+        da01 = ffma2(make_float2(w0, w0), make_float2(vv[i].x, vv[i].y), da01);
+        da23 = ffma2(make_float2(w0, w0), make_float2(vv[i].z, vv[i].w), da23);
+        db01 = ffma2(make_float2(w1, w1), make_float2(vv[i + 1].x, vv[i + 1].y), db01);
+        db23 = ffma2(make_float2(w1, w1), make_float2(vv[i + 1].z, vv[i + 1].w), db23);
+      }
+      const float2 d01 = fadd2(da01, db01), d23 = fadd2(da23, db23);
+      // compensated a <- a + (dn a + d + lo)
+      const float2 c2 = make_float2(dn, dn);
+      const float2 a01 = make_float2(a[0], a[1]), a23 = make_float2(a[2], a[3]);
+      const float2 e01 = fadd2(d01, ffma2(c2, a01, make_float2(lo[0], lo[1])));
+      const float2 e23 = fadd2(d23, ffma2(c2, a23, make_float2(lo[2], lo[3])));
+      const float2 t01 = fadd2(a01, e01), t23 = fadd2(a23, e23);
+      const float2 s01 = fsub2(e01, fsub2(t01, a01)), s23 = fsub2(e23, fsub2(t23, a23));
+      a[0] = t01.x, a[1] = t01.y, a[2] = t23.x, a[3] = t23.y;
+      lo[0] = s01.x, lo[1] = s01.y, lo[2] = s23.x, lo[3] = s23.y;
     }
     if (ai >= 0) store_a();
   }
 }
 
-template <bool SMALL>
-int launch_quadw_t(const SweepParams &q, cudaStream_t s) {
-  const size_t sm = quadw::bytes();
+template <bool SMALL, int NP, bool GRAM>
+int launch_quadw_t(const SweepParams &q0, int rpg, cudaStream_t s) {
+  SweepParams q = q0;
+  q.quadw_rpg = rpg;
+  using C = quadw::Cfg<NP>;
+  auto kern = factor_rows_quadw_kernel<SMALL, NP, GRAM>;
+  const size_t sm = C::bytes();
   static bool set = false;
   if (!set) {
-    cudaFuncSetAttribute(factor_rows_quadw_kernel<SMALL>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     set = true;
   }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_rows_quadw_kernel<SMALL>,
-                                                    quadw::THREADS, sm) != cudaSuccess ||
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, sm) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
-  int64_t g = (q.nrows + 3) / 4;
+  int64_t g = (q.nrows + rpg - 1) / rpg;
   const int64_t cap = (int64_t)sm_count() * per_sm;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
-  factor_rows_quadw_kernel<SMALL><<<(int)g, quadw::THREADS, sm, s>>>(q);
+  kern<<<(int)g, C::THREADS, sm, s>>>(q);
   return check_launch("ft_factor_sweep_rows(quadw)");
 }
 
+// Few rows per SM (the row-sharded multi-GPU sweeps: groups <= SMs): the Gram form, six
+// producers per group, 2 or 1 rows per group when 4 would leave SMs idle -- the serial chain is
+// the bound there.  Many rows (one GPU: 3.7 groups per SM): the per-step chain and two producers
+// -- there the producers' gathers / combine leave no room for the Gram blocks (measured: 5.9 vs
+// 7.5-7.9 ms on Netflix mode 2, profiles/r02_quadw_gram.md).  FT_QUADW_GRAM=0 / 1 forces one
+// form (A/B).
+template <bool SMALL>
+int launch_quadw_s(const SweepParams &q, cudaStream_t s) {
+  static const int forced = [] {
+    const char *e = getenv("FT_QUADW_GRAM");
+    return e ? atoi(e) : -1;
+  }();
+  const int64_t sms = sm_count();
+  int rpg = 4;
+  while (rpg > 1 && (q.nrows + rpg / 2 - 1) / (rpg / 2) <= sms) rpg /= 2;
+  const bool few = (q.nrows + 3) / 4 <= sms;
+  if (forced == 0 || (forced < 0 && !few)) return launch_quadw_t<SMALL, 2, 0>(q, 4, s);
+  return launch_quadw_t<SMALL, 6, 1>(q, few ? rpg : 4, s);
+}
+
 int launch_quadw(const SweepParams &q, cudaStream_t s) {
-  return q.J <= 16 && q.R <= 16 ? launch_quadw_t<true>(q, s) : launch_quadw_t<false>(q, s);
+  return q.J <= 16 && q.R <= 16 ? launch_quadw_s<true>(q, s) : launch_quadw_s<false>(q, s);
 }
 
 // the quad kernels run any J, R <= 32 (R % 4 == 0; padding columns are zero); J = R = 16 has

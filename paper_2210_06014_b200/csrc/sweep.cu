@@ -65,6 +65,7 @@ struct SweepParams {
   float lr, reg;
   float *partials;   // core: [grid][R*J]
   int64_t gather_bytes;  // bytes of the gathered C matrices (modes other than u)
+  int quadw_rpg;         // quadw: rows per warp group (0: 4)
 };
 
 // Fiber index of each of the batch's leaves (lane k -> leaf L0+k), given fcur = fiber holding

@@ -98,15 +98,19 @@ print('ok')
     ((60000, 64, 64), 200_000, 32, 32, 5e-3),     # more rows than row slots (row switching)
     ((4000, 300, 50), 500_000, 16, 12, 2e-3),     # J <= 16 (one m-tile), R = 12 (two k-tiles)
 ])
-@pytest.mark.parametrize("kernel", ["quadr", "quadr-stagedcore", "quadw"])
+@pytest.mark.parametrize("kernel", ["quadr", "quadr-stagedcore", "quadw", "quadw-gram", "quadw-chain"])
 def test_quad_sweeps_match_oracle(kernel, dims, nnz, J, R, lr):
     """-stagedcore: the K4 quad core with cp.async-staged gathers (FT_CORE_DIRECT=0; the default
-    above 64 MB of gathered C rows) instead of direct register loads."""
+    above 64 MB of gathered C rows) instead of direct register loads.  quadw picks its form by
+    the row count (the Gram / segment form for few rows, the per-step chain otherwise);
+    -gram / -chain force one form on every mode (FT_QUADW_GRAM)."""
     code = _CASE.format(dims=dims, nnz=nnz, J=J, R=R, lr=lr, seed=7)
     env = dict(os.environ, FT_FACTOR_KERNEL=kernel.split("-")[0])
     env.pop("FT_CORE_KERNEL", None)
     if kernel.endswith("-stagedcore"):
         env.update(FT_CORE_DIRECT="0")
+    if kernel.startswith("quadw-"):
+        env.update(FT_QUADW_GRAM="1" if kernel.endswith("-gram") else "0")
     out = subprocess.run([sys.executable, "-c", code], cwd=REPO, env=env, capture_output=True,
                          text=True, timeout=900)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]

@@ -856,105 +856,137 @@ __global__ void __launch_bounds__(quadw::Cfg<NP>::THREADS, NP <= 2 ? 4 : 1)
     for (int k = 0; k < 8; ++k) Dk[k + 1] = __fmaf_rn(cdec, 1.f + Dk[k], Dk[k]);
 #pragma unroll
     for (int i = 0; i < 8; ++i) wfull[i] = p.lr * (1.f + Dk[7 - i]);
-    for (int t = 0;; ++t) {
-      const int st = t % C::NS;
-      mbar_wait(full + st, (t / C::NS) & 1);
-      const int4 info = stage_info(st)[q];
-      if (info.w) break;  // stop (every quarter carries the flag)
-      if (info.y) {       // this quarter starts row info.z
-        if (ai >= 0) store_a();
-        const float4 v = *reinterpret_cast<const float4 *>(stage_a(st) + 32 * q + 4 * l);
-        a[0] = v.x, a[1] = v.y, a[2] = v.z, a[3] = v.w;
-        lo[0] = lo[1] = lo[2] = lo[3] = 0.f;
-        ai = info.z;
-      }
-      const float *Vq = stage_v(st) + 8 * q * QVS + 4 * l;
-      // the stage's 8 V rows (and operands) are loaded up front: independent LDS.128, one
-      // latency
-      float4 vv[QB];
-#pragma unroll
-      for (int kk = 0; kk < QB; ++kk) vv[kk] = *reinterpret_cast<const float4 *>(Vq + kk * QVS);
-      if (!GRAM) {  // the per-step chain: short batches run all 8 steps (padding: lr = 0)
+    if (!GRAM) {  // the per-step chain: short batches run all 8 steps (padding: lr = 0)
+      for (int t = 0;; ++t) {
+        const int st = t % C::NS;
+        mbar_wait(full + st, (t / C::NS) & 1);
+        const int4 info = stage_info(st)[q];
+        if (info.w) break;  // stop (every quarter carries the flag)
+        if (info.y) {       // this quarter starts row info.z
+          if (ai >= 0) store_a();
+          const float4 v = *reinterpret_cast<const float4 *>(stage_a(st) + 32 * q + 4 * l);
+          a[0] = v.x, a[1] = v.y, a[2] = v.z, a[3] = v.w;
+          lo[0] = lo[1] = lo[2] = lo[3] = 0.f;
+          ai = info.z;
+        }
+        // the stage's 8 V rows and step operands up front: independent LDS.128, one latency
+        const float *Vq = stage_v(st) + 8 * q * QVS + 4 * l;
         const float4 *mq = stage_meta(st) + q * MQ;
-        float4 mm[QB];
+        float4 vv[QB], mm[QB];
 #pragma unroll
-        for (int kk = 0; kk < QB; ++kk) mm[kk] = mq[kk];
+        for (int kk = 0; kk < QB; ++kk) {
+          vv[kk] = *reinterpret_cast<const float4 *>(Vq + kk * QVS);
+          mm[kk] = mq[kk];
+        }
         __syncwarp();
         mbar_arrive(empty + st);  // the stage is free once read
 #pragma unroll
         for (int kk = 0; kk < QB; ++kk) quad_chain_step_vc(a, lo, vv[kk], mm[kk]);
-        continue;
       }
-      float T[28], xk[QB];
-      {
+    } else {
+      // Gram form, software-pipelined: batch t + 1's stage is waited for, read into the other
+      // register set and released while batch t is solved, so the loads and the mbarrier round
+      // trip leave the serial path (butterfly -> solve -> update)
+      struct Batch {
+        int4 info;
+        float4 arow;
+        float4 vv[QB];
+        float T[28], xk[QB];
+      };
+      auto load = [&](Batch &B, int t) {
+        const int st = t % C::NS;
+        mbar_wait(full + st, (t / C::NS) & 1);
+        B.info = stage_info(st)[q];
+        B.arow = *reinterpret_cast<const float4 *>(stage_a(st) + 32 * q + 4 * l);
+        const float *Vq = stage_v(st) + 8 * q * QVS + 4 * l;
+#pragma unroll
+        for (int kk = 0; kk < QB; ++kk) B.vv[kk] = *reinterpret_cast<const float4 *>(Vq + kk * QVS);
         const float4 *tq4 = reinterpret_cast<const float4 *>(stage_t(st) + C::TQ * q);
 #pragma unroll
         for (int u = 0; u < 7; ++u) {
           const float4 t4 = tq4[u];
-          T[4 * u] = t4.x, T[4 * u + 1] = t4.y, T[4 * u + 2] = t4.z, T[4 * u + 3] = t4.w;
+          B.T[4 * u] = t4.x, B.T[4 * u + 1] = t4.y, B.T[4 * u + 2] = t4.z, B.T[4 * u + 3] = t4.w;
         }
         const float4 x0 = tq4[7], x1 = tq4[8];
-        xk[0] = x0.x, xk[1] = x0.y, xk[2] = x0.z, xk[3] = x0.w;
-        xk[4] = x1.x, xk[5] = x1.y, xk[6] = x1.z, xk[7] = x1.w;
+        B.xk[0] = x0.x, B.xk[1] = x0.y, B.xk[2] = x0.z, B.xk[3] = x0.w;
+        B.xk[4] = x1.x, B.xk[5] = x1.y, B.xk[6] = x1.z, B.xk[7] = x1.w;
+        __syncwarp();
+        mbar_arrive(empty + st);  // the stage is free once read
+      };
+      auto process = [&](const Batch &B) {
+        if (B.info.y) {  // this quarter starts row info.z
+          if (ai >= 0) store_a();
+          a[0] = B.arow.x, a[1] = B.arow.y, a[2] = B.arow.z, a[3] = B.arow.w;
+          lo[0] = lo[1] = lo[2] = lo[3] = 0.f;
+          ai = B.info.z;
+        }
+        // the eight dots a_0 . v_k: lane partials, one butterfly over the quarter's 8 lanes
+        float pk[QB];
+#pragma unroll
+        for (int kk = 0; kk < QB; ++kk) {
+          float2 pr = fmul2(make_float2(a[0], a[1]), make_float2(B.vv[kk].x, B.vv[kk].y));
+          pr = ffma2(make_float2(a[2], a[3]), make_float2(B.vv[kk].z, B.vv[kk].w), pr);
+          pk[kk] = pr.x + pr.y;
+        }
+#pragma unroll
+        for (int m = 4; m >= 1; m >>= 1)
+#pragma unroll
+          for (int kk = 0; kk < QB; ++kk) pk[kk] += __shfl_xor_sync(FULL, pk[kk], m);
+        // r_k = x_k - alpha^k p_k, then the unit lower-triangular solve (right-looking)
+        float r[QB];
+#pragma unroll
+        for (int kk = 0; kk < QB; ++kk) r[kk] = __fmaf_rn(-Dk[kk], pk[kk], B.xk[kk] - pk[kk]);
+#pragma unroll
+        for (int i = 0; i < QB - 1; ++i)
+#pragma unroll
+          for (int kk = i + 1; kk < QB; ++kk) r[kk] = __fmaf_rn(-B.T[quadw::tpos(i, kk)], r[i], r[kk]);
+        // a_nb = alpha^nb a_0 + sum_i lr alpha^(nb-1-i) e_i v_i: full batches use the constant
+        // weights; otherwise (a row's last batch, or a quarter without rows: nb = 0) the
+        // weights are rescaled by alpha^-(8-nb) and the padding zeroed -- selects, no loops
+        const int nb = B.info.x;
+        float wsc[QB], dn = Dk[QB];
+#pragma unroll
+        for (int i = 0; i < QB; ++i) wsc[i] = wfull[i];
+        if (!__all_sync(FULL, nb == QB)) {
+          float dd = 0.f;
+#pragma unroll
+          for (int m = 0; m < QB; ++m)
+            if (nb == m) dn = Dk[m], dd = Dk[QB - m];
+          const float sc = __fdividef(1.f, 1.f + dd);
+#pragma unroll
+          for (int i = 0; i < QB; ++i) wsc[i] = i < nb ? wfull[i] * sc : 0.f;
+        }
+        // d = sum_i w_i e_i v_i in two independent chains
+        float2 da01 = make_float2(0.f, 0.f), da23 = da01, db01 = da01, db23 = da01;
+#pragma unroll
+        for (int i = 0; i < QB; i += 2) {
+          const float w0 = wsc[i] * r[i], w1 = wsc[i + 1] * r[i + 1];
+          da01 = ffma2(make_float2(w0, w0), make_float2(B.vv[i].x, B.vv[i].y), da01);
+          da23 = ffma2(make_float2(w0, w0), make_float2(B.vv[i].z, B.vv[i].w), da23);
+          db01 = ffma2(make_float2(w1, w1), make_float2(B.vv[i + 1].x, B.vv[i + 1].y), db01);
+          db23 = ffma2(make_float2(w1, w1), make_float2(B.vv[i + 1].z, B.vv[i + 1].w), db23);
+        }
+        const float2 d01 = fadd2(da01, db01), d23 = fadd2(da23, db23);
+        // compensated a <- a + (dn a + d + lo)
+        const float2 c2 = make_float2(dn, dn);
+        const float2 a01 = make_float2(a[0], a[1]), a23 = make_float2(a[2], a[3]);
+        const float2 e01 = fadd2(d01, ffma2(c2, a01, make_float2(lo[0], lo[1])));
+        const float2 e23 = fadd2(d23, ffma2(c2, a23, make_float2(lo[2], lo[3])));
+        const float2 t01 = fadd2(a01, e01), t23 = fadd2(a23, e23);
+        const float2 s01 = fsub2(e01, fsub2(t01, a01)), s23 = fsub2(e23, fsub2(t23, a23));
+        a[0] = t01.x, a[1] = t01.y, a[2] = t23.x, a[3] = t23.y;
+        lo[0] = s01.x, lo[1] = s01.y, lo[2] = s23.x, lo[3] = s23.y;
+      };
+      Batch b0, b1;
+      load(b0, 0);
+      for (int t = 0;; t += 2) {
+        if (b0.info.w) break;  // stop (every quarter carries the flag)
+        load(b1, t + 1);
+        process(b0);
+        if (b1.info.w) break;
+        load(b0, t + 2);
+        process(b1);
       }
-      __syncwarp();
-      mbar_arrive(empty + st);  // the stage is free once read
-      // the eight dots a_0 . v_k: lane partials, one butterfly over the quarter's 8 lanes
-      float pk[QB];
-#pragma unroll
-      for (int kk = 0; kk < QB; ++kk) {
-        float2 pr = fmul2(make_float2(a[0], a[1]), make_float2(vv[kk].x, vv[kk].y));
-        pr = ffma2(make_float2(a[2], a[3]), make_float2(vv[kk].z, vv[kk].w), pr);
-        pk[kk] = pr.x + pr.y;
-      }
-#pragma unroll
-      for (int m = 4; m >= 1; m >>= 1)
-#pragma unroll
-        for (int kk = 0; kk < QB; ++kk) pk[kk] += __shfl_xor_sync(FULL, pk[kk], m);
-      // r_k = x_k - alpha^k p_k, then the unit lower-triangular solve (right-looking)
-      float r[QB];
-#pragma unroll
-      for (int kk = 0; kk < QB; ++kk) r[kk] = __fmaf_rn(-Dk[kk], pk[kk], xk[kk] - pk[kk]);
-#pragma unroll
-      for (int i = 0; i < QB - 1; ++i)
-#pragma unroll
-        for (int kk = i + 1; kk < QB; ++kk) r[kk] = __fmaf_rn(-T[quadw::tpos(i, kk)], r[i], r[kk]);
-      // a_nb = alpha^nb a_0 + sum_i lr alpha^(nb-1-i) e_i v_i: full batches use the constant
-      // weights; otherwise (a row's last batch, or a quarter without rows: nb = 0) the weights
-      // are rescaled by alpha^-(8-nb) and the padding zeroed -- selects, no divergent loops
-      const int nb = info.x;
-      float wsc[QB], dn = Dk[QB];
-#pragma unroll
-      for (int i = 0; i < QB; ++i) wsc[i] = wfull[i];
-      if (!__all_sync(FULL, nb == QB)) {
-        float dd = 0.f;
-#pragma unroll
-        for (int m = 0; m < QB; ++m)
-          if (nb == m) dn = Dk[m], dd = Dk[QB - m];
-        const float sc = __fdividef(1.f, 1.f + dd);
-#pragma unroll
-        for (int i = 0; i < QB; ++i) wsc[i] = i < nb ? wfull[i] * sc : 0.f;
-      }
-      // d = sum_i w_i e_i v_i in two independent chains
-      float2 da01 = make_float2(0.f, 0.f), da23 = da01, db01 = da01, db23 = da01;
-#pragma unroll
-      for (int i = 0; i < QB; i += 2) {
-        const float w0 = wsc[i] * r[i], w1 = wsc[i + 1] * r[i + 1];
-        da01 = ffma2(make_float2(w0, w0), make_float2(vv[i].x, vv[i].y), da01);
-        da23 = ffma2(make_float2(w0, w0), make_float2(vv[i].z, vv[i].w), da23);
-        db01 = ffma2(make_float2(w1, w1), make_float2(vv[i + 1].x, vv[i + 1].y), db01);
-        db23 = ffma2(make_float2(w1, w1), make_float2(vv[i + 1].z, vv[i + 1].w), db23);
-      }
-      const float2 d01 = fadd2(da01, db01), d23 = fadd2(da23, db23);
-      // compensated a <- a + (dn a + d + lo)
-      const float2 c2 = make_float2(dn, dn);
-      const float2 a01 = make_float2(a[0], a[1]), a23 = make_float2(a[2], a[3]);
-      const float2 e01 = fadd2(d01, ffma2(c2, a01, make_float2(lo[0], lo[1])));
-      const float2 e23 = fadd2(d23, ffma2(c2, a23, make_float2(lo[2], lo[3])));
-      const float2 t01 = fadd2(a01, e01), t23 = fadd2(a23, e23);
-      const float2 s01 = fsub2(e01, fsub2(t01, a01)), s23 = fsub2(e23, fsub2(t23, a23));
-      a[0] = t01.x, a[1] = t01.y, a[2] = t23.x, a[3] = t23.y;
-      lo[0] = s01.x, lo[1] = s01.y, lo[2] = s23.x, lo[3] = s23.y;
     }
     if (ai >= 0) store_a();
   }

@@ -557,15 +557,21 @@ __device__ __forceinline__ Rec next_batch(const SweepParams &p, Cursor &c, int64
   return r;
 }
 
+template <int NPRE>
 struct Leaf {
-  int lc, pc;
+  int lc, pc[NPRE];
   float x;
 };
-__device__ __forceinline__ Leaf load_leaf(const SweepParams &p, const Rec &r, int l) {
-  Leaf d{0, 0, 0.f};
+template <int NPRE>
+__device__ __forceinline__ Leaf<NPRE> load_leaf(const SweepParams &p, const Rec &r, int l) {
+  Leaf<NPRE> d;
+  d.lc = 0, d.x = 0.f;
+#pragma unroll
+  for (int k = 0; k < NPRE; ++k) d.pc[k] = 0;
   if (l < r.nb) {
     d.lc = __ldcs(p.leaf_coord + r.L0 + l);
-    d.pc = __ldcs(p.leaf_pc + r.L0 + l);
+#pragma unroll
+    for (int k = 0; k < NPRE; ++k) d.pc[k] = __ldcs(p.leaf_pc + (int64_t)(r.L0 + l) * NPRE + k);
     d.x = __ldcs(p.vals + r.L0 + l);
   }
   return d;
@@ -673,11 +679,11 @@ __device__ __forceinline__ void quadw_gram(const float *V, float *T, const int (
   }
 }
 
-template <bool SMALL, int NP, bool GRAM>
+template <bool SMALL, int NP, bool GRAM, int NPRE>
 __global__ void __launch_bounds__(quadw::Cfg<NP>::THREADS, NP <= 2 ? 4 : 1)
     factor_rows_quadw_kernel(const SweepParams p) {
   using namespace quad;
-  using quadp::Leaf;
+  using Leaf = quadp::Leaf<NPRE>;
   using quadp::Rec;
   using C = quadw::Cfg<NP>;
   extern __shared__ float4 smem4[];
@@ -743,17 +749,52 @@ __global__ void __launch_bounds__(quadw::Cfg<NP>::THREADS, NP <= 2 ? 4 : 1)
     const float *cpre = p.Cpre[0] + 4 * gc, *cleaf = p.Cleaf + 4 * gc;
     const int64_t Rs = p.R;
     const uint32_t xs = smem_u32(X + gs * XS + 4 * gc), ys = smem_u32(Y + gs * XS + 4 * gc);
-    auto gather = [&](const Leaf &d) {
+    // order 3: C_pre[0][pc] -> X and C_leaf[lc] -> Y in one async round, waited below; order 4:
+    // X <- C_pre[0][pc0], Y <- C_pre[1][pc1] now, then X *= Y and Y <- C_leaf[lc] at the wait
+    // (the reference's left-to-right prefix chain, as quad_gather)
+    auto issue = [&](uint32_t dst0, const float *C, int coord) {
 #pragma unroll
       for (int it = 0; it < 8; ++it) {
-        const int s = 4 * it + gs;
-        const int pcs = __shfl_sync(FULL, d.pc, s), lcs = __shfl_sync(FULL, d.lc, s);
-        if (gok) {
-          cp_async16_s(xs + it * 4 * XS * 4, cpre + pcs * Rs);
-          cp_async16_s(ys + it * 4 * XS * 4, cleaf + lcs * Rs);
+        const int cs = __shfl_sync(FULL, coord, 4 * it + gs);
+        if (gok) cp_async16_s(dst0 + it * 4 * XS * 4, C + 4 * gc + cs * Rs);
+      }
+    };
+    auto gather = [&](const Leaf &d) {
+      if (NPRE == 1) {
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int s = 4 * it + gs;
+          const int pcs = __shfl_sync(FULL, d.pc[0], s), lcs = __shfl_sync(FULL, d.lc, s);
+          if (gok) {
+            cp_async16_s(xs + it * 4 * XS * 4, cpre + pcs * Rs);
+            cp_async16_s(ys + it * 4 * XS * 4, cleaf + lcs * Rs);
+          }
         }
+      } else {
+        issue(xs, p.Cpre[0], d.pc[0]);
+        issue(ys, p.Cpre[1], d.pc[NPRE > 1 ? 1 : 0]);
       }
       cp_async_commit();
+    };
+    auto gather_finish = [&](const Leaf &d) {  // order 4: fold the prefix, then the leaf level
+      cp_async_wait_all();
+      __syncwarp();
+      if (NPRE > 1) {
+        float4 *xr = reinterpret_cast<float4 *>(X + lane * XS);
+        const float4 *yr = reinterpret_cast<const float4 *>(Y + lane * XS);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 x = xr[c], y = yr[c];
+          const float2 a2 = fmul2(make_float2(x.x, x.y), make_float2(y.x, y.y));
+          const float2 b2 = fmul2(make_float2(x.z, x.w), make_float2(y.z, y.w));
+          xr[c] = make_float4(a2.x, a2.y, b2.x, b2.y);
+        }
+        __syncwarp();
+        issue(ys, p.Cleaf, d.lc);
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncwarp();
+      }
     };
     auto load_arow = [&](const Rec &r) {  // A values of a row about to start (quarter lanes)
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -790,18 +831,17 @@ __global__ void __launch_bounds__(quadw::Cfg<NP>::THREADS, NP <= 2 ? 4 : 1)
       }
     for (int s = 0; s < k; ++s) (void)quadp::next_batch(p, cur, nstream);
     Rec r0 = next_mine(true);
-    Leaf d0 = quadp::load_leaf(p, r0, l);
+    Leaf d0 = quadp::load_leaf<NPRE>(p, r0, l);
     float4 av0 = load_arow(r0);
     float acc[2][4][4];
     for (int t = k;; t += NP) {
       const bool stop = !__any_sync(FULL, r0.nb > 0);
       if (!stop) gather(d0);
       const Rec r1 = next_mine(false);  // my next batch: indices and A values fly meanwhile
-      const Leaf d1 = quadp::load_leaf(p, r1, l);
+      const Leaf d1 = quadp::load_leaf<NPRE>(p, r1, l);
       const float4 av1 = load_arow(r1);
       if (!stop) {
-        cp_async_wait_all();
-        __syncwarp();
+        gather_finish(d0);
         quad_zero(acc);
 #pragma unroll
         for (int kt = 0; kt < KT; ++kt)
@@ -992,12 +1032,12 @@ __global__ void __launch_bounds__(quadw::Cfg<NP>::THREADS, NP <= 2 ? 4 : 1)
   }
 }
 
-template <bool SMALL, int NP, bool GRAM>
+template <bool SMALL, int NP, bool GRAM, int NPRE>
 int launch_quadw_t(const SweepParams &q0, int rpg, cudaStream_t s) {
   SweepParams q = q0;
   q.quadw_rpg = rpg;
   using C = quadw::Cfg<NP>;
-  auto kern = factor_rows_quadw_kernel<SMALL, NP, GRAM>;
+  auto kern = factor_rows_quadw_kernel<SMALL, NP, GRAM, NPRE>;
   const size_t sm = C::bytes();
   static bool set = false;
   if (!set) {
@@ -1022,7 +1062,7 @@ int launch_quadw_t(const SweepParams &q0, int rpg, cudaStream_t s) {
 // -- there the producers' gathers / combine leave no room for the Gram blocks (measured: 5.9 vs
 // 7.5-7.9 ms on Netflix mode 2, profiles/r02_quadw_gram.md).  FT_QUADW_GRAM=0 / 1 forces one
 // form (A/B).
-template <bool SMALL>
+template <bool SMALL, int NPRE>
 int launch_quadw_s(const SweepParams &q, cudaStream_t s) {
   static const int forced = [] {
     const char *e = getenv("FT_QUADW_GRAM");
@@ -1032,12 +1072,14 @@ int launch_quadw_s(const SweepParams &q, cudaStream_t s) {
   int rpg = 4;
   while (rpg > 1 && (q.nrows + rpg / 2 - 1) / (rpg / 2) <= sms) rpg /= 2;
   const bool few = (q.nrows + 3) / 4 <= sms;
-  if (forced == 0 || (forced < 0 && !few)) return launch_quadw_t<SMALL, 2, 0>(q, 4, s);
-  return launch_quadw_t<SMALL, 6, 1>(q, few ? rpg : 4, s);
+  if (forced == 0 || (forced < 0 && !few)) return launch_quadw_t<SMALL, 2, false, NPRE>(q, 4, s);
+  return launch_quadw_t<SMALL, 6, true, NPRE>(q, few ? rpg : 4, s);
 }
 
 int launch_quadw(const SweepParams &q, cudaStream_t s) {
-  return q.J <= 16 && q.R <= 16 ? launch_quadw_s<true>(q, s) : launch_quadw_s<false>(q, s);
+  const bool small = q.J <= 16 && q.R <= 16;
+  if (q.N == 4) return small ? launch_quadw_s<true, 2>(q, s) : launch_quadw_s<false, 2>(q, s);
+  return small ? launch_quadw_s<true, 1>(q, s) : launch_quadw_s<false, 1>(q, s);
 }
 
 // the quad kernels run any J, R <= 32 (R % 4 == 0; padding columns are zero); J = R = 16 has

@@ -1362,8 +1362,8 @@ template <int RP>
 int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
   // FT_FACTOR_KERNEL forces one warp-level K3b for A/B measurement (it also skips K3c):
   // quadr, quadw, dual, ws, gram.  auto: quadr for many rows at orders 3-4 (K3c takes most of
-  // these when the slot layout is present), quadw for few long rows at order 3, dual for many
-  // rows at orders 5-6, ws (order 3) / gram (orders 4-6) for few rows otherwise.
+  // these when the slot layout is present), quadw for few long rows at orders 3-4, dual for
+  // many rows at orders 5-6, gram for few rows at orders 5-6.
   static const int chosen = [] {
     const char *e = getenv("FT_FACTOR_KERNEL");
     if (!e) return 0;
@@ -1376,12 +1376,16 @@ int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
   }();
   int v = chosen;
   if ((v == 1 || v == 2) && !quad_ok(p)) v = 0;
-  if ((v == 1 && p.N > 4) || (v == 2 && p.N != 3) || (v == 4 && p.N != 3)) v = 0;
+  if ((v == 1 && p.N > 4) || (v == 2 && p.N > 4) || (v == 4 && p.N != 3)) v = 0;
   if (v == 0) {
-    const bool many = p.nrows >= (int64_t)2 * sm_count() * quad::WPB * 4;
+    // quadr from two rows per warp slot of the whole GPU up, quadw (orders 3-4) below:
+    // tools/time_shards.py on the row-sharded sweeps (Netflix mode 1 at 8.9 K / 4.4 K / 2.2 K
+    // rows: quadr 2.20 / 1.49 / 1.50 ms, quadw 2.86 / 1.45 / 0.74; order-4 10 K^4 at 2.5 K /
+    // 1.25 K rows: quadr 12.4 / 12.6, quadw 16.4 / 8.2)
+    const bool many = p.nrows >= (int64_t)sm_count() * quad::WPB * 2;
     if (quad_ok(p) && many && p.N <= 4)
       v = 1;
-    else if (quad_ok(p) && p.N == 3)
+    else if (quad_ok(p) && p.N <= 4)
       v = 2;
     else
       v = p.nrows >= (int64_t)2 * sm_count() * 16 ? 3 : (p.N == 3 ? 4 : 5);

@@ -97,6 +97,7 @@ print('ok')
     ((20000, 700, 9), 300_000, 24, 20, 1e-3),     # J < 32, R < 32 (padding), 1-3 leaf rows
     ((60000, 64, 64), 200_000, 32, 32, 5e-3),     # more rows than row slots (row switching)
     ((4000, 300, 50), 500_000, 16, 12, 2e-3),     # J <= 16 (one m-tile), R = 12 (two k-tiles)
+    ((2000, 300, 40, 25), 400_000, 32, 32, 2e-3),  # order 4 (two prefix levels), 10-16 K-update rows
 ])
 @pytest.mark.parametrize("kernel", ["quadr", "quadr-stagedcore", "quadw", "quadw-gram", "quadw-chain"])
 def test_quad_sweeps_match_oracle(kernel, dims, nnz, J, R, lr):

@@ -1378,11 +1378,12 @@ int launch_factor_rows(const SweepParams &p, cudaStream_t s) {
   if ((v == 1 || v == 2) && !quad_ok(p)) v = 0;
   if ((v == 1 && p.N > 4) || (v == 2 && p.N > 4) || (v == 4 && p.N != 3)) v = 0;
   if (v == 0) {
-    // quadr from two rows per warp slot of the whole GPU up, quadw (orders 3-4) below:
-    // tools/time_shards.py on the row-sharded sweeps (Netflix mode 1 at 8.9 K / 4.4 K / 2.2 K
-    // rows: quadr 2.20 / 1.49 / 1.50 ms, quadw 2.86 / 1.45 / 0.74; order-4 10 K^4 at 2.5 K /
-    // 1.25 K rows: quadr 12.4 / 12.6, quadw 16.4 / 8.2)
-    const bool many = p.nrows >= (int64_t)sm_count() * quad::WPB * 2;
+    // quadr from 4 (order 3) / 2 (order 4) rows per warp slot of the whole GPU up, quadw
+    // below: tools/time_shards.py on the row-sharded sweeps (Netflix mode 1 at 8.9 K / 4.4 K /
+    // 2.2 K rows: quadr 2.20 / 1.49 / 1.50 ms, quadw 2.86 / 1.45 / 0.74; Yahoo mode 2 at 3.1 K
+    // rows: 23.6 / 21.1; order-4 10 K^4 at 2.5 K / 1.25 K rows: quadr 12.4 / 12.6, quadw
+    // 16.4 / 8.2 -- its quadw producers gather two prefix levels)
+    const bool many = p.nrows >= (int64_t)sm_count() * quad::WPB * (p.N == 4 ? 2 : 4);
     if (quad_ok(p) && many && p.N <= 4)
       v = 1;
     else if (quad_ok(p) && p.N <= 4)

@@ -651,7 +651,9 @@ def run_e2e(ft, T, cfg, train_dev, args):
         main_stream.wait_event(ready)
         dev = ft.DeviceCoo(tuple(dims), bufs[slot][0], bufs[slot][1])
         model = ft.Model(dims, (J,) * N, R, init_f, init_c)
-        forest = ft.build_forest(dev, 128, compact=True)
+        # the exact schedule reads the leaf-major index only: no fiber coordinates (hogwild
+        # walks the fibers)
+        forest = ft.build_forest(dev, 128, compact=True, keep_fibers=args.schedule != "exact")
         counter = ft.OpCounter()
         cache = ft.precompute_cache(model, counter)
         m = T.run_epoch(model, forest, cache, dev, tcfg, counter, 1, None, evaluate_metrics=True)

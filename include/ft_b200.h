@@ -116,9 +116,11 @@ FT_API int ft_sm_count(int32_t *out);
  *   then node count per depth.  SYNCHRONOUS (sizes are data dependent).
  * Compact build: ptrs == NULL (and inds[d < N-1], sub_fiber_ptr, sub_leaf_ptr may be NULL)
  *   skips the reference-format per-depth arrays and subtensors, producing only what the sweep
- *   kernels read (leaf coordinates, values, fiber_ptr / fiber_coord, rows).
+ *   kernels read (leaf coordinates, values, fiber_ptr / fiber_coord, rows); a compact build may
+ *   also pass fiber_coord == NULL (no fiber coordinates: the row-owner sweeps read leaf_pc).
  * leaf_pc (optional, device int32 [nnz x (N-2)], 3 <= N <= 6): the leaf-major prefix index of
- *   ft_tree_leaf_index, written from the sorted level columns at no extra pass.
+ *   ft_tree_leaf_index, written from the sorted level columns at no extra pass (order 3: the
+ *   builder sorts straight into it).
  * Returns FT_ERR_DUPLICATE (with counts_out[3] set) if two entries share a coordinate. */
 FT_API int ft_build_tree(int32_t N, int64_t nnz, const int64_t *dims, const int32_t *idx,
                   const float *vals, int32_t root_mode, int64_t thr, float *leaf_vals,

@@ -237,12 +237,14 @@ def _trim(buf, n):
 
 
 def build_tree(tensor, root_mode: int, fiber_threshold=DEFAULT_FIBER_THRESHOLD,
-               stream=None, compact: bool = False) -> CsfTree:
+               stream=None, compact: bool = False, keep_fibers: bool = True) -> CsfTree:
     """GPU B-CSF build (csf.py:101-196).  ``tensor``: SparseCooTensor or DeviceCoo.
 
     ``compact=True`` keeps only what the sweep kernels read (leaf coordinates, values,
     fiber_ptr / fiber_coord, rows): the per-depth ``inds`` / ``ptrs`` and the subtensor arrays
-    -- reference-format fields -- are not built (saves ~40 % of a tree at order 4)."""
+    -- reference-format fields -- are not built (saves ~40 % of a tree at order 4).
+    ``keep_fibers=False`` (compact only) does not build fiber_coord at all and drops fiber_ptr
+    once the leaf-major index exists (CsfTree.drop_fibers)."""
     import torch
 
     L = _lib.lib()
@@ -272,11 +274,11 @@ def build_tree(tensor, root_mode: int, fiber_threshold=DEFAULT_FIBER_THRESHOLD,
         raise ValidationError(f"duplicate coordinate {tuple(int(c) + 1 for c in coord)}")
 
     return _build_with(call, N, nnz, dims, root_mode, compact, stream, "ft_build_tree",
-                       on_duplicate)
+                       on_duplicate, keep_fibers)
 
 
 def build_tree_derived(prev: CsfTree, fiber_threshold=DEFAULT_FIBER_THRESHOLD, stream=None,
-                       compact: bool = False):
+                       compact: bool = False, keep_fibers: bool = True):
     """The tree rooted at ``prev.root_mode + 1`` from ``prev``'s leaf order (K1 derived build,
     ``ft_build_tree_derived``): a stable radix sort on a 32-bit key instead of the full-width
     COO sort; bit-identical to ``build_tree``.  None when it does not apply (prev without the
@@ -295,7 +297,7 @@ def build_tree_derived(prev: CsfTree, fiber_threshold=DEFAULT_FIBER_THRESHOLD, s
 
     try:
         return _build_with(call, N, nnz, dims, root_mode, compact, stream,
-                           "ft_build_tree_derived", None)
+                           "ft_build_tree_derived", None, keep_fibers)
     except _Unsupported:
         return None
 
@@ -304,7 +306,8 @@ class _Unsupported(Exception):
     pass
 
 
-def _build_with(call, N, nnz, dims, root_mode, compact, stream, what, on_duplicate):
+def _build_with(call, N, nnz, dims, root_mode, compact, stream, what, on_duplicate,
+                keep_fibers=True):
     """Allocate a build's output buffers, run ``call`` (an ft_build_tree* entry point), trim and
     wrap them as a CsfTree with its leaf-major index."""
     import torch
@@ -315,7 +318,8 @@ def _build_with(call, N, nnz, dims, root_mode, compact, stream, what, on_duplica
     inds = [torch.empty(nnz, **i32) for _ in range(N - 1)] + [leaf] if not compact else [leaf]
     ptrs = [torch.empty(nnz + 1, **i32) for _ in range(N - 1)] if not compact else []
     fiber_ptr = torch.empty(nnz + 1, **i32)
-    fiber_coord = torch.empty(nnz * (N - 1), **i32)
+    no_coord = compact and not keep_fibers and 3 <= N <= _leaf_index_max_order()
+    fiber_coord = None if no_coord else torch.empty(nnz * (N - 1), **i32)
     sub_fiber_ptr = torch.empty(nnz + 1, **i32) if not compact else None
     sub_leaf_ptr = torch.empty(nnz + 1, **i32) if not compact else None
     row_fiber_ptr = torch.empty(nnz + 1, **i32)
@@ -327,7 +331,7 @@ def _build_with(call, N, nnz, dims, root_mode, compact, stream, what, on_duplica
     ptr_tab = None if compact else (ctypes.c_void_p * max(N - 1, 1))(*[a.data_ptr() for a in ptrs])
     out = {"dims": (ctypes.c_int64 * N)(*dims),
            "args": (leaf_vals.data_ptr(), ind_tab, ptr_tab, fiber_ptr.data_ptr(),
-                    fiber_coord.data_ptr(), _lib.ptr(sub_fiber_ptr), _lib.ptr(sub_leaf_ptr),
+                    _lib.ptr(fiber_coord), _lib.ptr(sub_fiber_ptr), _lib.ptr(sub_leaf_ptr),
                     row_fiber_ptr.data_ptr(), row_coord.data_ptr(),
                     counts.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), _lib.ptr(leaf_pc),
                     _lib.stream_handle(stream))}
@@ -356,7 +360,8 @@ def _build_with(call, N, nnz, dims, root_mode, compact, stream, what, on_duplica
         ptrs=ptrs_t,
         vals=leaf_vals,
         fiber_ptr=_trim(fiber_ptr, F + 1),
-        fiber_coord=_trim(fiber_coord, F * (N - 1)).view(F, N - 1),
+        fiber_coord=(torch.empty((0, N - 1), **i32) if fiber_coord is None
+                     else _trim(fiber_coord, F * (N - 1)).view(F, N - 1)),
         sub_fiber_ptr=sfp,
         sub_leaf_ptr=slp,
         row_fiber_ptr=_trim(row_fiber_ptr, rows + 1),
@@ -364,6 +369,8 @@ def _build_with(call, N, nnz, dims, root_mode, compact, stream, what, on_duplica
     )
     tree.num_subtensors_built = S
     add_leaf_index(tree, stream, leaf_pc=leaf_pc)
+    if no_coord:
+        tree.drop_fibers()
     return tree
 
 
@@ -439,15 +446,17 @@ def build_forest(tensor, fiber_threshold=DEFAULT_FIBER_THRESHOLD, stream=None,
         # applies (bit-identical; Netflix: 4 radix passes of 4-byte keys instead of 6 of 8-byte)
         # keep_fibers=False: each tree's fiber arrays are freed as soon as the next tree is
         # derived from it (tree t+1's build reads only tree t's leaf-major index)
-        trees = [build_tree(dev, 0, fiber_threshold, stream, compact)]
+        # (compact builds without fibers never compute fiber_coord at all)
+        kf = keep_fibers or not compact
+        trees = [build_tree(dev, 0, fiber_threshold, stream, compact, kf)]
         for t in range(1, N):
-            tree = build_tree_derived(trees[-1], fiber_threshold, stream, compact) \
+            tree = build_tree_derived(trees[-1], fiber_threshold, stream, compact, kf) \
                 if derived else None
-            if not keep_fibers:
+            if not keep_fibers and trees[-1].nfib < 0:
                 trees[-1].drop_fibers()
             trees.append(tree if tree is not None
-                         else build_tree(dev, t, fiber_threshold, stream, compact))
-        if not keep_fibers:
+                         else build_tree(dev, t, fiber_threshold, stream, compact, kf))
+        if not keep_fibers and trees[-1].nfib < 0:
             trees[-1].drop_fibers()
         return CsfForest(trees=tuple(trees), fiber_threshold=fiber_threshold)
     from concurrent.futures import ThreadPoolExecutor

@@ -312,22 +312,27 @@ struct DerivedArgs {
   int shift[FT_MAX_ORDER];  // new level d (< N-1) -> bit shift in the key
 };
 
+// N is a template parameter: the level loops unroll and the shift / mask / column tables stay in
+// registers (with a runtime N the parameter structs were copied to the stack per thread)
+template <int N>
 __global__ void pack_derived(const uint32_t *__restrict__ leaf_row, const int32_t *__restrict__ row_coord,
                              const int32_t *__restrict__ leaf_pc, const int32_t *__restrict__ leaf_coord,
                              const float *__restrict__ vals, int64_t nnz, DerivedArgs a,
                              uint32_t *__restrict__ keys, unsigned long long *__restrict__ pay) {
   const int64_t L = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (L >= nnz) return;
-  const int NP = a.N - 2;
+  constexpr int NP = N - 2;
   uint32_t k = 0;
   // new level d = old level d + 1: old levels 1..N-2 from leaf_pc, old level N-1 = leaf_coord
+#pragma unroll
   for (int d = 0; d < NP; ++d) k |= (uint32_t)__ldg(leaf_pc + L * NP + d) << a.shift[d];
-  k |= (uint32_t)__ldg(leaf_coord + L) << a.shift[a.N - 2];
+  k |= (uint32_t)__ldg(leaf_coord + L) << a.shift[N - 2];
   keys[L] = k;
   const uint32_t root = (uint32_t)__ldg(row_coord + __ldg(leaf_row + L));
   pay[L] = ((unsigned long long)root << 32) | __float_as_uint(__ldg(vals + L));
 }
 
+template <int N>
 __global__ void decode_derived(const uint32_t *__restrict__ keys,
                                const unsigned long long *__restrict__ pay, int64_t nnz,
                                DerivedArgs a, DecodeArgs da, float *__restrict__ vout,
@@ -336,35 +341,37 @@ __global__ void decode_derived(const uint32_t *__restrict__ keys,
   if (p >= nnz) return;
   const uint32_t k = keys[p];
   const unsigned long long q = pay[p];
-  for (int d = 0; d < a.N - 1; ++d) da.K[d][p] = (int32_t)((k >> a.shift[d]) & (uint32_t)da.mask[d]);
-  da.K[a.N - 1][p] = (int32_t)(q >> 32);
+#pragma unroll
+  for (int d = 0; d < N - 1; ++d) da.K[d][p] = (int32_t)((k >> a.shift[d]) & (uint32_t)da.mask[d]);
+  da.K[N - 1][p] = (int32_t)(q >> 32);
   vout[p] = __uint_as_float((uint32_t)q);
   int first = 0;
   if (p > 0) {
     const uint32_t x = k ^ keys[p - 1];
     if (x == 0) {
-      first = a.N - 1;  // same prefix: the entries differ in the (old root) leaf level
+      first = N - 1;  // same prefix: the entries differ in the (old root) leaf level
     } else {
+      // the most significant differing bit lies in the first (most significant) level whose
+      // field it falls in; levels are laid out from level 0 (top) down
       const int hb = 31 - __clz((int)x);
-      first = a.N - 2;
-      for (int d = 0; d < a.N - 1; ++d)
-        if (da.mask[d] && hb >= a.shift[d] && hb < a.shift[d] + 64 - __clzll((long long)da.mask[d])) {
-          first = d;
-          break;
-        }
+      first = N - 2;
+#pragma unroll
+      for (int d = N - 2; d >= 0; --d)
+        if (da.mask[d] && hb >= a.shift[d]) first = d < first ? d : first;
     }
   }
   fdl[p] = (uint8_t)first;
 }
 
 struct LeafPcArgs {
-  int NP;
   const int32_t *K[4];
 };
+template <int NP>
 __global__ void leaf_pc_from_levels(LeafPcArgs a, int64_t nnz, int32_t *__restrict__ out) {
   const int64_t L = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (L >= nnz) return;
-  for (int d = 0; d < a.NP; ++d) out[L * a.NP + d] = __ldg(a.K[d] + L);
+#pragma unroll
+  for (int d = 0; d < NP; ++d) out[L * NP + d] = __ldg(a.K[d] + L);
 }
 
 // Everything after the level columns K_d (sorted, level order) and first-differing levels are
@@ -375,11 +382,14 @@ int finish_tree(cudaStream_t s, Scratch &sc, int N, int64_t nnz, int64_t thr, bo
                 int32_t *sub_leaf_ptr, int32_t *row_fiber_ptr, int32_t *row_coord,
                 int64_t *counts_out, int32_t *leaf_pc) {
   const unsigned nb = blocks_for(nnz);
-  if (leaf_pc && N >= 3 && N <= 6) {  // every leaf carries its fiber's levels 1..N-2 in K_d
+  // every leaf carries its fiber's levels 1..N-2 in K_d; at order 3 K_1 IS the leaf_pc buffer
+  // (the builders alias it), at orders 4-6 the columns are interleaved into it
+  if (leaf_pc && N >= 4 && N <= 6) {
     LeafPcArgs la{};
-    la.NP = N - 2;
     for (int d = 0; d < N - 2; ++d) la.K[d] = K[d + 1];
-    leaf_pc_from_levels<<<nb, 256, 0, s>>>(la, nnz, leaf_pc);
+    if (N == 4) leaf_pc_from_levels<2><<<nb, 256, 0, s>>>(la, nnz, leaf_pc);
+    if (N == 5) leaf_pc_from_levels<3><<<nb, 256, 0, s>>>(la, nnz, leaf_pc);
+    if (N == 6) leaf_pc_from_levels<4><<<nb, 256, 0, s>>>(la, nnz, leaf_pc);
     if (int rc = check_launch("leaf_pc_from_levels")) return rc;
   }
   GatherArgs ga{};
@@ -437,9 +447,11 @@ int finish_tree(cudaStream_t s, Scratch &sc, int N, int64_t nnz, int64_t thr, bo
     set_i32<<<1, 1, 0, s>>>(sub_leaf_ptr + S, (int32_t)nnz);
   }
 
-  // fiber_coord[f, d] = K_d[fiber_ptr[f]]
-  for (int d = 0; d < N - 1; ++d)
-    gather_i32<<<blocks_for(F), 256, 0, s>>>(ga.K[d], fiber_ptr, F, fiber_coord + d, N - 1);
+  // fiber_coord[f, d] = K_d[fiber_ptr[f]] (NULL: a compact tree without fiber coordinates --
+  // build_forest(keep_fibers=False); the row-owner sweeps read the leaf-major index instead)
+  if (fiber_coord)
+    for (int d = 0; d < N - 1; ++d)
+      gather_i32<<<blocks_for(F), 256, 0, s>>>(ga.K[d], fiber_ptr, F, fiber_coord + d, N - 1);
 
   // per-depth node starts; inds / ptrs.  Depth N-1: every leaf (inds[N-1] already written).
   counts_out[4 + N - 1] = nnz;
@@ -496,7 +508,7 @@ extern "C" int ft_build_tree(int32_t N, int64_t nnz, const int64_t *dims, const 
   // arrays (reference-format fields) are neither computed nor stored
   const bool compact = ptrs == nullptr;
   if (!dims || !idx || !vals || !leaf_vals || !inds || !inds[N - 1] || !fiber_ptr ||
-      !fiber_coord || !row_fiber_ptr || !row_coord || !counts_out ||
+      (!fiber_coord && !compact) || !row_fiber_ptr || !row_coord || !counts_out ||
       (!compact && (!sub_fiber_ptr || !sub_leaf_ptr)))
     return fail(FT_ERR_ARG, "ft_build_tree: null argument");
   keep_pool();
@@ -548,7 +560,7 @@ extern "C" int ft_build_tree(int32_t N, int64_t nnz, const int64_t *dims, const 
   ga.N = N;
   for (int d = 0; d < N; ++d) {
     ga.lm[d] = lm[d];
-    ga.K[d] = (d == N - 1) ? inds[N - 1] : sc.get<int32_t>(nnz);
+    ga.K[d] = (d == N - 1) ? inds[N - 1] : (d == 1 && N == 3 && leaf_pc) ? leaf_pc : sc.get<int32_t>(nnz);
     if (!ga.K[d]) return fail(FT_ERR_CUDA, "ft_build_tree: out of device memory (levels)");
   }
   uint8_t *fdl = sc.get<uint8_t>(nnz);
@@ -699,8 +711,8 @@ extern "C" int ft_build_tree_derived(const ft_tree_t *prev, const int64_t *dims,
     return fail(FT_ERR_UNSUPPORTED, "ft_build_tree_derived: previous tree lacks the leaf index");
   if (nnz <= 0) return fail(FT_ERR_EMPTY, "cannot index an empty tensor");
   const bool compact = ptrs == nullptr;
-  if (!leaf_vals || !inds || !inds[N - 1] || !fiber_ptr || !fiber_coord || !row_fiber_ptr ||
-      !row_coord || !counts_out || (!compact && (!sub_fiber_ptr || !sub_leaf_ptr)))
+  if (!leaf_vals || !inds || !inds[N - 1] || !fiber_ptr || (!fiber_coord && !compact) ||
+      !row_fiber_ptr || !row_coord || !counts_out || (!compact && (!sub_fiber_ptr || !sub_leaf_ptr)))
     return fail(FT_ERR_ARG, "ft_build_tree_derived: null argument");
   const int root = (prev->root_mode + 1) % N;
   int lm[FT_MAX_ORDER], bits[FT_MAX_ORDER];
@@ -742,8 +754,15 @@ extern "C" int ft_build_tree_derived(const ft_tree_t *prev, const int64_t *dims,
     if (!t) return fail(FT_ERR_CUDA, "ft_build_tree_derived: out of device memory (scan)");
     FT_CUDA(cub::DeviceScan::InclusiveScan(t, b, mark, leaf_row, cub::Max(), nnz, s));
   }
-  pack_derived<<<nb, 256, 0, s>>>(leaf_row, prev->row_coord, prev->leaf_pc, prev->leaf_coord,
-                                  prev->vals, nnz, a, k0, q0);
+  switch (N) {
+#define FT_PACK(n)                                                                               \
+  case n:                                                                                        \
+    pack_derived<n><<<nb, 256, 0, s>>>(leaf_row, prev->row_coord, prev->leaf_pc, prev->leaf_coord, \
+                                       prev->vals, nnz, a, k0, q0);                              \
+    break;
+    FT_PACK(3) FT_PACK(4) FT_PACK(5) FT_PACK(6)
+#undef FT_PACK
+  }
   if (int rc = check_launch("pack_derived")) return rc;
   {
     size_t b = 0;
@@ -756,13 +775,20 @@ extern "C" int ft_build_tree_derived(const ft_tree_t *prev, const int64_t *dims,
   DecodeArgs da{};
   da.N = N;
   for (int d = 0; d < N; ++d) {
-    K[d] = (d == N - 1) ? inds[N - 1] : sc.get<int32_t>(nnz);
+    K[d] = (d == N - 1) ? inds[N - 1] : (d == 1 && N == 3 && leaf_pc) ? leaf_pc : sc.get<int32_t>(nnz);
     if (!K[d]) return fail(FT_ERR_CUDA, "ft_build_tree_derived: out of device memory (levels)");
     da.K[d] = K[d];
     da.mask[d] = bits[d] >= 64 ? ~0ull : ((1ull << bits[d]) - 1);
   }
   uint8_t *fdl = sc.get<uint8_t>(nnz);
-  decode_derived<<<nb, 256, 0, s>>>(k1, q1, nnz, a, da, leaf_vals, fdl);
+  switch (N) {
+#define FT_DECODE(n)                                                                   \
+  case n:                                                                              \
+    decode_derived<n><<<nb, 256, 0, s>>>(k1, q1, nnz, a, da, leaf_vals, fdl);          \
+    break;
+    FT_DECODE(3) FT_DECODE(4) FT_DECODE(5) FT_DECODE(6)
+#undef FT_DECODE
+  }
   if (int rc = check_launch("decode_derived")) return rc;
   for (int k = 0; k < 4 + N; ++k) counts_out[k] = 0;
   counts_out[3] = -1;

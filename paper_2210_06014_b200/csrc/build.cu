@@ -159,13 +159,18 @@ __global__ void flags_le(const uint8_t *__restrict__ fdl, const uint8_t *__restr
   out[p] = (fdl[p] <= lim) || (extra && extra[p]);
 }
 
-// root run flags over fibers: fiber f starts a new root slice iff level 0 changed at its first leaf
-__global__ void run_flags(const int32_t *__restrict__ fiber_ptr, const uint8_t *__restrict__ fdl,
-                          int64_t F, uint8_t *__restrict__ out) {
-  int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (f >= F) return;
-  out[f] = fdl[fiber_ptr[f]] == 0;
-}
+// select predicates over positions (DeviceSelect::If, no flag pass): a fiber starts where the
+// first differing level is <= N-2; a fiber starts a root slice where level 0 changed
+struct FdlLe {
+  const uint8_t *fdl;
+  int lim;
+  __device__ __forceinline__ bool operator()(int32_t i) const { return fdl[i] <= lim; }
+};
+struct RunStart {
+  const int32_t *fiber_ptr;
+  const uint8_t *fdl;
+  __device__ __forceinline__ bool operator()(int32_t f) const { return fdl[fiber_ptr[f]] == 0; }
+};
 
 __global__ void chunk_counts(const int32_t *__restrict__ run_start, int64_t nruns, int64_t F,
                              int64_t thr, int32_t *__restrict__ nch) {
@@ -280,20 +285,35 @@ struct Compactor {
   Compactor(cudaStream_t st, Scratch &scr, int64_t nmax) : s(st), sc(scr), n_max(nmax) {
     d_count = sc.get<int64_t>(1);
     thrust::counting_iterator<int32_t> it(0);
-    cub::DeviceSelect::Flagged(nullptr, tmp_bytes, it, (const uint8_t *)nullptr,
-                               (int32_t *)nullptr, d_count, nmax, s);
+    size_t b1 = 0, b2 = 0, b3 = 0;
+    cub::DeviceSelect::Flagged(nullptr, b1, it, (const uint8_t *)nullptr, (int32_t *)nullptr,
+                               d_count, nmax, s);
+    cub::DeviceSelect::If(nullptr, b2, it, (int32_t *)nullptr, d_count, nmax, FdlLe{nullptr, 0}, s);
+    cub::DeviceSelect::If(nullptr, b3, it, (int32_t *)nullptr, d_count, nmax, RunStart{nullptr, nullptr}, s);
+    tmp_bytes = b1 > b2 ? b1 : b2;
+    tmp_bytes = tmp_bytes > b3 ? tmp_bytes : b3;
     tmp = sc.get<uint8_t>(tmp_bytes);
   }
   int run(const uint8_t *flags, int64_t n, int32_t *out, int64_t *host_count) {
     thrust::counting_iterator<int32_t> it(0);
     size_t b = tmp_bytes;
     FT_CUDA(cub::DeviceSelect::Flagged(tmp, b, it, flags, out, d_count, n, s));
+    return fetch(host_count);
+  }
+  // positions i < n with pred(i), no flag array (the predicate reads fdl directly)
+  template <class Pred>
+  int run_if(Pred pred, int64_t n, int32_t *out, int64_t *host_count) {
+    thrust::counting_iterator<int32_t> it(0);
+    size_t b = tmp_bytes;
+    FT_CUDA(cub::DeviceSelect::If(tmp, b, it, out, d_count, n, pred, s));
+    return fetch(host_count);
+  }
+  int fetch(int64_t *host_count) {
     FT_CUDA(cudaMemcpyAsync(host_count, d_count, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     FT_CUDA(cudaStreamSynchronize(s));
     return FT_OK;
   }
 };
-
 
 // ---- derived build: tree (t+1) from tree t's leaf order -------------------------------------
 // Tree t holds the entries sorted by (i_t, i_{t+1}, ..., i_{t+N-1}); a STABLE sort of that
@@ -405,15 +425,12 @@ int finish_tree(cudaStream_t s, Scratch &sc, int N, int64_t nnz, int64_t thr, bo
 
   // fibers: runs of equal first N-1 levels
   int64_t F = 0;
-  flags_le<<<nb, 256, 0, s>>>(fdl, nullptr, nnz, N - 2, flagA);
-  if (int rc = comp.run(flagA, nnz, fiber_ptr, &F)) return rc;
+  if (int rc = comp.run_if(FdlLe{fdl, N - 2}, nnz, fiber_ptr, &F)) return rc;
   set_i32<<<1, 1, 0, s>>>(fiber_ptr + F, (int32_t)nnz);
 
   // root slices over fibers
-  uint8_t *rflag = sc.get<uint8_t>(F);
-  run_flags<<<blocks_for(F), 256, 0, s>>>(fiber_ptr, fdl, F, rflag);
   int64_t nruns = 0;
-  if (int rc = comp.run(rflag, F, row_fiber_ptr, &nruns)) return rc;
+  if (int rc = comp.run_if(RunStart{fiber_ptr, fdl}, F, row_fiber_ptr, &nruns)) return rc;
   set_i32<<<1, 1, 0, s>>>(row_fiber_ptr + nruns, (int32_t)F);
   // row_coord[r] = K_0[fiber_ptr[row_fiber_ptr[r]]]
   {

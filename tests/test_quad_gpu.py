@@ -219,3 +219,44 @@ def test_derived_tree_build_is_bit_identical(ft, dims, compact):
             np.testing.assert_array_equal(a.cpu().numpy(), b.cpu().numpy())
         assert got.num_subtensors == want.num_subtensors
         prev = got
+
+
+@pytest.mark.parametrize("dims", [(3000, 400, 60), (60, 50, 40, 30)])
+def test_forest_without_fibers_matches(ft, dims):
+    """build_forest(compact=True, keep_fibers=False) -- no fiber coordinates computed at all
+    (the exact-schedule e2e step) -- gives the same leaf-major trees as the full compact build,
+    refuses the fiber-walking hogwild sweep loudly, and trains to the same factors."""
+    import torch
+    from paper_2210_06014_b200 import csf
+
+    rng = np.random.default_rng(11 + len(dims))
+    lin = rng.choice(int(np.prod(dims)), size=200_000, replace=False)
+    idx = np.stack(np.unravel_index(lin, dims), axis=1)
+    dev = ft.DeviceCoo(dims, torch.from_numpy(idx.astype(np.int32)).cuda(),
+                       torch.from_numpy(rng.uniform(1, 5, len(lin)).astype(np.float32)).cuda())
+    full = csf.build_forest(dev, 16, compact=True)
+    lean = csf.build_forest(dev, 16, compact=True, keep_fibers=False)
+    for a, b in zip(full.trees, lean.trees):
+        assert b.fiber_coord.numel() == 0 and b.num_fibers == a.num_fibers
+        for name in ("vals", "row_fiber_ptr", "row_coord", "leaf_pc", "row_leaf_ptr", "seg_coord",
+                     "seg_leaf_ptr"):
+            np.testing.assert_array_equal(getattr(b, name).cpu().numpy(),
+                                          getattr(a, name).cpu().numpy(), err_msg=name)
+        np.testing.assert_array_equal(b.inds[-1].cpu().numpy(), a.inds[-1].cpu().numpy())
+    N = len(dims)
+    outs = []
+    for forest in (full, lean):
+        model = ft.default_init_model(dims, (16,) * N, 16, seed=3)
+        cache = ft.precompute_cache(model)
+        cfg = ft.TrainConfig(epochs=1)
+        for n in range(N):
+            ft.update_factor_mode(model, forest, cache, n, cfg)
+        for n in range(N):
+            ft.update_core_mode(model, forest, cache, n, cfg)
+        outs.append([f.cpu().numpy() for f in model.factors] + [c.cpu().numpy() for c in model.cores_t])
+    for a, b in zip(*outs):
+        np.testing.assert_array_equal(a, b)
+    model = ft.default_init_model(dims, (16,) * N, 16, seed=3)
+    with pytest.raises(Exception):
+        ft.update_factor_mode(model, lean, ft.precompute_cache(model), 0,
+                              ft.TrainConfig(epochs=1, schedule="hogwild"))

@@ -56,7 +56,7 @@ for rep in range(3):
     dev2 = ft.DeviceCoo(dims, idx_d, vals_d)
     m2 = ft.Model(dims, (32,) * 3, 32, init_f, init_c)
     ev[1].record()
-    f2 = ft.build_forest(dev2, 128, compact=True)
+    f2 = ft.build_forest(dev2, 128, compact=True, keep_fibers=False)
     ev[2].record()
     c2 = ft.precompute_cache(m2, ft.OpCounter())
     t_s0 = time.perf_counter()

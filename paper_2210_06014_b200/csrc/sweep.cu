@@ -66,6 +66,7 @@ struct SweepParams {
   float *partials;   // core: [grid][R*J]
   int64_t gather_bytes;  // bytes of the gathered C matrices (modes other than u)
   int quadw_rpg;         // quadw: rows per warp group (0: 4)
+  int quadw_la;          // quadw per-step form: one step of lookahead (quad_batch_lookahead)
 };
 
 // Fiber index of each of the batch's leaves (lane k -> leaf L0+k), given fcur = fiber holding
@@ -1500,8 +1501,9 @@ extern "C" int ft_core_sweep_rows(const ft_tree_t *tree, const ft_model_t *model
   // row's leaves), so few long rows fill the GPU too (Netflix mode 2: 2,182 rows -> 89 K
   // segments); without segments it needs rows to fill its 4-rows-per-warp slots
   const int64_t fill = (int64_t)2 * sm_count() * cquad::WPB * 4;
+  // (a tree without fiber arrays can only run quad: the fill rule is a speed choice only)
   const bool use_quad = !core_rows_forced && core_quad_ok(p) &&
-                        (p.nsegs > 0 ? p.nsegs : p.nrows) >= fill;
+                        ((p.nsegs > 0 ? p.nsegs : p.nrows) >= fill || !p.fiber_ptr);
   if (use_quad && p.nsegs > 0) {  // the quad kernel reads segments through the row fields
     p.nrows = p.nsegs;
     p.row_coord = p.seg_coord;

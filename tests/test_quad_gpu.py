@@ -99,12 +99,14 @@ print('ok')
     ((4000, 300, 50), 500_000, 16, 12, 2e-3),     # J <= 16 (one m-tile), R = 12 (two k-tiles)
     ((2000, 300, 40, 25), 400_000, 32, 32, 2e-3),  # order 4 (two prefix levels), 10-16 K-update rows
 ])
-@pytest.mark.parametrize("kernel", ["quadr", "quadr-stagedcore", "quadw", "quadw-gram", "quadw-chain"])
+@pytest.mark.parametrize("kernel", ["quadr", "quadr-stagedcore", "quadw", "quadw-gram", "quadw-chain",
+                                    "quadw-chain0", "quadw-chain2"])
 def test_quad_sweeps_match_oracle(kernel, dims, nnz, J, R, lr):
     """-stagedcore: the K4 quad core with cp.async-staged gathers (FT_CORE_DIRECT=0; the default
     above 64 MB of gathered C rows) instead of direct register loads.  quadw picks its form by
     the row count (the Gram / segment form for few rows, the per-step chain otherwise);
-    -gram / -chain force one form on every mode (FT_QUADW_GRAM)."""
+    -gram / -chain force one form on every mode (FT_QUADW_GRAM); -chain0 / -chain2: the
+    per-step chain without lookahead / with two steps of it (FT_QUADW_LA)."""
     code = _CASE.format(dims=dims, nnz=nnz, J=J, R=R, lr=lr, seed=7)
     env = dict(os.environ, FT_FACTOR_KERNEL=kernel.split("-")[0])
     env.pop("FT_CORE_KERNEL", None)
@@ -112,6 +114,8 @@ def test_quad_sweeps_match_oracle(kernel, dims, nnz, J, R, lr):
         env.update(FT_CORE_DIRECT="0")
     if kernel.startswith("quadw-"):
         env.update(FT_QUADW_GRAM="1" if kernel.endswith("-gram") else "0")
+        if kernel[-1] in "02":
+            env.update(FT_QUADW_LA=kernel[-1])
     out = subprocess.run([sys.executable, "-c", code], cwd=REPO, env=env, capture_output=True,
                          text=True, timeout=900)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
@@ -254,8 +258,14 @@ def test_forest_without_fibers_matches(ft, dims):
         for n in range(N):
             ft.update_core_mode(model, forest, cache, n, cfg)
         outs.append([f.cpu().numpy() for f in model.factors] + [c.cpu().numpy() for c in model.cores_t])
-    for a, b in zip(*outs):
-        np.testing.assert_array_equal(a, b)
+    # the factor sweeps run the same kernels (bit-identical); the core sweep of a tree without
+    # fibers always runs K4 quad, while the full tree may take the one-row-per-warp K4 on small
+    # shapes (another fixed summation order): the cores agree to fp32 rounding
+    for n, (a, b) in enumerate(zip(*outs)):
+        if n < N:
+            np.testing.assert_array_equal(a, b)
+        else:
+            np.testing.assert_allclose(a, b, rtol=1e-5, atol=1e-7)
     model = ft.default_init_model(dims, (16,) * N, 16, seed=3)
     with pytest.raises(Exception):
         ft.update_factor_mode(model, lean, ft.precompute_cache(model), 0,

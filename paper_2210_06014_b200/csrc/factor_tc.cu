@@ -43,11 +43,8 @@ constexpr int SLOTS = 128;
 constexpr int CWARPS = 4;                    // consumer warps: warp <-> TMEM lanes 32(w%4)..+31
 // PW producer warps per TMEM lane quadrant (they take alternate batches), 4 consumer warps, the
 // MMA warp
-// KB = 8 adds two chain warps (the 4 consumer warps then only stage V rows through shared memory)
-constexpr int CHAIN_WARPS = 2;
 template <int PW, int KB = 1>
-constexpr int tc_threads() { return (4 * PW + CWARPS + (KB > 1 ? CHAIN_WARPS : 0) + 1) * 32; }
-constexpr int VS = 2;  // KB = 8: V staging stages (TMEM -> shared memory -> chain warp)
+constexpr int tc_threads() { return (4 * PW + CWARPS + 1) * 32; }
 // TMEM: AS A stages (A_hi | A_lo, 64 columns each) then DS D stages (64 columns each).  The A
 // ring is the deep one: a producer reuses an A stage once that batch's MMAs completed, so the
 // producers run up to AS batches ahead of the tensor core; consumers trail the MMA closely.
@@ -146,6 +143,62 @@ __device__ __forceinline__ float2 f2sub(float2 a, float2 b) {
   return f2add(a, make_float2(-b.x, -b.y));
 }
 
+// K3c-wide (KB = 8) chain in the quad layout: lane (row group of 8 lanes, k) holds columns
+// 4k .. 4k + 3 of its row (the quadw consumer's arithmetic, sweep.cu / quad.cuh).
+namespace k3w {
+__device__ __forceinline__ float dot(const float (&a)[4], const float4 v) {
+  float2 pr = f2fma(make_float2(a[0], a[1]), make_float2(v.x, v.y), make_float2(0.f, 0.f));
+  pr = f2fma(make_float2(a[2], a[3]), make_float2(v.z, v.w), pr);
+  float s = pr.x + pr.y;
+  s += __shfl_xor_sync(FULL, s, 4);
+  s += __shfl_xor_sync(FULL, s, 2);
+  s += __shfl_xor_sync(FULL, s, 1);
+  return s;
+}
+// compensated update a <- a + (c a + lr e v) (Fast2Sum residue lo; m = (x, lr, c, c))
+__device__ __forceinline__ void update(float (&a)[4], float (&lo)[4], const float4 v, float4 m,
+                                       float e) {
+  const float2 l2 = make_float2(m.y * e, m.y * e), c2 = make_float2(m.z, m.w);
+  const float2 a01 = make_float2(a[0], a[1]), a23 = make_float2(a[2], a[3]);
+  const float2 d01 = f2fma(l2, make_float2(v.x, v.y), f2fma(c2, a01, make_float2(lo[0], lo[1])));
+  const float2 d23 = f2fma(l2, make_float2(v.z, v.w), f2fma(c2, a23, make_float2(lo[2], lo[3])));
+  const float2 t01 = f2add(a01, d01), t23 = f2add(a23, d23);
+  const float2 r01 = f2sub(d01, f2sub(t01, a01)), r23 = f2sub(d23, f2sub(t23, a23));
+  a[0] = t01.x, a[1] = t01.y, a[2] = t23.x, a[3] = t23.y;
+  lo[0] = r01.x, lo[1] = r01.y, lo[2] = r23.x, lo[3] = r23.y;
+}
+__device__ __forceinline__ void step(float (&a)[4], float (&lo)[4], const float4 v, float4 m) {
+  update(a, lo, v, m, m.x - dot(a, v));
+}
+// 8 consecutive updates of one row with one step of lookahead (quad.cuh quad_batch_lookahead):
+// e_k = x_k - (1 + c_{k-1}) (a_{k-1} . v_k) - lr_{k-1} (v_{k-1} . v_k) e_{k-1}
+__device__ __forceinline__ void batch_la(float (&a)[4], float (&lo)[4], const float4 (&vv)[8],
+                                         const float4 (&mm)[8]) {
+  float g[8];
+#pragma unroll
+  for (int kk = 1; kk < 8; ++kk) {
+    float2 pr = f2fma(make_float2(vv[kk - 1].x, vv[kk - 1].y), make_float2(vv[kk].x, vv[kk].y),
+                      make_float2(0.f, 0.f));
+    pr = f2fma(make_float2(vv[kk - 1].z, vv[kk - 1].w), make_float2(vv[kk].z, vv[kk].w), pr);
+    g[kk] = pr.x + pr.y;
+  }
+#pragma unroll
+  for (int msk = 4; msk >= 1; msk >>= 1)
+#pragma unroll
+    for (int kk = 1; kk < 8; ++kk) g[kk] += __shfl_xor_sync(FULL, g[kk], msk);
+  float pk = dot(a, vv[0]);
+  float e_prev = 0.f, lg = 0.f, cprev = 0.f;
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    const float pn = kk + 1 < 8 ? dot(a, vv[kk + 1]) : 0.f;
+    const float e = __fmaf_rn(-lg, e_prev, mm[kk].x - __fmaf_rn(cprev, pk, pk));
+    update(a, lo, vv[kk], mm[kk], e);
+    if (kk + 1 < 8) lg = mm[kk].y * g[kk + 1];
+    cprev = mm[kk].z, e_prev = e, pk = pn;
+  }
+}
+}  // namespace k3w
+
 struct TcParams {
   const int32_t *slot_lc;
   const int32_t *slot_pc;
@@ -173,7 +226,7 @@ struct TcPlan {
   static_assert(MS >= 2 * GS + AS + DS, "metadata ring too short");  // (2 GS - PW) + AS + DS + 1
   static constexpr int MSTRIDE = (NPRE + 2) * SLOTS * 4;  // lc|flags, pc[NPRE], x per stage
   static constexpr int NABUF = SLOTS * 128;              // each consumer's next A row
-  static constexpr int VBUF = KB > 1 ? VS * SLOTS * (128 + 8) : 0;  // V rows + (lc|flags, x)
+  static constexpr int VBUF = KB > 1 ? CWARPS * 32 * 128 : 0;  // KB = 8: per-warp V transpose
   static constexpr size_t SMEM =
       1024 + 2 * B_BYTES + (size_t)GS * STAGE + MS * MSTRIDE + NABUF + VBUF + 256;
 };
@@ -212,7 +265,7 @@ __device__ __forceinline__ void cp16p(uint32_t dst, const void *src, bool on) {
 template <int NPRE, int GS, bool R32, bool COMP, int PW, int KB>
 __global__ void __launch_bounds__(tc_threads<PW, KB>(), 1) factor_rows_tc_kernel(const TcParams p) {
   constexpr int THREADS = tc_threads<PW, KB>(), NPW = 4 * PW;  // producer warps: 0 .. NPW - 1
-  constexpr int WCHAIN = NPW + CWARPS, WMMA = NPW + CWARPS + (KB > 1 ? CHAIN_WARPS : 0);
+  constexpr int WMMA = NPW + CWARPS;
   static_assert(GS % PW == 0, "each producer parity owns GS / PW ring stages");
   constexpr int D = GS / PW;                               // per-warp gather lookahead
   using P = TcPlan<NPRE, GS, KB>;
@@ -224,14 +277,12 @@ __global__ void __launch_bounds__(tc_threads<PW, KB>(), 1) factor_rows_tc_kernel
   const uint32_t ring = sbase + 2 * P::B_BYTES;
   const uint32_t meta = ring + GS * P::STAGE;
   const uint32_t nabuf = meta + P::MS * P::MSTRIDE;
-  const uint32_t vbuf = nabuf + P::NABUF;                  // KB > 1: [VS][128 entries][128 B]
-  const uint32_t vmeta = vbuf + VS * SLOTS * 128;          // KB > 1: [VS][8 k][16 rs] int2
+  const uint32_t vbuf = nabuf + P::NABUF;                  // KB > 1: [4 warps][32 rows][128 B]
   const uint32_t bars = nabuf + P::NABUF + P::VBUF;
   uint8_t *gbase = smraw + (sbase - sraw);
   uint64_t *a_ready = reinterpret_cast<uint64_t *>(gbase + (bars - sbase));
   uint64_t *a_free = a_ready + AS, *v_ready = a_free + AS, *d_free = v_ready + DS;
-  uint64_t *vfull = d_free + DS, *vempty = vfull + VS;     // KB > 1: staging ring
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(vempty + VS);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(d_free + DS);
     const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const int J = p.J, R = R32 ? 32 : p.R;
 
@@ -267,7 +318,6 @@ __global__ void __launch_bounds__(tc_threads<PW, KB>(), 1) factor_rows_tc_kernel
   if (tid == 0) {
     for (int k = 0; k < AS; ++k) mbar_init(a_ready + k, CWARPS), mbar_init(a_free + k, 1);
     for (int k = 0; k < DS; ++k) mbar_init(v_ready + k, 1), mbar_init(d_free + k, CWARPS);
-    for (int k = 0; k < VS; ++k) mbar_init(vfull + k, CWARPS), mbar_init(vempty + k, CHAIN_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // B tiles -> tensor core
@@ -553,75 +603,44 @@ __global__ void __launch_bounds__(tc_threads<PW, KB>(), 1) factor_rows_tc_kernel
       }
     }
     if (have) store_row();
-  } else if (w < WCHAIN) {  // ---- KB > 1, stagers: TMEM D -> shared-memory V rows ----
-    const int rs = s >> 3, k = s & 7;
-    const uint32_t myv = vbuf + (uint32_t)(s * 128);
-    const uint32_t swz = (uint32_t)(k ^ (rs & 7));  // chunk c of entry s at c ^ k ^ (rs & 7)
-#pragma unroll 1
-    for (int b = 0; b < nb; ++b) {
-      const int st = b % DS;
-      mbar_wait(v_ready + st, (b / DS) & 1);
-      tc_fence_after();
-      float v[32], v2[32];
-      tmem_ld32(tlane + 64 * AS + 64 * st, v);
-      tmem_ld32(tlane + 64 * AS + 64 * st + 32, v2);
-      const uint32_t mb0 = my_meta + (uint32_t)((b & (P::MS - 1)) * P::MSTRIDE);
-      const int mlc = (int)lds32(mb0);
-      const int mx = (int)lds32(mb0 + 4 * SLOTS * (1 + NPRE));
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(d_free + st);
-      const int vs = b % VS;
-      if (b >= VS) mbar_wait(vempty + vs, (b / VS - 1) & 1);
-      const uint32_t dst = myv + (uint32_t)(vs * SLOTS * 128);
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const float2 t0 = f2add(make_float2(v[4 * c], v[4 * c + 1]), make_float2(v2[4 * c], v2[4 * c + 1]));
-        const float2 t1 = f2add(make_float2(v[4 * c + 2], v[4 * c + 3]), make_float2(v2[4 * c + 2], v2[4 * c + 3]));
-        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};\n" ::"r"(dst + (((uint32_t)c ^ swz) << 4)),
-                     "f"(t0.x), "f"(t0.y), "f"(t1.x), "f"(t1.y)
-                     : "memory");
-      }
-      asm volatile("st.shared.v2.b32 [%0], {%1,%2};\n" ::"r"(vmeta + (uint32_t)((vs * SLOTS + k * 16 + rs) * 8)),
-                   "r"(mlc), "r"(mx)
-                   : "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(vfull + vs);
-    }
-  } else {  // ---- KB > 1, chain warps: 8 row slots each, 4 lanes per row (8 columns each) ----
-    // lane = 4 rl + qq: row slot rs = 8 (w - WCHAIN) + rl, columns 8 qq .. 8 qq + 7; the step's
-    // dot product reduces over the row's 4 lanes (two xor shuffles), as quad does over 8
-    const int rl = lane >> 2, qq = lane & 3;
-    const int rs = 8 * (w - WCHAIN) + rl;
+  } else {  // ---- KB = 8: consumers in the quad layout (4 row slots per warp, 8 lanes each) ----
+    // TMEM lane s = 32 q + lane holds leaf k = lane & 7 of row slot rs = 4 q + (lane >> 3).  The
+    // warp transposes its 32 V rows through 4 KB of shared memory (8 STS.128 + 8 LDS.128 per
+    // lane, swizzled chunk c of row r at c ^ (r & 7): conflict-free both ways), so that lane
+    // (rl, k) holds columns 4k .. 4k + 3 of all 8 leaves of its row, and runs the row's chain in
+    // the quad layout (sweep.cu quadw): dot products over 8 lanes (3 shuffle levels), one step of
+    // lookahead inside a batch (k3w::batch_la).  A batch containing a row start or padding (once
+    // per row) takes the checked per-step path.
+    const int rl = lane >> 3, k = lane & 7;
+    const int rs = 4 * q + rl;
     const int64_t gslots = (int64_t)gridDim.x * (SLOTS / KB);
     const float lr = p.lr, cdec = -p.lr * p.reg;
-    float a[8], lo[8];
+    float a[4], lo[4];
     int64_t row = ((int64_t)blockIdx.x + (int64_t)gridDim.x * rs) * p.nrows / gslots;
     bool have = false;
     int64_t cur_i = -1;
     int ci1 = row < p.nrows ? __ldg(p.row_coord + row) : -1;
     int ci2 = row + 1 < p.nrows ? __ldg(p.row_coord + row + 1) : -1;
-    const uint32_t my_na = nabuf + (uint32_t)(rs * 128 + 32 * qq);
-    const int j0 = 8 * qq;
+    const uint32_t my_na = nabuf + (uint32_t)(rs * 128 + 16 * k);
+    const int j0 = 4 * k;
+    const uint32_t tb = vbuf + (uint32_t)(q * 32 * 128);
     auto prefetch_row = [&](int ci) {
       if (ci >= 0) {
         const float *ar = p.A + (int64_t)ci * J + j0;
         if (J == 32) {
           cp16(my_na, ar);
-          cp16(my_na + 16, ar + 4);
         } else {
-          for (int j = 0; j < 8; ++j) cp4(my_na + 4 * j, ar + j, j0 + j < J);
+          for (int j = 0; j < 4; ++j) cp4(my_na + 4 * j, ar + j, j0 + j < J);
         }
       }
       cp_commit();
     };
     auto install_row = [&]() {
       cp_wait<0>();
-      const float4 q0 = lds128(my_na), q1 = lds128(my_na + 16);
+      const float4 q0 = lds128(my_na);
       a[0] = q0.x, a[1] = q0.y, a[2] = q0.z, a[3] = q0.w;
-      a[4] = q1.x, a[5] = q1.y, a[6] = q1.z, a[7] = q1.w;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < 4; ++j) {
         if (j0 + j >= J) a[j] = 0.f;
         lo[j] = 0.f;
       }
@@ -630,95 +649,79 @@ __global__ void __launch_bounds__(tc_threads<PW, KB>(), 1) factor_rows_tc_kernel
       float *ar = p.A + cur_i * J + j0;
       if (J == 32) {
         *reinterpret_cast<float4 *>(ar) = make_float4(a[0], a[1], a[2], a[3]);
-        *reinterpret_cast<float4 *>(ar + 4) = make_float4(a[4], a[5], a[6], a[7]);
       } else {
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
+        for (int j = 0; j < 4; ++j)
           if (j0 + j < J) ar[j] = a[j];
       }
     };
-    // this lane's 8 columns of leaf kk's V row: chunks 2 qq, 2 qq + 1 (swizzled c ^ kk ^ (rs & 7))
-    auto load_v = [&](float (&v)[8], int vs, int kk) {
-      const uint32_t src = vbuf + (uint32_t)((vs * SLOTS + 8 * rs + kk) * 128);
-      const uint32_t sw = (uint32_t)(kk ^ (rs & 7));
-      const float4 q0 = lds128(src + ((((uint32_t)(2 * qq)) ^ sw) << 4));
-      const float4 q1 = lds128(src + ((((uint32_t)(2 * qq + 1)) ^ sw) << 4));
-      v[0] = q0.x, v[1] = q0.y, v[2] = q0.z, v[3] = q0.w;
-      v[4] = q1.x, v[5] = q1.y, v[6] = q1.z, v[7] = q1.w;
-    };
 #pragma unroll
-    for (int j = 0; j < 8; ++j) a[j] = 0.f, lo[j] = 0.f;
+    for (int j = 0; j < 4; ++j) a[j] = 0.f, lo[j] = 0.f;
     prefetch_row(ci1);
 #pragma unroll 1
     for (int b = 0; b < nb; ++b) {
-      const int vs = b % VS;
-      mbar_wait(vfull + vs, (b / VS) & 1);
-      float vv[8][8];
-      uint2 mm[8];
+      const int st = b % DS;
+      mbar_wait(v_ready + st, (b / DS) & 1);
+      tc_fence_after();
+      float v[32], v2[32];
+      tmem_ld32(tlane + 64 * AS + 64 * st, v);
+      tmem_ld32(tlane + 64 * AS + 64 * st + 32, v2);
+      // the row's 8 entries of the metadata stage: leaf coordinate | flags and value
+      const uint32_t mb0 = meta + (uint32_t)((b & (P::MS - 1)) * P::MSTRIDE) + 4 * (8 * rs);
+      const int4 lc0 = *reinterpret_cast<const int4 *>(gbase + (mb0 - sbase));
+      const int4 lc1 = *reinterpret_cast<const int4 *>(gbase + (mb0 + 16 - sbase));
+      const uint32_t xb = mb0 + 4 * SLOTS * (1 + NPRE);
+      const float4 x0 = *reinterpret_cast<const float4 *>(gbase + (xb - sbase));
+      const float4 x1 = *reinterpret_cast<const float4 *>(gbase + (xb + 16 - sbase));
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(d_free + st);
+      // transpose: my leaf's V row (sum of the two TMEM halves) -> row 8 rl + k of the buffer
+      const uint32_t myrow = tb + (uint32_t)((8 * rl + k) * 128);
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {  // the batch's 8 V slices and step operands up front
-        load_v(vv[kk], vs, kk);
-        asm volatile("ld.shared.v2.b32 {%0,%1}, [%2];\n"
-                     : "=r"(mm[kk].x), "=r"(mm[kk].y)
-                     : "r"(vmeta + (uint32_t)((vs * SLOTS + kk * 16 + rs) * 8))
+      for (int c = 0; c < 8; ++c) {
+        const float2 t0 = f2add(make_float2(v[4 * c], v[4 * c + 1]), make_float2(v2[4 * c], v2[4 * c + 1]));
+        const float2 t1 = f2add(make_float2(v[4 * c + 2], v[4 * c + 3]), make_float2(v2[4 * c + 2], v2[4 * c + 3]));
+        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};\n" ::"r"(myrow + (((uint32_t)(c ^ k)) << 4)),
+                     "f"(t0.x), "f"(t0.y), "f"(t1.x), "f"(t1.y)
                      : "memory");
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(vempty + vs);  // the stage is free once read
-      // one leaf step; SLOW: with the row-start / padding checks (divergent), else the plain
-      // chain (no branches: the shuffles and FMAs issue back to back)
-      auto step = [&](int kk, bool slow) {
-        const int mlc = (int)mm[kk].x;
-        const bool live = !slow || mlc != PAD;  // the shuffles stay warp-uniform either way
-        if (slow && live && ((uint32_t)mlc & ROW_START)) {
-          if (have) {
-            store_row();
-            row += 1;
-            ci1 = ci2;
-            ci2 = row + 1 < p.nrows ? __ldg(p.row_coord + row + 1) : -1;
-          }
-          have = true;
-          cur_i = ci1;
-          install_row();
-          prefetch_row(ci2);
-        }
-        const float *v = vv[kk];
-        float2 s2 = f2fma(make_float2(a[0], a[1]), make_float2(v[0], v[1]), make_float2(0.f, 0.f));
-        s2 = f2fma(make_float2(a[2], a[3]), make_float2(v[2], v[3]), s2);
-        float2 t2 = f2fma(make_float2(a[4], a[5]), make_float2(v[4], v[5]), make_float2(0.f, 0.f));
-        t2 = f2fma(make_float2(a[6], a[7]), make_float2(v[6], v[7]), t2);
-        float dot = (s2.x + s2.y) + (t2.x + t2.y);
-        dot += __shfl_xor_sync(FULL, dot, 1);
-        dot += __shfl_xor_sync(FULL, dot, 2);
-        const float e = __uint_as_float(mm[kk].y) - dot;
-        const float le = live ? lr * e : 0.f;
-        const float cd = live ? cdec : 0.f;
-        const float2 l2 = make_float2(le, le), c2 = make_float2(cd, cd);
+      float4 vv[8];
 #pragma unroll
-        for (int j = 0; j < 8; j += 2) {
-          const float2 aj = make_float2(a[j], a[j + 1]), vj = make_float2(v[j], v[j + 1]);
-          if (COMP) {
-            const float2 d = f2fma(l2, vj, f2fma(c2, aj, make_float2(lo[j], lo[j + 1])));
-            const float2 t = f2add(aj, d);
-            const float2 r = f2sub(d, f2sub(t, aj));
-            a[j] = t.x, a[j + 1] = t.y, lo[j] = r.x, lo[j + 1] = r.y;
-          } else {
-            const float2 t = f2fma(l2, vj, f2fma(c2, aj, aj));
-            a[j] = t.x, a[j + 1] = t.y;
-          }
-        }
-      };
-      // a row start or padding anywhere in this warp's batch: the checked path (rare: once
-      // per row, and at the stream's end)
+      for (int i = 0; i < 8; ++i)
+        vv[i] = lds128(tb + (uint32_t)((8 * rl + i) * 128) + (((uint32_t)(k ^ i)) << 4));
+      __syncwarp();  // every lane's reads are done before the next batch's stores
+      const int lcs[8] = {lc0.x, lc0.y, lc0.z, lc0.w, lc1.x, lc1.y, lc1.z, lc1.w};
+      const float xs[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
       bool odd = false;
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) odd |= (int)mm[kk].x == PAD || ((uint32_t)mm[kk].x & ROW_START);
-      if (__any_sync(FULL, odd)) {
+      for (int i = 0; i < 8; ++i) odd |= lcs[i] == PAD || ((uint32_t)lcs[i] & ROW_START);
+      float4 mm[8];
+      if (!__any_sync(FULL, odd)) {
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) step(kk, true);
+        for (int i = 0; i < 8; ++i) mm[i] = make_float4(xs[i], lr, cdec, cdec);
+        k3w::batch_la(a, lo, vv, mm);
       } else {
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) step(kk, false);
+        for (int i = 0; i < 8; ++i) {
+          const bool live = lcs[i] != PAD;
+          if (live && ((uint32_t)lcs[i] & ROW_START)) {  // the row group's lanes together
+            if (have) {
+              store_row();
+              row += 1;
+              ci1 = ci2;
+              ci2 = row + 1 < p.nrows ? __ldg(p.row_coord + row + 1) : -1;
+            }
+            have = true;
+            cur_i = ci1;
+            install_row();
+            prefetch_row(ci2);
+          }
+          __syncwarp();
+          const float4 m = live ? make_float4(xs[i], lr, cdec, cdec) : make_float4(0.f, 0.f, 0.f, 0.f);
+          k3w::step(a, lo, vv[i], m);
+        }
       }
     }
     if (have) store_row();
@@ -919,10 +922,10 @@ int launch_factor_tc(const ft_tree_t *t, const ft_model_t *m, float lr, float re
                                     : t->num_rows > 0 && t->nnz / t->num_rows > 8192;
   if (t->slot_kb == 8) {  // few long rows, order 3 (slot_kb_for): 16 rows per CTA
     if (q.R == 32)
-      return comp ? launch_tc_k<1, 4, true, true, 1, 8>(q, t->slot_grid, s)
-                  : launch_tc_k<1, 4, true, false, 1, 8>(q, t->slot_grid, s);
-    return comp ? launch_tc_k<1, 4, false, true, 1, 8>(q, t->slot_grid, s)
-                : launch_tc_k<1, 4, false, false, 1, 8>(q, t->slot_grid, s);
+      return comp ? launch_tc_k<1, 4, true, true, 2, 8>(q, t->slot_grid, s)
+                  : launch_tc_k<1, 4, true, false, 2, 8>(q, t->slot_grid, s);
+    return comp ? launch_tc_k<1, 4, false, true, 2, 8>(q, t->slot_grid, s)
+                : launch_tc_k<1, 4, false, false, 2, 8>(q, t->slot_grid, s);
   }
   if (t->slot_kb != 1) return -1;
   if (N == 3) return launch_tc_t<1, 4>(q, t->slot_grid, comp, s);
@@ -952,10 +955,11 @@ int slot_kb_for(const ft_tree_t *t, int J, int R) {
       !tc_shape_ok(t->order, J, R))
     return 0;
   if (rows >= tc_min_rows()) return 1;
-  // K3c-wide (16 rows x 8 leaves per batch, the chains in two 4-lanes-per-row warps) is opt-in
-  // (FT_TC_WIDE=1): correct (tests/test_factor_tc_gpu.py), but its chain warps run each row's
-  // 8 steps per batch back to back and measured slower than quadw on Netflix mode 2 (9.6 vs
-  // 5.9 ms; profiles/r02_factor_tc_ab.md)
+  // K3c-wide (16 rows x 8 leaves per batch, the consumers transpose V through shared memory
+  // and run the chains in the quad layout with one step of lookahead) is opt-in
+  // (FT_TC_WIDE=1): correct (tests/test_factor_tc_gpu.py), but each batch's 8 dependent steps
+  // (~3,000 cycles per batch vs ~1,200 for K3c) bound it and it measured slower than quadw on Netflix mode 2
+  // (8.6 vs 6.0 ms; the earlier chain-warp form 9.6 ms; profiles/r02_factor_tc_ab.md)
   static const bool wide = [] {
     const char *e = getenv("FT_TC_WIDE");
     return e && strcmp(e, "1") == 0;

@@ -196,122 +196,6 @@ __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
 // serial updates (Netflix mode 2: 45 K) otherwise drift ~1e-4 from the fp64 reference
 // (tests/test_netflix_parity_gpu.py); the residue costs two packed adds per column pair, off
 // the serial dependency except one FADD.
-// a . v over a quarter (8 lanes x 4 columns): lane partial, 3-level butterfly
-__device__ __forceinline__ float quad_dot(const float (&a)[4], const float4 v) {
-  float2 pr = fmul2(make_float2(a[0], a[1]), make_float2(v.x, v.y));
-  pr = ffma2(make_float2(a[2], a[3]), make_float2(v.z, v.w), pr);
-  float s = pr.x + pr.y;
-  s += __shfl_xor_sync(FULL, s, 4);
-  s += __shfl_xor_sync(FULL, s, 2);
-  s += __shfl_xor_sync(FULL, s, 1);
-  return s;
-}
-// the compensated row update of quad_chain_step_vc for a given error e
-__device__ __forceinline__ void quad_update_c(float (&a)[4], float (&lo)[4], const float4 v,
-                                              float4 m, float e) {
-  const float2 l2 = make_float2(m.y * e, m.y * e), c2 = make_float2(m.z, m.w);
-  const float2 a01 = make_float2(a[0], a[1]), a23 = make_float2(a[2], a[3]);
-  const float2 d01 = ffma2(l2, make_float2(v.x, v.y), ffma2(c2, a01, make_float2(lo[0], lo[1])));
-  const float2 d23 = ffma2(l2, make_float2(v.z, v.w), ffma2(c2, a23, make_float2(lo[2], lo[3])));
-  const float2 t01 = fadd2(a01, d01), t23 = fadd2(a23, d23);
-  const float2 r01 = fsub2(d01, fsub2(t01, a01)), r23 = fsub2(d23, fsub2(t23, a23));
-  a[0] = t01.x, a[1] = t01.y, a[2] = t23.x, a[3] = t23.y;
-  lo[0] = r01.x, lo[1] = r01.y, lo[2] = r23.x, lo[3] = r23.y;
-}
-
-// One quarter batch (QB consecutive updates of one row) with ONE STEP OF LOOKAHEAD.  With
-// a_{k+1} = a_k + c_k a_k + lr_k e_k v_k (c_k = -lr_k reg; padding steps lr = c = 0),
-//     a_k . v_k = (1 + c_{k-1}) (a_{k-1} . v_k) + lr_{k-1} e_{k-1} (v_{k-1} . v_k),
-// so the butterfly for step k+1's dot p_{k+1} = a_k . v_{k+1} starts as soon as a_k exists, i.e.
-// while e_k is still being formed, and e_k = x_k - (1 + c_{k-1}) p_k - lr_{k-1} g_k e_{k-1} is
-// two FMAs after e_{k-1} (g_k = v_{k-1} . v_k: independent of the row, reduced up front).  The
-// serial path per step drops from dot + butterfly + update to about half of it (the butterfly
-// of one step overlaps the FMAs and update of the previous one).  Exact algebra, the reference's
-// order of updates; the batch's first step takes the direct dot (no state crosses batches).
-__device__ __forceinline__ void quad_batch_lookahead(float (&a)[4], float (&lo)[4],
-                                                     const float4 (&vv)[quad::QB],
-                                                     const float4 (&mm)[quad::QB]) {
-  using quad::QB;
-  float g[QB];  // g[k] = v_{k-1} . v_k (k >= 1)
-#pragma unroll
-  for (int k = 1; k < QB; ++k) {
-    float2 pr = fmul2(make_float2(vv[k - 1].x, vv[k - 1].y), make_float2(vv[k].x, vv[k].y));
-    pr = ffma2(make_float2(vv[k - 1].z, vv[k - 1].w), make_float2(vv[k].z, vv[k].w), pr);
-    g[k] = pr.x + pr.y;
-  }
-#pragma unroll
-  for (int msk = 4; msk >= 1; msk >>= 1)
-#pragma unroll
-    for (int k = 1; k < QB; ++k) g[k] += __shfl_xor_sync(FULL, g[k], msk);
-  float p = quad_dot(a, vv[0]);
-  float e_prev = 0.f, lg = 0.f, cprev = 0.f;
-#pragma unroll
-  for (int k = 0; k < QB; ++k) {
-    const float pn = k + 1 < QB ? quad_dot(a, vv[k + 1]) : 0.f;  // a = a_k (before the update)
-    const float ap = __fmaf_rn(cprev, p, p);
-    const float e = __fmaf_rn(-lg, e_prev, mm[k].x - ap);
-    quad_update_c(a, lo, vv[k], mm[k], e);
-    if (k + 1 < QB) lg = mm[k].y * g[k + 1];
-    cprev = mm[k].z, e_prev = e, p = pn;
-  }
-}
-
-// ... with TWO steps of lookahead: p_k = a_{k-2} . v_k (issued when a_{k-2} exists), and
-//     a_k . v_k = (1 + c_{k-1}) (1 + c_{k-2}) p_k + (1 + c_{k-1}) lr_{k-2} e_{k-2} (v_{k-2} . v_k)
-//                 + lr_{k-1} e_{k-1} (v_{k-1} . v_k),
-// so one butterfly spans three steps of the serial path.  Steps 0 and 1 of a batch use the
-// direct / one-step forms from a_0.
-__device__ __forceinline__ void quad_batch_lookahead2(float (&a)[4], float (&lo)[4],
-                                                      const float4 (&vv)[quad::QB],
-                                                      const float4 (&mm)[quad::QB]) {
-  using quad::QB;
-  float g1[QB], g2[QB];  // g1[k] = v_{k-1} . v_k (k >= 1), g2[k] = v_{k-2} . v_k (k >= 2)
-  g1[0] = g2[0] = g2[1] = 0.f;
-#pragma unroll
-  for (int k = 1; k < QB; ++k) {
-    float2 pr = fmul2(make_float2(vv[k - 1].x, vv[k - 1].y), make_float2(vv[k].x, vv[k].y));
-    pr = ffma2(make_float2(vv[k - 1].z, vv[k - 1].w), make_float2(vv[k].z, vv[k].w), pr);
-    g1[k] = pr.x + pr.y;
-    if (k >= 2) {
-      float2 qr = fmul2(make_float2(vv[k - 2].x, vv[k - 2].y), make_float2(vv[k].x, vv[k].y));
-      qr = ffma2(make_float2(vv[k - 2].z, vv[k - 2].w), make_float2(vv[k].z, vv[k].w), qr);
-      g2[k] = qr.x + qr.y;
-    }
-  }
-#pragma unroll
-  for (int msk = 4; msk >= 1; msk >>= 1)
-#pragma unroll
-    for (int k = 1; k < QB; ++k) {
-      g1[k] += __shfl_xor_sync(FULL, g1[k], msk);
-      if (k >= 2) g2[k] += __shfl_xor_sync(FULL, g2[k], msk);
-    }
-  float pk = quad_dot(a, vv[0]), pk1 = quad_dot(a, vv[1]);  // p_k, p_{k+1}
-  float e1 = 0.f, e2 = 0.f;        // e_{k-1}, e_{k-2}
-  float c1 = 0.f, c2 = 0.f;        // c_{k-1}, c_{k-2}
-  float l1 = 0.f, l2 = 0.f;        // lr_{k-1}, lr_{k-2}
-#pragma unroll
-  for (int k = 0; k < QB; ++k) {
-    // p_{k+2} = a_k . v_{k+2} from the current row state (before step k's update)
-    const float pn = k + 2 < QB ? quad_dot(a, vv[k + 2]) : 0.f;
-    float e;
-    if (k == 0) {
-      e = mm[0].x - pk;
-    } else if (k == 1) {
-      e = __fmaf_rn(-l1 * g1[1], e1, mm[1].x - __fmaf_rn(c1, pk, pk));
-    } else {
-      const float d12 = __fmaf_rn(c1, c2, c1 + c2);           // (1 + c1)(1 + c2) - 1
-      const float t2 = __fmaf_rn(c1, l2, l2) * g2[k];           // (1 + c1) lr_{k-2} g2
-      const float part = mm[k].x - __fmaf_rn(d12, pk, pk) - t2 * e2;
-      e = __fmaf_rn(-l1 * g1[k], e1, part);
-    }
-    quad_update_c(a, lo, vv[k], mm[k], e);
-    e2 = e1, e1 = e;
-    c2 = c1, c1 = mm[k].z;
-    l2 = l1, l1 = mm[k].y;
-    pk = pk1, pk1 = pn;
-  }
-}
-
 __device__ __forceinline__ void quad_chain_step_vc(float (&a)[4], float (&lo)[4], const float4 v,
                                                    float4 m) {
   float2 pr = fmul2(make_float2(a[0], a[1]), make_float2(v.x, v.y));
@@ -1036,14 +920,8 @@ __global__ void __launch_bounds__(quadw::Cfg<NP>::THREADS, NP <= 2 ? 4 : 1)
         }
         __syncwarp();
         mbar_arrive(empty + st);  // the stage is free once read
-        if (p.quadw_la == 2) {
-          quad_batch_lookahead2(a, lo, vv, mm);
-        } else if (p.quadw_la == 1) {
-          quad_batch_lookahead(a, lo, vv, mm);
-        } else {
 #pragma unroll
-          for (int kk = 0; kk < QB; ++kk) quad_chain_step_vc(a, lo, vv[kk], mm[kk]);
-        }
+        for (int kk = 0; kk < QB; ++kk) quad_chain_step_vc(a, lo, vv[kk], mm[kk]);
       }
     } else {
       // Gram form, software-pipelined: batch t + 1's stage is waited for, read into the other
@@ -1194,15 +1072,7 @@ int launch_quadw_s(const SweepParams &q, cudaStream_t s) {
   int rpg = 4;
   while (rpg > 1 && (q.nrows + rpg / 2 - 1) / (rpg / 2) <= sms) rpg /= 2;
   const bool few = (q.nrows + 3) / 4 <= sms;
-  static const int la = [] {
-    const char *e = getenv("FT_QUADW_LA");
-    return e ? atoi(e) : 1;
-  }();
-  if (forced == 0 || (forced < 0 && !few)) {
-    SweepParams q2 = q;
-    q2.quadw_la = la;
-    return launch_quadw_t<SMALL, 2, false, NPRE>(q2, 4, s);
-  }
+  if (forced == 0 || (forced < 0 && !few)) return launch_quadw_t<SMALL, 2, false, NPRE>(q, 4, s);
   return launch_quadw_t<SMALL, 6, true, NPRE>(q, few ? rpg : 4, s);
 }
 

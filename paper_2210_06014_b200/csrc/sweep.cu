@@ -66,7 +66,6 @@ struct SweepParams {
   float *partials;   // core: [grid][R*J]
   int64_t gather_bytes;  // bytes of the gathered C matrices (modes other than u)
   int quadw_rpg;         // quadw: rows per warp group (0: 4)
-  int quadw_la;          // quadw per-step form: one step of lookahead (quad_batch_lookahead)
 };
 
 // Fiber index of each of the batch's leaves (lane k -> leaf L0+k), given fcur = fiber holding

@@ -99,14 +99,12 @@ print('ok')
     ((4000, 300, 50), 500_000, 16, 12, 2e-3),     # J <= 16 (one m-tile), R = 12 (two k-tiles)
     ((2000, 300, 40, 25), 400_000, 32, 32, 2e-3),  # order 4 (two prefix levels), 10-16 K-update rows
 ])
-@pytest.mark.parametrize("kernel", ["quadr", "quadr-stagedcore", "quadw", "quadw-gram", "quadw-chain",
-                                    "quadw-chain0", "quadw-chain2"])
+@pytest.mark.parametrize("kernel", ["quadr", "quadr-stagedcore", "quadw", "quadw-gram", "quadw-chain"])
 def test_quad_sweeps_match_oracle(kernel, dims, nnz, J, R, lr):
     """-stagedcore: the K4 quad core with cp.async-staged gathers (FT_CORE_DIRECT=0; the default
     above 64 MB of gathered C rows) instead of direct register loads.  quadw picks its form by
     the row count (the Gram / segment form for few rows, the per-step chain otherwise);
-    -gram / -chain force one form on every mode (FT_QUADW_GRAM); -chain0 / -chain2: the
-    per-step chain without lookahead / with two steps of it (FT_QUADW_LA)."""
+    -gram / -chain force one form on every mode (FT_QUADW_GRAM)."""
     code = _CASE.format(dims=dims, nnz=nnz, J=J, R=R, lr=lr, seed=7)
     env = dict(os.environ, FT_FACTOR_KERNEL=kernel.split("-")[0])
     env.pop("FT_CORE_KERNEL", None)
@@ -114,8 +112,6 @@ def test_quad_sweeps_match_oracle(kernel, dims, nnz, J, R, lr):
         env.update(FT_CORE_DIRECT="0")
     if kernel.startswith("quadw-"):
         env.update(FT_QUADW_GRAM="1" if kernel.endswith("-gram") else "0")
-        if kernel[-1] in "02":
-            env.update(FT_QUADW_LA=kernel[-1])
     out = subprocess.run([sys.executable, "-c", code], cwd=REPO, env=env, capture_output=True,
                          text=True, timeout=900)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]

@@ -170,33 +170,6 @@ __device__ __forceinline__ void update(float (&a)[4], float (&lo)[4], const floa
 __device__ __forceinline__ void step(float (&a)[4], float (&lo)[4], const float4 v, float4 m) {
   update(a, lo, v, m, m.x - dot(a, v));
 }
-// 8 consecutive updates of one row with one step of lookahead (quad.cuh quad_batch_lookahead):
-// e_k = x_k - (1 + c_{k-1}) (a_{k-1} . v_k) - lr_{k-1} (v_{k-1} . v_k) e_{k-1}
-__device__ __forceinline__ void batch_la(float (&a)[4], float (&lo)[4], const float4 (&vv)[8],
-                                         const float4 (&mm)[8]) {
-  float g[8];
-#pragma unroll
-  for (int kk = 1; kk < 8; ++kk) {
-    float2 pr = f2fma(make_float2(vv[kk - 1].x, vv[kk - 1].y), make_float2(vv[kk].x, vv[kk].y),
-                      make_float2(0.f, 0.f));
-    pr = f2fma(make_float2(vv[kk - 1].z, vv[kk - 1].w), make_float2(vv[kk].z, vv[kk].w), pr);
-    g[kk] = pr.x + pr.y;
-  }
-#pragma unroll
-  for (int msk = 4; msk >= 1; msk >>= 1)
-#pragma unroll
-    for (int kk = 1; kk < 8; ++kk) g[kk] += __shfl_xor_sync(FULL, g[kk], msk);
-  float pk = dot(a, vv[0]);
-  float e_prev = 0.f, lg = 0.f, cprev = 0.f;
-#pragma unroll
-  for (int kk = 0; kk < 8; ++kk) {
-    const float pn = kk + 1 < 8 ? dot(a, vv[kk + 1]) : 0.f;
-    const float e = __fmaf_rn(-lg, e_prev, mm[kk].x - __fmaf_rn(cprev, pk, pk));
-    update(a, lo, vv[kk], mm[kk], e);
-    if (kk + 1 < 8) lg = mm[kk].y * g[kk + 1];
-    cprev = mm[kk].z, e_prev = e, pk = pn;
-  }
-}
 }  // namespace k3w
 
 struct TcParams {
@@ -608,9 +581,11 @@ __global__ void __launch_bounds__(tc_threads<PW, KB>(), 1) factor_rows_tc_kernel
     // warp transposes its 32 V rows through 4 KB of shared memory (8 STS.128 + 8 LDS.128 per
     // lane, swizzled chunk c of row r at c ^ (r & 7): conflict-free both ways), so that lane
     // (rl, k) holds columns 4k .. 4k + 3 of all 8 leaves of its row, and runs the row's chain in
-    // the quad layout (sweep.cu quadw): dot products over 8 lanes (3 shuffle levels), one step of
-    // lookahead inside a batch (k3w::batch_la).  A batch containing a row start or padding (once
-    // per row) takes the checked per-step path.
+    // the quad layout (sweep.cu quadw): dot products over 8 lanes (3 shuffle levels).  A batch
+    // containing a row start or padding (once per row) takes the checked per-step path.
+    // (Measured: shared-memory / MIO-bound with the producers' gathers -- the producers spin on
+    // a_free 38 % of the samples, and one step of lookahead in the chain changed nothing:
+    // profiles/r02_factor_tc_ab.md.)
     const int rl = lane >> 3, k = lane & 7;
     const int rs = 4 * q + rl;
     const int64_t gslots = (int64_t)gridDim.x * (SLOTS / KB);
@@ -701,7 +676,8 @@ __global__ void __launch_bounds__(tc_threads<PW, KB>(), 1) factor_rows_tc_kernel
       if (!__any_sync(FULL, odd)) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) mm[i] = make_float4(xs[i], lr, cdec, cdec);
-        k3w::batch_la(a, lo, vv, mm);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) k3w::step(a, lo, vv[i], mm[i]);
       } else {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -956,10 +932,11 @@ int slot_kb_for(const ft_tree_t *t, int J, int R) {
     return 0;
   if (rows >= tc_min_rows()) return 1;
   // K3c-wide (16 rows x 8 leaves per batch, the consumers transpose V through shared memory
-  // and run the chains in the quad layout with one step of lookahead) is opt-in
-  // (FT_TC_WIDE=1): correct (tests/test_factor_tc_gpu.py), but each batch's 8 dependent steps
-  // (~3,000 cycles per batch vs ~1,200 for K3c) bound it and it measured slower than quadw on Netflix mode 2
-  // (8.6 vs 6.0 ms; the earlier chain-warp form 9.6 ms; profiles/r02_factor_tc_ab.md)
+  // and run the chains in the quad layout) is opt-in (FT_TC_WIDE=1): correct
+  // (tests/test_factor_tc_gpu.py), but its consumers need ~3,000 cycles per batch (vs ~1,200
+  // for K3c's production; shared-memory pipe contention) and it measured slower than quadw on
+  // Netflix mode 2 (8.4 vs 6.0 ms; the earlier chain-warp form 9.6 ms;
+  // profiles/r02_factor_tc_ab.md)
   static const bool wide = [] {
     const char *e = getenv("FT_TC_WIDE");
     return e && strcmp(e, "1") == 0;

@@ -50,6 +50,10 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
   return *reinterpret_cast<float2 *>(&d);
 }
 
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ void cp_async16_s(uint32_t dst, const float *src) {
   // .ca: the leaf-level C rows of a sweep are often a small matrix (Netflix C_2: 280 KB) that
   // stays L1-resident -- measured .cg (L2 only): core sweep modes 0/1 3.2 -> 4.2-4.6 ms
@@ -83,6 +87,22 @@ __device__ __forceinline__ void quad_afrag_init(const SweepParams &p, uint4 *afr
     afr[f] = make_uint4(hv[0], hv[1], hv[2], hv[3]);
     afr[KT * MT * 32 + f] = make_uint4(lv[0], lv[1], lv[2], lv[3]);
   }
+}
+
+// ... one lane's (kt, mt) quads straight into registers (quadw DB: no shared-memory copy)
+__device__ __forceinline__ void quad_afrag_lane(const SweepParams &p, int kt, int mt, int ll,
+                                                uint4 &ah, uint4 &al) {
+  const int g = ll >> 2, t = ll & 3;
+  uint32_t hv[4], lv[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int r = 8 * kt + 2 * t + (e >> 1), j = 16 * mt + g + 8 * (e & 1);
+    const float bv = (r < p.R && j < p.J) ? __ldg(p.Bt + r * p.J + j) : 0.f;
+    hv[e] = to_tf32(bv);
+    lv[e] = to_tf32(bv - __uint_as_float(hv[e]));
+  }
+  ah = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+  al = make_uint4(lv[0], lv[1], lv[2], lv[3]);
 }
 
 // One k-tile of the transposed combine for n-tiles [nt0, nt0 + NN): acc[mt][nt] += Bt^T * cross^T,
@@ -196,6 +216,66 @@ __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
 // serial updates (Netflix mode 2: 45 K) otherwise drift ~1e-4 from the fp64 reference
 // (tests/test_netflix_parity_gpu.py); the residue costs two packed adds per column pair, off
 // the serial dependency except one FADD.
+// a . v over a quarter (8 lanes x 4 columns): lane partial, 3-level butterfly
+__device__ __forceinline__ float quad_dot(const float (&a)[4], const float4 v) {
+  float2 pr = fmul2(make_float2(a[0], a[1]), make_float2(v.x, v.y));
+  pr = ffma2(make_float2(a[2], a[3]), make_float2(v.z, v.w), pr);
+  float s = pr.x + pr.y;
+  s += __shfl_xor_sync(FULL, s, 4);
+  s += __shfl_xor_sync(FULL, s, 2);
+  s += __shfl_xor_sync(FULL, s, 1);
+  return s;
+}
+// the compensated row update of quad_chain_step_vc for a given error e
+__device__ __forceinline__ void quad_update_c(float (&a)[4], float (&lo)[4], const float4 v,
+                                              float4 m, float e) {
+  const float2 l2 = make_float2(m.y * e, m.y * e), c2 = make_float2(m.z, m.w);
+  const float2 a01 = make_float2(a[0], a[1]), a23 = make_float2(a[2], a[3]);
+  const float2 d01 = ffma2(l2, make_float2(v.x, v.y), ffma2(c2, a01, make_float2(lo[0], lo[1])));
+  const float2 d23 = ffma2(l2, make_float2(v.z, v.w), ffma2(c2, a23, make_float2(lo[2], lo[3])));
+  const float2 t01 = fadd2(a01, d01), t23 = fadd2(a23, d23);
+  const float2 r01 = fsub2(d01, fsub2(t01, a01)), r23 = fsub2(d23, fsub2(t23, a23));
+  a[0] = t01.x, a[1] = t01.y, a[2] = t23.x, a[3] = t23.y;
+  lo[0] = r01.x, lo[1] = r01.y, lo[2] = r23.x, lo[3] = r23.y;
+}
+
+// One quarter batch (QB consecutive updates of one row) with ONE STEP OF LOOKAHEAD.  With
+// a_{k+1} = a_k + c_k a_k + lr_k e_k v_k (c_k = -lr_k reg; padding steps lr = c = 0),
+//     a_k . v_k = (1 + c_{k-1}) (a_{k-1} . v_k) + lr_{k-1} e_{k-1} (v_{k-1} . v_k),
+// so the butterfly for step k+1's dot p_{k+1} = a_k . v_{k+1} starts as soon as a_k exists, i.e.
+// while e_k is still being formed, and e_k = x_k - (1 + c_{k-1}) p_k - lr_{k-1} g_k e_{k-1} is
+// two FMAs after e_{k-1} (g_k = v_{k-1} . v_k: independent of the row, reduced up front).  The
+// serial path per step drops from dot + butterfly + update to about half of it (the butterfly
+// of one step overlaps the FMAs and update of the previous one).  Exact algebra, the reference's
+// order of updates; the batch's first step takes the direct dot (no state crosses batches).
+__device__ __forceinline__ void quad_batch_lookahead(float (&a)[4], float (&lo)[4],
+                                                     const float4 (&vv)[quad::QB],
+                                                     const float4 (&mm)[quad::QB]) {
+  using quad::QB;
+  float g[QB];  // g[k] = v_{k-1} . v_k (k >= 1)
+#pragma unroll
+  for (int k = 1; k < QB; ++k) {
+    float2 pr = fmul2(make_float2(vv[k - 1].x, vv[k - 1].y), make_float2(vv[k].x, vv[k].y));
+    pr = ffma2(make_float2(vv[k - 1].z, vv[k - 1].w), make_float2(vv[k].z, vv[k].w), pr);
+    g[k] = pr.x + pr.y;
+  }
+#pragma unroll
+  for (int msk = 4; msk >= 1; msk >>= 1)
+#pragma unroll
+    for (int k = 1; k < QB; ++k) g[k] += __shfl_xor_sync(FULL, g[k], msk);
+  float p = quad_dot(a, vv[0]);
+  float e_prev = 0.f, lg = 0.f, cprev = 0.f;
+#pragma unroll
+  for (int k = 0; k < QB; ++k) {
+    const float pn = k + 1 < QB ? quad_dot(a, vv[k + 1]) : 0.f;  // a = a_k (before the update)
+    const float ap = __fmaf_rn(cprev, p, p);
+    const float e = __fmaf_rn(-lg, e_prev, mm[k].x - ap);
+    quad_update_c(a, lo, vv[k], mm[k], e);
+    if (k + 1 < QB) lg = mm[k].y * g[k + 1];
+    cprev = mm[k].z, e_prev = e, p = pn;
+  }
+}
+
 __device__ __forceinline__ void quad_chain_step_vc(float (&a)[4], float (&lo)[4], const float4 v,
                                                    float4 m) {
   float2 pr = fmul2(make_float2(a[0], a[1]), make_float2(v.x, v.y));
@@ -600,21 +680,25 @@ __device__ __forceinline__ Leaf<NPRE> load_leaf(const SweepParams &p, const Rec 
 // 3 shuffles + update) to one butterfly + 7 FMAs: what bounds the sweep when few rows share an
 // SM (the row-sharded multi-GPU epoch) -- tools/time_shards.py.
 namespace quadw {
-template <int NP>
+// DB: the double-buffered per-step form (order 3): two X / Y tile pairs per producer, a 2-stage
+// ring, the Bt^T fragments built straight into registers (no shared-memory copy)
+template <int NP, bool DB = false>
 struct Cfg {
-  static constexpr int NS = NP <= 2 ? 4 : 2 * NP;  // ring stages (producer k writes k, k + NP, ..)
+  static constexpr int NS = DB ? 2 : NP <= 2 ? 4 : 2 * NP;  // ring stages (producer k writes k, k + NP, ..)
   static constexpr int VREG = 32 * quad::QVS + 32;  // V tile
   // stage: V [32][QVS] | meta float4 [4][MQ] | info int4 [4] | A rows [4][32] |
   //        GRAM: per quarter T [28] + x [8] + pad [4]
   static constexpr int META = VREG, INFO = META + 4 * quad::MQ * 4, AROW = INFO + 16,
                        TCOEF = AROW + 4 * 32, TQ = 40;
   static constexpr int STAGE_FLOATS = TCOEF + 4 * TQ;
-  // ring + X, Y per producer
-  static constexpr int GROUP_FLOATS = NS * STAGE_FLOATS + NP * 2 * quad::TILE;
+  // ring + X, Y per producer (two pairs when DB)
+  static constexpr int XY_FLOATS = (DB ? 4 : 2) * quad::TILE;
+  static constexpr int GROUP_FLOATS = NS * STAGE_FLOATS + NP * XY_FLOATS;
   static constexpr int BAR_BYTES = 2 * NS * 8 + 16;
+  static constexpr int FRAG_BYTES = DB ? 0 : quad::BFRAG_U4 * 16;
   static constexpr int THREADS = (NP + 1) * 32;
   static constexpr size_t bytes() {
-    return (size_t)quad::BFRAG_U4 * 16 + BAR_BYTES + (size_t)GROUP_FLOATS * 4;
+    return (size_t)FRAG_BYTES + BAR_BYTES + (size_t)GROUP_FLOATS * 4;
   }
 };
 // position of T_ik (i < k) in a quarter's packed 28-float block: rows i = 0..6, columns k > i
@@ -679,30 +763,31 @@ __device__ __forceinline__ void quadw_gram(const float *V, float *T, const int (
   }
 }
 
-template <bool SMALL, int NP, bool GRAM, int NPRE>
-__global__ void __launch_bounds__(quadw::Cfg<NP>::THREADS, NP <= 2 ? 4 : 1)
+template <bool SMALL, int NP, bool GRAM, int NPRE, bool DB = false>
+__global__ void __launch_bounds__(quadw::Cfg<NP, DB>::THREADS, NP <= 2 ? 4 : 1)
     factor_rows_quadw_kernel(const SweepParams p) {
   using namespace quad;
   using Leaf = quadp::Leaf<NPRE>;
   using quadp::Rec;
-  using C = quadw::Cfg<NP>;
+  using C = quadw::Cfg<NP, DB>;
+  static_assert(!DB || (NPRE == 1 && !GRAM), "DB: the order-3 per-step form");
   extern __shared__ float4 smem4[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;  // w 0: consumer, 1..NP: producers
   const int q = lane >> 3, l = lane & 7;
   uint4 *afr = reinterpret_cast<uint4 *>(smem4);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(afr + BFRAG_U4);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(smem4) + C::FRAG_BYTES);
   uint64_t *full = bars, *empty = bars + C::NS;
-  float *ring = reinterpret_cast<float *>(reinterpret_cast<char *>(afr + BFRAG_U4) + C::BAR_BYTES);
+  float *ring = reinterpret_cast<float *>(reinterpret_cast<char *>(bars) + C::BAR_BYTES);
   if (w > 0) {
-    float *tiles = ring + C::NS * C::STAGE_FLOATS + (w - 1) * 2 * TILE;
-    for (int k = lane; k < 2 * TILE; k += 32) tiles[k] = 0.f;
+    float *tiles = ring + C::NS * C::STAGE_FLOATS + (w - 1) * C::XY_FLOATS;
+    for (int k = lane; k < C::XY_FLOATS; k += 32) tiles[k] = 0.f;
   }
   if (threadIdx.x == 0)
     for (int st = 0; st < C::NS; ++st) {
       mbar_init(full + st, 32);
       mbar_init(empty + st, 32);
     }
-  quad_afrag_init(p, afr);
+  if (!DB) quad_afrag_init(p, afr);
   __syncthreads();
   // m-tiles (j) / k-tiles (r) in use: compile-time (SMALL: J <= 16 and R <= 16), so the
   // unrolled combine keeps no runtime guards; other shapes compute their zero padding
@@ -734,7 +819,7 @@ __global__ void __launch_bounds__(quadw::Cfg<NP>::THREADS, NP <= 2 ? 4 : 1)
   if (w > 0) {
     // ===================================== producers =====================================
     const int k = w - 1;  // this producer runs batches t = k, k + NP, ...
-    float *X = ring + C::NS * C::STAGE_FLOATS + k * 2 * TILE, *Y = X + TILE;
+    float *X = ring + C::NS * C::STAGE_FLOATS + k * C::XY_FLOATS, *Y = X + TILE;
     const int64_t nstream = (int64_t)gridDim.x * rpg;
     quadp::Cursor cur;
     cur.row = (int64_t)q * gridDim.x + blockIdx.x - nstream;
@@ -826,27 +911,17 @@ __global__ void __launch_bounds__(quadw::Cfg<NP>::THREADS, NP <= 2 ? 4 : 1)
     for (int kt = 0; kt < KT; ++kt)
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
-        AH[kt][mt] = afr[(mt * KT + kt) * 32 + lane];
-        AL[kt][mt] = afr[KT * MT * 32 + (mt * KT + kt) * 32 + lane];
+        if (DB) {
+          quad_afrag_lane(p, kt, mt, lane, AH[kt][mt], AL[kt][mt]);
+        } else {
+          AH[kt][mt] = afr[(mt * KT + kt) * 32 + lane];
+          AL[kt][mt] = afr[KT * MT * 32 + (mt * KT + kt) * 32 + lane];
+        }
       }
     for (int s = 0; s < k; ++s) (void)quadp::next_batch(p, cur, nstream);
-    Rec r0 = next_mine(true);
-    Leaf d0 = quadp::load_leaf<NPRE>(p, r0, l);
-    float4 av0 = load_arow(r0);
     float acc[2][4][4];
-    for (int t = k;; t += NP) {
-      const bool stop = !__any_sync(FULL, r0.nb > 0);
-      if (!stop) gather(d0);
-      const Rec r1 = next_mine(false);  // my next batch: indices and A values fly meanwhile
-      const Leaf d1 = quadp::load_leaf<NPRE>(p, r1, l);
-      const float4 av1 = load_arow(r1);
-      if (!stop) {
-        gather_finish(d0);
-        quad_zero(acc);
-#pragma unroll
-        for (int kt = 0; kt < KT; ++kt)
-          if (kt < nkt) quad_mma_kt_r<NT>(X, Y, AH[kt], AL[kt], kt, 0, lane, acc, mts);
-      }
+    // publish batch t (V, step operands, row start / stop record) into ring stage t % NS
+    auto publish = [&](int t, bool stop, const Rec &r0, const Leaf &d0, const float4 &av0) {
       const int st = t % C::NS;
       if (t >= C::NS) mbar_wait(empty + st, ((t / C::NS) - 1) & 1);
       int4 *info = stage_info(st);
@@ -870,8 +945,77 @@ __global__ void __launch_bounds__(quadw::Cfg<NP>::THREADS, NP <= 2 ? 4 : 1)
       }
       __syncwarp();
       mbar_arrive(full + st);
-      if (stop) break;
-      r0 = r1, d0 = d1, av0 = av1;
+    };
+    if (DB) {
+      // double-buffered: the gathers of my next batch go into the other X / Y pair at the top
+      // of the iteration and fly under this batch's combine and publication (two cp.async
+      // groups in flight); leaf records two batches ahead
+      const uint32_t tile2 = (uint32_t)(2 * TILE * 4);  // bytes between the two X / Y pairs
+      auto gather_into = [&](int b, const Leaf &d) {
+        const uint32_t off = b ? tile2 : 0u;
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int s = 4 * it + gs;
+          const int pcs = __shfl_sync(FULL, d.pc[0], s), lcs = __shfl_sync(FULL, d.lc, s);
+          if (gok) {
+            cp_async16_s(xs + off + it * 4 * XS * 4, cpre + pcs * Rs);
+            cp_async16_s(ys + off + it * 4 * XS * 4, cleaf + lcs * Rs);
+          }
+        }
+        cp_async_commit();
+      };
+      Rec r0 = next_mine(true);
+      Leaf d0 = quadp::load_leaf<NPRE>(p, r0, l);
+      float4 av0 = load_arow(r0);
+      bool stop0 = !__any_sync(FULL, r0.nb > 0);
+      if (!stop0) gather_into(0, d0);
+      Rec r1 = next_mine(false);
+      Leaf d1 = quadp::load_leaf<NPRE>(p, r1, l);
+      float4 av1 = load_arow(r1);
+      int buf = 0;
+      for (int t = k;; t += NP) {
+        const bool stop1 = !__any_sync(FULL, r1.nb > 0);
+        if (!stop0 && !stop1) gather_into(buf ^ 1, d1);
+        const Rec r2 = next_mine(false);
+        const Leaf d2 = quadp::load_leaf<NPRE>(p, r2, l);
+        const float4 av2 = load_arow(r2);
+        if (!stop0) {
+          if (!stop1) cp_async_wait_group<1>();
+          else cp_async_wait_all();
+          __syncwarp();
+          const float *Xb = X + (buf ? 2 * TILE : 0), *Yb = Y + (buf ? 2 * TILE : 0);
+          quad_zero(acc);
+#pragma unroll
+          for (int kt = 0; kt < KT; ++kt)
+            if (kt < nkt) quad_mma_kt_r<NT>(Xb, Yb, AH[kt], AL[kt], kt, 0, lane, acc, mts);
+        }
+        publish(t, stop0, r0, d0, av0);  // ends in __syncwarp: X / Y [buf] are free again
+        if (stop0) break;
+        r0 = r1, d0 = d1, av0 = av1, stop0 = stop1;
+        r1 = r2, d1 = d2, av1 = av2;
+        buf ^= 1;
+      }
+    } else {
+      Rec r0 = next_mine(true);
+      Leaf d0 = quadp::load_leaf<NPRE>(p, r0, l);
+      float4 av0 = load_arow(r0);
+      for (int t = k;; t += NP) {
+        const bool stop = !__any_sync(FULL, r0.nb > 0);
+        if (!stop) gather(d0);
+        const Rec r1 = next_mine(false);  // my next batch: indices and A values fly meanwhile
+        const Leaf d1 = quadp::load_leaf<NPRE>(p, r1, l);
+        const float4 av1 = load_arow(r1);
+        if (!stop) {
+          gather_finish(d0);
+          quad_zero(acc);
+#pragma unroll
+          for (int kt = 0; kt < KT; ++kt)
+            if (kt < nkt) quad_mma_kt_r<NT>(X, Y, AH[kt], AL[kt], kt, 0, lane, acc, mts);
+        }
+        publish(t, stop, r0, d0, av0);
+        if (stop) break;
+        r0 = r1, d0 = d1, av0 = av1;
+      }
     }
     cp_async_wait_all();
   } else {
@@ -920,8 +1064,12 @@ __global__ void __launch_bounds__(quadw::Cfg<NP>::THREADS, NP <= 2 ? 4 : 1)
         }
         __syncwarp();
         mbar_arrive(empty + st);  // the stage is free once read
+        if (DB) {  // one step of lookahead: the chain at about half the serial latency
+          quad_batch_lookahead(a, lo, vv, mm);
+        } else {
 #pragma unroll
-        for (int kk = 0; kk < QB; ++kk) quad_chain_step_vc(a, lo, vv[kk], mm[kk]);
+          for (int kk = 0; kk < QB; ++kk) quad_chain_step_vc(a, lo, vv[kk], mm[kk]);
+        }
       }
     } else {
       // Gram form, software-pipelined: batch t + 1's stage is waited for, read into the other
@@ -1032,12 +1180,12 @@ __global__ void __launch_bounds__(quadw::Cfg<NP>::THREADS, NP <= 2 ? 4 : 1)
   }
 }
 
-template <bool SMALL, int NP, bool GRAM, int NPRE>
+template <bool SMALL, int NP, bool GRAM, int NPRE, bool DB = false>
 int launch_quadw_t(const SweepParams &q0, int rpg, cudaStream_t s) {
   SweepParams q = q0;
   q.quadw_rpg = rpg;
-  using C = quadw::Cfg<NP>;
-  auto kern = factor_rows_quadw_kernel<SMALL, NP, GRAM, NPRE>;
+  using C = quadw::Cfg<NP, DB>;
+  auto kern = factor_rows_quadw_kernel<SMALL, NP, GRAM, NPRE, DB>;
   const size_t sm = C::bytes();
   static bool set = false;
   if (!set) {
@@ -1072,7 +1220,15 @@ int launch_quadw_s(const SweepParams &q, cudaStream_t s) {
   int rpg = 4;
   while (rpg > 1 && (q.nrows + rpg / 2 - 1) / (rpg / 2) <= sms) rpg /= 2;
   const bool few = (q.nrows + 3) / 4 <= sms;
-  if (forced == 0 || (forced < 0 && !few)) return launch_quadw_t<SMALL, 2, false, NPRE>(q, 4, s);
+  static const bool db = [] {  // FT_QUADW_DB=0: the single-buffered per-step form (A/B)
+    const char *e = getenv("FT_QUADW_DB");
+    return !(e && e[0] == '0');
+  }();
+  if (forced == 0 || (forced < 0 && !few)) {
+    if constexpr (NPRE == 1)
+      if (db) return launch_quadw_t<SMALL, 2, false, NPRE, true>(q, 4, s);
+    return launch_quadw_t<SMALL, 2, false, NPRE>(q, 4, s);
+  }
   return launch_quadw_t<SMALL, 6, true, NPRE>(q, few ? rpg : 4, s);
 }
 
@@ -1105,6 +1261,11 @@ constexpr int TILE = 32 * XS;
 constexpr int WARP_FLOATS = 2 * TILE + 4 * 32 + 32;  // X, Y, C_u rows [4][32], e [32]
 constexpr int WPB = 8;
 constexpr size_t bytes() { return (size_t)WPB * WARP_FLOATS * 4; }
+// the DIRECT form stages nothing: its shared memory is only the block's fixed-order reduction
+// (R x J floats per warp), so the rest of the SM's 256 KB stays L1 data cache -- where the small
+// gathered C matrices (Netflix C_2: 280 KB) hit instead of going to L2
+constexpr int DIRECT_WS = FT_MAX_RANK * FT_MAX_RANK;
+constexpr size_t direct_bytes() { return (size_t)WPB * DIRECT_WS * 4; }
 }  // namespace cquad
 
 // SSE = true: the same walk scores the tree's leaves instead (K6b, evaluate over the training
@@ -1119,12 +1280,15 @@ __global__ void __launch_bounds__(cquad::WPB * 32, 2) core_rows_quad_kernel(cons
   extern __shared__ float4 smem4[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int q = lane >> 3, l = lane & 7;
-  float *X = reinterpret_cast<float *>(smem4) + w * WARP_FLOATS;
+  constexpr int WS = DIRECT ? DIRECT_WS : WARP_FLOATS;  // per-warp shared-memory floats
+  float *X = reinterpret_cast<float *>(smem4) + w * WS;
   float *Y = X + TILE;
-  float *cus = Y + TILE;  // [4][32]
+  float *cus = Y + TILE;  // [4][32] (staged form only)
   float *es = cus + 128;  // [32]
-  for (int k = lane; k < WARP_FLOATS; k += 32) X[k] = 0.f;
-  __syncwarp();
+  if (!DIRECT) {
+    for (int k = lane; k < WARP_FLOATS; k += 32) X[k] = 0.f;
+    __syncwarp();
+  }
   const int J = p.J, R = p.R;
   const int64_t nstream = (int64_t)gridDim.x * cquad::WPB * 4;
   int64_t row = (int64_t)(4 * w + q) * gridDim.x + blockIdx.x;  // block-fastest (see quad)
@@ -1394,12 +1558,12 @@ __global__ void __launch_bounds__(cquad::WPB * 32, 2) core_rows_quad_kernel(cons
   if (lane < R) {
 #pragma unroll
     for (int j = 0; j < FT_MAX_RANK; ++j)
-      if (j < J) red[w * WARP_FLOATS + lane * J + j] = acc[j];
+      if (j < J) red[w * WS + lane * J + j] = acc[j];
   }
   __syncthreads();
   for (int k = threadIdx.x; k < RJ; k += blockDim.x) {
     float s = 0.f;
-    for (int ww = 0; ww < cquad::WPB; ++ww) s += red[ww * cquad::WARP_FLOATS + k];
+    for (int ww = 0; ww < cquad::WPB; ++ww) s += red[ww * WS + k];
     p.partials[(int64_t)blockIdx.x * RJ + k] = s;
   }
 }
@@ -1417,7 +1581,10 @@ int core_quad_grid_t(const SweepParams &p) {
     cudaFuncSetAttribute(core_rows_quad_kernel<SSE, NPRE>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     cudaFuncSetAttribute(core_rows_quad_kernel<SSE, NPRE, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cquad::direct_bytes());
+    // two blocks x 32 KB of reduction space: the smallest carveout that holds them, the rest L1
+    cudaFuncSetAttribute(core_rows_quad_kernel<SSE, NPRE, true>,
+                         cudaFuncAttributePreferredSharedMemoryCarveout, 30);
     set = true;
   }
   int per_sm = 0;
@@ -1455,22 +1622,22 @@ int launch_core_quad_t(const SweepParams &p, int g, cudaStream_t s) {
   }();
   const bool direct = direct_env >= 0 ? direct_env == 1 : p.gather_bytes <= (64ll << 20);
   const dim3 b(cquad::WPB * 32);
-  const size_t sm = cquad::bytes();
+  const size_t sm = cquad::bytes(), smd = cquad::direct_bytes();
   switch (p.N) {
     case 3:
-      if (direct) core_rows_quad_kernel<SSE, 1, true><<<g, b, sm, s>>>(p);
+      if (direct) core_rows_quad_kernel<SSE, 1, true><<<g, b, smd, s>>>(p);
       else core_rows_quad_kernel<SSE, 1><<<g, b, sm, s>>>(p);
       break;
     case 4:
-      if (direct) core_rows_quad_kernel<SSE, 2, true><<<g, b, sm, s>>>(p);
+      if (direct) core_rows_quad_kernel<SSE, 2, true><<<g, b, smd, s>>>(p);
       else core_rows_quad_kernel<SSE, 2><<<g, b, sm, s>>>(p);
       break;
     case 5:
-      if (direct) core_rows_quad_kernel<SSE, 3, true><<<g, b, sm, s>>>(p);
+      if (direct) core_rows_quad_kernel<SSE, 3, true><<<g, b, smd, s>>>(p);
       else core_rows_quad_kernel<SSE, 3><<<g, b, sm, s>>>(p);
       break;
     default:
-      if (direct) core_rows_quad_kernel<SSE, 4, true><<<g, b, sm, s>>>(p);
+      if (direct) core_rows_quad_kernel<SSE, 4, true><<<g, b, smd, s>>>(p);
       else core_rows_quad_kernel<SSE, 4><<<g, b, sm, s>>>(p);
       break;
   }

@@ -1274,8 +1274,11 @@ constexpr size_t direct_bytes() { return (size_t)WPB * DIRECT_WS * 4; }
 #ifndef CORE_FUSED
 #define CORE_FUSED 1  // K4 quad: fused single pass in the quarter layout (0: lane-per-slot s-pass)
 #endif
+// DIRECT (gradient form): the R x J accumulator lives in the warp's shared-memory slice
+// ([j][lane r], conflict-free) instead of 32 registers per lane, so three blocks fit an SM --
+// more gathers in flight for a kernel that waits on them (the long-scoreboard stalls)
 template <bool SSE, int NPRE, bool DIRECT = false>
-__global__ void __launch_bounds__(cquad::WPB * 32, 2) core_rows_quad_kernel(const SweepParams p) {
+__global__ void __launch_bounds__(cquad::WPB * 32, DIRECT ? 3 : 2) core_rows_quad_kernel(const SweepParams p) {
   using namespace cquad;
   extern __shared__ float4 smem4[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1285,8 +1288,14 @@ __global__ void __launch_bounds__(cquad::WPB * 32, 2) core_rows_quad_kernel(cons
   float *Y = X + TILE;
   float *cus = Y + TILE;  // [4][32] (staged form only)
   float *es = cus + 128;  // [32]
+  constexpr bool SMACC = DIRECT && !SSE;
+  float *accs = X;  // SMACC: [j][r] accumulator slice of this warp
   if (!DIRECT) {
     for (int k = lane; k < WARP_FLOATS; k += 32) X[k] = 0.f;
+    __syncwarp();
+  } else if (SMACC) {
+#pragma unroll
+    for (int j = 0; j < FT_MAX_RANK; ++j) accs[j * 32 + lane] = 0.f;
     __syncwarp();
   }
   const int J = p.J, R = p.R;
@@ -1344,7 +1353,21 @@ __global__ void __launch_bounds__(cquad::WPB * 32, 2) core_rows_quad_kernel(cons
       const float c2 = __shfl_sync(FULL, g23.x, src), c3 = __shfl_sync(FULL, g23.y, src);
       const float gr = comp == 0 ? c0 : comp == 1 ? c1 : comp == 2 ? c2 : c3;  // g_qq[lane]
       const float *ar = p.A + (int64_t)__shfl_sync(FULL, ci, 8 * qq) * J;
-      if (j32) {
+      if (SMACC) {
+        float *ac = accs + lane;
+        if (j32) {
+#pragma unroll
+          for (int j4 = 0; j4 < 8; ++j4) {
+            const float4 a4 = __ldg(reinterpret_cast<const float4 *>(ar) + j4);
+            ac[(4 * j4) * 32] = __fmaf_rn(gr, a4.x, ac[(4 * j4) * 32]);
+            ac[(4 * j4 + 1) * 32] = __fmaf_rn(gr, a4.y, ac[(4 * j4 + 1) * 32]);
+            ac[(4 * j4 + 2) * 32] = __fmaf_rn(gr, a4.z, ac[(4 * j4 + 2) * 32]);
+            ac[(4 * j4 + 3) * 32] = __fmaf_rn(gr, a4.w, ac[(4 * j4 + 3) * 32]);
+          }
+        } else {
+          for (int j = 0; j < J; ++j) ac[j * 32] = __fmaf_rn(gr, __ldg(ar + j), ac[j * 32]);
+        }
+      } else if (j32) {
 #pragma unroll
         for (int j4 = 0; j4 < 8; ++j4) {
           const float4 a4 = __ldg(reinterpret_cast<const float4 *>(ar) + j4);
@@ -1555,6 +1578,16 @@ __global__ void __launch_bounds__(cquad::WPB * 32, 2) core_rows_quad_kernel(cons
   }
   const int RJ = R * J;
   float *red = reinterpret_cast<float *>(smem4);
+  if (SMACC) {  // the warps' [j][r] slices are already in place
+    __syncthreads();
+    for (int k = threadIdx.x; k < RJ; k += blockDim.x) {
+      const int r = k / J, j = k - r * J;
+      float s = 0.f;
+      for (int ww = 0; ww < cquad::WPB; ++ww) s += red[ww * WS + j * 32 + r];
+      p.partials[(int64_t)blockIdx.x * RJ + k] = s;
+    }
+    return;
+  }
   if (lane < R) {
 #pragma unroll
     for (int j = 0; j < FT_MAX_RANK; ++j)
@@ -1573,6 +1606,20 @@ bool core_quad_ok(const SweepParams &p) {
          p.R * p.J <= cquad::WARP_FLOATS;
 }
 
+// K4 direct (register gathers) while the gathered C matrices sit in L2, staged above
+bool core_direct(const SweepParams &p) {
+  // direct register loads keep 4 leaves in flight per lane, the staged pass 32 rows per warp:
+  // direct wins while the gathered C matrices sit in L2 (Netflix32 61 MB: core 2.41 -> 2.20 ms
+  // per mode; order-4 10K^4 19.9 -> 12.7 ms), staging wins once their misses go to HBM
+  // (Yahoo32 mode 2, 208 MB: 8.1 vs 9.3 ms; modes 0 / 1, 80 MB: 6.5 vs 6.8 ms).
+  // FT_CORE_DIRECT=0 / 1 forces either.
+  static const int direct_env = [] {
+    const char *e = getenv("FT_CORE_DIRECT");
+    return e && e[0] ? (e[0] == '0' ? 0 : 1) : -1;
+  }();
+  return direct_env >= 0 ? direct_env == 1 : p.gather_bytes <= (64ll << 20);
+}
+
 template <bool SSE, int NPRE>
 int core_quad_grid_t(const SweepParams &p) {
   const size_t sm = cquad::bytes();
@@ -1582,16 +1629,20 @@ int core_quad_grid_t(const SweepParams &p) {
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     cudaFuncSetAttribute(core_rows_quad_kernel<SSE, NPRE, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cquad::direct_bytes());
-    // two blocks x 32 KB of reduction space: the smallest carveout that holds them, the rest L1
+    // three blocks x 32 KB (accumulators / reduction): the smallest carveout that holds them,
+    // the rest of the SM's 256 KB stays L1
     cudaFuncSetAttribute(core_rows_quad_kernel<SSE, NPRE, true>,
-                         cudaFuncAttributePreferredSharedMemoryCarveout, 30);
+                         cudaFuncAttributePreferredSharedMemoryCarveout, 45);
     set = true;
   }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, core_rows_quad_kernel<SSE, NPRE>,
-                                                    cquad::WPB * 32, sm) != cudaSuccess ||
-      per_sm < 1)
-    per_sm = 1;
+  const bool direct = core_direct(p);
+  cudaError_t oc = direct
+      ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, core_rows_quad_kernel<SSE, NPRE, true>,
+                                                      cquad::WPB * 32, cquad::direct_bytes())
+      : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, core_rows_quad_kernel<SSE, NPRE>,
+                                                      cquad::WPB * 32, sm);
+  if (oc != cudaSuccess || per_sm < 1) per_sm = 1;
   int64_t g = (p.nrows + 4 * cquad::WPB - 1) / (4 * cquad::WPB);
   const int64_t cap = (int64_t)sm_count() * per_sm;
   if (g > cap) g = cap;
@@ -1611,16 +1662,7 @@ int core_quad_grid(const SweepParams &p) {
 
 template <bool SSE>
 int launch_core_quad_t(const SweepParams &p, int g, cudaStream_t s) {
-  // direct register loads keep 4 leaves in flight per lane, the staged pass 32 rows per warp:
-  // direct wins while the gathered C matrices sit in L2 (Netflix32 61 MB: core 2.41 -> 2.20 ms
-  // per mode; order-4 10K^4 19.9 -> 12.7 ms), staging wins once their misses go to HBM
-  // (Yahoo32 mode 2, 208 MB: 8.1 vs 9.3 ms; modes 0 / 1, 80 MB: 6.5 vs 6.8 ms).
-  // FT_CORE_DIRECT=0 / 1 forces either.
-  static const int direct_env = [] {
-    const char *e = getenv("FT_CORE_DIRECT");
-    return e && e[0] ? (e[0] == '0' ? 0 : 1) : -1;
-  }();
-  const bool direct = direct_env >= 0 ? direct_env == 1 : p.gather_bytes <= (64ll << 20);
+  const bool direct = core_direct(p);
   const dim3 b(cquad::WPB * 32);
   const size_t sm = cquad::bytes(), smd = cquad::direct_bytes();
   switch (p.N) {

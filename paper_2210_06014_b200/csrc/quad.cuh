@@ -424,6 +424,7 @@ __device__ __forceinline__ void quadr_direct_combine(const SweepParams &p, const
   }
 }
 
+constexpr int QR_META = 4 * quad::MQ;  // float4 step operands per warp (4 rows x MQ)
 template <bool SMALL, int NPRE, int WPBT>
 __global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quadr_kernel(const SweepParams p) {
   using namespace quad;
@@ -433,10 +434,9 @@ __global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quadr_kernel(const S
   const int srho = (lane >> 1) & 3;              // slot layout: lane s holds slot s = leaf
   const int sk = 2 * (lane >> 3) + (lane & 1);   //   sk of row srho
   uint4 *afr = reinterpret_cast<uint4 *>(smem4);
-  float *X = reinterpret_cast<float *>(afr + BFRAG_U4) + w * quad::WARP_FLOATS;
-  float *Y = X + TILE;
-  float4 *meta = reinterpret_cast<float4 *>(Y + TILE);
-  for (int k = lane; k < 2 * TILE; k += 32) X[k] = 0.f;
+  // shared memory: the Bt^T fragments and each warp's step operands only -- the direct combine
+  // stages nothing, so the rest of the SM's 256 KB serves the gathered C rows as L1
+  float4 *meta = reinterpret_cast<float4 *>(afr + BFRAG_U4) + w * QR_META;
   quad_afrag_init<SMALL ? 4 : 8>(p, afr);
   __syncthreads();
 
@@ -562,11 +562,14 @@ __global__ void __launch_bounds__(WPBT * 32, 2) factor_rows_quadr_kernel(const S
 
 template <bool SMALL, int NPRE, int WPBT>
 int launch_quadr_t(const SweepParams &q, cudaStream_t s) {
-  const size_t sm = (size_t)quad::BFRAG_U4 * 16 + (size_t)WPBT * quad::WARP_FLOATS * 4 + WPBT * 8;
+  const size_t sm = (size_t)quad::BFRAG_U4 * 16 + (size_t)WPBT * QR_META * 16;
   static bool set = false;
   if (!set) {
     cudaFuncSetAttribute(factor_rows_quadr_kernel<SMALL, NPRE, WPBT>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    // two blocks x ~13 KB: the smallest carveout, the rest L1 for the gathered rows
+    cudaFuncSetAttribute(factor_rows_quadr_kernel<SMALL, NPRE, WPBT>,
+                         cudaFuncAttributePreferredSharedMemoryCarveout, 15);
     set = true;
   }
   int per_sm = 0;

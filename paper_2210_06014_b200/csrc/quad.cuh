@@ -276,62 +276,6 @@ __device__ __forceinline__ void quad_batch_lookahead(float (&a)[4], float (&lo)[
   }
 }
 
-// ... with TWO steps of lookahead: p_k = a_{k-2} . v_k (issued when a_{k-2} exists), and
-//     a_k . v_k = (1 + c_{k-1}) (1 + c_{k-2}) p_k + (1 + c_{k-1}) lr_{k-2} e_{k-2} (v_{k-2} . v_k)
-//                 + lr_{k-1} e_{k-1} (v_{k-1} . v_k),
-// so one butterfly spans three steps of the serial path.  Steps 0 and 1 of a batch use the
-// direct / one-step forms from a_0.
-__device__ __forceinline__ void quad_batch_lookahead2(float (&a)[4], float (&lo)[4],
-                                                      const float4 (&vv)[quad::QB],
-                                                      const float4 (&mm)[quad::QB]) {
-  using quad::QB;
-  float g1[QB], g2[QB];  // g1[k] = v_{k-1} . v_k (k >= 1), g2[k] = v_{k-2} . v_k (k >= 2)
-  g1[0] = g2[0] = g2[1] = 0.f;
-#pragma unroll
-  for (int k = 1; k < QB; ++k) {
-    float2 pr = fmul2(make_float2(vv[k - 1].x, vv[k - 1].y), make_float2(vv[k].x, vv[k].y));
-    pr = ffma2(make_float2(vv[k - 1].z, vv[k - 1].w), make_float2(vv[k].z, vv[k].w), pr);
-    g1[k] = pr.x + pr.y;
-    if (k >= 2) {
-      float2 qr = fmul2(make_float2(vv[k - 2].x, vv[k - 2].y), make_float2(vv[k].x, vv[k].y));
-      qr = ffma2(make_float2(vv[k - 2].z, vv[k - 2].w), make_float2(vv[k].z, vv[k].w), qr);
-      g2[k] = qr.x + qr.y;
-    }
-  }
-#pragma unroll
-  for (int msk = 4; msk >= 1; msk >>= 1)
-#pragma unroll
-    for (int k = 1; k < QB; ++k) {
-      g1[k] += __shfl_xor_sync(FULL, g1[k], msk);
-      if (k >= 2) g2[k] += __shfl_xor_sync(FULL, g2[k], msk);
-    }
-  float pk = quad_dot(a, vv[0]), pk1 = quad_dot(a, vv[1]);  // p_k, p_{k+1}
-  float e1 = 0.f, e2 = 0.f;        // e_{k-1}, e_{k-2}
-  float c1 = 0.f, c2 = 0.f;        // c_{k-1}, c_{k-2}
-  float l1 = 0.f, l2 = 0.f;        // lr_{k-1}, lr_{k-2}
-#pragma unroll
-  for (int k = 0; k < QB; ++k) {
-    // p_{k+2} = a_k . v_{k+2} from the current row state (before step k's update)
-    const float pn = k + 2 < QB ? quad_dot(a, vv[k + 2]) : 0.f;
-    float e;
-    if (k == 0) {
-      e = mm[0].x - pk;
-    } else if (k == 1) {
-      e = __fmaf_rn(-l1 * g1[1], e1, mm[1].x - __fmaf_rn(c1, pk, pk));
-    } else {
-      const float d12 = __fmaf_rn(c1, c2, c1 + c2);           // (1 + c1)(1 + c2) - 1
-      const float t2 = __fmaf_rn(c1, l2, l2) * g2[k];           // (1 + c1) lr_{k-2} g2
-      const float part = mm[k].x - __fmaf_rn(d12, pk, pk) - t2 * e2;
-      e = __fmaf_rn(-l1 * g1[k], e1, part);
-    }
-    quad_update_c(a, lo, vv[k], mm[k], e);
-    e2 = e1, e1 = e;
-    c2 = c1, c1 = mm[k].z;
-    l2 = l1, l1 = mm[k].y;
-    pk = pk1, pk1 = pn;
-  }
-}
-
 __device__ __forceinline__ void quad_chain_step_vc(float (&a)[4], float (&lo)[4], const float4 v,
                                                    float4 m) {
   float2 pr = fmul2(make_float2(a[0], a[1]), make_float2(v.x, v.y));
@@ -873,7 +817,7 @@ __global__ void __launch_bounds__(quadw::Cfg<NP, DB>::THREADS, NP <= 2 ? 4 : 1)
   }
   // rows per group (runtime): 4 quarters normally, 2 or 1 when the rows leave SMs idle (the
   // quarters past rpg stream nothing and run padding)
-  const int rpg = p.quadw_rpg % 1000 > 0 ? p.quadw_rpg % 1000 : 4;
+  const int rpg = p.quadw_rpg > 0 ? p.quadw_rpg : 4;
 
   if (w > 0) {
     // ===================================== producers =====================================
@@ -1124,7 +1068,6 @@ __global__ void __launch_bounds__(quadw::Cfg<NP, DB>::THREADS, NP <= 2 ? 4 : 1)
         __syncwarp();
         mbar_arrive(empty + st);  // the stage is free once read
         if (DB) {  // one step of lookahead: the chain at about half the serial latency
-          if (p.quadw_rpg >= 1000) quad_batch_lookahead2(a, lo, vv, mm); else
           quad_batch_lookahead(a, lo, vv, mm);
         } else {
 #pragma unroll
@@ -1256,7 +1199,7 @@ int launch_quadw_t(const SweepParams &q0, int rpg, cudaStream_t s) {
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, sm) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
-  int64_t g = (q.nrows + rpg % 1000 - 1) / (rpg % 1000);
+  int64_t g = (q.nrows + rpg - 1) / rpg;
   const int64_t cap = (int64_t)sm_count() * per_sm;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
@@ -1286,10 +1229,7 @@ int launch_quadw_s(const SweepParams &q, cudaStream_t s) {
   }();
   if (forced == 0 || (forced < 0 && !few)) {
     if constexpr (NPRE == 1)
-      if (db) {
-        static const int la2 = [] { const char *e = getenv("FT_QW_LA2"); return e ? atoi(e) : 0; }();
-        return launch_quadw_t<SMALL, 2, false, NPRE, true>(q, 4 + 1000 * la2, s);
-      }
+      if (db) return launch_quadw_t<SMALL, 2, false, NPRE, true>(q, 4, s);
     return launch_quadw_t<SMALL, 2, false, NPRE>(q, 4, s);
   }
   return launch_quadw_t<SMALL, 6, true, NPRE>(q, few ? rpg : 4, s);
